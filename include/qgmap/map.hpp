@@ -1,0 +1,159 @@
+// qgmap/map.hpp -- filter / validate / map entry points of the B200 mapper
+// (the spec-only modules of SPEC.md: filtration :318-361, validation
+// :363-420, postprocess strata :422-472, run_map core :531-539), as thin
+// C++ wrappers of include/qgm_c.h.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "qgmap/qgroup_index.hpp"
+#include "qgmap/reference.hpp"
+
+namespace qgmap {
+
+// ------------------------------------------------------------- filtration
+// Hit extended with the strand and chromosome of the
+// streamed reference q-gram. d = p - (p' mod m) on the forward strand
+// (Alg. 2 line 12); d = p + o + q - n for a reverse-complement match.
+struct Hit {
+  std::int64_t d;
+  std::uint32_t r;
+  std::uint32_t chrom;
+  std::uint8_t strand;
+  auto operator<=>(const Hit&) const = default;
+};
+
+enum class FilterMode { full = QGM_FILTER_FULL, run_start = QGM_FILTER_RUN_START };
+
+// filter_reference over every unmasked reference position of
+// every chromosome, both strands by default. Sorted by (r, strand, chrom, d).
+template <class W>
+std::vector<Hit> filter_reference(const DeviceReference& ref, const QGroupIndex<W>& index,
+                                  FilterMode mode = FilterMode::full, int strands = QGM_STRAND_BOTH,
+                                  bool unique = false) {
+  auto ctx = index.device_index().ctx;
+  qgm_cands* c = nullptr;
+  ctx->check(qgm_filter(ctx->get(), index.device_index().get(), index.device_reads().get(), ref.get(), strands,
+                        int(mode), &c));
+  std::unique_ptr<qgm_cands, void (*)(qgm_cands*)> guard(c, qgm_cands_destroy);
+  if (unique) ctx->check(qgm_cands_unique(ctx->get(), c));
+  std::uint64_t n = 0;
+  ctx->check(qgm_cands_count(c, &n));
+  std::vector<qgm_candidate> raw(n);
+  ctx->check(qgm_cands_download(ctx->get(), c, raw.data()));
+  std::vector<Hit> out(n);
+  for (std::uint64_t i = 0; i < n; ++i)
+    out[i] = {raw[i].diagonal, raw[i].read_id, raw[i].chrom, std::uint8_t(raw[i].strand)};
+  return out;
+}
+
+// ------------------------------------------------------------- validation
+struct BandConfig {
+  unsigned band_width = 32;
+  double identity_threshold = 0.80;
+  unsigned percent() const { return unsigned(std::lround(identity_threshold * 100.0)); }
+};
+
+struct ValidatedHit {
+  std::uint32_t r;
+  std::uint32_t chrom;
+  std::uint32_t ref_start;
+  int k;
+  double identity;
+  std::int64_t d;
+  std::uint8_t strand;
+};
+
+// validate_hits: one ValidatedHit per input hit whose
+// identity (n-k)/n reaches the threshold (integer test 100(n-k) >= pct*n).
+template <class W>
+std::vector<ValidatedHit> validate_hits(const std::vector<Hit>& hits, const QGroupIndex<W>& index,
+                                        const PackedReadText& text, const DeviceReference& ref,
+                                        BandConfig band = {}) {
+  auto ctx = index.device_index().ctx;
+  std::vector<qgm_candidate> in(hits.size());
+  for (std::size_t i = 0; i < hits.size(); ++i) in[i] = {hits[i].d, hits[i].r, hits[i].chrom, hits[i].strand, 0};
+  std::vector<qgm_validated> res(hits.size());
+  ctx->check(qgm_validate(ctx->get(), index.device_reads().get(), ref.get(), in.data(), in.size(), band.band_width,
+                          band.percent(), res.data()));
+  std::vector<ValidatedHit> out;
+  for (std::size_t i = 0; i < hits.size(); ++i) {
+    if (!res[i].kept || !res[i].in_range) continue;
+    const double n = double(text.read_lengths[hits[i].r]);
+    out.push_back({hits[i].r, hits[i].chrom, res[i].ref_start, res[i].edits, (n - res[i].edits) / n, hits[i].d,
+                   hits[i].strand});
+  }
+  return out;
+}
+
+struct MyersResult {
+  int k;
+  unsigned start_offset;
+};
+
+// myers_banded for one read and one window; the band width
+// is implied by the window: B = |window| - |read| + 1 (1..64).
+inline MyersResult myers_banded(std::span<const base_code> read, std::span<const base_code> window,
+                                std::shared_ptr<device::Context> ctx = device::Context::default_context()) {
+  if (read.empty() || window.size() < read.size() || window.size() - read.size() + 1 > 64)
+    throw input_error("myers_banded: need 1 <= |window| - |read| + 1 <= 64");
+  const unsigned B = unsigned(window.size() - read.size() + 1);
+  Reference R;
+  R.names = {"window"};
+  R.codes.assign(window.begin(), window.end());
+  R.chrom_begin = {0, window.size()};
+  DeviceReference dref(R, ctx);
+  std::vector<std::vector<base_code>> one{std::vector<base_code>(read.begin(), read.end())};
+  auto text = pack_encoded_reads(one, std::uint32_t(read.size()), 1);
+  auto reads = device::upload_reads(text, ctx);
+  const qgm_candidate c{std::int64_t((B - 1) / 2), 0, 0, 0, 0};
+  qgm_validated v{};
+  ctx->check(qgm_validate(ctx->get(), reads.get(), dref.get(), &c, 1, B, 0, &v));
+  return {v.edits, v.start};
+}
+
+// ------------------------------------------------------------- map
+enum class StratumMode { best_stratum = QGM_MODE_BEST_STRATUM, all = QGM_MODE_ALL };
+
+struct MapParams {
+  unsigned q = 16;
+  unsigned group_width = 32;
+  bool sampled = false;
+  BandConfig band{};
+  StratumMode mode = StratumMode::best_stratum;
+  int strands = QGM_STRAND_BOTH;
+};
+
+struct MappedHit {
+  std::uint32_t read_id, chrom, ref_start;
+  std::uint16_t edits;
+  std::uint8_t strand;
+  auto operator<=>(const MappedHit&) const = default;
+};
+
+// One read buffer against the whole reference: index build, filtration,
+// candidate sort/dedup, validation, dedup + strata -- all on the device.
+// Output sorted by (read, chrom, ref_start, strand).
+inline std::vector<MappedHit> map_reads(const DeviceReference& ref, const PackedReadText& text,
+                                        const MapParams& p = {}, qgm_map_stats* stats = nullptr) {
+  auto ctx = ref.context();
+  auto reads = device::upload_reads(text, ctx);
+  const qgm_map_params mp{p.q, p.group_width, p.sampled ? 1u : 0u, p.band.band_width, p.band.percent(),
+                          unsigned(p.mode), unsigned(p.strands), 0};
+  qgm_hits* h = nullptr;
+  ctx->check(qgm_map(ctx->get(), reads.get(), ref.get(), &mp, &h));
+  std::unique_ptr<qgm_hits, void (*)(qgm_hits*)> guard(h, qgm_hits_destroy);
+  std::uint64_t n = 0;
+  ctx->check(qgm_hits_count(h, &n));
+  if (stats) ctx->check(qgm_hits_stats(h, stats));
+  std::vector<qgm_hit> raw(n);
+  ctx->check(qgm_hits_download(ctx->get(), h, raw.data()));
+  std::vector<MappedHit> out(n);
+  for (std::uint64_t i = 0; i < n; ++i)
+    out[i] = {raw[i].read_id, raw[i].chrom, raw[i].ref_start, raw[i].edits, raw[i].strand};
+  return out;
+}
+
+}  // namespace qgmap

@@ -1,0 +1,463 @@
+"""paper_1403_1706_b200 -- B200-native (sm_100a) PEANUT read-mapping hot path.
+
+Python mirror of the reference's qgmap operator surface over the C ABI in
+include/qgm_c.h (libqgm_b200.so, built in-tree by `make`). Names and argument
+meaning follow the reference (proj/include/qgmap/{seq,qgroup_index}.hpp) and
+SPEC.md for the spec-only stages:
+
+    Context                      one CUDA device + stream (qgm_ctx)
+    Reads.from_codes / upload    PackedReadText (seq.hpp:98-140)
+    Index.build                  build_qgroup_index<W> (qgroup_index.hpp:124-180)
+      .sample / .normalize       sample_group_starts (:185-196) / per-interval sort
+      .occupancy .group_starts   the four arrays (:42-45)
+      .occ_starts .positions
+      .index_pair(codes)         Indexpair (:50-57)
+    Reference.from_codes         ReferenceIndex sequences
+    Context.filter               Alg. 2 filtration
+    Context.validate             myers_banded / validate_hits
+    Context.map / map_host       run_map core
+
+There is no CPU fallback: if the shared library or a CUDA device is missing,
+every entry point raises. Errors map like the reference: QGM_ERR_INPUT ->
+InputError (qgmap::input_error), QGM_ERR_INTERNAL -> LogicError
+(std::logic_error), QGM_ERR_CUDA -> CudaError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqgm_b200.so")
+SYNTH_PATH = os.path.join(_HERE, "libqgm_synth.so")
+
+MODE_BEST_STRATUM = 0
+MODE_ALL = 1
+FILTER_FULL = 0
+FILTER_RUN_START = 1
+STAGES = ("reads", "index", "filter", "sort_unique", "validate", "strata", "d2h", "other")
+
+CANDIDATE_DTYPE = np.dtype([("diagonal", "<i8"), ("read_id", "<u4"), ("chrom", "<u4"),
+                            ("strand", "<u4"), ("reserved", "<u4")])
+VALIDATED_DTYPE = np.dtype([("edits", "<i4"), ("start", "<u4"), ("ref_start", "<u4"), ("kept", "u1"),
+                            ("in_range", "u1"), ("r0", "u1"), ("r1", "u1"), ("r2", "<u4")])
+HIT_DTYPE = np.dtype([("read_id", "<u4"), ("chrom", "<u4"), ("ref_start", "<u4"), ("edits", "<u2"),
+                      ("strand", "u1"), ("reserved", "u1")])
+assert CANDIDATE_DTYPE.itemsize == 24 and VALIDATED_DTYPE.itemsize == 20 and HIT_DTYPE.itemsize == 16
+
+
+class QgmError(RuntimeError):
+    pass
+
+
+class InputError(QgmError, ValueError):
+    """qgmap::input_error (seq.hpp:13-16)."""
+
+
+class LogicError(QgmError):
+    """std::logic_error (parallel.hpp:176,181)."""
+
+
+class CudaError(QgmError):
+    pass
+
+
+class MapParams(C.Structure):
+    _fields_ = [("q", C.c_uint32), ("group_width", C.c_uint32), ("sampled", C.c_uint32),
+                ("band_width", C.c_uint32), ("pct_identity", C.c_uint32), ("mode", C.c_uint32),
+                ("strands", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+class IndexInfo(C.Structure):
+    _fields_ = [("q", C.c_uint32), ("group_width", C.c_uint32), ("sampled", C.c_uint32), ("reserved", C.c_uint32),
+                ("group_count", C.c_uint64), ("group_starts_len", C.c_uint64), ("distinct", C.c_uint64),
+                ("occurrences", C.c_uint64)]
+
+
+class MapStats(C.Structure):
+    _fields_ = [("raw_candidates", C.c_uint64), ("unique_candidates", C.c_uint64), ("validated", C.c_uint64),
+                ("hits", C.c_uint64)]
+
+
+# Every symbol include/qgm_c.h declares (checked by tests/test_capi_symbols.py).
+EXPORTS = (
+    "qgm_ctx_create", "qgm_ctx_set_stream", "qgm_ctx_stream", "qgm_ctx_destroy", "qgm_last_error",
+    "qgm_ctx_synchronize", "qgm_ctx_profile", "qgm_ctx_stage_times", "qgm_ctx_launches", "qgm_pack_codes",
+    "qgm_pack_reads", "qgm_reads_upload", "qgm_reads_from_device", "qgm_reads_destroy", "qgm_index_build",
+    "qgm_index_sample", "qgm_index_normalize", "qgm_index_info_get", "qgm_index_download", "qgm_index_lookup",
+    "qgm_index_destroy", "qgm_ref_upload", "qgm_ref_destroy", "qgm_filter", "qgm_cands_count",
+    "qgm_cands_download", "qgm_cands_unique", "qgm_cands_destroy", "qgm_validate", "qgm_map", "qgm_hits_count",
+    "qgm_hits_stats", "qgm_hits_download", "qgm_hits_destroy", "qgm_map_host", "qgm_exclusive_scan_u32",
+)
+
+_lib = None
+_synth = None
+P = C.c_void_p
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libqgm_b200.so and declare the C ABI. Raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `make` (or __graft_entry__.build()); there is no CPU fallback")
+    lib = C.CDLL(path)
+    u32, u64, i32 = C.c_uint32, C.c_uint64, C.c_int
+    sig = {
+        "qgm_ctx_create": (i32, [i32, C.POINTER(P)]),
+        "qgm_ctx_set_stream": (i32, [P, P]),
+        "qgm_ctx_stream": (P, [P]),
+        "qgm_ctx_destroy": (None, [P]),
+        "qgm_last_error": (C.c_char_p, [P]),
+        "qgm_ctx_synchronize": (i32, [P]),
+        "qgm_ctx_profile": (i32, [P, i32]),
+        "qgm_ctx_stage_times": (i32, [P, P, i32, i32]),
+        "qgm_ctx_launches": (u64, [P, i32]),
+        "qgm_pack_codes": (i32, [P, u64, P]),
+        "qgm_pack_reads": (i32, [P, u32, u32, P]),
+        "qgm_reads_upload": (i32, [P, P, P, u32, u32, C.POINTER(P)]),
+        "qgm_reads_from_device": (i32, [P, P, P, u32, u32, C.POINTER(P)]),
+        "qgm_reads_destroy": (None, [P]),
+        "qgm_index_build": (i32, [P, P, u32, u32, i32, C.POINTER(P)]),
+        "qgm_index_sample": (i32, [P, P, C.POINTER(P)]),
+        "qgm_index_normalize": (i32, [P, P]),
+        "qgm_index_info_get": (i32, [P, C.POINTER(IndexInfo)]),
+        "qgm_index_download": (i32, [P, P, P, P, P, P]),
+        "qgm_index_lookup": (i32, [P, P, P, u64, P, P]),
+        "qgm_index_destroy": (None, [P]),
+        "qgm_ref_upload": (i32, [P, P, P, u32, P, C.POINTER(P)]),
+        "qgm_ref_destroy": (None, [P]),
+        "qgm_filter": (i32, [P, P, P, P, i32, i32, C.POINTER(P)]),
+        "qgm_cands_count": (i32, [P, C.POINTER(u64)]),
+        "qgm_cands_download": (i32, [P, P, P]),
+        "qgm_cands_unique": (i32, [P, P]),
+        "qgm_cands_destroy": (None, [P]),
+        "qgm_validate": (i32, [P, P, P, P, u64, u32, u32, P]),
+        "qgm_map": (i32, [P, P, P, C.POINTER(MapParams), C.POINTER(P)]),
+        "qgm_hits_count": (i32, [P, C.POINTER(u64)]),
+        "qgm_hits_stats": (i32, [P, C.POINTER(MapStats)]),
+        "qgm_hits_download": (i32, [P, P, P]),
+        "qgm_hits_destroy": (None, [P]),
+        "qgm_map_host": (i32, [P, P, P, u32, u32, P, C.POINTER(MapParams), P, u64, C.POINTER(u64),
+                               C.POINTER(MapStats)]),
+        "qgm_exclusive_scan_u32": (i32, [P, P, u64, P, P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def load_synth(path: str = SYNTH_PATH):
+    global _synth
+    if _synth is None:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not built: run `make`")
+        s = C.CDLL(path)
+        s.qgs_random_reference.argtypes = [C.c_uint64, C.c_uint64, P]
+        s.qgs_repetitive_reference.argtypes = [C.c_uint64, C.c_uint64, P]
+        s.qgs_simulate_reads.argtypes = [C.c_uint64, P, P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_double,
+                                         C.c_uint32, P, P, P, P, P]
+        s.qgs_pack.argtypes = [P, C.c_uint64, P]
+        s.qgs_pack_reads.argtypes = [P, C.c_uint32, C.c_uint32, P]
+        _synth = s
+    return _synth
+
+
+# ----------------------------------------------------------------- host codec
+def pack_codes(codes: np.ndarray) -> np.ndarray:
+    """1-byte codes (0..3) -> 2-bit MSB-first uint64 words (qgm_c.h layout)."""
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    words = np.zeros((codes.size + 31) // 32 + 1, dtype=np.uint64)
+    load_synth().qgs_pack(_ptr(codes), codes.size, _ptr(words))
+    return words
+
+
+def pack_read_codes(codes: np.ndarray, stride: int) -> np.ndarray:
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    n = codes.size // stride if stride else 0
+    W = (stride + 31) // 32
+    words = np.zeros(max(n * W, 1), dtype=np.uint64)
+    if n:
+        load_synth().qgs_pack_reads(_ptr(codes), stride, n, _ptr(words))
+    return words
+
+
+def random_reference(seed: int, length: int) -> np.ndarray:
+    out = np.empty(length, dtype=np.uint8)
+    load_synth().qgs_random_reference(seed, length, _ptr(out))
+    return out
+
+
+def repetitive_reference(seed: int, length: int) -> np.ndarray:
+    out = np.empty(length, dtype=np.uint8)
+    load_synth().qgs_repetitive_reference(seed, length, _ptr(out))
+    return out
+
+
+def simulate_reads(seed, ref_codes, chrom_begin, n_reads, length, err, stride=None):
+    """Returns (codes[n_reads*stride], lengths, truth_chrom, truth_pos, truth_strand)."""
+    stride = stride or length
+    ref_codes = np.ascontiguousarray(ref_codes, dtype=np.uint8)
+    cb = np.ascontiguousarray(chrom_begin, dtype=np.uint64)
+    codes = np.zeros(n_reads * stride, dtype=np.uint8)
+    lengths = np.zeros(n_reads, dtype=np.uint32)
+    tc = np.zeros(n_reads, dtype=np.uint32)
+    tp = np.zeros(n_reads, dtype=np.uint64)
+    ts = np.zeros(n_reads, dtype=np.uint8)
+    rc = load_synth().qgs_simulate_reads(seed, _ptr(ref_codes), _ptr(cb), cb.size - 1, n_reads, length, err, stride,
+                                         _ptr(codes), _ptr(lengths), _ptr(tc), _ptr(tp), _ptr(ts))
+    if rc:
+        raise InputError("simulate_reads: bad arguments")
+    return codes, lengths, tc, tp, ts
+
+
+# ----------------------------------------------------------------- objects
+class Context:
+    """One device + stream (qgm_ctx). All objects must be released before it."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self.lib = load_library()
+        h = P()
+        self._check(self.lib.qgm_ctx_create(device, C.byref(h)), None)
+        self.h = h
+        if stream is not None:
+            self._check(self.lib.qgm_ctx_set_stream(self.h, P(stream)))
+
+    def _check(self, rc, h=...):
+        if rc == 0:
+            return
+        msg = self.lib.qgm_last_error(self.h if h is ... else h)
+        msg = msg.decode() if msg else f"error {rc}"
+        raise {1: InputError, 2: LogicError, 3: CudaError}.get(rc, QgmError)(msg)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.qgm_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        self._check(self.lib.qgm_ctx_synchronize(self.h))
+
+    def set_stream(self, stream: int | None):
+        self._check(self.lib.qgm_ctx_set_stream(self.h, P(stream) if stream else None))
+
+    def profile(self, enable=True):
+        self._check(self.lib.qgm_ctx_profile(self.h, int(enable)))
+
+    def stage_times(self, reset=True) -> dict:
+        ms = np.zeros(len(STAGES), dtype=np.float64)
+        self._check(self.lib.qgm_ctx_stage_times(self.h, _ptr(ms), len(STAGES), int(reset)))
+        return dict(zip(STAGES, ms.tolist()))
+
+    def launches(self, reset=False) -> int:
+        return int(self.lib.qgm_ctx_launches(self.h, int(reset)))
+
+    # --- stage entry points
+    def filter(self, index, reads, ref, strands=3, mode=FILTER_FULL, unique=False) -> np.ndarray:
+        h = P()
+        self._check(self.lib.qgm_filter(self.h, index.h, reads.h, ref.h, strands, mode, C.byref(h)))
+        try:
+            if unique:
+                self._check(self.lib.qgm_cands_unique(self.h, h))
+            n = C.c_uint64()
+            self._check(self.lib.qgm_cands_count(h, C.byref(n)))
+            out = np.zeros(n.value, dtype=CANDIDATE_DTYPE)
+            self._check(self.lib.qgm_cands_download(self.h, h, _ptr(out)))
+            return out
+        finally:
+            self.lib.qgm_cands_destroy(h)
+
+    def validate(self, reads, ref, cands: np.ndarray, band_width=32, pct_identity=80) -> np.ndarray:
+        cands = np.ascontiguousarray(cands, dtype=CANDIDATE_DTYPE)
+        out = np.zeros(cands.size, dtype=VALIDATED_DTYPE)
+        self._check(self.lib.qgm_validate(self.h, reads.h, ref.h, _ptr(cands), cands.size, band_width,
+                                          pct_identity, _ptr(out)))
+        return out
+
+    def map(self, reads, ref, params: MapParams | None = None, **kw):
+        """Returns (hits[HIT_DTYPE], stats dict)."""
+        p = params or make_params(**kw)
+        h = P()
+        self._check(self.lib.qgm_map(self.h, reads.h, ref.h, C.byref(p), C.byref(h)))
+        try:
+            n = C.c_uint64()
+            self._check(self.lib.qgm_hits_count(h, C.byref(n)))
+            st = MapStats()
+            self._check(self.lib.qgm_hits_stats(h, C.byref(st)))
+            out = np.zeros(n.value, dtype=HIT_DTYPE)
+            self._check(self.lib.qgm_hits_download(self.h, h, _ptr(out)))
+            return out, {f: getattr(st, f) for f, _ in MapStats._fields_}
+        finally:
+            self.lib.qgm_hits_destroy(h)
+
+    def map_host(self, words: np.ndarray, lengths: np.ndarray, stride: int, ref, params=None, out=None, **kw):
+        """e2e entry: host reads in, host hits out (qgm_map_host)."""
+        p = params or make_params(**kw)
+        lengths = np.ascontiguousarray(lengths, dtype=np.uint32)
+        if out is None:
+            out = np.zeros(max(64, lengths.size * 4), dtype=HIT_DTYPE)
+        n = C.c_uint64()
+        st = MapStats()
+        rc = self.lib.qgm_map_host(self.h, _ptr(words), _ptr(lengths), lengths.size, stride, ref.h, C.byref(p),
+                                   _ptr(out), out.size, C.byref(n), C.byref(st))
+        if rc == 1 and n.value > out.size:
+            out = np.zeros(n.value, dtype=HIT_DTYPE)
+            rc = self.lib.qgm_map_host(self.h, _ptr(words), _ptr(lengths), lengths.size, stride, ref.h, C.byref(p),
+                                       _ptr(out), out.size, C.byref(n), C.byref(st))
+        self._check(rc)
+        return out[: n.value], {f: getattr(st, f) for f, _ in MapStats._fields_}
+
+    def exclusive_scan(self, values: np.ndarray):
+        """par::exclusive_scan (parallel.hpp:116-121) on the device: (sums, total)."""
+        v = np.ascontiguousarray(values, dtype=np.uint32)
+        out = np.zeros(v.size, dtype=np.uint32)
+        tot = C.c_uint32()
+        self._check(self.lib.qgm_exclusive_scan_u32(self.h, _ptr(v), v.size, _ptr(out), C.byref(tot)))
+        return out, tot.value
+
+
+def make_params(q=16, group_width=32, sampled=False, band_width=32, pct_identity=80, mode=MODE_BEST_STRATUM,
+                strands=3) -> MapParams:
+    return MapParams(q, group_width, int(sampled), band_width, pct_identity, mode, strands, 0)
+
+
+class Reads:
+    """A read buffer on the device (PackedReadText, seq.hpp:98-115)."""
+
+    def __init__(self, ctx: Context, words: np.ndarray, lengths: np.ndarray, stride: int):
+        self.ctx = ctx
+        lengths = np.ascontiguousarray(lengths, dtype=np.uint32)
+        words = np.ascontiguousarray(words, dtype=np.uint64)
+        self.n, self.stride = lengths.size, stride
+        h = P()
+        ctx._check(ctx.lib.qgm_reads_upload(ctx.h, _ptr(words), _ptr(lengths), lengths.size, stride, C.byref(h)))
+        self.h = h
+
+    @classmethod
+    def from_codes(cls, ctx, codes: np.ndarray, lengths: np.ndarray, stride: int):
+        return cls(ctx, pack_read_codes(codes, stride), lengths, stride)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.qgm_reads_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Reference:
+    """Reference sequences on the device (concatenated chromosomes, optional repeat mask)."""
+
+    def __init__(self, ctx: Context, words: np.ndarray, chrom_begin, mask_bits: np.ndarray | None = None):
+        self.ctx = ctx
+        cb = np.ascontiguousarray(chrom_begin, dtype=np.uint64)
+        self.chrom_begin = cb
+        words = np.ascontiguousarray(words, dtype=np.uint64)
+        mb = None if mask_bits is None else np.ascontiguousarray(mask_bits, dtype=np.uint64)
+        h = P()
+        ctx._check(ctx.lib.qgm_ref_upload(ctx.h, _ptr(words), _ptr(cb), cb.size - 1, _ptr(mb), C.byref(h)))
+        self.h = h
+
+    @classmethod
+    def from_codes(cls, ctx, codes: np.ndarray, chrom_begin, mask: np.ndarray | None = None):
+        mb = None
+        if mask is not None:
+            m = np.ascontiguousarray(mask, dtype=np.uint8).astype(bool)
+            padded = np.zeros((m.size + 63) // 64 * 64, dtype=bool)
+            padded[: m.size] = m
+            mb = np.packbits(padded, bitorder="little").view(np.uint64).copy() \
+                if padded.size else np.zeros(1, np.uint64)
+        return cls(ctx, pack_codes(codes), chrom_begin, mb)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.qgm_ref_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Index:
+    """QGroupIndex<W> on the device (qgroup_index.hpp:28-104)."""
+
+    def __init__(self, ctx: Context, h):
+        self.ctx, self.h = ctx, h
+        info = IndexInfo()
+        ctx._check(ctx.lib.qgm_index_info_get(h, C.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in IndexInfo._fields_}
+        self._arrays = None
+
+    @classmethod
+    def build(cls, ctx: Context, reads: Reads, q: int, group_width: int = 32, sampled: bool = False):
+        h = P()
+        ctx._check(ctx.lib.qgm_index_build(ctx.h, reads.h, q, group_width, int(sampled), C.byref(h)))
+        return cls(ctx, h)
+
+    def sample(self) -> "Index":
+        h = P()
+        self.ctx._check(self.ctx.lib.qgm_index_sample(self.ctx.h, self.h, C.byref(h)))
+        return Index(self.ctx, h)
+
+    def normalize(self):
+        self.ctx._check(self.ctx.lib.qgm_index_normalize(self.ctx.h, self.h))
+        self._arrays = None
+        return self
+
+    def arrays(self):
+        if self._arrays is None:
+            i = self.info
+            wd = np.uint32 if i["group_width"] == 32 else np.uint64
+            I = np.zeros(i["group_count"], dtype=wd)
+            S = np.zeros(i["group_starts_len"], dtype=np.uint32)
+            S1 = np.zeros(i["distinct"] + 1, dtype=np.uint32)
+            O = np.zeros(i["occurrences"], dtype=np.uint32)
+            self.ctx._check(self.ctx.lib.qgm_index_download(self.ctx.h, self.h, _ptr(I), _ptr(S), _ptr(S1), _ptr(O)))
+            self._arrays = (I, S, S1, O)
+        return self._arrays
+
+    occupancy = property(lambda self: self.arrays()[0])
+    group_starts = property(lambda self: self.arrays()[1])
+    occ_starts = property(lambda self: self.arrays()[2])
+    positions = property(lambda self: self.arrays()[3])
+
+    def index_pair(self, codes):
+        codes = np.ascontiguousarray(np.atleast_1d(codes), dtype=np.uint32)
+        b = np.zeros(codes.size, dtype=np.uint32)
+        e = np.zeros(codes.size, dtype=np.uint32)
+        self.ctx._check(self.ctx.lib.qgm_index_lookup(self.ctx.h, self.h, _ptr(codes), codes.size, _ptr(b), _ptr(e)))
+        return b, e
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.qgm_index_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,744 @@
+// capi.cu -- the extern "C" boundary (include/qgm_c.h): context and object
+// lifetime, host<->device staging, and the orchestration of the five stages
+// for qgm_map. No exception crosses this file's exported functions.
+#include <cstring>
+#include <memory>
+
+#include "../../include/qgm_c.h"
+#include "internal.hpp"
+
+struct qgm_ctx {
+  qgm::Ctx c;
+};
+struct qgm_reads {
+  qgm_ctx* owner;
+  qgm::Reads r;
+};
+struct qgm_ref {
+  qgm_ctx* owner;
+  qgm::Ref r;
+};
+struct qgm_index {
+  qgm_ctx* owner;
+  qgm::Index i;
+};
+struct qgm_cands {
+  qgm_ctx* owner;
+  qgm::Cands c;
+};
+struct qgm_hits {
+  qgm_ctx* owner;
+  qgm::HitsObj h;
+};
+
+namespace qgm {
+
+// ------------------------------------------------------------------ Ctx
+cudaEvent_t Ctx::take_event() {
+  if (!ev_pool.empty()) {
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  QGM_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void Ctx::stage_begin(int s) {
+  if (!profile || cur_stage >= 0) return;  // nested stages are folded into the outer one
+  cur_stage = s;
+  cur_a = take_event();
+  QGM_CUDA(cudaEventRecord(cur_a, stream));
+}
+
+void Ctx::stage_end() {
+  if (!profile || cur_stage < 0) return;
+  cudaEvent_t b = take_event();
+  QGM_CUDA(cudaEventRecord(b, stream));
+  marks.push_back({cur_stage, cur_a, b});
+  cur_stage = -1;
+  cur_a = nullptr;
+}
+
+void Ctx::fold_marks() {
+  for (auto& m : marks) {
+    QGM_CUDA(cudaEventSynchronize(m.b));
+    float ms = 0;
+    QGM_CUDA(cudaEventElapsedTime(&ms, m.a, m.b));
+    stage_ms[m.stage] += ms;
+    ev_pool.push_back(m.a);
+    ev_pool.push_back(m.b);
+  }
+  marks.clear();
+}
+
+namespace {
+
+// ------------------------------------------------------------------ planes
+__device__ __forceinline__ uint32_t compress_even(uint64_t x) {  // bit 2i -> bit i
+  x &= 0x5555555555555555ull;
+  x = (x | (x >> 1)) & 0x3333333333333333ull;
+  x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+  x = (x | (x >> 4)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x >> 8)) & 0x0000FFFF0000FFFFull;
+  x = (x | (x >> 16)) & 0x00000000FFFFFFFFull;
+  return uint32_t(x);
+}
+
+// 2-bit word (32 bases, MSB-first) -> {lo bits, hi bits}, bit 31-j = base j.
+__device__ __forceinline__ uint2 to_planes(uint64_t w) { return make_uint2(compress_even(w), compress_even(w >> 1)); }
+
+__global__ void k_read_planes(const uint64_t* __restrict__ words, uint32_t n_reads, uint32_t W, uint32_t Wp,
+                              uint2* __restrict__ planes) {
+  const uint64_t total = uint64_t(n_reads) * Wp;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total; t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = t / Wp;
+    const uint32_t c = uint32_t(t - r * Wp);
+    planes[t] = (c >= 1 && c <= W) ? to_planes(words[r * W + c - 1]) : make_uint2(0u, 0u);
+  }
+}
+
+__global__ void k_ref_planes(const uint64_t* __restrict__ words, uint64_t nw, uint2* __restrict__ planes) {
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < nw; k += uint64_t(gridDim.x) * blockDim.x)
+    planes[k + 2] = to_planes(words[k]);
+}
+
+__global__ void k_max_u32(const uint32_t* __restrict__ v, uint64_t n, uint32_t* __restrict__ out) {
+  uint32_t m = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    m = max(m, v[i]);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
+  if (lane_id() == 0) atomicMax(out, m);
+}
+
+unsigned read_bits_for(uint32_t n_reads) { return std::max(1u, bit_width_u64(n_reads ? n_reads - 1 : 0)); }
+
+}  // namespace
+
+void make_read_planes(Ctx& c, Reads& r) {
+  r.Wp = r.W + 2;
+  r.planes.alloc(c, std::max<uint64_t>(uint64_t(r.n) * r.Wp, 1));
+  const uint64_t total = uint64_t(r.n) * r.Wp;
+  if (total)
+    QGM_KERNEL(c, k_read_planes, unsigned(std::min<uint64_t>(ceil_div(total, 256), kSMs * 16)), 256, 0, r.words.p,
+               r.n, r.W, r.Wp, r.planes.p);
+}
+
+void make_ref_planes(Ctx& c, Ref& ref) {
+  const uint64_t nw = ceil_div(ref.total, 32);
+  ref.planes.alloc(c, nw + 4);
+  ref.planes.zero();
+  if (nw)
+    QGM_KERNEL(c, k_ref_planes, unsigned(std::min<uint64_t>(ceil_div(nw, 256), kSMs * 16)), 256, 0, ref.words.p, nw,
+               ref.planes.p);
+}
+
+// ------------------------------------------------------------------ pipeline
+static void finish_reads(Ctx& c, Reads& r) {
+  make_read_planes(c, r);
+  DBuf<uint32_t> mx(c, 1);
+  mx.zero();
+  if (r.n)
+    QGM_KERNEL(c, k_max_u32, unsigned(std::min<uint64_t>(ceil_div(r.n, 256), kSMs * 4)), 256, 0, r.lengths.p,
+               uint64_t(r.n), mx.p);
+  QGM_CUDA(cudaMemcpyAsync(&r.max_len, mx.p, 4, cudaMemcpyDeviceToHost, c.stream));
+  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  if (r.max_len > r.stride) throw InputError("read longer than the stride");
+}
+
+static void check_reads_shape(uint32_t n_reads, uint32_t stride) {
+  if (uint64_t(n_reads) * stride > 0xFFFFFFFFull) throw InputError("read text exceeds 2^32 positions");
+  if (n_reads > (1u << 27)) throw InputError("at most 2^27 reads per batch");
+}
+
+static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_map_params& P) {
+  if (P.q == 0 || P.q > 16) throw InputError("q must be in [1, 16]");
+  if (P.band_width == 0 || P.band_width > 64) throw InputError("band width must be in [1, 64]");
+  if (P.pct_identity > 100) throw InputError("percent identity must be in [0, 100]");
+  if (P.mode > 1) throw InputError("mode must be best-stratum (0) or all (1)");
+  const int strands = P.strands ? int(P.strands) : 3;
+  const unsigned rb = read_bits_for(reads.n);
+  const int key_bits = int(rb + 1 + ref.diag_bits);
+  HitsObj out;
+  Index idx;
+  {
+    StageScope s(c, kStageIndex);
+    build_index(c, reads, P.q, P.group_width ? P.group_width : 32, P.sampled != 0, idx);
+  }
+  DBuf<uint64_t> keys, alt;
+  uint64_t n_raw, n_u;
+  {
+    StageScope s(c, kStageFilter);
+    n_raw = filter_reference(c, idx, reads, ref, strands, QGM_FILTER_RUN_START, rb, keys);
+  }
+  idx = Index();  // the index is per batch; release it before validation
+  {
+    StageScope s(c, kStageSort);
+    radix_sort(c, keys, alt, nullptr, nullptr, n_raw, 0, key_bits);
+    if (alt.n < n_raw) alt.alloc(c, std::max<uint64_t>(n_raw, 1));
+    n_u = select_u64(c, keys.p, nullptr, nullptr, n_raw, alt.p, nullptr);
+  }
+  DBuf<uint64_t> hkeys(c, std::max<uint64_t>(n_u, 1)), hkeys_alt;
+  DBuf<uint32_t> hvals(c, std::max<uint64_t>(n_u, 1)), hvals_alt;
+  uint64_t n_val = 0;
+  {
+    StageScope s(c, kStageValidate);
+    DBuf<unsigned long long> cnt(c, 1);
+    cnt.zero();
+    validate_candidates(c, reads, ref, alt.p, n_u, rb, P.band_width, P.pct_identity, 0, hkeys.p, hvals.p, cnt.p,
+                        nullptr);
+    unsigned long long h = 0;
+    QGM_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    n_val = h;
+  }
+  keys.release();
+  alt.release();
+  {
+    StageScope s(c, kStageStrata);
+    radix_sort(c, hkeys, hkeys_alt, &hvals, &hvals_alt, n_val, 0, key_bits);
+    out.n = stratify_hits(c, ref, hkeys.p, hvals.p, n_val, reads.n, rb, int(P.mode), out.hits);
+  }
+  out.stats[0] = n_raw;
+  out.stats[1] = n_u;
+  out.stats[2] = n_val;
+  out.stats[3] = out.n;
+  return out;
+}
+
+}  // namespace qgm
+
+// ===================================================================== C ABI
+namespace {
+
+template <class Fn>
+int guard(qgm_ctx* ctx, Fn&& fn) {
+  try {
+    fn();
+    return QGM_OK;
+  } catch (const qgm::InputError& e) {
+    if (ctx) ctx->c.err = e.what();
+    return QGM_ERR_INPUT;
+  } catch (const qgm::InternalError& e) {
+    if (ctx) ctx->c.err = e.what();
+    return QGM_ERR_INTERNAL;
+  } catch (const qgm::CudaError& e) {
+    if (ctx) ctx->c.err = e.what();
+    return QGM_ERR_CUDA;
+  } catch (const std::bad_alloc& e) {
+    if (ctx) ctx->c.err = std::string("host allocation failed: ") + e.what();
+    return QGM_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->c.err = e.what();
+    return QGM_ERR_INTERNAL;
+  }
+}
+
+void require(bool ok, const char* what) {
+  if (!ok) throw qgm::InputError(what);
+}
+
+void activate(qgm_ctx* ctx) { QGM_CUDA(cudaSetDevice(ctx->c.device)); }
+
+}  // namespace
+
+extern "C" {
+
+int qgm_ctx_create(int device, qgm_ctx** out) {
+  if (!out) return QGM_ERR_INPUT;
+  *out = nullptr;
+  auto ctx = std::make_unique<qgm_ctx>();
+  int rc = guard(ctx.get(), [&] {
+    int n = 0;
+    QGM_CUDA(cudaGetDeviceCount(&n));
+    require(device >= 0 && device < n, "no such CUDA device");
+    ctx->c.device = device;
+    QGM_CUDA(cudaSetDevice(device));
+    QGM_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+    ctx->c.own_stream = true;
+    cudaMemPool_t pool;
+    QGM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = ~uint64_t(0);
+    QGM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  });
+  if (rc == QGM_OK) *out = ctx.release();
+  return rc;
+}
+
+int qgm_ctx_set_stream(qgm_ctx* ctx, void* stream) {
+  if (!ctx) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    QGM_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    if (stream) {
+      if (ctx->c.own_stream) QGM_CUDA(cudaStreamDestroy(ctx->c.stream));
+      ctx->c.stream = static_cast<cudaStream_t>(stream);
+      ctx->c.own_stream = false;
+    } else if (!ctx->c.own_stream) {
+      QGM_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+      ctx->c.own_stream = true;
+    }
+  });
+}
+
+void* qgm_ctx_stream(qgm_ctx* ctx) { return ctx ? ctx->c.stream : nullptr; }
+
+void qgm_ctx_destroy(qgm_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->c.device);
+  cudaStreamSynchronize(ctx->c.stream);
+  for (auto& m : ctx->c.marks) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
+  for (auto e : ctx->c.ev_pool) cudaEventDestroy(e);
+  if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+  delete ctx;
+}
+
+const char* qgm_last_error(const qgm_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "null context"; }
+
+int qgm_ctx_synchronize(qgm_ctx* ctx) {
+  if (!ctx) return QGM_ERR_INPUT;
+  return guard(ctx, [&] { QGM_CUDA(cudaStreamSynchronize(ctx->c.stream)); });
+}
+
+int qgm_ctx_profile(qgm_ctx* ctx, int enable) {
+  if (!ctx) return QGM_ERR_INPUT;
+  ctx->c.profile = enable != 0;
+  return QGM_OK;
+}
+
+int qgm_ctx_stage_times(qgm_ctx* ctx, double* ms, int n, int reset) {
+  if (!ctx) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    ctx->c.fold_marks();
+    for (int i = 0; i < n && i < qgm::kNumStages; ++i) ms[i] = ctx->c.stage_ms[i];
+    if (reset) for (double& v : ctx->c.stage_ms) v = 0;
+  });
+}
+
+uint64_t qgm_ctx_launches(qgm_ctx* ctx, int reset) {
+  if (!ctx) return 0;
+  const uint64_t n = ctx->c.launches;
+  if (reset) ctx->c.launches = 0;
+  return n;
+}
+
+int qgm_pack_codes(const uint8_t* codes, uint64_t n, uint64_t* words) {
+  if ((!codes && n) || (!words && n)) return QGM_ERR_INPUT;
+  const uint64_t nw = (n + 31) / 32;
+  for (uint64_t k = 0; k < nw; ++k) {
+    uint64_t w = 0;
+    const uint64_t b = k * 32, e = std::min<uint64_t>(n, b + 32);
+    for (uint64_t j = b; j < e; ++j) {
+      if (codes[j] > 3) return QGM_ERR_INPUT;
+      w |= uint64_t(codes[j]) << (62 - 2 * (j - b));
+    }
+    words[k] = w;
+  }
+  return QGM_OK;
+}
+
+int qgm_pack_reads(const uint8_t* codes, uint32_t stride, uint32_t n_reads, uint64_t* words) {
+  const uint32_t W = (stride + 31) / 32;
+  for (uint32_t r = 0; r < n_reads; ++r) {
+    int rc = qgm_pack_codes(codes + uint64_t(r) * stride, stride, words + uint64_t(r) * W);
+    if (rc) return rc;
+  }
+  return QGM_OK;
+}
+
+static int reads_common(qgm_ctx* ctx, const uint64_t* w, const uint32_t* len, uint32_t n_reads, uint32_t stride,
+                        qgm_reads** out, cudaMemcpyKind kind) {
+  if (!ctx || !out) return QGM_ERR_INPUT;
+  *out = nullptr;
+  auto rd = std::make_unique<qgm_reads>();
+  rd->owner = ctx;
+  int rc = guard(ctx, [&] {
+    activate(ctx);
+    qgm::Ctx& c = ctx->c;
+    qgm::check_reads_shape(n_reads, stride);
+    require(n_reads == 0 || (w && len), "null read buffers");
+    qgm::StageScope s(c, qgm::kStageReads);
+    auto& r = rd->r;
+    r.n = n_reads;
+    r.stride = stride;
+    r.W = (stride + 31) / 32;
+    const uint64_t nw = uint64_t(n_reads) * r.W;
+    r.words.alloc(c, nw + 1);
+    r.lengths.alloc(c, std::max<uint32_t>(n_reads, 1));
+    if (nw) QGM_CUDA(cudaMemcpyAsync(r.words.p, w, nw * 8, kind, c.stream));
+    QGM_CUDA(cudaMemsetAsync(r.words.p + nw, 0, 8, c.stream));
+    if (n_reads) QGM_CUDA(cudaMemcpyAsync(r.lengths.p, len, uint64_t(n_reads) * 4, kind, c.stream));
+    qgm::finish_reads(c, r);
+  });
+  if (rc == QGM_OK) *out = rd.release();
+  return rc;
+}
+
+int qgm_reads_upload(qgm_ctx* ctx, const uint64_t* w, const uint32_t* len, uint32_t n_reads, uint32_t stride,
+                     qgm_reads** out) {
+  return reads_common(ctx, w, len, n_reads, stride, out, cudaMemcpyHostToDevice);
+}
+
+int qgm_reads_from_device(qgm_ctx* ctx, const uint64_t* w, const uint32_t* len, uint32_t n_reads, uint32_t stride,
+                          qgm_reads** out) {
+  return reads_common(ctx, w, len, n_reads, stride, out, cudaMemcpyDeviceToDevice);
+}
+
+void qgm_reads_destroy(qgm_reads* r) {
+  if (!r) return;
+  cudaSetDevice(r->owner->c.device);
+  delete r;
+}
+
+int qgm_index_build(qgm_ctx* ctx, const qgm_reads* reads, uint32_t q, uint32_t w, int sampled, qgm_index** out) {
+  if (!ctx || !reads || !out) return QGM_ERR_INPUT;
+  *out = nullptr;
+  auto ix = std::make_unique<qgm_index>();
+  ix->owner = ctx;
+  int rc = guard(ctx, [&] {
+    activate(ctx);
+    qgm::StageScope s(ctx->c, qgm::kStageIndex);
+    qgm::build_index(ctx->c, reads->r, q, w, sampled != 0, ix->i);
+  });
+  if (rc == QGM_OK) *out = ix.release();
+  return rc;
+}
+
+int qgm_index_sample(qgm_ctx* ctx, const qgm_index* in, qgm_index** out) {
+  if (!ctx || !in || !out) return QGM_ERR_INPUT;
+  *out = nullptr;
+  auto ix = std::make_unique<qgm_index>();
+  ix->owner = ctx;
+  int rc = guard(ctx, [&] {
+    activate(ctx);
+    qgm::sample_index(ctx->c, in->i, ix->i);
+  });
+  if (rc == QGM_OK) *out = ix.release();
+  return rc;
+}
+
+int qgm_index_normalize(qgm_ctx* ctx, qgm_index* idx) {
+  if (!ctx || !idx) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    qgm::normalize_index(ctx->c, idx->i);
+  });
+}
+
+int qgm_index_info_get(const qgm_index* idx, qgm_index_info* o) {
+  if (!idx || !o) return QGM_ERR_INPUT;
+  const auto& i = idx->i;
+  o->q = i.q;
+  o->group_width = i.w;
+  o->sampled = i.sampled;
+  o->reserved = 0;
+  o->group_count = i.groups;
+  o->group_starts_len = i.gs_len;
+  o->distinct = i.distinct;
+  o->occurrences = i.occ;
+  return QGM_OK;
+}
+
+int qgm_index_download(qgm_ctx* ctx, const qgm_index* idx, void* I, uint32_t* S, uint32_t* S1, uint32_t* O) {
+  if (!ctx || !idx) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    const auto& i = idx->i;
+    cudaStream_t st = ctx->c.stream;
+    if (I && i.groups) QGM_CUDA(cudaMemcpyAsync(I, i.I.p, i.groups * (i.w / 8), cudaMemcpyDeviceToHost, st));
+    if (S) QGM_CUDA(cudaMemcpyAsync(S, i.S.p, i.gs_len * 4, cudaMemcpyDeviceToHost, st));
+    if (S1) QGM_CUDA(cudaMemcpyAsync(S1, i.S1.p, (i.distinct + 1) * 4, cudaMemcpyDeviceToHost, st));
+    if (O && i.occ) QGM_CUDA(cudaMemcpyAsync(O, i.O.p, i.occ * 4, cudaMemcpyDeviceToHost, st));
+    QGM_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int qgm_index_lookup(qgm_ctx* ctx, const qgm_index* idx, const uint32_t* codes, uint64_t n, uint32_t* begin,
+                     uint32_t* end) {
+  if (!ctx || !idx) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    qgm::Ctx& c = ctx->c;
+    const uint64_t space = uint64_t(1) << (2 * idx->i.q);
+    for (uint64_t t = 0; t < n; ++t) require(codes[t] < space, "q-gram code out of range");
+    qgm::DBuf<uint32_t> dc(c, std::max<uint64_t>(n, 1)), db(c, std::max<uint64_t>(n, 1)),
+        de(c, std::max<uint64_t>(n, 1));
+    if (n) QGM_CUDA(cudaMemcpyAsync(dc.p, codes, n * 4, cudaMemcpyHostToDevice, c.stream));
+    qgm::lookup_index(c, idx->i, dc.p, n, db.p, de.p);
+    if (n) {
+      QGM_CUDA(cudaMemcpyAsync(begin, db.p, n * 4, cudaMemcpyDeviceToHost, c.stream));
+      QGM_CUDA(cudaMemcpyAsync(end, de.p, n * 4, cudaMemcpyDeviceToHost, c.stream));
+    }
+    QGM_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+void qgm_index_destroy(qgm_index* idx) {
+  if (!idx) return;
+  cudaSetDevice(idx->owner->c.device);
+  delete idx;
+}
+
+int qgm_ref_upload(qgm_ctx* ctx, const uint64_t* ref2bit, const uint64_t* chrom_begin, uint32_t n_chrom,
+                   const uint64_t* mask_bits, qgm_ref** out) {
+  if (!ctx || !out) return QGM_ERR_INPUT;
+  *out = nullptr;
+  auto rf = std::make_unique<qgm_ref>();
+  rf->owner = ctx;
+  int rc = guard(ctx, [&] {
+    activate(ctx);
+    qgm::Ctx& c = ctx->c;
+    require(n_chrom >= 1 && chrom_begin, "need at least one chromosome");
+    require(chrom_begin[0] == 0, "chrom_begin[0] must be 0");
+    for (uint32_t k = 0; k < n_chrom; ++k) {
+      require(chrom_begin[k + 1] >= chrom_begin[k], "chrom_begin must be non-decreasing");
+      require(chrom_begin[k + 1] - chrom_begin[k] < 0xFFFFFFFFull, "chromosome longer than 2^32-1 bases");
+    }
+    auto& r = rf->r;
+    r.n_chrom = n_chrom;
+    r.total = chrom_begin[n_chrom];
+    require(r.total == 0 || ref2bit, "null reference buffer");
+    r.gap = uint64_t(1) << 16;
+    r.cb.assign(chrom_begin, chrom_begin + n_chrom + 1);
+    r.cbp.resize(n_chrom + 1);
+    for (uint32_t k = 0; k <= n_chrom; ++k) r.cbp[k] = r.cb[k] + uint64_t(k + 1) * r.gap;
+    r.padded_total = r.total + uint64_t(n_chrom + 1) * r.gap;
+    r.diag_bits = qgm::bit_width_u64(r.padded_total);
+    require(r.diag_bits <= 40, "reference too large");
+    const uint64_t nw = qgm::ceil_div(r.total, 32);
+    r.words.alloc(c, nw + 1);
+    if (nw) QGM_CUDA(cudaMemcpyAsync(r.words.p, ref2bit, nw * 8, cudaMemcpyHostToDevice, c.stream));
+    QGM_CUDA(cudaMemsetAsync(r.words.p + nw, 0, 8, c.stream));
+    r.d_cb.alloc(c, n_chrom + 1);
+    r.d_cbp.alloc(c, n_chrom + 1);
+    QGM_CUDA(cudaMemcpyAsync(r.d_cb.p, r.cb.data(), (n_chrom + 1) * 8, cudaMemcpyHostToDevice, c.stream));
+    QGM_CUDA(cudaMemcpyAsync(r.d_cbp.p, r.cbp.data(), (n_chrom + 1) * 8, cudaMemcpyHostToDevice, c.stream));
+    if (mask_bits) {
+      const uint64_t mw = qgm::ceil_div(r.total, 64);
+      r.mask.alloc(c, std::max<uint64_t>(mw, 1));
+      if (mw) QGM_CUDA(cudaMemcpyAsync(r.mask.p, mask_bits, mw * 8, cudaMemcpyHostToDevice, c.stream));
+    }
+    qgm::make_ref_planes(c, r);
+    QGM_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  if (rc == QGM_OK) *out = rf.release();
+  return rc;
+}
+
+void qgm_ref_destroy(qgm_ref* r) {
+  if (!r) return;
+  cudaSetDevice(r->owner->c.device);
+  delete r;
+}
+
+int qgm_filter(qgm_ctx* ctx, const qgm_index* idx, const qgm_reads* reads, const qgm_ref* ref, int strands, int mode,
+               qgm_cands** out) {
+  if (!ctx || !idx || !reads || !ref || !out) return QGM_ERR_INPUT;
+  *out = nullptr;
+  auto cd = std::make_unique<qgm_cands>();
+  cd->owner = ctx;
+  int rc = guard(ctx, [&] {
+    activate(ctx);
+    require(strands >= 1 && strands <= 3, "strands must be 1, 2 or 3");
+    require(mode == QGM_FILTER_FULL || mode == QGM_FILTER_RUN_START, "unknown filter mode");
+    qgm::Ctx& c = ctx->c;
+    auto& C = cd->c;
+    C.read_bits = qgm::read_bits_for(reads->r.n);
+    C.diag_bits = ref->r.diag_bits;
+    C.cbp = ref->r.cbp;
+    {
+      qgm::StageScope s(c, qgm::kStageFilter);
+      C.n = qgm::filter_reference(c, idx->i, reads->r, ref->r, strands, mode, C.read_bits, C.keys);
+    }
+    qgm::StageScope s(c, qgm::kStageSort);
+    qgm::DBuf<uint64_t> alt;
+    qgm::radix_sort(c, C.keys, alt, nullptr, nullptr, C.n, 0, int(C.read_bits + 1 + C.diag_bits));
+  });
+  if (rc == QGM_OK) *out = cd.release();
+  return rc;
+}
+
+int qgm_cands_count(const qgm_cands* c, uint64_t* n) {
+  if (!c || !n) return QGM_ERR_INPUT;
+  *n = c->c.n;
+  return QGM_OK;
+}
+
+int qgm_cands_unique(qgm_ctx* ctx, qgm_cands* cd) {
+  if (!ctx || !cd) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    qgm::Ctx& c = ctx->c;
+    auto& C = cd->c;
+    qgm::DBuf<uint64_t> u(c, std::max<uint64_t>(C.n, 1));
+    C.n = qgm::select_u64(c, C.keys.p, nullptr, nullptr, C.n, u.p, nullptr);
+    C.keys.swap(u);
+  });
+}
+
+int qgm_cands_download(qgm_ctx* ctx, const qgm_cands* cd, qgm_candidate* out) {
+  if (!ctx || !cd || (!out && cd->c.n)) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    const auto& C = cd->c;
+    std::vector<uint64_t> k(C.n);
+    if (C.n) QGM_CUDA(cudaMemcpyAsync(k.data(), C.keys.p, C.n * 8, cudaMemcpyDeviceToHost, ctx->c.stream));
+    QGM_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    const uint64_t dmask = (uint64_t(1) << C.diag_bits) - 1;
+    const uint64_t gap = C.cbp.size() >= 2 ? (C.cbp[0]) : 0;  // cbp[0] = gap
+    for (uint64_t i = 0; i < C.n; ++i) {
+      const uint64_t key = k[i];
+      const uint64_t gp = key & dmask;
+      // largest c with cbp[c] - gap <= gp
+      size_t lo = 0, hi = C.cbp.size() - 1;
+      while (hi - lo > 1) {
+        size_t mid = (lo + hi) / 2;
+        if (C.cbp[mid] - gap <= gp) lo = mid; else hi = mid;
+      }
+      out[i].diagonal = int64_t(gp) - int64_t(C.cbp[lo]);
+      out[i].read_id = uint32_t(key >> (C.diag_bits + 1));
+      out[i].chrom = uint32_t(lo);
+      out[i].strand = uint32_t((key >> C.diag_bits) & 1);
+      out[i].reserved = 0;
+    }
+  });
+}
+
+void qgm_cands_destroy(qgm_cands* c) {
+  if (!c) return;
+  cudaSetDevice(c->owner->c.device);
+  delete c;
+}
+
+int qgm_validate(qgm_ctx* ctx, const qgm_reads* reads, const qgm_ref* ref, const qgm_candidate* cands, uint64_t n,
+                 uint32_t band, uint32_t pct, qgm_validated* out) {
+  if (!ctx || !reads || !ref || ((!cands || !out) && n)) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    qgm::Ctx& c = ctx->c;
+    const auto& R = ref->r;
+    const unsigned rb = qgm::read_bits_for(reads->r.n);
+    require(rb + 1 + R.diag_bits <= 64, "read batch too large for the 64-bit key");
+    std::vector<uint64_t> keys(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      const auto& cd = cands[i];
+      require(cd.read_id < reads->r.n, "candidate read id out of range");
+      require(cd.chrom < R.n_chrom, "candidate chromosome out of range");
+      require(cd.strand <= 1, "candidate strand must be 0 or 1");
+      const int64_t Lc = int64_t(R.cb[cd.chrom + 1] - R.cb[cd.chrom]);
+      require(cd.diagonal > -int64_t(R.gap) + 64 && cd.diagonal < Lc, "candidate diagonal out of range");
+      keys[i] = (uint64_t(cd.read_id) << (R.diag_bits + 1)) | (uint64_t(cd.strand) << R.diag_bits) |
+                uint64_t(int64_t(R.cbp[cd.chrom]) + cd.diagonal);
+    }
+    qgm::StageScope s(c, qgm::kStageValidate);
+    qgm::DBuf<uint64_t> dk(c, std::max<uint64_t>(n, 1));
+    qgm::DBuf<uint8_t> dv(c, std::max<uint64_t>(n * 20, 20));
+    if (n) QGM_CUDA(cudaMemcpyAsync(dk.p, keys.data(), n * 8, cudaMemcpyHostToDevice, c.stream));
+    qgm::validate_candidates(c, reads->r, R, dk.p, n, rb, band, pct, 1, nullptr, nullptr, nullptr, dv.p);
+    std::vector<uint32_t> raw(n * 5);
+    if (n) QGM_CUDA(cudaMemcpyAsync(raw.data(), dv.p, n * 20, cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    for (uint64_t i = 0; i < n; ++i) {
+      out[i].edits = int32_t(raw[i * 5]);
+      out[i].start = raw[i * 5 + 1];
+      out[i].ref_start = raw[i * 5 + 2];
+      out[i].kept = uint8_t(raw[i * 5 + 3] & 0xFF);
+      out[i].in_range = uint8_t((raw[i * 5 + 3] >> 8) & 0xFF);
+      out[i].reserved0 = out[i].reserved1 = 0;
+      out[i].reserved2 = 0;
+    }
+  });
+}
+
+int qgm_map(qgm_ctx* ctx, const qgm_reads* reads, const qgm_ref* ref, const qgm_map_params* P, qgm_hits** out) {
+  if (!ctx || !reads || !ref || !P || !out) return QGM_ERR_INPUT;
+  *out = nullptr;
+  auto h = std::make_unique<qgm_hits>();
+  h->owner = ctx;
+  int rc = guard(ctx, [&] {
+    activate(ctx);
+    h->h = qgm::map_reads(ctx->c, reads->r, ref->r, *P);
+  });
+  if (rc == QGM_OK) *out = h.release();
+  return rc;
+}
+
+int qgm_hits_count(const qgm_hits* h, uint64_t* n) {
+  if (!h || !n) return QGM_ERR_INPUT;
+  *n = h->h.n;
+  return QGM_OK;
+}
+
+int qgm_hits_stats(const qgm_hits* h, qgm_map_stats* o) {
+  if (!h || !o) return QGM_ERR_INPUT;
+  o->raw_candidates = h->h.stats[0];
+  o->unique_candidates = h->h.stats[1];
+  o->validated = h->h.stats[2];
+  o->hits = h->h.stats[3];
+  return QGM_OK;
+}
+
+int qgm_hits_download(qgm_ctx* ctx, const qgm_hits* h, qgm_hit* out) {
+  if (!ctx || !h || (!out && h->h.n)) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    qgm::StageScope s(ctx->c, qgm::kStageD2H);
+    if (h->h.n)
+      QGM_CUDA(cudaMemcpyAsync(out, h->h.hits.p, h->h.n * 16, cudaMemcpyDeviceToHost, ctx->c.stream));
+    QGM_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+void qgm_hits_destroy(qgm_hits* h) {
+  if (!h) return;
+  cudaSetDevice(h->owner->c.device);
+  delete h;
+}
+
+int qgm_map_host(qgm_ctx* ctx, const uint64_t* reads2bit, const uint32_t* lengths, uint32_t n_reads, uint32_t stride,
+                 const qgm_ref* ref, const qgm_map_params* P, qgm_hit* out, uint64_t cap, uint64_t* n_out,
+                 qgm_map_stats* stats) {
+  if (!ctx || !ref || !P || !n_out) return QGM_ERR_INPUT;
+  qgm_reads* rd = nullptr;
+  int rc = qgm_reads_upload(ctx, reads2bit, lengths, n_reads, stride, &rd);
+  if (rc) return rc;
+  qgm_hits* h = nullptr;
+  rc = qgm_map(ctx, rd, ref, P, &h);
+  if (rc == QGM_OK) {
+    *n_out = h->h.n;
+    if (stats) qgm_hits_stats(h, stats);
+    if (h->h.n > cap) {
+      ctx->c.err = "output capacity too small";
+      rc = QGM_ERR_INPUT;
+    } else {
+      rc = qgm_hits_download(ctx, h, out);
+    }
+  }
+  qgm_hits_destroy(h);
+  qgm_reads_destroy(rd);
+  return rc;
+}
+
+int qgm_exclusive_scan_u32(qgm_ctx* ctx, const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* total) {
+  if (!ctx || ((!in || !out) && n)) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    qgm::Ctx& c = ctx->c;
+    qgm::DBuf<uint32_t> d(c, std::max<uint64_t>(n, 1));
+    qgm::DBuf<uint32_t> t(c, 1);
+    qgm::DBuf<int> ov(c, 1);
+    if (n) QGM_CUDA(cudaMemcpyAsync(d.p, in, n * 4, cudaMemcpyHostToDevice, c.stream));
+    qgm::exclusive_scan_u32(c, d.p, d.p, n, t.p, ov.p);
+    int o = 0;
+    uint32_t tot = 0;
+    QGM_CUDA(cudaMemcpyAsync(&o, ov.p, 4, cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaMemcpyAsync(&tot, t.p, 4, cudaMemcpyDeviceToHost, c.stream));
+    if (n) QGM_CUDA(cudaMemcpyAsync(out, d.p, n * 4, cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    if (o) throw qgm::InputError("prefix sum overflows the index word");
+    if (total) *total = tot;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,161 @@
+// common.cuh -- shared device helpers for the sm_100a read-mapping kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace qgm {
+
+// ------------------------------------------------------------------ errors
+struct InputError : std::runtime_error {  // -> QGM_ERR_INPUT (qgmap::input_error)
+  explicit InputError(const std::string& w) : std::runtime_error(w) {}
+};
+struct InternalError : std::runtime_error {  // -> QGM_ERR_INTERNAL (std::logic_error)
+  explicit InternalError(const std::string& w) : std::runtime_error(w) {}
+};
+struct CudaError : std::runtime_error {  // -> QGM_ERR_CUDA
+  explicit CudaError(const std::string& w) : std::runtime_error(w) {}
+};
+
+#define QGM_CUDA(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t qgm_e_ = (expr);                                                            \
+    if (qgm_e_ != cudaSuccess)                                                              \
+      throw ::qgm::CudaError(std::string(#expr) + ": " + cudaGetErrorString(qgm_e_) + " (" + \
+                             __FILE__ + ":" + std::to_string(__LINE__) + ")");              \
+  } while (0)
+
+#define QGM_LAUNCH_CHECK() QGM_CUDA(cudaGetLastError())
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+
+__host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------ 2-bit codec
+// Base j of a 2-bit MSB-first stream: bits [62-2(j%32), 63-2(j%32)] of word j/32.
+__device__ __forceinline__ uint32_t base_at(const uint64_t* __restrict__ w, uint64_t j) {
+  return uint32_t(__ldg(w + (j >> 5)) >> (62 - 2 * (j & 31))) & 3u;
+}
+
+// q-gram code at base offset j (encode_qgram, seq.hpp:80-84: first base in the
+// most significant digit). Requires one readable word past the last base.
+__device__ __forceinline__ uint32_t qgram_at(const uint64_t* __restrict__ w, uint64_t j, unsigned q) {
+  const uint64_t k = j >> 5;
+  const unsigned s = unsigned(j & 31) * 2;
+  uint64_t hi = __ldg(w + k) << s;
+  if (s) hi |= __ldg(w + k + 1) >> (64 - s);
+  return uint32_t(hi >> (64 - 2 * q));
+}
+
+// Code of the reverse complement of the q-gram with code g: complement every
+// 2-bit digit (c -> 3-c == c^3) and reverse the digit order.
+__device__ __forceinline__ uint32_t rc_code(uint32_t g, unsigned q) {
+  uint32_t x = ~g;
+  x = __brev(x);
+  x = ((x >> 1) & 0x55555555u) | ((x & 0x55555555u) << 1);
+  return x >> (32 - 2 * q);
+}
+
+// ------------------------------------------------------------------ group words
+template <class W> struct GroupTraits;
+template <> struct GroupTraits<uint32_t> {
+  static constexpr unsigned width = 32;
+  __device__ static __forceinline__ unsigned popc(uint32_t x) { return __popc(x); }
+};
+template <> struct GroupTraits<uint64_t> {
+  static constexpr unsigned width = 64;
+  __device__ static __forceinline__ unsigned popc(uint64_t x) { return __popcll(x); }
+};
+
+// Grouprank (qgroup_index.hpp:80-83): set bits of `word` strictly below bit j.
+template <class W>
+__device__ __forceinline__ uint32_t rank_below(W word, unsigned j) {
+  const W m = (W(1) << j) - W(1);  // j < width; j==0 -> 0
+  return GroupTraits<W>::popc(word & m);
+}
+
+// ------------------------------------------------------------------ warp utils
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(kFull, v, o);
+    if (lane_id() >= unsigned(o)) v += n;
+  }
+  return v;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_reduce_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Exclusive scan of one value per thread across the block (blockDim.x <= 1024,
+// multiple of 32). `ws` must hold 33 entries. Returns the exclusive prefix;
+// *total receives the block sum. Contains __syncthreads.
+template <class T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* ws, T* total) {
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  T inc = warp_inclusive_scan(v);
+  if (lane == 31) ws[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T s = lane < nw ? ws[lane] : T(0);
+    T si = warp_inclusive_scan(s);
+    if (lane < nw) ws[lane] = si - s;
+    if (lane == 31) ws[32] = si;  // nw <= 32: lane 31 holds the full sum
+  }
+  __syncthreads();
+  T res = ws[warp] + inc - v;
+  if (total) *total = ws[32];
+  __syncthreads();
+  return res;
+}
+
+// In-place exclusive scan of n (<= blockDim.x * per) u32 values in shared
+// memory; each thread scans a contiguous run. Returns the total. All threads
+// of the block must call it.
+__device__ __forceinline__ uint32_t block_scan_smem(uint32_t* a, uint32_t n, uint32_t* ws) {
+  const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+  const uint32_t b = threadIdx.x * per, e = min(n, b + per);
+  uint32_t s = 0;
+  for (uint32_t i = b; i < e; ++i) s += a[i];
+  uint32_t tot;
+  uint32_t run = block_exclusive_scan<uint32_t>(s, ws, &tot);
+  for (uint32_t i = b; i < e; ++i) {
+    uint32_t v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  __syncthreads();
+  return tot;
+}
+
+// Warp-aggregated append: every lane of the (converged) warp calls it; lanes
+// with pred get consecutive slots from *counter. Returns the slot (valid only
+// where pred).
+__device__ __forceinline__ unsigned long long warp_append(bool pred, unsigned long long* counter) {
+  const unsigned m = __ballot_sync(kFull, pred);
+  unsigned long long base = 0;
+  if (m) {
+    const int leader = __ffs(m) - 1;
+    if (int(lane_id()) == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
+    base = __shfl_sync(kFull, base, leader);
+  }
+  return base + __popc(m & lanemask_lt());
+}
+
+}  // namespace qgm

@@ -1,0 +1,359 @@
+// index_build.cu -- stage 1: on-the-fly q-group index over one read buffer.
+//
+// Same arrays and semantics as build_qgroup_index<W> (qgroup_index.hpp:124-180,
+// Alg. 1 of PAPER.md:153-193): occupancy I, group starts S (+ sentinel,
+// optionally sampled), per-q-gram occurrence starts S' (+ sentinel), positions
+// O bucketed by numeric q-gram order. Position order inside one interval is
+// unspecified, exactly as in the reference (qgroup_index.hpp:120-123);
+// qgm_index_normalize sorts it.
+//
+// B200 design (a two-level counting sort on the q-gram code instead of the
+// reference's six passes of random atomics into 4^q/w-sized arrays):
+//   K1 rank    : one thread per read q-gram; code g, bucket = g >> lb (top
+//                2q-lb bits); warp-aggregated atomicAdd on a per-bucket count
+//                (L2 resident) returns the item's rank inside its bucket.
+//   scan       : bucket offsets.
+//   K2 scatter : (g & lowmask, position) pairs into their bucket.
+//   K3 occupy  : one CTA per bucket (2^lb codes = 2^lb/w group words) builds the
+//                bucket's occupancy words in shared memory, writes I and the
+//                bucket's distinct count.
+//   scan       : distinct offsets (the global base of S for every bucket).
+//   K4 emit    : one CTA per bucket rebuilds the local ranks from I, writes
+//                S (popcount prefix), S' (occurrence prefix) and scatters the
+//                positions into O through shared-memory cursors.
+// Every HBM write of I/S/S'/O is coalesced; the only random traffic is the
+// bucket scatter, whose tails stay L2 resident.
+#include "internal.hpp"
+
+namespace qgm {
+namespace {
+
+constexpr unsigned kLowBits = 13;  // codes per bucket = 8192
+constexpr int kBuildThreads = 256;
+
+struct Geometry {
+  unsigned q, w, lb, hb;
+  uint64_t groups, buckets, gpb;  // gpb = group words per bucket
+};
+
+Geometry geometry(unsigned q, unsigned w) {
+  Geometry g;
+  g.q = q;
+  g.w = w;
+  g.lb = std::min(2 * q, kLowBits);
+  g.hb = 2 * q - g.lb;
+  const uint64_t space = uint64_t(1) << (2 * q);
+  g.groups = ceil_div(space, w);
+  g.buckets = uint64_t(1) << g.hb;
+  g.gpb = std::max<uint64_t>(1, (uint64_t(1) << g.lb) / w);
+  if (g.buckets * g.gpb != g.groups) throw InternalError("index geometry mismatch");
+  return g;
+}
+
+// One slot per (read, offset) with offset <= stride-q; slots past a read's
+// length are idle (seq.hpp:135-137: only windows inside a read are indexed).
+__global__ void k_bucket_rank(const uint64_t* __restrict__ words, const uint32_t* __restrict__ lengths,
+                              uint32_t n_reads, uint32_t W, uint32_t span, unsigned q, unsigned lb,
+                              uint32_t* __restrict__ bucket_cnt, uint32_t* __restrict__ rank) {
+  const uint64_t total = uint64_t(n_reads) * span;
+  for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < total; base += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t t = base + threadIdx.x;
+    bool ok = t < total;
+    uint32_t r = 0, o = 0, b = 0xFFFFFFFFu;
+    if (ok) {
+      r = uint32_t(t / span);
+      o = uint32_t(t - uint64_t(r) * span);
+      ok = o + q <= __ldg(lengths + r);
+      if (ok) b = qgram_at(words + uint64_t(r) * W, o, q) >> lb;
+    }
+    const unsigned peers = __match_any_sync(kFull, b);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base_rank = 0;
+    if (ok && int(lane_id()) == leader) base_rank = atomicAdd(bucket_cnt + b, __popc(peers));
+    base_rank = __shfl_sync(kFull, base_rank, leader);
+    if (ok) rank[t] = base_rank + __popc(peers & lanemask_lt());
+  }
+}
+
+__global__ void k_bucket_scatter(const uint64_t* __restrict__ words, const uint32_t* __restrict__ lengths,
+                                 uint32_t n_reads, uint32_t W, uint32_t span, uint32_t stride, unsigned q,
+                                 unsigned lb, const uint32_t* __restrict__ boff, const uint32_t* __restrict__ rank,
+                                 uint64_t* __restrict__ pairs) {
+  const uint64_t total = uint64_t(n_reads) * span;
+  const uint32_t lmask = (1u << lb) - 1u;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t r = uint32_t(t / span);
+    const uint32_t o = uint32_t(t - uint64_t(r) * span);
+    if (o + q > __ldg(lengths + r)) continue;
+    const uint32_t g = qgram_at(words + uint64_t(r) * W, o, q);
+    const uint32_t p = r * stride + o;
+    pairs[boff[g >> lb] + rank[t]] = (uint64_t(g & lmask) << 32) | p;
+  }
+}
+
+template <class W>
+__global__ void __launch_bounds__(kBuildThreads) k_bucket_occupy(const uint64_t* __restrict__ pairs,
+                                                                 const uint32_t* __restrict__ boff,
+                                                                 uint64_t buckets, uint32_t gpb,
+                                                                 W* __restrict__ I, uint32_t* __restrict__ dcnt) {
+  constexpr unsigned w = GroupTraits<W>::width;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  W* occ = reinterpret_cast<W*>(smem_raw);
+  __shared__ uint32_t ws[33];
+  for (uint64_t bk = blockIdx.x; bk < buckets; bk += gridDim.x) {
+    for (uint32_t i = threadIdx.x; i < gpb; i += blockDim.x) occ[i] = W(0);
+    __syncthreads();
+    const uint32_t b0 = boff[bk], b1 = boff[bk + 1];
+    for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      const uint32_t gl = uint32_t(pairs[i] >> 32);
+      atomicOr(reinterpret_cast<typename std::conditional<sizeof(W) == 8, unsigned long long, unsigned>::type*>(
+                   occ + gl / w),
+               (typename std::conditional<sizeof(W) == 8, unsigned long long, unsigned>::type)(W(1) << (gl % w)));
+    }
+    __syncthreads();
+    uint32_t pc = 0;
+    for (uint32_t i = threadIdx.x; i < gpb; i += blockDim.x) {
+      const W x = occ[i];
+      I[bk * gpb + i] = x;
+      pc += GroupTraits<W>::popc(x);
+    }
+    uint32_t tot;
+    block_exclusive_scan<uint32_t>(pc, ws, &tot);
+    if (threadIdx.x == 0) dcnt[bk] = tot;
+    __syncthreads();
+  }
+}
+
+template <class W, bool kSampled>
+__global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* __restrict__ pairs,
+                                                               const uint32_t* __restrict__ boff,
+                                                               const uint32_t* __restrict__ dbase,
+                                                               uint64_t buckets, uint32_t gpb,
+                                                               const W* __restrict__ I, uint32_t* __restrict__ S,
+                                                               uint32_t* __restrict__ S1, uint32_t* __restrict__ O) {
+  constexpr unsigned w = GroupTraits<W>::width;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  W* occ = reinterpret_cast<W*>(smem_raw);
+  uint32_t* sloc = reinterpret_cast<uint32_t*>(occ + gpb);
+  uint32_t* cnt = sloc + gpb;  // up to gpb*w counters
+  __shared__ uint32_t ws[33];
+  for (uint64_t bk = blockIdx.x; bk < buckets; bk += gridDim.x) {
+    for (uint32_t i = threadIdx.x; i < gpb; i += blockDim.x) {
+      const W x = I[bk * gpb + i];
+      occ[i] = x;
+      sloc[i] = GroupTraits<W>::popc(x);
+    }
+    __syncthreads();
+    const uint32_t D = block_scan_smem(sloc, gpb, ws);
+    const uint32_t db = dbase[bk];
+    for (uint32_t i = threadIdx.x; i < gpb; i += blockDim.x) {
+      const uint64_t gi = bk * gpb + i;
+      if (!kSampled) S[gi] = db + sloc[i];
+      else if ((gi & 1) == 0) S[gi >> 1] = db + sloc[i];
+    }
+    for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const uint32_t b0 = boff[bk], b1 = boff[bk + 1];
+    for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      const uint32_t gl = uint32_t(pairs[i] >> 32);
+      const uint32_t wi = gl / w;
+      atomicAdd(cnt + sloc[wi] + rank_below<W>(occ[wi], gl % w), 1u);
+    }
+    __syncthreads();
+    block_scan_smem(cnt, D, ws);
+    for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) S1[db + i] = b0 + cnt[i];
+    __syncthreads();
+    for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      const uint64_t pr = pairs[i];
+      const uint32_t gl = uint32_t(pr >> 32);
+      const uint32_t wi = gl / w;
+      const uint32_t slot = atomicAdd(cnt + sloc[wi] + rank_below<W>(occ[wi], gl % w), 1u);
+      O[b0 + slot] = uint32_t(pr);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
+
+__global__ void k_sample_S(const uint32_t* __restrict__ S, uint64_t len_in, uint32_t* __restrict__ out,
+                           uint64_t len_out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < len_out; i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = S[2 * i];
+}
+
+// Thread per interval: insertion sort for short intervals, heap sort otherwise.
+__global__ void k_sort_intervals(const uint32_t* __restrict__ S1, uint64_t distinct, uint32_t* __restrict__ O) {
+  for (uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b < distinct; b += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t* a = O + S1[b];
+    const uint32_t n = S1[b + 1] - S1[b];
+    if (n <= 32) {
+      for (uint32_t i = 1; i < n; ++i) {
+        const uint32_t x = a[i];
+        uint32_t j = i;
+        while (j > 0 && a[j - 1] > x) { a[j] = a[j - 1]; --j; }
+        a[j] = x;
+      }
+    } else {
+      auto sift = [&](uint32_t root, uint32_t end) {
+        while (2 * root + 1 < end) {
+          uint32_t ch = 2 * root + 1;
+          if (ch + 1 < end && a[ch] < a[ch + 1]) ++ch;
+          if (a[root] >= a[ch]) return;
+          const uint32_t t = a[root]; a[root] = a[ch]; a[ch] = t;
+          root = ch;
+        }
+      };
+      for (uint32_t s = n / 2; s-- > 0;) sift(s, n);
+      for (uint32_t e = n; e-- > 1;) {
+        const uint32_t t = a[0]; a[0] = a[e]; a[e] = t;
+        sift(0, e);
+      }
+    }
+  }
+}
+
+template <class W>
+__global__ void k_lookup(const W* __restrict__ I, const uint32_t* __restrict__ S, const uint32_t* __restrict__ S1,
+                         bool sampled, const uint32_t* __restrict__ codes, uint64_t n, uint32_t* __restrict__ begin,
+                         uint32_t* __restrict__ end) {
+  constexpr unsigned w = GroupTraits<W>::width;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n; t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t g = codes[t];
+    const uint64_t i = g / w;
+    const unsigned j = g % w;
+    const W word = I[i];
+    uint32_t b0 = 0xFFFFFFFFu, b1 = 0xFFFFFFFFu;
+    if ((word >> j) & W(1)) {
+      uint32_t base = sampled ? S[i >> 1] + ((i & 1) ? GroupTraits<W>::popc(I[i - 1]) : 0u) : S[i];
+      base += rank_below<W>(word, j);
+      b0 = S1[base];
+      b1 = S1[base + 1];
+    }
+    begin[t] = b0;
+    end[t] = b1;
+  }
+}
+
+template <class W>
+void build_impl(Ctx& c, const Reads& reads, const Geometry& G, bool sampled, Index& out) {
+  const unsigned q = G.q;
+  const uint32_t span = reads.stride >= q ? reads.stride - q + 1 : 0;
+  const uint64_t slots = uint64_t(reads.n) * span;
+
+  DBuf<uint32_t> bucket_cnt(c, G.buckets + 1);
+  bucket_cnt.zero();
+  DBuf<uint32_t> rank(c, std::max<uint64_t>(slots, 1));
+  const unsigned grid_items = unsigned(std::min<uint64_t>(std::max<uint64_t>(ceil_div(slots, 256), 1), kSMs * 32));
+  if (slots)
+    QGM_KERNEL(c, k_bucket_rank, grid_items, 256, 0, reads.words.p, reads.lengths.p, reads.n, reads.W, span, q, G.lb,
+               bucket_cnt.p, rank.p);
+  DBuf<uint32_t> boff(c, G.buckets + 1);
+  DBuf<uint32_t> vtotal(c, 1);
+  exclusive_scan_u32(c, bucket_cnt.p, boff.p, G.buckets + 1, vtotal.p, nullptr);
+  uint32_t V = 0;
+  QGM_CUDA(cudaMemcpyAsync(&V, vtotal.p, 4, cudaMemcpyDeviceToHost, c.stream));
+  QGM_CUDA(cudaStreamSynchronize(c.stream));
+
+  DBuf<uint64_t> pairs(c, std::max<uint64_t>(V, 1));
+  if (slots)
+    QGM_KERNEL(c, k_bucket_scatter, grid_items, 256, 0, reads.words.p, reads.lengths.p, reads.n, reads.W, span,
+               reads.stride, q, G.lb, boff.p, rank.p, pairs.p);
+  rank.release();
+
+  out.q = q;
+  out.w = G.w;
+  out.sampled = sampled;
+  out.groups = G.groups;
+  out.gs_len = sampled ? (G.groups + 1 + 1) / 2 : G.groups + 1;
+  out.occ = V;
+  out.stride = reads.stride;
+  out.n_reads = reads.n;
+  out.I.alloc(c, G.groups * sizeof(W));
+  out.S.alloc(c, out.gs_len);
+  out.O.alloc(c, std::max<uint64_t>(V, 1));
+
+  const unsigned grid_b = unsigned(std::min<uint64_t>(G.buckets, uint64_t(kSMs) * 8));
+  DBuf<uint32_t> dcnt(c, G.buckets + 1);
+  QGM_CUDA(cudaMemsetAsync(dcnt.p + G.buckets, 0, 4, c.stream));
+  const size_t smem_occ = G.gpb * sizeof(W);
+  QGM_KERNEL(c, k_bucket_occupy<W>, grid_b, kBuildThreads, smem_occ, pairs.p, boff.p, G.buckets, uint32_t(G.gpb),
+             reinterpret_cast<W*>(out.I.p), dcnt.p);
+  DBuf<uint32_t> dbase(c, G.buckets + 1);
+  DBuf<uint32_t> dtotal(c, 1);
+  exclusive_scan_u32(c, dcnt.p, dbase.p, G.buckets + 1, dtotal.p, nullptr);
+  uint32_t D = 0;
+  QGM_CUDA(cudaMemcpyAsync(&D, dtotal.p, 4, cudaMemcpyDeviceToHost, c.stream));
+  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  out.distinct = D;
+  out.S1.alloc(c, uint64_t(D) + 1);
+
+  const size_t smem_emit = G.gpb * sizeof(W) + G.gpb * 4 + (G.gpb * G.w) * 4;
+  if (sampled) {
+    QGM_CUDA(cudaFuncSetAttribute(k_bucket_emit<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_emit)));
+    QGM_KERNEL(c, (k_bucket_emit<W, true>), grid_b, kBuildThreads, smem_emit, pairs.p, boff.p, dbase.p, G.buckets,
+               uint32_t(G.gpb), reinterpret_cast<const W*>(out.I.p), out.S.p, out.S1.p, out.O.p);
+  } else {
+    QGM_CUDA(cudaFuncSetAttribute(k_bucket_emit<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_emit)));
+    QGM_KERNEL(c, (k_bucket_emit<W, false>), grid_b, kBuildThreads, smem_emit, pairs.p, boff.p, dbase.p, G.buckets,
+               uint32_t(G.gpb), reinterpret_cast<const W*>(out.I.p), out.S.p, out.S1.p, out.O.p);
+  }
+  // sentinels: S[groups] = D (kept by sampling iff groups is even), S'[D] = V
+  if (!sampled) QGM_KERNEL(c, k_set_u32, 1, 1, 0, out.S.p + G.groups, D);
+  else if ((G.groups & 1) == 0) QGM_KERNEL(c, k_set_u32, 1, 1, 0, out.S.p + G.groups / 2, D);
+  QGM_KERNEL(c, k_set_u32, 1, 1, 0, out.S1.p + D, V);
+}
+
+}  // namespace
+
+void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sampled, Index& out) {
+  if (q == 0 || q > 16) throw InputError("q must be in [1, 16]");
+  if (w != 32 && w != 64) throw InputError("group width must be 32 or 64");
+  const Geometry G = geometry(q, w);
+  if (w == 32) build_impl<uint32_t>(c, reads, G, sampled, out);
+  else build_impl<uint64_t>(c, reads, G, sampled, out);
+}
+
+void sample_index(Ctx& c, const Index& in, Index& out) {
+  out.q = in.q; out.w = in.w; out.groups = in.groups; out.distinct = in.distinct; out.occ = in.occ;
+  out.stride = in.stride; out.n_reads = in.n_reads;
+  out.I.alloc(c, in.I.n);
+  QGM_CUDA(cudaMemcpyAsync(out.I.p, in.I.p, in.I.n, cudaMemcpyDeviceToDevice, c.stream));
+  out.S1.alloc(c, in.S1.n);
+  QGM_CUDA(cudaMemcpyAsync(out.S1.p, in.S1.p, in.S1.n * 4, cudaMemcpyDeviceToDevice, c.stream));
+  out.O.alloc(c, in.O.n);
+  QGM_CUDA(cudaMemcpyAsync(out.O.p, in.O.p, in.O.n * 4, cudaMemcpyDeviceToDevice, c.stream));
+  if (in.sampled) {
+    out.sampled = true;
+    out.gs_len = in.gs_len;
+    out.S.alloc(c, in.S.n);
+    QGM_CUDA(cudaMemcpyAsync(out.S.p, in.S.p, in.S.n * 4, cudaMemcpyDeviceToDevice, c.stream));
+    return;
+  }
+  out.sampled = true;
+  out.gs_len = (in.gs_len + 1) / 2;
+  out.S.alloc(c, out.gs_len);
+  QGM_KERNEL(c, k_sample_S, unsigned(std::min<uint64_t>(ceil_div(out.gs_len, 256), kSMs * 8)), 256, 0, in.S.p,
+             in.gs_len, out.S.p, out.gs_len);
+}
+
+void normalize_index(Ctx& c, Index& idx) {
+  if (idx.distinct == 0) return;
+  QGM_KERNEL(c, k_sort_intervals, unsigned(std::min<uint64_t>(ceil_div(idx.distinct, 128), kSMs * 16)), 128, 0,
+             idx.S1.p, idx.distinct, idx.O.p);
+}
+
+void lookup_index(Ctx& c, const Index& idx, const uint32_t* d_codes, uint64_t n, uint32_t* d_begin,
+                  uint32_t* d_end) {
+  if (n == 0) return;
+  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), kSMs * 16));
+  if (idx.w == 32)
+    QGM_KERNEL(c, k_lookup<uint32_t>, grid, 256, 0, reinterpret_cast<const uint32_t*>(idx.I.p), idx.S.p, idx.S1.p,
+               idx.sampled, d_codes, n, d_begin, d_end);
+  else
+    QGM_KERNEL(c, k_lookup<uint64_t>, grid, 256, 0, reinterpret_cast<const uint64_t*>(idx.I.p), idx.S.p, idx.S1.p,
+               idx.sampled, d_codes, n, d_begin, d_end);
+}
+
+}  // namespace qgm

@@ -1,0 +1,203 @@
+// internal.hpp -- host-side objects behind the C ABI and the launcher API of
+// the kernel files. Not installed; include/qgm_c.h is the public surface.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <type_traits>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+namespace qgm {
+
+// --------------------------------------------------------------- context
+enum Stage { kStageReads = 0, kStageIndex, kStageFilter, kStageSort, kStageValidate, kStageStrata, kStageD2H,
+             kStageOther, kNumStages };
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  uint64_t launches = 0;
+  bool profile = false;
+  struct Mark { int stage; cudaEvent_t a, b; };
+  std::vector<Mark> marks;          // recorded, not yet folded into stage_ms
+  std::vector<cudaEvent_t> ev_pool; // reusable events
+  double stage_ms[kNumStages] = {0};
+  int cur_stage = -1;
+  cudaEvent_t cur_a = nullptr;
+
+  cudaEvent_t take_event();
+  void stage_begin(int s);
+  void stage_end();
+  void fold_marks();  // synchronises the recorded events
+};
+
+struct StageScope {
+  Ctx& c;
+  StageScope(Ctx& ctx, int s) : c(ctx) { c.stage_begin(s); }
+  ~StageScope() { c.stage_end(); }
+};
+
+// Launch on the context stream, count it, surface launch errors.
+#define QGM_KERNEL(ctx, kernel, grid, block, smem, ...)                          \
+  do {                                                                         \
+    kernel<<<(grid), (block), (smem), (ctx).stream>>>(__VA_ARGS__);            \
+    ++(ctx).launches;                                                          \
+    QGM_LAUNCH_CHECK();                                                        \
+  } while (0)
+
+// --------------------------------------------------------------- memory
+// Stream-ordered device buffer from the device's default memory pool
+// (cudaMallocAsync; the pool keeps freed blocks cached across batches).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  Ctx* ctx = nullptr;
+  DBuf() = default;
+  DBuf(Ctx& c, size_t count) { alloc(c, count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept { *this = std::move(o); }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; ctx = o.ctx;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(Ctx& c, size_t count) {
+    release();
+    ctx = &c;
+    n = count;
+    if (count) QGM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), c.stream));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, ctx->stream);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+  void zero() {
+    if (n) QGM_CUDA(cudaMemsetAsync(p, 0, bytes(), ctx->stream));
+  }
+  void swap(DBuf& o) { std::swap(p, o.p); std::swap(n, o.n); std::swap(ctx, o.ctx); }
+};
+
+// --------------------------------------------------------------- objects
+// One read buffer (PackedReadText, seq.hpp:98-115) in the 2-bit layout, plus
+// per-read bit planes (lo/hi bit of every base, MSB-first, one guard word in
+// front) for the validation kernel.
+struct Reads {
+  uint32_t n = 0, stride = 0, W = 0, Wp = 0, max_len = 0;
+  DBuf<uint64_t> words;    // n * W
+  DBuf<uint32_t> lengths;  // n
+  DBuf<uint2> planes;      // n * Wp, word 0 of every read is a zero guard
+};
+
+// Reference sequences (ReferenceIndex): the concatenated
+// chromosomes in 2-bit (+1 guard word) and as lo/hi bit planes (2 guard words
+// on both sides). Diagonals are keyed in a padded coordinate space where
+// chromosome c starts at cbp[c] = cb[c] + (c+1)*gap, so (chrom, diagonal)
+// round-trips through one unsigned integer.
+struct Ref {
+  uint32_t n_chrom = 0;
+  uint64_t total = 0;
+  uint64_t gap = 0;
+  uint64_t padded_total = 0;
+  unsigned diag_bits = 0;
+  std::vector<uint64_t> cb;   // host copy, n_chrom+1
+  std::vector<uint64_t> cbp;  // host copy, n_chrom+1 (padded begins)
+  DBuf<uint64_t> words;       // ceil(total/32)+1
+  DBuf<uint2> planes;         // ceil(total/32)+4 (lo, hi)
+  DBuf<uint64_t> mask;        // nullable: bit x = masked
+  DBuf<uint64_t> d_cb, d_cbp; // n_chrom+1 each
+};
+
+// q-group index (QGroupIndex<W>, qgroup_index.hpp:28-104) in device memory.
+struct Index {
+  unsigned q = 0, w = 32;
+  bool sampled = false;
+  uint64_t groups = 0, gs_len = 0, distinct = 0, occ = 0;
+  uint32_t stride = 0, n_reads = 0;
+  DBuf<uint8_t> I;        // groups words of w bits
+  DBuf<uint32_t> S;       // gs_len
+  DBuf<uint32_t> S1;      // distinct + 1
+  DBuf<uint32_t> O;       // occ
+};
+
+struct Cands {
+  uint64_t n = 0;
+  unsigned read_bits = 0, diag_bits = 0;
+  std::vector<uint64_t> cbp;  // decode: padded chromosome begins
+  DBuf<uint64_t> keys;        // (read, strand, padded diagonal), sorted
+};
+
+struct HitsObj {
+  uint64_t n = 0;
+  uint64_t stats[4] = {0, 0, 0, 0};
+  DBuf<uint8_t> hits;  // n * 16-byte qgm_hit
+};
+
+// --------------------------------------------------------------- launchers
+// scan.cu -- exclusive scan of u32 values (u64 running sums). d_total and
+// d_overflow (set to 1 when the total exceeds 2^32-1) are optional device
+// outputs. in may equal out.
+void exclusive_scan_u32(Ctx& c, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* d_total,
+                        int* d_overflow);
+// Order-preserving selection of keys[i] with flag[i] != 0 (or, if flags is
+// null, keys that differ from their predecessor: unique of a sorted array).
+// Returns the count (host sync).
+uint64_t select_u64(Ctx& c, const uint64_t* keys, const uint32_t* vals, const uint32_t* flags, uint64_t n,
+                    uint64_t* out_keys, uint32_t* out_vals);
+
+// radix_sort.cu -- stable LSD radix sort of u64 keys (+ optional u32 values)
+// on bits [begin_bit, end_bit). Sorted data ends up in keys/vals (buffers may
+// be swapped with the alternates).
+void radix_sort(Ctx& c, DBuf<uint64_t>& keys, DBuf<uint64_t>& keys_alt, DBuf<uint32_t>* vals,
+                DBuf<uint32_t>* vals_alt, uint64_t n, int begin_bit, int end_bit);
+
+// reads / ref preparation (capi.cu)
+void make_read_planes(Ctx& c, Reads& r);
+void make_ref_planes(Ctx& c, Ref& ref);
+
+// index_build.cu
+void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sampled, Index& out);
+void sample_index(Ctx& c, const Index& in, Index& out);
+void normalize_index(Ctx& c, Index& idx);
+void lookup_index(Ctx& c, const Index& idx, const uint32_t* d_codes, uint64_t n, uint32_t* d_begin,
+                  uint32_t* d_end);
+
+// filter.cu -- raw candidate keys (unsorted) appended to `keys` (grown and
+// re-run on overflow). Returns the count.
+uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Ref& ref, int strands, int mode,
+                          unsigned read_bits, DBuf<uint64_t>& keys);
+
+// validate.cu
+// mode 0: append kept hits as (hit key, k) to hit_keys/hit_vals (counter in
+//         *d_count); mode 1: write one qgm_validated per candidate.
+void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint64_t* cand_keys, uint64_t n,
+                         unsigned read_bits, unsigned band, unsigned pct, int mode, uint64_t* hit_keys,
+                         uint32_t* hit_vals, unsigned long long* d_count, void* d_validated);
+
+// strata.cu -- dedup (read, chrom, ref_start, strand) keeping min k, then
+// best-stratum / all; writes qgm_hit records, returns their count.
+uint64_t stratify_hits(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const uint32_t* hit_vals, uint64_t n,
+                       uint32_t n_reads, unsigned read_bits, int mode, DBuf<uint8_t>& out);
+
+inline unsigned bit_width_u64(uint64_t x) {
+  unsigned b = 0;
+  while (x) { ++b; x >>= 1; }
+  return b;
+}
+
+}  // namespace qgm

@@ -1,0 +1,133 @@
+// scan.cu -- device exclusive scan and order-preserving selection: the B200
+// equivalents of par::exclusive_scan_in_place (parallel.hpp:64-108, with the
+// u32 overflow check of :53-58) and par::compact (parallel.hpp:124-141).
+//
+// Reduce-then-scan over 4096-element tiles: (1) per-tile u64 sums, (2) one
+// CTA scans the tile sums, (3) every tile re-reads its elements, scans them in
+// shared memory and writes out. HBM traffic: 2 reads + 1 write per element.
+#include "internal.hpp"
+
+namespace qgm {
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanPer = 16;
+constexpr int kScanTile = kScanThreads * kScanPer;
+
+__device__ __forceinline__ uint32_t pad_idx(uint32_t i) { return i + (i >> 5); }
+
+__global__ void __launch_bounds__(kScanThreads) k_tile_sums(const uint32_t* __restrict__ in, uint64_t n,
+                                                            uint64_t* __restrict__ sums) {
+  __shared__ uint64_t ws[33];
+  const uint64_t base = uint64_t(blockIdx.x) * kScanTile;
+  uint64_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanPer; ++j) {
+    const uint64_t i = base + uint64_t(j) * kScanThreads + threadIdx.x;
+    if (i < n) s += in[i];
+  }
+  uint64_t tot;
+  block_exclusive_scan<uint64_t>(s, ws, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_sums(uint64_t* __restrict__ sums, uint64_t n_tiles,
+                                                    uint32_t* __restrict__ d_total, int* __restrict__ d_overflow) {
+  __shared__ uint64_t ws[33];
+  uint64_t carry = 0;
+  for (uint64_t b = 0; b < n_tiles; b += blockDim.x) {
+    const uint64_t i = b + threadIdx.x;
+    const uint64_t v = i < n_tiles ? sums[i] : 0;
+    uint64_t tot;
+    const uint64_t ex = block_exclusive_scan<uint64_t>(v, ws, &tot);
+    if (i < n_tiles) sums[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    if (d_total) *d_total = uint32_t(carry);
+    if (d_overflow) *d_overflow = carry > 0xFFFFFFFFull ? 1 : 0;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_tile_scan(const uint32_t* in, uint32_t* out, uint64_t n,
+                                                            const uint64_t* __restrict__ sums) {
+  __shared__ uint32_t tile[kScanTile + kScanTile / 32];
+  __shared__ uint64_t ws[33];
+  const uint64_t base = uint64_t(blockIdx.x) * kScanTile;
+#pragma unroll
+  for (int j = 0; j < kScanPer; ++j) {
+    const uint32_t li = j * kScanThreads + threadIdx.x;
+    const uint64_t i = base + li;
+    tile[pad_idx(li)] = i < n ? in[i] : 0u;
+  }
+  __syncthreads();
+  uint64_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanPer; ++j) s += tile[pad_idx(threadIdx.x * kScanPer + j)];
+  uint64_t run = block_exclusive_scan<uint64_t>(s, ws, nullptr) + sums[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kScanPer; ++j) {
+    const uint32_t li = pad_idx(threadIdx.x * kScanPer + j);
+    const uint32_t v = tile[li];
+    tile[li] = uint32_t(run);
+    run += v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kScanPer; ++j) {
+    const uint32_t li = j * kScanThreads + threadIdx.x;
+    const uint64_t i = base + li;
+    if (i < n) out[i] = tile[pad_idx(li)];
+  }
+}
+
+__global__ void k_select_flags(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ flags, uint64_t n,
+                               uint32_t* __restrict__ f) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    f[i] = flags ? (flags[i] != 0) : (i == 0 || keys[i] != keys[i - 1]);
+}
+
+__global__ void k_select_scatter(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                 const uint32_t* __restrict__ flags, const uint32_t* __restrict__ pos, uint64_t n,
+                                 uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const bool sel = flags ? (flags[i] != 0) : (i == 0 || keys[i] != keys[i - 1]);
+    if (sel) {
+      out_keys[pos[i]] = keys[i];
+      if (vals) out_vals[pos[i]] = vals[i];
+    }
+  }
+}
+
+}  // namespace
+
+void exclusive_scan_u32(Ctx& c, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* d_total,
+                        int* d_overflow) {
+  if (n == 0) {
+    if (d_total) QGM_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), c.stream));
+    if (d_overflow) QGM_CUDA(cudaMemsetAsync(d_overflow, 0, sizeof(int), c.stream));
+    return;
+  }
+  const uint64_t tiles = ceil_div(n, kScanTile);
+  DBuf<uint64_t> sums(c, tiles);
+  QGM_KERNEL(c, k_tile_sums, unsigned(tiles), kScanThreads, 0, in, n, sums.p);
+  QGM_KERNEL(c, k_scan_sums, 1, 1024, 0, sums.p, tiles, d_total, d_overflow);
+  QGM_KERNEL(c, k_tile_scan, unsigned(tiles), kScanThreads, 0, in, out, n, sums.p);
+}
+
+uint64_t select_u64(Ctx& c, const uint64_t* keys, const uint32_t* vals, const uint32_t* flags, uint64_t n,
+                    uint64_t* out_keys, uint32_t* out_vals) {
+  if (n == 0) return 0;
+  DBuf<uint32_t> f(c, n);
+  DBuf<uint32_t> total(c, 1);
+  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
+  QGM_KERNEL(c, k_select_flags, grid, 256, 0, keys, flags, n, f.p);
+  exclusive_scan_u32(c, f.p, f.p, n, total.p, nullptr);
+  QGM_KERNEL(c, k_select_scatter, grid, 256, 0, keys, vals, flags, f.p, n, out_keys, out_vals);
+  uint32_t h = 0;
+  QGM_CUDA(cudaMemcpyAsync(&h, total.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  return h;
+}
+
+}  // namespace qgm

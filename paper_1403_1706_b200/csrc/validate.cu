@@ -1,0 +1,253 @@
+// validate.cu -- stage 4: banded bit-parallel semi-global validation
+// (Myers 1999 / Hyyro 2003 banded; contract of
+// oracle::banded_semiglobal_distance, oracles.hpp:86-111, band j-i in [0,B),
+// and SPEC.md:378-395; window/start/threshold frozen by SURVEY Appendix B.4-B.6).
+//
+// One thread per unique candidate; candidates are sorted by read, so the lanes
+// of a warp mostly share one read (its bit planes are L1 hits). The DP runs
+// over the REVERSED read and window so that one pass yields both the distance
+// k and the smallest optimal start (the reversed bottom row at diagonal t is
+// the best cost of an alignment starting at forward column B-1-t).
+//
+// State per read row i (diagonal coordinates t = j - i in [0,B), one bit per
+// diagonal in a 32- or 64-bit word):
+//   Eq  : read'[i] == window'[i+t]  (bit planes -> 2 funnel shifts + 2 LOP3)
+//   X   = Eq | Mv>>1                 (zero diagonal step from above/diagonal)
+//   Z   = carry chain of zero steps along t through Pv (Myers' addition trick)
+//   new Pv/Mv from the diagonal deltas D1 = ~Z and D1<<1; score of t=0 += D1&1
+// ~20 integer ops per row (VALIDATE_OPS_PER_ROW in DESIGN.md).
+#include "internal.hpp"
+
+namespace qgm {
+namespace {
+
+constexpr int kValThreads = 128;
+
+struct ValArgs {
+  const uint2* rplanes;
+  const uint32_t* rlen;
+  uint32_t Wp;
+  const uint2* fplanes;  // reference planes; word (x>>5)+2 holds global bases [x&~31, +32)
+  const uint64_t* cb;
+  const uint64_t* cbp;
+  uint32_t n_chrom;
+  uint64_t gap;
+  const uint64_t* keys;
+  uint64_t n;
+  unsigned diag_bits;
+  unsigned B;
+  unsigned pct;
+  int mode;
+  uint64_t* hit_keys;
+  uint32_t* hit_vals;
+  unsigned long long* counter;
+  void* validated;
+};
+
+struct Win { uint32_t lo, hi, v; };
+
+// 32 forward window bases starting at global position a, MSB-first (bit 31-j
+// = base a+j), masked to the chromosome [cbeg, cend).
+__device__ __forceinline__ Win load_win(const uint2* __restrict__ fp, int64_t a, int64_t cbeg, int64_t cend,
+                                        bool interior) {
+  Win w{0u, 0u, 0u};
+  if (!interior && (a + 32 <= cbeg || a >= cend)) return w;
+  const int64_t idx = (a >> 5) + 2;
+  const unsigned s = unsigned(a & 31);
+  const uint2 h = __ldg(fp + idx);
+  const uint2 l = __ldg(fp + idx + 1);
+  w.lo = __funnelshift_l(l.x, h.x, s);
+  w.hi = __funnelshift_l(l.y, h.y, s);
+  if (interior) {
+    w.v = 0xFFFFFFFFu;
+  } else {
+    const int64_t lo = cbeg - a > 0 ? cbeg - a : 0, hi = cend - a < 32 ? cend - a : 32;
+    uint32_t m = 0;
+    if (hi > lo) {
+      m = lo >= 32 ? 0u : (0xFFFFFFFFu >> lo);
+      if (hi < 32) m &= ~(0xFFFFFFFFu >> hi);
+    }
+    w.v = m;
+  }
+  return w;
+}
+
+template <class T> struct Band;
+template <> struct Band<uint32_t> {
+  static constexpr int kWords = 1;
+  __device__ static __forceinline__ uint32_t eq(const Win* w, unsigned t, uint32_t rl, uint32_t rh, bool chk) {
+    const uint32_t lo = __funnelshift_r(w[0].lo, w[1].lo, t);
+    const uint32_t hi = __funnelshift_r(w[0].hi, w[1].hi, t);
+    uint32_t e = ~((lo ^ rl) | (hi ^ rh));
+    if (chk) e &= __funnelshift_r(w[0].v, w[1].v, t);
+    return e;
+  }
+};
+template <> struct Band<uint64_t> {
+  static constexpr int kWords = 2;
+  __device__ static __forceinline__ uint64_t eq(const Win* w, unsigned t, uint32_t rl, uint32_t rh, bool chk) {
+    const uint32_t lo0 = __funnelshift_r(w[0].lo, w[1].lo, t), lo1 = __funnelshift_r(w[1].lo, w[2].lo, t);
+    const uint32_t hi0 = __funnelshift_r(w[0].hi, w[1].hi, t), hi1 = __funnelshift_r(w[1].hi, w[2].hi, t);
+    uint32_t e0 = ~((lo0 ^ rl) | (hi0 ^ rh));
+    uint32_t e1 = ~((lo1 ^ rl) | (hi1 ^ rh));
+    if (chk) {
+      e0 &= __funnelshift_r(w[0].v, w[1].v, t);
+      e1 &= __funnelshift_r(w[1].v, w[2].v, t);
+    }
+    return (uint64_t(e1) << 32) | e0;
+  }
+};
+
+template <class T, bool kCheck>
+__device__ __forceinline__ void myers_rows(const ValArgs& a, uint32_t r, bool rev, uint32_t n, int64_t F, uint32_t L,
+                                           int64_t cbeg, int64_t cend, T mask, T& Pv, T& Mv, int& score0) {
+  constexpr int NW = Band<T>::kWords;
+  const uint2* rp = a.rplanes + uint64_t(r) * a.Wp;
+  Win w[NW + 1];
+#pragma unroll
+  for (int i = 0; i <= NW; ++i) w[i] = load_win(a.fplanes, F + int64_t(L) - 32 * (i + 1), cbeg, cend, !kCheck);
+  const uint32_t chunks = (n + 31) >> 5;
+  for (uint32_t c = 0; c < chunks; ++c) {
+    if (c > 0) {
+#pragma unroll
+      for (int i = 0; i < NW; ++i) w[i] = w[i + 1];
+      w[NW] = load_win(a.fplanes, F + int64_t(L) - 32 * int64_t(c + NW + 1), cbeg, cend, !kCheck);
+    }
+    // read' reversed, rows 32c..32c+31 with row t at bit 31-t
+    uint32_t rl, rh;
+    if (rev) {  // rr[x] = complement(read[x])
+      const uint2 v = __ldg(rp + c + 1);
+      rl = ~v.x;
+      rh = ~v.y;
+    } else {  // rr[x] = read[n-1-x]: bases [n-32(c+1), n-32c), bit-reversed
+      const int64_t a0 = int64_t(n) - 32 * int64_t(c + 1);
+      const int64_t idx = (a0 >> 5) + 1;
+      const unsigned s = unsigned(a0 & 31);
+      const uint2 h = __ldg(rp + idx);
+      const uint2 l = __ldg(rp + idx + 1);
+      rl = __brev(__funnelshift_l(l.x, h.x, s));
+      rh = __brev(__funnelshift_l(l.y, h.y, s));
+    }
+    const uint32_t rows = min(32u, n - 32 * c);
+#pragma unroll 4
+    for (uint32_t t = 0; t < rows; ++t) {
+      const uint32_t Rl = uint32_t(int32_t(rl << t) >> 31);
+      const uint32_t Rh = uint32_t(int32_t(rh << t) >> 31);
+      const T Eq = Band<T>::eq(w, t, Rl, Rh, kCheck) & mask;
+      const T X = Eq | (Mv >> 1);
+      const T Pp = Pv >> 1;
+      const T Z = ((((X & Pp) + Pp) ^ Pp) | X) & mask;
+      const T D1 = ~Z & mask;
+      const T Bs = (D1 << 1) & mask;
+      const T up = Bs & ~D1, dn = D1 & ~Bs, zr = ~(Pv | Mv);
+      const T nP = ((Pv & ~up) | (zr & dn)) & mask & ~T(1);
+      const T nM = ((Mv & ~dn) | (zr & up)) & mask & ~T(1);
+      Pv = nP;
+      Mv = nM;
+      score0 += int(D1 & T(1));
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a) {
+  const T mask = a.B >= sizeof(T) * 8 ? T(~T(0)) : T((T(1) << a.B) - 1);
+  const uint64_t dmask = (uint64_t(1) << a.diag_bits) - 1;
+  for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < a.n; base += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    bool kept = false, in_range = false;
+    int k = 0;
+    uint32_t start = 0, ref_start = 0, r = 0, c = 0;
+    bool rev = false;
+    if (i < a.n) {
+      const uint64_t key = a.keys[i];
+      r = uint32_t(key >> (a.diag_bits + 1));
+      rev = (key >> a.diag_bits) & 1;
+      const uint64_t gp = key & dmask;
+      uint32_t lo = 0, hi = a.n_chrom;  // largest c with cbp[c]-gap <= gp
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(a.cbp + mid) - a.gap <= gp) lo = mid; else hi = mid;
+      }
+      c = lo;
+      const int64_t d = int64_t(gp) - int64_t(__ldg(a.cbp + c));
+      const int64_t cbeg = int64_t(__ldg(a.cb + c)), cend = int64_t(__ldg(a.cb + c + 1));
+      const int64_t Lc = cend - cbeg;
+      const uint32_t n = __ldg(a.rlen + r);
+      const uint32_t L = n + a.B - 1;
+      const int64_t H = (int64_t(a.B) - 1) / 2;
+      const int64_t w0 = d - H;
+      if (n > 0 && w0 + int64_t(L) > 0 && w0 < Lc) {
+        in_range = true;
+        T Pv = 0, Mv = 0;
+        int score0 = 0;
+        const int64_t F = cbeg + w0;
+        if (w0 >= 0 && w0 + int64_t(L) <= Lc) myers_rows<T, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0);
+        else myers_rows<T, true>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0);
+        int v = score0, best = score0;
+        unsigned tbest = 0;
+        for (unsigned t = 1; t < a.B; ++t) {
+          v += int((Pv >> t) & T(1)) - int((Mv >> t) & T(1));
+          if (v <= best) { best = v; tbest = t; }
+        }
+        k = best;
+        start = a.B - 1 - tbest;
+        int64_t rs = w0 + int64_t(start);
+        rs = rs < 0 ? 0 : (rs > Lc - 1 ? Lc - 1 : rs);
+        ref_start = uint32_t(rs);
+        kept = k <= int(n) && uint64_t(100) * uint64_t(int64_t(n) - k) >= uint64_t(a.pct) * n;
+      }
+    }
+    if (a.mode == 0) {
+      const bool emit = i < a.n && in_range && kept;
+      const unsigned long long slot = warp_append(emit, a.counter);
+      if (emit) {
+        const uint64_t gstart = __ldg(a.cbp + c) + ref_start;
+        a.hit_keys[slot] = (uint64_t(r) << (a.diag_bits + 1)) | (gstart << 1) | uint64_t(rev);
+        a.hit_vals[slot] = uint32_t(k);
+      }
+    } else if (i < a.n) {
+      uint32_t* o = reinterpret_cast<uint32_t*>(static_cast<char*>(a.validated) + i * 20);
+      o[0] = uint32_t(k);
+      o[1] = start;
+      o[2] = ref_start;
+      o[3] = uint32_t(kept) | (uint32_t(in_range) << 8);
+      o[4] = 0;
+    }
+  }
+}
+
+}  // namespace
+
+void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint64_t* cand_keys, uint64_t n,
+                         unsigned read_bits, unsigned band, unsigned pct, int mode, uint64_t* hit_keys,
+                         uint32_t* hit_vals, unsigned long long* d_count, void* d_validated) {
+  if (band == 0 || band > 64) throw InputError("band width must be in [1, 64]");
+  if (pct > 100) throw InputError("percent identity must be in [0, 100]");
+  if (read_bits + 1 + ref.diag_bits > 64) throw InputError("read batch too large for the 64-bit hit key");
+  if (n == 0) return;
+  ValArgs a;
+  a.rplanes = reads.planes.p;
+  a.rlen = reads.lengths.p;
+  a.Wp = reads.Wp;
+  a.fplanes = ref.planes.p;
+  a.cb = ref.d_cb.p;
+  a.cbp = ref.d_cbp.p;
+  a.n_chrom = ref.n_chrom;
+  a.gap = ref.gap;
+  a.keys = cand_keys;
+  a.n = n;
+  a.diag_bits = ref.diag_bits;
+  a.B = band;
+  a.pct = pct;
+  a.mode = mode;
+  a.hit_keys = hit_keys;
+  a.hit_vals = hit_vals;
+  a.counter = d_count;
+  a.validated = d_validated;
+  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, kValThreads), uint64_t(kSMs) * 32));
+  if (band <= 32) QGM_KERNEL(c, k_validate<uint32_t>, grid, kValThreads, 0, a);
+  else QGM_KERNEL(c, k_validate<uint64_t>, grid, kValThreads, 0, a);
+}
+
+}  // namespace qgm

@@ -1,0 +1,139 @@
+// GPU parity tests of the whole path (qgm_map): index build -> filtration ->
+// candidate radix sort/unique -> validation -> dedup + strata, against the CPU
+// restatement (qgm_oracle::map_with_index) on seeded inputs, plus the
+// postprocess examples of SPEC.md:443-471.
+#include <catch2/catch_amalgamated.hpp>
+
+#include "testutil.hpp"
+
+using namespace qgmap;
+
+namespace {
+void map_vs_oracle(std::uint64_t seed, unsigned q, unsigned w, bool sampled, unsigned band, unsigned pct,
+                   StratumMode mode, bool mask, unsigned n_reads, std::size_t chrom_len, double err, int strands = 3) {
+  std::mt19937_64 g(seed);
+  auto in = tu::make_instance(g, 1 + unsigned(g() % 4), chrom_len, n_reads, 40, 110, err, q, mask, 6);
+  DeviceReference ref(in.ref);
+  MapParams p;
+  p.q = q;
+  p.group_width = w;
+  p.sampled = sampled;
+  p.band = BandConfig{band, pct / 100.0};
+  p.mode = mode;
+  p.strands = strands;
+  qgm_map_stats st{};
+  const auto got = tu::to_oracle(map_reads(ref, in.text, p, &st));
+  qgm_oracle::Params op;
+  op.q = q; op.band = band; op.pct = pct; op.mode = int(mode); op.strands = strands;
+  qgm_oracle::Stats ost;
+  const auto ox = qgm_oracle::build_index<std::uint32_t>(in.oreads, q);
+  const auto want = qgm_oracle::map_with_index(in.oref, in.oreads, ox, op, 4, &ost);
+  INFO("seed=" << seed << " q=" << q << " w=" << w << " band=" << band << " pct=" << pct << " mode=" << int(mode)
+                << " hits=" << want.size() << "/" << got.size());
+  CHECK(st.unique_candidates == ost.unique);
+  CHECK(st.validated == ost.validated_kept);
+  REQUIRE(got.size() == want.size());
+  CHECK(got == want);
+}
+}  // namespace
+
+TEST_CASE("map equals the oracle: best-stratum, q=12 (C1 shape, scaled down)") {
+  map_vs_oracle(1, 12, 32, false, 32, 80, StratumMode::best_stratum, false, 600, 40000, 0.03);
+  map_vs_oracle(2, 12, 32, false, 32, 80, StratumMode::best_stratum, false, 600, 40000, 0.08);
+}
+
+TEST_CASE("map equals the oracle: all mode, q=16 and q=10") {
+  map_vs_oracle(3, 16, 32, false, 32, 80, StratumMode::all, false, 500, 30000, 0.03);
+  map_vs_oracle(4, 10, 32, false, 32, 60, StratumMode::all, false, 400, 20000, 0.05);
+}
+
+TEST_CASE("map equals the oracle: u64 groups, sampled S, repeat mask, single strands") {
+  map_vs_oracle(5, 11, 64, true, 32, 80, StratumMode::all, true, 400, 20000, 0.04);
+  map_vs_oracle(6, 9, 32, true, 32, 80, StratumMode::best_stratum, true, 300, 15000, 0.04, 1);
+  map_vs_oracle(7, 9, 64, false, 32, 80, StratumMode::all, false, 300, 15000, 0.04, 2);
+}
+
+TEST_CASE("map equals the oracle: bands 1..64 and identity thresholds") {
+  map_vs_oracle(8, 12, 32, false, 16, 90, StratumMode::all, false, 300, 20000, 0.05);
+  map_vs_oracle(9, 12, 32, false, 48, 70, StratumMode::best_stratum, false, 300, 20000, 0.08);
+  map_vs_oracle(10, 12, 32, false, 64, 0, StratumMode::all, false, 150, 8000, 0.10);
+  map_vs_oracle(11, 12, 32, false, 1, 95, StratumMode::all, false, 300, 20000, 0.02);
+}
+
+TEST_CASE("two identical chromosome copies: best-stratum keeps both equal hits (SPEC.md:470)") {
+  std::mt19937_64 g(3);
+  const auto chrom = tu::random_codes(2000, g);
+  Reference R;
+  R.names = {"a", "b"};
+  R.codes = chrom;
+  R.codes.insert(R.codes.end(), chrom.begin(), chrom.end());
+  R.chrom_begin = {0, 2000, 4000};
+  DeviceReference ref(R);
+  std::vector<std::vector<base_code>> reads{std::vector<base_code>(chrom.begin() + 500, chrom.begin() + 600)};
+  reads[0][50] = base_code((reads[0][50] + 1) & 3);  // one substitution
+  const auto text = pack_encoded_reads(reads, 100, 16);
+  MapParams p;
+  const auto best = map_reads(ref, text, p);
+  REQUIRE(best.size() == 2);
+  CHECK(best[0].chrom == 0);
+  CHECK(best[1].chrom == 1);
+  CHECK(best[0].ref_start == 500);
+  CHECK(best[0].edits == 1);
+  CHECK(best[1].edits == 1);
+  p.mode = StratumMode::all;
+  const auto all = map_reads(ref, text, p);
+  CHECK(all.size() >= best.size());  // best-stratum is a subset of all
+}
+
+TEST_CASE("cluster duplicates of one alignment collapse to a single record (SPEC.md:445)") {
+  std::mt19937_64 g(4);
+  const auto chrom = tu::random_codes(5000, g);
+  Reference R;
+  R.names = {"c"};
+  R.codes = chrom;
+  R.chrom_begin = {0, 5000};
+  DeviceReference ref(R);
+  std::vector<std::vector<base_code>> reads{std::vector<base_code>(chrom.begin() + 1000, chrom.begin() + 1100)};
+  reads[0].erase(reads[0].begin() + 40);  // a deletion splits the q-gram runs over two diagonals
+  reads[0].push_back(chrom[1100]);
+  const auto text = pack_encoded_reads(reads, 100, 12);
+  MapParams p;
+  p.q = 12;
+  p.mode = StratumMode::all;
+  qgm_map_stats st{};
+  const auto hits = map_reads(ref, text, p, &st);
+  CHECK(st.unique_candidates >= 2);
+  std::size_t at_origin = 0;
+  for (const auto& h : hits) at_origin += (h.ref_start == 1000 && h.strand == 0);
+  CHECK(at_origin == 1);
+}
+
+TEST_CASE("empty read buffer maps to no hits") {
+  std::mt19937_64 g(1);
+  Reference R;
+  R.names = {"c"};
+  R.codes = tu::random_codes(1000, g);
+  R.chrom_begin = {0, 1000};
+  DeviceReference ref(R);
+  const auto text = pack_encoded_reads({}, 100, 16);
+  CHECK(map_reads(ref, text).empty());
+}
+
+TEST_CASE("bad parameters raise input_error") {
+  std::mt19937_64 g(1);
+  Reference R;
+  R.names = {"c"};
+  R.codes = tu::random_codes(1000, g);
+  R.chrom_begin = {0, 1000};
+  DeviceReference ref(R);
+  const auto text = pack_encoded_reads({tu::random_codes(50, g)}, 50, 8);
+  MapParams p;
+  p.band.band_width = 65;
+  CHECK_THROWS_AS(map_reads(ref, text, p), input_error);
+  p.band.band_width = 32;
+  p.band.identity_threshold = 1.5;
+  CHECK_THROWS_AS(map_reads(ref, text, p), input_error);
+  p.band.identity_threshold = 0.8;
+  p.q = 0;
+  CHECK_THROWS_AS(map_reads(ref, text, p), input_error);
+}

@@ -1,0 +1,74 @@
+"""CPU checks of the drop-in boundary: libqgm_b200.so loads, exports every
+function include/qgm_c.h declares, and fails loudly (status code, no crash)
+when no CUDA device is present."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from qgm_testutil import HAS_GPU, ROOT
+
+HEADER = os.path.join(ROOT, "include", "qgm_c.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(qgm_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_python_export_list():
+    import paper_1403_1706_b200 as qgm
+    assert declared_functions() == sorted(qgm.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_1403_1706_b200 as qgm
+    lib = C.CDLL(qgm.LIB_PATH)
+    missing = [f for f in declared_functions() if not hasattr(lib, f)]
+    assert not missing, missing
+
+
+def test_library_is_built_for_sm_100a():
+    import subprocess
+    import paper_1403_1706_b200 as qgm
+    out = subprocess.run(["cuobjdump", "--list-elf", qgm.LIB_PATH], capture_output=True, text=True)
+    assert out.returncode == 0
+    assert "sm_100a" in out.stdout
+
+
+@pytest.mark.skipif(HAS_GPU, reason="checks the no-device error path")
+def test_no_device_is_a_loud_error_not_a_fallback():
+    import paper_1403_1706_b200 as qgm
+    with pytest.raises(qgm.QgmError):
+        qgm.Context(0)
+
+
+def test_host_packing_matches_the_documented_layout():
+    import numpy as np
+    import paper_1403_1706_b200 as qgm
+    codes = np.array([0, 1, 2, 3] * 10, dtype=np.uint8)  # 40 bases
+    w = qgm.pack_codes(codes)
+    # base j at bits [62-2(j%32), 63-2(j%32)] of word j/32
+    for j, c in enumerate(codes):
+        assert (int(w[j // 32]) >> (62 - 2 * (j % 32))) & 3 == c
+    lib = qgm.load_library()
+    out = np.zeros(3, dtype=np.uint64)
+    assert lib.qgm_pack_codes(codes.ctypes.data, codes.size, out.ctypes.data) == 0
+    assert (out[:2] == w[:2]).all()
+    bad = np.array([4], dtype=np.uint8)
+    assert lib.qgm_pack_codes(bad.ctypes.data, 1, out.ctypes.data) == 1
+
+
+def test_reference_unit_tests_pass_against_this_repos_headers():
+    """proj/tests/test_seq.cpp and test_parallel.cpp, compiled unchanged against
+    include/qgmap (oracle/Makefile), pass: the host API is source-compatible."""
+    import subprocess
+    for name in ("test_seq_b200", "test_parallel_b200"):
+        exe = os.path.join(ROOT, "oracle", "_ref", name)
+        if not os.path.exists(exe):
+            pytest.skip("reference tests not built (needs /root/reference at build time)")
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+        assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+        assert " 0 failed" in out.stdout.splitlines()[-1]

@@ -1,0 +1,124 @@
+"""GPU parity tests through the C ABI (libqgm_b200.so) against the CPU oracle.
+
+* the C++ parity suites in tests/cpp (Catch2-style, reading like the
+  reference's own tests) -- one pytest case per binary;
+* config C1 at full size (1 Mbp random reference, 10k simulated 100 bp reads
+  at 3% edits, q=12, best-stratum) through the python binding, hit-for-hit
+  against the oracle, plus all-mode and q=16 variants;
+* size-independent properties at the bench size (C2 shape): e2e host entry ==
+  device entry, best-stratum subset of all, truth recall.
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from qgm_testutil import ROOT
+
+pytestmark = pytest.mark.gpu
+
+CPP = ["test_qgroup_index", "test_filter", "test_validate", "test_map"]
+
+
+@pytest.mark.parametrize("name", CPP)
+def test_cpp_parity_suite(name):
+    exe = os.path.join(ROOT, "tests", "cpp", "build", name)
+    assert os.path.exists(exe), f"{exe} not built (make tests)"
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=1800)
+    tail = out.stdout[-3000:] + "\n" + out.stderr[-3000:]
+    assert out.returncode == 0, tail
+    assert " 0 failed" in out.stdout.strip().splitlines()[-1], tail
+
+
+def _c1(qgm, n_reads=10_000, L=1_000_000, err=0.03, seed=1):
+    ref = qgm.random_reference(seed, L)
+    cb = np.array([0, L], np.uint64)
+    codes, lengths, tc, tp, ts = qgm.simulate_reads(seed + 1, ref, cb, n_reads, 100, err)
+    return ref, cb, codes, lengths, tp, ts
+
+
+def _same(a, b):
+    cols = ("read_id", "chrom", "ref_start", "edits", "strand")
+    return a.size == b.size and all(np.array_equal(a[c], b[c]) for c in cols)
+
+
+@pytest.mark.parametrize("mode,q", [(0, 12), (1, 12), (0, 16), (1, 16)])
+def test_c1_full_size_matches_oracle(ctx, oracle, mode, q):
+    import paper_1403_1706_b200 as qgm
+    ref, cb, codes, lengths, tp, ts = _c1(qgm)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    got, st = ctx.map(reads, R, q=q, mode=mode)
+    want, ost = oracle.map(ref, cb, codes, 100, lengths, q=q, mode=mode)
+    assert st["unique_candidates"] == ost["unique_candidates"]
+    assert st["validated"] == ost["validated"]
+    assert _same(got, want), (got.size, want.size)
+    # sensitivity sanity: most reads map at their true origin (3% edits, q=12)
+    if q == 12 and mode == 0:
+        mapped = np.zeros(lengths.size, bool)
+        mapped[got["read_id"]] = True
+        assert mapped.mean() > 0.97
+
+
+def test_repetitive_reference_and_mask_match_oracle(ctx, oracle):
+    import paper_1403_1706_b200 as qgm
+    L = 300_000
+    ref = qgm.repetitive_reference(5, L)
+    cb = np.array([0, 100_000, L], np.uint64)
+    codes, lengths, *_ = qgm.simulate_reads(6, ref, cb, 3000, 100, 0.03)
+    # repeat mask: forward q-gram frequency per chromosome > 20
+    q = 12
+    mask = np.zeros(L, np.uint8)
+    for c in range(2):
+        seq = ref[cb[c]:cb[c + 1]]
+        w = np.lib.stride_tricks.sliding_window_view(seq, q)
+        codes_c = (w.astype(np.uint64) * (4 ** np.arange(q - 1, -1, -1, dtype=np.uint64))).sum(1)
+        u, inv, cnt = np.unique(codes_c, return_inverse=True, return_counts=True)
+        mask[cb[c]:cb[c] + w.shape[0]] = (cnt[inv] > 20)
+    for m in (None, mask):
+        R = qgm.Reference.from_codes(ctx, ref, cb, mask=m)
+        reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+        got, st = ctx.map(reads, R, q=q, mode=1)
+        want, ost = oracle.map(ref, cb, codes, 100, lengths, q=q, mode=1, mask=m)
+        assert _same(got, want), (m is None, got.size, want.size)
+
+
+def test_device_scan_matches_reference_semantics(ctx):
+    import paper_1403_1706_b200 as qgm
+    sums, tot = ctx.exclusive_scan(np.array([3, 0, 2], np.uint32))
+    assert sums.tolist() == [0, 3, 3] and tot == 5
+    v = np.random.default_rng(1).integers(0, 100, 1_000_003).astype(np.uint32)
+    sums, tot = ctx.exclusive_scan(v)
+    assert np.array_equal(sums, (np.cumsum(v, dtype=np.uint64) - v).astype(np.uint32))
+    with pytest.raises(qgm.InputError):
+        ctx.exclusive_scan(np.full(3, 0xF0000000, np.uint32))
+
+
+def test_c2_shape_properties(ctx):
+    """Bench-size batch (1M reads against a 100 Mbp reference, q=16): the e2e
+    host entry point equals the device-resident one; best-stratum hits are a
+    subset of all-mode hits; nearly every read maps at its true origin."""
+    import paper_1403_1706_b200 as qgm
+    L, N = 100_000_000, 1_000_000
+    ref = qgm.random_reference(11, L)
+    cb = np.array([0, L], np.uint64)
+    codes, lengths, tc, tp, ts = qgm.simulate_reads(12, ref, cb, N, 100, 0.03)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    words = qgm.pack_read_codes(codes, 100)
+    reads = qgm.Reads(ctx, words, lengths, 100)
+    best, st = ctx.map(reads, R, q=16, mode=0)
+    allm, _ = ctx.map(reads, R, q=16, mode=1)
+    host, st2 = ctx.map_host(words, lengths, 100, R, q=16, mode=0)
+    assert _same(best, host) and st == st2
+    key = lambda h: set(zip(h["read_id"].tolist(), h["chrom"].tolist(), h["ref_start"].tolist(),
+                            h["strand"].tolist()))
+    assert key(best) <= key(allm)
+    # truth: forward start of the fragment; the hit may start a few bases off
+    # when the first bases carry edits, so test within +-8 bp.
+    first = np.full(N, -1, np.int64)
+    strand = np.zeros(N, np.uint8)
+    first[best["read_id"][::-1]] = best["ref_start"][::-1].astype(np.int64)
+    strand[best["read_id"][::-1]] = best["strand"][::-1]
+    ok = (np.abs(first - tp.astype(np.int64)) <= 8) & (strand == ts)
+    assert ok.mean() > 0.95, ok.mean()
