@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark of the read-mapping hot path: reads/s mapped per B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+One step = one read buffer (config C2 by default: 1M simulated 100 bp reads at
+3% edits against a 100 Mbp random reference, q=16, all-hits mode, band 32, 80%
+identity) through index build -> filtration -> candidate sort/unique ->
+banded Myers validation -> dedup/strata.
+
+* value    : reads in HBM (2-bit words) when the step starts; step = read prep
+             (device-to-device copy + bit planes) + qgm_map; CUDA events on the
+             library's stream, per step, L2 flushed between steps (a 512 MiB
+             write, outside the step's events). Sum of the K step times, max
+             over ranks.
+* e2e      : the public C ABI call qgm_map_host from pinned host buffers:
+             H2D of the reads + the whole path + D2H of the hits, per step.
+* roofline : the dominant kernel of the step (largest CUDA-event time among
+             the hot kernels), algorithmic bytes per launch (DESIGN.md section
+             4) / its measured launch time, against MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline (rank 0, N=1): the reference's build_qgroup_index + the oracle
+             restatement of stages 2-5 (oracle/_ref/libqgm_ref.so) on the host
+             cores, on one full C2 batch.
+Multi-GPU (torchrun): reads are sharded -- every rank maps its own 1M-read
+batch against its own copy of the reference (weak scaling, no data-path
+collective); NCCL only carries the barrier and the max-over-ranks timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "reads/sec mapped (100 bp, best & all mode) at 1/2/4/8 B200 vs host-CPU ref"
+
+CONFIGS = {
+    # name: (ref_bp, n_chrom, reads, read_len, err, q, mode, band, pct, repetitive)
+    "C1": (1_000_000, 1, 10_000, 100, 0.03, 12, 0, 32, 80, False),
+    "C2": (100_000_000, 1, 1_000_000, 100, 0.03, 16, 1, 32, 80, False),
+    "C2q12": (100_000_000, 1, 1_000_000, 100, 0.03, 12, 1, 32, 80, False),
+    "C3": (3_100_000_000, 24, 1_250_000, 100, 0.03, 16, 0, 32, 80, False),
+    "C4": (100_000_000, 1, 1_000_000, 250, 0.08, 16, 1, 32, 80, False),
+    "C5": (100_000_000, 1, 1_000_000, 100, 0.03, 16, 1, 32, 80, True),
+}
+DESCR = {
+    "C1": "C1: 1 Mbp random reference + 10k simulated 100 bp reads (3% edits), q=12, best-stratum",
+    "C2": "C2: 100 Mbp random reference + 1M simulated 100 bp reads (3% edits), q=16, all-hits",
+    "C2q12": "C2 at q=12 (stress): 100 Mbp + 1M 100 bp reads, all-hits",
+    "C3": "C3 shard: 3.1 Gbp (24 chromosomes) + 1.25M 100 bp reads per GPU, q=16, best-stratum",
+    "C4": "C4: 100 Mbp + 1M 250 bp reads at 8% edits, q=16, all-hits",
+    "C5": "C5: 100 Mbp repetitive reference + 1M 100 bp reads, q=16, all-hits",
+}
+
+
+def chrom_begin(total, n):
+    if n == 1:
+        return np.array([0, total], np.uint64)
+    # human-like decreasing chromosome lengths
+    w = np.linspace(2.0, 0.5, n)
+    lens = np.floor(w / w.sum() * total).astype(np.uint64)
+    lens[-1] += np.uint64(total - int(lens.sum()))
+    return np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7 and parts[0].isdigit():
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [int(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() in ("active", "1")})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]), "samples": len(rows),
+                "reasons": reasons}
+
+
+def make_inputs(qgm, cfg, rank):
+    ref_bp, n_chrom, n_reads, rlen, err, q, mode, band, pct, rep = cfg
+    ref = qgm.repetitive_reference(7, ref_bp) if rep else qgm.random_reference(7, ref_bp)
+    cb = chrom_begin(ref_bp, n_chrom)
+    codes, lengths, *_ = qgm.simulate_reads(1000 + rank, ref, cb, n_reads, rlen, err)
+    return ref, cb, codes, lengths
+
+
+def algorithmic_bytes(kernel, cfg, st, ref_bp, n_reads):
+    """Algorithmic HBM bytes of one launch of `kernel` (DESIGN.md section 4 /
+    SURVEY.md section 8(d))."""
+    q, rlen = cfg[5], cfg[3]
+    groups = (4 ** q) // 32
+    V, D = st["index_occurrences"], st["index_distinct"]
+    if kernel == "k_filter":
+        n_look = 2 * (ref_bp - q + 1)
+        return ref_bp / 4 + 4 * n_look + 12 * st["lookups_hit"] + 4 * st["occurrences"] + 8 * st["raw_candidates"]
+    if kernel == "k_bucket_rank":
+        return n_reads * rlen / 4 + 4 * V
+    if kernel == "k_bucket_scatter":
+        return n_reads * rlen / 4 + 4 * V + 8 * V
+    if kernel == "k_bucket_occupy":
+        return 8 * V + 4 * groups
+    if kernel == "k_bucket_emit":
+        return 16 * V + 4 * groups + 4 * (groups + 1) + 4 * (D + 1) + 4 * V
+    if kernel == "radix_sort_keys":
+        return 8 * st["raw_candidates"] + 8 * st["unique_candidates"]
+    if kernel == "k_validate":
+        u = st["unique_candidates"]
+        return u * (8 + rlen / 4 + (rlen + cfg[7] - 1) / 4 + 12)
+    return None
+
+
+def run_gpu(args):
+    import torch
+    import paper_1403_1706_b200 as qgm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    cfg = CONFIGS[args.config]
+    ref_bp, n_chrom, n_reads, rlen, err, q, mode, band, pct, rep = cfg
+    ref, cb, codes, lengths = make_inputs(qgm, cfg, rank)
+    stream = torch.cuda.Stream(local)
+    ctx = qgm.Context(local, stream=stream.cuda_stream)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    words = qgm.pack_read_codes(codes, rlen)
+    params = qgm.make_params(q=q, mode=mode, band_width=band, pct_identity=pct)
+    lib = ctx.lib
+    import ctypes as C
+
+    # device-resident inputs for `value`
+    d_words = torch.from_numpy(words.view(np.int64)).to(f"cuda:{local}")
+    d_len = torch.from_numpy(lengths.view(np.int32)).to(f"cuda:{local}")
+    # pinned host inputs / outputs for `e2e`
+    h_words = torch.from_numpy(words.view(np.int64)).pin_memory()
+    h_len = torch.from_numpy(lengths.view(np.int32)).pin_memory()
+    cap = n_reads * 64
+    h_hits = torch.empty(cap * 16, dtype=torch.uint8).pin_memory()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def step_device():
+        rd = C.c_void_p()
+        ctx._check(lib.qgm_reads_from_device(ctx.h, C.c_void_p(d_words.data_ptr()), C.c_void_p(d_len.data_ptr()),
+                                             n_reads, rlen, C.byref(rd)))
+        h = C.c_void_p()
+        ctx._check(lib.qgm_map(ctx.h, rd, R.h, C.byref(params), C.byref(h)))
+        st = qgm.MapStats()
+        lib.qgm_hits_stats(h, C.byref(st))
+        lib.qgm_hits_destroy(h)
+        lib.qgm_reads_destroy(rd)
+        return {f: getattr(st, f) for f, _ in qgm.MapStats._fields_}
+
+    def step_e2e():
+        n = C.c_uint64()
+        st = qgm.MapStats()
+        ctx._check(lib.qgm_map_host(ctx.h, C.c_void_p(h_words.data_ptr()), C.c_void_p(h_len.data_ptr()), n_reads,
+                                    rlen, R.h, C.byref(params), C.c_void_p(h_hits.data_ptr()), cap, C.byref(n),
+                                    C.byref(st)))
+        return n.value
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, K, with_profile=False):
+        times = []
+        out = None
+        launches = 0
+        for _ in range(K):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.launches(reset=True)
+            out = fn()
+            launches += ctx.launches()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        return times, out, launches
+
+    for _ in range(args.warmup):
+        step_device()
+    barrier()
+    with ClockSampler(local) as clk:
+        times, st, launches = timed(step_device, args.steps)
+        barrier()
+    clocks = clk.summary()
+    dev_ms = sum(times)
+    # profile pass (per-kernel CUDA events; not part of `value`)
+    ctx.profile(True)
+    ctx.kernel_times(reset=True)
+    ctx.stage_times(reset=True)
+    prof_steps = max(1, min(3, args.steps))
+    timed(step_device, prof_steps)
+    ktimes = ctx.kernel_times(reset=True)
+    stimes = ctx.stage_times(reset=True)
+    ctx.profile(False)
+    # e2e pass
+    for _ in range(max(1, args.warmup // 2)):
+        step_e2e()
+    barrier()
+    e2e_times, n_hits, _ = timed(step_e2e, args.steps)
+    barrier()
+    e2e_ms = sum(e2e_times)
+
+    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, e2e_ms = t.tolist()
+    total_reads = n_reads * args.steps * world
+    value = total_reads / (dev_ms / 1e3)
+    e2e_value = total_reads / (e2e_ms / 1e3)
+
+    # roofline of the dominant kernel
+    peak, peak_kind = load_peaks()
+    per_launch = {k: v[0] / v[1] for k, v in ktimes.items()}
+    dom = max(per_launch, key=per_launch.get) if per_launch else None
+    roof = None
+    if dom:
+        ab = algorithmic_bytes(dom, cfg, st, ref_bp, n_reads)
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(dom)
+        if ab is not None:
+            ach = ab / (per_launch[dom] / 1e3) / 1e9
+            roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(ach / peak, 4), "traffic": traffic, "peak_source": peak_kind,
+                    "algorithmic_bytes": int(ab), "launch_ms": round(per_launch[dom], 4),
+                    "share_of_step": round(ktimes[dom][0] / prof_steps / (sum(times) / len(times)), 4)}
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "reads/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": DESCR[args.config], "reads_per_gpu": n_reads, "read_len": rlen, "ref_bp": ref_bp,
+                   "chromosomes": n_chrom, "q": q, "mode": ("best-stratum", "all")[mode], "band": band,
+                   "pct_identity": pct, "parallelism": f"read-sharded x{world} (reference replicated)",
+                   "l2": "flushed between steps (512 MiB device write outside the step events)"},
+        "e2e": {"value": round(e2e_value, 1), "unit": "reads/s", "ms_per_step": round(e2e_ms / args.steps, 3),
+                "h2d_bytes_per_step": int(words.nbytes + lengths.nbytes), "d2h_bytes_per_step": int(n_hits * 16 + 64)},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "clocks": clocks,
+        "stages_ms_per_step": {k: round(v / prof_steps, 4) for k, v in stimes.items() if v},
+        "kernels_ms_per_launch": {k: round(v, 4) for k, v in per_launch.items()},
+        "counts": st,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args, cfg, ref, cb, codes, lengths, samples=1)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    del R
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(args, cfg, ref, cb, codes, lengths, samples=1):
+    """The reference's build_qgroup_index + restated stages 2-5 on the host cores."""
+    from oracle.pyoracle import RefShim, Oracle, REF_SO
+    ref_bp, n_chrom, n_reads, rlen, err, q, mode, band, pct, rep = cfg
+    threads = os.cpu_count() or 1
+    kind = "reference" if os.path.exists(REF_SO) else "port"
+    impl = RefShim() if kind == "reference" else Oracle()
+    times = []
+    st = None
+    for _ in range(samples):
+        t0 = time.perf_counter()
+        hits, st = impl.map(ref, cb, codes, rlen, lengths, q=q, mode=mode, band=band, pct=pct, threads=threads)
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    return {"value": round(n_reads / best, 1), "unit": "reads/s", "cores": threads, "kind": kind,
+            "sample": f"one full {args.config} batch ({n_reads} reads vs {ref_bp} bp); "
+                      f"index = reference build_qgroup_index (qgroup_index.hpp:124-180), stages 2-5 = oracle "
+                      f"restatement; best of {samples}, {best:.2f} s", "hits": int(hits.size), "counts": st}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path on the host cores, rank 0 only."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    import paper_1403_1706_b200 as qgm
+    cfg = CONFIGS[args.config]
+    ref, cb, codes, lengths = make_inputs(qgm, cfg, 0)
+    from oracle.pyoracle import RefShim, Oracle, REF_SO
+    ref_bp, n_chrom, n_reads, rlen, err, q, mode, band, pct, rep = cfg
+    threads = os.cpu_count() or 1
+    kind = "reference" if os.path.exists(REF_SO) else "port"
+    impl = RefShim() if kind == "reference" else Oracle()
+    for _ in range(args.warmup):
+        impl.map(ref, cb, codes, rlen, lengths, q=q, mode=mode, band=band, pct=pct, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        hits, st = impl.map(ref, cb, codes, rlen, lengths, q=q, mode=mode, band=band, pct=pct, threads=threads)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = n_reads * args.steps / total
+    line = {"metric": METRIC, "value": round(value, 1), "unit": "reads/s", "n_gpus": int(os.environ.get("WORLD_SIZE", 1)),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": DESCR[args.config], "reads_per_step": n_reads, "ref_bp": ref_bp, "q": q,
+                       "mode": ("best-stratum", "all")[mode]},
+            "cpu_baseline": {"value": round(value, 1), "unit": "reads/s", "cores": threads, "kind": kind,
+                             "sample": f"{args.steps} full {args.config} batches; index = reference "
+                                       f"build_qgroup_index, stages 2-5 = oracle restatement (no reference code)"},
+            "e2e": {"value": round(value, 1), "unit": "reads/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "counts": st, "hits": int(hits.size)}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -110,6 +110,10 @@ typedef struct qgm_map_stats {
   uint64_t unique_candidates; /* after radix sort + unique */
   uint64_t validated;         /* candidates passing the identity threshold */
   uint64_t hits;              /* after dedup + strata */
+  uint64_t index_distinct;    /* distinct read q-grams (|S'|-1) */
+  uint64_t index_occurrences; /* indexed read q-grams (|O|) */
+  uint64_t lookups_hit;       /* reference lookups whose occupancy bit was set */
+  uint64_t occurrences;       /* (position, occurrence) pairs visited by filtration */
 } qgm_map_stats;
 
 /* ---- context ------------------------------------------------------------ */
@@ -126,6 +130,9 @@ int qgm_ctx_synchronize(qgm_ctx* ctx);
 #define QGM_NUM_STAGES 8
 int qgm_ctx_profile(qgm_ctx* ctx, int enable);
 int qgm_ctx_stage_times(qgm_ctx* ctx, double* ms, int n, int reset);
+/* Per-kernel CUDA-event times of the hot kernels (profile mode): writes
+ * "name<TAB>total_ms<TAB>launches\n" lines into buf (NUL-terminated). */
+int qgm_ctx_kernel_times(qgm_ctx* ctx, char* buf, uint64_t cap, int reset);
 /* Kernels launched on ctx since the last reset. */
 uint64_t qgm_ctx_launches(qgm_ctx* ctx, int reset);
 

@@ -92,6 +92,7 @@ class QGroupIndex {
   void normalize() {
     dev_.ctx->check(qgm_index_normalize(dev_.ctx->get(), dev_.get()));
     mirror_.reset();
+    once_ = std::make_shared<std::once_flag>();
   }
 
   const device::IndexHandle& device_index() const { return dev_; }

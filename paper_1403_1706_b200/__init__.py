@@ -78,13 +78,14 @@ class IndexInfo(C.Structure):
 
 class MapStats(C.Structure):
     _fields_ = [("raw_candidates", C.c_uint64), ("unique_candidates", C.c_uint64), ("validated", C.c_uint64),
-                ("hits", C.c_uint64)]
+                ("hits", C.c_uint64), ("index_distinct", C.c_uint64), ("index_occurrences", C.c_uint64),
+                ("lookups_hit", C.c_uint64), ("occurrences", C.c_uint64)]
 
 
 # Every symbol include/qgm_c.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = (
     "qgm_ctx_create", "qgm_ctx_set_stream", "qgm_ctx_stream", "qgm_ctx_destroy", "qgm_last_error",
-    "qgm_ctx_synchronize", "qgm_ctx_profile", "qgm_ctx_stage_times", "qgm_ctx_launches", "qgm_pack_codes",
+    "qgm_ctx_synchronize", "qgm_ctx_profile", "qgm_ctx_stage_times", "qgm_ctx_kernel_times", "qgm_ctx_launches", "qgm_pack_codes",
     "qgm_pack_reads", "qgm_reads_upload", "qgm_reads_from_device", "qgm_reads_destroy", "qgm_index_build",
     "qgm_index_sample", "qgm_index_normalize", "qgm_index_info_get", "qgm_index_download", "qgm_index_lookup",
     "qgm_index_destroy", "qgm_ref_upload", "qgm_ref_destroy", "qgm_filter", "qgm_cands_count",
@@ -119,6 +120,7 @@ def load_library(path: str = LIB_PATH):
         "qgm_ctx_synchronize": (i32, [P]),
         "qgm_ctx_profile": (i32, [P, i32]),
         "qgm_ctx_stage_times": (i32, [P, P, i32, i32]),
+        "qgm_ctx_kernel_times": (i32, [P, C.c_char_p, u64, i32]),
         "qgm_ctx_launches": (u64, [P, i32]),
         "qgm_pack_codes": (i32, [P, u64, P]),
         "qgm_pack_reads": (i32, [P, u32, u32, P]),
@@ -264,6 +266,16 @@ class Context:
         ms = np.zeros(len(STAGES), dtype=np.float64)
         self._check(self.lib.qgm_ctx_stage_times(self.h, _ptr(ms), len(STAGES), int(reset)))
         return dict(zip(STAGES, ms.tolist()))
+
+    def kernel_times(self, reset=True) -> dict:
+        """{kernel: (total_ms, launches)} for the timed hot kernels (profile mode)."""
+        buf = C.create_string_buffer(1 << 16)
+        self._check(self.lib.qgm_ctx_kernel_times(self.h, buf, len(buf), int(reset)))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, ms, n = line.split("\t")
+            out[name] = (float(ms), int(n))
+        return out
 
     def launches(self, reset=False) -> int:
         return int(self.lib.qgm_ctx_launches(self.h, int(reset)))

@@ -71,6 +71,17 @@ void Ctx::fold_marks() {
     ev_pool.push_back(m.b);
   }
   marks.clear();
+  for (auto& m : kmarks) {
+    QGM_CUDA(cudaEventSynchronize(m.b));
+    float ms = 0;
+    QGM_CUDA(cudaEventElapsedTime(&ms, m.a, m.b));
+    auto it = std::find_if(kernel_ms.begin(), kernel_ms.end(), [&](auto& e) { return e.first == m.name; });
+    if (it == kernel_ms.end()) kernel_ms.push_back({m.name, {ms, 1}});
+    else { it->second.first += ms; it->second.second += 1; }
+    ev_pool.push_back(m.a);
+    ev_pool.push_back(m.b);
+  }
+  kmarks.clear();
 }
 
 namespace {
@@ -168,10 +179,15 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   }
   DBuf<uint64_t> keys, alt;
   uint64_t n_raw, n_u;
+  uint64_t fst[2] = {0, 0};
+  out.stats[4] = idx.distinct;
+  out.stats[5] = idx.occ;
   {
     StageScope s(c, kStageFilter);
-    n_raw = filter_reference(c, idx, reads, ref, strands, QGM_FILTER_RUN_START, rb, keys);
+    n_raw = filter_reference(c, idx, reads, ref, strands, QGM_FILTER_RUN_START, rb, keys, fst);
   }
+  out.stats[6] = fst[0];
+  out.stats[7] = fst[1];
   idx = Index();  // the index is per batch; release it before validation
   {
     StageScope s(c, kStageSort);
@@ -313,6 +329,22 @@ int qgm_ctx_stage_times(qgm_ctx* ctx, double* ms, int n, int reset) {
     ctx->c.fold_marks();
     for (int i = 0; i < n && i < qgm::kNumStages; ++i) ms[i] = ctx->c.stage_ms[i];
     if (reset) for (double& v : ctx->c.stage_ms) v = 0;
+  });
+}
+
+int qgm_ctx_kernel_times(qgm_ctx* ctx, char* buf, uint64_t cap, int reset) {
+  if (!ctx || (!buf && cap)) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    ctx->c.fold_marks();
+    std::string s;
+    for (auto& e : ctx->c.kernel_ms)
+      s += e.first + "\t" + std::to_string(e.second.first) + "\t" + std::to_string(e.second.second) + "\n";
+    if (cap) {
+      const size_t n = std::min<size_t>(s.size(), cap - 1);
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+    if (reset) ctx->c.kernel_ms.clear();
   });
 }
 
@@ -676,6 +708,10 @@ int qgm_hits_stats(const qgm_hits* h, qgm_map_stats* o) {
   o->unique_candidates = h->h.stats[1];
   o->validated = h->h.stats[2];
   o->hits = h->h.stats[3];
+  o->index_distinct = h->h.stats[4];
+  o->index_occurrences = h->h.stats[5];
+  o->lookups_hit = h->h.stats[6];
+  o->occurrences = h->h.stats[7];
   return QGM_OK;
 }
 

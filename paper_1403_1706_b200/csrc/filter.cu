@@ -45,6 +45,7 @@ struct FilterArgs {
   uint64_t* out;
   uint64_t cap;
   unsigned long long* counter;
+  unsigned long long* stats;  // {lookups with bit set, occurrences visited}
 };
 
 __device__ __forceinline__ bool is_masked(const uint64_t* mask, uint64_t x) {
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(FilterArgs a) {
   const uint64_t nwarps = (uint64_t(gridDim.x) * kFilterThreads) >> 5;
   const unsigned q = a.q;
   uint32_t staged = 0;
+  unsigned long long n_hit = 0, n_occ = 0;
 
   auto flush = [&]() {
     unsigned long long base = 0;
@@ -127,6 +129,8 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(FilterArgs a) {
         }
       }
     }
+    n_hit += nr;
+    n_occ += cnt;
     // lay out this warp's occurrence intervals in shared memory
     const uint32_t r_off = warp_inclusive_scan(nr) - nr;
     const uint32_t o_inc = warp_inclusive_scan(cnt);
@@ -188,6 +192,12 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(FilterArgs a) {
     }
   }
   flush();
+  n_hit = warp_reduce_sum(n_hit);
+  n_occ = warp_reduce_sum(n_occ);
+  if (lane == 0 && a.stats && n_hit) {
+    atomicAdd(a.stats, n_hit);
+    atomicAdd(a.stats + 1, n_occ);
+  }
 }
 
 template <class W, bool kSampled>
@@ -199,7 +209,7 @@ void launch_filter(Ctx& c, const FilterArgs& a, int mode, unsigned grid) {
 }  // namespace
 
 uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Ref& ref, int strands, int mode,
-                          unsigned read_bits, DBuf<uint64_t>& keys) {
+                          unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats) {
   if (idx.stride != reads.stride || idx.n_reads != reads.n)
     throw InputError("index was built over a different read buffer");
   if (read_bits + 1 + ref.diag_bits > 64) throw InputError("read batch too large for the 64-bit candidate key");
@@ -222,7 +232,9 @@ uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Re
   a.m = reads.stride;
   a.strands = strands;
   a.diag_bits = ref.diag_bits;
-  DBuf<unsigned long long> counter(c, 1);
+  DBuf<unsigned long long> counter(c, 3);  // {emitted, lookups hit, occurrences}
+  a.counter = counter.p;
+  a.stats = counter.p + 1;
   if (keys.n == 0) keys.alloc(c, std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16));
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(ref.total, kFilterThreads * 4),
                                                                           uint64_t(kSMs) * 8)));
@@ -231,6 +243,7 @@ uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Re
     a.out = keys.p;
     a.cap = keys.n;
     if (ref.total > 0) {
+      KernelScope ks(c, "k_filter");
       if (idx.w == 32) {
         if (idx.sampled) launch_filter<uint32_t, true>(c, a, mode, grid);
         else launch_filter<uint32_t, false>(c, a, mode, grid);
@@ -239,11 +252,15 @@ uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Re
         else launch_filter<uint64_t, false>(c, a, mode, grid);
       }
     }
-    unsigned long long n = 0;
-    QGM_CUDA(cudaMemcpyAsync(&n, counter.p, sizeof(n), cudaMemcpyDeviceToHost, c.stream));
+    unsigned long long h[3] = {0, 0, 0};
+    QGM_CUDA(cudaMemcpyAsync(h, counter.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     QGM_CUDA(cudaStreamSynchronize(c.stream));
-    if (n <= keys.n) return n;
-    keys.alloc(c, n + n / 8);  // exact size known now: one re-run
+    if (fstats) {
+      fstats[0] = h[1];
+      fstats[1] = h[2];
+    }
+    if (h[0] <= keys.n) return h[0];
+    keys.alloc(c, h[0] + h[0] / 8);  // exact size known now: one re-run
   }
   throw InternalError("filtration: candidate buffer overflow after resize");
 }

@@ -246,9 +246,11 @@ void build_impl(Ctx& c, const Reads& reads, const Geometry& G, bool sampled, Ind
   bucket_cnt.zero();
   DBuf<uint32_t> rank(c, std::max<uint64_t>(slots, 1));
   const unsigned grid_items = unsigned(std::min<uint64_t>(std::max<uint64_t>(ceil_div(slots, 256), 1), kSMs * 32));
-  if (slots)
+  if (slots) {
+    KernelScope ks(c, "k_bucket_rank");
     QGM_KERNEL(c, k_bucket_rank, grid_items, 256, 0, reads.words.p, reads.lengths.p, reads.n, reads.W, span, q, G.lb,
                bucket_cnt.p, rank.p);
+  }
   DBuf<uint32_t> boff(c, G.buckets + 1);
   DBuf<uint32_t> vtotal(c, 1);
   exclusive_scan_u32(c, bucket_cnt.p, boff.p, G.buckets + 1, vtotal.p, nullptr);
@@ -257,9 +259,11 @@ void build_impl(Ctx& c, const Reads& reads, const Geometry& G, bool sampled, Ind
   QGM_CUDA(cudaStreamSynchronize(c.stream));
 
   DBuf<uint64_t> pairs(c, std::max<uint64_t>(V, 1));
-  if (slots)
+  if (slots) {
+    KernelScope ks(c, "k_bucket_scatter");
     QGM_KERNEL(c, k_bucket_scatter, grid_items, 256, 0, reads.words.p, reads.lengths.p, reads.n, reads.W, span,
                reads.stride, q, G.lb, boff.p, rank.p, pairs.p);
+  }
   rank.release();
 
   out.q = q;
@@ -278,8 +282,11 @@ void build_impl(Ctx& c, const Reads& reads, const Geometry& G, bool sampled, Ind
   DBuf<uint32_t> dcnt(c, G.buckets + 1);
   QGM_CUDA(cudaMemsetAsync(dcnt.p + G.buckets, 0, 4, c.stream));
   const size_t smem_occ = G.gpb * sizeof(W);
-  QGM_KERNEL(c, k_bucket_occupy<W>, grid_b, kBuildThreads, smem_occ, pairs.p, boff.p, G.buckets, uint32_t(G.gpb),
+  {
+    KernelScope ks(c, "k_bucket_occupy");
+    QGM_KERNEL(c, k_bucket_occupy<W>, grid_b, kBuildThreads, smem_occ, pairs.p, boff.p, G.buckets, uint32_t(G.gpb),
              reinterpret_cast<W*>(out.I.p), dcnt.p);
+  }
   DBuf<uint32_t> dbase(c, G.buckets + 1);
   DBuf<uint32_t> dtotal(c, 1);
   exclusive_scan_u32(c, dcnt.p, dbase.p, G.buckets + 1, dtotal.p, nullptr);
@@ -290,6 +297,7 @@ void build_impl(Ctx& c, const Reads& reads, const Geometry& G, bool sampled, Ind
   out.S1.alloc(c, uint64_t(D) + 1);
 
   const size_t smem_emit = G.gpb * sizeof(W) + G.gpb * 4 + (G.gpb * G.w) * 4;
+  KernelScope ks_emit(c, "k_bucket_emit");
   if (sampled) {
     QGM_CUDA(cudaFuncSetAttribute(k_bucket_emit<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_emit)));
     QGM_KERNEL(c, (k_bucket_emit<W, true>), grid_b, kBuildThreads, smem_emit, pairs.p, boff.p, dbase.p, G.buckets,

@@ -32,6 +32,10 @@ struct Ctx {
   double stage_ms[kNumStages] = {0};
   int cur_stage = -1;
   cudaEvent_t cur_a = nullptr;
+  // per-kernel timing of the hot kernels (name -> total ms, launches)
+  struct KMark { const char* name; cudaEvent_t a, b; };
+  std::vector<KMark> kmarks;
+  std::vector<std::pair<std::string, std::pair<double, uint64_t>>> kernel_ms;
 
   cudaEvent_t take_event();
   void stage_begin(int s);
@@ -43,6 +47,25 @@ struct StageScope {
   Ctx& c;
   StageScope(Ctx& ctx, int s) : c(ctx) { c.stage_begin(s); }
   ~StageScope() { c.stage_end(); }
+};
+
+// CUDA-event timing of one kernel launch (profile mode only).
+struct KernelScope {
+  Ctx& c;
+  const char* name;
+  cudaEvent_t a = nullptr;
+  KernelScope(Ctx& ctx, const char* n) : c(ctx), name(n) {
+    if (c.profile) {
+      a = c.take_event();
+      QGM_CUDA(cudaEventRecord(a, c.stream));
+    }
+  }
+  ~KernelScope() {
+    if (!a) return;
+    cudaEvent_t b = c.take_event();
+    cudaEventRecord(b, c.stream);
+    c.kmarks.push_back({name, a, b});
+  }
 };
 
 // Launch on the context stream, count it, surface launch errors.
@@ -144,7 +167,9 @@ struct Cands {
 
 struct HitsObj {
   uint64_t n = 0;
-  uint64_t stats[4] = {0, 0, 0, 0};
+  // raw, unique, validated, hits, index distinct, index occurrences,
+  // filtration lookups with the occupancy bit set, occurrences visited
+  uint64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   DBuf<uint8_t> hits;  // n * 16-byte qgm_hit
 };
 
@@ -179,8 +204,9 @@ void lookup_index(Ctx& c, const Index& idx, const uint32_t* d_codes, uint64_t n,
 
 // filter.cu -- raw candidate keys (unsorted) appended to `keys` (grown and
 // re-run on overflow). Returns the count.
+// fstats (optional, host): {lookups with the occupancy bit set, occurrences visited}.
 uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Ref& ref, int strands, int mode,
-                          unsigned read_bits, DBuf<uint64_t>& keys);
+                          unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats = nullptr);
 
 // validate.cu
 // mode 0: append kept hits as (hit key, k) to hit_keys/hit_vals (counter in

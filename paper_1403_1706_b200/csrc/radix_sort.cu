@@ -128,6 +128,7 @@ void radix_sort(Ctx& c, DBuf<uint64_t>& keys, DBuf<uint64_t>& keys_alt, DBuf<uin
   if (vals && vals_alt->n < n) vals_alt->alloc(c, n);
   const uint32_t tiles = uint32_t(ceil_div(n, kRadixTile));
   DBuf<uint32_t> hist(c, uint64_t(kBins) * tiles);
+  KernelScope ks(c, vals ? "radix_sort_kv" : "radix_sort_keys");
   for (int shift = begin_bit; shift < end_bit; shift += 8) {
     QGM_KERNEL(c, k_upsweep, tiles, kRadixThreads, 0, keys.p, n, shift, hist.p, tiles);
     exclusive_scan_u32(c, hist.p, hist.p, uint64_t(kBins) * tiles, nullptr, nullptr);

@@ -246,6 +246,7 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
   a.counter = d_count;
   a.validated = d_validated;
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, kValThreads), uint64_t(kSMs) * 32));
+  KernelScope ks(c, "k_validate");
   if (band <= 32) QGM_KERNEL(c, k_validate<uint32_t>, grid, kValThreads, 0, a);
   else QGM_KERNEL(c, k_validate<uint64_t>, grid, kValThreads, 0, a);
 }

@@ -4,6 +4,7 @@
 #include <cstring>
 
 int main(int argc, char** argv) {
+  std::setvbuf(stdout, nullptr, _IOLBF, 0);
   const char* filter = argc > 1 ? argv[1] : nullptr;
   long cases = 0, failed_cases = 0;
   for (const auto& tc : catch_shim::registry()) {
