@@ -4,7 +4,7 @@
  * plain pointers and sizes, no C++ or torch types, no exceptions. Every entry
  * point names the reference interface it replaces (paths relative to the
  * reference checkout, proj/include/qgmap/... ; SPEC.md for the spec-only
- * stages). The C++ mirror of the reference API (include/qgmap/*.hpp) and the
+ * stages). The C++ mirror of the reference API (the include/qgmap headers) and the
  * python binding (paper_1403_1706_b200/__init__.py) are thin layers over it.
  *
  * Sequence format ("2-bit MSB-first"): base j of a sequence lives in 64-bit
@@ -46,6 +46,7 @@ extern "C" {
 
 #define QGM_FILTER_FULL 0      /* Alg. 2 multiset */
 #define QGM_FILTER_RUN_START 1 /* leftmost q-gram of each run per diagonal (same set) */
+#define QGM_FILTER_JOIN 2      /* flag: bucket-ordered join with the reference q-group index */
 
 typedef struct qgm_ctx qgm_ctx;
 typedef struct qgm_reads qgm_reads;
@@ -176,6 +177,11 @@ void qgm_index_destroy(qgm_index* idx);
  * position x excluded from P (repeat mask). */
 int qgm_ref_upload(qgm_ctx* ctx, const uint64_t* ref2bit, const uint64_t* chrom_begin, uint32_t n_chrom,
                    const uint64_t* mask_bits, qgm_ref** out);
+/* Build (and cache on ref) the reference-side q-group indexes for q, one per
+ * strand: the precomputed reference index of SPEC.md:262-316 with P ordered by
+ * q-gram. qgm_map does this lazily on first use of a q; call it
+ * ahead of time to keep it out of the first batch. References < 2^32 bases. */
+int qgm_ref_prepare(qgm_ctx* ctx, qgm_ref* ref, uint32_t q);
 void qgm_ref_destroy(qgm_ref* ref);
 
 /* ---- filtration: Alg. 2 -------------- */

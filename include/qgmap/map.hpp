@@ -25,7 +25,15 @@ struct Hit {
   auto operator<=>(const Hit&) const = default;
 };
 
-enum class FilterMode { full = QGM_FILTER_FULL, run_start = QGM_FILTER_RUN_START };
+// full / run_start: stream the reference against the read index (filter.cu);
+// *_join: bucket-ordered join of the read q-grams with the reference q-group
+// indexes (join.cu, the path qgm_map uses). All four give the same candidate set.
+enum class FilterMode {
+  full = QGM_FILTER_FULL,
+  run_start = QGM_FILTER_RUN_START,
+  full_join = QGM_FILTER_FULL | QGM_FILTER_JOIN,
+  run_start_join = QGM_FILTER_RUN_START | QGM_FILTER_JOIN
+};
 
 // filter_reference over every unmasked reference position of
 // every chromosome, both strands by default. Sorted by (r, strand, chrom, d).

@@ -37,6 +37,7 @@ MODE_BEST_STRATUM = 0
 MODE_ALL = 1
 FILTER_FULL = 0
 FILTER_RUN_START = 1
+FILTER_JOIN = 2  # flag: bucket-ordered join with the reference q-group index (join.cu)
 STAGES = ("reads", "index", "filter", "sort_unique", "validate", "strata", "d2h", "other")
 
 CANDIDATE_DTYPE = np.dtype([("diagonal", "<i8"), ("read_id", "<u4"), ("chrom", "<u4"),
@@ -88,7 +89,7 @@ EXPORTS = (
     "qgm_ctx_synchronize", "qgm_ctx_profile", "qgm_ctx_stage_times", "qgm_ctx_kernel_times", "qgm_ctx_launches", "qgm_pack_codes",
     "qgm_pack_reads", "qgm_reads_upload", "qgm_reads_from_device", "qgm_reads_destroy", "qgm_index_build",
     "qgm_index_sample", "qgm_index_normalize", "qgm_index_info_get", "qgm_index_download", "qgm_index_lookup",
-    "qgm_index_destroy", "qgm_ref_upload", "qgm_ref_destroy", "qgm_filter", "qgm_cands_count",
+    "qgm_index_destroy", "qgm_ref_upload", "qgm_ref_prepare", "qgm_ref_destroy", "qgm_filter", "qgm_cands_count",
     "qgm_cands_download", "qgm_cands_unique", "qgm_cands_destroy", "qgm_validate", "qgm_map", "qgm_hits_count",
     "qgm_hits_stats", "qgm_hits_download", "qgm_hits_destroy", "qgm_map_host", "qgm_exclusive_scan_u32",
 )
@@ -135,6 +136,7 @@ def load_library(path: str = LIB_PATH):
         "qgm_index_lookup": (i32, [P, P, P, u64, P, P]),
         "qgm_index_destroy": (None, [P]),
         "qgm_ref_upload": (i32, [P, P, P, u32, P, C.POINTER(P)]),
+        "qgm_ref_prepare": (i32, [P, P, u32]),
         "qgm_ref_destroy": (None, [P]),
         "qgm_filter": (i32, [P, P, P, P, i32, i32, C.POINTER(P)]),
         "qgm_cands_count": (i32, [P, C.POINTER(u64)]),
@@ -400,6 +402,11 @@ class Reference:
             mb = np.packbits(padded, bitorder="little").view(np.uint64).copy() \
                 if padded.size else np.zeros(1, np.uint64)
         return cls(ctx, pack_codes(codes), chrom_begin, mb)
+
+    def prepare(self, q: int):
+        """Build the per-strand reference q-group indexes for q (qgm_ref_prepare)."""
+        self.ctx._check(self.ctx.lib.qgm_ref_prepare(self.ctx.h, self.h, q))
+        return self
 
     def close(self):
         if getattr(self, "h", None):

@@ -172,23 +172,39 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   const unsigned rb = read_bits_for(reads.n);
   const int key_bits = int(rb + 1 + ref.diag_bits);
   HitsObj out;
-  Index idx;
-  {
-    StageScope s(c, kStageIndex);
-    build_index(c, reads, P.q, P.group_width ? P.group_width : 32, P.sampled != 0, idx);
-  }
   DBuf<uint64_t> keys, alt;
   uint64_t n_raw, n_u;
   uint64_t fst[2] = {0, 0};
-  out.stats[4] = idx.distinct;
-  out.stats[5] = idx.occ;
-  {
+  if (P.group_width && P.group_width != 32 && P.group_width != 64) throw InputError("group width must be 32 or 64");
+  if (ref.total < (uint64_t(1) << 32)) {
+    // production path: read q-grams bucket-sorted by code, joined with the
+    // per-strand reference q-group indexes (join.cu). group_width / sampled
+    // only change the layout of an index that is never materialised here.
+    prepare_ref_index(c, ref, P.q);  // once per reference and q (cached)
+    Buckets rbk;
+    {
+      StageScope s(c, kStageIndex);
+      bucket_reads(c, reads, P.q, 32, rbk);
+    }
+    out.stats[5] = rbk.V;
+    {
+      StageScope s(c, kStageFilter);
+      n_raw = join_filter(c, rbk, reads, ref, strands, QGM_FILTER_RUN_START, rb, keys, fst);
+    }
+  } else {
+    // references beyond 2^32 bases: stream the reference against the read index (filter.cu)
+    Index idx;
+    {
+      StageScope s(c, kStageIndex);
+      build_index(c, reads, P.q, P.group_width ? P.group_width : 32, P.sampled != 0, idx);
+    }
+    out.stats[4] = idx.distinct;
+    out.stats[5] = idx.occ;
     StageScope s(c, kStageFilter);
     n_raw = filter_reference(c, idx, reads, ref, strands, QGM_FILTER_RUN_START, rb, keys, fst);
   }
   out.stats[6] = fst[0];
   out.stats[7] = fst[1];
-  idx = Index();  // the index is per batch; release it before validation
   {
     StageScope s(c, kStageSort);
     radix_sort(c, keys, alt, nullptr, nullptr, n_raw, 0, key_bits);
@@ -558,6 +574,17 @@ int qgm_ref_upload(qgm_ctx* ctx, const uint64_t* ref2bit, const uint64_t* chrom_
   return rc;
 }
 
+int qgm_ref_prepare(qgm_ctx* ctx, qgm_ref* ref, uint32_t q) {
+  if (!ctx || !ref) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    require(q >= 1 && q <= 16, "q must be in [1, 16]");
+    require(ref->r.total < (uint64_t(1) << 32), "reference index: more than 2^32-1 bases");
+    qgm::prepare_ref_index(ctx->c, ref->r, q);
+    QGM_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
 void qgm_ref_destroy(qgm_ref* r) {
   if (!r) return;
   cudaSetDevice(r->owner->c.device);
@@ -573,15 +600,23 @@ int qgm_filter(qgm_ctx* ctx, const qgm_index* idx, const qgm_reads* reads, const
   int rc = guard(ctx, [&] {
     activate(ctx);
     require(strands >= 1 && strands <= 3, "strands must be 1, 2 or 3");
-    require(mode == QGM_FILTER_FULL || mode == QGM_FILTER_RUN_START, "unknown filter mode");
+    const int base_mode = mode & ~QGM_FILTER_JOIN;
+    require(base_mode == QGM_FILTER_FULL || base_mode == QGM_FILTER_RUN_START, "unknown filter mode");
     qgm::Ctx& c = ctx->c;
     auto& C = cd->c;
     C.read_bits = qgm::read_bits_for(reads->r.n);
     C.diag_bits = ref->r.diag_bits;
     C.cbp = ref->r.cbp;
-    {
+    if (idx->i.stride != reads->r.stride || idx->i.n_reads != reads->r.n)
+      throw qgm::InputError("index was built over a different read buffer");
+    if (mode & QGM_FILTER_JOIN) {
+      qgm::Buckets rbk;
+      qgm::bucket_reads(c, reads->r, idx->i.q, 32, rbk);
       qgm::StageScope s(c, qgm::kStageFilter);
-      C.n = qgm::filter_reference(c, idx->i, reads->r, ref->r, strands, mode, C.read_bits, C.keys);
+      C.n = qgm::join_filter(c, rbk, reads->r, ref->r, strands, base_mode, C.read_bits, C.keys);
+    } else {
+      qgm::StageScope s(c, qgm::kStageFilter);
+      C.n = qgm::filter_reference(c, idx->i, reads->r, ref->r, strands, base_mode, C.read_bits, C.keys);
     }
     qgm::StageScope s(c, qgm::kStageSort);
     qgm::DBuf<uint64_t> alt;

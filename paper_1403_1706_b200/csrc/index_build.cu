@@ -1,4 +1,4 @@
-// index_build.cu -- stage 1: on-the-fly q-group index over one read buffer.
+// index_build.cu -- stage 1: the q-group index, built on the device.
 //
 // Same arrays and semantics as build_qgroup_index<W> (qgroup_index.hpp:124-180,
 // Alg. 1 of PAPER.md:153-193): occupancy I, group starts S (+ sentinel,
@@ -7,22 +7,25 @@
 // unspecified, exactly as in the reference (qgroup_index.hpp:120-123);
 // qgm_index_normalize sorts it.
 //
-// B200 design (a two-level counting sort on the q-gram code instead of the
-// reference's six passes of random atomics into 4^q/w-sized arrays):
-//   K1 rank    : one thread per read q-gram; code g, bucket = g >> lb (top
-//                2q-lb bits); warp-aggregated atomicAdd on a per-bucket count
-//                (L2 resident) returns the item's rank inside its bucket.
+// B200 design: a two-level counting sort on the q-gram code instead of the
+// reference's six passes of random atomics into 4^q/w-sized arrays.
+//   K1 rank    : one thread per item (a read q-gram, or a reference position
+//                of one strand); code g, bucket = g >> lb (the top 2q-lb
+//                bits); warp-aggregated atomicAdd on the bucket's count (L2
+//                resident) returns the item's rank inside the bucket.
 //   scan       : bucket offsets.
-//   K2 scatter : (g & lowmask, position) pairs into their bucket.
-//   K3 occupy  : one CTA per bucket (2^lb codes = 2^lb/w group words) builds the
-//                bucket's occupancy words in shared memory, writes I and the
-//                bucket's distinct count.
+//   K2 scatter : (extra, g & lowmask, position) packed in one u64 per item.
+//   -- the bucketed items are all the per-batch join of join.cu needs --
+//   K3 occupy  : one CTA per bucket (2^lb codes = 2^lb/w group words) builds
+//                the bucket's occupancy words in shared memory, writes I and
+//                the bucket's distinct count.
 //   scan       : distinct offsets (the global base of S for every bucket).
-//   K4 emit    : one CTA per bucket rebuilds the local ranks from I, writes
-//                S (popcount prefix), S' (occurrence prefix) and scatters the
-//                positions into O through shared-memory cursors.
+//   K4 emit    : one CTA per bucket rebuilds the local ranks from I, writes S
+//                (popcount prefix), S' (occurrence prefix) and scatters the
+//                positions (and the per-item extra byte) into O through
+//                shared-memory cursors.
 // Every HBM write of I/S/S'/O is coalesced; the only random traffic is the
-// bucket scatter, whose tails stay L2 resident.
+// bucket scatter of K2.
 #include "internal.hpp"
 
 namespace qgm {
@@ -30,42 +33,75 @@ namespace {
 
 constexpr unsigned kLowBits = 13;  // codes per bucket = 8192
 constexpr int kBuildThreads = 256;
+constexpr uint64_t kLowMask = (1u << kLowBits) - 1;
 
-struct Geometry {
-  unsigned q, w, lb, hb;
-  uint64_t groups, buckets, gpb;  // gpb = group words per bucket
+// Read q-grams: one slot per (read, offset) with offset <= stride-q; slots
+// past a read's length are idle (seq.hpp:135-137).
+struct ReadSource {
+  const uint64_t* words;
+  const uint32_t* lengths;
+  uint32_t W, span, stride;
+  unsigned q;
+  __device__ __forceinline__ bool item(uint64_t t, uint32_t& g, uint32_t& pos, uint32_t& extra) const {
+    const uint32_t r = uint32_t(t / span);
+    const uint32_t o = uint32_t(t - uint64_t(r) * span);
+    if (o + q > __ldg(lengths + r)) return false;
+    g = qgram_at(words + uint64_t(r) * W, o, q);
+    pos = r * stride + o;
+    extra = 0;
+    return true;
+  }
 };
 
-Geometry geometry(unsigned q, unsigned w) {
-  Geometry g;
-  g.q = q;
-  g.w = w;
-  g.lb = std::min(2 * q, kLowBits);
-  g.hb = 2 * q - g.lb;
-  const uint64_t space = uint64_t(1) << (2 * q);
-  g.groups = ceil_div(space, w);
-  g.buckets = uint64_t(1) << g.hb;
-  g.gpb = std::max<uint64_t>(1, (uint64_t(1) << g.lb) / w);
-  if (g.buckets * g.gpb != g.groups) throw InternalError("index geometry mismatch");
-  return g;
-}
-
-// One slot per (read, offset) with offset <= stride-q; slots past a read's
-// length are idle (seq.hpp:135-137: only windows inside a read are indexed).
-__global__ void k_bucket_rank(const uint64_t* __restrict__ words, const uint32_t* __restrict__ lengths,
-                              uint32_t n_reads, uint32_t W, uint32_t span, unsigned q, unsigned lb,
-                              uint32_t* __restrict__ bucket_cnt, uint32_t* __restrict__ rank) {
-  const uint64_t total = uint64_t(n_reads) * span;
-  for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < total; base += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t t = base + threadIdx.x;
-    bool ok = t < total;
-    uint32_t r = 0, o = 0, b = 0xFFFFFFFFu;
-    if (ok) {
-      r = uint32_t(t / span);
-      o = uint32_t(t - uint64_t(r) * span);
-      ok = o + q <= __ldg(lengths + r);
-      if (ok) b = qgram_at(words + uint64_t(r) * W, o, q) >> lb;
+// Reference positions of one strand: every global position whose window lies
+// inside its chromosome and is not masked. The code is the
+// forward q-gram, or the code of its reverse complement for the RC strand.
+// extra = the base the run-start rule compares (ref[p-1], or its complement
+// on the RC strand), or 4 when p-1 is outside the chromosome or masked.
+struct RefSource {
+  const uint64_t* ref;
+  const uint64_t* mask;
+  const uint64_t* cb;
+  uint32_t n_chrom;
+  unsigned q;
+  bool rc;
+  __device__ __forceinline__ bool masked(uint64_t x) const {
+    return mask && ((__ldg(mask + (x >> 6)) >> (x & 63)) & 1ull);
+  }
+  __device__ __forceinline__ bool item(uint64_t x, uint32_t& g, uint32_t& pos, uint32_t& extra) const {
+    if (masked(x)) return false;
+    uint32_t lo = 0, hi = n_chrom;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(cb + mid) <= x) lo = mid; else hi = mid;
     }
+    const uint64_t cbeg = __ldg(cb + lo), p = x - cbeg;
+    if (p + q > __ldg(cb + lo + 1) - cbeg) return false;
+    g = qgram_at(ref, x, q);
+    if (rc) g = rc_code(g, q);
+    pos = uint32_t(x);
+    extra = 4;
+    if (p >= 1 && !masked(x - 1)) {
+      const uint32_t b = base_at(ref, x - 1);
+      extra = rc ? 3u - b : b;
+    }
+    return true;
+  }
+};
+
+__device__ __forceinline__ uint64_t pack_item(uint32_t extra, uint32_t glow, uint32_t pos) {
+  return (uint64_t(extra) << 45) | (uint64_t(glow) << 32) | pos;
+}
+__device__ __forceinline__ uint32_t item_glow(uint64_t pr) { return uint32_t(pr >> 32) & uint32_t(kLowMask); }
+
+template <class Src>
+__global__ void k_bucket_rank(Src src, uint64_t n_items, unsigned lb, uint32_t* __restrict__ bucket_cnt,
+                              uint32_t* __restrict__ rank) {
+  for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < n_items; base += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t t = base + threadIdx.x;
+    uint32_t g = 0, pos, extra, b = 0xFFFFFFFFu;
+    const bool ok = t < n_items && src.item(t, g, pos, extra);
+    if (ok) b = g >> lb;
     const unsigned peers = __match_any_sync(kFull, b);
     const int leader = __ffs(peers) - 1;
     uint32_t base_rank = 0;
@@ -75,20 +111,15 @@ __global__ void k_bucket_rank(const uint64_t* __restrict__ words, const uint32_t
   }
 }
 
-__global__ void k_bucket_scatter(const uint64_t* __restrict__ words, const uint32_t* __restrict__ lengths,
-                                 uint32_t n_reads, uint32_t W, uint32_t span, uint32_t stride, unsigned q,
-                                 unsigned lb, const uint32_t* __restrict__ boff, const uint32_t* __restrict__ rank,
-                                 uint64_t* __restrict__ pairs) {
-  const uint64_t total = uint64_t(n_reads) * span;
+template <class Src>
+__global__ void k_bucket_scatter(Src src, uint64_t n_items, unsigned lb, const uint32_t* __restrict__ boff,
+                                 const uint32_t* __restrict__ rank, uint64_t* __restrict__ pairs) {
   const uint32_t lmask = (1u << lb) - 1u;
-  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n_items;
        t += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t r = uint32_t(t / span);
-    const uint32_t o = uint32_t(t - uint64_t(r) * span);
-    if (o + q > __ldg(lengths + r)) continue;
-    const uint32_t g = qgram_at(words + uint64_t(r) * W, o, q);
-    const uint32_t p = r * stride + o;
-    pairs[boff[g >> lb] + rank[t]] = (uint64_t(g & lmask) << 32) | p;
+    uint32_t g, pos, extra;
+    if (!src.item(t, g, pos, extra)) continue;
+    pairs[boff[g >> lb] + rank[t]] = pack_item(extra, g & lmask, pos);
   }
 }
 
@@ -97,6 +128,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_occupy(const uint64_t*
                                                                  const uint32_t* __restrict__ boff,
                                                                  uint64_t buckets, uint32_t gpb,
                                                                  W* __restrict__ I, uint32_t* __restrict__ dcnt) {
+  using AW = typename std::conditional<sizeof(W) == 8, unsigned long long, unsigned>::type;
   constexpr unsigned w = GroupTraits<W>::width;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   W* occ = reinterpret_cast<W*>(smem_raw);
@@ -106,10 +138,8 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_occupy(const uint64_t*
     __syncthreads();
     const uint32_t b0 = boff[bk], b1 = boff[bk + 1];
     for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-      const uint32_t gl = uint32_t(pairs[i] >> 32);
-      atomicOr(reinterpret_cast<typename std::conditional<sizeof(W) == 8, unsigned long long, unsigned>::type*>(
-                   occ + gl / w),
-               (typename std::conditional<sizeof(W) == 8, unsigned long long, unsigned>::type)(W(1) << (gl % w)));
+      const uint32_t gl = item_glow(pairs[i]);
+      atomicOr(reinterpret_cast<AW*>(occ + gl / w), AW(W(1) << (gl % w)));
     }
     __syncthreads();
     uint32_t pc = 0;
@@ -125,13 +155,14 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_occupy(const uint64_t*
   }
 }
 
-template <class W, bool kSampled>
+template <class W, bool kSampled, bool kExtra>
 __global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* __restrict__ pairs,
                                                                const uint32_t* __restrict__ boff,
                                                                const uint32_t* __restrict__ dbase,
                                                                uint64_t buckets, uint32_t gpb,
                                                                const W* __restrict__ I, uint32_t* __restrict__ S,
-                                                               uint32_t* __restrict__ S1, uint32_t* __restrict__ O) {
+                                                               uint32_t* __restrict__ S1, uint32_t* __restrict__ O,
+                                                               uint8_t* __restrict__ X) {
   constexpr unsigned w = GroupTraits<W>::width;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   W* occ = reinterpret_cast<W*>(smem_raw);
@@ -156,7 +187,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* _
     __syncthreads();
     const uint32_t b0 = boff[bk], b1 = boff[bk + 1];
     for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-      const uint32_t gl = uint32_t(pairs[i] >> 32);
+      const uint32_t gl = item_glow(pairs[i]);
       const uint32_t wi = gl / w;
       atomicAdd(cnt + sloc[wi] + rank_below<W>(occ[wi], gl % w), 1u);
     }
@@ -166,10 +197,11 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* _
     __syncthreads();
     for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
       const uint64_t pr = pairs[i];
-      const uint32_t gl = uint32_t(pr >> 32);
+      const uint32_t gl = item_glow(pr);
       const uint32_t wi = gl / w;
       const uint32_t slot = atomicAdd(cnt + sloc[wi] + rank_below<W>(occ[wi], gl % w), 1u);
       O[b0 + slot] = uint32_t(pr);
+      if (kExtra) X[b0 + slot] = uint8_t(pr >> 45);
     }
     __syncthreads();
   }
@@ -236,91 +268,143 @@ __global__ void k_lookup(const W* __restrict__ I, const uint32_t* __restrict__ S
   }
 }
 
-template <class W>
-void build_impl(Ctx& c, const Reads& reads, const Geometry& G, bool sampled, Index& out) {
-  const unsigned q = G.q;
-  const uint32_t span = reads.stride >= q ? reads.stride - q + 1 : 0;
-  const uint64_t slots = uint64_t(reads.n) * span;
-
-  DBuf<uint32_t> bucket_cnt(c, G.buckets + 1);
+template <class Src>
+void bucket_impl(Ctx& c, const Src& src, uint64_t n_items, Buckets& B) {
+  DBuf<uint32_t> bucket_cnt(c, B.buckets + 1);
   bucket_cnt.zero();
-  DBuf<uint32_t> rank(c, std::max<uint64_t>(slots, 1));
-  const unsigned grid_items = unsigned(std::min<uint64_t>(std::max<uint64_t>(ceil_div(slots, 256), 1), kSMs * 32));
-  if (slots) {
+  DBuf<uint32_t> rank(c, std::max<uint64_t>(n_items, 1));
+  const unsigned grid = unsigned(std::min<uint64_t>(std::max<uint64_t>(ceil_div(n_items, 256), 1), kSMs * 32));
+  if (n_items) {
     KernelScope ks(c, "k_bucket_rank");
-    QGM_KERNEL(c, k_bucket_rank, grid_items, 256, 0, reads.words.p, reads.lengths.p, reads.n, reads.W, span, q, G.lb,
-               bucket_cnt.p, rank.p);
+    QGM_KERNEL(c, k_bucket_rank<Src>, grid, 256, 0, src, n_items, B.lb, bucket_cnt.p, rank.p);
   }
-  DBuf<uint32_t> boff(c, G.buckets + 1);
+  B.boff.alloc(c, B.buckets + 1);
   DBuf<uint32_t> vtotal(c, 1);
-  exclusive_scan_u32(c, bucket_cnt.p, boff.p, G.buckets + 1, vtotal.p, nullptr);
+  exclusive_scan_u32(c, bucket_cnt.p, B.boff.p, B.buckets + 1, vtotal.p, nullptr);
   uint32_t V = 0;
   QGM_CUDA(cudaMemcpyAsync(&V, vtotal.p, 4, cudaMemcpyDeviceToHost, c.stream));
   QGM_CUDA(cudaStreamSynchronize(c.stream));
-
-  DBuf<uint64_t> pairs(c, std::max<uint64_t>(V, 1));
-  if (slots) {
+  B.V = V;
+  B.pairs.alloc(c, std::max<uint64_t>(V, 1));
+  if (n_items) {
     KernelScope ks(c, "k_bucket_scatter");
-    QGM_KERNEL(c, k_bucket_scatter, grid_items, 256, 0, reads.words.p, reads.lengths.p, reads.n, reads.W, span,
-               reads.stride, q, G.lb, boff.p, rank.p, pairs.p);
+    QGM_KERNEL(c, k_bucket_scatter<Src>, grid, 256, 0, src, n_items, B.lb, B.boff.p, rank.p, B.pairs.p);
   }
-  rank.release();
+}
 
-  out.q = q;
-  out.w = G.w;
+template <class W>
+void finish_impl(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_t>* extra) {
+  out.q = B.q;
+  out.w = B.w;
   out.sampled = sampled;
-  out.groups = G.groups;
-  out.gs_len = sampled ? (G.groups + 1 + 1) / 2 : G.groups + 1;
-  out.occ = V;
-  out.stride = reads.stride;
-  out.n_reads = reads.n;
-  out.I.alloc(c, G.groups * sizeof(W));
+  out.groups = B.groups;
+  out.gs_len = sampled ? (B.groups + 1 + 1) / 2 : B.groups + 1;
+  out.occ = B.V;
+  out.I.alloc(c, B.groups * sizeof(W));
   out.S.alloc(c, out.gs_len);
-  out.O.alloc(c, std::max<uint64_t>(V, 1));
+  out.O.alloc(c, std::max<uint64_t>(B.V, 1));
+  if (extra) extra->alloc(c, std::max<uint64_t>(B.V, 1));
 
-  const unsigned grid_b = unsigned(std::min<uint64_t>(G.buckets, uint64_t(kSMs) * 8));
-  DBuf<uint32_t> dcnt(c, G.buckets + 1);
-  QGM_CUDA(cudaMemsetAsync(dcnt.p + G.buckets, 0, 4, c.stream));
-  const size_t smem_occ = G.gpb * sizeof(W);
+  const unsigned grid_b = unsigned(std::min<uint64_t>(B.buckets, uint64_t(kSMs) * 8));
+  DBuf<uint32_t> dcnt(c, B.buckets + 1);
+  QGM_CUDA(cudaMemsetAsync(dcnt.p + B.buckets, 0, 4, c.stream));
   {
     KernelScope ks(c, "k_bucket_occupy");
-    QGM_KERNEL(c, k_bucket_occupy<W>, grid_b, kBuildThreads, smem_occ, pairs.p, boff.p, G.buckets, uint32_t(G.gpb),
-             reinterpret_cast<W*>(out.I.p), dcnt.p);
+    QGM_KERNEL(c, k_bucket_occupy<W>, grid_b, kBuildThreads, B.gpb * sizeof(W), B.pairs.p, B.boff.p, B.buckets,
+               uint32_t(B.gpb), reinterpret_cast<W*>(out.I.p), dcnt.p);
   }
-  DBuf<uint32_t> dbase(c, G.buckets + 1);
+  DBuf<uint32_t> dbase(c, B.buckets + 1);
   DBuf<uint32_t> dtotal(c, 1);
-  exclusive_scan_u32(c, dcnt.p, dbase.p, G.buckets + 1, dtotal.p, nullptr);
+  exclusive_scan_u32(c, dcnt.p, dbase.p, B.buckets + 1, dtotal.p, nullptr);
   uint32_t D = 0;
   QGM_CUDA(cudaMemcpyAsync(&D, dtotal.p, 4, cudaMemcpyDeviceToHost, c.stream));
   QGM_CUDA(cudaStreamSynchronize(c.stream));
   out.distinct = D;
   out.S1.alloc(c, uint64_t(D) + 1);
 
-  const size_t smem_emit = G.gpb * sizeof(W) + G.gpb * 4 + (G.gpb * G.w) * 4;
-  KernelScope ks_emit(c, "k_bucket_emit");
+  const size_t smem = B.gpb * sizeof(W) + B.gpb * 4 + (B.gpb * B.w) * 4;
+  auto launch = [&](auto kernel) {
+    QGM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    KernelScope ks(c, "k_bucket_emit");
+    QGM_KERNEL(c, kernel, grid_b, kBuildThreads, smem, B.pairs.p, B.boff.p, dbase.p, B.buckets, uint32_t(B.gpb),
+               reinterpret_cast<const W*>(out.I.p), out.S.p, out.S1.p, out.O.p, extra ? extra->p : nullptr);
+  };
   if (sampled) {
-    QGM_CUDA(cudaFuncSetAttribute(k_bucket_emit<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_emit)));
-    QGM_KERNEL(c, (k_bucket_emit<W, true>), grid_b, kBuildThreads, smem_emit, pairs.p, boff.p, dbase.p, G.buckets,
-               uint32_t(G.gpb), reinterpret_cast<const W*>(out.I.p), out.S.p, out.S1.p, out.O.p);
+    if (extra) launch(k_bucket_emit<W, true, true>);
+    else launch(k_bucket_emit<W, true, false>);
   } else {
-    QGM_CUDA(cudaFuncSetAttribute(k_bucket_emit<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_emit)));
-    QGM_KERNEL(c, (k_bucket_emit<W, false>), grid_b, kBuildThreads, smem_emit, pairs.p, boff.p, dbase.p, G.buckets,
-               uint32_t(G.gpb), reinterpret_cast<const W*>(out.I.p), out.S.p, out.S1.p, out.O.p);
+    if (extra) launch(k_bucket_emit<W, false, true>);
+    else launch(k_bucket_emit<W, false, false>);
   }
   // sentinels: S[groups] = D (kept by sampling iff groups is even), S'[D] = V
-  if (!sampled) QGM_KERNEL(c, k_set_u32, 1, 1, 0, out.S.p + G.groups, D);
-  else if ((G.groups & 1) == 0) QGM_KERNEL(c, k_set_u32, 1, 1, 0, out.S.p + G.groups / 2, D);
-  QGM_KERNEL(c, k_set_u32, 1, 1, 0, out.S1.p + D, V);
+  if (!sampled) QGM_KERNEL(c, k_set_u32, 1, 1, 0, out.S.p + B.groups, D);
+  else if ((B.groups & 1) == 0) QGM_KERNEL(c, k_set_u32, 1, 1, 0, out.S.p + B.groups / 2, D);
+  QGM_KERNEL(c, k_set_u32, 1, 1, 0, out.S1.p + D, B.V);
+}
+
+void init_geometry(Buckets& B, unsigned q, unsigned w) {
+  if (q == 0 || q > 16) throw InputError("q must be in [1, 16]");
+  if (w != 32 && w != 64) throw InputError("group width must be 32 or 64");
+  B.q = q;
+  B.w = w;
+  B.lb = std::min(2 * q, kLowBits);
+  B.hb = 2 * q - B.lb;
+  const uint64_t space = uint64_t(1) << (2 * q);
+  B.groups = ceil_div(space, w);
+  B.buckets = uint64_t(1) << B.hb;
+  B.gpb = std::max<uint64_t>(1, (uint64_t(1) << B.lb) / w);
+  if (B.buckets * B.gpb != B.groups) throw InternalError("index geometry mismatch");
 }
 
 }  // namespace
 
+void bucket_reads(Ctx& c, const Reads& reads, unsigned q, unsigned w, Buckets& out) {
+  init_geometry(out, q, w);
+  ReadSource src;
+  src.words = reads.words.p;
+  src.lengths = reads.lengths.p;
+  src.W = reads.W;
+  src.span = reads.stride >= q ? reads.stride - q + 1 : 0;
+  src.stride = reads.stride;
+  src.q = q;
+  bucket_impl(c, src, uint64_t(reads.n) * src.span, out);
+}
+
+void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool rc, Buckets& out) {
+  init_geometry(out, q, 32);
+  if (ref.total >= (uint64_t(1) << 32)) throw InputError("reference index: more than 2^32-1 bases");
+  RefSource src;
+  src.ref = ref.words.p;
+  src.mask = ref.mask.p;
+  src.cb = ref.d_cb.p;
+  src.n_chrom = ref.n_chrom;
+  src.q = q;
+  src.rc = rc;
+  bucket_impl(c, src, ref.total, out);
+}
+
+void index_from_buckets(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_t>* extra) {
+  if (B.w == 32) finish_impl<uint32_t>(c, B, sampled, out, extra);
+  else finish_impl<uint64_t>(c, B, sampled, out, extra);
+}
+
 void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sampled, Index& out) {
-  if (q == 0 || q > 16) throw InputError("q must be in [1, 16]");
-  if (w != 32 && w != 64) throw InputError("group width must be 32 or 64");
-  const Geometry G = geometry(q, w);
-  if (w == 32) build_impl<uint32_t>(c, reads, G, sampled, out);
-  else build_impl<uint64_t>(c, reads, G, sampled, out);
+  Buckets B;
+  bucket_reads(c, reads, q, w, B);
+  index_from_buckets(c, B, sampled, out, nullptr);
+  out.stride = reads.stride;
+  out.n_reads = reads.n;
+}
+
+void prepare_ref_index(Ctx& c, const Ref& ref, unsigned q) {
+  if (ref.qidx.q == q) return;
+  ref.qidx = RefQIndex();
+  for (int rc = 0; rc < 2; ++rc) {
+    Buckets B;
+    bucket_ref(c, ref, q, rc != 0, B);
+    index_from_buckets(c, B, false, rc ? ref.qidx.rc : ref.qidx.fwd, rc ? &ref.qidx.prev_rc : &ref.qidx.prev_fwd);
+  }
+  ref.qidx.q = q;
 }
 
 void sample_index(Ctx& c, const Index& in, Index& out) {

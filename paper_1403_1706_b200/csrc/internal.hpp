@@ -127,6 +127,40 @@ struct Reads {
   DBuf<uint2> planes;      // n * Wp, word 0 of every read is a zero guard
 };
 
+// q-group index (QGroupIndex<W>, qgroup_index.hpp:28-104) in device memory.
+struct Index {
+  unsigned q = 0, w = 32;
+  bool sampled = false;
+  uint64_t groups = 0, gs_len = 0, distinct = 0, occ = 0;
+  uint32_t stride = 0, n_reads = 0;
+  DBuf<uint8_t> I;        // groups words of w bits
+  DBuf<uint32_t> S;       // gs_len
+  DBuf<uint32_t> S1;      // distinct + 1
+  DBuf<uint32_t> O;       // occ
+};
+
+// Items bucketed by the top 2q-13 bits of their q-gram code (the first half
+// of the index build, index_build.cu). pairs[i] = extra << 45 | (code & 8191)
+// << 32 | position; bucket k holds pairs[boff[k], boff[k+1]).
+struct Buckets {
+  unsigned q = 0, w = 32, lb = 0, hb = 0;
+  uint64_t groups = 0, buckets = 0, gpb = 0;
+  uint32_t V = 0;
+  DBuf<uint32_t> boff;
+  DBuf<uint64_t> pairs;
+};
+
+// q-group indexes over the reference itself, one per strand (the RC index is
+// keyed by the code of the reverse-complemented window), with the base the
+// run-start rule compares stored next to every position (4 = none). Built
+// once per reference and q (SPEC.md:262-316's precomputed reference index,
+// with P ordered by q-gram as in PAPER.md:344).
+struct RefQIndex {
+  unsigned q = 0;
+  Index fwd, rc;
+  DBuf<uint8_t> prev_fwd, prev_rc;
+};
+
 // Reference sequences (ReferenceIndex): the concatenated
 // chromosomes in 2-bit (+1 guard word) and as lo/hi bit planes (2 guard words
 // on both sides). Diagonals are keyed in a padded coordinate space where
@@ -144,18 +178,7 @@ struct Ref {
   DBuf<uint2> planes;         // ceil(total/32)+4 (lo, hi)
   DBuf<uint64_t> mask;        // nullable: bit x = masked
   DBuf<uint64_t> d_cb, d_cbp; // n_chrom+1 each
-};
-
-// q-group index (QGroupIndex<W>, qgroup_index.hpp:28-104) in device memory.
-struct Index {
-  unsigned q = 0, w = 32;
-  bool sampled = false;
-  uint64_t groups = 0, gs_len = 0, distinct = 0, occ = 0;
-  uint32_t stride = 0, n_reads = 0;
-  DBuf<uint8_t> I;        // groups words of w bits
-  DBuf<uint32_t> S;       // gs_len
-  DBuf<uint32_t> S1;      // distinct + 1
-  DBuf<uint32_t> O;       // occ
+  mutable RefQIndex qidx;     // cache, built lazily per q (prepare_ref_index)
 };
 
 struct Cands {
@@ -196,7 +219,11 @@ void make_read_planes(Ctx& c, Reads& r);
 void make_ref_planes(Ctx& c, Ref& ref);
 
 // index_build.cu
+void bucket_reads(Ctx& c, const Reads& reads, unsigned q, unsigned w, Buckets& out);
+void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool rc, Buckets& out);
+void index_from_buckets(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_t>* extra);
 void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sampled, Index& out);
+void prepare_ref_index(Ctx& c, const Ref& ref, unsigned q);
 void sample_index(Ctx& c, const Index& in, Index& out);
 void normalize_index(Ctx& c, Index& idx);
 void lookup_index(Ctx& c, const Index& idx, const uint32_t* d_codes, uint64_t n, uint32_t* d_begin,
@@ -207,6 +234,11 @@ void lookup_index(Ctx& c, const Index& idx, const uint32_t* d_codes, uint64_t n,
 // fstats (optional, host): {lookups with the occupancy bit set, occurrences visited}.
 uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Ref& ref, int strands, int mode,
                           unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats = nullptr);
+
+// join.cu -- the same candidates as filter_reference, from a bucket-ordered
+// join of the batch's read q-grams with the reference q-group indexes.
+uint64_t join_filter(Ctx& c, const Buckets& rb, const Reads& reads, const Ref& ref, int strands, int mode,
+                     unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats = nullptr);
 
 // validate.cu
 // mode 0: append kept hits as (hit key, k) to hit_keys/hit_vals (counter in
