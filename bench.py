@@ -81,44 +81,52 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled through NVML every 200 ms in a
+    background thread during the timed region (in-process NVML: no nvidia-smi
+    subprocess contending for the driver while kernels are timed)."""
 
-    def __init__(self, device):
-        self.device = device
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        self.p = None
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, device, period=0.2):
+        self.device, self.period = device, period
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = None
+
+    def _run(self):
+        import pynvml
+        h = pynvml.nvmlDeviceGetHandleByIndex(self._nvml_index)
+        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.reasons |= {k for k, v in self.REASONS.items() if mask & v}
+            self._stop.wait(self.period)
 
     def __enter__(self):
+        import threading
         try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
-        except FileNotFoundError:
-            self.p = None
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            self._nvml_index = int(vis.split(",")[self.device]) if vis and vis.split(",")[0].isdigit() else self.device
+            self._stop = threading.Event()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._stop = None
         return self
 
     def __exit__(self, *a):
-        if self.p:
-            self.p.terminate()
-            self.p.wait()
+        if self._stop:
+            self._stop.set()
+            self._t.join()
 
     def summary(self):
-        self.f.flush()
-        rows = []
-        for line in open(self.f.name):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 7 and parts[0].isdigit():
-                rows.append(parts)
-        os.unlink(self.f.name)
-        if not rows:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [int(r[0]) for r in rows]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() in ("active", "1")})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]), "samples": len(rows),
-                "reasons": reasons}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "reasons": sorted(self.reasons)}
 
 
 def make_inputs(qgm, cfg, rank):

@@ -181,10 +181,10 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
     // per-strand reference q-group indexes (join.cu). group_width / sampled
     // only change the layout of an index that is never materialised here.
     prepare_ref_index(c, ref, P.q);  // once per reference and q (cached)
-    Buckets rbk;
+    Partitioned rbk;
     {
       StageScope s(c, kStageIndex);
-      bucket_reads(c, reads, P.q, 32, rbk);
+      partition_reads(c, reads, P.q, rbk);
     }
     out.stats[5] = rbk.V;
     {
@@ -610,8 +610,8 @@ int qgm_filter(qgm_ctx* ctx, const qgm_index* idx, const qgm_reads* reads, const
     if (idx->i.stride != reads->r.stride || idx->i.n_reads != reads->r.n)
       throw qgm::InputError("index was built over a different read buffer");
     if (mode & QGM_FILTER_JOIN) {
-      qgm::Buckets rbk;
-      qgm::bucket_reads(c, reads->r, idx->i.q, 32, rbk);
+      qgm::Partitioned rbk;
+      qgm::partition_reads(c, reads->r, idx->i.q, rbk);
       qgm::StageScope s(c, qgm::kStageFilter);
       C.n = qgm::join_filter(c, rbk, reads->r, ref->r, strands, base_mode, C.read_bits, C.keys);
     } else {

@@ -235,9 +235,19 @@ void lookup_index(Ctx& c, const Index& idx, const uint32_t* d_codes, uint64_t n,
 uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Ref& ref, int strands, int mode,
                           unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats = nullptr);
 
-// join.cu -- the same candidates as filter_reference, from a bucket-ordered
-// join of the batch's read q-grams with the reference q-group indexes.
-uint64_t join_filter(Ctx& c, const Buckets& rb, const Reads& reads, const Ref& ref, int strands, int mode,
+// partition.cu -- the batch's read q-grams, (code << 32 | position), grouped
+// by the top min(2q,12) bits of the code.
+struct Partitioned {
+  unsigned q = 0;
+  uint32_t bins = 0, V = 0;
+  DBuf<uint32_t> boff;
+  DBuf<uint64_t> pairs;
+};
+void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out);
+
+// join.cu -- the same candidates as filter_reference, from a code-ordered
+// join of the partitioned read q-grams with the reference q-group indexes.
+uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Ref& ref, int strands, int mode,
                      unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats = nullptr);
 
 // validate.cu
