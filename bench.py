@@ -262,7 +262,7 @@ def run_gpu(args):
     prof_steps = max(1, min(3, args.steps))
     timed(step_device, prof_steps)
     ktimes = ctx.kernel_times(reset=True)
-    stimes = ctx.stage_times(reset=True)
+    stimes = ctx.stage_times(reset=True, host=True)
     ctx.profile(False)
     # e2e pass
     for _ in range(max(1, args.warmup // 2)):

@@ -127,7 +127,8 @@ const char* qgm_last_error(const qgm_ctx* ctx);
 int qgm_ctx_synchronize(qgm_ctx* ctx);
 /* Per-stage CUDA-event timing (ms, accumulated until reset). Stage ids:
  * 0 reads prep, 1 index build, 2 filtration, 3 candidate sort+unique,
- * 4 validation, 5 strata, 6 hit D2H. */
+ * 4 validation, 5 strata, 6 hit D2H; entries 8..15 (if n > 8) are the host
+ * wall-clock ms spent inside the same stages. */
 #define QGM_NUM_STAGES 8
 int qgm_ctx_profile(qgm_ctx* ctx, int enable);
 int qgm_ctx_stage_times(qgm_ctx* ctx, double* ms, int n, int reset);

@@ -264,10 +264,14 @@ class Context:
     def profile(self, enable=True):
         self._check(self.lib.qgm_ctx_profile(self.h, int(enable)))
 
-    def stage_times(self, reset=True) -> dict:
-        ms = np.zeros(len(STAGES), dtype=np.float64)
-        self._check(self.lib.qgm_ctx_stage_times(self.h, _ptr(ms), len(STAGES), int(reset)))
-        return dict(zip(STAGES, ms.tolist()))
+    def stage_times(self, reset=True, host=False) -> dict:
+        """GPU (CUDA-event) ms per stage; with host=True also the host wall ms."""
+        ms = np.zeros(2 * len(STAGES), dtype=np.float64)
+        self._check(self.lib.qgm_ctx_stage_times(self.h, _ptr(ms), ms.size, int(reset)))
+        out = dict(zip(STAGES, ms[:len(STAGES)].tolist()))
+        if host:
+            out.update({"host_" + k: v for k, v in zip(STAGES, ms[len(STAGES):].tolist())})
+        return out
 
     def kernel_times(self, reset=True) -> dict:
         """{kernel: (total_ms, launches)} for the timed hot kernels (profile mode)."""

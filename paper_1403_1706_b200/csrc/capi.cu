@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary (include/qgm_c.h): context and object
 // lifetime, host<->device staging, and the orchestration of the five stages
 // for qgm_map. No exception crosses this file's exported functions.
+#include <chrono>
 #include <cstring>
 #include <memory>
 
@@ -48,6 +49,7 @@ cudaEvent_t Ctx::take_event() {
 void Ctx::stage_begin(int s) {
   if (!profile || cur_stage >= 0) return;  // nested stages are folded into the outer one
   cur_stage = s;
+  cur_host = std::chrono::steady_clock::now();
   cur_a = take_event();
   QGM_CUDA(cudaEventRecord(cur_a, stream));
 }
@@ -57,6 +59,7 @@ void Ctx::stage_end() {
   cudaEvent_t b = take_event();
   QGM_CUDA(cudaEventRecord(b, stream));
   marks.push_back({cur_stage, cur_a, b});
+  host_ms[cur_stage] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - cur_host).count();
   cur_stage = -1;
   cur_a = nullptr;
 }
@@ -344,7 +347,11 @@ int qgm_ctx_stage_times(qgm_ctx* ctx, double* ms, int n, int reset) {
   return guard(ctx, [&] {
     ctx->c.fold_marks();
     for (int i = 0; i < n && i < qgm::kNumStages; ++i) ms[i] = ctx->c.stage_ms[i];
-    if (reset) for (double& v : ctx->c.stage_ms) v = 0;
+    for (int i = qgm::kNumStages; i < n && i < 2 * qgm::kNumStages; ++i) ms[i] = ctx->c.host_ms[i - qgm::kNumStages];
+    if (reset) {
+      for (double& v : ctx->c.stage_ms) v = 0;
+      for (double& v : ctx->c.host_ms) v = 0;
+    }
   });
 }
 

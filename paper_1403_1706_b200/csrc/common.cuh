@@ -60,6 +60,17 @@ __device__ __forceinline__ uint32_t rc_code(uint32_t g, unsigned q) {
   return x >> (32 - 2 * q);
 }
 
+// Exact division of a 32-bit numerator by a runtime divisor d >= 1 with one
+// 64-bit multiply-high: M = floor((2^64-1)/d) + 1 (d == 1 is the identity).
+// Error of t*M/2^64 vs t/d is < t/2^64 < 1/d for t < 2^32, so the floor is exact.
+struct FastDiv {
+  uint64_t M = 0;
+  uint32_t d = 1;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t div) : M(div > 1 ? ~uint64_t(0) / div + 1 : 0), d(div) {}
+  __device__ __forceinline__ uint32_t div(uint32_t t) const { return d == 1 ? t : uint32_t(__umul64hi(t, M)); }
+};
+
 // ------------------------------------------------------------------ group words
 template <class W> struct GroupTraits;
 template <> struct GroupTraits<uint32_t> {

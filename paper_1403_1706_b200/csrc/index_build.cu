@@ -41,10 +41,11 @@ struct ReadSource {
   const uint64_t* words;
   const uint32_t* lengths;
   uint32_t W, span, stride;
+  FastDiv by_span;
   unsigned q;
   __device__ __forceinline__ bool item(uint64_t t, uint32_t& g, uint32_t& pos, uint32_t& extra) const {
-    const uint32_t r = uint32_t(t / span);
-    const uint32_t o = uint32_t(t - uint64_t(r) * span);
+    const uint32_t r = by_span.div(uint32_t(t));  // slots < 2^32 (checked on the host)
+    const uint32_t o = uint32_t(t) - r * span;
     if (o + q > __ldg(lengths + r)) return false;
     g = qgram_at(words + uint64_t(r) * W, o, q);
     pos = r * stride + o;
@@ -366,7 +367,9 @@ void bucket_reads(Ctx& c, const Reads& reads, unsigned q, unsigned w, Buckets& o
   src.W = reads.W;
   src.span = reads.stride >= q ? reads.stride - q + 1 : 0;
   src.stride = reads.stride;
+  src.by_span = FastDiv(std::max<uint32_t>(src.span, 1));
   src.q = q;
+  if (uint64_t(reads.n) * src.span > 0xFFFFFFFFull) throw InputError("read batch has more than 2^32-1 q-gram slots");
   bucket_impl(c, src, uint64_t(reads.n) * src.span, out);
 }
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <type_traits>
 #include <string>
@@ -30,6 +31,8 @@ struct Ctx {
   std::vector<Mark> marks;          // recorded, not yet folded into stage_ms
   std::vector<cudaEvent_t> ev_pool; // reusable events
   double stage_ms[kNumStages] = {0};
+  double host_ms[kNumStages] = {0};  // host wall time spent inside each stage
+  std::chrono::steady_clock::time_point cur_host;
   int cur_stage = -1;
   cudaEvent_t cur_a = nullptr;
   // per-kernel timing of the hot kernels (name -> total ms, launches)

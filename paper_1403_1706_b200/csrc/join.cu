@@ -44,6 +44,7 @@ struct JoinArgs {
   const uint64_t* rwords;
   const uint32_t* rlen;
   uint32_t W, m;
+  FastDiv by_m;
   const uint64_t* cb;
   const uint64_t* cbp;
   uint32_t n_chrom;
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kJoinThreads, 5) k_join(JoinArgs a) {
         const uint32_t pp = pw & 0x7FFFFFFFu;
         const uint32_t k = s_k0[wid][lo] + (j - s_pre[wid][lo]);
         const uint32_t x = __ldg((rev ? a.Or : a.Of) + k);
-        const uint32_t r = pp / a.m, o = pp - r * a.m;
+        const uint32_t r = a.by_m.div(pp), o = pp - r * a.m;
         const uint64_t* rw = a.rwords + uint64_t(r) * a.W;
         emit = true;
         uint32_t c = 0, hi2 = a.n_chrom;  // chromosome of x
@@ -219,6 +220,7 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   a.rlen = reads.lengths.p;
   a.W = reads.W;
   a.m = reads.stride;
+  a.by_m = FastDiv(std::max<uint32_t>(reads.stride, 1));
   a.cb = ref.d_cb.p;
   a.cbp = ref.d_cbp.p;
   a.n_chrom = ref.n_chrom;

@@ -24,10 +24,11 @@ struct ItemGen {
   const uint64_t* words;
   const uint32_t* lengths;
   uint32_t W, span, stride;
+  FastDiv by_span;
   unsigned q;
   __device__ __forceinline__ bool item(uint64_t t, uint32_t& g, uint32_t& pos) const {
-    const uint32_t r = uint32_t(t / span);
-    const uint32_t o = uint32_t(t - uint64_t(r) * span);
+    const uint32_t r = by_span.div(uint32_t(t));  // slots < 2^32 (checked on the host)
+    const uint32_t o = uint32_t(t) - r * span;
     if (o + q > __ldg(lengths + r)) return false;
     g = qgram_at(words + uint64_t(r) * W, o, q);
     pos = r * stride + o;
@@ -87,7 +88,9 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   gen.span = reads.stride >= q ? reads.stride - q + 1 : 0;
   gen.stride = reads.stride;
   gen.q = q;
+  gen.by_span = FastDiv(std::max<uint32_t>(gen.span, 1));
   const uint64_t n_items = uint64_t(reads.n) * gen.span;
+  if (n_items > 0xFFFFFFFFull) throw InputError("read batch has more than 2^32-1 q-gram slots");
   const unsigned bits = std::min(2 * q, kMaxBinBits);
   const uint32_t bins = 1u << bits;
   const unsigned shift = 2 * q - bits;
