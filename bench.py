@@ -250,7 +250,7 @@ def run_gpu(args):
     for _ in range(args.warmup):
         step_device()
     barrier()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, period=args.clock_period) as clk:
         times, st, launches = timed(step_device, args.steps)
         barrier()
     clocks = clk.summary()
@@ -310,6 +310,8 @@ def run_gpu(args):
         "gpu_launches": int(launches),
         "roofline": roof,
         "clocks": clocks,
+        "step_ms": [round(t, 3) for t in times],
+        "e2e_step_ms": [round(t, 3) for t in e2e_times],
         "stages_ms_per_step": {k: round(v / prof_steps, 4) for k, v in stimes.items() if v},
         "kernels_ms_per_launch": {k: round(v, 4) for k, v in per_launch.items()},
         "counts": st,
@@ -388,6 +390,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--clock-period", type=float, default=0.2, help="NVML clock sampling period (s)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

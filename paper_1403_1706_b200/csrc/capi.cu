@@ -46,6 +46,51 @@ cudaEvent_t Ctx::take_event() {
   return e;
 }
 
+void* Ctx::block_alloc(size_t bytes, size_t& cls) {
+  cls = size_class(bytes);
+  // best fit among cached blocks no larger than 1.5x the request's class
+  size_t best = free_blocks.size();
+  for (size_t i = 0; i < free_blocks.size(); ++i) {
+    const size_t c = free_blocks[i].first;
+    if (c >= cls && c <= cls + cls / 2 && (best == free_blocks.size() || c < free_blocks[best].first)) best = i;
+  }
+  if (best < free_blocks.size()) {
+    void* p = free_blocks[best].second;
+    cls = free_blocks[best].first;
+    free_blocks[best] = free_blocks.back();
+    free_blocks.pop_back();
+    cached_bytes -= cls;
+    live_bytes += cls;
+    return p;
+  }
+  if (cached_bytes > (size_t(16) << 30)) block_trim();  // bound the cache when sizes drift
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, cls, stream);
+  if (e == cudaErrorMemoryAllocation && !free_blocks.empty()) {
+    cudaGetLastError();
+    block_trim();  // give cached blocks of other sizes back, then retry once
+    e = cudaMallocAsync(&p, cls, stream);
+  }
+  if (e != cudaSuccess)
+    throw CudaError(std::string("device allocation of ") + std::to_string(cls) + " bytes failed: " +
+                    cudaGetErrorString(e));
+  live_bytes += cls;
+  return p;
+}
+
+void Ctx::block_free(void* p, size_t cls) {
+  free_blocks.push_back({cls, p});
+  live_bytes -= cls;
+  cached_bytes += cls;
+}
+
+void Ctx::block_trim() {
+  for (auto& b : free_blocks) cudaFreeAsync(b.second, stream);
+  free_blocks.clear();
+  cached_bytes = 0;
+  cudaStreamSynchronize(stream);
+}
+
 void Ctx::stage_begin(int s) {
   if (!profile || cur_stage >= 0) return;  // nested stages are folded into the outer one
   cur_stage = s;
@@ -323,6 +368,7 @@ void qgm_ctx_destroy(qgm_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
+  ctx->c.block_trim();
   for (auto& m : ctx->c.marks) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
   for (auto e : ctx->c.ev_pool) cudaEventDestroy(e);
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);

@@ -40,11 +40,30 @@ struct Ctx {
   std::vector<KMark> kmarks;
   std::vector<std::pair<std::string, std::pair<double, uint64_t>>> kernel_ms;
 
+  // Block cache: every device buffer of this context comes from here. Blocks
+  // are rounded up to size classes (<= 25% slack) and return to a free list
+  // on release; all work of a context runs on its one stream, so a released
+  // block can be handed out again without synchronisation (stream order).
+  // Steady-state batches therefore never call the driver allocator.
+  std::vector<std::pair<size_t, void*>> free_blocks;
+  size_t cached_bytes = 0, live_bytes = 0;
+
   cudaEvent_t take_event();
   void stage_begin(int s);
   void stage_end();
   void fold_marks();  // synchronises the recorded events
+  void* block_alloc(size_t bytes, size_t& cls);
+  void block_free(void* p, size_t cls);
+  void block_trim();  // frees every cached block (synchronises the stream)
 };
+
+// Size class of an allocation: 1/4-octave granularity above 4 KiB.
+inline size_t size_class(size_t bytes) {
+  if (bytes <= 4096) return 4096;
+  size_t top = size_t(1) << (63 - __builtin_clzll(bytes - 1));  // largest power of two < bytes
+  const size_t step = top / 4;
+  return (bytes + step - 1) / step * step;
+}
 
 struct StageScope {
   Ctx& c;
@@ -80,12 +99,12 @@ struct KernelScope {
   } while (0)
 
 // --------------------------------------------------------------- memory
-// Stream-ordered device buffer from the device's default memory pool
-// (cudaMallocAsync; the pool keeps freed blocks cached across batches).
+// Device buffer from the context's block cache (Ctx::block_alloc).
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  size_t cls = 0;
   Ctx* ctx = nullptr;
   DBuf() = default;
   DBuf(Ctx& c, size_t count) { alloc(c, count); }
@@ -95,8 +114,8 @@ struct DBuf {
   DBuf& operator=(DBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p; n = o.n; ctx = o.ctx;
-      o.p = nullptr; o.n = 0;
+      p = o.p; n = o.n; cls = o.cls; ctx = o.ctx;
+      o.p = nullptr; o.n = 0; o.cls = 0;
     }
     return *this;
   }
@@ -105,18 +124,21 @@ struct DBuf {
     release();
     ctx = &c;
     n = count;
-    if (count) QGM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), c.stream));
+    if (count) p = static_cast<T*>(c.block_alloc(count * sizeof(T), cls));
   }
   void release() {
-    if (p) cudaFreeAsync(p, ctx->stream);
+    if (p) ctx->block_free(p, cls);
     p = nullptr;
     n = 0;
+    cls = 0;
   }
   size_t bytes() const { return n * sizeof(T); }
   void zero() {
     if (n) QGM_CUDA(cudaMemsetAsync(p, 0, bytes(), ctx->stream));
   }
-  void swap(DBuf& o) { std::swap(p, o.p); std::swap(n, o.n); std::swap(ctx, o.ctx); }
+  void swap(DBuf& o) {
+    std::swap(p, o.p); std::swap(n, o.n); std::swap(cls, o.cls); std::swap(ctx, o.ctx);
+  }
 };
 
 // --------------------------------------------------------------- objects
