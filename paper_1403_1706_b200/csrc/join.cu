@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kJoinThreads = 256;
 constexpr int kJoinWarps = kJoinThreads / 32;
-constexpr int kItems = 2;                    // read q-grams per lane per step
+constexpr int kItems = 4;                    // read q-grams per lane per step
 constexpr int kRanges = 32 * kItems * 2;     // both strands
 constexpr int kStage = 256;                  // staged keys per warp
 
@@ -150,31 +150,25 @@ __global__ void __launch_bounds__(kJoinThreads, 5) k_join(JoinArgs a) {
         const bool rev = pw >> 31;
         const uint32_t pp = pw & 0x7FFFFFFFu;
         const uint32_t k = s_k0[wid][lo] + (j - s_pre[wid][lo]);
-        const uint32_t x = __ldg((rev ? a.Or : a.Of) + k);
         const uint32_t r = a.by_m.div(pp), o = pp - r * a.m;
-        const uint64_t* rw = a.rwords + uint64_t(r) * a.W;
+        // four independent loads in flight: occurrence, its stored predecessor
+        // base, the read length and the read word holding the compared base
+        const uint32_t cmp = rev ? o + q : (o ? o - 1 : 0);  // read offset the run-start rule compares
+        const uint32_t x = __ldg((rev ? a.Or : a.Of) + k);
+        const uint32_t pv = kRunStart ? uint32_t(__ldg((rev ? a.Xr : a.Xf) + k)) : 4u;
+        const uint32_t n = __ldg(a.rlen + r);
+        const uint64_t rword = kRunStart ? __ldg(a.rwords + uint64_t(r) * a.W + (cmp >> 5)) : 0ull;
         emit = true;
+        if (kRunStart && pv != 4 && (rev ? (o + q + 1 <= n) : (o >= 1)) &&
+            pv == (uint32_t(rword >> (62 - 2 * (cmp & 31))) & 3u))
+          emit = false;
         uint32_t c = 0, hi2 = a.n_chrom;  // chromosome of x
         while (hi2 - c > 1) {
           const uint32_t mid = (c + hi2) >> 1;
           if (__ldg(a.cb + mid) <= x) c = mid; else hi2 = mid;
         }
         const int64_t p = int64_t(x) - int64_t(__ldg(a.cb + c));
-        int64_t d;
-        if (!rev) {
-          d = p - int64_t(o);
-          if (kRunStart && o >= 1) {
-            const uint32_t pv = __ldg(a.Xf + k);
-            if (pv != 4 && pv == base_at(rw, o - 1)) emit = false;
-          }
-        } else {
-          const uint32_t n = __ldg(a.rlen + r);
-          d = p + int64_t(o) + int64_t(q) - int64_t(n);
-          if (kRunStart && o + q + 1 <= n) {
-            const uint32_t pv = __ldg(a.Xr + k);
-            if (pv != 4 && pv == base_at(rw, o + q)) emit = false;
-          }
-        }
+        const int64_t d = rev ? p + int64_t(o) + int64_t(q) - int64_t(n) : p - int64_t(o);
         const uint64_t gp = uint64_t(int64_t(__ldg(a.cbp + c)) + d);
         key = (uint64_t(r) << (a.diag_bits + 1)) | (uint64_t(rev) << a.diag_bits) | gp;
       }

@@ -1,16 +1,21 @@
 // partition.cu -- per-batch read q-gram partition for the join (map path).
 //
 // The join (join.cu) only needs the batch's read q-grams grouped by the top
-// bits of their code, so that consecutive items touch the same few KiB of the
-// reference index; it never needs the full read-side index. Two passes over
-// the (L2-resident) 2-bit reads, no per-item rank array:
-//   P0 histogram : per-CTA shared-memory histogram over 2^cbits code bins
-//                  (cbits = min(2q, 12)), one global atomic per non-empty bin;
+// bits of their code, so that the warps in flight touch a few MiB of the
+// reference index (L2-resident) instead of all of it; it never needs the full
+// read-side q-group index. Two passes over the (L2-resident) 2-bit reads, no
+// per-item rank array:
+//   P0 histogram : per-CTA shared-memory histogram over 2^bits code bins
+//                  (bits = min(2q, 8)), one global atomic per non-empty bin;
 //   scan         : bin offsets;
-//   P1 scatter   : the CTA re-derives its items, reserves one contiguous run
-//                  per bin with one global atomic, and writes its items into
-//                  the run through shared-memory cursors, so each bin receives
-//                  a contiguous block of ~35 items (coalesced) per CTA.
+//   P1 scatter   : per chunk of 4096 q-gram slots, a local counting sort by
+//                  bin in shared memory, one global atomic per bin to reserve
+//                  the chunk's run, then runs copied out with consecutive
+//                  threads writing consecutive 8-byte slots (full sectors;
+//                  ~16 items = one 128 B line per bin per chunk at q=16).
+// ncu on the previous single-pass scatter (12-bit bins, items written
+// straight from registers) showed 1.6 GB of read-for-ownership and 2.1 GB of
+// writes for 0.68 GB of output: partial sectors of 2.4M concurrently open runs.
 // Item = (full code << 32) | text position (r*stride + o), 8 bytes.
 #include "internal.hpp"
 
@@ -18,7 +23,10 @@ namespace qgm {
 namespace {
 
 constexpr int kPartThreads = 512;
-constexpr unsigned kMaxBinBits = 12;
+constexpr unsigned kBinBits = 8;
+constexpr uint32_t kBins = 1u << kBinBits;
+constexpr uint32_t kChunk = 4096;  // q-gram slots per chunk; staging = 32 KiB
+constexpr uint32_t kPer = kChunk / kPartThreads;
 
 struct ItemGen {
   const uint64_t* words;
@@ -26,9 +34,9 @@ struct ItemGen {
   uint32_t W, span, stride;
   FastDiv by_span;
   unsigned q;
-  __device__ __forceinline__ bool item(uint64_t t, uint32_t& g, uint32_t& pos) const {
-    const uint32_t r = by_span.div(uint32_t(t));  // slots < 2^32 (checked on the host)
-    const uint32_t o = uint32_t(t) - r * span;
+  __device__ __forceinline__ bool item(uint32_t t, uint32_t& g, uint32_t& pos) const {
+    const uint32_t r = by_span.div(t);
+    const uint32_t o = t - r * span;
     if (o + q > __ldg(lengths + r)) return false;
     g = qgram_at(words + uint64_t(r) * W, o, q);
     pos = r * stride + o;
@@ -36,44 +44,65 @@ struct ItemGen {
   }
 };
 
-__global__ void __launch_bounds__(kPartThreads) k_part_hist(ItemGen gen, uint64_t n_items, uint64_t chunk,
-                                                            unsigned shift, uint32_t bins, uint32_t* __restrict__ hist) {
-  extern __shared__ uint32_t h[];
-  for (uint32_t b = threadIdx.x; b < bins; b += kPartThreads) h[b] = 0;
+__global__ void __launch_bounds__(kPartThreads) k_part_hist(ItemGen gen, uint32_t n_items, uint32_t chunk,
+                                                            unsigned shift, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[kBins];
+  for (uint32_t b = threadIdx.x; b < kBins; b += kPartThreads) h[b] = 0;
   __syncthreads();
-  const uint64_t c0 = blockIdx.x * chunk, c1 = min(n_items, c0 + chunk);
-  for (uint64_t t = c0 + threadIdx.x; t < c1; t += kPartThreads) {
+  const uint32_t c0 = blockIdx.x * chunk, c1 = min(n_items, c0 + chunk);
+  for (uint32_t t = c0 + threadIdx.x; t < c1; t += kPartThreads) {
     uint32_t g, pos;
     if (gen.item(t, g, pos)) atomicAdd(h + (g >> shift), 1u);
   }
   __syncthreads();
-  for (uint32_t b = threadIdx.x; b < bins; b += kPartThreads)
+  for (uint32_t b = threadIdx.x; b < kBins; b += kPartThreads)
     if (h[b]) atomicAdd(hist + b, h[b]);
 }
 
-__global__ void __launch_bounds__(kPartThreads) k_part_scatter(ItemGen gen, uint64_t n_items, uint64_t chunk,
-                                                               unsigned shift, uint32_t bins,
-                                                               const uint32_t* __restrict__ boff,
-                                                               uint32_t* __restrict__ cursor,
-                                                               uint64_t* __restrict__ out) {
-  extern __shared__ uint32_t h[];  // [bins] counts -> run bases, [bins] local cursors
-  uint32_t* cur = h + bins;
-  for (uint32_t b = threadIdx.x; b < bins; b += kPartThreads) { h[b] = 0; cur[b] = 0; }
-  __syncthreads();
-  const uint64_t c0 = blockIdx.x * chunk, c1 = min(n_items, c0 + chunk);
-  for (uint64_t t = c0 + threadIdx.x; t < c1; t += kPartThreads) {
-    uint32_t g, pos;
-    if (gen.item(t, g, pos)) atomicAdd(h + (g >> shift), 1u);
-  }
-  __syncthreads();
-  for (uint32_t b = threadIdx.x; b < bins; b += kPartThreads)
-    if (h[b]) h[b] = boff[b] + atomicAdd(cursor + b, h[b]);
-  __syncthreads();
-  for (uint64_t t = c0 + threadIdx.x; t < c1; t += kPartThreads) {
-    uint32_t g, pos;
-    if (!gen.item(t, g, pos)) continue;
-    const uint32_t b = g >> shift;
-    out[h[b] + atomicAdd(cur + b, 1u)] = (uint64_t(g) << 32) | pos;
+__global__ void __launch_bounds__(kPartThreads, 4) k_part_scatter(ItemGen gen, uint32_t n_items, unsigned shift,
+                                                                  const uint32_t* __restrict__ boff,
+                                                                  uint32_t* __restrict__ cursor,
+                                                                  uint64_t* __restrict__ out) {
+  extern __shared__ uint64_t stage[];  // kChunk items, bin-sorted
+  __shared__ uint32_t cnt[kBins], lofs[kBins], gdst[kBins];
+  __shared__ uint32_t ws[33];
+  const uint32_t n_chunks = (n_items + kChunk - 1) / kChunk;
+  for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+    const uint32_t c0 = ch * kChunk;
+    for (uint32_t b = threadIdx.x; b < kBins; b += kPartThreads) cnt[b] = 0;
+    __syncthreads();
+    uint32_t g[kPer], pos[kPer];
+    bool ok[kPer];
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k) {
+      const uint32_t t = c0 + k * kPartThreads + threadIdx.x;
+      ok[k] = t < n_items && gen.item(t, g[k], pos[k]);
+      if (ok[k]) atomicAdd(cnt + (g[k] >> shift), 1u);
+    }
+    __syncthreads();
+    {  // local exclusive offsets; reserve the chunk's run in every bin
+      const uint32_t b = threadIdx.x;
+      const uint32_t v = b < kBins ? cnt[b] : 0u;
+      uint32_t tot;
+      const uint32_t ex = block_exclusive_scan<uint32_t>(v, ws, &tot);
+      if (b < kBins) {
+        lofs[b] = ex;
+        gdst[b] = v ? boff[b] + atomicAdd(cursor + b, v) : 0u;
+        cnt[b] = ex;  // becomes the local placement cursor
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k)
+      if (ok[k]) stage[atomicAdd(cnt + (g[k] >> shift), 1u)] = (uint64_t(g[k]) << 32) | pos[k];
+    __syncthreads();
+    const uint32_t total = cnt[kBins - 1];  // == number of valid items in the chunk
+    for (uint32_t i = threadIdx.x; i < total; i += kPartThreads) {
+      const uint64_t it = stage[i];
+      const uint32_t b = uint32_t(it >> 32) >> shift;
+      out[gdst[b] + (i - lofs[b])] = it;
+    }
+    __syncthreads();
   }
 }
 
@@ -87,44 +116,47 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   gen.W = reads.W;
   gen.span = reads.stride >= q ? reads.stride - q + 1 : 0;
   gen.stride = reads.stride;
-  gen.q = q;
   gen.by_span = FastDiv(std::max<uint32_t>(gen.span, 1));
-  const uint64_t n_items = uint64_t(reads.n) * gen.span;
-  if (n_items > 0xFFFFFFFFull) throw InputError("read batch has more than 2^32-1 q-gram slots");
-  const unsigned bits = std::min(2 * q, kMaxBinBits);
-  const uint32_t bins = 1u << bits;
+  gen.q = q;
+  const uint64_t n_items64 = uint64_t(reads.n) * gen.span;
+  if (n_items64 > 0xFFFFFFFFull - kChunk) throw InputError("read batch has more than 2^32-1 q-gram slots");
+  const uint32_t n_items = uint32_t(n_items64);
+  const unsigned bits = std::min(2 * q, kBinBits);
   const unsigned shift = 2 * q - bits;
   out.q = q;
-  out.bins = bins;
-  out.boff.alloc(c, bins + 1);
+  out.bins = 1u << bits;
+  out.boff.alloc(c, kBins + 1);
   if (n_items == 0) {
     out.boff.zero();
     out.V = 0;
     out.pairs.alloc(c, 1);
     return;
   }
-  // ~36 items per bin per CTA keeps the per-bin runs coalesced
-  const uint64_t chunk = std::max<uint64_t>(uint64_t(bins) * 36, ceil_div(n_items, uint64_t(kSMs) * 16));
-  const unsigned grid = unsigned(ceil_div(n_items, chunk));
-  DBuf<uint32_t> hist(c, bins + 1);
+  const uint32_t chunk = uint32_t(std::max<uint64_t>(kChunk, ceil_div(n_items, uint64_t(kSMs) * 8)));
+  DBuf<uint32_t> hist(c, kBins + 1);
   hist.zero();
   {
     KernelScope ks(c, "k_part_hist");
-    QGM_KERNEL(c, k_part_hist, grid, kPartThreads, bins * 4, gen, n_items, chunk, shift, bins, hist.p);
+    QGM_KERNEL(c, k_part_hist, unsigned(ceil_div(n_items, chunk)), kPartThreads, 0, gen, n_items, chunk, shift,
+               hist.p);
   }
   DBuf<uint32_t> total(c, 1);
-  exclusive_scan_u32(c, hist.p, out.boff.p, bins + 1, total.p, nullptr);
+  exclusive_scan_u32(c, hist.p, out.boff.p, kBins + 1, total.p, nullptr);
   uint32_t V = 0;
   QGM_CUDA(cudaMemcpyAsync(&V, total.p, 4, cudaMemcpyDeviceToHost, c.stream));
   QGM_CUDA(cudaStreamSynchronize(c.stream));
   out.V = V;
   out.pairs.alloc(c, std::max<uint64_t>(V, 1));
   hist.zero();  // reused as the per-bin global cursors
-  {
-    KernelScope ks(c, "k_part_scatter");
-    QGM_KERNEL(c, k_part_scatter, grid, kPartThreads, bins * 8, gen, n_items, chunk, shift, bins, out.boff.p, hist.p,
-               out.pairs.p);
+  const size_t smem = kChunk * sizeof(uint64_t);
+  static bool attr = false;
+  if (!attr) {
+    QGM_CUDA(cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
   }
+  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n_items, kChunk), uint64_t(kSMs) * 4));
+  KernelScope ks(c, "k_part_scatter");
+  QGM_KERNEL(c, k_part_scatter, grid, kPartThreads, smem, gen, n_items, shift, out.boff.p, hist.p, out.pairs.p);
 }
 
 }  // namespace qgm
