@@ -106,6 +106,99 @@ __global__ void __launch_bounds__(kPartThreads, 4) k_part_scatter(ItemGen gen, u
   }
 }
 
+// ---------------------------------------------------------------- refinement
+// Second MSD pass: items already grouped by their top 8 code bits are
+// regrouped by their top `key_bits` (<= 16) bits. A chunk of 4096 consecutive
+// items spans few top-8 bins, so its keys fall in a small window
+// [first_bin << sub, (last_bin + 1) << sub); the window is counted and
+// staged in shared memory exactly like P1 (kLocal keys max), with a
+// per-item global fallback for chunks whose window is wider (tiny bins).
+constexpr uint32_t kLocal = 2048;
+
+__device__ __forceinline__ uint32_t key_of(uint64_t it, unsigned kshift) { return uint32_t(it >> 32) >> kshift; }
+
+__global__ void __launch_bounds__(kPartThreads) k_refine_hist(const uint64_t* __restrict__ in, uint32_t n,
+                                                              unsigned kshift, unsigned sub,
+                                                              uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[kLocal];
+  const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
+  for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+    const uint32_t c0 = ch * kChunk, c1 = min(n, c0 + kChunk);
+    const uint32_t base = (key_of(in[c0], kshift) >> sub) << sub;
+    const uint32_t width = (((key_of(in[c1 - 1], kshift) >> sub) + 1) << sub) - base;
+    if (width > kLocal) {  // rare: many tiny bins in one chunk
+      for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) atomicAdd(hist + key_of(in[i], kshift), 1u);
+      continue;
+    }
+    for (uint32_t b = threadIdx.x; b < width; b += kPartThreads) h[b] = 0;
+    __syncthreads();
+    for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) atomicAdd(h + key_of(in[i], kshift) - base, 1u);
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < width; b += kPartThreads)
+      if (h[b]) atomicAdd(hist + base + b, h[b]);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kPartThreads, 4) k_refine_scatter(const uint64_t* __restrict__ in, uint32_t n,
+                                                                    unsigned kshift, unsigned sub,
+                                                                    const uint32_t* __restrict__ off,
+                                                                    uint32_t* __restrict__ cursor,
+                                                                    uint64_t* __restrict__ out) {
+  extern __shared__ uint64_t stage[];
+  __shared__ uint32_t cnt[kLocal], lofs[kLocal], gdst[kLocal];
+  __shared__ uint32_t ws[33];
+  const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
+  for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+    const uint32_t c0 = ch * kChunk, c1 = min(n, c0 + kChunk);
+    const uint32_t base = (key_of(in[c0], kshift) >> sub) << sub;
+    const uint32_t width = (((key_of(in[c1 - 1], kshift) >> sub) + 1) << sub) - base;
+    if (width > kLocal) {
+      for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) {
+        const uint64_t it = in[i];
+        const uint32_t k = key_of(it, kshift);
+        out[off[k] + atomicAdd(cursor + k, 1u)] = it;
+      }
+      continue;
+    }
+    for (uint32_t b = threadIdx.x; b < width; b += kPartThreads) cnt[b] = 0;
+    __syncthreads();
+    uint64_t v[kPer];
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k) {
+      const uint32_t i = c0 + k * kPartThreads + threadIdx.x;
+      v[k] = i < c1 ? in[i] : ~0ull;
+      if (i < c1) atomicAdd(cnt + key_of(v[k], kshift) - base, 1u);
+    }
+    __syncthreads();
+    // exclusive scan of cnt[0, width): each thread owns a contiguous run
+    const uint32_t per = (width + kPartThreads - 1) / kPartThreads;
+    const uint32_t b0 = threadIdx.x * per, b1 = min(width, b0 + per);
+    uint32_t s = 0;
+    for (uint32_t b = b0; b < b1; ++b) s += cnt[b];
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan<uint32_t>(s, ws, &tot);
+    for (uint32_t b = b0; b < b1; ++b) {
+      const uint32_t cv = cnt[b];
+      lofs[b] = run;
+      gdst[b] = cv ? off[base + b] + atomicAdd(cursor + base + b, cv) : 0u;
+      cnt[b] = run;
+      run += cv;
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k)
+      if (v[k] != ~0ull) stage[atomicAdd(cnt + key_of(v[k], kshift) - base, 1u)] = v[k];
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < c1 - c0; i += kPartThreads) {
+      const uint64_t it = stage[i];
+      const uint32_t b = key_of(it, kshift) - base;
+      out[gdst[b] + (i - lofs[b])] = it;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
@@ -155,8 +248,37 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
     attr = true;
   }
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n_items, kChunk), uint64_t(kSMs) * 4));
-  KernelScope ks(c, "k_part_scatter");
-  QGM_KERNEL(c, k_part_scatter, grid, kPartThreads, smem, gen, n_items, shift, out.boff.p, hist.p, out.pairs.p);
+  {
+    KernelScope ks(c, "k_part_scatter");
+    QGM_KERNEL(c, k_part_scatter, grid, kPartThreads, smem, gen, n_items, shift, out.boff.p, hist.p, out.pairs.p);
+  }
+  // P2: refine to the top min(2q, 16) code bits (short reuse distance of the
+  // reference-index sectors in the join)
+  const unsigned key_bits = std::min(2 * q, 16u);
+  if (key_bits <= bits || V == 0) return;
+  const unsigned kshift = 2 * q - key_bits, sub = key_bits - bits;
+  const uint32_t keys = 1u << key_bits;
+  DBuf<uint32_t> h2(c, keys + 1), off(c, keys + 1);
+  h2.zero();
+  const unsigned grid2 = unsigned(std::min<uint64_t>(ceil_div(V, kChunk), uint64_t(kSMs) * 4));
+  {
+    KernelScope ks(c, "k_refine_hist");
+    QGM_KERNEL(c, k_refine_hist, grid2, kPartThreads, 0, out.pairs.p, V, kshift, sub, h2.p);
+  }
+  exclusive_scan_u32(c, h2.p, off.p, keys + 1, nullptr, nullptr);
+  h2.zero();  // per-key cursors
+  DBuf<uint64_t> refined(c, std::max<uint64_t>(V, 1));
+  static bool attr2 = false;
+  if (!attr2) {
+    QGM_CUDA(cudaFuncSetAttribute(k_refine_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr2 = true;
+  }
+  {
+    KernelScope ks(c, "k_refine_scatter");
+    QGM_KERNEL(c, k_refine_scatter, grid2, kPartThreads, smem, out.pairs.p, V, kshift, sub, off.p, h2.p,
+               refined.p);
+  }
+  out.pairs.swap(refined);
 }
 
 }  // namespace qgm
