@@ -287,6 +287,16 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
 uint64_t stratify_hits(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const uint32_t* hit_vals, uint64_t n,
                        uint32_t n_reads, unsigned read_bits, int mode, DBuf<uint8_t>& out);
 
+// Persistent-grid size: SMs x resident CTAs per SM for this kernel/config
+// (one full wave; grid-stride kernels then never run a partial second wave).
+inline unsigned resident_grid(const void* kernel, int threads, size_t smem) {
+  int dev = 0, sms = kSMs, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+  return unsigned(std::max(1, sms * std::max(1, per)));
+}
+
 inline unsigned bit_width_u64(uint64_t x) {
   unsigned b = 0;
   while (x) { ++b; x >>= 1; }

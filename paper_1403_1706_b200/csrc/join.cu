@@ -56,18 +56,6 @@ struct JoinArgs {
   unsigned long long* stats;
 };
 
-__device__ __forceinline__ bool ref_pair(const uint32_t* __restrict__ I, const uint32_t* __restrict__ S,
-                                         const uint32_t* __restrict__ S1, uint32_t g, uint32_t& k0, uint32_t& k1) {
-  const uint32_t wi = g >> 5, bit = g & 31;
-  const uint32_t w = __ldg(I + wi);
-  const uint32_t s = __ldg(S + wi);
-  if (!((w >> bit) & 1u)) return false;
-  const uint32_t b = s + __popc(w & ((1u << bit) - 1u));
-  k0 = __ldg(S1 + b);
-  k1 = __ldg(S1 + b + 1);
-  return true;
-}
-
 template <bool kRunStart>
 __global__ void __launch_bounds__(kJoinThreads, 5) k_join(JoinArgs a) {
   __shared__ uint32_t s_k0[kJoinWarps][kRanges];
@@ -103,22 +91,33 @@ __global__ void __launch_bounds__(kJoinThreads, 5) k_join(JoinArgs a) {
       const uint64_t it = i0 + u * 32 + lane;
       pr[u] = it < a.n_items ? __ldg(a.items + it) : ~0ull;
     }
+    // all occupancy / group-start words first (16 independent loads per
+    // lane), then all S' pairs: no load waits behind another lookup
+    uint32_t wI[kSlots], wS[kSlots];
 #pragma unroll
     for (int u = 0; u < kItems; ++u) {
-      const uint32_t g = uint32_t(pr[u] >> 32), pos = uint32_t(pr[u]);
-      const bool ok = pr[u] != ~0ull;
-      uint32_t k0 = 0, k1 = 0;
-      rn[2 * u] = rn[2 * u + 1] = 0;
-      rk0[2 * u] = rk0[2 * u + 1] = 0;
-      rpos[2 * u] = pos;
-      rpos[2 * u + 1] = pos | 0x80000000u;
-      if (ok && (a.strands & 1) && ref_pair(a.If, a.Sf, a.S1f, g, k0, k1)) { rk0[2 * u] = k0; rn[2 * u] = k1 - k0; }
-      if (ok && (a.strands & 2) && ref_pair(a.Ir, a.Sr, a.S1r, g, k0, k1)) {
-        rk0[2 * u + 1] = k0;
-        rn[2 * u + 1] = k1 - k0;
-      }
-      cnt += rn[2 * u] + rn[2 * u + 1];
-      nr += (rn[2 * u] != 0) + (rn[2 * u + 1] != 0);
+      const uint32_t wi = pr[u] == ~0ull ? 0u : uint32_t(pr[u] >> 37);
+      wI[2 * u] = (a.strands & 1) ? __ldg(a.If + wi) : 0u;
+      wS[2 * u] = (a.strands & 1) ? __ldg(a.Sf + wi) : 0u;
+      wI[2 * u + 1] = (a.strands & 2) ? __ldg(a.Ir + wi) : 0u;
+      wS[2 * u + 1] = (a.strands & 2) ? __ldg(a.Sr + wi) : 0u;
+    }
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) {
+      const int u = s >> 1;
+      const uint32_t bit = uint32_t(pr[u] >> 32) & 31u;
+      const bool hit = pr[u] != ~0ull && ((wI[s] >> bit) & 1u);
+      const uint32_t b = wS[s] + __popc(wI[s] & ((1u << bit) - 1u));
+      const uint32_t* S1 = (s & 1) ? a.S1r : a.S1f;
+      rk0[s] = hit ? __ldg(S1 + b) : 0u;
+      rn[s] = hit ? __ldg(S1 + b + 1) : 0u;
+      rpos[s] = uint32_t(pr[u]) | ((s & 1) ? 0x80000000u : 0u);
+    }
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) {
+      rn[s] -= rk0[s];
+      cnt += rn[s];
+      nr += rn[s] != 0;
     }
     n_hit += nr;
     n_occ += cnt;
@@ -224,8 +223,10 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   a.counter = counter.p;
   a.stats = counter.p + 1;
   if (keys.n == 0) keys.alloc(c, std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16));
-  const unsigned grid = unsigned(
-      std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(rp.V, kJoinThreads * kItems), uint64_t(kSMs) * 8)));
+  const unsigned grid = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>(ceil_div(rp.V, kJoinThreads * kItems),
+                            resident_grid(mode == 1 ? (const void*)k_join<true> : (const void*)k_join<false>,
+                                          kJoinThreads, 0))));
   for (int attempt = 0; attempt < 2; ++attempt) {
     counter.zero();
     a.out = keys.p;
