@@ -265,7 +265,9 @@ uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Re
 struct Partitioned {
   unsigned q = 0;
   uint32_t bins = 0, V = 0;
-  DBuf<uint32_t> boff;
+  unsigned sub_bits = 0;  // sub-bin = code >> (2q - sub_bits); sub_bits = min(2q, 16)
+  DBuf<uint32_t> boff;    // 8-bit bin offsets (first pass)
+  DBuf<uint32_t> soff;    // sub-bin offsets, 2^sub_bits + 1 entries
   DBuf<uint64_t> pairs;
 };
 void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out);

@@ -8,17 +8,22 @@
 // Why a join: streaming the 2L reference q-grams against a 4^q-code read
 // index makes every lookup a random probe into a 512 MiB occupancy array
 // (q=16); ncu shows each probe costing ~100 B of HBM traffic
-// (profiles/r01_c2_stream_filter.md). Here the reference side is a q-group
-// index built once per reference and q (prepare_ref_index -- the paper's
-// reference index with P ordered by q-gram), one per strand,
-// and the batch's read q-grams are partitioned by the top 12 bits of their
-// code (partition.cu). Walking the partitioned q-grams in order, consecutive
-// lookups of a warp land in the same few KiB of I/S/S'/O of the reference
-// index, so every HBM stream is read about once and sequentially.
+// (profiles/r01/README.md). Here the reference side is a q-group index built
+// once per reference and q (prepare_ref_index -- the paper's reference index
+// with P ordered by q-gram), one per strand, and the batch's read
+// q-grams are partitioned by the top 16 bits of their code (partition.cu).
 //
-// Per warp step: 64 read q-grams (2 per lane, for memory-level parallelism),
-// both strands looked up (I and S words, then the two S' entries), then the
-// union of the occurrence intervals expanded cooperatively, one
+// One CTA owns one code sub-bin at a time (2^(2q-16) codes; 2048 group words
+// per array at q=16): it stages the sub-bin's occupancy and group-start words
+// of both reference strands in shared memory with one coalesced load, so all
+// Group-And-Bit / Grouprank lookups of the sub-bin's read q-grams are shared
+// memory hits; the S' / O / prev reads that follow fall in the sub-bin's
+// contiguous slice of the reference index and are L1/L2 local to the CTA. The
+// occupancy/group-start arrays are read from HBM exactly once per batch, in
+// order.
+//
+// Per warp step: up to 4 read q-grams per lane, both strands looked up, then
+// the union of the occurrence intervals expanded cooperatively, one
 // (reference occurrence, read occurrence) pair per lane. The run-start rule
 // uses the base stored next to every reference occurrence (prev_fwd/prev_rc,
 // 4 = no predecessor) against the read base at o-1 (forward) or o+q (RC).
@@ -29,13 +34,18 @@ namespace {
 
 constexpr int kJoinThreads = 256;
 constexpr int kJoinWarps = kJoinThreads / 32;
-constexpr int kItems = 4;                    // read q-grams per lane per step
-constexpr int kRanges = 32 * kItems * 2;     // both strands
-constexpr int kStage = 256;                  // staged keys per warp
+constexpr int kItems = 4;                 // read q-grams per lane per step
+constexpr int kSlots = 2 * kItems;        // (item, strand) lookups per lane
+constexpr int kRanges = 32 * kSlots;
+constexpr int kStage = 128;               // staged keys per warp
+constexpr uint32_t kMaxWords = 2048;      // group words per sub-bin and array (q = 16)
 
 struct JoinArgs {
   const uint64_t* items;
-  uint64_t n_items;
+  const uint32_t* soff;
+  uint32_t n_sub;
+  unsigned code_shift;  // sub-bin = code >> code_shift
+  uint32_t words;       // group words per sub-bin (>= 1)
   unsigned q;
   const uint32_t *If, *Sf, *S1f, *Of;
   const uint8_t* Xf;
@@ -57,15 +67,16 @@ struct JoinArgs {
 };
 
 template <bool kRunStart>
-__global__ void __launch_bounds__(kJoinThreads, 5) k_join(JoinArgs a) {
+__global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
+  extern __shared__ uint32_t s_words[];  // [I fwd | I rc | S fwd | S rc], a.words each
+  uint32_t* sI[2] = {s_words, s_words + a.words};
+  uint32_t* sS[2] = {s_words + 2 * a.words, s_words + 3 * a.words};
   __shared__ uint32_t s_k0[kJoinWarps][kRanges];
   __shared__ uint32_t s_pre[kJoinWarps][kRanges + 1];
   __shared__ uint32_t s_pos[kJoinWarps][kRanges];  // read text position | strand << 31
   __shared__ uint64_t s_out[kJoinWarps][kStage];
 
   const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
-  const uint64_t gwarp = (uint64_t(blockIdx.x) * kJoinThreads + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * kJoinThreads) >> 5;
   const unsigned q = a.q;
   uint32_t staged = 0;
   unsigned long long n_hit = 0, n_occ = 0;
@@ -80,103 +91,102 @@ __global__ void __launch_bounds__(kJoinThreads, 5) k_join(JoinArgs a) {
     __syncwarp();
   };
 
-  for (uint64_t i0 = gwarp * (32 * kItems); i0 < a.n_items; i0 += nwarps * (32 * kItems)) {
-    // fixed slots (item u, strand s) -> lane*4 + 2u + s; empty slots have
-    // length 0 and are never selected by the expansion's search below
-    constexpr int kSlots = 2 * kItems;
-    uint32_t cnt = 0, nr = 0, rk0[kSlots], rn[kSlots], rpos[kSlots];
-    uint64_t pr[kItems];
-#pragma unroll
-    for (int u = 0; u < kItems; ++u) {
-      const uint64_t it = i0 + u * 32 + lane;
-      pr[u] = it < a.n_items ? __ldg(a.items + it) : ~0ull;
+  for (uint32_t sb = blockIdx.x; sb < a.n_sub; sb += gridDim.x) {
+    const uint32_t b0 = __ldg(a.soff + sb), b1 = __ldg(a.soff + sb + 1);
+    if (b0 == b1) continue;  // CTA-uniform
+    // first group word of the sub-bin (sub-bins narrower than a word share it)
+    const uint32_t w0 = uint32_t((uint64_t(sb) << a.code_shift) >> 5);
+    for (uint32_t i = threadIdx.x; i < a.words; i += kJoinThreads) {
+      if (a.strands & 1) { sI[0][i] = __ldg(a.If + w0 + i); sS[0][i] = __ldg(a.Sf + w0 + i); }
+      if (a.strands & 2) { sI[1][i] = __ldg(a.Ir + w0 + i); sS[1][i] = __ldg(a.Sr + w0 + i); }
     }
-    // all occupancy / group-start words first (16 independent loads per
-    // lane), then all S' pairs: no load waits behind another lookup
-    uint32_t wI[kSlots], wS[kSlots];
+    __syncthreads();
+    const uint32_t step = kJoinThreads * kItems;
+    for (uint32_t base = b0 + wid * 32 * kItems; base < b1; base += step) {  // warp-uniform bound
+      uint32_t cnt = 0, nr = 0, rk0[kSlots], rn[kSlots], rpos[kSlots];
+      uint64_t pr[kItems];
 #pragma unroll
-    for (int u = 0; u < kItems; ++u) {
-      const uint32_t wi = pr[u] == ~0ull ? 0u : uint32_t(pr[u] >> 37);
-      wI[2 * u] = (a.strands & 1) ? __ldg(a.If + wi) : 0u;
-      wS[2 * u] = (a.strands & 1) ? __ldg(a.Sf + wi) : 0u;
-      wI[2 * u + 1] = (a.strands & 2) ? __ldg(a.Ir + wi) : 0u;
-      wS[2 * u + 1] = (a.strands & 2) ? __ldg(a.Sr + wi) : 0u;
-    }
-#pragma unroll
-    for (int s = 0; s < kSlots; ++s) {
-      const int u = s >> 1;
-      const uint32_t bit = uint32_t(pr[u] >> 32) & 31u;
-      const bool hit = pr[u] != ~0ull && ((wI[s] >> bit) & 1u);
-      const uint32_t b = wS[s] + __popc(wI[s] & ((1u << bit) - 1u));
-      const uint32_t* S1 = (s & 1) ? a.S1r : a.S1f;
-      rk0[s] = hit ? __ldg(S1 + b) : 0u;
-      rn[s] = hit ? __ldg(S1 + b + 1) : 0u;
-      rpos[s] = uint32_t(pr[u]) | ((s & 1) ? 0x80000000u : 0u);
-    }
-#pragma unroll
-    for (int s = 0; s < kSlots; ++s) {
-      rn[s] -= rk0[s];
-      cnt += rn[s];
-      nr += rn[s] != 0;
-    }
-    n_hit += nr;
-    n_occ += cnt;
-    const uint32_t o_inc = warp_inclusive_scan(cnt);
-    const uint32_t T = __shfl_sync(kFull, o_inc, 31);
-    if (T == 0) continue;
-    constexpr uint32_t R = 32 * kSlots;
-    uint32_t run = o_inc - cnt;
-#pragma unroll
-    for (int i = 0; i < kSlots; ++i) {
-      s_k0[wid][lane * kSlots + i] = rk0[i];
-      s_pre[wid][lane * kSlots + i] = run;
-      s_pos[wid][lane * kSlots + i] = rpos[i];
-      run += rn[i];
-    }
-    if (lane == 0) s_pre[wid][R] = T;
-    __syncwarp();
-    for (uint32_t j0 = 0; j0 < T; j0 += 32) {
-      const uint32_t j = j0 + lane;
-      bool emit = false;
-      uint64_t key = 0;
-      if (j < T) {
-        uint32_t lo = 0, hi = R;  // largest e with s_pre[e] <= j
-        while (hi - lo > 1) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (s_pre[wid][mid] <= j) lo = mid; else hi = mid;
-        }
-        const uint32_t pw = s_pos[wid][lo];
-        const bool rev = pw >> 31;
-        const uint32_t pp = pw & 0x7FFFFFFFu;
-        const uint32_t k = s_k0[wid][lo] + (j - s_pre[wid][lo]);
-        const uint32_t r = a.by_m.div(pp), o = pp - r * a.m;
-        // four independent loads in flight: occurrence, its stored predecessor
-        // base, the read length and the read word holding the compared base
-        const uint32_t cmp = rev ? o + q : (o ? o - 1 : 0);  // read offset the run-start rule compares
-        const uint32_t x = __ldg((rev ? a.Or : a.Of) + k);
-        const uint32_t pv = kRunStart ? uint32_t(__ldg((rev ? a.Xr : a.Xf) + k)) : 4u;
-        const uint32_t n = __ldg(a.rlen + r);
-        const uint64_t rword = kRunStart ? __ldg(a.rwords + uint64_t(r) * a.W + (cmp >> 5)) : 0ull;
-        emit = true;
-        if (kRunStart && pv != 4 && (rev ? (o + q + 1 <= n) : (o >= 1)) &&
-            pv == (uint32_t(rword >> (62 - 2 * (cmp & 31))) & 3u))
-          emit = false;
-        uint32_t c = 0, hi2 = a.n_chrom;  // chromosome of x
-        while (hi2 - c > 1) {
-          const uint32_t mid = (c + hi2) >> 1;
-          if (__ldg(a.cb + mid) <= x) c = mid; else hi2 = mid;
-        }
-        const int64_t p = int64_t(x) - int64_t(__ldg(a.cb + c));
-        const int64_t d = rev ? p + int64_t(o) + int64_t(q) - int64_t(n) : p - int64_t(o);
-        const uint64_t gp = uint64_t(int64_t(__ldg(a.cbp + c)) + d);
-        key = (uint64_t(r) << (a.diag_bits + 1)) | (uint64_t(rev) << a.diag_bits) | gp;
+      for (int u = 0; u < kItems; ++u) {
+        const uint32_t it = base + u * 32 + lane;
+        pr[u] = it < b1 ? __ldg(a.items + it) : ~0ull;
       }
-      const unsigned m = __ballot_sync(kFull, emit);
-      if (emit) s_out[wid][staged + __popc(m & lanemask_lt())] = key;
-      staged += __popc(m);
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s) {
+        const int u = s >> 1, st = s & 1;
+        const bool ok = pr[u] != ~0ull && (a.strands & (1 << st));
+        const uint32_t g = uint32_t(pr[u] >> 32);
+        const uint32_t wl = (g >> 5) - w0, bit = g & 31u;
+        const uint32_t w = ok ? sI[st][wl] : 0u;
+        const bool hit = (w >> bit) & 1u;
+        const uint32_t b = (hit ? sS[st][wl] : 0u) + __popc(w & ((1u << bit) - 1u));
+        const uint32_t* S1 = st ? a.S1r : a.S1f;
+        rk0[s] = hit ? __ldg(S1 + b) : 0u;
+        rn[s] = hit ? __ldg(S1 + b + 1) : 0u;
+        rpos[s] = uint32_t(pr[u]) | (st ? 0x80000000u : 0u);
+      }
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s) {
+        rn[s] -= rk0[s];
+        cnt += rn[s];
+        nr += rn[s] != 0;
+      }
+      n_hit += nr;
+      n_occ += cnt;
+      const uint32_t o_inc = warp_inclusive_scan(cnt);
+      const uint32_t T = __shfl_sync(kFull, o_inc, 31);
+      if (T == 0) continue;
+      uint32_t run = o_inc - cnt;
+#pragma unroll
+      for (int i = 0; i < kSlots; ++i) {
+        s_k0[wid][lane * kSlots + i] = rk0[i];
+        s_pre[wid][lane * kSlots + i] = run;
+        s_pos[wid][lane * kSlots + i] = rpos[i];
+        run += rn[i];
+      }
+      if (lane == 0) s_pre[wid][kRanges] = T;
       __syncwarp();
-      if (staged > kStage - 32) flush();
+      for (uint32_t j0 = 0; j0 < T; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        bool emit = false;
+        uint64_t key = 0;
+        if (j < T) {
+          uint32_t lo = 0, hi = kRanges;  // largest e with s_pre[e] <= j (empty slots never win)
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (s_pre[wid][mid] <= j) lo = mid; else hi = mid;
+          }
+          const uint32_t pw = s_pos[wid][lo];
+          const bool rev = pw >> 31;
+          const uint32_t pp = pw & 0x7FFFFFFFu;
+          const uint32_t k = s_k0[wid][lo] + (j - s_pre[wid][lo]);
+          const uint32_t r = a.by_m.div(pp), o = pp - r * a.m;
+          // independent loads: occurrence, its stored predecessor base, the
+          // read length and the read word holding the compared base
+          const uint32_t cmp = rev ? o + q : (o ? o - 1 : 0);
+          const uint32_t x = __ldg((rev ? a.Or : a.Of) + k);
+          const uint32_t pv = kRunStart ? uint32_t(__ldg((rev ? a.Xr : a.Xf) + k)) : 4u;
+          const uint32_t n = __ldg(a.rlen + r);
+          const uint64_t rword = kRunStart ? __ldg(a.rwords + uint64_t(r) * a.W + (cmp >> 5)) : 0ull;
+          emit = !(kRunStart && pv != 4 && (rev ? (o + q + 1 <= n) : (o >= 1)) &&
+                   pv == (uint32_t(rword >> (62 - 2 * (cmp & 31))) & 3u));
+          uint32_t c = 0, hi2 = a.n_chrom;  // chromosome of x
+          while (hi2 - c > 1) {
+            const uint32_t mid = (c + hi2) >> 1;
+            if (__ldg(a.cb + mid) <= x) c = mid; else hi2 = mid;
+          }
+          const int64_t p = int64_t(x) - int64_t(__ldg(a.cb + c));
+          const int64_t d = rev ? p + int64_t(o) + int64_t(q) - int64_t(n) : p - int64_t(o);
+          const uint64_t gp = uint64_t(int64_t(__ldg(a.cbp + c)) + d);
+          key = (uint64_t(r) << (a.diag_bits + 1)) | (uint64_t(rev) << a.diag_bits) | gp;
+        }
+        const unsigned m = __ballot_sync(kFull, emit);
+        if (emit) s_out[wid][staged + __popc(m & lanemask_lt())] = key;
+        staged += __popc(m);
+        __syncwarp();
+        if (staged > kStage - 32) flush();
+      }
     }
+    __syncthreads();  // shared words are reloaded for the next sub-bin
   }
   flush();
   n_hit = warp_reduce_sum(n_hit);
@@ -197,7 +207,11 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   const RefQIndex& X = ref.qidx;
   JoinArgs a;
   a.items = rp.pairs.p;
-  a.n_items = rp.V;
+  a.soff = rp.soff.p;
+  a.n_sub = 1u << rp.sub_bits;
+  a.code_shift = 2 * rp.q - rp.sub_bits;
+  a.words = std::max<uint32_t>(1, (1u << a.code_shift) / 32);
+  if (a.words > kMaxWords) throw InternalError("join: sub-bin wider than the shared staging");
   a.q = rp.q;
   a.If = reinterpret_cast<const uint32_t*>(X.fwd.I.p);
   a.Sf = X.fwd.S.p;
@@ -223,18 +237,18 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   a.counter = counter.p;
   a.stats = counter.p + 1;
   if (keys.n == 0) keys.alloc(c, std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16));
-  const unsigned grid = unsigned(std::max<uint64_t>(
-      1, std::min<uint64_t>(ceil_div(rp.V, kJoinThreads * kItems),
-                            resident_grid(mode == 1 ? (const void*)k_join<true> : (const void*)k_join<false>,
-                                          kJoinThreads, 0))));
+  const void* kfn = mode == 1 ? (const void*)k_join<true> : (const void*)k_join<false>;
+  const size_t smem = size_t(4) * a.words * sizeof(uint32_t);
+  QGM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const unsigned grid = std::min<unsigned>(a.n_sub, resident_grid(kfn, kJoinThreads, smem));
   for (int attempt = 0; attempt < 2; ++attempt) {
     counter.zero();
     a.out = keys.p;
     a.cap = keys.n;
     if (rp.V > 0) {
       KernelScope ks(c, "k_join");
-      if (mode == 1) QGM_KERNEL(c, k_join<true>, grid, kJoinThreads, 0, a);
-      else QGM_KERNEL(c, k_join<false>, grid, kJoinThreads, 0, a);
+      if (mode == 1) QGM_KERNEL(c, k_join<true>, grid, kJoinThreads, smem, a);
+      else QGM_KERNEL(c, k_join<false>, grid, kJoinThreads, smem, a);
     }
     unsigned long long h[3] = {0, 0, 0};
     QGM_CUDA(cudaMemcpyAsync(h, counter.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));

@@ -255,10 +255,18 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   // P2: refine to the top min(2q, 16) code bits (short reuse distance of the
   // reference-index sectors in the join)
   const unsigned key_bits = std::min(2 * q, 16u);
-  if (key_bits <= bits || V == 0) return;
+  out.sub_bits = key_bits;
+  if (key_bits <= bits || V == 0) {  // the first pass already grouped by every code bit (2q <= 8)
+    out.soff.alloc(c, kBins + 1);
+    QGM_CUDA(cudaMemcpyAsync(out.soff.p, out.boff.p, (kBins + 1) * 4, cudaMemcpyDeviceToDevice, c.stream));
+    out.sub_bits = bits;
+    return;
+  }
   const unsigned kshift = 2 * q - key_bits, sub = key_bits - bits;
   const uint32_t keys = 1u << key_bits;
-  DBuf<uint32_t> h2(c, keys + 1), off(c, keys + 1);
+  DBuf<uint32_t> h2(c, keys + 1);
+  out.soff.alloc(c, keys + 1);
+  DBuf<uint32_t>& off = out.soff;
   h2.zero();
   const unsigned grid2 = unsigned(std::min<uint64_t>(ceil_div(V, kChunk), uint64_t(kSMs) * 4));
   {
