@@ -171,9 +171,9 @@ def run_gpu(args):
     import torch
     import paper_1403_1706_b200 as qgm
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_1403_1706_b200 import sharding
+
+    rank, world, local = sharding.world()
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -272,13 +272,10 @@ def run_gpu(args):
     barrier()
     e2e_ms = sum(e2e_times)
 
-    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_ms, e2e_ms = t.tolist()
+    dev_ms, e2e_ms = sharding.max_over_ranks([dev_ms, e2e_ms], dist, device=f"cuda:{local}")
     total_reads = n_reads * args.steps * world
-    value = total_reads / (dev_ms / 1e3)
-    e2e_value = total_reads / (e2e_ms / 1e3)
+    value = sharding.weak_scaling_value(n_reads, args.steps, world, dev_ms)
+    e2e_value = sharding.weak_scaling_value(n_reads, args.steps, world, e2e_ms)
 
     # roofline of the dominant kernel
     peak, peak_kind = load_peaks()

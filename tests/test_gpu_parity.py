@@ -122,3 +122,20 @@ def test_c2_shape_properties(ctx):
     strand[best["read_id"][::-1]] = best["strand"][::-1]
     ok = (np.abs(first - tp.astype(np.int64)) <= 8) & (strand == ts)
     assert ok.mean() > 0.95, ok.mean()
+
+
+def test_c2_full_size_hit_parity_with_oracle(ctx, oracle):
+    """The bench workload itself (100 Mbp, 1M reads, q=16, all-hits): every
+    hit identical to the CPU oracle (Alg. 2 multiset + sort/unique + banded DP
+    restatement + strata)."""
+    import paper_1403_1706_b200 as qgm
+    L, N = 100_000_000, 1_000_000
+    ref = qgm.random_reference(7, L)
+    cb = np.array([0, L], np.uint64)
+    codes, lengths, *_ = qgm.simulate_reads(1000, ref, cb, N, 100, 0.03)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    got, st = ctx.map(reads, R, q=16, mode=1)
+    want, ost = oracle.map(ref, cb, codes, 100, lengths, q=16, mode=1)
+    assert st["unique_candidates"] == ost["unique_candidates"]
+    assert _same(got, want), (got.size, want.size)
