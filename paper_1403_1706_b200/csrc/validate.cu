@@ -72,6 +72,9 @@ __device__ __forceinline__ Win load_win(const uint2* __restrict__ fp, int64_t a,
   return w;
 }
 
+__device__ __forceinline__ unsigned popcount_t(uint32_t x) { return __popc(x); }
+__device__ __forceinline__ unsigned popcount_t(uint64_t x) { return __popcll(x); }
+
 template <class T> struct Band;
 template <> struct Band<uint32_t> {
   static constexpr int kWords = 1;
@@ -98,9 +101,14 @@ template <> struct Band<uint64_t> {
   }
 };
 
+// Returns false when the candidate was abandoned early: every path crosses
+// every row with non-decreasing cost, so k >= min_t D[i][t] >= D[i][0] -
+// popc(Mv) at any row i; once that bound exceeds kmax the candidate cannot
+// pass the identity threshold (used by the map path only, kmax < 0 = never).
 template <class T, bool kCheck>
-__device__ __forceinline__ void myers_rows(const ValArgs& a, uint32_t r, bool rev, uint32_t n, int64_t F, uint32_t L,
-                                           int64_t cbeg, int64_t cend, T mask, T& Pv, T& Mv, int& score0) {
+__device__ __forceinline__ bool myers_rows(const ValArgs& a, uint32_t r, bool rev, uint32_t n, int64_t F, uint32_t L,
+                                           int64_t cbeg, int64_t cend, T mask, T& Pv, T& Mv, int& score0,
+                                           int kmax) {
   constexpr int NW = Band<T>::kWords;
   const uint2* rp = a.rplanes + uint64_t(r) * a.Wp;
   Win w[NW + 1];
@@ -145,8 +153,10 @@ __device__ __forceinline__ void myers_rows(const ValArgs& a, uint32_t r, bool re
       Pv = nP;
       Mv = nM;
       score0 += int(D1 & T(1));
+      if ((t & 15) == 15 && kmax >= 0 && score0 - int(popcount_t(Mv)) > kmax) return false;
     }
   }
+  return true;
 }
 
 template <class T>
@@ -182,8 +192,11 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a) {
         T Pv = 0, Mv = 0;
         int score0 = 0;
         const int64_t F = cbeg + w0;
-        if (w0 >= 0 && w0 + int64_t(L) <= Lc) myers_rows<T, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0);
-        else myers_rows<T, true>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0);
+        // map path: abandon candidates that can no longer reach the threshold
+        const int kmax = a.mode == 0 ? int((uint64_t(100 - a.pct) * n) / 100) : -1;
+        const bool done = (w0 >= 0 && w0 + int64_t(L) <= Lc)
+                              ? myers_rows<T, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax)
+                              : myers_rows<T, true>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax);
         int v = score0, best = score0;
         unsigned tbest = 0;
         for (unsigned t = 1; t < a.B; ++t) {
@@ -195,7 +208,7 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a) {
         int64_t rs = w0 + int64_t(start);
         rs = rs < 0 ? 0 : (rs > Lc - 1 ? Lc - 1 : rs);
         ref_start = uint32_t(rs);
-        kept = k <= int(n) && uint64_t(100) * uint64_t(int64_t(n) - k) >= uint64_t(a.pct) * n;
+        kept = done && k <= int(n) && uint64_t(100) * uint64_t(int64_t(n) - k) >= uint64_t(a.pct) * n;
       }
     }
     if (a.mode == 0) {
