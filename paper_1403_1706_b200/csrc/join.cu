@@ -100,15 +100,30 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
       if (a.strands & 1) { sI[0][i] = __ldg(a.If + w0 + i); sS[0][i] = __ldg(a.Sf + w0 + i); }
       if (a.strands & 2) { sI[1][i] = __ldg(a.Ir + w0 + i); sS[1][i] = __ldg(a.Sr + w0 + i); }
     }
+    // warm L2 with the next sub-bin's words while this one is processed
+    {
+      const uint32_t nsb = sb + gridDim.x;
+      const uint32_t bytes = a.words * 4u;
+      if (nsb < a.n_sub && threadIdx.x * 128u < 4u * bytes) {
+        const uint32_t arr = (threadIdx.x * 128u) / bytes, off = (threadIdx.x * 128u) % bytes;
+        const uint32_t* src = arr == 0 ? a.If : arr == 1 ? a.Ir : arr == 2 ? a.Sf : a.Sr;
+        const char* p = reinterpret_cast<const char*>(src + uint32_t((uint64_t(nsb) << a.code_shift) >> 5)) + off;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+      }
+    }
     __syncthreads();
-    const uint32_t step = kJoinThreads * kItems;
-    for (uint32_t base = b0 + wid * 32 * kItems; base < b1; base += step) {  // warp-uniform bound
+    // the sub-bin's items split evenly over the warps (no warp idles at the
+    // end-of-sub-bin barrier while another runs a second full round)
+    const uint32_t nitems = b1 - b0;
+    const uint32_t my_lo = b0 + uint32_t(uint64_t(nitems) * wid / kJoinWarps);
+    const uint32_t my_hi = b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kJoinWarps);
+    for (uint32_t base = my_lo; base < my_hi; base += 32 * kItems) {  // warp-uniform bound
       uint32_t cnt = 0, nr = 0, rk0[kSlots], rn[kSlots], rpos[kSlots];
       uint64_t pr[kItems];
 #pragma unroll
       for (int u = 0; u < kItems; ++u) {
         const uint32_t it = base + u * 32 + lane;
-        pr[u] = it < b1 ? __ldg(a.items + it) : ~0ull;
+        pr[u] = it < my_hi ? __ldg(a.items + it) : ~0ull;
       }
 #pragma unroll
       for (int s = 0; s < kSlots; ++s) {
