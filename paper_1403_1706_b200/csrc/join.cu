@@ -38,6 +38,7 @@ constexpr int kItems = 4;                 // read q-grams per lane per step
 constexpr int kSlots = 2 * kItems;        // (item, strand) lookups per lane
 constexpr int kRanges = 32 * kSlots;
 constexpr int kStage = 128;               // staged keys per warp
+constexpr uint32_t kInline = 4;           // intervals up to this length are expanded in-lane
 constexpr uint32_t kMaxWords = 2048;      // group words per sub-bin and array (q = 16)
 
 struct JoinArgs {
@@ -66,6 +67,36 @@ struct JoinArgs {
   unsigned long long* stats;
 };
 
+// One (reference occurrence k, read q-gram pw) pair -> candidate key; false if
+// the run-start rule suppresses it (the (q+1)-gram one base to the left on the
+// same diagonal also matches).
+template <bool kRunStart>
+__device__ __forceinline__ bool expand(const JoinArgs& a, unsigned q, uint32_t k, uint32_t pw, uint64_t& key) {
+  const bool rev = pw >> 31;
+  const uint32_t pp = pw & 0x7FFFFFFFu;
+  const uint32_t r = a.by_m.div(pp), o = pp - r * a.m;
+  // independent loads: occurrence, its stored predecessor base, the read
+  // length and the read word holding the compared base
+  const uint32_t cmp = rev ? o + q : (o ? o - 1 : 0);
+  const uint32_t x = __ldg((rev ? a.Or : a.Of) + k);
+  const uint32_t pv = kRunStart ? uint32_t(__ldg((rev ? a.Xr : a.Xf) + k)) : 4u;
+  const uint32_t n = __ldg(a.rlen + r);
+  const uint64_t rword = kRunStart ? __ldg(a.rwords + uint64_t(r) * a.W + (cmp >> 5)) : 0ull;
+  if (kRunStart && pv != 4 && (rev ? (o + q + 1 <= n) : (o >= 1)) &&
+      pv == (uint32_t(rword >> (62 - 2 * (cmp & 31))) & 3u))
+    return false;
+  uint32_t c = 0, hi = a.n_chrom;  // chromosome of x
+  while (hi - c > 1) {
+    const uint32_t mid = (c + hi) >> 1;
+    if (__ldg(a.cb + mid) <= x) c = mid; else hi = mid;
+  }
+  const int64_t p = int64_t(x) - int64_t(__ldg(a.cb + c));
+  const int64_t d = rev ? p + int64_t(o) + int64_t(q) - int64_t(n) : p - int64_t(o);
+  const uint64_t gp = uint64_t(int64_t(__ldg(a.cbp + c)) + d);
+  key = (uint64_t(r) << (a.diag_bits + 1)) | (uint64_t(rev) << a.diag_bits) | gp;
+  return true;
+}
+
 template <bool kRunStart>
 __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
   extern __shared__ uint32_t s_words[];  // [I fwd | I rc | S fwd | S rc], a.words each
@@ -89,6 +120,13 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
       if (base + i < a.cap) a.out[base + i] = s_out[wid][i];
     staged = 0;
     __syncwarp();
+  };
+  auto stage_key = [&](bool emit, uint64_t key) {  // all lanes call it
+    const unsigned m = __ballot_sync(kFull, emit);
+    if (emit) s_out[wid][staged + __popc(m & lanemask_lt())] = key;
+    staged += __popc(m);
+    __syncwarp();
+    if (staged > kStage - 32) flush();
   };
 
   for (uint32_t sb = blockIdx.x; sb < a.n_sub; sb += gridDim.x) {
@@ -147,59 +185,55 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
       }
       n_hit += nr;
       n_occ += cnt;
-      const uint32_t o_inc = warp_inclusive_scan(cnt);
-      const uint32_t T = __shfl_sync(kFull, o_inc, 31);
-      if (T == 0) continue;
-      uint32_t run = o_inc - cnt;
+      if (__all_sync(kFull, cnt == 0)) continue;
+      // compact the non-empty (q-gram, strand) lookups of the warp into a list
+      uint32_t nent = 0;
 #pragma unroll
-      for (int i = 0; i < kSlots; ++i) {
-        s_k0[wid][lane * kSlots + i] = rk0[i];
-        s_pre[wid][lane * kSlots + i] = run;
-        s_pos[wid][lane * kSlots + i] = rpos[i];
-        run += rn[i];
-      }
-      if (lane == 0) s_pre[wid][kRanges] = T;
-      __syncwarp();
-      for (uint32_t j0 = 0; j0 < T; j0 += 32) {
-        const uint32_t j = j0 + lane;
-        bool emit = false;
-        uint64_t key = 0;
-        if (j < T) {
-          uint32_t lo = 0, hi = kRanges;  // largest e with s_pre[e] <= j (empty slots never win)
-          while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (s_pre[wid][mid] <= j) lo = mid; else hi = mid;
-          }
-          const uint32_t pw = s_pos[wid][lo];
-          const bool rev = pw >> 31;
-          const uint32_t pp = pw & 0x7FFFFFFFu;
-          const uint32_t k = s_k0[wid][lo] + (j - s_pre[wid][lo]);
-          const uint32_t r = a.by_m.div(pp), o = pp - r * a.m;
-          // independent loads: occurrence, its stored predecessor base, the
-          // read length and the read word holding the compared base
-          const uint32_t cmp = rev ? o + q : (o ? o - 1 : 0);
-          const uint32_t x = __ldg((rev ? a.Or : a.Of) + k);
-          const uint32_t pv = kRunStart ? uint32_t(__ldg((rev ? a.Xr : a.Xf) + k)) : 4u;
-          const uint32_t n = __ldg(a.rlen + r);
-          const uint64_t rword = kRunStart ? __ldg(a.rwords + uint64_t(r) * a.W + (cmp >> 5)) : 0ull;
-          emit = !(kRunStart && pv != 4 && (rev ? (o + q + 1 <= n) : (o >= 1)) &&
-                   pv == (uint32_t(rword >> (62 - 2 * (cmp & 31))) & 3u));
-          uint32_t c = 0, hi2 = a.n_chrom;  // chromosome of x
-          while (hi2 - c > 1) {
-            const uint32_t mid = (c + hi2) >> 1;
-            if (__ldg(a.cb + mid) <= x) c = mid; else hi2 = mid;
-          }
-          const int64_t p = int64_t(x) - int64_t(__ldg(a.cb + c));
-          const int64_t d = rev ? p + int64_t(o) + int64_t(q) - int64_t(n) : p - int64_t(o);
-          const uint64_t gp = uint64_t(int64_t(__ldg(a.cbp + c)) + d);
-          key = (uint64_t(r) << (a.diag_bits + 1)) | (uint64_t(rev) << a.diag_bits) | gp;
+      for (int s = 0; s < kSlots; ++s) {
+        const bool has = rn[s] != 0;
+        const unsigned bm = __ballot_sync(kFull, has);
+        if (has) {
+          const uint32_t e = nent + __popc(bm & lanemask_lt());
+          s_k0[wid][e] = rk0[s];
+          s_pre[wid][e] = rn[s];
+          s_pos[wid][e] = rpos[s];
         }
-        const unsigned m = __ballot_sync(kFull, emit);
-        if (emit) s_out[wid][staged + __popc(m & lanemask_lt())] = key;
-        staged += __popc(m);
-        __syncwarp();
-        if (staged > kStage - 32) flush();
+        nent += __popc(bm);
       }
+      __syncwarp();
+      // one list entry per lane per round; intervals of up to kInline
+      // occurrences (almost all of them) are expanded in the lane, longer ones
+      // (repeats) by the whole warp, one interval at a time
+      for (uint32_t e0 = 0; e0 < nent; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        uint32_t k0 = 0, len = 0, pw = 0;
+        if (e < nent) {
+          k0 = s_k0[wid][e];
+          len = s_pre[wid][e];
+          pw = s_pos[wid][e];
+        }
+        const bool longi = len > kInline;
+        const uint32_t nin = longi ? 0u : len;
+        const uint32_t rounds = __reduce_max_sync(kFull, nin);
+        for (uint32_t t = 0; t < rounds; ++t) {
+          uint64_t key = 0;
+          const bool emit = t < nin && expand<kRunStart>(a, q, k0 + t, pw, key);
+          stage_key(emit, key);
+        }
+        unsigned lm = __ballot_sync(kFull, longi);
+        while (lm) {
+          const int src = __ffs(lm) - 1;
+          lm &= lm - 1;
+          const uint32_t lk0 = __shfl_sync(kFull, k0, src), llen = __shfl_sync(kFull, len, src);
+          const uint32_t lpw = __shfl_sync(kFull, pw, src);
+          for (uint32_t t0 = 0; t0 < llen; t0 += 32) {
+            uint64_t key = 0;
+            const bool emit = t0 + lane < llen && expand<kRunStart>(a, q, lk0 + t0 + lane, lpw, key);
+            stage_key(emit, key);
+          }
+        }
+      }
+      __syncwarp();
     }
     __syncthreads();  // shared words are reloaded for the next sub-bin
   }
