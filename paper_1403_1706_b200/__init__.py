@@ -30,7 +30,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqgm_b200.so")
+LIB_PATH = os.environ.get("QGM_LIB") or os.path.join(_HERE, "libqgm_b200.so")
 SYNTH_PATH = os.path.join(_HERE, "libqgm_synth.so")
 
 MODE_BEST_STRATUM = 0

@@ -99,12 +99,9 @@ __device__ __forceinline__ bool expand(const JoinArgs& a, unsigned q, uint32_t k
 
 template <bool kRunStart>
 __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
-  extern __shared__ uint32_t s_words[];  // [I fwd | I rc], a.words each (group starts are read through L1)
-  const uint32_t nw = a.words;
-  const uint32_t* __restrict__ S1f = a.S1f;
-  const uint32_t* __restrict__ S1r = a.S1r;
-  // strands not requested read as empty occupancy words
-  const uint32_t sm_f = (a.strands & 1) ? ~0u : 0u, sm_r = (a.strands & 2) ? ~0u : 0u;
+  extern __shared__ uint32_t s_words[];  // [I fwd | I rc | S fwd | S rc], a.words each
+  uint32_t* sI[2] = {s_words, s_words + a.words};
+  uint32_t* sS[2] = {s_words + 2 * a.words, s_words + 3 * a.words};
   __shared__ uint32_t s_k0[kJoinWarps][kRanges];
   __shared__ uint32_t s_pre[kJoinWarps][kRanges + 1];
   __shared__ uint32_t s_pos[kJoinWarps][kRanges];  // read text position | strand << 31
@@ -138,8 +135,8 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
     // first group word of the sub-bin (sub-bins narrower than a word share it)
     const uint32_t w0 = uint32_t((uint64_t(sb) << a.code_shift) >> 5);
     for (uint32_t i = threadIdx.x; i < a.words; i += kJoinThreads) {
-      if (a.strands & 1) s_words[i] = __ldg(a.If + w0 + i);
-      if (a.strands & 2) s_words[nw + i] = __ldg(a.Ir + w0 + i);
+      if (a.strands & 1) { sI[0][i] = __ldg(a.If + w0 + i); sS[0][i] = __ldg(a.Sf + w0 + i); }
+      if (a.strands & 2) { sI[1][i] = __ldg(a.Ir + w0 + i); sS[1][i] = __ldg(a.Sr + w0 + i); }
     }
     // warm L2 with the next sub-bin's words while this one is processed
     {
@@ -167,22 +164,18 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
         pr[u] = it < my_hi ? __ldg(a.items + it) : ~0ull;
       }
 #pragma unroll
-      for (int u = 0; u < kItems; ++u) {
+      for (int s = 0; s < kSlots; ++s) {
+        const int u = s >> 1, st = s & 1;
+        const bool ok = pr[u] != ~0ull && (a.strands & (1 << st));
         const uint32_t g = uint32_t(pr[u] >> 32);
-        const uint32_t wl = pr[u] == ~0ull ? 0u : (g >> 5) - w0, bit = g & 31u;
-        const uint32_t below = (1u << bit) - 1u;
-        // shared-memory words at fixed offsets: [I fwd | I rc | S fwd | S rc]
-        const uint32_t wf = s_words[wl] & sm_f, wr = s_words[nw + wl] & sm_r;
-        const uint32_t sf = __ldg(a.Sf + w0 + wl), sr = __ldg(a.Sr + w0 + wl);
-        const bool ok = pr[u] != ~0ull;
-        const bool hf = ok && ((wf >> bit) & 1u), hr = ok && ((wr >> bit) & 1u);
-        const uint32_t bf = sf + __popc(wf & below), br = sr + __popc(wr & below);
-        rk0[2 * u] = hf ? __ldg(S1f + bf) : 0u;
-        rn[2 * u] = hf ? __ldg(S1f + bf + 1) : 0u;
-        rk0[2 * u + 1] = hr ? __ldg(S1r + br) : 0u;
-        rn[2 * u + 1] = hr ? __ldg(S1r + br + 1) : 0u;
-        rpos[2 * u] = uint32_t(pr[u]);
-        rpos[2 * u + 1] = uint32_t(pr[u]) | 0x80000000u;
+        const uint32_t wl = (g >> 5) - w0, bit = g & 31u;
+        const uint32_t w = ok ? sI[st][wl] : 0u;
+        const bool hit = (w >> bit) & 1u;
+        const uint32_t b = (hit ? sS[st][wl] : 0u) + __popc(w & ((1u << bit) - 1u));
+        const uint32_t* S1 = st ? a.S1r : a.S1f;
+        rk0[s] = hit ? __ldg(S1 + b) : 0u;
+        rn[s] = hit ? __ldg(S1 + b + 1) : 0u;
+        rpos[s] = uint32_t(pr[u]) | (st ? 0x80000000u : 0u);
       }
 #pragma unroll
       for (int s = 0; s < kSlots; ++s) {
@@ -294,7 +287,7 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   a.stats = counter.p + 1;
   if (keys.n == 0) keys.alloc(c, std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16));
   const void* kfn = mode == 1 ? (const void*)k_join<true> : (const void*)k_join<false>;
-  const size_t smem = size_t(2) * a.words * sizeof(uint32_t);
+  const size_t smem = size_t(4) * a.words * sizeof(uint32_t);
   QGM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const unsigned grid = std::min<unsigned>(a.n_sub, resident_grid(kfn, kJoinThreads, smem));
   for (int attempt = 0; attempt < 2; ++attempt) {
