@@ -224,7 +224,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   uint64_t n_raw, n_u;
   uint64_t fst[2] = {0, 0};
   if (P.group_width && P.group_width != 32 && P.group_width != 64) throw InputError("group width must be 32 or 64");
-  if (ref.total < (uint64_t(1) << 32)) {
+  if (ref.padded_total < (uint64_t(1) << 32)) {
     // production path: read q-grams bucket-sorted by code, joined with the
     // per-strand reference q-group indexes (join.cu). group_width / sampled
     // only change the layout of an index that is never materialised here.
@@ -632,7 +632,7 @@ int qgm_ref_prepare(qgm_ctx* ctx, qgm_ref* ref, uint32_t q) {
   return guard(ctx, [&] {
     activate(ctx);
     require(q >= 1 && q <= 16, "q must be in [1, 16]");
-    require(ref->r.total < (uint64_t(1) << 32), "reference index: more than 2^32-1 bases");
+    require(ref->r.padded_total < (uint64_t(1) << 32), "reference index: more than 2^32-1 padded bases");
     qgm::prepare_ref_index(ctx->c, ref->r, q);
     QGM_CUDA(cudaStreamSynchronize(ctx->c.stream));
   });

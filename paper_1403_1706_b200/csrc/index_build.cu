@@ -26,6 +26,8 @@
 //                shared-memory cursors.
 // Every HBM write of I/S/S'/O is coalesced; the only random traffic is the
 // bucket scatter of K2.
+#include <cstdlib>
+
 #include "internal.hpp"
 
 namespace qgm {
@@ -57,15 +59,18 @@ struct ReadSource {
 // Reference positions of one strand: every global position whose window lies
 // inside its chromosome and is not masked. The code is the
 // forward q-gram, or the code of its reverse complement for the RC strand.
-// extra = the base the run-start rule compares (ref[p-1], or its complement
-// on the RC strand), or 4 when p-1 is outside the chromosome or masked.
+// pos = the padded coordinate cbp[c] + p (RefQIndex); extra = the base the
+// run-start rule compares (ref[p-1], or its complement on the RC strand), or 4
+// when p-1 is outside the chromosome or masked. With `packed`, extra goes into
+// pos's top 3 bits instead.
 struct RefSource {
   const uint64_t* ref;
   const uint64_t* mask;
   const uint64_t* cb;
   uint32_t n_chrom;
   unsigned q;
-  bool rc;
+  bool rc, packed;
+  uint64_t gap;
   __device__ __forceinline__ bool masked(uint64_t x) const {
     return mask && ((__ldg(mask + (x >> 6)) >> (x & 63)) & 1ull);
   }
@@ -80,11 +85,15 @@ struct RefSource {
     if (p + q > __ldg(cb + lo + 1) - cbeg) return false;
     g = qgram_at(ref, x, q);
     if (rc) g = rc_code(g, q);
-    pos = uint32_t(x);
+    pos = uint32_t(x + uint64_t(lo + 1) * gap);
     extra = 4;
     if (p >= 1 && !masked(x - 1)) {
       const uint32_t b = base_at(ref, x - 1);
       extra = rc ? 3u - b : b;
+    }
+    if (packed) {
+      pos |= extra << kPackedPosBits;
+      extra = 0;
     }
     return true;
   }
@@ -373,9 +382,9 @@ void bucket_reads(Ctx& c, const Reads& reads, unsigned q, unsigned w, Buckets& o
   bucket_impl(c, src, uint64_t(reads.n) * src.span, out);
 }
 
-void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool rc, Buckets& out) {
+void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool rc, bool packed, Buckets& out) {
   init_geometry(out, q, 32);
-  if (ref.total >= (uint64_t(1) << 32)) throw InputError("reference index: more than 2^32-1 bases");
+  if (ref.padded_total >= (uint64_t(1) << 32)) throw InputError("reference index: more than 2^32-1 padded bases");
   RefSource src;
   src.ref = ref.words.p;
   src.mask = ref.mask.p;
@@ -383,6 +392,8 @@ void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool rc, Buckets& out) {
   src.n_chrom = ref.n_chrom;
   src.q = q;
   src.rc = rc;
+  src.packed = packed;
+  src.gap = ref.gap;
   bucket_impl(c, src, ref.total, out);
 }
 
@@ -402,11 +413,17 @@ void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sample
 void prepare_ref_index(Ctx& c, const Ref& ref, unsigned q) {
   if (ref.qidx.q == q) return;
   ref.qidx = RefQIndex();
+  // QGM_REF_UNPACKED=1 forces the separate compare-base array (test knob: the
+  // packed layout covers every reference below 2^29 padded bases)
+  const char* force = std::getenv("QGM_REF_UNPACKED");
+  const bool packed = ref.padded_total < (uint64_t(1) << kPackedPosBits) && !(force && force[0] == '1');
   for (int rc = 0; rc < 2; ++rc) {
     Buckets B;
-    bucket_ref(c, ref, q, rc != 0, B);
-    index_from_buckets(c, B, false, rc ? ref.qidx.rc : ref.qidx.fwd, rc ? &ref.qidx.prev_rc : &ref.qidx.prev_fwd);
+    bucket_ref(c, ref, q, rc != 0, packed, B);
+    DBuf<uint8_t>* prev = packed ? nullptr : (rc ? &ref.qidx.prev_rc : &ref.qidx.prev_fwd);
+    index_from_buckets(c, B, false, rc ? ref.qidx.rc : ref.qidx.fwd, prev);
   }
+  ref.qidx.packed = packed;
   ref.qidx.q = q;
 }
 

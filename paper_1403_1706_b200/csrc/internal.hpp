@@ -180,11 +180,17 @@ struct Buckets {
 // run-start rule compares stored next to every position (4 = none). Built
 // once per reference and q (SPEC.md:262-316's precomputed reference index,
 // with P ordered by q-gram as in PAPER.md:344).
+// O holds padded coordinates (chromosome c's position p -> cbp[c] + p), so a
+// candidate diagonal is O - offset with no chromosome search. When the padded
+// reference is < 2^29 the compared base is packed into O's top 3 bits
+// (packed = true, prev_* empty); otherwise it is a separate byte array.
 struct RefQIndex {
   unsigned q = 0;
+  bool packed = false;
   Index fwd, rc;
   DBuf<uint8_t> prev_fwd, prev_rc;
 };
+constexpr unsigned kPackedPosBits = 29;
 
 // Reference sequences (ReferenceIndex): the concatenated
 // chromosomes in 2-bit (+1 guard word) and as lo/hi bit planes (2 guard words
@@ -245,7 +251,7 @@ void make_ref_planes(Ctx& c, Ref& ref);
 
 // index_build.cu
 void bucket_reads(Ctx& c, const Reads& reads, unsigned q, unsigned w, Buckets& out);
-void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool rc, Buckets& out);
+void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool rc, bool packed, Buckets& out);
 void index_from_buckets(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_t>* extra);
 void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sampled, Index& out);
 void prepare_ref_index(Ctx& c, const Ref& ref, unsigned q);
@@ -260,8 +266,16 @@ void lookup_index(Ctx& c, const Index& idx, const uint32_t* d_codes, uint64_t n,
 uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Ref& ref, int strands, int mode,
                           unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats = nullptr);
 
-// partition.cu -- the batch's read q-grams, (code << 32 | position), grouped
-// by the top min(2q,12) bits of the code.
+// partition.cu -- the batch's read q-grams grouped by the top min(2q,16)
+// bits of their code (sub-bins), one 64-bit join item each:
+//   bits  0..31  read text position pp = r * stride + o
+//   bits 32..41  tail = n_r - q - o (clamped to 1023; the join reloads n_r when
+//                stride - q > 1023)
+//   bits 42..44  read base at o - 1 (forward run-start compare), 4 = none
+//   bits 45..47  read base at o + q (RC run-start compare), 4 = none
+//   bits 48..63  the code bits below the sub-bin prefix
+constexpr unsigned kItemTailShift = 32, kItemFbShift = 42, kItemRbShift = 45, kItemCodeShift = 48;
+constexpr uint32_t kItemTailMax = 1023;
 struct Partitioned {
   unsigned q = 0;
   uint32_t bins = 0, V = 0;

@@ -14,19 +14,24 @@
 // q-grams are partitioned by the top 16 bits of their code (partition.cu).
 //
 // One CTA owns one code sub-bin at a time (2^(2q-16) codes; 2048 group words
-// per array at q=16): it stages the sub-bin's occupancy and group-start words
-// of both reference strands in shared memory with one coalesced load, so all
-// Group-And-Bit / Grouprank lookups of the sub-bin's read q-grams are shared
-// memory hits; the S' / O / prev reads that follow fall in the sub-bin's
-// contiguous slice of the reference index and are L1/L2 local to the CTA. The
-// occupancy/group-start arrays are read from HBM exactly once per batch, in
-// order.
+// per strand at q=16): it stages the sub-bin's occupancy words of both
+// reference strands in shared memory with one coalesced load and rebuilds the
+// group starts on chip (popcount prefix, u16 relative to S at the sub-bin's
+// first word -- one global S read per sub-bin and strand), so all
+// Group-And-Bit / Grouprank lookups (qgroup_index.hpp:50-57, 80-96) of the
+// sub-bin's read q-grams are shared-memory hits. The S' / O reads that follow
+// fall in the sub-bin's contiguous slice of the reference index and are L1/L2
+// local to the CTA. The occupancy array is read from HBM exactly once per
+// batch, in order; S is not read at all.
 //
 // Per warp step: up to 4 read q-grams per lane, both strands looked up, then
 // the union of the occurrence intervals expanded cooperatively, one
-// (reference occurrence, read occurrence) pair per lane. The run-start rule
-// uses the base stored next to every reference occurrence (prev_fwd/prev_rc,
-// 4 = no predecessor) against the read base at o-1 (forward) or o+q (RC).
+// (reference occurrence, read occurrence) pair per lane. Everything the
+// expansion needs travels in the join item (partition.cu) or in O: O holds the
+// padded coordinate of the occurrence (so the diagonal is O - offset, no
+// chromosome search) and -- for references below 2^29 padded bases -- the
+// base the run-start rule compares in its top 3 bits; the item holds the
+// read's own compare bases (o-1 forward, o+q RC) and n - q - o.
 #include "internal.hpp"
 
 namespace qgm {
@@ -34,12 +39,23 @@ namespace {
 
 constexpr int kJoinThreads = 256;
 constexpr int kJoinWarps = kJoinThreads / 32;
-constexpr int kItems = 4;                 // read q-grams per lane per step
+#ifndef QGM_JOIN_ITEMS
+#define QGM_JOIN_ITEMS 4
+#endif
+constexpr int kItems = QGM_JOIN_ITEMS;    // read q-grams per lane per step
 constexpr int kSlots = 2 * kItems;        // (item, strand) lookups per lane
 constexpr int kRanges = 32 * kSlots;
 constexpr int kStage = 128;               // staged keys per warp
 constexpr uint32_t kInline = 4;           // intervals up to this length are expanded in-lane
-constexpr uint32_t kMaxWords = 2048;      // group words per sub-bin and array (q = 16)
+constexpr uint32_t kMaxWords = 2048;      // group words per sub-bin and strand (q = 16)
+constexpr uint32_t kPosMask = (1u << kPackedPosBits) - 1u;
+
+// Shared-memory swizzle of the staged words: thread t of the group-start scan
+// reads words t*per .. t*per+per-1 (per = 16 at q=16), which would put 16
+// lanes of a warp on one bank; XOR-ing the low 4 index bits with the 32-word
+// row number makes every step of that scan (u32 words and u16 starts alike)
+// conflict-free. Lookups pay one shift/and/xor.
+__device__ __forceinline__ uint32_t swz(uint32_t w) { return w ^ ((w >> 5) & 15u); }
 
 struct JoinArgs {
   const uint64_t* items;
@@ -48,17 +64,12 @@ struct JoinArgs {
   unsigned code_shift;  // sub-bin = code >> code_shift
   uint32_t words;       // group words per sub-bin (>= 1)
   unsigned q;
-  const uint32_t *If, *Sf, *S1f, *Of;
-  const uint8_t* Xf;
-  const uint32_t *Ir, *Sr, *S1r, *Or;
-  const uint8_t* Xr;
-  const uint64_t* rwords;
+  const uint32_t *I[2], *S[2], *S1[2], *O[2];
+  const uint8_t* X[2];  // compared base per occurrence (unpacked layout only)
   const uint32_t* rlen;
-  uint32_t W, m;
+  uint32_t m;
   FastDiv by_m;
-  const uint64_t* cb;
-  const uint64_t* cbp;
-  uint32_t n_chrom;
+  int tail_ok;  // item tails are exact (stride - q <= kItemTailMax)
   int strands;
   unsigned diag_bits;
   uint64_t* out;
@@ -67,48 +78,41 @@ struct JoinArgs {
   unsigned long long* stats;
 };
 
-// One (reference occurrence k, read q-gram pw) pair -> candidate key; false if
-// the run-start rule suppresses it (the (q+1)-gram one base to the left on the
-// same diagonal also matches).
-template <bool kRunStart>
-__device__ __forceinline__ bool expand(const JoinArgs& a, unsigned q, uint32_t k, uint32_t pw, uint64_t& key) {
-  const bool rev = pw >> 31;
-  const uint32_t pp = pw & 0x7FFFFFFFu;
-  const uint32_t r = a.by_m.div(pp), o = pp - r * a.m;
-  // independent loads: occurrence, its stored predecessor base, the read
-  // length and the read word holding the compared base
-  const uint32_t cmp = rev ? o + q : (o ? o - 1 : 0);
-  const uint32_t x = __ldg((rev ? a.Or : a.Of) + k);
-  const uint32_t pv = kRunStart ? uint32_t(__ldg((rev ? a.Xr : a.Xf) + k)) : 4u;
-  const uint32_t n = __ldg(a.rlen + r);
-  const uint64_t rword = kRunStart ? __ldg(a.rwords + uint64_t(r) * a.W + (cmp >> 5)) : 0ull;
-  if (kRunStart && pv != 4 && (rev ? (o + q + 1 <= n) : (o >= 1)) &&
-      pv == (uint32_t(rword >> (62 - 2 * (cmp & 31))) & 3u))
-    return false;
-  uint32_t c = 0, hi = a.n_chrom;  // chromosome of x
-  while (hi - c > 1) {
-    const uint32_t mid = (c + hi) >> 1;
-    if (__ldg(a.cb + mid) <= x) c = mid; else hi = mid;
+// One (reference occurrence k, join item it) pair on strand `rev` ->
+// candidate key; false if the run-start rule suppresses it (the (q+1)-gram one
+// base to the left on the same diagonal also matches).
+template <bool kRunStart, bool kPacked>
+__device__ __forceinline__ bool expand(const JoinArgs& a, uint32_t k, uint64_t it, uint32_t rev, uint64_t& key) {
+  const uint32_t ov = __ldg(a.O[rev] + k);
+  const uint32_t xp = kPacked ? (ov & kPosMask) : ov;
+  if (kRunStart) {
+    const uint32_t pv = kPacked ? (ov >> kPackedPosBits) : uint32_t(__ldg(a.X[rev] + k));
+    const uint32_t rbase = uint32_t(it >> (rev ? kItemRbShift : kItemFbShift)) & 7u;
+    if (pv == rbase && rbase < 4) return false;
   }
-  const int64_t p = int64_t(x) - int64_t(__ldg(a.cb + c));
-  const int64_t d = rev ? p + int64_t(o) + int64_t(q) - int64_t(n) : p - int64_t(o);
-  const uint64_t gp = uint64_t(int64_t(__ldg(a.cbp + c)) + d);
-  key = (uint64_t(r) << (a.diag_bits + 1)) | (uint64_t(rev) << a.diag_bits) | gp;
+  const uint32_t pp = uint32_t(it);
+  const uint32_t r = a.by_m.div(pp), o = pp - r * a.m;
+  uint32_t off = o;  // forward: d = p - o
+  if (rev) off = a.tail_ok ? uint32_t(it >> kItemTailShift) & kItemTailMax : __ldg(a.rlen + r) - a.q - o;  // d = p - (n - q - o)
+  key = (uint64_t(r) << (a.diag_bits + 1)) | (uint64_t(rev) << a.diag_bits) | uint64_t(xp - off);
   return true;
 }
 
-template <bool kRunStart>
+template <bool kRunStart, bool kPacked>
 __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
-  extern __shared__ uint32_t s_words[];  // [I fwd | I rc | S fwd | S rc], a.words each
-  uint32_t* sI[2] = {s_words, s_words + a.words};
-  uint32_t* sS[2] = {s_words + 2 * a.words, s_words + 3 * a.words};
+  extern __shared__ uint32_t s_dyn[];  // I words [fwd | rc], then u16 group starts [fwd | rc]
+  const uint32_t nw = a.words;
+  uint32_t* sI = s_dyn;
+  uint16_t* sR = reinterpret_cast<uint16_t*>(s_dyn + 2 * nw);
   __shared__ uint32_t s_k0[kJoinWarps][kRanges];
-  __shared__ uint32_t s_pre[kJoinWarps][kRanges + 1];
-  __shared__ uint32_t s_pos[kJoinWarps][kRanges];  // read text position | strand << 31
+  __shared__ uint32_t s_k1[kJoinWarps][kRanges];
+  __shared__ uint16_t s_meta[kJoinWarps][kRanges];  // item slot (u*32 + lane) | strand << 15
   __shared__ uint64_t s_out[kJoinWarps][kStage];
+  __shared__ uint32_t s_ws[33];
+  __shared__ uint32_t s_split;
 
   const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
-  const unsigned q = a.q;
+  const uint32_t smask[2] = {(a.strands & 1) ? ~0u : 0u, (a.strands & 2) ? ~0u : 0u};
   uint32_t staged = 0;
   unsigned long long n_hit = 0, n_occ = 0;
 
@@ -129,24 +133,48 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
     if (staged > kStage - 32) flush();
   };
 
+  // rank prefix layout: 2*nw words, `per` consecutive words per thread (per
+  // divides nw, so no thread straddles the two strands)
+  const uint32_t per = max(1u, (2 * nw) / kJoinThreads);
+  const uint32_t my_w0 = threadIdx.x * per;
+  const bool scan_active = my_w0 < 2 * nw;
+
   for (uint32_t sb = blockIdx.x; sb < a.n_sub; sb += gridDim.x) {
     const uint32_t b0 = __ldg(a.soff + sb), b1 = __ldg(a.soff + sb + 1);
     if (b0 == b1) continue;  // CTA-uniform
     // first group word of the sub-bin (sub-bins narrower than a word share it)
     const uint32_t w0 = uint32_t((uint64_t(sb) << a.code_shift) >> 5);
-    for (uint32_t i = threadIdx.x; i < a.words; i += kJoinThreads) {
-      if (a.strands & 1) { sI[0][i] = __ldg(a.If + w0 + i); sS[0][i] = __ldg(a.Sf + w0 + i); }
-      if (a.strands & 2) { sI[1][i] = __ldg(a.Ir + w0 + i); sS[1][i] = __ldg(a.Sr + w0 + i); }
+    const uint32_t gbase[2] = {(a.strands & 1) ? __ldg(a.S[0] + w0) : 0u, (a.strands & 2) ? __ldg(a.S[1] + w0) : 0u};
+    for (uint32_t i = threadIdx.x; i < nw; i += kJoinThreads) {
+      sI[swz(i)] = (a.strands & 1) ? __ldg(a.I[0] + w0 + i) : 0u;
+      sI[swz(nw + i)] = (a.strands & 2) ? __ldg(a.I[1] + w0 + i) : 0u;
     }
-    // warm L2 with the next sub-bin's words while this one is processed
+    // warm L2 with the next sub-bin's occupancy words while this one is processed
     {
       const uint32_t nsb = sb + gridDim.x;
-      const uint32_t bytes = a.words * 4u;
-      if (nsb < a.n_sub && threadIdx.x * 128u < 4u * bytes) {
+      const uint32_t bytes = nw * 4u;
+      if (nsb < a.n_sub && threadIdx.x * 128u < 2u * bytes) {
         const uint32_t arr = (threadIdx.x * 128u) / bytes, off = (threadIdx.x * 128u) % bytes;
-        const uint32_t* src = arr == 0 ? a.If : arr == 1 ? a.Ir : arr == 2 ? a.Sf : a.Sr;
-        const char* p = reinterpret_cast<const char*>(src + uint32_t((uint64_t(nsb) << a.code_shift) >> 5)) + off;
+        const char* p = reinterpret_cast<const char*>(a.I[arr] + uint32_t((uint64_t(nsb) << a.code_shift) >> 5)) + off;
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+      }
+    }
+    __syncthreads();
+    {  // group starts on chip: exclusive popcount prefix per strand
+      uint32_t sum = 0;
+      if (scan_active)
+        for (uint32_t i = 0; i < per; ++i) sum += __popc(sI[swz(my_w0 + i)]);
+      uint32_t tot;
+      uint32_t run = block_exclusive_scan<uint32_t>(sum, s_ws, &tot);
+      if (scan_active && my_w0 == nw) s_split = run;
+      __syncthreads();
+      if (scan_active) {
+        if (my_w0 >= nw) run -= s_split;
+        for (uint32_t i = 0; i < per; ++i) {
+          const uint32_t x = swz(my_w0 + i);
+          sR[x] = uint16_t(run);
+          run += __popc(sI[x]);
+        }
       }
     }
     __syncthreads();
@@ -155,8 +183,9 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
     const uint32_t nitems = b1 - b0;
     const uint32_t my_lo = b0 + uint32_t(uint64_t(nitems) * wid / kJoinWarps);
     const uint32_t my_hi = b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kJoinWarps);
+    const uint32_t gsub = sb << a.code_shift;
     for (uint32_t base = my_lo; base < my_hi; base += 32 * kItems) {  // warp-uniform bound
-      uint32_t cnt = 0, nr = 0, rk0[kSlots], rn[kSlots], rpos[kSlots];
+      uint32_t cnt = 0, nr = 0, rk0[kSlots], rk1[kSlots];
       uint64_t pr[kItems];
 #pragma unroll
       for (int u = 0; u < kItems; ++u) {
@@ -166,22 +195,21 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
 #pragma unroll
       for (int s = 0; s < kSlots; ++s) {
         const int u = s >> 1, st = s & 1;
-        const bool ok = pr[u] != ~0ull && (a.strands & (1 << st));
-        const uint32_t g = uint32_t(pr[u] >> 32);
-        const uint32_t wl = (g >> 5) - w0, bit = g & 31u;
-        const uint32_t w = ok ? sI[st][wl] : 0u;
-        const bool hit = (w >> bit) & 1u;
-        const uint32_t b = (hit ? sS[st][wl] : 0u) + __popc(w & ((1u << bit) - 1u));
-        const uint32_t* S1 = st ? a.S1r : a.S1f;
-        rk0[s] = hit ? __ldg(S1 + b) : 0u;
-        rn[s] = hit ? __ldg(S1 + b + 1) : 0u;
-        rpos[s] = uint32_t(pr[u]) | (st ? 0x80000000u : 0u);
+        const bool ok = pr[u] != ~0ull;
+        const uint32_t g = gsub | uint32_t(pr[u] >> kItemCodeShift);
+        const uint32_t wl = ok ? (g >> 5) - w0 : 0u, bit = g & 31u;
+        const uint32_t x = swz(st * nw + wl);
+        const uint32_t w = sI[x] & smask[st];
+        const bool hit = ok && ((w >> bit) & 1u);
+        const uint32_t b = gbase[st] + sR[x] + __popc(w & ((1u << bit) - 1u));
+        rk0[s] = hit ? __ldg(a.S1[st] + b) : 0u;
+        rk1[s] = hit ? __ldg(a.S1[st] + b + 1) : 0u;
       }
 #pragma unroll
       for (int s = 0; s < kSlots; ++s) {
-        rn[s] -= rk0[s];
-        cnt += rn[s];
-        nr += rn[s] != 0;
+        const uint32_t len = rk1[s] - rk0[s];
+        cnt += len;
+        nr += len != 0;
       }
       n_hit += nr;
       n_occ += cnt;
@@ -190,13 +218,13 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
       uint32_t nent = 0;
 #pragma unroll
       for (int s = 0; s < kSlots; ++s) {
-        const bool has = rn[s] != 0;
+        const bool has = rk1[s] != rk0[s];
         const unsigned bm = __ballot_sync(kFull, has);
         if (has) {
           const uint32_t e = nent + __popc(bm & lanemask_lt());
           s_k0[wid][e] = rk0[s];
-          s_pre[wid][e] = rn[s];
-          s_pos[wid][e] = rpos[s];
+          s_k1[wid][e] = rk1[s];
+          s_meta[wid][e] = uint16_t(((s >> 1) * 32 + lane) | ((s & 1) << 15));
         }
         nent += __popc(bm);
       }
@@ -206,18 +234,20 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
       // (repeats) by the whole warp, one interval at a time
       for (uint32_t e0 = 0; e0 < nent; e0 += 32) {
         const uint32_t e = e0 + lane;
-        uint32_t k0 = 0, len = 0, pw = 0;
+        uint32_t k0 = 0, len = 0, meta = 0;
         if (e < nent) {
           k0 = s_k0[wid][e];
-          len = s_pre[wid][e];
-          pw = s_pos[wid][e];
+          len = s_k1[wid][e] - k0;
+          meta = s_meta[wid][e];
         }
+        const uint64_t it = e < nent ? __ldg(a.items + base + (meta & 0x7FFFu)) : 0ull;
+        const uint32_t rev = meta >> 15;
         const bool longi = len > kInline;
         const uint32_t nin = longi ? 0u : len;
         const uint32_t rounds = __reduce_max_sync(kFull, nin);
         for (uint32_t t = 0; t < rounds; ++t) {
           uint64_t key = 0;
-          const bool emit = t < nin && expand<kRunStart>(a, q, k0 + t, pw, key);
+          const bool emit = t < nin && expand<kRunStart, kPacked>(a, k0 + t, it, rev, key);
           stage_key(emit, key);
         }
         unsigned lm = __ballot_sync(kFull, longi);
@@ -225,10 +255,11 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
           const int src = __ffs(lm) - 1;
           lm &= lm - 1;
           const uint32_t lk0 = __shfl_sync(kFull, k0, src), llen = __shfl_sync(kFull, len, src);
-          const uint32_t lpw = __shfl_sync(kFull, pw, src);
+          const uint64_t lit = __shfl_sync(kFull, it, src);
+          const uint32_t lrev = __shfl_sync(kFull, rev, src);
           for (uint32_t t0 = 0; t0 < llen; t0 += 32) {
             uint64_t key = 0;
-            const bool emit = t0 + lane < llen && expand<kRunStart>(a, q, lk0 + t0 + lane, lpw, key);
+            const bool emit = t0 + lane < llen && expand<kRunStart, kPacked>(a, lk0 + t0 + lane, lit, lrev, key);
             stage_key(emit, key);
           }
         }
@@ -262,32 +293,29 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   a.words = std::max<uint32_t>(1, (1u << a.code_shift) / 32);
   if (a.words > kMaxWords) throw InternalError("join: sub-bin wider than the shared staging");
   a.q = rp.q;
-  a.If = reinterpret_cast<const uint32_t*>(X.fwd.I.p);
-  a.Sf = X.fwd.S.p;
-  a.S1f = X.fwd.S1.p;
-  a.Of = X.fwd.O.p;
-  a.Xf = X.prev_fwd.p;
-  a.Ir = reinterpret_cast<const uint32_t*>(X.rc.I.p);
-  a.Sr = X.rc.S.p;
-  a.S1r = X.rc.S1.p;
-  a.Or = X.rc.O.p;
-  a.Xr = X.prev_rc.p;
-  a.rwords = reads.words.p;
+  const Index* ix[2] = {&X.fwd, &X.rc};
+  for (int st = 0; st < 2; ++st) {
+    a.I[st] = reinterpret_cast<const uint32_t*>(ix[st]->I.p);
+    a.S[st] = ix[st]->S.p;
+    a.S1[st] = ix[st]->S1.p;
+    a.O[st] = ix[st]->O.p;
+  }
+  a.X[0] = X.prev_fwd.p;
+  a.X[1] = X.prev_rc.p;
   a.rlen = reads.lengths.p;
-  a.W = reads.W;
   a.m = reads.stride;
   a.by_m = FastDiv(std::max<uint32_t>(reads.stride, 1));
-  a.cb = ref.d_cb.p;
-  a.cbp = ref.d_cbp.p;
-  a.n_chrom = ref.n_chrom;
+  a.tail_ok = reads.stride < rp.q + kItemTailMax;
   a.strands = strands;
   a.diag_bits = ref.diag_bits;
   DBuf<unsigned long long> counter(c, 3);
   a.counter = counter.p;
   a.stats = counter.p + 1;
   if (keys.n == 0) keys.alloc(c, std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16));
-  const void* kfn = mode == 1 ? (const void*)k_join<true> : (const void*)k_join<false>;
-  const size_t smem = size_t(4) * a.words * sizeof(uint32_t);
+  const bool rs = mode == 1;
+  const void* kfn = X.packed ? (rs ? (const void*)k_join<true, true> : (const void*)k_join<false, true>)
+                             : (rs ? (const void*)k_join<true, false> : (const void*)k_join<false, false>);
+  const size_t smem = size_t(2) * a.words * (sizeof(uint32_t) + sizeof(uint16_t));
   QGM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const unsigned grid = std::min<unsigned>(a.n_sub, resident_grid(kfn, kJoinThreads, smem));
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -296,8 +324,9 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
     a.cap = keys.n;
     if (rp.V > 0) {
       KernelScope ks(c, "k_join");
-      if (mode == 1) QGM_KERNEL(c, k_join<true>, grid, kJoinThreads, smem, a);
-      else QGM_KERNEL(c, k_join<false>, grid, kJoinThreads, smem, a);
+      void* args[] = {&a};
+      QGM_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(kJoinThreads), args, smem, c.stream));
+      ++c.launches;
     }
     unsigned long long h[3] = {0, 0, 0};
     QGM_CUDA(cudaMemcpyAsync(h, counter.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));

@@ -16,7 +16,10 @@
 // ncu on the previous single-pass scatter (12-bit bins, items written
 // straight from registers) showed 1.6 GB of read-for-ownership and 2.1 GB of
 // writes for 0.68 GB of output: partial sectors of 2.4M concurrently open runs.
-// Item = (full code << 32) | text position (r*stride + o), 8 bytes.
+// First-pass item = (full code << 32) | text position (r*stride + o), 8 bytes;
+// the refinement pass writes the final join items (internal.hpp: position,
+// tail, the two run-start compare bases, the code bits below the sub-bin), so
+// the join never touches the read text.
 #include "internal.hpp"
 
 namespace qgm {
@@ -117,6 +120,29 @@ constexpr uint32_t kLocal = 2048;
 
 __device__ __forceinline__ uint32_t key_of(uint64_t it, unsigned kshift) { return uint32_t(it >> 32) >> kshift; }
 
+// first-pass item -> join item (layout in internal.hpp). The read words and
+// lengths are L2-resident; consecutive items of a chunk come from ascending
+// reads.
+struct ItemConv {
+  const uint64_t* words;
+  const uint32_t* lengths;
+  uint32_t W, stride;
+  FastDiv by_stride;
+  unsigned q;
+  uint32_t lmask;  // code bits below the sub-bin prefix
+  __device__ __forceinline__ uint64_t operator()(uint64_t it) const {
+    const uint32_t pp = uint32_t(it), g = uint32_t(it >> 32);
+    const uint32_t r = by_stride.div(pp), o = pp - r * stride;
+    const uint32_t n = __ldg(lengths + r);
+    const uint64_t* w = words + uint64_t(r) * W;
+    const uint32_t fb = o ? base_at(w, o - 1) : 4u;
+    const uint32_t rb = o + q < n ? base_at(w, o + q) : 4u;
+    const uint32_t tail = min(n - q - o, kItemTailMax);
+    return (uint64_t(g & lmask) << kItemCodeShift) | (uint64_t(rb) << kItemRbShift) |
+           (uint64_t(fb) << kItemFbShift) | (uint64_t(tail) << kItemTailShift) | pp;
+  }
+};
+
 __global__ void __launch_bounds__(kPartThreads) k_refine_hist(const uint64_t* __restrict__ in, uint32_t n,
                                                               unsigned kshift, unsigned sub,
                                                               uint32_t* __restrict__ hist) {
@@ -140,12 +166,13 @@ __global__ void __launch_bounds__(kPartThreads) k_refine_hist(const uint64_t* __
   }
 }
 
-__global__ void __launch_bounds__(kPartThreads, 4) k_refine_scatter(const uint64_t* __restrict__ in, uint32_t n,
+__global__ void __launch_bounds__(kPartThreads, 2) k_refine_scatter(const uint64_t* __restrict__ in, uint32_t n,
                                                                     unsigned kshift, unsigned sub,
                                                                     const uint32_t* __restrict__ off,
                                                                     uint32_t* __restrict__ cursor,
-                                                                    uint64_t* __restrict__ out) {
-  extern __shared__ uint64_t stage[];
+                                                                    ItemConv conv, uint64_t* __restrict__ out) {
+  extern __shared__ uint64_t stage[];  // kChunk converted items, then kChunk u16 window keys
+  uint16_t* skey = reinterpret_cast<uint16_t*>(stage + kChunk);
   __shared__ uint32_t cnt[kLocal], lofs[kLocal], gdst[kLocal];
   __shared__ uint32_t ws[33];
   const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
@@ -157,18 +184,23 @@ __global__ void __launch_bounds__(kPartThreads, 4) k_refine_scatter(const uint64
       for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) {
         const uint64_t it = in[i];
         const uint32_t k = key_of(it, kshift);
-        out[off[k] + atomicAdd(cursor + k, 1u)] = it;
+        out[off[k] + atomicAdd(cursor + k, 1u)] = conv(it);
       }
       continue;
     }
     for (uint32_t b = threadIdx.x; b < width; b += kPartThreads) cnt[b] = 0;
     __syncthreads();
+    // convert on load: consecutive first-pass items come from the same few
+    // reads, so the read-word / length loads of a warp hit the same lines
     uint64_t v[kPer];
+    uint32_t kk[kPer];
 #pragma unroll
     for (uint32_t k = 0; k < kPer; ++k) {
       const uint32_t i = c0 + k * kPartThreads + threadIdx.x;
-      v[k] = i < c1 ? in[i] : ~0ull;
-      if (i < c1) atomicAdd(cnt + key_of(v[k], kshift) - base, 1u);
+      const uint64_t it = i < c1 ? in[i] : 0ull;
+      kk[k] = i < c1 ? key_of(it, kshift) - base : ~0u;
+      v[k] = i < c1 ? conv(it) : 0ull;
+      if (i < c1) atomicAdd(cnt + kk[k], 1u);
     }
     __syncthreads();
     // exclusive scan of cnt[0, width): each thread owns a contiguous run
@@ -188,12 +220,15 @@ __global__ void __launch_bounds__(kPartThreads, 4) k_refine_scatter(const uint64
     __syncthreads();
 #pragma unroll
     for (uint32_t k = 0; k < kPer; ++k)
-      if (v[k] != ~0ull) stage[atomicAdd(cnt + key_of(v[k], kshift) - base, 1u)] = v[k];
+      if (kk[k] != ~0u) {
+        const uint32_t slot = atomicAdd(cnt + kk[k], 1u);
+        stage[slot] = v[k];
+        skey[slot] = uint16_t(kk[k]);
+      }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < c1 - c0; i += kPartThreads) {
-      const uint64_t it = stage[i];
-      const uint32_t b = key_of(it, kshift) - base;
-      out[gdst[b] + (i - lofs[b])] = it;
+      const uint32_t b = skey[i];
+      out[gdst[b] + (i - lofs[b])] = stage[i];
     }
     __syncthreads();
   }
@@ -242,24 +277,21 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   out.pairs.alloc(c, std::max<uint64_t>(V, 1));
   hist.zero();  // reused as the per-bin global cursors
   const size_t smem = kChunk * sizeof(uint64_t);
-  static bool attr = false;
-  if (!attr) {
-    QGM_CUDA(cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
+  QGM_CUDA(cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n_items, kChunk), uint64_t(kSMs) * 4));
   {
     KernelScope ks(c, "k_part_scatter");
     QGM_KERNEL(c, k_part_scatter, grid, kPartThreads, smem, gen, n_items, shift, out.boff.p, hist.p, out.pairs.p);
   }
   // P2: refine to the top min(2q, 16) code bits (short reuse distance of the
-  // reference-index sectors in the join)
+  // reference-index sectors in the join) and convert to join items. Runs even
+  // when the first pass already grouped by every key bit (2q <= 8): then it
+  // only converts.
   const unsigned key_bits = std::min(2 * q, 16u);
   out.sub_bits = key_bits;
-  if (key_bits <= bits || V == 0) {  // the first pass already grouped by every code bit (2q <= 8)
-    out.soff.alloc(c, kBins + 1);
-    QGM_CUDA(cudaMemcpyAsync(out.soff.p, out.boff.p, (kBins + 1) * 4, cudaMemcpyDeviceToDevice, c.stream));
-    out.sub_bits = bits;
+  if (V == 0) {  // every read shorter than q
+    out.soff.alloc(c, (1u << key_bits) + 1);
+    out.soff.zero();
     return;
   }
   const unsigned kshift = 2 * q - key_bits, sub = key_bits - bits;
@@ -276,14 +308,19 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   exclusive_scan_u32(c, h2.p, off.p, keys + 1, nullptr, nullptr);
   h2.zero();  // per-key cursors
   DBuf<uint64_t> refined(c, std::max<uint64_t>(V, 1));
-  static bool attr2 = false;
-  if (!attr2) {
-    QGM_CUDA(cudaFuncSetAttribute(k_refine_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr2 = true;
-  }
+  const size_t smem2 = kChunk * (sizeof(uint64_t) + sizeof(uint16_t));
+  QGM_CUDA(cudaFuncSetAttribute(k_refine_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+  ItemConv conv;
+  conv.words = reads.words.p;
+  conv.lengths = reads.lengths.p;
+  conv.W = reads.W;
+  conv.stride = reads.stride;
+  conv.by_stride = FastDiv(std::max<uint32_t>(reads.stride, 1));
+  conv.q = q;
+  conv.lmask = kshift ? (1u << kshift) - 1u : 0u;
   {
     KernelScope ks(c, "k_refine_scatter");
-    QGM_KERNEL(c, k_refine_scatter, grid2, kPartThreads, smem, out.pairs.p, V, kshift, sub, off.p, h2.p,
+    QGM_KERNEL(c, k_refine_scatter, grid2, kPartThreads, smem2, out.pairs.p, V, kshift, sub, off.p, h2.p, conv,
                refined.p);
   }
   out.pairs.swap(refined);

@@ -61,8 +61,14 @@ def test_c1_full_size_matches_oracle(ctx, oracle, mode, q):
         assert mapped.mean() > 0.97
 
 
-def test_repetitive_reference_and_mask_match_oracle(ctx, oracle):
+@pytest.mark.parametrize("unpacked", [False, True])
+def test_repetitive_reference_and_mask_match_oracle(ctx, oracle, monkeypatch, unpacked):
+    """Repeats (long occurrence intervals, warp-cooperative expansion), two
+    chromosomes, a repeat mask; both reference-index layouts (compare base
+    packed into O, or the separate byte array used above 2^29 padded bases)."""
     import paper_1403_1706_b200 as qgm
+    if unpacked:
+        monkeypatch.setenv("QGM_REF_UNPACKED", "1")
     L = 300_000
     ref = qgm.repetitive_reference(5, L)
     cb = np.array([0, 100_000, L], np.uint64)
