@@ -56,41 +56,52 @@ struct ReadSource {
   }
 };
 
-// Reference positions of one strand: every global position whose window lies
-// inside its chromosome and is not masked. The code is the
-// forward q-gram, or the code of its reverse complement for the RC strand.
-// pos = the padded coordinate cbp[c] + p (RefQIndex); extra = the base the
-// run-start rule compares (ref[p-1], or its complement on the RC strand), or 4
-// when p-1 is outside the chromosome or masked. With `packed`, extra goes into
-// pos's top 3 bits instead.
+// Reference positions under canonical codes (RefQIndex): source index t < L
+// is position t; t >= L is the palindromic position pal[t - L], listed a
+// second time with flag 1. A position is indexed iff its window lies inside
+// its chromosome and it is not masked.
+// pos = the padded coordinate cbp[c] + p; extra = b | flag << 3, b = ref[x-1]
+// or 4 when x-1 is outside the chromosome or masked; with `packed`, extra
+// goes into pos's top 4 bits.
+__device__ __forceinline__ uint32_t canon_code(uint32_t g, unsigned q) { return min(g, rc_code(g, q)); }
+
 struct RefSource {
   const uint64_t* ref;
   const uint64_t* mask;
   const uint64_t* cb;
+  const uint64_t* pal;
+  uint64_t L;
   uint32_t n_chrom;
   unsigned q;
-  bool rc, packed;
+  bool packed;
   uint64_t gap;
   __device__ __forceinline__ bool masked(uint64_t x) const {
     return mask && ((__ldg(mask + (x >> 6)) >> (x & 63)) & 1ull);
   }
-  __device__ __forceinline__ bool item(uint64_t x, uint32_t& g, uint32_t& pos, uint32_t& extra) const {
+  // window of x inside its chromosome and unmasked; returns the chromosome
+  __device__ __forceinline__ bool indexed(uint64_t x, uint32_t& chrom, uint64_t& p) const {
     if (masked(x)) return false;
     uint32_t lo = 0, hi = n_chrom;
     while (hi - lo > 1) {
       const uint32_t mid = (lo + hi) >> 1;
       if (__ldg(cb + mid) <= x) lo = mid; else hi = mid;
     }
-    const uint64_t cbeg = __ldg(cb + lo), p = x - cbeg;
-    if (p + q > __ldg(cb + lo + 1) - cbeg) return false;
-    g = qgram_at(ref, x, q);
-    if (rc) g = rc_code(g, q);
-    pos = uint32_t(x + uint64_t(lo + 1) * gap);
-    extra = 4;
-    if (p >= 1 && !masked(x - 1)) {
-      const uint32_t b = base_at(ref, x - 1);
-      extra = rc ? 3u - b : b;
-    }
+    const uint64_t cbeg = __ldg(cb + lo);
+    p = x - cbeg;
+    chrom = lo;
+    return p + q <= __ldg(cb + lo + 1) - cbeg;
+  }
+  __device__ __forceinline__ bool item(uint64_t t, uint32_t& g, uint32_t& pos, uint32_t& extra) const {
+    const bool dup = t >= L;
+    const uint64_t x = dup ? __ldg(pal + (t - L)) : t;
+    uint32_t c;
+    uint64_t p;
+    if (!indexed(x, c, p)) return false;
+    const uint32_t f = qgram_at(ref, x, q);
+    g = canon_code(f, q);
+    pos = uint32_t(x + uint64_t(c + 1) * gap);
+    const uint32_t b = (p >= 1 && !masked(x - 1)) ? base_at(ref, x - 1) : 4u;
+    extra = b | (uint32_t(dup || f != g) << 3);
     if (packed) {
       pos |= extra << kPackedPosBits;
       extra = 0;
@@ -99,6 +110,23 @@ struct RefSource {
   }
 };
 
+// Palindromic indexed positions (f == rc(f); even q only): count, then list.
+__global__ void k_pal_scan(RefSource src, uint64_t* __restrict__ out, unsigned long long* __restrict__ count) {
+  for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < src.L; base += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t x = base + threadIdx.x;
+    uint32_t c;
+    uint64_t p;
+    bool pal = false;
+    if (x < src.L && src.indexed(x, c, p)) {
+      const uint32_t f = qgram_at(src.ref, x, src.q);
+      pal = f == rc_code(f, src.q);
+    }
+    const unsigned long long slot = warp_append(pal, count);
+    if (pal && out) out[slot] = x;
+  }
+}
+
+// bucketed item: extra (4 bits) << 45 | low code bits (13) << 32 | pos
 __device__ __forceinline__ uint64_t pack_item(uint32_t extra, uint32_t glow, uint32_t pos) {
   return (uint64_t(extra) << 45) | (uint64_t(glow) << 32) | pos;
 }
@@ -382,19 +410,37 @@ void bucket_reads(Ctx& c, const Reads& reads, unsigned q, unsigned w, Buckets& o
   bucket_impl(c, src, uint64_t(reads.n) * src.span, out);
 }
 
-void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool rc, bool packed, Buckets& out) {
+void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool packed, Buckets& out, uint64_t* n_pal) {
   init_geometry(out, q, 32);
   if (ref.padded_total >= (uint64_t(1) << 32)) throw InputError("reference index: more than 2^32-1 padded bases");
   RefSource src;
   src.ref = ref.words.p;
   src.mask = ref.mask.p;
   src.cb = ref.d_cb.p;
+  src.pal = nullptr;
+  src.L = ref.total;
   src.n_chrom = ref.n_chrom;
   src.q = q;
-  src.rc = rc;
   src.packed = packed;
   src.gap = ref.gap;
-  bucket_impl(c, src, ref.total, out);
+  DBuf<uint64_t> pal;
+  unsigned long long np = 0;
+  if (q % 2 == 0 && ref.total) {
+    DBuf<unsigned long long> cnt(c, 1);
+    cnt.zero();
+    const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(ref.total, 256), kSMs * 32));
+    QGM_KERNEL(c, k_pal_scan, grid, 256, 0, src, nullptr, cnt.p);
+    QGM_CUDA(cudaMemcpyAsync(&np, cnt.p, sizeof(np), cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    if (np) {
+      pal.alloc(c, np);
+      cnt.zero();
+      QGM_KERNEL(c, k_pal_scan, grid, 256, 0, src, pal.p, cnt.p);
+      src.pal = pal.p;
+    }
+  }
+  *n_pal = np;
+  bucket_impl(c, src, ref.total + np, out);
 }
 
 void index_from_buckets(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_t>* extra) {
@@ -413,17 +459,16 @@ void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sample
 void prepare_ref_index(Ctx& c, const Ref& ref, unsigned q) {
   if (ref.qidx.q == q) return;
   ref.qidx = RefQIndex();
-  // QGM_REF_UNPACKED=1 forces the separate compare-base array (test knob: the
-  // packed layout covers every reference below 2^29 padded bases)
+  // QGM_REF_UNPACKED=1 forces the separate extra-byte array (test knob: the
+  // packed layout covers every reference below 2^28 padded bases)
   const char* force = std::getenv("QGM_REF_UNPACKED");
   const bool packed = ref.padded_total < (uint64_t(1) << kPackedPosBits) && !(force && force[0] == '1');
-  for (int rc = 0; rc < 2; ++rc) {
-    Buckets B;
-    bucket_ref(c, ref, q, rc != 0, packed, B);
-    DBuf<uint8_t>* prev = packed ? nullptr : (rc ? &ref.qidx.prev_rc : &ref.qidx.prev_fwd);
-    index_from_buckets(c, B, false, rc ? ref.qidx.rc : ref.qidx.fwd, prev);
-  }
+  Buckets B;
+  uint64_t n_pal = 0;
+  bucket_ref(c, ref, q, packed, B, &n_pal);
+  index_from_buckets(c, B, false, ref.qidx.can, packed ? nullptr : &ref.qidx.extra);
   ref.qidx.packed = packed;
+  ref.qidx.palindromes = n_pal;
   ref.qidx.q = q;
 }
 

@@ -175,22 +175,27 @@ struct Buckets {
   DBuf<uint64_t> pairs;
 };
 
-// q-group indexes over the reference itself, one per strand (the RC index is
-// keyed by the code of the reverse-complemented window), with the base the
-// run-start rule compares stored next to every position (4 = none). Built
-// once per reference and q (SPEC.md:262-316's precomputed reference index,
-// with P ordered by q-gram as in PAPER.md:344).
-// O holds padded coordinates (chromosome c's position p -> cbp[c] + p), so a
-// candidate diagonal is O - offset with no chromosome search. When the padded
-// reference is < 2^29 the compared base is packed into O's top 3 bits
-// (packed = true, prev_* empty); otherwise it is a separate byte array.
+// q-group index over the reference itself, keyed by CANONICAL q-gram codes
+// (min(code, rc(code)); SPEC.md:262-316's precomputed reference index with P
+// ordered by q-gram as in PAPER.md:344, both strands in one index). Every
+// position x is listed under the canonical code of its forward window with
+// flag = (forward code != canonical); a position whose q-gram is its own
+// reverse complement (even q only) is listed twice, with flag 0 and 1. A read
+// q-gram with code g looks up canon(g) once: an occurrence matches the
+// forward strand iff flag == (g != canon(g)), else the reverse strand.
+// Per occurrence: O = padded coordinate cbp[c] + p (the candidate diagonal is
+// O - offset, no chromosome search) and extra = b | flag << 3 with b =
+// ref[x-1] (4 = none: chromosome start or masked), the base the run-start
+// rule compares. When the padded reference is < 2^28, extra is packed into
+// O's top 4 bits (packed = true, `extra` empty).
 struct RefQIndex {
   unsigned q = 0;
   bool packed = false;
-  Index fwd, rc;
-  DBuf<uint8_t> prev_fwd, prev_rc;
+  uint64_t palindromes = 0;  // positions listed twice
+  Index can;
+  DBuf<uint8_t> extra;
 };
-constexpr unsigned kPackedPosBits = 29;
+constexpr unsigned kPackedPosBits = 28;
 
 // Reference sequences (ReferenceIndex): the concatenated
 // chromosomes in 2-bit (+1 guard word) and as lo/hi bit planes (2 guard words
@@ -251,7 +256,7 @@ void make_ref_planes(Ctx& c, Ref& ref);
 
 // index_build.cu
 void bucket_reads(Ctx& c, const Reads& reads, unsigned q, unsigned w, Buckets& out);
-void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool rc, bool packed, Buckets& out);
+void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool packed, Buckets& out, uint64_t* n_pal);
 void index_from_buckets(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_t>* extra);
 void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sampled, Index& out);
 void prepare_ref_index(Ctx& c, const Ref& ref, unsigned q);
@@ -267,15 +272,17 @@ uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Re
                           unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats = nullptr);
 
 // partition.cu -- the batch's read q-grams grouped by the top min(2q,16)
-// bits of their code (sub-bins), one 64-bit join item each:
+// bits of their CANONICAL code (sub-bins), one 64-bit join item each:
 //   bits  0..31  read text position pp = r * stride + o
-//   bits 32..41  tail = n_r - q - o (clamped to 1023; the join reloads n_r when
-//                stride - q > 1023)
-//   bits 42..44  read base at o - 1 (forward run-start compare), 4 = none
-//   bits 45..47  read base at o + q (RC run-start compare), 4 = none
-//   bits 48..63  the code bits below the sub-bin prefix
-constexpr unsigned kItemTailShift = 32, kItemFbShift = 42, kItemRbShift = 45, kItemCodeShift = 48;
-constexpr uint32_t kItemTailMax = 1023;
+//   bits 32..40  tail = n_r - q - o (clamped to 511; the join reloads n_r when
+//                stride - q > 511)
+//   bits 41..43  read base at o - 1 (forward run-start compare), 4 = none
+//   bits 44..46  complement of the read base at o + q (reverse run-start
+//                compare), 4 = none
+//   bit  47      fr = (read code != canonical code)
+//   bits 48..63  the canonical code bits below the sub-bin prefix
+constexpr unsigned kItemTailShift = 32, kItemFbShift = 41, kItemRbShift = 44, kItemFrShift = 47, kItemCodeShift = 48;
+constexpr uint32_t kItemTailMax = 511;
 struct Partitioned {
   unsigned q = 0;
   uint32_t bins = 0, V = 0;

@@ -13,25 +13,28 @@
 // with P ordered by q-gram), one per strand, and the batch's read
 // q-grams are partitioned by the top 16 bits of their code (partition.cu).
 //
-// One CTA owns one code sub-bin at a time (2^(2q-16) codes; 2048 group words
-// per strand at q=16): it stages the sub-bin's occupancy words of both
-// reference strands in shared memory with one coalesced load and rebuilds the
-// group starts on chip (popcount prefix, u16 relative to S at the sub-bin's
-// first word -- one global S read per sub-bin and strand), so all
-// Group-And-Bit / Grouprank lookups (qgroup_index.hpp:50-57, 80-96) of the
-// sub-bin's read q-grams are shared-memory hits. The S' / O reads that follow
-// fall in the sub-bin's contiguous slice of the reference index and are L1/L2
-// local to the CTA. The occupancy array is read from HBM exactly once per
-// batch, in order; S is not read at all.
+// Both strands come from ONE lookup per read q-gram: the reference index and
+// the read partition are keyed by canonical codes min(g, rc(g)) (RefQIndex),
+// and each occurrence's strand is flag(occurrence) XOR fr(read q-gram).
 //
-// Per warp step: up to 4 read q-grams per lane, both strands looked up, then
-// the union of the occurrence intervals expanded cooperatively, one
-// (reference occurrence, read occurrence) pair per lane. Everything the
-// expansion needs travels in the join item (partition.cu) or in O: O holds the
-// padded coordinate of the occurrence (so the diagonal is O - offset, no
-// chromosome search) and -- for references below 2^29 padded bases -- the
-// base the run-start rule compares in its top 3 bits; the item holds the
-// read's own compare bases (o-1 forward, o+q RC) and n - q - o.
+// One CTA owns one code sub-bin at a time (2^(2q-16) codes; 2048 group words
+// at q=16): it stages the sub-bin's occupancy words in shared memory with one
+// coalesced load and rebuilds the group starts on chip (popcount prefix, u16
+// relative to S at the sub-bin's first word -- one global S read per
+// sub-bin), so every Group-And-Bit / Grouprank lookup (qgroup_index.hpp:50-57,
+// 80-96) of the sub-bin's read q-grams is a shared-memory hit. The S' / O
+// reads that follow fall in the sub-bin's contiguous slice of the reference
+// index and are L1/L2 local to the CTA. The occupancy array is read from HBM
+// exactly once per batch, in order; S is not read at all.
+//
+// Per warp step: kItems read q-grams per lane looked up, then the union of the
+// occurrence intervals expanded cooperatively, one (reference occurrence,
+// read occurrence) pair per lane. Everything the expansion needs travels in
+// the join item (partition.cu) or in O: O holds the padded coordinate of the
+// occurrence (the diagonal is O - offset, no chromosome search) and -- for
+// references below 2^28 padded bases -- the strand flag and the base the
+// run-start rule compares in its top 4 bits; the item holds the read's own
+// compare bases (o-1 forward, complement of o+q reverse) and n - q - o.
 #include "internal.hpp"
 
 namespace qgm {
@@ -42,19 +45,17 @@ constexpr int kJoinWarps = kJoinThreads / 32;
 #ifndef QGM_JOIN_ITEMS
 #define QGM_JOIN_ITEMS 4
 #endif
-constexpr int kItems = QGM_JOIN_ITEMS;    // read q-grams per lane per step
-constexpr int kSlots = 2 * kItems;        // (item, strand) lookups per lane
-constexpr int kRanges = 32 * kSlots;
-constexpr int kStage = 128;               // staged keys per warp
+constexpr int kItems = QGM_JOIN_ITEMS;    // read q-grams (= lookups) per lane per step
+constexpr int kRanges = 32 * kItems;
+constexpr int kStage = 64;                // staged keys per warp
 constexpr uint32_t kInline = 4;           // intervals up to this length are expanded in-lane
-constexpr uint32_t kMaxWords = 2048;      // group words per sub-bin and strand (q = 16)
+constexpr uint32_t kMaxWords = 2048;      // group words per sub-bin (q = 16)
 constexpr uint32_t kPosMask = (1u << kPackedPosBits) - 1u;
 
 // Shared-memory swizzle of the staged words: thread t of the group-start scan
-// reads words t*per .. t*per+per-1 (per = 16 at q=16), which would put 16
-// lanes of a warp on one bank; XOR-ing the low 4 index bits with the 32-word
-// row number makes every step of that scan (u32 words and u16 starts alike)
-// conflict-free. Lookups pay one shift/and/xor.
+// reads words t*per .. t*per+per-1, which would put up to 16 lanes of a warp
+// on one bank; XOR-ing the low 4 index bits with the 32-word row number makes
+// every step of that scan (u32 words and u16 starts alike) conflict-free.
 __device__ __forceinline__ uint32_t swz(uint32_t w) { return w ^ ((w >> 5) & 15u); }
 
 struct JoinArgs {
@@ -64,8 +65,8 @@ struct JoinArgs {
   unsigned code_shift;  // sub-bin = code >> code_shift
   uint32_t words;       // group words per sub-bin (>= 1)
   unsigned q;
-  const uint32_t *I[2], *S[2], *S1[2], *O[2];
-  const uint8_t* X[2];  // compared base per occurrence (unpacked layout only)
+  const uint32_t *I, *S, *S1, *O;
+  const uint8_t* X;  // extra byte per occurrence (unpacked layout only)
   const uint32_t* rlen;
   uint32_t m;
   FastDiv by_m;
@@ -78,17 +79,19 @@ struct JoinArgs {
   unsigned long long* stats;
 };
 
-// One (reference occurrence k, join item it) pair on strand `rev` ->
-// candidate key; false if the run-start rule suppresses it (the (q+1)-gram one
-// base to the left on the same diagonal also matches).
+// One (reference occurrence k, join item it) pair -> candidate key; false if
+// its strand is not requested or the run-start rule suppresses it (the
+// (q+1)-gram one base to the left on the same diagonal also matches).
 template <bool kRunStart, bool kPacked>
-__device__ __forceinline__ bool expand(const JoinArgs& a, uint32_t k, uint64_t it, uint32_t rev, uint64_t& key) {
-  const uint32_t ov = __ldg(a.O[rev] + k);
+__device__ __forceinline__ bool expand(const JoinArgs& a, uint32_t k, uint64_t it, uint64_t& key) {
+  const uint32_t ov = __ldg(a.O + k);
   const uint32_t xp = kPacked ? (ov & kPosMask) : ov;
+  const uint32_t ex = kPacked ? (ov >> kPackedPosBits) : uint32_t(__ldg(a.X + k));
+  const uint32_t rev = ((ex >> 3) ^ uint32_t(it >> kItemFrShift)) & 1u;
+  if (!((a.strands >> rev) & 1)) return false;
   if (kRunStart) {
-    const uint32_t pv = kPacked ? (ov >> kPackedPosBits) : uint32_t(__ldg(a.X[rev] + k));
     const uint32_t rbase = uint32_t(it >> (rev ? kItemRbShift : kItemFbShift)) & 7u;
-    if (pv == rbase && rbase < 4) return false;
+    if ((ex & 7u) == rbase && rbase < 4) return false;
   }
   const uint32_t pp = uint32_t(it);
   const uint32_t r = a.by_m.div(pp), o = pp - r * a.m;
@@ -100,19 +103,17 @@ __device__ __forceinline__ bool expand(const JoinArgs& a, uint32_t k, uint64_t i
 
 template <bool kRunStart, bool kPacked>
 __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
-  extern __shared__ uint32_t s_dyn[];  // I words [fwd | rc], then u16 group starts [fwd | rc]
+  extern __shared__ uint32_t s_dyn[];  // I words, then u16 group starts
   const uint32_t nw = a.words;
   uint32_t* sI = s_dyn;
-  uint16_t* sR = reinterpret_cast<uint16_t*>(s_dyn + 2 * nw);
+  uint16_t* sR = reinterpret_cast<uint16_t*>(s_dyn + nw);
   __shared__ uint32_t s_k0[kJoinWarps][kRanges];
   __shared__ uint32_t s_k1[kJoinWarps][kRanges];
-  __shared__ uint16_t s_meta[kJoinWarps][kRanges];  // item slot (u*32 + lane) | strand << 15
+  __shared__ uint8_t s_slot[kJoinWarps][kRanges];  // item slot u*32 + lane
   __shared__ uint64_t s_out[kJoinWarps][kStage];
   __shared__ uint32_t s_ws[33];
-  __shared__ uint32_t s_split;
 
   const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
-  const uint32_t smask[2] = {(a.strands & 1) ? ~0u : 0u, (a.strands & 2) ? ~0u : 0u};
   uint32_t staged = 0;
   unsigned long long n_hit = 0, n_occ = 0;
 
@@ -133,49 +134,39 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
     if (staged > kStage - 32) flush();
   };
 
-  // rank prefix layout: 2*nw words, `per` consecutive words per thread (per
-  // divides nw, so no thread straddles the two strands)
-  const uint32_t per = max(1u, (2 * nw) / kJoinThreads);
+  // group-start scan: `per` consecutive words per thread
+  const uint32_t per = max(1u, nw / kJoinThreads);
   const uint32_t my_w0 = threadIdx.x * per;
-  const bool scan_active = my_w0 < 2 * nw;
+  const bool scan_active = my_w0 < nw;
 
   for (uint32_t sb = blockIdx.x; sb < a.n_sub; sb += gridDim.x) {
     const uint32_t b0 = __ldg(a.soff + sb), b1 = __ldg(a.soff + sb + 1);
     if (b0 == b1) continue;  // CTA-uniform
     // first group word of the sub-bin (sub-bins narrower than a word share it)
     const uint32_t w0 = uint32_t((uint64_t(sb) << a.code_shift) >> 5);
-    const uint32_t gbase[2] = {(a.strands & 1) ? __ldg(a.S[0] + w0) : 0u, (a.strands & 2) ? __ldg(a.S[1] + w0) : 0u};
-    for (uint32_t i = threadIdx.x; i < nw; i += kJoinThreads) {
-      sI[swz(i)] = (a.strands & 1) ? __ldg(a.I[0] + w0 + i) : 0u;
-      sI[swz(nw + i)] = (a.strands & 2) ? __ldg(a.I[1] + w0 + i) : 0u;
-    }
+    const uint32_t gbase = __ldg(a.S + w0);
+    for (uint32_t i = threadIdx.x; i < nw; i += kJoinThreads) sI[swz(i)] = __ldg(a.I + w0 + i);
     // warm L2 with the next sub-bin's occupancy words while this one is processed
     {
       const uint32_t nsb = sb + gridDim.x;
-      const uint32_t bytes = nw * 4u;
-      if (nsb < a.n_sub && threadIdx.x * 128u < 2u * bytes) {
-        const uint32_t arr = (threadIdx.x * 128u) / bytes, off = (threadIdx.x * 128u) % bytes;
-        const char* p = reinterpret_cast<const char*>(a.I[arr] + uint32_t((uint64_t(nsb) << a.code_shift) >> 5)) + off;
+      if (nsb < a.n_sub && threadIdx.x * 32u < nw) {
+        const uint32_t* p = a.I + uint32_t((uint64_t(nsb) << a.code_shift) >> 5) + threadIdx.x * 32u;
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
       }
     }
     __syncthreads();
-    {  // group starts on chip: exclusive popcount prefix per strand
+    {  // group starts on chip: exclusive popcount prefix
       uint32_t sum = 0;
       if (scan_active)
         for (uint32_t i = 0; i < per; ++i) sum += __popc(sI[swz(my_w0 + i)]);
       uint32_t tot;
       uint32_t run = block_exclusive_scan<uint32_t>(sum, s_ws, &tot);
-      if (scan_active && my_w0 == nw) s_split = run;
-      __syncthreads();
-      if (scan_active) {
-        if (my_w0 >= nw) run -= s_split;
+      if (scan_active)
         for (uint32_t i = 0; i < per; ++i) {
           const uint32_t x = swz(my_w0 + i);
           sR[x] = uint16_t(run);
           run += __popc(sI[x]);
         }
-      }
     }
     __syncthreads();
     // the sub-bin's items split evenly over the warps (no warp idles at the
@@ -184,47 +175,49 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
     const uint32_t my_lo = b0 + uint32_t(uint64_t(nitems) * wid / kJoinWarps);
     const uint32_t my_hi = b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kJoinWarps);
     const uint32_t gsub = sb << a.code_shift;
+    uint64_t pn[kItems];  // next step's items, loaded one step ahead
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) {
+      const uint32_t it = my_lo + u * 32 + lane;
+      pn[u] = it < my_hi ? __ldg(a.items + it) : ~0ull;
+    }
     for (uint32_t base = my_lo; base < my_hi; base += 32 * kItems) {  // warp-uniform bound
-      uint32_t cnt = 0, nr = 0, rk0[kSlots], rk1[kSlots];
-      uint64_t pr[kItems];
+      uint32_t cnt = 0, nr = 0, rk0[kItems], rk1[kItems];
 #pragma unroll
       for (int u = 0; u < kItems; ++u) {
-        const uint32_t it = base + u * 32 + lane;
-        pr[u] = it < my_hi ? __ldg(a.items + it) : ~0ull;
-      }
-#pragma unroll
-      for (int s = 0; s < kSlots; ++s) {
-        const int u = s >> 1, st = s & 1;
-        const bool ok = pr[u] != ~0ull;
-        const uint32_t g = gsub | uint32_t(pr[u] >> kItemCodeShift);
+        const uint64_t pr = pn[u];
+        const uint32_t itn = base + 32 * kItems + u * 32 + lane;
+        pn[u] = itn < my_hi ? __ldg(a.items + itn) : ~0ull;
+        const bool ok = pr != ~0ull;
+        const uint32_t g = gsub | uint32_t(pr >> kItemCodeShift);
         const uint32_t wl = ok ? (g >> 5) - w0 : 0u, bit = g & 31u;
-        const uint32_t x = swz(st * nw + wl);
-        const uint32_t w = sI[x] & smask[st];
+        const uint32_t x = swz(wl);
+        const uint32_t w = sI[x];
         const bool hit = ok && ((w >> bit) & 1u);
-        const uint32_t b = gbase[st] + sR[x] + __popc(w & ((1u << bit) - 1u));
-        rk0[s] = hit ? __ldg(a.S1[st] + b) : 0u;
-        rk1[s] = hit ? __ldg(a.S1[st] + b + 1) : 0u;
+        const uint32_t b = gbase + sR[x] + __popc(w & ((1u << bit) - 1u));
+        rk0[u] = hit ? __ldg(a.S1 + b) : 0u;
+        rk1[u] = hit ? __ldg(a.S1 + b + 1) : 0u;
       }
 #pragma unroll
-      for (int s = 0; s < kSlots; ++s) {
-        const uint32_t len = rk1[s] - rk0[s];
+      for (int u = 0; u < kItems; ++u) {
+        const uint32_t len = rk1[u] - rk0[u];
         cnt += len;
         nr += len != 0;
       }
       n_hit += nr;
       n_occ += cnt;
       if (__all_sync(kFull, cnt == 0)) continue;
-      // compact the non-empty (q-gram, strand) lookups of the warp into a list
+      // compact the non-empty lookups of the warp into a list
       uint32_t nent = 0;
 #pragma unroll
-      for (int s = 0; s < kSlots; ++s) {
-        const bool has = rk1[s] != rk0[s];
+      for (int u = 0; u < kItems; ++u) {
+        const bool has = rk1[u] != rk0[u];
         const unsigned bm = __ballot_sync(kFull, has);
         if (has) {
           const uint32_t e = nent + __popc(bm & lanemask_lt());
-          s_k0[wid][e] = rk0[s];
-          s_k1[wid][e] = rk1[s];
-          s_meta[wid][e] = uint16_t(((s >> 1) * 32 + lane) | ((s & 1) << 15));
+          s_k0[wid][e] = rk0[u];
+          s_k1[wid][e] = rk1[u];
+          s_slot[wid][e] = uint8_t(u * 32 + lane);
         }
         nent += __popc(bm);
       }
@@ -234,20 +227,19 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
       // (repeats) by the whole warp, one interval at a time
       for (uint32_t e0 = 0; e0 < nent; e0 += 32) {
         const uint32_t e = e0 + lane;
-        uint32_t k0 = 0, len = 0, meta = 0;
+        uint32_t k0 = 0, len = 0;
+        uint64_t it = 0;
         if (e < nent) {
           k0 = s_k0[wid][e];
           len = s_k1[wid][e] - k0;
-          meta = s_meta[wid][e];
+          it = __ldg(a.items + base + s_slot[wid][e]);
         }
-        const uint64_t it = e < nent ? __ldg(a.items + base + (meta & 0x7FFFu)) : 0ull;
-        const uint32_t rev = meta >> 15;
         const bool longi = len > kInline;
         const uint32_t nin = longi ? 0u : len;
         const uint32_t rounds = __reduce_max_sync(kFull, nin);
         for (uint32_t t = 0; t < rounds; ++t) {
           uint64_t key = 0;
-          const bool emit = t < nin && expand<kRunStart, kPacked>(a, k0 + t, it, rev, key);
+          const bool emit = t < nin && expand<kRunStart, kPacked>(a, k0 + t, it, key);
           stage_key(emit, key);
         }
         unsigned lm = __ballot_sync(kFull, longi);
@@ -256,17 +248,16 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
           lm &= lm - 1;
           const uint32_t lk0 = __shfl_sync(kFull, k0, src), llen = __shfl_sync(kFull, len, src);
           const uint64_t lit = __shfl_sync(kFull, it, src);
-          const uint32_t lrev = __shfl_sync(kFull, rev, src);
           for (uint32_t t0 = 0; t0 < llen; t0 += 32) {
             uint64_t key = 0;
-            const bool emit = t0 + lane < llen && expand<kRunStart, kPacked>(a, lk0 + t0 + lane, lit, lrev, key);
+            const bool emit = t0 + lane < llen && expand<kRunStart, kPacked>(a, lk0 + t0 + lane, lit, key);
             stage_key(emit, key);
           }
         }
       }
       __syncwarp();
     }
-    __syncthreads();  // shared words are reloaded for the next sub-bin
+    __syncthreads();  // sI / sR are rewritten for the next sub-bin
   }
   flush();
   n_hit = warp_reduce_sum(n_hit);
@@ -293,19 +284,15 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   a.words = std::max<uint32_t>(1, (1u << a.code_shift) / 32);
   if (a.words > kMaxWords) throw InternalError("join: sub-bin wider than the shared staging");
   a.q = rp.q;
-  const Index* ix[2] = {&X.fwd, &X.rc};
-  for (int st = 0; st < 2; ++st) {
-    a.I[st] = reinterpret_cast<const uint32_t*>(ix[st]->I.p);
-    a.S[st] = ix[st]->S.p;
-    a.S1[st] = ix[st]->S1.p;
-    a.O[st] = ix[st]->O.p;
-  }
-  a.X[0] = X.prev_fwd.p;
-  a.X[1] = X.prev_rc.p;
+  a.I = reinterpret_cast<const uint32_t*>(X.can.I.p);
+  a.S = X.can.S.p;
+  a.S1 = X.can.S1.p;
+  a.O = X.can.O.p;
+  a.X = X.extra.p;
   a.rlen = reads.lengths.p;
   a.m = reads.stride;
   a.by_m = FastDiv(std::max<uint32_t>(reads.stride, 1));
-  a.tail_ok = reads.stride < rp.q + kItemTailMax;
+  a.tail_ok = reads.stride <= rp.q + kItemTailMax;
   a.strands = strands;
   a.diag_bits = ref.diag_bits;
   DBuf<unsigned long long> counter(c, 3);
@@ -315,7 +302,7 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   const bool rs = mode == 1;
   const void* kfn = X.packed ? (rs ? (const void*)k_join<true, true> : (const void*)k_join<false, true>)
                              : (rs ? (const void*)k_join<true, false> : (const void*)k_join<false, false>);
-  const size_t smem = size_t(2) * a.words * (sizeof(uint32_t) + sizeof(uint16_t));
+  const size_t smem = size_t(a.words) * (sizeof(uint32_t) + sizeof(uint16_t));
   QGM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const unsigned grid = std::min<unsigned>(a.n_sub, resident_grid(kfn, kJoinThreads, smem));
   for (int attempt = 0; attempt < 2; ++attempt) {

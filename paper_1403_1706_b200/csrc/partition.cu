@@ -16,7 +16,8 @@
 // ncu on the previous single-pass scatter (12-bit bins, items written
 // straight from registers) showed 1.6 GB of read-for-ownership and 2.1 GB of
 // writes for 0.68 GB of output: partial sectors of 2.4M concurrently open runs.
-// First-pass item = (full code << 32) | text position (r*stride + o), 8 bytes;
+// q-grams are keyed by their canonical code min(g, rc(g)) (RefQIndex).
+// First-pass item = (canonical code << 32) | text position (r*stride + o);
 // the refinement pass writes the final join items (internal.hpp: position,
 // tail, the two run-start compare bases, the code bits below the sub-bin), so
 // the join never touches the read text.
@@ -41,7 +42,8 @@ struct ItemGen {
     const uint32_t r = by_span.div(t);
     const uint32_t o = t - r * span;
     if (o + q > __ldg(lengths + r)) return false;
-    g = qgram_at(words + uint64_t(r) * W, o, q);
+    const uint32_t f = qgram_at(words + uint64_t(r) * W, o, q);
+    g = min(f, rc_code(f, q));  // canonical code (RefQIndex)
     pos = r * stride + o;
     return true;
   }
@@ -131,15 +133,19 @@ struct ItemConv {
   unsigned q;
   uint32_t lmask;  // code bits below the sub-bin prefix
   __device__ __forceinline__ uint64_t operator()(uint64_t it) const {
-    const uint32_t pp = uint32_t(it), g = uint32_t(it >> 32);
+    const uint32_t pp = uint32_t(it), c = uint32_t(it >> 32);
     const uint32_t r = by_stride.div(pp), o = pp - r * stride;
+    // all loads depend only on (r, o): issue them together
     const uint32_t n = __ldg(lengths + r);
     const uint64_t* w = words + uint64_t(r) * W;
-    const uint32_t fb = o ? base_at(w, o - 1) : 4u;
-    const uint32_t rb = o + q < n ? base_at(w, o + q) : 4u;
+    const uint32_t f = qgram_at(w, o, q);
+    const uint32_t bf = base_at(w, o ? o - 1 : 0);
+    const uint32_t br = base_at(w, min(o + q, stride - 1));
+    const uint32_t fb = o ? bf : 4u;
+    const uint32_t rb = o + q < n ? 3u - br : 4u;
     const uint32_t tail = min(n - q - o, kItemTailMax);
-    return (uint64_t(g & lmask) << kItemCodeShift) | (uint64_t(rb) << kItemRbShift) |
-           (uint64_t(fb) << kItemFbShift) | (uint64_t(tail) << kItemTailShift) | pp;
+    return (uint64_t(c & lmask) << kItemCodeShift) | (uint64_t(f != c) << kItemFrShift) |
+           (uint64_t(rb) << kItemRbShift) | (uint64_t(fb) << kItemFbShift) | (uint64_t(tail) << kItemTailShift) | pp;
   }
 };
 
