@@ -163,12 +163,21 @@ __global__ void k_ref_planes(const uint64_t* __restrict__ words, uint64_t nw, ui
     planes[k + 2] = to_planes(words[k]);
 }
 
-__global__ void k_max_u32(const uint32_t* __restrict__ v, uint64_t n, uint32_t* __restrict__ out) {
-  uint32_t m = 0;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+// out[0] = max, out[1] = ~min (both folded with atomicMax; out zeroed)
+__global__ void k_minmax_u32(const uint32_t* __restrict__ v, uint64_t n, uint32_t* __restrict__ out) {
+  uint32_t m = 0, nm = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     m = max(m, v[i]);
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
-  if (lane_id() == 0) atomicMax(out, m);
+    nm = max(nm, ~v[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = max(m, __shfl_xor_sync(kFull, m, o));
+    nm = max(nm, __shfl_xor_sync(kFull, nm, o));
+  }
+  if (lane_id() == 0) {
+    atomicMax(out, m);
+    atomicMax(out + 1, nm);
+  }
 }
 
 unsigned read_bits_for(uint32_t n_reads) { return std::max(1u, bit_width_u64(n_reads ? n_reads - 1 : 0)); }
@@ -196,13 +205,16 @@ void make_ref_planes(Ctx& c, Ref& ref) {
 // ------------------------------------------------------------------ pipeline
 static void finish_reads(Ctx& c, Reads& r) {
   make_read_planes(c, r);
-  DBuf<uint32_t> mx(c, 1);
+  DBuf<uint32_t> mx(c, 2);
   mx.zero();
   if (r.n)
-    QGM_KERNEL(c, k_max_u32, unsigned(std::min<uint64_t>(ceil_div(r.n, 256), kSMs * 4)), 256, 0, r.lengths.p,
+    QGM_KERNEL(c, k_minmax_u32, unsigned(std::min<uint64_t>(ceil_div(r.n, 256), kSMs * 4)), 256, 0, r.lengths.p,
                uint64_t(r.n), mx.p);
-  QGM_CUDA(cudaMemcpyAsync(&r.max_len, mx.p, 4, cudaMemcpyDeviceToHost, c.stream));
+  uint32_t h[2] = {0, 0};
+  QGM_CUDA(cudaMemcpyAsync(h, mx.p, 8, cudaMemcpyDeviceToHost, c.stream));
   QGM_CUDA(cudaStreamSynchronize(c.stream));
+  r.max_len = h[0];
+  r.min_len = r.n ? ~h[1] : 0;
   if (r.max_len > r.stride) throw InputError("read longer than the stride");
 }
 

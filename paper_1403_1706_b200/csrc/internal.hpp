@@ -146,7 +146,7 @@ struct DBuf {
 // per-read bit planes (lo/hi bit of every base, MSB-first, one guard word in
 // front) for the validation kernel.
 struct Reads {
-  uint32_t n = 0, stride = 0, W = 0, Wp = 0, max_len = 0;
+  uint32_t n = 0, stride = 0, W = 0, Wp = 0, max_len = 0, min_len = 0;
   DBuf<uint64_t> words;    // n * W
   DBuf<uint32_t> lengths;  // n
   DBuf<uint2> planes;      // n * Wp, word 0 of every read is a zero guard

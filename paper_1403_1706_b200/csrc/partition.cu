@@ -1,10 +1,9 @@
 // partition.cu -- per-batch read q-gram partition for the join (map path).
 //
 // The join (join.cu) only needs the batch's read q-grams grouped by the top
-// bits of their code, so that the warps in flight touch a few MiB of the
-// reference index (L2-resident) instead of all of it; it never needs the full
-// read-side q-group index. Two passes over the (L2-resident) 2-bit reads, no
-// per-item rank array:
+// bits of their canonical code min(g, rc(g)) (RefQIndex), so that the warps in
+// flight touch a few MiB of the reference index (L2-resident) instead of all
+// of it; it never needs the full read-side q-group index. Passes:
 //   P0 histogram : per-CTA shared-memory histogram over 2^bits code bins
 //                  (bits = min(2q, 8)), one global atomic per non-empty bin;
 //   scan         : bin offsets;
@@ -12,15 +11,22 @@
 //                  bin in shared memory, one global atomic per bin to reserve
 //                  the chunk's run, then runs copied out with consecutive
 //                  threads writing consecutive 8-byte slots (full sectors;
-//                  ~16 items = one 128 B line per bin per chunk at q=16).
-// ncu on the previous single-pass scatter (12-bit bins, items written
-// straight from registers) showed 1.6 GB of read-for-ownership and 2.1 GB of
-// writes for 0.68 GB of output: partial sectors of 2.4M concurrently open runs.
-// q-grams are keyed by their canonical code min(g, rc(g)) (RefQIndex).
-// First-pass item = (canonical code << 32) | text position (r*stride + o);
-// the refinement pass writes the final join items (internal.hpp: position,
-// tail, the two run-start compare bases, the code bits below the sub-bin), so
-// the join never touches the read text.
+//                  ~16 items = one 128 B line per bin per chunk at q=16);
+//   P2 refine    : the same staged counting sort on the next code bits (up to
+//                  16 in total), per chunk of 4096 bin-ordered items, writing
+//                  the final join items.
+// ncu on an earlier single-pass scatter (12-bit bins, items written straight
+// from registers) showed 1.6 GB of read-for-ownership and 2.1 GB of writes for
+// 0.68 GB of output: partial sectors of 2.4M concurrently open runs.
+//
+// Everything the join needs from the read text is gathered in P1, where the
+// read words are at hand (the join and P2 never touch the reads' bases). P1
+// item (the bin's code bits are implied by the item's position):
+//   bits  0..31 pp = r * stride + o        bits 33..35 read base at o-1 (4 = none)
+//   bits 36..38 complement of read[o+q]    bit  39     fr = (code != canonical)
+//   bits 40..63 canonical code bits below the P1 bin
+// P2 drops the next 8 implied bits and adds tail = n - q - o (join item layout
+// in internal.hpp).
 #include "internal.hpp"
 
 namespace qgm {
@@ -31,21 +37,51 @@ constexpr unsigned kBinBits = 8;
 constexpr uint32_t kBins = 1u << kBinBits;
 constexpr uint32_t kChunk = 4096;  // q-gram slots per chunk; staging = 32 KiB
 constexpr uint32_t kPer = kChunk / kPartThreads;
+constexpr unsigned kP1CodeShift = 40, kP1MetaShift = 33;
+
+// One q-gram slot t = r * span + o: every load depends only on t, so a
+// thread issues the loads of all its slots before using any of them (the
+// read-word loads of a warp's 32 consecutive slots hit the same few lines).
+struct Slot {
+  uint32_t r, o, n;
+  uint64_t wm, w0, w1;  // read words k-1 (kMeta only), k, k+1 with k = o / 32
+};
 
 struct ItemGen {
   const uint64_t* words;
   const uint32_t* lengths;
-  uint32_t W, span, stride;
+  uint32_t W, span, stride, n_items;
   FastDiv by_span;
   unsigned q;
-  __device__ __forceinline__ bool item(uint32_t t, uint32_t& g, uint32_t& pos) const {
-    const uint32_t r = by_span.div(t);
-    const uint32_t o = t - r * span;
-    if (o + q > __ldg(lengths + r)) return false;
-    const uint32_t f = qgram_at(words + uint64_t(r) * W, o, q);
-    g = min(f, rc_code(f, q));  // canonical code (RefQIndex)
-    pos = r * stride + o;
-    return true;
+  template <bool kMeta>
+  __device__ __forceinline__ void fetch(uint32_t t, Slot& s) const {
+    t = min(t, n_items - 1);  // slots past the end load something valid and are dropped
+    s.r = by_span.div(t);
+    s.o = t - s.r * span;
+    s.n = __ldg(lengths + s.r);
+    const uint64_t* w = words + uint64_t(s.r) * W + (s.o >> 5);
+    s.w0 = __ldg(w);
+    s.w1 = __ldg(w + 1);  // the read's own words, or the next read's / the guard word
+    s.wm = kMeta && s.o >= 32 ? __ldg(w - 1) : 0ull;
+  }
+  // canonical code g of a fetched slot; f = the read's own code
+  __device__ __forceinline__ bool code(uint32_t t, const Slot& s, uint32_t& f, uint32_t& g) const {
+    const unsigned sh = 2 * (s.o & 31);
+    const uint64_t hi = sh ? (s.w0 << sh) | (s.w1 >> (64 - sh)) : s.w0;
+    f = uint32_t(hi >> (64 - 2 * q));
+    g = min(f, rc_code(f, q));
+    return t < n_items && s.o + q <= s.n;
+  }
+  // P1 fields: read base at o-1 (4 = none), complement of the base at o+q
+  // (4 = none), fr = (f != g)
+  __device__ __forceinline__ uint32_t meta(const Slot& s, uint32_t f, uint32_t g) const {
+    const int rel_l = int(s.o & 31) - 1;               // in [-1, 30]
+    const uint32_t rel_r = (s.o & 31) + q;             // in [1, 47]
+    const uint32_t bl = rel_l < 0 ? uint32_t(s.wm) & 3u : uint32_t(s.w0 >> (62 - 2 * rel_l)) & 3u;
+    const uint32_t br = rel_r < 32 ? uint32_t(s.w0 >> (62 - 2 * rel_r)) & 3u : uint32_t(s.w1 >> (62 - 2 * (rel_r - 32))) & 3u;
+    const uint32_t fb = s.o ? bl : 4u;
+    const uint32_t rb = s.o + q < s.n ? 3u - br : 4u;
+    return fb | (rb << 3) | (uint32_t(f != g) << 6);
   }
 };
 
@@ -55,34 +91,53 @@ __global__ void __launch_bounds__(kPartThreads) k_part_hist(ItemGen gen, uint32_
   for (uint32_t b = threadIdx.x; b < kBins; b += kPartThreads) h[b] = 0;
   __syncthreads();
   const uint32_t c0 = blockIdx.x * chunk, c1 = min(n_items, c0 + chunk);
-  for (uint32_t t = c0 + threadIdx.x; t < c1; t += kPartThreads) {
-    uint32_t g, pos;
-    if (gen.item(t, g, pos)) atomicAdd(h + (g >> shift), 1u);
+  for (uint32_t t0 = c0; t0 < c1; t0 += 4 * kPartThreads) {
+    Slot sl[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) gen.fetch<false>(t0 + k * kPartThreads + threadIdx.x, sl[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t t = t0 + k * kPartThreads + threadIdx.x;
+      uint32_t f, g;
+      if (t < c1 && gen.code(t, sl[k], f, g)) atomicAdd(h + (g >> shift), 1u);
+    }
   }
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < kBins; b += kPartThreads)
     if (h[b]) atomicAdd(hist + b, h[b]);
 }
 
-__global__ void __launch_bounds__(kPartThreads, 4) k_part_scatter(ItemGen gen, uint32_t n_items, unsigned shift,
+__global__ void __launch_bounds__(kPartThreads, 2) k_part_scatter(ItemGen gen, uint32_t n_items, unsigned shift,
                                                                   const uint32_t* __restrict__ boff,
                                                                   uint32_t* __restrict__ cursor,
                                                                   uint64_t* __restrict__ out) {
-  extern __shared__ uint64_t stage[];  // kChunk items, bin-sorted
+  extern __shared__ uint64_t stage[];  // kChunk items, bin-sorted, then kChunk u8 bins
+  uint8_t* sbin = reinterpret_cast<uint8_t*>(stage + kChunk);
   __shared__ uint32_t cnt[kBins], lofs[kBins], gdst[kBins];
   __shared__ uint32_t ws[33];
+  const uint32_t lmask = shift ? (1u << shift) - 1u : 0u;
   const uint32_t n_chunks = (n_items + kChunk - 1) / kChunk;
   for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
     const uint32_t c0 = ch * kChunk;
     for (uint32_t b = threadIdx.x; b < kBins; b += kPartThreads) cnt[b] = 0;
     __syncthreads();
-    uint32_t g[kPer], pos[kPer];
-    bool ok[kPer];
+    uint64_t item[kPer];
+    uint32_t bin[kPer];  // ~0u = no q-gram at this slot
 #pragma unroll
-    for (uint32_t k = 0; k < kPer; ++k) {
-      const uint32_t t = c0 + k * kPartThreads + threadIdx.x;
-      ok[k] = t < n_items && gen.item(t, g[k], pos[k]);
-      if (ok[k]) atomicAdd(cnt + (g[k] >> shift), 1u);
+    for (uint32_t h = 0; h < kPer; h += 4) {
+      Slot sl[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) gen.fetch<true>(c0 + (h + k) * kPartThreads + threadIdx.x, sl[k]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t t = c0 + (h + k) * kPartThreads + threadIdx.x;
+        uint32_t f, g;
+        const bool ok = gen.code(t, sl[k], f, g);
+        const uint32_t pos = sl[k].r * gen.stride + sl[k].o;
+        item[h + k] = (uint64_t(g & lmask) << kP1CodeShift) | (uint64_t(gen.meta(sl[k], f, g)) << kP1MetaShift) | pos;
+        bin[h + k] = ok ? g >> shift : ~0u;
+        if (ok) atomicAdd(cnt + bin[h + k], 1u);
+      }
     }
     __syncthreads();
     {  // local exclusive offsets; reserve the chunk's run in every bin
@@ -99,128 +154,160 @@ __global__ void __launch_bounds__(kPartThreads, 4) k_part_scatter(ItemGen gen, u
     __syncthreads();
 #pragma unroll
     for (uint32_t k = 0; k < kPer; ++k)
-      if (ok[k]) stage[atomicAdd(cnt + (g[k] >> shift), 1u)] = (uint64_t(g[k]) << 32) | pos[k];
+      if (bin[k] != ~0u) {
+        const uint32_t slot = atomicAdd(cnt + bin[k], 1u);
+        stage[slot] = item[k];
+        sbin[slot] = uint8_t(bin[k]);
+      }
     __syncthreads();
     const uint32_t total = cnt[kBins - 1];  // == number of valid items in the chunk
     for (uint32_t i = threadIdx.x; i < total; i += kPartThreads) {
-      const uint64_t it = stage[i];
-      const uint32_t b = uint32_t(it >> 32) >> shift;
-      out[gdst[b] + (i - lofs[b])] = it;
+      const uint32_t b = sbin[i];
+      out[gdst[b] + (i - lofs[b])] = stage[i];
     }
     __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------- refinement
-// Second MSD pass: items already grouped by their top 8 code bits are
+// Second MSD pass: items grouped by their P1 bin (top `bits` code bits) are
 // regrouped by their top `key_bits` (<= 16) bits. A chunk of 4096 consecutive
-// items spans few top-8 bins, so its keys fall in a small window
-// [first_bin << sub, (last_bin + 1) << sub); the window is counted and
-// staged in shared memory exactly like P1 (kLocal keys max), with a
-// per-item global fallback for chunks whose window is wider (tiny bins).
+// items spans few P1 bins, so its keys fall in a small window
+// [first_bin << sub, (last_bin + 1) << sub); the window is counted and staged
+// in shared memory exactly like P1 (kLocal keys max), with a per-item global
+// fallback for chunks whose window is wider (tiny bins). The P1 bin of item i
+// is found from the bin offsets (staged in shared memory) with a per-thread
+// cursor that only moves forward.
 constexpr uint32_t kLocal = 2048;
 
-__device__ __forceinline__ uint32_t key_of(uint64_t it, unsigned kshift) { return uint32_t(it >> 32) >> kshift; }
-
-// first-pass item -> join item (layout in internal.hpp). The read words and
-// lengths are L2-resident; consecutive items of a chunk come from ascending
-// reads.
-struct ItemConv {
-  const uint64_t* words;
+struct Refine {
+  unsigned shift;    // code bits below the P1 bin (in the P1 item)
+  unsigned kshift;   // code bits below the refined key (in the join item)
+  uint32_t nbins;    // P1 bins
+  // join-item conversion
   const uint32_t* lengths;
-  uint32_t W, stride;
+  uint32_t stride;
   FastDiv by_stride;
   unsigned q;
-  uint32_t lmask;  // code bits below the sub-bin prefix
-  __device__ __forceinline__ uint64_t operator()(uint64_t it) const {
-    const uint32_t pp = uint32_t(it), c = uint32_t(it >> 32);
+  int uniform;
+  __device__ __forceinline__ uint32_t key(uint64_t it, uint32_t bin) const {
+    return (bin << (shift - kshift)) | (uint32_t(it >> kP1CodeShift) >> kshift);
+  }
+  __device__ __forceinline__ uint64_t convert(uint64_t it) const {
+    const uint32_t pp = uint32_t(it);
     const uint32_t r = by_stride.div(pp), o = pp - r * stride;
-    // all loads depend only on (r, o): issue them together
-    const uint32_t n = __ldg(lengths + r);
-    const uint64_t* w = words + uint64_t(r) * W;
-    const uint32_t f = qgram_at(w, o, q);
-    const uint32_t bf = base_at(w, o ? o - 1 : 0);
-    const uint32_t br = base_at(w, min(o + q, stride - 1));
-    const uint32_t fb = o ? bf : 4u;
-    const uint32_t rb = o + q < n ? 3u - br : 4u;
+    // every read of the batch has length `stride` (the usual case): no load
+    const uint32_t n = uniform ? stride : __ldg(lengths + r);
     const uint32_t tail = min(n - q - o, kItemTailMax);
-    return (uint64_t(c & lmask) << kItemCodeShift) | (uint64_t(f != c) << kItemFrShift) |
-           (uint64_t(rb) << kItemRbShift) | (uint64_t(fb) << kItemFbShift) | (uint64_t(tail) << kItemTailShift) | pp;
+    const uint32_t lmask = kshift ? (1u << kshift) - 1u : 0u;
+    return (uint64_t(uint32_t(it >> kP1CodeShift) & lmask) << kItemCodeShift) |
+           (uint64_t((it >> kP1MetaShift) & 0x7Fu) << kItemFbShift) | (uint64_t(tail) << kItemTailShift) | pp;
   }
 };
 
+// largest b with boff[b] <= i (i < total)
+__device__ __forceinline__ uint32_t bin_search(const uint32_t* sboff, uint32_t nbins, uint32_t i) {
+  uint32_t lo = 0, hi = nbins;  // invariant: boff[lo] <= i < boff[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (sboff[mid] <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 __global__ void __launch_bounds__(kPartThreads) k_refine_hist(const uint64_t* __restrict__ in, uint32_t n,
-                                                              unsigned kshift, unsigned sub,
-                                                              uint32_t* __restrict__ hist) {
+                                                              const uint32_t* __restrict__ boff, Refine rf,
+                                                              unsigned sub, uint32_t* __restrict__ hist) {
   __shared__ uint32_t h[kLocal];
+  __shared__ uint32_t sboff[kBins + 1];
+  for (uint32_t b = threadIdx.x; b <= rf.nbins; b += kPartThreads) sboff[b] = boff[b];
+  __syncthreads();
   const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
   for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
     const uint32_t c0 = ch * kChunk, c1 = min(n, c0 + kChunk);
-    const uint32_t base = (key_of(in[c0], kshift) >> sub) << sub;
-    const uint32_t width = (((key_of(in[c1 - 1], kshift) >> sub) + 1) << sub) - base;
+    const uint32_t bfirst = bin_search(sboff, rf.nbins, c0), blast = bin_search(sboff, rf.nbins, c1 - 1);
+    const uint32_t base = (rf.key(in[c0], bfirst) >> sub) << sub;
+    const uint32_t width = (((rf.key(in[c1 - 1], blast) >> sub) + 1) << sub) - base;
+    uint32_t b = bfirst;
     if (width > kLocal) {  // rare: many tiny bins in one chunk
-      for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) atomicAdd(hist + key_of(in[i], kshift), 1u);
+      for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) {
+        while (sboff[b + 1] <= i) ++b;
+        atomicAdd(hist + rf.key(in[i], b), 1u);
+      }
       continue;
     }
-    for (uint32_t b = threadIdx.x; b < width; b += kPartThreads) h[b] = 0;
+    for (uint32_t k = threadIdx.x; k < width; k += kPartThreads) h[k] = 0;
     __syncthreads();
-    for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) atomicAdd(h + key_of(in[i], kshift) - base, 1u);
+    if (bfirst == blast) {  // the common case: the chunk lies in one P1 bin
+      for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) atomicAdd(h + rf.key(in[i], b) - base, 1u);
+    } else {
+      for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) {
+        while (sboff[b + 1] <= i) ++b;
+        atomicAdd(h + rf.key(in[i], b) - base, 1u);
+      }
+    }
     __syncthreads();
-    for (uint32_t b = threadIdx.x; b < width; b += kPartThreads)
-      if (h[b]) atomicAdd(hist + base + b, h[b]);
+    for (uint32_t k = threadIdx.x; k < width; k += kPartThreads)
+      if (h[k]) atomicAdd(hist + base + k, h[k]);
     __syncthreads();
   }
 }
 
 __global__ void __launch_bounds__(kPartThreads, 2) k_refine_scatter(const uint64_t* __restrict__ in, uint32_t n,
-                                                                    unsigned kshift, unsigned sub,
-                                                                    const uint32_t* __restrict__ off,
+                                                                    const uint32_t* __restrict__ boff, Refine rf,
+                                                                    unsigned sub, const uint32_t* __restrict__ off,
                                                                     uint32_t* __restrict__ cursor,
-                                                                    ItemConv conv, uint64_t* __restrict__ out) {
-  extern __shared__ uint64_t stage[];  // kChunk converted items, then kChunk u16 window keys
+                                                                    uint64_t* __restrict__ out) {
+  extern __shared__ uint64_t stage[];  // kChunk join items, then kChunk u16 window keys
   uint16_t* skey = reinterpret_cast<uint16_t*>(stage + kChunk);
   __shared__ uint32_t cnt[kLocal], lofs[kLocal], gdst[kLocal];
+  __shared__ uint32_t sboff[kBins + 1];
   __shared__ uint32_t ws[33];
+  for (uint32_t b = threadIdx.x; b <= rf.nbins; b += kPartThreads) sboff[b] = boff[b];
+  __syncthreads();
   const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
   for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
     const uint32_t c0 = ch * kChunk, c1 = min(n, c0 + kChunk);
-    const uint32_t base = (key_of(in[c0], kshift) >> sub) << sub;
-    const uint32_t width = (((key_of(in[c1 - 1], kshift) >> sub) + 1) << sub) - base;
+    const uint32_t bfirst = bin_search(sboff, rf.nbins, c0), blast = bin_search(sboff, rf.nbins, c1 - 1);
+    const uint32_t base = (rf.key(in[c0], bfirst) >> sub) << sub;
+    const uint32_t width = (((rf.key(in[c1 - 1], blast) >> sub) + 1) << sub) - base;
+    uint32_t b = bfirst;
     if (width > kLocal) {
       for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) {
+        while (sboff[b + 1] <= i) ++b;
         const uint64_t it = in[i];
-        const uint32_t k = key_of(it, kshift);
-        out[off[k] + atomicAdd(cursor + k, 1u)] = conv(it);
+        const uint32_t k = rf.key(it, b);
+        out[off[k] + atomicAdd(cursor + k, 1u)] = rf.convert(it);
       }
       continue;
     }
-    for (uint32_t b = threadIdx.x; b < width; b += kPartThreads) cnt[b] = 0;
+    for (uint32_t k = threadIdx.x; k < width; k += kPartThreads) cnt[k] = 0;
     __syncthreads();
-    // convert on load: consecutive first-pass items come from the same few
-    // reads, so the read-word / length loads of a warp hit the same lines
     uint64_t v[kPer];
     uint32_t kk[kPer];
 #pragma unroll
     for (uint32_t k = 0; k < kPer; ++k) {
       const uint32_t i = c0 + k * kPartThreads + threadIdx.x;
       const uint64_t it = i < c1 ? in[i] : 0ull;
-      kk[k] = i < c1 ? key_of(it, kshift) - base : ~0u;
-      v[k] = i < c1 ? conv(it) : 0ull;
+      if (i < c1 && bfirst != blast)
+        while (sboff[b + 1] <= i) ++b;
+      kk[k] = i < c1 ? rf.key(it, b) - base : ~0u;
+      v[k] = i < c1 ? rf.convert(it) : 0ull;
       if (i < c1) atomicAdd(cnt + kk[k], 1u);
     }
     __syncthreads();
     // exclusive scan of cnt[0, width): each thread owns a contiguous run
     const uint32_t per = (width + kPartThreads - 1) / kPartThreads;
-    const uint32_t b0 = threadIdx.x * per, b1 = min(width, b0 + per);
+    const uint32_t k0 = threadIdx.x * per, k1 = min(width, k0 + per);
     uint32_t s = 0;
-    for (uint32_t b = b0; b < b1; ++b) s += cnt[b];
+    for (uint32_t k = k0; k < k1; ++k) s += cnt[k];
     uint32_t tot;
     uint32_t run = block_exclusive_scan<uint32_t>(s, ws, &tot);
-    for (uint32_t b = b0; b < b1; ++b) {
-      const uint32_t cv = cnt[b];
-      lofs[b] = run;
-      gdst[b] = cv ? off[base + b] + atomicAdd(cursor + base + b, cv) : 0u;
-      cnt[b] = run;
+    for (uint32_t k = k0; k < k1; ++k) {
+      const uint32_t cv = cnt[k];
+      lofs[k] = run;
+      gdst[k] = cv ? off[base + k] + atomicAdd(cursor + base + k, cv) : 0u;
+      cnt[k] = run;
       run += cv;
     }
     __syncthreads();
@@ -233,8 +320,8 @@ __global__ void __launch_bounds__(kPartThreads, 2) k_refine_scatter(const uint64
       }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < c1 - c0; i += kPartThreads) {
-      const uint32_t b = skey[i];
-      out[gdst[b] + (i - lofs[b])] = stage[i];
+      const uint32_t k = skey[i];
+      out[gdst[k] + (i - lofs[k])] = stage[i];
     }
     __syncthreads();
   }
@@ -255,17 +342,22 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   const uint64_t n_items64 = uint64_t(reads.n) * gen.span;
   if (n_items64 > 0xFFFFFFFFull - kChunk) throw InputError("read batch has more than 2^32-1 q-gram slots");
   const uint32_t n_items = uint32_t(n_items64);
+  gen.n_items = n_items;
   const unsigned bits = std::min(2 * q, kBinBits);
   const unsigned shift = 2 * q - bits;
+  const unsigned key_bits = std::min(2 * q, 16u);
   out.q = q;
   out.bins = 1u << bits;
+  out.sub_bits = key_bits;
   out.boff.alloc(c, kBins + 1);
-  if (n_items == 0) {
+  out.V = 0;
+  auto empty = [&] {  // no read has a q-gram
     out.boff.zero();
-    out.V = 0;
     out.pairs.alloc(c, 1);
-    return;
-  }
+    out.soff.alloc(c, (1u << key_bits) + 1);
+    out.soff.zero();
+  };
+  if (n_items == 0) return empty();
   const uint32_t chunk = uint32_t(std::max<uint64_t>(kChunk, ceil_div(n_items, uint64_t(kSMs) * 8)));
   DBuf<uint32_t> hist(c, kBins + 1);
   hist.zero();
@@ -279,57 +371,49 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   uint32_t V = 0;
   QGM_CUDA(cudaMemcpyAsync(&V, total.p, 4, cudaMemcpyDeviceToHost, c.stream));
   QGM_CUDA(cudaStreamSynchronize(c.stream));
+  if (V == 0) return empty();
   out.V = V;
-  out.pairs.alloc(c, std::max<uint64_t>(V, 1));
+  DBuf<uint64_t> p1(c, V);
   hist.zero();  // reused as the per-bin global cursors
-  const size_t smem = kChunk * sizeof(uint64_t);
+  const size_t smem = kChunk * (sizeof(uint64_t) + sizeof(uint8_t));
   QGM_CUDA(cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n_items, kChunk), uint64_t(kSMs) * 4));
   {
     KernelScope ks(c, "k_part_scatter");
-    QGM_KERNEL(c, k_part_scatter, grid, kPartThreads, smem, gen, n_items, shift, out.boff.p, hist.p, out.pairs.p);
+    QGM_KERNEL(c, k_part_scatter, grid, kPartThreads, smem, gen, n_items, shift, out.boff.p, hist.p, p1.p);
   }
   // P2: refine to the top min(2q, 16) code bits (short reuse distance of the
   // reference-index sectors in the join) and convert to join items. Runs even
-  // when the first pass already grouped by every key bit (2q <= 8): then it
-  // only converts.
-  const unsigned key_bits = std::min(2 * q, 16u);
-  out.sub_bits = key_bits;
-  if (V == 0) {  // every read shorter than q
-    out.soff.alloc(c, (1u << key_bits) + 1);
-    out.soff.zero();
-    return;
-  }
-  const unsigned kshift = 2 * q - key_bits, sub = key_bits - bits;
+  // when P1 already grouped by every key bit (2q <= 8): then it only converts.
+  Refine rf;
+  rf.shift = shift;
+  rf.kshift = 2 * q - key_bits;
+  rf.nbins = 1u << bits;
+  rf.lengths = reads.lengths.p;
+  rf.stride = reads.stride;
+  rf.by_stride = FastDiv(std::max<uint32_t>(reads.stride, 1));
+  rf.q = q;
+  rf.uniform = reads.min_len == reads.stride;
+  const unsigned sub = key_bits - bits;
   const uint32_t keys = 1u << key_bits;
   DBuf<uint32_t> h2(c, keys + 1);
   out.soff.alloc(c, keys + 1);
-  DBuf<uint32_t>& off = out.soff;
   h2.zero();
   const unsigned grid2 = unsigned(std::min<uint64_t>(ceil_div(V, kChunk), uint64_t(kSMs) * 4));
   {
     KernelScope ks(c, "k_refine_hist");
-    QGM_KERNEL(c, k_refine_hist, grid2, kPartThreads, 0, out.pairs.p, V, kshift, sub, h2.p);
+    QGM_KERNEL(c, k_refine_hist, grid2, kPartThreads, 0, p1.p, V, out.boff.p, rf, sub, h2.p);
   }
-  exclusive_scan_u32(c, h2.p, off.p, keys + 1, nullptr, nullptr);
+  exclusive_scan_u32(c, h2.p, out.soff.p, keys + 1, nullptr, nullptr);
   h2.zero();  // per-key cursors
-  DBuf<uint64_t> refined(c, std::max<uint64_t>(V, 1));
+  out.pairs.alloc(c, V);
   const size_t smem2 = kChunk * (sizeof(uint64_t) + sizeof(uint16_t));
   QGM_CUDA(cudaFuncSetAttribute(k_refine_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
-  ItemConv conv;
-  conv.words = reads.words.p;
-  conv.lengths = reads.lengths.p;
-  conv.W = reads.W;
-  conv.stride = reads.stride;
-  conv.by_stride = FastDiv(std::max<uint32_t>(reads.stride, 1));
-  conv.q = q;
-  conv.lmask = kshift ? (1u << kshift) - 1u : 0u;
   {
     KernelScope ks(c, "k_refine_scatter");
-    QGM_KERNEL(c, k_refine_scatter, grid2, kPartThreads, smem2, out.pairs.p, V, kshift, sub, off.p, h2.p, conv,
-               refined.p);
+    QGM_KERNEL(c, k_refine_scatter, grid2, kPartThreads, smem2, p1.p, V, out.boff.p, rf, sub, out.soff.p, h2.p,
+               out.pairs.p);
   }
-  out.pairs.swap(refined);
 }
 
 }  // namespace qgm

@@ -145,3 +145,26 @@ def test_c2_full_size_hit_parity_with_oracle(ctx, oracle):
     want, ost = oracle.map(ref, cb, codes, 100, lengths, q=16, mode=1)
     assert st["unique_candidates"] == ost["unique_candidates"]
     assert _same(got, want), (got.size, want.size)
+
+
+@pytest.mark.parametrize("stride,band", [(130, 32), (600, 64)])
+def test_variable_length_reads_match_oracle(ctx, oracle, stride, band):
+    """Reads of mixed lengths (some shorter than q, some filling the stride),
+    several chromosomes, both modes: exercises the per-read length paths (the
+    join item's n - q - o field, and -- for strides above q + 511 -- the
+    join's reload of the read length)."""
+    import paper_1403_1706_b200 as qgm
+    L = 400_000
+    ref = qgm.random_reference(21, L)
+    cb = np.array([0, 150_000, 260_000, L], np.uint64)
+    codes, lengths, *_ = qgm.simulate_reads(22, ref, cb, 2000, stride, 0.03)
+    rng = np.random.default_rng(5)
+    lengths = np.minimum(lengths, rng.integers(5, stride + 1, lengths.size).astype(np.uint32))
+    lengths[:7] = stride
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, stride)
+    for mode in (0, 1):
+        got, st = ctx.map(reads, R, q=12, mode=mode, band_width=band)
+        want, ost = oracle.map(ref, cb, codes, stride, lengths, q=12, mode=mode, band=band)
+        assert st["unique_candidates"] == ost["unique_candidates"]
+        assert _same(got, want), (mode, got.size, want.size)
