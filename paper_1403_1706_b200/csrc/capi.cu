@@ -267,9 +267,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   out.stats[7] = fst[1];
   {
     StageScope s(c, kStageSort);
-    radix_sort(c, keys, alt, nullptr, nullptr, n_raw, 0, key_bits);
-    if (alt.n < n_raw) alt.alloc(c, std::max<uint64_t>(n_raw, 1));
-    n_u = select_u64(c, keys.p, nullptr, nullptr, n_raw, alt.p, nullptr);
+    n_u = dedup_keys(c, keys.p, n_raw, alt);  // unique candidates, any order (validation is per key)
   }
   DBuf<uint64_t> hkeys(c, std::max<uint64_t>(n_u, 1)), hkeys_alt;
   DBuf<uint32_t> hvals(c, std::max<uint64_t>(n_u, 1)), hvals_alt;

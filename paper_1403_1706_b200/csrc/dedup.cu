@@ -1,0 +1,95 @@
+// dedup.cu -- stage 3 on the map path: the unique (read, strand, diagonal)
+// candidate keys, by hashing instead of sorting.
+//
+// Validation is a pure function of the key and the strata stage sorts its
+// hits itself, so the unique candidates need no order: every raw key is
+// inserted into an open-addressing table (64-bit atomicCAS, linear probing,
+// load factor <= 2/3) and the table is compacted in slot order. Replaces the
+// 6-pass LSD radix sort + adjacent-unique of the standalone qgm_cands_unique
+// (radix_sort.cu), which cost ~0.5 ms on C2's 5.2M keys; here: one memset,
+// one insert pass (8 B read + one CAS per key) and two streaming passes over
+// the table.
+#include "internal.hpp"
+
+namespace qgm {
+namespace {
+
+constexpr uint64_t kEmpty = ~0ull;  // never a key (the padded diagonal field is < 2^diag_bits - 1)
+constexpr int kTile = 4096;         // table slots per compaction tile
+constexpr int kDedupThreads = 256;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+
+__global__ void k_hash_insert(const uint64_t* __restrict__ keys, uint64_t n, uint64_t* __restrict__ table,
+                              uint64_t tmask) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t key = keys[i];
+    uint64_t slot = mix64(key) & tmask;
+    while (true) {
+      const uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(table + slot), kEmpty, key);
+      if (prev == kEmpty || prev == key) break;
+      slot = (slot + 1) & tmask;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kDedupThreads) k_tile_count(const uint64_t* __restrict__ table, uint64_t T,
+                                                              uint32_t* __restrict__ counts) {
+  __shared__ uint32_t ws[33];
+  const uint64_t base = uint64_t(blockIdx.x) * kTile;
+  uint32_t c = 0;
+  for (uint32_t j = threadIdx.x; j < kTile; j += kDedupThreads) c += table[base + j] != kEmpty;
+  uint32_t tot;
+  block_exclusive_scan<uint32_t>(c, ws, &tot);
+  if (threadIdx.x == 0) counts[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kDedupThreads) k_tile_emit(const uint64_t* __restrict__ table,
+                                                             const uint32_t* __restrict__ offs,
+                                                             uint64_t* __restrict__ out) {
+  __shared__ uint32_t ws[33];
+  const uint64_t base = uint64_t(blockIdx.x) * kTile;
+  uint32_t run = offs[blockIdx.x];
+  for (uint32_t j0 = 0; j0 < kTile; j0 += kDedupThreads) {
+    const uint64_t v = table[base + j0 + threadIdx.x];
+    const uint32_t f = v != kEmpty;
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan<uint32_t>(f, ws, &tot);
+    if (f) out[run + ex] = v;
+    run += tot;
+  }
+}
+
+}  // namespace
+
+uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out) {
+  if (n == 0) return 0;
+  uint64_t T = kTile;
+  while (T < n + n / 2) T <<= 1;  // load factor <= 2/3: at C2 the table (64 MiB) stays L2-resident
+  DBuf<uint64_t> table(c, T);
+  QGM_CUDA(cudaMemsetAsync(table.p, 0xFF, T * sizeof(uint64_t), c.stream));
+  {
+    KernelScope ks(c, "k_hash_insert");
+    const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
+    QGM_KERNEL(c, k_hash_insert, grid, 256, 0, keys, n, table.p, T - 1);
+  }
+  const uint32_t tiles = uint32_t(T / kTile);
+  DBuf<uint32_t> counts(c, tiles + 1), total(c, 1);
+  QGM_KERNEL(c, k_tile_count, tiles, kDedupThreads, 0, table.p, T, counts.p);
+  exclusive_scan_u32(c, counts.p, counts.p, tiles, total.p, nullptr);
+  uint32_t h = 0;
+  QGM_CUDA(cudaMemcpyAsync(&h, total.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  if (out.n < h) out.alloc(c, std::max<uint64_t>(h, 1));
+  QGM_KERNEL(c, k_tile_emit, tiles, kDedupThreads, 0, table.p, counts.p, out.p);
+  return h;
+}
+
+}  // namespace qgm

@@ -244,6 +244,10 @@ void exclusive_scan_u32(Ctx& c, const uint32_t* in, uint32_t* out, uint64_t n, u
 uint64_t select_u64(Ctx& c, const uint64_t* keys, const uint32_t* vals, const uint32_t* flags, uint64_t n,
                     uint64_t* out_keys, uint32_t* out_vals);
 
+// dedup.cu -- unique keys (any order) of keys[0, n) into `out` (grown as
+// needed); returns their count.
+uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out);
+
 // radix_sort.cu -- stable LSD radix sort of u64 keys (+ optional u32 values)
 // on bits [begin_bit, end_bit). Sorted data ends up in keys/vals (buffers may
 // be swapped with the alternates).
