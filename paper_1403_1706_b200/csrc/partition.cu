@@ -239,7 +239,12 @@ __global__ void __launch_bounds__(kPartThreads) k_refine_hist(const uint64_t* __
     for (uint32_t k = threadIdx.x; k < width; k += kPartThreads) h[k] = 0;
     __syncthreads();
     if (bfirst == blast) {  // the common case: the chunk lies in one P1 bin
-      for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) atomicAdd(h + rf.key(in[i], b) - base, 1u);
+      uint64_t v[kPer];
+#pragma unroll
+      for (uint32_t k = 0; k < kPer; ++k) v[k] = __ldg(in + min(c0 + k * kPartThreads + threadIdx.x, c1 - 1));
+#pragma unroll
+      for (uint32_t k = 0; k < kPer; ++k)
+        if (c0 + k * kPartThreads + threadIdx.x < c1) atomicAdd(h + rf.key(v[k], b) - base, 1u);
     } else {
       for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) {
         while (sboff[b + 1] <= i) ++b;
@@ -286,13 +291,17 @@ __global__ void __launch_bounds__(kPartThreads, 2) k_refine_scatter(const uint64
     uint64_t v[kPer];
     uint32_t kk[kPer];
 #pragma unroll
+    for (uint32_t k = 0; k < kPer; ++k) {  // every load first
+      const uint32_t i = c0 + k * kPartThreads + threadIdx.x;
+      v[k] = __ldg(in + min(i, c1 - 1));
+    }
+#pragma unroll
     for (uint32_t k = 0; k < kPer; ++k) {
       const uint32_t i = c0 + k * kPartThreads + threadIdx.x;
-      const uint64_t it = i < c1 ? in[i] : 0ull;
       if (i < c1 && bfirst != blast)
         while (sboff[b + 1] <= i) ++b;
-      kk[k] = i < c1 ? rf.key(it, b) - base : ~0u;
-      v[k] = i < c1 ? rf.convert(it) : 0ull;
+      kk[k] = i < c1 ? rf.key(v[k], b) - base : ~0u;
+      v[k] = rf.convert(v[k]);
       if (i < c1) atomicAdd(cnt + kk[k], 1u);
     }
     __syncthreads();
