@@ -60,6 +60,18 @@ __device__ __forceinline__ uint32_t rc_code(uint32_t g, unsigned q) {
   return x >> (32 - 2 * q);
 }
 
+// Canonical code of the pair {g, rc(g)} used to key both strands with one
+// lookup (RefQIndex): the member with the smaller g * 0x9E3779B1 mod 2^32 (an
+// odd multiplier is a bijection, so the two members tie only for a
+// palindrome, g == rc(g)). Choosing by this hash rather than min(g, rc(g))
+// keeps canonical codes uniformly spread over the code space (min() would put
+// 7/16 of them below 4^(q-1)), so partition bins and join sub-bins stay
+// balanced.
+__device__ __forceinline__ uint32_t canon_code(uint32_t g, unsigned q) {
+  const uint32_t r = rc_code(g, q);
+  return g * 0x9E3779B1u <= r * 0x9E3779B1u ? g : r;
+}
+
 // Exact division of a 32-bit numerator by a runtime divisor d >= 1 with one
 // 64-bit multiply-high: M = floor((2^64-1)/d) + 1 (d == 1 is the identity).
 // Error of t*M/2^64 vs t/d is < t/2^64 < 1/d for t < 2^32, so the floor is exact.

@@ -63,8 +63,6 @@ struct ReadSource {
 // pos = the padded coordinate cbp[c] + p; extra = b | flag << 3, b = ref[x-1]
 // or 4 when x-1 is outside the chromosome or masked; with `packed`, extra
 // goes into pos's top 4 bits.
-__device__ __forceinline__ uint32_t canon_code(uint32_t g, unsigned q) { return min(g, rc_code(g, q)); }
-
 struct RefSource {
   const uint64_t* ref;
   const uint64_t* mask;

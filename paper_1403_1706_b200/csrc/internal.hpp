@@ -176,7 +176,7 @@ struct Buckets {
 };
 
 // q-group index over the reference itself, keyed by CANONICAL q-gram codes
-// (min(code, rc(code)); SPEC.md:262-316's precomputed reference index with P
+// (canon_code: one fixed member of {code, rc(code)}; SPEC.md:262-316's precomputed reference index with P
 // ordered by q-gram as in PAPER.md:344, both strands in one index). Every
 // position x is listed under the canonical code of its forward window with
 // flag = (forward code != canonical); a position whose q-gram is its own

@@ -14,7 +14,7 @@
 // q-grams are partitioned by the top 16 bits of their code (partition.cu).
 //
 // Both strands come from ONE lookup per read q-gram: the reference index and
-// the read partition are keyed by canonical codes min(g, rc(g)) (RefQIndex),
+// the read partition are keyed by canonical codes (canon_code, RefQIndex),
 // and each occurrence's strand is flag(occurrence) XOR fr(read q-gram).
 //
 // One CTA owns one code sub-bin at a time (2^(2q-16) codes; 2048 group words

@@ -1,7 +1,7 @@
 // partition.cu -- per-batch read q-gram partition for the join (map path).
 //
 // The join (join.cu) only needs the batch's read q-grams grouped by the top
-// bits of their canonical code min(g, rc(g)) (RefQIndex), so that the warps in
+// bits of their canonical code (canon_code, RefQIndex), so that the warps in
 // flight touch a few MiB of the reference index (L2-resident) instead of all
 // of it; it never needs the full read-side q-group index. Passes:
 //   P0 histogram : per-CTA shared-memory histogram over 2^bits code bins
@@ -69,7 +69,7 @@ struct ItemGen {
     const unsigned sh = 2 * (s.o & 31);
     const uint64_t hi = sh ? (s.w0 << sh) | (s.w1 >> (64 - sh)) : s.w0;
     f = uint32_t(hi >> (64 - 2 * q));
-    g = min(f, rc_code(f, q));
+    g = canon_code(f, q);
     return t < n_items && s.o + q <= s.n;
   }
   // P1 fields: read base at o-1 (4 = none), complement of the base at o+q
