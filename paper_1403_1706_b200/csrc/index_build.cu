@@ -245,6 +245,25 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* _
 
 __global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
 
+// group start of word w relative to its sub-bin (< 2^16: a sub-bin holds at
+// most 2^16 codes and this is an exclusive prefix)
+__global__ void k_rank16(const uint32_t* __restrict__ S, uint64_t groups, unsigned wshift,
+                         const uint32_t* __restrict__ sb_d, uint16_t* __restrict__ r16) {
+  for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < groups; w += uint64_t(gridDim.x) * blockDim.x)
+    r16[w] = uint16_t(S[w] - sb_d[w >> wshift]);
+}
+
+// sub-bin s covers group words [(s << cs) / 32, ((s+1) << cs) / 32): its S'
+// range starts at S of its first word, its O range at S' of that
+__global__ void k_subbin_bounds(const uint32_t* __restrict__ S, const uint32_t* __restrict__ S1, uint32_t n_sub,
+                                unsigned cs, uint32_t* __restrict__ sb_d, uint32_t* __restrict__ sb_o) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s <= n_sub; s += gridDim.x * blockDim.x) {
+    const uint32_t d = S[uint32_t((uint64_t(s) << cs) >> 5)];
+    sb_d[s] = d;
+    sb_o[s] = S1[d];
+  }
+}
+
 __global__ void k_sample_S(const uint32_t* __restrict__ S, uint64_t len_in, uint32_t* __restrict__ out,
                            uint64_t len_out) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < len_out; i += uint64_t(gridDim.x) * blockDim.x)
@@ -467,6 +486,19 @@ void prepare_ref_index(Ctx& c, const Ref& ref, unsigned q) {
   index_from_buckets(c, B, false, ref.qidx.can, packed ? nullptr : &ref.qidx.extra);
   ref.qidx.packed = packed;
   ref.qidx.palindromes = n_pal;
+  const unsigned sub_bits = std::min(2 * q, 16u), cs = 2 * q - sub_bits;
+  ref.qidx.sub_bits = sub_bits;
+  if (cs >= 8) {  // >= 8 group words per sub-bin: whole 16-byte bulk copies of I and r16
+    const uint32_t n_sub = 1u << sub_bits;
+    ref.qidx.sb_d.alloc(c, n_sub + 1);
+    ref.qidx.sb_o.alloc(c, n_sub + 1);
+    QGM_KERNEL(c, k_subbin_bounds, unsigned(ceil_div(n_sub + 1, 256)), 256, 0, ref.qidx.can.S.p,
+               ref.qidx.can.S1.p, n_sub, cs, ref.qidx.sb_d.p, ref.qidx.sb_o.p);
+    const uint64_t groups = ref.qidx.can.groups;
+    ref.qidx.r16.alloc(c, groups);
+    QGM_KERNEL(c, k_rank16, unsigned(std::min<uint64_t>(ceil_div(groups, 256), kSMs * 16)), 256, 0,
+               ref.qidx.can.S.p, groups, cs - 5, ref.qidx.sb_d.p, ref.qidx.r16.p);
+  }
   ref.qidx.q = q;
 }
 

@@ -194,6 +194,13 @@ struct RefQIndex {
   uint64_t palindromes = 0;  // positions listed twice
   Index can;
   DBuf<uint8_t> extra;
+  // per join sub-bin s (the 2^sub_bits prefixes of the partition, sub_bits =
+  // min(2q, 16)): its distinct-code range [sb_d[s], sb_d[s+1]) of S' and
+  // occurrence range [sb_o[s], sb_o[s+1]) of O; built when a sub-bin spans
+  // >= 8 group words (the join stages these slices with bulk copies)
+  unsigned sub_bits = 0;
+  DBuf<uint32_t> sb_d, sb_o;
+  DBuf<uint16_t> r16;  // per group word: S[w] - sb_d[sub-bin of w] (group start inside its sub-bin)
 };
 constexpr unsigned kPackedPosBits = 28;
 

@@ -18,14 +18,16 @@
 // and each occurrence's strand is flag(occurrence) XOR fr(read q-gram).
 //
 // One CTA owns one code sub-bin at a time (2^(2q-16) codes; 2048 group words
-// at q=16): it stages the sub-bin's occupancy words in shared memory with one
-// coalesced load and rebuilds the group starts on chip (popcount prefix, u16
-// relative to S at the sub-bin's first word -- one global S read per
-// sub-bin), so every Group-And-Bit / Grouprank lookup (qgroup_index.hpp:50-57,
-// 80-96) of the sub-bin's read q-grams is a shared-memory hit. The S' / O
-// reads that follow fall in the sub-bin's contiguous slice of the reference
-// index and are L1/L2 local to the CTA. The occupancy array is read from HBM
-// exactly once per batch, in order; S is not read at all.
+// at q=16). One elected thread stages, with 1-D TMA bulk copies completing on
+// an mbarrier, the sub-bin's occupancy words and -- when they fit the staging
+// buffers (every sub-bin of a 100 Mbp reference) -- its contiguous slices of
+// S' and O; the group starts are rebuilt on chip (warp-scanned popcount
+// prefix, u16 relative to the sub-bin's first distinct code). Every
+// Group-And-Bit / Grouprank lookup (qgroup_index.hpp:50-57, 80-96) and, for a
+// staged sub-bin, every S' and O read of its read q-grams is then a
+// shared-memory hit; unstaged sub-bins (huge references, repeat-dense
+// sub-bins) read S' / O through L1/L2. The reference index is read from HBM
+// once per batch, in order, as bulk transfers; S is not read at all.
 //
 // Per warp step: kItems read q-grams per lane looked up, then the union of the
 // occurrence intervals expanded cooperatively, one (reference occurrence,
@@ -67,6 +69,9 @@ struct JoinArgs {
   unsigned q;
   const uint32_t *I, *S, *S1, *O;
   const uint8_t* X;  // extra byte per occurrence (unpacked layout only)
+  const uint32_t *sb_d, *sb_o;  // per sub-bin S' / O ranges (staging; null = never stage)
+  const uint16_t* r16;          // group starts inside the sub-bin (null: sub-bins of < 4 words)
+  uint32_t cap;                 // staging capacity of S' and of O (entries, multiple of 4)
   const uint32_t* rlen;
   uint32_t m;
   FastDiv by_m;
@@ -74,7 +79,7 @@ struct JoinArgs {
   int strands;
   unsigned diag_bits;
   uint64_t* out;
-  uint64_t cap;
+  uint64_t cap_out;
   unsigned long long* counter;
   unsigned long long* stats;
 };
@@ -82,9 +87,11 @@ struct JoinArgs {
 // One (reference occurrence k, join item it) pair -> candidate key; false if
 // its strand is not requested or the run-start rule suppresses it (the
 // (q+1)-gram one base to the left on the same diagonal also matches).
+// Op: O, or the shared-memory slice of a staged sub-bin (generic pointer).
 template <bool kRunStart, bool kPacked>
-__device__ __forceinline__ bool expand(const JoinArgs& a, uint32_t k, uint64_t it, uint64_t& key) {
-  const uint32_t ov = __ldg(a.O + k);
+__device__ __forceinline__ bool expand(const JoinArgs& a, const uint32_t* Op, uint32_t k, uint64_t it,
+                                       uint64_t& key) {
+  const uint32_t ov = Op[k];
   const uint32_t xp = kPacked ? (ov & kPosMask) : ov;
   const uint32_t ex = kPacked ? (ov >> kPackedPosBits) : uint32_t(__ldg(a.X + k));
   const uint32_t rev = ((ex >> 3) ^ uint32_t(it >> kItemFrShift)) & 1u;
@@ -103,49 +110,90 @@ __device__ __forceinline__ bool expand(const JoinArgs& a, uint32_t k, uint64_t i
 
 template <bool kRunStart, bool kPacked>
 __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
-  extern __shared__ uint32_t s_dyn[];  // I words, then u16 group starts
+  // dynamic: I words [nw], u16 group starts [nw] (+pad to 16 B), S' slice
+  // [cap], O slice [cap]
+  extern __shared__ __align__(16) uint32_t s_dyn[];
   const uint32_t nw = a.words;
   uint32_t* sI = s_dyn;
   uint16_t* sR = reinterpret_cast<uint16_t*>(s_dyn + nw);
+  uint32_t* sS1 = s_dyn + nw + (((nw + 1) / 2 + 3) & ~3u);
+  uint32_t* sO = sS1 + a.cap;
   __shared__ uint32_t s_k0[kJoinWarps][kRanges];
   __shared__ uint32_t s_k1[kJoinWarps][kRanges];
   __shared__ uint8_t s_slot[kJoinWarps][kRanges];  // item slot u*32 + lane
   __shared__ uint64_t s_out[kJoinWarps][kStage];
-  __shared__ uint32_t s_ws[33];
+  __shared__ __align__(8) uint64_t s_bar;
 
   const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
-  uint32_t staged = 0;
+  uint32_t staged_keys = 0;
   unsigned long long n_hit = 0, n_occ = 0;
+  const bool bulk_I = a.r16 != nullptr;  // sub-bins of >= 8 group words: whole 16-byte chunks
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
 
   auto flush = [&]() {
     unsigned long long base = 0;
-    if (lane == 0 && staged) base = atomicAdd(a.counter, (unsigned long long)staged);
+    if (lane == 0 && staged_keys) base = atomicAdd(a.counter, (unsigned long long)staged_keys);
     base = __shfl_sync(kFull, base, 0);
-    for (uint32_t i = lane; i < staged; i += 32)
-      if (base + i < a.cap) a.out[base + i] = s_out[wid][i];
-    staged = 0;
+    for (uint32_t i = lane; i < staged_keys; i += 32)
+      if (base + i < a.cap_out) a.out[base + i] = s_out[wid][i];
+    staged_keys = 0;
     __syncwarp();
   };
   auto stage_key = [&](bool emit, uint64_t key) {  // all lanes call it
     const unsigned m = __ballot_sync(kFull, emit);
-    if (emit) s_out[wid][staged + __popc(m & lanemask_lt())] = key;
-    staged += __popc(m);
+    if (emit) s_out[wid][staged_keys + __popc(m & lanemask_lt())] = key;
+    staged_keys += __popc(m);
     __syncwarp();
-    if (staged > kStage - 32) flush();
+    if (staged_keys > kStage - 32) flush();
   };
 
-  // group-start scan: `per` consecutive words per thread
-  const uint32_t per = max(1u, nw / kJoinThreads);
-  const uint32_t my_w0 = threadIdx.x * per;
-  const bool scan_active = my_w0 < nw;
 
   for (uint32_t sb = blockIdx.x; sb < a.n_sub; sb += gridDim.x) {
     const uint32_t b0 = __ldg(a.soff + sb), b1 = __ldg(a.soff + sb + 1);
     if (b0 == b1) continue;  // CTA-uniform
     // first group word of the sub-bin (sub-bins narrower than a word share it)
     const uint32_t w0 = uint32_t((uint64_t(sb) << a.code_shift) >> 5);
-    const uint32_t gbase = __ldg(a.S + w0);
-    for (uint32_t i = threadIdx.x; i < nw; i += kJoinThreads) sI[swz(i)] = __ldg(a.I + w0 + i);
+    uint32_t d0, sA = 0, oA = 0;
+    bool staged = false;
+    uint32_t sN = 0, oN = 0;
+    if (a.sb_d) {
+      d0 = __ldg(a.sb_d + sb);
+      const uint32_t d1 = __ldg(a.sb_d + sb + 1), o0 = __ldg(a.sb_o + sb), o1 = __ldg(a.sb_o + sb + 1);
+      sA = d0 & ~3u;
+      sN = ((d1 + 1 + 3) & ~3u) - sA;  // S'[d0 .. d1] inclusive, 16-byte aligned
+      oA = o0 & ~3u;
+      oN = ((o1 + 3) & ~3u) - oA;
+      staged = kPacked && sN <= a.cap && oN <= a.cap;
+    } else {
+      d0 = __ldg(a.S + w0);
+    }
+    const uint32_t bytes = (bulk_I ? nw * 6u : 0u) + (staged ? (sN + oN) * 4u : 0u);
+    if (threadIdx.x == 0 && bytes) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&s_bar, bytes);
+      if (bulk_I) {
+        bulk_g2s(sI, a.I + w0, nw * 4u, &s_bar);
+        bulk_g2s(sR, a.r16 + w0, nw * 2u, &s_bar);
+      }
+      if (staged) {
+        bulk_g2s(sS1, a.S1 + sA, sN * 4u, &s_bar);
+        bulk_g2s(sO, a.O + oA, oN * 4u, &s_bar);
+      }
+    }
+    if (!bulk_I) {  // sub-bins of < 8 group words: load and rank on the spot
+      if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (uint32_t i = 0; i < nw; ++i) {
+          const uint32_t w = __ldg(a.I + w0 + i);
+          sI[i] = w;
+          sR[i] = uint16_t(run);
+          run += __popc(w);
+        }
+      }
+      __syncthreads();
+    }
     // warm L2 with the next sub-bin's occupancy words while this one is processed
     {
       const uint32_t nsb = sb + gridDim.x;
@@ -154,21 +202,12 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
       }
     }
-    __syncthreads();
-    {  // group starts on chip: exclusive popcount prefix
-      uint32_t sum = 0;
-      if (scan_active)
-        for (uint32_t i = 0; i < per; ++i) sum += __popc(sI[swz(my_w0 + i)]);
-      uint32_t tot;
-      uint32_t run = block_exclusive_scan<uint32_t>(sum, s_ws, &tot);
-      if (scan_active)
-        for (uint32_t i = 0; i < per; ++i) {
-          const uint32_t x = swz(my_w0 + i);
-          sR[x] = uint16_t(run);
-          run += __popc(sI[x]);
-        }
+    if (bytes) {
+      mbar_wait(&s_bar, phase);
+      phase ^= 1u;
     }
-    __syncthreads();
+    const uint32_t* S1p = staged ? sS1 - sA : a.S1;
+    const uint32_t* Op = staged ? sO - oA : a.O;
     // the sub-bin's items split evenly over the warps (no warp idles at the
     // end-of-sub-bin barrier while another runs a second full round)
     const uint32_t nitems = b1 - b0;
@@ -191,12 +230,11 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
         const bool ok = pr != ~0ull;
         const uint32_t g = gsub | uint32_t(pr >> kItemCodeShift);
         const uint32_t wl = ok ? (g >> 5) - w0 : 0u, bit = g & 31u;
-        const uint32_t x = swz(wl);
-        const uint32_t w = sI[x];
+        const uint32_t w = sI[wl];
         const bool hit = ok && ((w >> bit) & 1u);
-        const uint32_t b = gbase + sR[x] + __popc(w & ((1u << bit) - 1u));
-        rk0[u] = hit ? __ldg(a.S1 + b) : 0u;
-        rk1[u] = hit ? __ldg(a.S1 + b + 1) : 0u;
+        const uint32_t b = d0 + sR[wl] + __popc(w & ((1u << bit) - 1u));
+        rk0[u] = hit ? S1p[b] : 0u;
+        rk1[u] = hit ? S1p[b + 1] : 0u;
       }
 #pragma unroll
       for (int u = 0; u < kItems; ++u) {
@@ -239,7 +277,7 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
         const uint32_t rounds = __reduce_max_sync(kFull, nin);
         for (uint32_t t = 0; t < rounds; ++t) {
           uint64_t key = 0;
-          const bool emit = t < nin && expand<kRunStart, kPacked>(a, k0 + t, it, key);
+          const bool emit = t < nin && expand<kRunStart, kPacked>(a, Op, k0 + t, it, key);
           stage_key(emit, key);
         }
         unsigned lm = __ballot_sync(kFull, longi);
@@ -250,14 +288,14 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
           const uint64_t lit = __shfl_sync(kFull, it, src);
           for (uint32_t t0 = 0; t0 < llen; t0 += 32) {
             uint64_t key = 0;
-            const bool emit = t0 + lane < llen && expand<kRunStart, kPacked>(a, lk0 + t0 + lane, lit, key);
+            const bool emit = t0 + lane < llen && expand<kRunStart, kPacked>(a, Op, lk0 + t0 + lane, lit, key);
             stage_key(emit, key);
           }
         }
       }
       __syncwarp();
     }
-    __syncthreads();  // sI / sR are rewritten for the next sub-bin
+    __syncthreads();  // the staging buffers are rewritten for the next sub-bin
   }
   flush();
   n_hit = warp_reduce_sum(n_hit);
@@ -302,13 +340,27 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   const bool rs = mode == 1;
   const void* kfn = X.packed ? (rs ? (const void*)k_join<true, true> : (const void*)k_join<false, true>)
                              : (rs ? (const void*)k_join<true, false> : (const void*)k_join<false, false>);
-  const size_t smem = size_t(a.words) * (sizeof(uint32_t) + sizeof(uint16_t));
+  // staging capacity: what is left of a quarter of the SM's shared memory
+  // (4 resident CTAs) after the static arrays, I words and group starts
+  cudaFuncAttributes fa;
+  QGM_CUDA(cudaFuncGetAttributes(&fa, kfn));
+  int dev = 0, smem_sm = 0;
+  QGM_CUDA(cudaGetDevice(&dev));
+  QGM_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  const size_t fixed = size_t(a.words) * 4 + (size_t((a.words + 1) / 2 + 3) & ~size_t(3)) * 4;
+  const int64_t room = int64_t(smem_sm) / 4 - 1024 - int64_t(fa.sharedSizeBytes) - int64_t(fixed);
+  const bool can_stage = X.packed && X.sb_d.p && X.sub_bits == rp.sub_bits && room >= 2 * 4 * 256;
+  a.r16 = X.sub_bits == rp.sub_bits ? X.r16.p : nullptr;
+  a.sb_d = can_stage ? X.sb_d.p : nullptr;
+  a.sb_o = can_stage ? X.sb_o.p : nullptr;
+  a.cap = can_stage ? uint32_t(room / 8) & ~3u : 0u;
+  const size_t smem = fixed + size_t(2) * a.cap * 4;
   QGM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const unsigned grid = std::min<unsigned>(a.n_sub, resident_grid(kfn, kJoinThreads, smem));
   for (int attempt = 0; attempt < 2; ++attempt) {
     counter.zero();
     a.out = keys.p;
-    a.cap = keys.n;
+    a.cap_out = keys.n;
     if (rp.V > 0) {
       KernelScope ks(c, "k_join");
       void* args[] = {&a};
