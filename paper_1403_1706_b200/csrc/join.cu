@@ -150,25 +150,37 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
   };
 
 
+  // the sub-bin's bounds (item range, S' range, O range), loaded one
+  // iteration ahead
+  struct Bounds { uint32_t b0, b1, d0, d1, o0, o1; };
+  auto load_bounds = [&](uint32_t s, Bounds& bd) {
+    if (s >= a.n_sub) return;
+    bd.b0 = __ldg(a.soff + s);
+    bd.b1 = __ldg(a.soff + s + 1);
+    if (a.sb_d) {
+      bd.d0 = __ldg(a.sb_d + s);
+      bd.d1 = __ldg(a.sb_d + s + 1);
+      bd.o0 = __ldg(a.sb_o + s);
+      bd.o1 = __ldg(a.sb_o + s + 1);
+    } else {
+      bd.d0 = __ldg(a.S + uint32_t((uint64_t(s) << a.code_shift) >> 5));
+      bd.d1 = bd.o0 = bd.o1 = 0;
+    }
+  };
+  Bounds nxt{};
+  load_bounds(blockIdx.x, nxt);
   for (uint32_t sb = blockIdx.x; sb < a.n_sub; sb += gridDim.x) {
-    const uint32_t b0 = __ldg(a.soff + sb), b1 = __ldg(a.soff + sb + 1);
+    const Bounds cur = nxt;
+    load_bounds(sb + gridDim.x, nxt);
+    const uint32_t b0 = cur.b0, b1 = cur.b1;
     if (b0 == b1) continue;  // CTA-uniform
     // first group word of the sub-bin (sub-bins narrower than a word share it)
     const uint32_t w0 = uint32_t((uint64_t(sb) << a.code_shift) >> 5);
-    uint32_t d0, sA = 0, oA = 0;
-    bool staged = false;
-    uint32_t sN = 0, oN = 0;
-    if (a.sb_d) {
-      d0 = __ldg(a.sb_d + sb);
-      const uint32_t d1 = __ldg(a.sb_d + sb + 1), o0 = __ldg(a.sb_o + sb), o1 = __ldg(a.sb_o + sb + 1);
-      sA = d0 & ~3u;
-      sN = ((d1 + 1 + 3) & ~3u) - sA;  // S'[d0 .. d1] inclusive, 16-byte aligned
-      oA = o0 & ~3u;
-      oN = ((o1 + 3) & ~3u) - oA;
-      staged = kPacked && sN <= a.cap && oN <= a.cap;
-    } else {
-      d0 = __ldg(a.S + w0);
-    }
+    const uint32_t d0 = cur.d0;
+    const uint32_t sA = d0 & ~3u, oA = cur.o0 & ~3u;
+    const uint32_t sN = ((cur.d1 + 1 + 3) & ~3u) - sA;  // S'[d0 .. d1] inclusive, 16-byte aligned
+    const uint32_t oN = ((cur.o1 + 3) & ~3u) - oA;
+    const bool staged = kPacked && a.sb_d && sN <= a.cap && oN <= a.cap;
     const uint32_t bytes = (bulk_I ? nw * 6u : 0u) + (staged ? (sN + oN) * 4u : 0u);
     if (threadIdx.x == 0 && bytes) {
       fence_proxy_async();
@@ -182,6 +194,20 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
         bulk_g2s(sO, a.O + oA, oN * 4u, &s_bar);
       }
     }
+    // warm L2 with the next sub-bin's slices while this one is processed
+    if (threadIdx.x == 32 && sb + gridDim.x < a.n_sub && nxt.b0 != nxt.b1) {
+      const uint32_t nw0 = uint32_t((uint64_t(sb + gridDim.x) << a.code_shift) >> 5);
+      if (bulk_I) {
+        bulk_prefetch_l2(a.I + nw0, nw * 4u);
+        bulk_prefetch_l2(a.r16 + nw0, nw * 2u);
+      }
+      const uint32_t nsA = nxt.d0 & ~3u, noA = nxt.o0 & ~3u;
+      const uint32_t nsN = ((nxt.d1 + 1 + 3) & ~3u) - nsA, noN = ((nxt.o1 + 3) & ~3u) - noA;
+      if (kPacked && a.sb_d && nsN <= a.cap && noN <= a.cap) {
+        bulk_prefetch_l2(a.S1 + nsA, nsN * 4u);
+        bulk_prefetch_l2(a.O + noA, noN * 4u);
+      }
+    }
     if (!bulk_I) {  // sub-bins of < 8 group words: load and rank on the spot
       if (threadIdx.x == 0) {
         uint32_t run = 0;
@@ -193,14 +219,6 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
         }
       }
       __syncthreads();
-    }
-    // warm L2 with the next sub-bin's occupancy words while this one is processed
-    {
-      const uint32_t nsb = sb + gridDim.x;
-      if (nsb < a.n_sub && threadIdx.x * 32u < nw) {
-        const uint32_t* p = a.I + uint32_t((uint64_t(nsb) << a.code_shift) >> 5) + threadIdx.x * 32u;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-      }
     }
     if (bytes) {
       mbar_wait(&s_bar, phase);
