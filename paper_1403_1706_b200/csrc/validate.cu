@@ -105,10 +105,12 @@ template <> struct Band<uint64_t> {
 // every row with non-decreasing cost, so k >= min_t D[i][t] >= D[i][0] -
 // popc(Mv) at any row i; once that bound exceeds kmax the candidate cannot
 // pass the identity threshold (used by the map path only, kmax < 0 = never).
-template <class T, bool kCheck>
+template <class T, bool kCheck, bool kFull>
 __device__ __forceinline__ bool myers_rows(const ValArgs& a, uint32_t r, bool rev, uint32_t n, int64_t F, uint32_t L,
-                                           int64_t cbeg, int64_t cend, T mask, T& Pv, T& Mv, int& score0,
+                                           int64_t cbeg, int64_t cend, T mask_rt, T& Pv, T& Mv, int& score0,
                                            int kmax) {
+  // kFull: the band fills the word (B = 32 / 64), every mask is a no-op
+  const T mask = kFull ? T(~T(0)) : mask_rt;
   constexpr int NW = Band<T>::kWords;
   const uint2* rp = a.rplanes + uint64_t(r) * a.Wp;
   Win w[NW + 1];
@@ -194,9 +196,15 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a) {
         const int64_t F = cbeg + w0;
         // map path: abandon candidates that can no longer reach the threshold
         const int kmax = a.mode == 0 ? int((uint64_t(100 - a.pct) * n) / 100) : -1;
-        const bool done = (w0 >= 0 && w0 + int64_t(L) <= Lc)
-                              ? myers_rows<T, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax)
-                              : myers_rows<T, true>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax);
+        const bool interior = w0 >= 0 && w0 + int64_t(L) <= Lc;
+        const bool full = a.B == sizeof(T) * 8;
+        bool done;
+        if (interior && full)
+          done = myers_rows<T, false, true>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax);
+        else if (interior)
+          done = myers_rows<T, false, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax);
+        else
+          done = myers_rows<T, true, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax);
         int v = score0, best = score0;
         unsigned tbest = 0;
         for (unsigned t = 1; t < a.B; ++t) {
