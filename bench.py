@@ -147,10 +147,19 @@ def algorithmic_bytes(kernel, cfg, st, ref_bp, n_reads):
         n_look = 2 * (ref_bp - q + 1)
         return ref_bp / 4 + 4 * n_look + 12 * st["lookups_hit"] + 4 * st["occurrences"] + 8 * st["raw_candidates"]
     if kernel == "k_join":
-        # bucketed read q-grams (8 B) + both strands' I and S words (4+4 B per
-        # group, every bucket holds read q-grams at these batch sizes) + two S'
-        # entries per hit + O (4 B) and prev (1 B) per occurrence + 8 B per key
-        return 8 * V + 16 * groups + 8 * st["lookups_hit"] + 5 * st["occurrences"] + 8 * st["raw_candidates"]
+        # canonical-code join (join.cu): read join items (8 B) + the occupancy
+        # words (4 B) and u16 group starts (2 B) of the one canonical index,
+        # each once + the two S' entries per lookup hit + one O word per
+        # occurrence visited + 8 B per candidate key written
+        return 8 * V + 6 * groups + 8 * st["lookups_hit"] + 4 * st["occurrences"] + 8 * st["raw_candidates"]
+    if kernel == "k_part_hist":
+        return n_reads * rlen / 4 + 4 * n_reads
+    if kernel in ("k_part_scatter", "k_refine_scatter"):
+        return (n_reads * rlen / 4 + 4 * n_reads if kernel == "k_part_scatter" else 8 * V) + 8 * V
+    if kernel == "k_refine_hist":
+        return 8 * V
+    if kernel == "k_hash_insert":
+        return 8 * st["raw_candidates"] + 8 * st["unique_candidates"]
     if kernel == "k_bucket_rank":
         return n_reads * rlen / 4 + 4 * V
     if kernel == "k_bucket_scatter":
@@ -297,6 +306,26 @@ def run_gpu(args):
                     "frac": round(ach / peak, 4), "traffic": traffic, "peak_source": peak_kind,
                     "algorithmic_bytes": int(ab), "launch_ms": round(per_launch[dom], 4),
                     "share_of_step": round(ktimes[dom][0] / prof_steps / (sum(times) / len(times)), 4)}
+    # every timed kernel against its own bound (HBM bytes, or for the
+    # INT-ALU-bound validation the warp-instruction issue rate: 4 per SM per
+    # clock, instruction count from the committed ncu profile)
+    stage_roof = {}
+    for kname, ms in per_launch.items():
+        ab = algorithmic_bytes(kname, cfg, st, ref_bp, n_reads)
+        if ab is not None and kname != "k_validate":
+            ach = ab / (ms / 1e3) / 1e9
+            stage_roof[kname] = {"bound": "hbm", "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 4)}
+    if "k_validate" in per_launch:
+        ip = os.path.join(ROOT, "profiles", f"instructions_{args.config}.json")
+        inst = json.load(open(ip)).get("k_validate") if os.path.exists(ip) else None
+        if inst:
+            clk = (clocks.get("sm_mhz") or 1965) * 1e6
+            peak_issue = 148 * 4 * clk
+            ach = inst / (per_launch["k_validate"] / 1e3)
+            stage_roof["k_validate"] = {"bound": "issue (INT ALU)", "achieved_warp_inst_per_s": round(ach / 1e9, 1),
+                                        "peak": round(peak_issue / 1e9, 1), "unit": "G warp-inst/s",
+                                        "frac": round(ach / peak_issue, 4),
+                                        }
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "reads/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 3), "higher_is_better": True,
@@ -309,6 +338,7 @@ def run_gpu(args):
                 "h2d_bytes_per_step": int(words.nbytes + lengths.nbytes), "d2h_bytes_per_step": int(n_hits * 16 + 64)},
         "gpu_launches": int(launches),
         "roofline": roof,
+        "stage_roofline": stage_roof,
         "clocks": clocks,
         "step_ms": [round(t, 3) for t in times],
         "e2e_step_ms": [round(t, 3) for t in e2e_times],
@@ -390,7 +420,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--clock-period", type=float, default=0.2, help="NVML clock sampling period (s)")
+    ap.add_argument("--clock-period", type=float, default=0.005, help="NVML clock sampling period (s)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
