@@ -287,8 +287,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   alt.release();
   {
     StageScope s(c, kStageStrata);
-    radix_sort(c, hkeys, hkeys_alt, &hvals, &hvals_alt, n_val, 0, key_bits);
-    out.n = stratify_hits(c, ref, hkeys.p, hvals.p, n_val, reads.n, rb, int(P.mode), out.hits);
+    out.n = stratify_unsorted(c, ref, hkeys, hvals, n_val, reads.n, int(P.mode), out.hits);
   }
   out.stats[0] = n_raw;
   out.stats[1] = n_u;

@@ -318,6 +318,9 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
 
 // strata.cu -- dedup (read, chrom, ref_start, strand) keeping min k, then
 // best-stratum / all; writes qgm_hit records, returns their count.
+// Same output from hits in any order (per-read counting sort; map path).
+uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBuf<uint32_t>& hit_vals, uint64_t n,
+                           uint32_t n_reads, int mode, DBuf<uint8_t>& out);
 uint64_t stratify_hits(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const uint32_t* hit_vals, uint64_t n,
                        uint32_t n_reads, unsigned read_bits, int mode, DBuf<uint8_t>& out);
 

@@ -168,3 +168,30 @@ def test_variable_length_reads_match_oracle(ctx, oracle, stride, band):
         want, ost = oracle.map(ref, cb, codes, stride, lengths, q=12, mode=mode, band=band)
         assert st["unique_candidates"] == ost["unique_candidates"]
         assert _same(got, want), (mode, got.size, want.size)
+
+
+def test_reads_with_many_hits_match_oracle(ctx, oracle):
+    """A 300 bp unit repeated 60 times (with a few point differences per copy)
+    between random flanks: reads from the unit have more than 32 hits each in
+    all mode, which sends them through the strata stage's radix-sorted
+    big-segment path; best-stratum keeps the exact-copy ties."""
+    import paper_1403_1706_b200 as qgm
+    rng = np.random.default_rng(9)
+    unit = rng.integers(0, 4, 300).astype(np.uint8)
+    copies = []
+    for _ in range(60):
+        u = unit.copy()
+        pos = rng.integers(0, 300, 2)
+        u[pos] = rng.integers(0, 4, 2)
+        copies.append(u)
+    ref = np.concatenate([qgm.random_reference(3, 50_000), *copies, qgm.random_reference(4, 50_000)]).astype(np.uint8)
+    cb = np.array([0, ref.size], np.uint64)
+    codes, lengths, *_ = qgm.simulate_reads(8, ref, cb, 1500, 100, 0.02)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    for mode in (1, 0):
+        got, st = ctx.map(reads, R, q=12, mode=mode)
+        want, ost = oracle.map(ref, cb, codes, 100, lengths, q=12, mode=mode)
+        assert _same(got, want), (mode, got.size, want.size)
+        if mode == 1:
+            assert np.bincount(got["read_id"]).max() > 32
