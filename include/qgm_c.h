@@ -183,6 +183,14 @@ int qgm_ref_upload(qgm_ctx* ctx, const uint64_t* ref2bit, const uint64_t* chrom_
  * q-gram. qgm_map does this lazily on first use of a q; call it
  * ahead of time to keep it out of the first batch. References < 2^32 bases. */
 int qgm_ref_prepare(qgm_ctx* ctx, qgm_ref* ref, uint32_t q);
+/* Repeat mask on the device (build_reference_index's masking, SPEC.md:270,
+ * 302; default threshold 1000): every position whose forward q-gram occurs
+ * more than `threshold` times among the windows of its own chromosome is
+ * removed from P (ORed into the upload mask). Drops the cached reference
+ * index; call before qgm_ref_prepare / qgm_map. */
+int qgm_ref_mask_repeats(qgm_ctx* ctx, qgm_ref* ref, uint32_t q, uint64_t threshold);
+/* The current mask, ceil(total/64) words (all zero when there is none). */
+int qgm_ref_mask_download(qgm_ctx* ctx, const qgm_ref* ref, uint64_t* mask_bits);
 void qgm_ref_destroy(qgm_ref* ref);
 
 /* ---- filtration: Alg. 2 -------------- */

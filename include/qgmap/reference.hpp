@@ -32,19 +32,8 @@ struct Reference {
     if (!mask.empty()) mask.resize(codes.size(), 0);
   }
 
-  // Repeat mask: drop positions whose forward q-gram occurs
-  // more than `threshold` times in its own chromosome.
-  void mask_repeats(unsigned q, std::uint64_t threshold) {
-    mask.assign(codes.size(), 0);
-    for (std::uint32_t c = 0; c < chromosome_count(); ++c) {
-      const std::uint64_t b = chrom_begin[c], L = length(c);
-      if (L < q) continue;
-      std::map<qgram_code, std::uint64_t> freq;
-      for (std::uint64_t p = 0; p + q <= L; ++p) ++freq[encode_qgram({codes.data() + b + p, q})];
-      for (std::uint64_t p = 0; p + q <= L; ++p)
-        if (freq[encode_qgram({codes.data() + b + p, q})] > threshold) mask[b + p] = 1;
-    }
-  }
+  // The repeat mask is computed on the device:
+  // DeviceReference::mask_repeats.
 };
 
 class DeviceReference {
@@ -66,6 +55,20 @@ class DeviceReference {
     ctx->check(qgm_ref_upload(ctx->get(), words.data(), ref.chrom_begin.data(),
                               std::uint32_t(ref.chrom_begin.size() - 1), mbits.empty() ? nullptr : mbits.data(), &r));
     h_ = device::RefHandle(ctx, r);
+  }
+  // Repeat mask on the device (qgm_ref_mask_repeats): positions whose forward
+  // q-gram occurs more than `threshold` times in their chromosome leave P.
+  void mask_repeats(unsigned q, std::uint64_t threshold = 1000) {
+    context()->check(qgm_ref_mask_repeats(context()->get(), get(), q, threshold));
+  }
+  // The current mask, one byte per base (1 = not in P).
+  std::vector<std::uint8_t> mask() const {
+    const std::uint64_t total = chrom_begin_.back();
+    std::vector<std::uint64_t> w((total + 63) / 64 + 1, 0);
+    context()->check(qgm_ref_mask_download(context()->get(), get(), w.data()));
+    std::vector<std::uint8_t> m(total);
+    for (std::uint64_t x = 0; x < total; ++x) m[x] = std::uint8_t((w[x >> 6] >> (x & 63)) & 1u);
+    return m;
   }
   qgm_ref* get() const { return h_.get(); }
   const std::shared_ptr<device::Context>& context() const { return h_.ctx; }

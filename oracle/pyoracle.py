@@ -254,3 +254,20 @@ def sort_intervals(S1, O):
 
 def rc_codes(codes):
     return (3 - np.asarray(codes, dtype=np.uint8)[::-1]).astype(np.uint8)
+
+
+def repeat_mask(ref_codes, chrom_begin, q, threshold):
+    """SPEC.md:302 restated in numpy: 1 for every position whose forward
+    q-gram occurs more than `threshold` times among its chromosome's windows."""
+    ref_codes = np.asarray(ref_codes, dtype=np.uint8)
+    mask = np.zeros(ref_codes.size, np.uint8)
+    for c in range(len(chrom_begin) - 1):
+        b, e = int(chrom_begin[c]), int(chrom_begin[c + 1])
+        if e - b < q:
+            continue
+        code = np.zeros(e - b - q + 1, np.uint64)
+        for t in range(q):
+            code = (code << np.uint64(2)) | ref_codes[b + t:e - q + 1 + t].astype(np.uint64)
+        _, inv, cnt = np.unique(code, return_inverse=True, return_counts=True)
+        mask[b:b + code.size] = cnt[inv] > threshold
+    return mask

@@ -122,6 +122,27 @@ inline std::vector<uint8_t> reverse_complement(const uint8_t* s, size_t n) {
 // q-group index restatement (Alg. 1; qgroup_index.hpp:124-180). Positions are
 // written in ascending text order, so each O interval is sorted -- the
 // normalisation test_parallel.cpp:121-122 applies before comparing.
+// Repeat mask of build_reference_index: 1 for every
+// position whose forward q-gram occurs more than `threshold` times among the
+// windows of its own chromosome (counted over all windows).
+inline std::vector<uint8_t> repeat_mask(const std::vector<uint8_t>& codes, const std::vector<uint64_t>& chrom_begin,
+                                        unsigned q, uint64_t threshold) {
+  std::vector<uint8_t> mask(codes.size(), 0);
+  for (size_t c = 0; c + 1 < chrom_begin.size(); ++c) {
+    const uint64_t b = chrom_begin[c], L = chrom_begin[c + 1] - b;
+    if (L < q) continue;
+    std::vector<uint32_t> g(L - q + 1);
+    for (uint64_t p = 0; p + q <= L; ++p) g[p] = encode_qgram(codes.data() + b + p, q);
+    std::vector<uint32_t> s = g;
+    std::sort(s.begin(), s.end());
+    for (uint64_t p = 0; p + q <= L; ++p) {
+      const auto r = std::equal_range(s.begin(), s.end(), g[p]);
+      if (uint64_t(r.second - r.first) > threshold) mask[b + p] = 1;
+    }
+  }
+  return mask;
+}
+
 template <class W>
 struct Index {
   static constexpr unsigned group_width = std::numeric_limits<W>::digits;

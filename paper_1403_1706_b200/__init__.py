@@ -89,7 +89,8 @@ EXPORTS = (
     "qgm_ctx_synchronize", "qgm_ctx_profile", "qgm_ctx_stage_times", "qgm_ctx_kernel_times", "qgm_ctx_launches", "qgm_pack_codes",
     "qgm_pack_reads", "qgm_reads_upload", "qgm_reads_from_device", "qgm_reads_destroy", "qgm_index_build",
     "qgm_index_sample", "qgm_index_normalize", "qgm_index_info_get", "qgm_index_download", "qgm_index_lookup",
-    "qgm_index_destroy", "qgm_ref_upload", "qgm_ref_prepare", "qgm_ref_destroy", "qgm_filter", "qgm_cands_count",
+    "qgm_index_destroy", "qgm_ref_upload", "qgm_ref_prepare", "qgm_ref_mask_repeats", "qgm_ref_mask_download",
+    "qgm_ref_destroy", "qgm_filter", "qgm_cands_count",
     "qgm_cands_download", "qgm_cands_unique", "qgm_cands_destroy", "qgm_validate", "qgm_map", "qgm_hits_count",
     "qgm_hits_stats", "qgm_hits_download", "qgm_hits_destroy", "qgm_map_host", "qgm_exclusive_scan_u32",
 )
@@ -137,6 +138,8 @@ def load_library(path: str = LIB_PATH):
         "qgm_index_destroy": (None, [P]),
         "qgm_ref_upload": (i32, [P, P, P, u32, P, C.POINTER(P)]),
         "qgm_ref_prepare": (i32, [P, P, u32]),
+        "qgm_ref_mask_repeats": (i32, [P, P, u32, u64]),
+        "qgm_ref_mask_download": (i32, [P, P, P]),
         "qgm_ref_destroy": (None, [P]),
         "qgm_filter": (i32, [P, P, P, P, i32, i32, C.POINTER(P)]),
         "qgm_cands_count": (i32, [P, C.POINTER(u64)]),
@@ -407,8 +410,21 @@ class Reference:
                 if padded.size else np.zeros(1, np.uint64)
         return cls(ctx, pack_codes(codes), chrom_begin, mb)
 
+    def mask_repeats(self, q: int, threshold: int = 1000):
+        """Repeat mask on the device: positions whose forward
+        q-gram occurs more than `threshold` times in their chromosome leave P."""
+        self.ctx._check(self.ctx.lib.qgm_ref_mask_repeats(self.ctx.h, self.h, q, threshold))
+        return self
+
+    def mask(self) -> np.ndarray:
+        """The current mask as one uint8 per base (1 = not in P)."""
+        total = int(self.chrom_begin[-1])
+        words = np.zeros(max((total + 63) // 64, 1), np.uint64)
+        self.ctx._check(self.ctx.lib.qgm_ref_mask_download(self.ctx.h, self.h, _ptr(words)))
+        return np.unpackbits(words.view(np.uint8), bitorder="little")[:total]
+
     def prepare(self, q: int):
-        """Build the per-strand reference q-group indexes for q (qgm_ref_prepare)."""
+        """Build the reference-side q-group index for q (qgm_ref_prepare)."""
         self.ctx._check(self.ctx.lib.qgm_ref_prepare(self.ctx.h, self.h, q))
         return self
 

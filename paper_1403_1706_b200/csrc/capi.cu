@@ -647,6 +647,30 @@ int qgm_ref_prepare(qgm_ctx* ctx, qgm_ref* ref, uint32_t q) {
   });
 }
 
+int qgm_ref_mask_repeats(qgm_ctx* ctx, qgm_ref* ref, uint32_t q, uint64_t threshold) {
+  if (!ctx || !ref) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    require(q >= 1 && q <= 16, "q must be in [1, 16]");
+    qgm::mask_repeats(ctx->c, ref->r, q, threshold);
+    QGM_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int qgm_ref_mask_download(qgm_ctx* ctx, const qgm_ref* ref, uint64_t* mask_bits) {
+  if (!ctx || !ref || !mask_bits) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    const uint64_t mw = qgm::ceil_div(ref->r.total, 64);
+    if (!ref->r.mask.p) {
+      std::fill(mask_bits, mask_bits + mw, 0ull);
+      return;
+    }
+    if (mw) QGM_CUDA(cudaMemcpyAsync(mask_bits, ref->r.mask.p, mw * 8, cudaMemcpyDeviceToHost, ctx->c.stream));
+    QGM_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
 void qgm_ref_destroy(qgm_ref* r) {
   if (!r) return;
   cudaSetDevice(r->owner->c.device);

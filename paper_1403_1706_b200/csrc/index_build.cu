@@ -108,6 +108,48 @@ struct RefSource {
   }
 };
 
+// Forward q-grams of one chromosome [c0, c1) for the repeat mask: every
+// window inside the chromosome (the existing mask is ignored: frequencies are
+// over all windows); pos = the chromosome-relative position.
+struct FwdChromSource {
+  const uint64_t* ref;
+  uint64_t c0, c1;
+  unsigned q;
+  __device__ __forceinline__ bool item(uint64_t t, uint32_t& g, uint32_t& pos, uint32_t& extra) const {
+    const uint64_t x = c0 + t;
+    if (x + q > c1) return false;
+    g = qgram_at(ref, x, q);
+    pos = uint32_t(t);
+    extra = 0;
+    return true;
+  }
+};
+
+// One CTA per bucket of 2^lb codes: count the bucket's codes in shared memory,
+// then set the mask bit of every position whose code occurs more than
+// `threshold` times (positions of too-frequent q-grams leave P).
+__global__ void __launch_bounds__(kBuildThreads) k_bucket_mask(const uint64_t* __restrict__ pairs,
+                                                               const uint32_t* __restrict__ boff, uint64_t buckets,
+                                                               uint32_t lmask, uint64_t threshold, uint64_t c0,
+                                                               unsigned long long* __restrict__ mask) {
+  extern __shared__ uint32_t cnt[];  // 2^lb counters
+  for (uint64_t bk = blockIdx.x; bk < buckets; bk += gridDim.x) {
+    for (uint32_t i = threadIdx.x; i <= lmask; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const uint32_t b0 = boff[bk], b1 = boff[bk + 1];
+    for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) atomicAdd(cnt + (uint32_t(pairs[i] >> 32) & lmask), 1u);
+    __syncthreads();
+    for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      const uint64_t pr = pairs[i];
+      if (cnt[uint32_t(pr >> 32) & lmask] > threshold) {
+        const uint64_t x = c0 + uint32_t(pr);
+        atomicOr(mask + (x >> 6), 1ull << (x & 63));
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Palindromic indexed positions (f == rc(f); even q only): count, then list.
 __global__ void k_pal_scan(RefSource src, uint64_t* __restrict__ out, unsigned long long* __restrict__ count) {
   for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < src.L; base += uint64_t(gridDim.x) * blockDim.x) {
@@ -458,6 +500,31 @@ void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool packed, Buckets& out, u
   }
   *n_pal = np;
   bucket_impl(c, src, ref.total + np, out);
+}
+
+void mask_repeats(Ctx& c, Ref& ref, unsigned q, uint64_t threshold) {
+  if (q == 0 || q > 16) throw InputError("q must be in [1, 16]");
+  const uint64_t mw = ceil_div(ref.total, 64);
+  if (!ref.mask.p) {
+    ref.mask.alloc(c, std::max<uint64_t>(mw, 1));
+    ref.mask.zero();
+  }
+  for (uint32_t k = 0; k < ref.n_chrom; ++k) {
+    const uint64_t c0 = ref.cb[k], c1 = ref.cb[k + 1];
+    if (c1 - c0 < q) continue;
+    Buckets B;
+    init_geometry(B, q, 32);
+    FwdChromSource src{ref.words.p, c0, c1, q};
+    bucket_impl(c, src, c1 - c0, B);
+    if (B.V == 0) continue;
+    const uint32_t lmask = uint32_t((uint64_t(1) << B.lb) - 1);
+    const size_t smem = size_t(lmask + 1) * sizeof(uint32_t);
+    QGM_CUDA(cudaFuncSetAttribute(k_bucket_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    QGM_KERNEL(c, k_bucket_mask, unsigned(std::min<uint64_t>(B.buckets, uint64_t(kSMs) * 8)), kBuildThreads, smem,
+               B.pairs.p, B.boff.p, B.buckets, lmask, threshold, c0,
+               reinterpret_cast<unsigned long long*>(ref.mask.p));
+  }
+  ref.qidx = RefQIndex();  // the reference index depends on the mask
 }
 
 void index_from_buckets(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_t>* extra) {

@@ -268,6 +268,10 @@ void make_ref_planes(Ctx& c, Ref& ref);
 // index_build.cu
 void bucket_reads(Ctx& c, const Reads& reads, unsigned q, unsigned w, Buckets& out);
 void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool packed, Buckets& out, uint64_t* n_pal);
+// Repeat mask on the device: set the mask bit of every
+// position whose forward q-gram occurs more than `threshold` times among the
+// windows of its chromosome; drops the cached reference index.
+void mask_repeats(Ctx& c, Ref& ref, unsigned q, uint64_t threshold);
 void index_from_buckets(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_t>* extra);
 void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sampled, Index& out);
 void prepare_ref_index(Ctx& c, const Ref& ref, unsigned q);

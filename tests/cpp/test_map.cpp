@@ -137,3 +137,51 @@ TEST_CASE("bad parameters raise input_error") {
   p.q = 0;
   CHECK_THROWS_AS(map_reads(ref, text, p), input_error);
 }
+
+TEST_CASE("device repeat mask: SPEC examples (SPEC.md:283-284)") {
+  rng_engine rng(1);
+  {  // "AAAAAAAA", q=2, threshold=3: code 0 occurs 7 > 3 times -> P empty
+    Reference R;
+    R.add_chromosome("a", "AAAAAAAA", rng);
+    DeviceReference ref(R);
+    ref.mask_repeats(2, 3);
+    const auto m = ref.mask();
+    REQUIRE(m.size() == 8);
+    for (int x = 0; x < 7; ++x) CHECK(m[x] == 1);
+    CHECK(m[7] == 0);  // no full window at the last base
+  }
+  {  // "ACGTACGT", q=2, threshold=100: nothing masked
+    Reference R;
+    R.add_chromosome("a", "ACGTACGT", rng);
+    DeviceReference ref(R);
+    ref.mask_repeats(2, 100);
+    const auto m = ref.mask();
+    CHECK(std::count(m.begin(), m.end(), 1) == 0);
+  }
+}
+
+TEST_CASE("device repeat mask equals the oracle's, per chromosome, and maps identically") {
+  for (std::uint64_t seed : {21u, 22u, 23u}) {
+    std::mt19937_64 g(seed);
+    for (unsigned q : {8u, 12u, 16u}) {
+      auto in = tu::make_instance(g, 1 + unsigned(g() % 4), 30000, 200, 40, 110, 0.02, q, false);
+      const unsigned thr = 1 + unsigned(g() % 3);
+      // chromosome copies inside the instance make some q-grams frequent
+      const auto want = qgm_oracle::repeat_mask(in.ref.codes, in.ref.chrom_begin, q, thr);
+      DeviceReference ref(in.ref);
+      ref.mask_repeats(q, thr);
+      INFO("seed=" << seed << " q=" << q << " thr=" << thr);
+      REQUIRE(ref.mask() == want);
+      MapParams p;
+      p.q = q;
+      p.mode = StratumMode::all;
+      const auto got = tu::to_oracle(map_reads(ref, in.text, p));
+      in.oref.mask = want;
+      qgm_oracle::Params op;
+      op.q = q; op.mode = 1;
+      const auto ox = qgm_oracle::build_index<std::uint32_t>(in.oreads, q);
+      const auto oh = qgm_oracle::map_with_index(in.oref, in.oreads, ox, op, 4, nullptr);
+      CHECK(got == oh);
+    }
+  }
+}

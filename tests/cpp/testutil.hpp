@@ -67,7 +67,7 @@ inline Instance make_instance(std::mt19937_64& g, unsigned n_chrom, std::size_t 
     in.ref.codes.insert(in.ref.codes.end(), s.begin(), s.end());
     in.ref.chrom_begin.push_back(in.ref.codes.size());
   }
-  if (mask) in.ref.mask_repeats(q, mask_threshold);
+  if (mask) in.ref.mask = qgm_oracle::repeat_mask(in.ref.codes, in.ref.chrom_begin, q, mask_threshold);
   std::vector<std::vector<base_code>> reads;
   for (unsigned r = 0; r < n_reads; ++r) {
     const unsigned len = lmin + unsigned(g() % (lmax - lmin + 1));

@@ -195,3 +195,30 @@ def test_reads_with_many_hits_match_oracle(ctx, oracle):
         assert _same(got, want), (mode, got.size, want.size)
         if mode == 1:
             assert np.bincount(got["read_id"]).max() > 32
+
+
+def test_device_repeat_mask_matches_numpy_and_maps_like_the_oracle(ctx, oracle):
+    """qgm_ref_mask_repeats (per-chromosome forward q-gram
+    frequency) equals a numpy count on a repetitive two-chromosome reference;
+    the masked reference then maps exactly like the oracle given that mask."""
+    import paper_1403_1706_b200 as qgm
+    L = 300_000
+    ref = qgm.repetitive_reference(15, L)
+    cb = np.array([0, 120_000, L], np.uint64)
+    q, thr = 12, 30
+    want = np.zeros(L, np.uint8)
+    for c in range(2):
+        seq = ref[cb[c]:cb[c + 1]]
+        w = np.lib.stride_tricks.sliding_window_view(seq, q)
+        codes_c = (w.astype(np.uint64) * (4 ** np.arange(q - 1, -1, -1, dtype=np.uint64))).sum(1)
+        u, inv, cnt = np.unique(codes_c, return_inverse=True, return_counts=True)
+        want[cb[c]:cb[c] + w.shape[0]] = cnt[inv] > thr
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    R.mask_repeats(q, thr)
+    got_mask = R.mask()
+    assert want.sum() > 0 and np.array_equal(got_mask, want)
+    codes, lengths, *_ = qgm.simulate_reads(16, ref, cb, 3000, 100, 0.03)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    got, st = ctx.map(reads, R, q=q, mode=1)
+    exp, ost = oracle.map(ref, cb, codes, 100, lengths, q=q, mode=1, mask=want)
+    assert _same(got, exp), (got.size, exp.size)
