@@ -225,6 +225,27 @@ int qgm_map_host(qgm_ctx* ctx, const uint64_t* reads2bit, const uint32_t* length
                  uint32_t stride, const qgm_ref* ref, const qgm_map_params* params, qgm_hit* out, uint64_t cap,
                  uint64_t* n_out, qgm_map_stats* stats);
 
+/* One read buffer of a streamed run (run_map's bounded-queue pipeline,
+ * SPEC.md:521-528 / PAPER.md:238-262). Host buffers; pinned memory lets the
+ * copies overlap the mapping. */
+typedef struct qgm_batch {
+  const uint64_t* reads2bit; /* qgm_pack_reads layout */
+  const uint32_t* lengths;
+  uint32_t n_reads;
+  uint32_t stride;
+  qgm_hit* out;              /* capacity `cap` records */
+  uint64_t cap;
+  uint64_t n_out;            /* out: hit count (the required capacity when it exceeds cap) */
+  qgm_map_stats stats;       /* out */
+} qgm_batch;
+/* Maps the batches in order, same results as qgm_map_host per batch: the
+ * reads of batch i+1 are uploaded on a second stream while batch i is
+ * mapped, the hits of batch i are downloaded while batch i+1 is mapped.
+ * Fails with QGM_ERR_INPUT if any batch's hits exceed its cap (every n_out is
+ * still set). */
+int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, const qgm_ref* ref,
+                         const qgm_map_params* params);
+
 /* ---- data-parallel primitive: par::exclusive_scan (parallel.hpp:64-121) --- */
 /* Device exclusive scan of host u32 values; QGM_ERR_INPUT on u32 overflow. */
 int qgm_exclusive_scan_u32(qgm_ctx* ctx, const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* total);

@@ -83,6 +83,12 @@ class MapStats(C.Structure):
                 ("lookups_hit", C.c_uint64), ("occurrences", C.c_uint64)]
 
 
+class Batch(C.Structure):
+    """qgm_batch (include/qgm_c.h): one read buffer of qgm_map_host_batches."""
+    _fields_ = [("reads2bit", C.c_void_p), ("lengths", C.c_void_p), ("n_reads", C.c_uint32), ("stride", C.c_uint32),
+                ("out", C.c_void_p), ("cap", C.c_uint64), ("n_out", C.c_uint64), ("stats", MapStats)]
+
+
 # Every symbol include/qgm_c.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = (
     "qgm_ctx_create", "qgm_ctx_set_stream", "qgm_ctx_stream", "qgm_ctx_destroy", "qgm_last_error",
@@ -92,7 +98,8 @@ EXPORTS = (
     "qgm_index_destroy", "qgm_ref_upload", "qgm_ref_prepare", "qgm_ref_mask_repeats", "qgm_ref_mask_download",
     "qgm_ref_destroy", "qgm_filter", "qgm_cands_count",
     "qgm_cands_download", "qgm_cands_unique", "qgm_cands_destroy", "qgm_validate", "qgm_map", "qgm_hits_count",
-    "qgm_hits_stats", "qgm_hits_download", "qgm_hits_destroy", "qgm_map_host", "qgm_exclusive_scan_u32",
+    "qgm_hits_stats", "qgm_hits_download", "qgm_hits_destroy", "qgm_map_host", "qgm_map_host_batches",
+    "qgm_exclusive_scan_u32",
 )
 
 _lib = None
@@ -154,6 +161,7 @@ def load_library(path: str = LIB_PATH):
         "qgm_hits_destroy": (None, [P]),
         "qgm_map_host": (i32, [P, P, P, u32, u32, P, C.POINTER(MapParams), P, u64, C.POINTER(u64),
                                C.POINTER(MapStats)]),
+        "qgm_map_host_batches": (i32, [P, P, u32, P, C.POINTER(MapParams)]),
         "qgm_exclusive_scan_u32": (i32, [P, P, u64, P, P]),
     }
     for name, (res, args) in sig.items():
@@ -343,6 +351,30 @@ class Context:
                                        _ptr(out), out.size, C.byref(n), C.byref(st))
         self._check(rc)
         return out[: n.value], {f: getattr(st, f) for f, _ in MapStats._fields_}
+
+    def map_host_batches(self, batches, ref, params=None, **kw):
+        """Streamed e2e entry (qgm_map_host_batches): `batches` is a list of
+        (words, lengths, stride) host arrays; returns [(hits, stats), ...].
+        Pinned host arrays let the copies overlap the mapping."""
+        p = params or make_params(**kw)
+        arr = (Batch * len(batches))()
+        keep = []
+        for i, (words, lengths, stride) in enumerate(batches):
+            lengths = np.ascontiguousarray(lengths, dtype=np.uint32)
+            out = np.zeros(max(64, lengths.size * 4), dtype=HIT_DTYPE)
+            keep.append((words, lengths, out))
+            arr[i] = Batch(_ptr(words), _ptr(lengths), lengths.size, stride, _ptr(out), out.size, 0, MapStats())
+        rc = self.lib.qgm_map_host_batches(self.h, arr, len(batches), ref.h, C.byref(p))
+        if rc == 1 and any(arr[i].n_out > arr[i].cap for i in range(len(batches))):
+            for i, (words, lengths, out) in enumerate(keep):
+                if arr[i].n_out > arr[i].cap:
+                    out = np.zeros(arr[i].n_out, dtype=HIT_DTYPE)
+                    keep[i] = (words, lengths, out)
+                    arr[i].out, arr[i].cap = _ptr(out), out.size
+            rc = self.lib.qgm_map_host_batches(self.h, arr, len(batches), ref.h, C.byref(p))
+        self._check(rc)
+        return [(keep[i][2][: arr[i].n_out], {f: getattr(arr[i].stats, f) for f, _ in MapStats._fields_})
+                for i in range(len(batches))]
 
     def exclusive_scan(self, values: np.ndarray):
         """par::exclusive_scan (parallel.hpp:116-121) on the device: (sums, total)."""

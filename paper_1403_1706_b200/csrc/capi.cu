@@ -3,6 +3,7 @@
 // for qgm_map. No exception crosses this file's exported functions.
 #include <chrono>
 #include <cstring>
+#include <functional>
 #include <memory>
 
 #include "../../include/qgm_c.h"
@@ -223,7 +224,12 @@ static void check_reads_shape(uint32_t n_reads, uint32_t stride) {
   if (n_reads > (1u << 27)) throw InputError("at most 2^27 reads per batch");
 }
 
-static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_map_params& P) {
+// after_filter: called (host side) once filtration and candidate dedup are
+// done -- qgm_map_host_batches enqueues its copies there, so they overlap the
+// compute-bound validation rather than the L2-sensitive partition, join and
+// hash dedup.
+static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_map_params& P,
+                         const std::function<void()>& after_filter = {}) {
   if (P.q == 0 || P.q > 16) throw InputError("q must be in [1, 16]");
   if (P.band_width == 0 || P.band_width > 64) throw InputError("band width must be in [1, 64]");
   if (P.pct_identity > 100) throw InputError("percent identity must be in [0, 100]");
@@ -269,6 +275,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
     StageScope s(c, kStageSort);
     n_u = dedup_keys(c, keys.p, n_raw, alt);  // unique candidates, any order (validation is per key)
   }
+  if (after_filter) after_filter();
   DBuf<uint64_t> hkeys(c, std::max<uint64_t>(n_u, 1)), hkeys_alt;
   DBuf<uint32_t> hvals(c, std::max<uint64_t>(n_u, 1)), hvals_alt;
   uint64_t n_val = 0;
@@ -381,6 +388,7 @@ void qgm_ctx_destroy(qgm_ctx* ctx) {
   for (auto& m : ctx->c.marks) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
   for (auto e : ctx->c.ev_pool) cudaEventDestroy(e);
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+  if (ctx->c.copy_stream) cudaStreamDestroy(ctx->c.copy_stream);
   delete ctx;
 }
 
@@ -874,6 +882,139 @@ int qgm_map_host(qgm_ctx* ctx, const uint64_t* reads2bit, const uint32_t* length
   }
   qgm_hits_destroy(h);
   qgm_reads_destroy(rd);
+  return rc;
+}
+
+// Streamed batches (the paper's overlapped pipeline): the
+// reads of batch i+1 are copied in on the context's copy stream while batch i
+// is mapped on the compute stream, and the hits of batch i are copied out
+// while batch i+1 is mapped. Two device input slots; a batch's hit buffer is
+// released only after its D2H completed (the block cache hands blocks out in
+// compute-stream order only).
+int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, const qgm_ref* ref,
+                         const qgm_map_params* P) {
+  if (!ctx || !ref || !P || (n_batches && !batches)) return QGM_ERR_INPUT;
+  struct Slot {
+    qgm::DBuf<uint64_t> words;
+    qgm::DBuf<uint32_t> lens;
+    cudaEvent_t h2d = nullptr;
+  };
+  struct Pending {
+    qgm::HitsObj h;
+    cudaEvent_t comp = nullptr, done = nullptr;
+    bool live = false;
+  };
+  Slot slot[2];
+  Pending pend[2];
+  int overflow = 0;
+  int rc = guard(ctx, [&] {
+    activate(ctx);
+    qgm::Ctx& c = ctx->c;
+    if (!c.copy_stream) QGM_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+    const cudaStream_t cs = c.copy_stream;
+    for (auto& s : slot) QGM_CUDA(cudaEventCreateWithFlags(&s.h2d, cudaEventDisableTiming));
+    for (auto& p : pend) {
+      QGM_CUDA(cudaEventCreateWithFlags(&p.comp, cudaEventDisableTiming));
+      QGM_CUDA(cudaEventCreateWithFlags(&p.done, cudaEventDisableTiming));
+    }
+    // both slots sized for the largest batch up front (allocated on the
+    // compute stream's block cache, released after both streams are idle)
+    uint64_t max_w = 1, max_n = 1;
+    for (uint32_t i = 0; i < n_batches; ++i) {
+      const qgm_batch& b = batches[i];
+      qgm::check_reads_shape(b.n_reads, b.stride);
+      require(b.n_reads == 0 || (b.reads2bit && b.lengths), "null read buffers");
+      max_w = std::max<uint64_t>(max_w, uint64_t(b.n_reads) * ((b.stride + 31) / 32) + 1);
+      max_n = std::max<uint64_t>(max_n, b.n_reads);
+    }
+    for (auto& s : slot) {
+      s.words.alloc(c, max_w);
+      s.lens.alloc(c, max_n);
+    }
+    QGM_CUDA(cudaStreamSynchronize(c.stream));  // allocations visible before the copy stream writes
+    auto h2d = [&](uint32_t i) {
+      const qgm_batch& b = batches[i];
+      Slot& s = slot[i & 1];
+      const uint64_t nw = uint64_t(b.n_reads) * ((b.stride + 31) / 32);
+      if (nw) QGM_CUDA(cudaMemcpyAsync(s.words.p, b.reads2bit, nw * 8, cudaMemcpyHostToDevice, cs));
+      QGM_CUDA(cudaMemsetAsync(s.words.p + nw, 0, 8, cs));
+      if (b.n_reads) QGM_CUDA(cudaMemcpyAsync(s.lens.p, b.lengths, uint64_t(b.n_reads) * 4, cudaMemcpyHostToDevice, cs));
+      QGM_CUDA(cudaEventRecord(s.h2d, cs));
+    };
+    auto d2h = [&](uint32_t i) {  // batch i's hits, after its mapping (comp event)
+      qgm_batch& b = batches[i];
+      Pending& p = pend[i & 1];
+      if (p.h.n > b.cap) {
+        overflow = 1;
+      } else if (p.h.n) {
+        QGM_CUDA(cudaStreamWaitEvent(cs, p.comp, 0));
+        QGM_CUDA(cudaMemcpyAsync(b.out, p.h.hits.p, p.h.n * 16, cudaMemcpyDeviceToHost, cs));
+      }
+      QGM_CUDA(cudaEventRecord(p.done, cs));
+    };
+    if (n_batches) h2d(0);
+    for (uint32_t i = 0; i < n_batches; ++i) {
+      qgm_batch& b = batches[i];
+      Slot& s = slot[i & 1];
+      QGM_CUDA(cudaStreamWaitEvent(c.stream, s.h2d, 0));
+      qgm::Reads r;
+      r.n = b.n_reads;
+      r.stride = b.stride;
+      r.W = (b.stride + 31) / 32;
+      r.words.swap(s.words);
+      r.lengths.swap(s.lens);
+      struct Back {  // the slot keeps its buffers whatever happens
+        qgm::Reads& r;
+        Slot& s;
+        ~Back() { r.words.swap(s.words); r.lengths.swap(s.lens); }
+      } back{r, s};
+      {
+        qgm::StageScope st(c, qgm::kStageReads);
+        qgm::finish_reads(c, r);
+      }
+      Pending& p = pend[i & 1];
+      if (p.live) {  // batch i-2's hits must be downloaded before its buffer goes back to the cache
+        QGM_CUDA(cudaEventSynchronize(p.done));
+        p.h = qgm::HitsObj();
+        p.live = false;
+      }
+      // the copies run while the compute-bound validation of batch i runs:
+      // batch i-1's hits out, batch i+1's reads in (slot (i+1)&1 was last read
+      // by batch i-1, finished)
+      p.h = qgm::map_reads(c, r, ref->r, *P, [&] {
+        if (i >= 1) d2h(i - 1);
+        if (i + 1 < n_batches) h2d(i + 1);
+      });
+      QGM_CUDA(cudaEventRecord(p.comp, c.stream));
+      p.live = true;
+      b.n_out = p.h.n;
+      std::memset(&b.stats, 0, sizeof(b.stats));
+      b.stats.raw_candidates = p.h.stats[0];
+      b.stats.unique_candidates = p.h.stats[1];
+      b.stats.validated = p.h.stats[2];
+      b.stats.hits = p.h.stats[3];
+      b.stats.index_distinct = p.h.stats[4];
+      b.stats.index_occurrences = p.h.stats[5];
+      b.stats.lookups_hit = p.h.stats[6];
+      b.stats.occurrences = p.h.stats[7];
+    }
+    if (n_batches) d2h(n_batches - 1);
+    QGM_CUDA(cudaStreamSynchronize(cs));
+    QGM_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  if (ctx->c.copy_stream) cudaStreamSynchronize(ctx->c.copy_stream);
+  cudaStreamSynchronize(ctx->c.stream);
+  for (auto& p : pend) {
+    p.h = qgm::HitsObj();
+    if (p.comp) cudaEventDestroy(p.comp);
+    if (p.done) cudaEventDestroy(p.done);
+  }
+  for (auto& s : slot)
+    if (s.h2d) cudaEventDestroy(s.h2d);
+  if (rc == QGM_OK && overflow) {
+    ctx->c.err = "output capacity too small (see qgm_batch.n_out)";
+    return QGM_ERR_INPUT;
+  }
   return rc;
 }
 

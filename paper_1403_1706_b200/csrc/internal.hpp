@@ -24,6 +24,7 @@ struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t copy_stream = nullptr;  // H2D / D2H of qgm_map_host_batches (created on first use)
   std::string err;
   uint64_t launches = 0;
   bool profile = false;

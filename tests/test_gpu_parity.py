@@ -222,3 +222,22 @@ def test_device_repeat_mask_matches_numpy_and_maps_like_the_oracle(ctx, oracle):
     got, st = ctx.map(reads, R, q=q, mode=1)
     exp, ost = oracle.map(ref, cb, codes, 100, lengths, q=q, mode=1, mask=want)
     assert _same(got, exp), (got.size, exp.size)
+
+
+def test_streamed_batches_equal_single_calls(ctx):
+    """qgm_map_host_batches (copies of batch i+1 / hits of batch i-1 overlap
+    the mapping of batch i) returns, batch for batch, exactly what
+    qgm_map_host returns; batches of different sizes and strides."""
+    import paper_1403_1706_b200 as qgm
+    L = 500_000
+    ref = qgm.random_reference(31, L)
+    cb = np.array([0, 200_000, L], np.uint64)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    batches = []
+    for i, (n, stride) in enumerate([(3000, 100), (500, 150), (4000, 100), (1, 100), (2500, 120)]):
+        codes, lengths, *_ = qgm.simulate_reads(40 + i, ref, cb, n, stride, 0.03)
+        batches.append((qgm.pack_read_codes(codes, stride), lengths, stride))
+    got = ctx.map_host_batches(batches, R, q=14, mode=1)
+    for (words, lengths, stride), (hits, st) in zip(batches, got):
+        want, wst = ctx.map_host(words, lengths, stride, R, q=14, mode=1)
+        assert _same(hits, want) and st == wst
