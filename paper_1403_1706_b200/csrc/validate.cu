@@ -138,9 +138,7 @@ __device__ __forceinline__ bool myers_rows(const ValArgs& a, uint32_t r, bool re
       rl = __brev(__funnelshift_l(l.x, h.x, s));
       rh = __brev(__funnelshift_l(l.y, h.y, s));
     }
-    const uint32_t rows = min(32u, n - 32 * c);
-#pragma unroll 4
-    for (uint32_t t = 0; t < rows; ++t) {
+    auto row = [&](uint32_t t) {
       const uint32_t Rl = uint32_t(int32_t(rl << t) >> 31);
       const uint32_t Rh = uint32_t(int32_t(rh << t) >> 31);
       const T Eq = Band<T>::eq(w, t, Rl, Rh, kCheck) & mask;
@@ -155,7 +153,20 @@ __device__ __forceinline__ bool myers_rows(const ValArgs& a, uint32_t r, bool re
       Pv = nP;
       Mv = nM;
       score0 += int(D1 & T(1));
-      if ((t & 15) == 15 && kmax >= 0 && score0 - int(popcount_t(Mv)) > kmax) return false;
+    };
+    const uint32_t rows = min(32u, n - 32 * c);
+    if (rows == 32) {  // whole chunk: constant shift amounts, no per-row loop control
+#pragma unroll
+      for (uint32_t t = 0; t < 32; ++t) {
+        row(t);
+        if ((t & 15) == 15 && kmax >= 0 && score0 - int(popcount_t(Mv)) > kmax) return false;
+      }
+    } else {
+#pragma unroll 4
+      for (uint32_t t = 0; t < rows; ++t) {
+        row(t);
+        if ((t & 15) == 15 && kmax >= 0 && score0 - int(popcount_t(Mv)) > kmax) return false;
+      }
     }
   }
   return true;
