@@ -37,6 +37,8 @@
 // references below 2^28 padded bases -- the strand flag and the base the
 // run-start rule compares in its top 4 bits; the item holds the read's own
 // compare bases (o-1 forward, complement of o+q reverse) and n - q - o.
+#include <cstdlib>
+
 #include "internal.hpp"
 
 namespace qgm {
@@ -53,12 +55,6 @@ constexpr int kStage = 64;                // staged keys per warp
 constexpr uint32_t kInline = 4;           // intervals up to this length are expanded in-lane
 constexpr uint32_t kMaxWords = 2048;      // group words per sub-bin (q = 16)
 constexpr uint32_t kPosMask = (1u << kPackedPosBits) - 1u;
-
-// Shared-memory swizzle of the staged words: thread t of the group-start scan
-// reads words t*per .. t*per+per-1, which would put up to 16 lanes of a warp
-// on one bank; XOR-ing the low 4 index bits with the 32-word row number makes
-// every step of that scan (u32 words and u16 starts alike) conflict-free.
-__device__ __forceinline__ uint32_t swz(uint32_t w) { return w ^ ((w >> 5) & 15u); }
 
 struct JoinArgs {
   const uint64_t* items;
@@ -108,6 +104,135 @@ __device__ __forceinline__ bool expand(const JoinArgs& a, const uint32_t* Op, ui
   return true;
 }
 
+// Per-warp join state: the compaction list and the key staging buffer.
+struct WarpLists {
+  uint32_t* k0;
+  uint32_t* k1;
+  uint8_t* slot;
+  uint64_t* out;
+  uint32_t staged = 0;
+  unsigned long long n_hit = 0, n_occ = 0;
+};
+
+__device__ __forceinline__ void flush_keys(const JoinArgs& a, WarpLists& L) {
+  const unsigned lane = lane_id();
+  unsigned long long base = 0;
+  if (lane == 0 && L.staged) base = atomicAdd(a.counter, (unsigned long long)L.staged);
+  base = __shfl_sync(kFull, base, 0);
+  for (uint32_t i = lane; i < L.staged; i += 32)
+    if (base + i < a.cap_out) a.out[base + i] = L.out[i];
+  L.staged = 0;
+  __syncwarp();
+}
+
+// The read q-gram items [my_lo, my_hi) of sub-bin `sb` (one warp): look up
+// the staged occupancy words / group starts, expand the occurrence intervals
+// (S1p / Op: global arrays, or generic pointers into the staged slices), emit
+// the candidate keys.
+template <bool kRunStart, bool kPacked>
+__device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI, const uint16_t* sR,
+                                           const uint32_t* S1p, const uint32_t* Op, uint32_t d0, uint32_t w0,
+                                           uint32_t gsub, uint32_t my_lo, uint32_t my_hi, WarpLists& L) {
+  const unsigned lane = lane_id();
+  auto stage_key = [&](bool emit, uint64_t key) {  // all lanes call it
+    const unsigned m = __ballot_sync(kFull, emit);
+    if (emit) L.out[L.staged + __popc(m & lanemask_lt())] = key;
+    L.staged += __popc(m);
+    __syncwarp();
+    if (L.staged > kStage - 32) flush_keys(a, L);
+  };
+  uint64_t pn[kItems];  // next step's items, loaded one step ahead
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    const uint32_t it = my_lo + u * 32 + lane;
+    pn[u] = it < my_hi ? __ldg(a.items + it) : ~0ull;
+  }
+  for (uint32_t base = my_lo; base < my_hi; base += 32 * kItems) {  // warp-uniform bound
+    uint32_t cnt = 0, nr = 0, rk0[kItems], rk1[kItems];
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) {
+      const uint64_t pr = pn[u];
+      const uint32_t itn = base + 32 * kItems + u * 32 + lane;
+      pn[u] = itn < my_hi ? __ldg(a.items + itn) : ~0ull;
+      const bool ok = pr != ~0ull;
+      const uint32_t g = gsub | uint32_t(pr >> kItemCodeShift);
+      const uint32_t wl = ok ? (g >> 5) - w0 : 0u, bit = g & 31u;
+      const uint32_t w = sI[wl];
+      const bool hit = ok && ((w >> bit) & 1u);
+      const uint32_t b = d0 + sR[wl] + __popc(w & ((1u << bit) - 1u));
+      rk0[u] = hit ? S1p[b] : 0u;
+      rk1[u] = hit ? S1p[b + 1] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) {
+      const uint32_t len = rk1[u] - rk0[u];
+      cnt += len;
+      nr += len != 0;
+    }
+    L.n_hit += nr;
+    L.n_occ += cnt;
+    if (__all_sync(kFull, cnt == 0)) continue;
+    // compact the non-empty lookups of the warp into a list
+    uint32_t nent = 0;
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) {
+      const bool has = rk1[u] != rk0[u];
+      const unsigned bm = __ballot_sync(kFull, has);
+      if (has) {
+        const uint32_t e = nent + __popc(bm & lanemask_lt());
+        L.k0[e] = rk0[u];
+        L.k1[e] = rk1[u];
+        L.slot[e] = uint8_t(u * 32 + lane);
+      }
+      nent += __popc(bm);
+    }
+    __syncwarp();
+    // one list entry per lane per round; intervals of up to kInline
+    // occurrences (almost all of them) are expanded in the lane, longer ones
+    // (repeats) by the whole warp, one interval at a time
+    for (uint32_t e0 = 0; e0 < nent; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      uint32_t k0 = 0, len = 0;
+      uint64_t it = 0;
+      if (e < nent) {
+        k0 = L.k0[e];
+        len = L.k1[e] - k0;
+        it = __ldg(a.items + base + L.slot[e]);
+      }
+      const bool longi = len > kInline;
+      const uint32_t nin = longi ? 0u : len;
+      const uint32_t rounds = __reduce_max_sync(kFull, nin);
+      for (uint32_t t = 0; t < rounds; ++t) {
+        uint64_t key = 0;
+        const bool emit = t < nin && expand<kRunStart, kPacked>(a, Op, k0 + t, it, key);
+        stage_key(emit, key);
+      }
+      unsigned lm = __ballot_sync(kFull, longi);
+      while (lm) {
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint32_t lk0 = __shfl_sync(kFull, k0, src), llen = __shfl_sync(kFull, len, src);
+        const uint64_t lit = __shfl_sync(kFull, it, src);
+        for (uint32_t t0 = 0; t0 < llen; t0 += 32) {
+          uint64_t key = 0;
+          const bool emit = t0 + lane < llen && expand<kRunStart, kPacked>(a, Op, lk0 + t0 + lane, lit, key);
+          stage_key(emit, key);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ void join_stats(const JoinArgs& a, WarpLists& L) {
+  flush_keys(a, L);
+  const unsigned long long h = warp_reduce_sum(L.n_hit), o = warp_reduce_sum(L.n_occ);
+  if (lane_id() == 0 && a.stats && h) {
+    atomicAdd(a.stats, h);
+    atomicAdd(a.stats + 1, o);
+  }
+}
+
 template <bool kRunStart, bool kPacked>
 __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
   // dynamic: I words [nw], u16 group starts [nw] (+pad to 16 B), S' slice
@@ -124,31 +249,16 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
   __shared__ uint64_t s_out[kJoinWarps][kStage];
   __shared__ __align__(8) uint64_t s_bar;
 
-  const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
-  uint32_t staged_keys = 0;
-  unsigned long long n_hit = 0, n_occ = 0;
+  const unsigned wid = threadIdx.x >> 5;
+  WarpLists L;
+  L.k0 = s_k0[wid];
+  L.k1 = s_k1[wid];
+  L.slot = s_slot[wid];
+  L.out = s_out[wid];
   const bool bulk_I = a.r16 != nullptr;  // sub-bins of >= 8 group words: whole 16-byte chunks
   if (threadIdx.x == 0) mbar_init(&s_bar, 1);
   __syncthreads();
   uint32_t phase = 0;
-
-  auto flush = [&]() {
-    unsigned long long base = 0;
-    if (lane == 0 && staged_keys) base = atomicAdd(a.counter, (unsigned long long)staged_keys);
-    base = __shfl_sync(kFull, base, 0);
-    for (uint32_t i = lane; i < staged_keys; i += 32)
-      if (base + i < a.cap_out) a.out[base + i] = s_out[wid][i];
-    staged_keys = 0;
-    __syncwarp();
-  };
-  auto stage_key = [&](bool emit, uint64_t key) {  // all lanes call it
-    const unsigned m = __ballot_sync(kFull, emit);
-    if (emit) s_out[wid][staged_keys + __popc(m & lanemask_lt())] = key;
-    staged_keys += __popc(m);
-    __syncwarp();
-    if (staged_keys > kStage - 32) flush();
-  };
-
 
   // the sub-bin's bounds (item range, S' range, O range), loaded one
   // iteration ahead
@@ -231,97 +341,149 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
     const uint32_t nitems = b1 - b0;
     const uint32_t my_lo = b0 + uint32_t(uint64_t(nitems) * wid / kJoinWarps);
     const uint32_t my_hi = b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kJoinWarps);
-    const uint32_t gsub = sb << a.code_shift;
-    uint64_t pn[kItems];  // next step's items, loaded one step ahead
-#pragma unroll
-    for (int u = 0; u < kItems; ++u) {
-      const uint32_t it = my_lo + u * 32 + lane;
-      pn[u] = it < my_hi ? __ldg(a.items + it) : ~0ull;
-    }
-    for (uint32_t base = my_lo; base < my_hi; base += 32 * kItems) {  // warp-uniform bound
-      uint32_t cnt = 0, nr = 0, rk0[kItems], rk1[kItems];
-#pragma unroll
-      for (int u = 0; u < kItems; ++u) {
-        const uint64_t pr = pn[u];
-        const uint32_t itn = base + 32 * kItems + u * 32 + lane;
-        pn[u] = itn < my_hi ? __ldg(a.items + itn) : ~0ull;
-        const bool ok = pr != ~0ull;
-        const uint32_t g = gsub | uint32_t(pr >> kItemCodeShift);
-        const uint32_t wl = ok ? (g >> 5) - w0 : 0u, bit = g & 31u;
-        const uint32_t w = sI[wl];
-        const bool hit = ok && ((w >> bit) & 1u);
-        const uint32_t b = d0 + sR[wl] + __popc(w & ((1u << bit) - 1u));
-        rk0[u] = hit ? S1p[b] : 0u;
-        rk1[u] = hit ? S1p[b + 1] : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < kItems; ++u) {
-        const uint32_t len = rk1[u] - rk0[u];
-        cnt += len;
-        nr += len != 0;
-      }
-      n_hit += nr;
-      n_occ += cnt;
-      if (__all_sync(kFull, cnt == 0)) continue;
-      // compact the non-empty lookups of the warp into a list
-      uint32_t nent = 0;
-#pragma unroll
-      for (int u = 0; u < kItems; ++u) {
-        const bool has = rk1[u] != rk0[u];
-        const unsigned bm = __ballot_sync(kFull, has);
-        if (has) {
-          const uint32_t e = nent + __popc(bm & lanemask_lt());
-          s_k0[wid][e] = rk0[u];
-          s_k1[wid][e] = rk1[u];
-          s_slot[wid][e] = uint8_t(u * 32 + lane);
-        }
-        nent += __popc(bm);
-      }
-      __syncwarp();
-      // one list entry per lane per round; intervals of up to kInline
-      // occurrences (almost all of them) are expanded in the lane, longer ones
-      // (repeats) by the whole warp, one interval at a time
-      for (uint32_t e0 = 0; e0 < nent; e0 += 32) {
-        const uint32_t e = e0 + lane;
-        uint32_t k0 = 0, len = 0;
-        uint64_t it = 0;
-        if (e < nent) {
-          k0 = s_k0[wid][e];
-          len = s_k1[wid][e] - k0;
-          it = __ldg(a.items + base + s_slot[wid][e]);
-        }
-        const bool longi = len > kInline;
-        const uint32_t nin = longi ? 0u : len;
-        const uint32_t rounds = __reduce_max_sync(kFull, nin);
-        for (uint32_t t = 0; t < rounds; ++t) {
-          uint64_t key = 0;
-          const bool emit = t < nin && expand<kRunStart, kPacked>(a, Op, k0 + t, it, key);
-          stage_key(emit, key);
-        }
-        unsigned lm = __ballot_sync(kFull, longi);
-        while (lm) {
-          const int src = __ffs(lm) - 1;
-          lm &= lm - 1;
-          const uint32_t lk0 = __shfl_sync(kFull, k0, src), llen = __shfl_sync(kFull, len, src);
-          const uint64_t lit = __shfl_sync(kFull, it, src);
-          for (uint32_t t0 = 0; t0 < llen; t0 += 32) {
-            uint64_t key = 0;
-            const bool emit = t0 + lane < llen && expand<kRunStart, kPacked>(a, Op, lk0 + t0 + lane, lit, key);
-            stage_key(emit, key);
-          }
-        }
-      }
-      __syncwarp();
-    }
+    join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, d0, w0, sb << a.code_shift, my_lo, my_hi, L);
     __syncthreads();  // the staging buffers are rewritten for the next sub-bin
   }
-  flush();
-  n_hit = warp_reduce_sum(n_hit);
-  n_occ = warp_reduce_sum(n_occ);
-  if (lane == 0 && a.stats && n_hit) {
-    atomicAdd(a.stats, n_hit);
-    atomicAdd(a.stats + 1, n_occ);
+  join_stats(a, L);
+}
+
+
+// ---------------------------------------------------------------------------
+// Warp-specialised variant: one producer warp stages sub-bin k+1 (and k+2)
+// into a second buffer while kWsCons consumer warps join sub-bin k. Full /
+// empty mbarriers per buffer replace the CTA barrier, so a consumer warp that
+// finishes its share of sub-bin k moves straight on to sub-bin k+1.
+#ifndef QGM_JOIN_WS_CONS
+#define QGM_JOIN_WS_CONS 12
+#endif
+constexpr int kWsCons = QGM_JOIN_WS_CONS;
+constexpr int kWsThreads = (kWsCons + 1) * 32;
+
+struct StageMeta {
+  uint32_t sb, b0, b1, d0, sA, oA, staged, end;
+};
+
+template <bool kRunStart, bool kPacked>
+__global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t stage_words) {
+  extern __shared__ __align__(16) uint32_t s_dyn[];  // 2 stages: I [nw] | u16 starts | S' [cap] | O [cap]
+  const uint32_t nw = a.words;
+  __shared__ uint32_t s_k0[kWsCons][kRanges];
+  __shared__ uint32_t s_k1[kWsCons][kRanges];
+  __shared__ uint8_t s_slot[kWsCons][kRanges];
+  __shared__ uint64_t s_out[kWsCons][kStage];
+  __shared__ StageMeta meta[2];
+  __shared__ __align__(8) uint64_t full[2], empty[2];
+  const unsigned wid = threadIdx.x >> 5, lane = lane_id();
+  const bool bulk_I = a.r16 != nullptr;
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], kWsCons);
+    mbar_init(&empty[1], kWsCons);
   }
+  __syncthreads();
+  auto stage = [&](uint32_t s, uint32_t*& sI, uint16_t*& sR, uint32_t*& sS1, uint32_t*& sO) {
+    uint32_t* base = s_dyn + s * stage_words;
+    sI = base;
+    sR = reinterpret_cast<uint16_t*>(base + nw);
+    sS1 = base + nw + (((nw + 1) / 2 + 3) & ~3u);
+    sO = sS1 + a.cap;
+  };
+  if (wid == kWsCons) {  // producer
+    if (lane != 0) return;
+    uint32_t k = 0;
+    for (uint32_t sb = blockIdx.x;; sb += gridDim.x) {
+      const bool end = sb >= a.n_sub;
+      uint32_t b0 = 0, b1 = 0;
+      if (!end) {
+        b0 = __ldg(a.soff + sb);
+        b1 = __ldg(a.soff + sb + 1);
+        if (b0 == b1) continue;
+      }
+      const uint32_t s = k & 1, j = k >> 1;
+      if (j > 0) mbar_wait(&empty[s], (j - 1) & 1u);  // the consumers released this buffer's previous sub-bin
+      StageMeta& M = meta[s];
+      if (end) {
+        M.end = 1;
+        mbar_arrive(&full[s]);
+        break;
+      }
+      const uint32_t w0 = uint32_t((uint64_t(sb) << a.code_shift) >> 5);
+      uint32_t d0, d1 = 0, o0 = 0, o1 = 0;
+      if (a.sb_d) {
+        d0 = __ldg(a.sb_d + sb);
+        d1 = __ldg(a.sb_d + sb + 1);
+        o0 = __ldg(a.sb_o + sb);
+        o1 = __ldg(a.sb_o + sb + 1);
+      } else {
+        d0 = __ldg(a.S + w0);
+      }
+      const uint32_t sA = d0 & ~3u, oA = o0 & ~3u;
+      const uint32_t sN = ((d1 + 1 + 3) & ~3u) - sA, oN = ((o1 + 3) & ~3u) - oA;
+      const bool staged = kPacked && a.sb_d && sN <= a.cap && oN <= a.cap;
+      M.sb = sb;
+      M.b0 = b0;
+      M.b1 = b1;
+      M.d0 = d0;
+      M.sA = sA;
+      M.oA = oA;
+      M.staged = staged;
+      M.end = 0;
+      uint32_t *sI, *sS1, *sO;
+      uint16_t* sR;
+      stage(s, sI, sR, sS1, sO);
+      if (!bulk_I) {  // sub-bins of < 8 group words
+        uint32_t run = 0;
+        for (uint32_t i = 0; i < nw; ++i) {
+          const uint32_t w = __ldg(a.I + w0 + i);
+          sI[i] = w;
+          sR[i] = uint16_t(run);
+          run += __popc(w);
+        }
+      }
+      const uint32_t bytes = (bulk_I ? nw * 6u : 0u) + (staged ? (sN + oN) * 4u : 0u);
+      fence_proxy_async();
+      if (bytes) {
+        mbar_arrive_expect_tx(&full[s], bytes);
+        if (bulk_I) {
+          bulk_g2s(sI, a.I + w0, nw * 4u, &full[s]);
+          bulk_g2s(sR, a.r16 + w0, nw * 2u, &full[s]);
+        }
+        if (staged) {
+          bulk_g2s(sS1, a.S1 + sA, sN * 4u, &full[s]);
+          bulk_g2s(sO, a.O + oA, oN * 4u, &full[s]);
+        }
+      } else {
+        mbar_arrive(&full[s]);
+      }
+      ++k;
+    }
+    return;
+  }
+  WarpLists L;
+  L.k0 = s_k0[wid];
+  L.k1 = s_k1[wid];
+  L.slot = s_slot[wid];
+  L.out = s_out[wid];
+  for (uint32_t k = 0;; ++k) {
+    const uint32_t s = k & 1, j = k >> 1;
+    mbar_wait(&full[s], j & 1u);
+    const StageMeta M = meta[s];
+    if (M.end) break;
+    uint32_t *sI, *sS1, *sO;
+    uint16_t* sR;
+    stage(s, sI, sR, sS1, sO);
+    const uint32_t* S1p = M.staged ? sS1 - M.sA : a.S1;
+    const uint32_t* Op = M.staged ? sO - M.oA : a.O;
+    const uint32_t w0 = uint32_t((uint64_t(M.sb) << a.code_shift) >> 5);
+    const uint32_t nitems = M.b1 - M.b0;
+    const uint32_t my_lo = M.b0 + uint32_t(uint64_t(nitems) * wid / kWsCons);
+    const uint32_t my_hi = M.b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kWsCons);
+    join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  join_stats(a, L);
 }
 
 }  // namespace
@@ -356,33 +518,53 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   a.stats = counter.p + 1;
   if (keys.n == 0) keys.alloc(c, std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16));
   const bool rs = mode == 1;
-  const void* kfn = X.packed ? (rs ? (const void*)k_join<true, true> : (const void*)k_join<false, true>)
-                             : (rs ? (const void*)k_join<true, false> : (const void*)k_join<false, false>);
-  // staging capacity: what is left of a quarter of the SM's shared memory
-  // (4 resident CTAs) after the static arrays, I words and group starts
+  // Kernel choice (measured, profiles/r01/README.md): the warp-specialised
+  // pipeline wins when sub-bins are staged and hold a few hundred to a couple
+  // of thousand read q-grams (C2: 0.89 vs 0.97 ms), where the per-sub-bin
+  // barrier and staging wait of k_join are a large share; with tiny sub-bins
+  // (C1) its single producer thread is the bottleneck, with unstaged or very
+  // full ones (C3, C4) k_join's 4 CTAs per SM hide latency better.
+  // QGM_JOIN_WS=0/1 forces either.
+  const double per_sub = double(rp.V) / double(a.n_sub);
+  const bool stageable = X.packed && X.sb_d.p && X.sub_bits == rp.sub_bits;
+  const char* ws_env = std::getenv("QGM_JOIN_WS");
+  const bool use_ws = ws_env && ws_env[0] ? ws_env[0] == '1' : (stageable && per_sub >= 256 && per_sub <= 2048);
+  const void* kfn;
+  if (use_ws)
+    kfn = X.packed ? (rs ? (const void*)k_join_ws<true, true> : (const void*)k_join_ws<false, true>)
+                   : (rs ? (const void*)k_join_ws<true, false> : (const void*)k_join_ws<false, false>);
+  else
+    kfn = X.packed ? (rs ? (const void*)k_join<true, true> : (const void*)k_join<false, true>)
+                   : (rs ? (const void*)k_join<true, false> : (const void*)k_join<false, false>);
+  const int threads = use_ws ? kWsThreads : kJoinThreads;
+  const int per_sm = use_ws ? 2 : 4;     // resident CTAs the staging is sized for
+  const int stages = use_ws ? 2 : 1;
+  // staging capacity: what is left of the SM's shared memory share of one
+  // CTA after the static arrays, I words and group starts (per stage)
   cudaFuncAttributes fa;
   QGM_CUDA(cudaFuncGetAttributes(&fa, kfn));
   int dev = 0, smem_sm = 0;
   QGM_CUDA(cudaGetDevice(&dev));
   QGM_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
   const size_t fixed = size_t(a.words) * 4 + (size_t((a.words + 1) / 2 + 3) & ~size_t(3)) * 4;
-  const int64_t room = int64_t(smem_sm) / 4 - 1024 - int64_t(fa.sharedSizeBytes) - int64_t(fixed);
+  const int64_t room = (int64_t(smem_sm) / per_sm - 1024 - int64_t(fa.sharedSizeBytes)) / stages - int64_t(fixed);
   const bool can_stage = X.packed && X.sb_d.p && X.sub_bits == rp.sub_bits && room >= 2 * 4 * 256;
   a.r16 = X.sub_bits == rp.sub_bits ? X.r16.p : nullptr;
   a.sb_d = can_stage ? X.sb_d.p : nullptr;
   a.sb_o = can_stage ? X.sb_o.p : nullptr;
   a.cap = can_stage ? uint32_t(room / 8) & ~3u : 0u;
-  const size_t smem = fixed + size_t(2) * a.cap * 4;
+  uint32_t stage_words = uint32_t(fixed / 4) + 2 * a.cap;
+  const size_t smem = size_t(stages) * stage_words * 4;
   QGM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  const unsigned grid = std::min<unsigned>(a.n_sub, resident_grid(kfn, kJoinThreads, smem));
+  const unsigned grid = std::min<unsigned>(a.n_sub, resident_grid(kfn, threads, smem));
   for (int attempt = 0; attempt < 2; ++attempt) {
     counter.zero();
     a.out = keys.p;
     a.cap_out = keys.n;
     if (rp.V > 0) {
       KernelScope ks(c, "k_join");
-      void* args[] = {&a};
-      QGM_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(kJoinThreads), args, smem, c.stream));
+      void* args[] = {&a, &stage_words};
+      QGM_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(threads), args, smem, c.stream));
       ++c.launches;
     }
     unsigned long long h[3] = {0, 0, 0};
