@@ -127,12 +127,13 @@ __device__ __forceinline__ void flush_keys(const JoinArgs& a, WarpLists& L) {
 
 // The read q-gram items [my_lo, my_hi) of sub-bin `sb` (one warp): look up
 // the staged occupancy words / group starts, expand the occurrence intervals
-// (S1p / Op: global arrays, or generic pointers into the staged slices), emit
+// (S1p / Op / Ip: global arrays, or generic pointers into the staged slices), emit
 // the candidate keys.
 template <bool kRunStart, bool kPacked>
 __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI, const uint16_t* sR,
-                                           const uint32_t* S1p, const uint32_t* Op, uint32_t d0, uint32_t w0,
-                                           uint32_t gsub, uint32_t my_lo, uint32_t my_hi, WarpLists& L) {
+                                           const uint32_t* S1p, const uint32_t* Op, const uint64_t* Ip, uint32_t d0,
+                                           uint32_t w0, uint32_t gsub, uint32_t my_lo, uint32_t my_hi,
+                                           WarpLists& L) {
   const unsigned lane = lane_id();
   auto stage_key = [&](bool emit, uint64_t key) {  // all lanes call it
     const unsigned m = __ballot_sync(kFull, emit);
@@ -145,7 +146,7 @@ __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI
 #pragma unroll
   for (int u = 0; u < kItems; ++u) {
     const uint32_t it = my_lo + u * 32 + lane;
-    pn[u] = it < my_hi ? __ldg(a.items + it) : ~0ull;
+    pn[u] = it < my_hi ? Ip[it] : ~0ull;
   }
   for (uint32_t base = my_lo; base < my_hi; base += 32 * kItems) {  // warp-uniform bound
     uint32_t cnt = 0, nr = 0, rk0[kItems], rk1[kItems];
@@ -153,7 +154,7 @@ __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI
     for (int u = 0; u < kItems; ++u) {
       const uint64_t pr = pn[u];
       const uint32_t itn = base + 32 * kItems + u * 32 + lane;
-      pn[u] = itn < my_hi ? __ldg(a.items + itn) : ~0ull;
+      pn[u] = itn < my_hi ? Ip[itn] : ~0ull;
       const bool ok = pr != ~0ull;
       const uint32_t g = gsub | uint32_t(pr >> kItemCodeShift);
       const uint32_t wl = ok ? (g >> 5) - w0 : 0u, bit = g & 31u;
@@ -197,7 +198,7 @@ __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI
       if (e < nent) {
         k0 = L.k0[e];
         len = L.k1[e] - k0;
-        it = __ldg(a.items + base + L.slot[e]);
+        it = Ip[base + L.slot[e]];
       }
       const bool longi = len > kInline;
       const uint32_t nin = longi ? 0u : len;
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
   const uint32_t nw = a.words;
   uint32_t* sI = s_dyn;
   uint16_t* sR = reinterpret_cast<uint16_t*>(s_dyn + nw);
-  uint32_t* sS1 = s_dyn + nw + (((nw + 1) / 2 + 3) & ~3u);
+  uint32_t* sS1 = s_dyn + ((nw + (((nw + 1) / 2 + 3) & ~3u) + 3) & ~3u);
   uint32_t* sO = sS1 + a.cap;
   __shared__ uint32_t s_k0[kJoinWarps][kRanges];
   __shared__ uint32_t s_k1[kJoinWarps][kRanges];
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
     const uint32_t nitems = b1 - b0;
     const uint32_t my_lo = b0 + uint32_t(uint64_t(nitems) * wid / kJoinWarps);
     const uint32_t my_hi = b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kJoinWarps);
-    join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, d0, w0, sb << a.code_shift, my_lo, my_hi, L);
+    join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi, L);
     __syncthreads();  // the staging buffers are rewritten for the next sub-bin
   }
   join_stats(a, L);
@@ -360,12 +361,13 @@ constexpr int kWsCons = QGM_JOIN_WS_CONS;
 constexpr int kWsThreads = (kWsCons + 1) * 32;
 
 struct StageMeta {
-  uint32_t sb, b0, b1, d0, sA, oA, staged, end;
+  uint32_t sb, b0, b1, d0, sA, oA, iA, staged, items_staged, end;
 };
 
 template <bool kRunStart, bool kPacked>
-__global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t stage_words) {
-  extern __shared__ __align__(16) uint32_t s_dyn[];  // 2 stages: I [nw] | u16 starts | S' [cap] | O [cap]
+__global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t stage_words, uint32_t icap) {
+  // 2 stages: I [nw] | u16 starts | S' [cap] | O [cap] | items [icap] (u64)
+  extern __shared__ __align__(16) uint32_t s_dyn[];
   const uint32_t nw = a.words;
   __shared__ uint32_t s_k0[kWsCons][kRanges];
   __shared__ uint32_t s_k1[kWsCons][kRanges];
@@ -382,12 +384,13 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
     mbar_init(&empty[1], kWsCons);
   }
   __syncthreads();
-  auto stage = [&](uint32_t s, uint32_t*& sI, uint16_t*& sR, uint32_t*& sS1, uint32_t*& sO) {
+  auto stage = [&](uint32_t s, uint32_t*& sI, uint16_t*& sR, uint32_t*& sS1, uint32_t*& sO, uint64_t*& sIt) {
     uint32_t* base = s_dyn + s * stage_words;
     sI = base;
     sR = reinterpret_cast<uint16_t*>(base + nw);
-    sS1 = base + nw + (((nw + 1) / 2 + 3) & ~3u);
+    sS1 = base + ((nw + (((nw + 1) / 2 + 3) & ~3u) + 3) & ~3u);
     sO = sS1 + a.cap;
+    sIt = reinterpret_cast<uint64_t*>(sO + a.cap);
   };
   if (wid == kWsCons) {  // producer
     if (lane != 0) return;
@@ -421,6 +424,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
       const uint32_t sA = d0 & ~3u, oA = o0 & ~3u;
       const uint32_t sN = ((d1 + 1 + 3) & ~3u) - sA, oN = ((o1 + 3) & ~3u) - oA;
       const bool staged = kPacked && a.sb_d && sN <= a.cap && oN <= a.cap;
+      const uint32_t iA = b0 & ~1u, iN = ((b1 + 1) & ~1u) - iA;  // items, 16-byte aligned
+      const bool items_staged = iN <= icap;
       M.sb = sb;
       M.b0 = b0;
       M.b1 = b1;
@@ -428,10 +433,13 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
       M.sA = sA;
       M.oA = oA;
       M.staged = staged;
+      M.iA = iA;
+      M.items_staged = items_staged;
       M.end = 0;
       uint32_t *sI, *sS1, *sO;
       uint16_t* sR;
-      stage(s, sI, sR, sS1, sO);
+      uint64_t* sIt;
+      stage(s, sI, sR, sS1, sO, sIt);
       if (!bulk_I) {  // sub-bins of < 8 group words
         uint32_t run = 0;
         for (uint32_t i = 0; i < nw; ++i) {
@@ -441,10 +449,12 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
           run += __popc(w);
         }
       }
-      const uint32_t bytes = (bulk_I ? nw * 6u : 0u) + (staged ? (sN + oN) * 4u : 0u);
+      const uint32_t bytes =
+          (bulk_I ? nw * 6u : 0u) + (staged ? (sN + oN) * 4u : 0u) + (items_staged ? iN * 8u : 0u);
       fence_proxy_async();
       if (bytes) {
         mbar_arrive_expect_tx(&full[s], bytes);
+        if (items_staged) bulk_g2s(sIt, a.items + iA, iN * 8u, &full[s]);
         if (bulk_I) {
           bulk_g2s(sI, a.I + w0, nw * 4u, &full[s]);
           bulk_g2s(sR, a.r16 + w0, nw * 2u, &full[s]);
@@ -472,14 +482,16 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
     if (M.end) break;
     uint32_t *sI, *sS1, *sO;
     uint16_t* sR;
-    stage(s, sI, sR, sS1, sO);
+    uint64_t* sIt;
+    stage(s, sI, sR, sS1, sO, sIt);
     const uint32_t* S1p = M.staged ? sS1 - M.sA : a.S1;
     const uint32_t* Op = M.staged ? sO - M.oA : a.O;
+    const uint64_t* Ip = M.items_staged ? sIt - M.iA : a.items;
     const uint32_t w0 = uint32_t((uint64_t(M.sb) << a.code_shift) >> 5);
     const uint32_t nitems = M.b1 - M.b0;
     const uint32_t my_lo = M.b0 + uint32_t(uint64_t(nitems) * wid / kWsCons);
     const uint32_t my_hi = M.b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kWsCons);
-    join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
+    join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, Ip, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -546,14 +558,26 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   int dev = 0, smem_sm = 0;
   QGM_CUDA(cudaGetDevice(&dev));
   QGM_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-  const size_t fixed = size_t(a.words) * 4 + (size_t((a.words + 1) / 2 + 3) & ~size_t(3)) * 4;
-  const int64_t room = (int64_t(smem_sm) / per_sm - 1024 - int64_t(fa.sharedSizeBytes)) / stages - int64_t(fixed);
+  // I words + u16 starts, padded to 16 bytes (the S'/O/item slices that follow are bulk-copy targets)
+  const size_t fixed = (size_t(a.words) * 4 + (size_t((a.words + 1) / 2 + 3) & ~size_t(3)) * 4 + 15) & ~size_t(15);
+  int64_t room = (int64_t(smem_sm) / per_sm - 1024 - int64_t(fa.sharedSizeBytes)) / stages - int64_t(fixed);
+  // the warp-specialised kernel also stages the sub-bin's items when room is
+  // left for ~1.15x the average sub-bin (beyond the S'/O slices, sized first)
+  uint32_t icap = 0;
+  if (use_ws) {
+    const uint64_t want = (uint64_t(per_sub * 1.15) + 64) & ~uint64_t(1);
+    const uint64_t so_need = 2 * 4 * (uint64_t(double(X.can.distinct) / a.n_sub * 1.15) + 64);
+    if (room > int64_t(so_need + 8 * want)) {
+      icap = uint32_t(want);
+      room -= int64_t(8 * icap);
+    }
+  }
   const bool can_stage = X.packed && X.sb_d.p && X.sub_bits == rp.sub_bits && room >= 2 * 4 * 256;
   a.r16 = X.sub_bits == rp.sub_bits ? X.r16.p : nullptr;
   a.sb_d = can_stage ? X.sb_d.p : nullptr;
   a.sb_o = can_stage ? X.sb_o.p : nullptr;
   a.cap = can_stage ? uint32_t(room / 8) & ~3u : 0u;
-  uint32_t stage_words = uint32_t(fixed / 4) + 2 * a.cap;
+  uint32_t stage_words = uint32_t(fixed / 4) + 2 * a.cap + 2 * icap;
   const size_t smem = size_t(stages) * stage_words * 4;
   QGM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const unsigned grid = std::min<unsigned>(a.n_sub, resident_grid(kfn, threads, smem));
@@ -563,7 +587,7 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
     a.cap_out = keys.n;
     if (rp.V > 0) {
       KernelScope ks(c, "k_join");
-      void* args[] = {&a, &stage_words};
+      void* args[] = {&a, &stage_words, &icap};
       QGM_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(threads), args, smem, c.stream));
       ++c.launches;
     }

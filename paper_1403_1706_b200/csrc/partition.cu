@@ -415,7 +415,7 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   }
   exclusive_scan_u32(c, h2.p, out.soff.p, keys + 1, nullptr, nullptr);
   h2.zero();  // per-key cursors
-  out.pairs.alloc(c, V);
+  out.pairs.alloc(c, V + 2);  // +2: the join bulk-copies whole 16-byte pairs of items
   const size_t smem2 = kChunk * (sizeof(uint64_t) + sizeof(uint16_t));
   QGM_CUDA(cudaFuncSetAttribute(k_refine_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
   {
