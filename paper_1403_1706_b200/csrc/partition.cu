@@ -4,9 +4,10 @@
 // bits of their canonical code (canon_code, RefQIndex), so that the warps in
 // flight touch a few MiB of the reference index (L2-resident) instead of all
 // of it; it never needs the full read-side q-group index. Passes:
-//   P0 histogram : per-CTA shared-memory histogram over 2^bits code bins
-//                  (bits = min(2q, 8)), one global atomic per non-empty bin;
-//   scan         : bin offsets;
+//   P0 histogram : one CTA per SM counts the refined keys (top min(2q, 16)
+//                  code bits) in shared memory (packed u16 counters) and
+//                  flushes them with global atomics;
+//   scan         : sub-bin offsets; the P1 bin offsets are their prefixes;
 //   P1 scatter   : per chunk of 4096 q-gram slots, a local counting sort by
 //                  bin in shared memory, one global atomic per bin to reserve
 //                  the chunk's run, then runs copied out with consecutive
@@ -14,7 +15,7 @@
 //                  ~16 items = one 128 B line per bin per chunk at q=16);
 //   P2 refine    : the same staged counting sort on the next code bits (up to
 //                  16 in total), per chunk of 4096 bin-ordered items, writing
-//                  the final join items.
+//                  the final join items at the offsets P0 already counted.
 // ncu on an earlier single-pass scatter (12-bit bins, items written straight
 // from registers) showed 1.6 GB of read-for-ownership and 2.1 GB of writes for
 // 0.68 GB of output: partial sectors of 2.4M concurrently open runs.
@@ -85,26 +86,54 @@ struct ItemGen {
   }
 };
 
-__global__ void __launch_bounds__(kPartThreads) k_part_hist(ItemGen gen, uint32_t n_items, uint32_t chunk,
-                                                            unsigned shift, uint32_t* __restrict__ hist) {
-  __shared__ uint32_t h[kBins];
-  for (uint32_t b = threadIdx.x; b < kBins; b += kPartThreads) h[b] = 0;
+// P0 over the refined keys: one CTA per SM counts the top key_bits bits of
+// its contiguous share of the slots in shared memory -- two u16 counters per
+// u32 word (128 KiB for 16-bit keys) -- and flushes the non-zero counts with
+// global atomics. The P1 bin offsets and the P2 sub-bin offsets both come
+// from this one histogram, so the refinement needs no counting pass. A u16
+// counter that wraps (more than 65535 equal keys in one CTA's share) hands
+// 65536 to the global count and takes back the carry it pushed into its
+// neighbour.
+constexpr int kHistThreads = 1024;
+__global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen gen, uint32_t n_items, uint32_t per_cta,
+                                                                 unsigned kshift, uint32_t keys,
+                                                                 uint32_t* __restrict__ hist) {
+  extern __shared__ uint32_t h2[];  // keys / 2 words (keys >= 2)
+  const uint32_t words = (keys + 1) / 2;
+  for (uint32_t i = threadIdx.x; i < words; i += kHistThreads) h2[i] = 0;
   __syncthreads();
-  const uint32_t c0 = blockIdx.x * chunk, c1 = min(n_items, c0 + chunk);
-  for (uint32_t t0 = c0; t0 < c1; t0 += 4 * kPartThreads) {
+  const uint32_t c0 = blockIdx.x * per_cta, c1 = min(n_items, c0 + per_cta);
+  auto count = [&](uint32_t key) {
+    const uint32_t sh = (key & 1u) * 16u;
+    const uint32_t old = atomicAdd(h2 + (key >> 1), 1u << sh);
+    if (((old >> sh) & 0xFFFFu) == 0xFFFFu) {  // wrapped
+      atomicAdd(hist + key, 65536u);
+      if (sh == 0) atomicSub(h2 + (key >> 1), 1u << 16);  // the carry went into the high counter
+    }
+  };
+  for (uint32_t t0 = c0; t0 < c1; t0 += 4 * kHistThreads) {
     Slot sl[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) gen.fetch<false>(t0 + k * kPartThreads + threadIdx.x, sl[k]);
+    for (int k = 0; k < 4; ++k) gen.fetch<false>(t0 + k * kHistThreads + threadIdx.x, sl[k]);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t t = t0 + k * kPartThreads + threadIdx.x;
+      const uint32_t t = t0 + k * kHistThreads + threadIdx.x;
       uint32_t f, g;
-      if (t < c1 && gen.code(t, sl[k], f, g)) atomicAdd(h + (g >> shift), 1u);
+      if (t < c1 && gen.code(t, sl[k], f, g)) count(g >> kshift);
     }
   }
   __syncthreads();
-  for (uint32_t b = threadIdx.x; b < kBins; b += kPartThreads)
-    if (h[b]) atomicAdd(hist + b, h[b]);
+  for (uint32_t i = threadIdx.x; i < words; i += kHistThreads) {
+    const uint32_t w = h2[i];
+    if (w & 0xFFFFu) atomicAdd(hist + 2 * i, w & 0xFFFFu);
+    if (w >> 16) atomicAdd(hist + 2 * i + 1, w >> 16);
+  }
+}
+
+// P1 bin offsets from the refined-key offsets: boff[b] = soff[b << sub]
+__global__ void k_bin_offsets(const uint32_t* __restrict__ soff, uint32_t nbins, unsigned sub,
+                              uint32_t* __restrict__ boff) {
+  for (uint32_t b = threadIdx.x; b <= nbins; b += blockDim.x) boff[b] = soff[b << sub];
 }
 
 __global__ void __launch_bounds__(kPartThreads, 2) k_part_scatter(ItemGen gen, uint32_t n_items, unsigned shift,
@@ -213,49 +242,6 @@ __device__ __forceinline__ uint32_t bin_search(const uint32_t* sboff, uint32_t n
     if (sboff[mid] <= i) lo = mid; else hi = mid;
   }
   return lo;
-}
-
-__global__ void __launch_bounds__(kPartThreads) k_refine_hist(const uint64_t* __restrict__ in, uint32_t n,
-                                                              const uint32_t* __restrict__ boff, Refine rf,
-                                                              unsigned sub, uint32_t* __restrict__ hist) {
-  __shared__ uint32_t h[kLocal];
-  __shared__ uint32_t sboff[kBins + 1];
-  for (uint32_t b = threadIdx.x; b <= rf.nbins; b += kPartThreads) sboff[b] = boff[b];
-  __syncthreads();
-  const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
-  for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
-    const uint32_t c0 = ch * kChunk, c1 = min(n, c0 + kChunk);
-    const uint32_t bfirst = bin_search(sboff, rf.nbins, c0), blast = bin_search(sboff, rf.nbins, c1 - 1);
-    const uint32_t base = (rf.key(in[c0], bfirst) >> sub) << sub;
-    const uint32_t width = (((rf.key(in[c1 - 1], blast) >> sub) + 1) << sub) - base;
-    uint32_t b = bfirst;
-    if (width > kLocal) {  // rare: many tiny bins in one chunk
-      for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) {
-        while (sboff[b + 1] <= i) ++b;
-        atomicAdd(hist + rf.key(in[i], b), 1u);
-      }
-      continue;
-    }
-    for (uint32_t k = threadIdx.x; k < width; k += kPartThreads) h[k] = 0;
-    __syncthreads();
-    if (bfirst == blast) {  // the common case: the chunk lies in one P1 bin
-      uint64_t v[kPer];
-#pragma unroll
-      for (uint32_t k = 0; k < kPer; ++k) v[k] = __ldg(in + min(c0 + k * kPartThreads + threadIdx.x, c1 - 1));
-#pragma unroll
-      for (uint32_t k = 0; k < kPer; ++k)
-        if (c0 + k * kPartThreads + threadIdx.x < c1) atomicAdd(h + rf.key(v[k], b) - base, 1u);
-    } else {
-      for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) {
-        while (sboff[b + 1] <= i) ++b;
-        atomicAdd(h + rf.key(in[i], b) - base, 1u);
-      }
-    }
-    __syncthreads();
-    for (uint32_t k = threadIdx.x; k < width; k += kPartThreads)
-      if (h[k]) atomicAdd(hist + base + k, h[k]);
-    __syncthreads();
-  }
 }
 
 __global__ void __launch_bounds__(kPartThreads, 2) k_refine_scatter(const uint64_t* __restrict__ in, uint32_t n,
@@ -367,23 +353,31 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
     out.soff.zero();
   };
   if (n_items == 0) return empty();
-  const uint32_t chunk = uint32_t(std::max<uint64_t>(kChunk, ceil_div(n_items, uint64_t(kSMs) * 8)));
-  DBuf<uint32_t> hist(c, kBins + 1);
-  hist.zero();
+  // P0: histogram of the refined keys (the P1 bins are its prefixes)
+  const uint32_t keys = 1u << key_bits;
+  const unsigned sub = key_bits - bits;
+  out.soff.alloc(c, keys + 1);
+  DBuf<uint32_t> h2(c, keys + 1);
+  h2.zero();
   {
+    const uint32_t per_cta = uint32_t(ceil_div(ceil_div(n_items, uint64_t(kSMs)), 4 * kHistThreads) * 4 * kHistThreads);
+    const size_t hsmem = size_t((keys + 1) / 2) * 4;
+    QGM_CUDA(cudaFuncSetAttribute(k_part_hist16, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsmem)));
     KernelScope ks(c, "k_part_hist");
-    QGM_KERNEL(c, k_part_hist, unsigned(ceil_div(n_items, chunk)), kPartThreads, 0, gen, n_items, chunk, shift,
-               hist.p);
+    QGM_KERNEL(c, k_part_hist16, unsigned(ceil_div(n_items, per_cta)), kHistThreads, hsmem, gen, n_items, per_cta,
+               2 * q - key_bits, keys, h2.p);
   }
   DBuf<uint32_t> total(c, 1);
-  exclusive_scan_u32(c, hist.p, out.boff.p, kBins + 1, total.p, nullptr);
+  exclusive_scan_u32(c, h2.p, out.soff.p, keys + 1, total.p, nullptr);
+  QGM_KERNEL(c, k_bin_offsets, 1, 256, 0, out.soff.p, 1u << bits, sub, out.boff.p);
   uint32_t V = 0;
   QGM_CUDA(cudaMemcpyAsync(&V, total.p, 4, cudaMemcpyDeviceToHost, c.stream));
   QGM_CUDA(cudaStreamSynchronize(c.stream));
   if (V == 0) return empty();
   out.V = V;
+  DBuf<uint32_t> hist(c, kBins + 1);  // per-bin cursors of P1
+  hist.zero();
   DBuf<uint64_t> p1(c, V);
-  hist.zero();  // reused as the per-bin global cursors
   const size_t smem = kChunk * (sizeof(uint64_t) + sizeof(uint8_t));
   QGM_CUDA(cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n_items, kChunk), uint64_t(kSMs) * 4));
@@ -403,17 +397,7 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   rf.by_stride = FastDiv(std::max<uint32_t>(reads.stride, 1));
   rf.q = q;
   rf.uniform = reads.min_len == reads.stride;
-  const unsigned sub = key_bits - bits;
-  const uint32_t keys = 1u << key_bits;
-  DBuf<uint32_t> h2(c, keys + 1);
-  out.soff.alloc(c, keys + 1);
-  h2.zero();
   const unsigned grid2 = unsigned(std::min<uint64_t>(ceil_div(V, kChunk), uint64_t(kSMs) * 4));
-  {
-    KernelScope ks(c, "k_refine_hist");
-    QGM_KERNEL(c, k_refine_hist, grid2, kPartThreads, 0, p1.p, V, out.boff.p, rf, sub, h2.p);
-  }
-  exclusive_scan_u32(c, h2.p, out.soff.p, keys + 1, nullptr, nullptr);
   h2.zero();  // per-key cursors
   out.pairs.alloc(c, V + 2);  // +2: the join bulk-copies whole 16-byte pairs of items
   const size_t smem2 = kChunk * (sizeof(uint64_t) + sizeof(uint16_t));

@@ -241,3 +241,24 @@ def test_streamed_batches_equal_single_calls(ctx):
     for (words, lengths, stride), (hits, st) in zip(batches, got):
         want, wst = ctx.map_host(words, lengths, stride, R, q=14, mode=1)
         assert _same(hits, want) and st == wst
+
+
+def test_partition_counter_wrap_with_a_dominant_qgram(ctx, oracle):
+    """100k poly-A reads first in the batch put more than 65535 copies of one
+    canonical q-gram into a single histogram CTA's share (the packed u16
+    shared-memory counters wrap and hand 65536 to the global count); the
+    20k ordinary reads behind them must still map exactly like the oracle."""
+    import paper_1403_1706_b200 as qgm
+    L = 400_000
+    ref = qgm.random_reference(61, L)
+    cb = np.array([0, L], np.uint64)
+    codes, lengths, *_ = qgm.simulate_reads(62, ref, cb, 20_000, 100, 0.03)
+    n_poly = 100_000
+    codes = np.concatenate([np.zeros(n_poly * 100, np.uint8), codes])
+    lengths = np.concatenate([np.full(n_poly, 100, np.uint32), lengths])
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    got, st = ctx.map(reads, R, q=16, mode=0)
+    want, ost = oracle.map(ref, cb, codes, 100, lengths, q=16, mode=0)
+    assert st["index_occurrences"] == lengths.size * 85
+    assert _same(got, want), (got.size, want.size)
