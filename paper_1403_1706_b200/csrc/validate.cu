@@ -22,6 +22,9 @@ namespace qgm {
 namespace {
 
 constexpr int kValThreads = 128;
+#ifdef QGM_VAL_HIST
+__device__ unsigned long long g_exit_hist[16];  // debug: abandon row / 16, [15] = ran to the end
+#endif
 
 struct ValArgs {
   const uint2* rplanes;
@@ -105,20 +108,25 @@ template <> struct Band<uint64_t> {
 // every row with non-decreasing cost, so k >= min_t D[i][t] >= D[i][0] -
 // popc(Mv) at any row i; once that bound exceeds kmax the candidate cannot
 // pass the identity threshold (used by the map path only, kmax < 0 = never).
+// Rows of chunks [c_begin, c_end) (32 rows per chunk). Returns kAbandoned,
+// kDone (the last row was processed) or kPaused (stopped at c_end < chunks).
+constexpr int kAbandoned = 0, kDone = 1, kPaused = 2;
 template <class T, bool kCheck, bool kFull>
-__device__ __forceinline__ bool myers_rows(const ValArgs& a, uint32_t r, bool rev, uint32_t n, int64_t F, uint32_t L,
-                                           int64_t cbeg, int64_t cend, T mask_rt, T& Pv, T& Mv, int& score0,
-                                           int kmax) {
+__device__ __forceinline__ int myers_rows(const ValArgs& a, uint32_t r, bool rev, uint32_t n, int64_t F, uint32_t L,
+                                          int64_t cbeg, int64_t cend, T mask_rt, T& Pv, T& Mv, int& score0,
+                                          int kmax, uint32_t c_begin, uint32_t c_end) {
   // kFull: the band fills the word (B = 32 / 64), every mask is a no-op
   const T mask = kFull ? T(~T(0)) : mask_rt;
   constexpr int NW = Band<T>::kWords;
   const uint2* rp = a.rplanes + uint64_t(r) * a.Wp;
   Win w[NW + 1];
 #pragma unroll
-  for (int i = 0; i <= NW; ++i) w[i] = load_win(a.fplanes, F + int64_t(L) - 32 * (i + 1), cbeg, cend, !kCheck);
+  for (int i = 0; i <= NW; ++i)
+    w[i] = load_win(a.fplanes, F + int64_t(L) - 32 * int64_t(c_begin + i + 1), cbeg, cend, !kCheck);
   const uint32_t chunks = (n + 31) >> 5;
-  for (uint32_t c = 0; c < chunks; ++c) {
-    if (c > 0) {
+  const uint32_t c_stop = min(chunks, c_end);
+  for (uint32_t c = c_begin; c < c_stop; ++c) {
+    if (c > c_begin) {
 #pragma unroll
       for (int i = 0; i < NW; ++i) w[i] = w[i + 1];
       w[NW] = load_win(a.fplanes, F + int64_t(L) - 32 * int64_t(c + NW + 1), cbeg, cend, !kCheck);
@@ -159,30 +167,79 @@ __device__ __forceinline__ bool myers_rows(const ValArgs& a, uint32_t r, bool re
 #pragma unroll
       for (uint32_t t = 0; t < 32; ++t) {
         row(t);
-        if ((t & 15) == 15 && kmax >= 0 && score0 - int(popcount_t(Mv)) > kmax) return false;
+        if ((t & 15) == 15 && kmax >= 0 && score0 - int(popcount_t(Mv)) > kmax) {
+#ifdef QGM_VAL_HIST
+          atomicAdd(&g_exit_hist[min(14u, (32 * c + t) / 16)], 1ull);
+#endif
+          return kAbandoned;
+        }
       }
     } else {
 #pragma unroll 4
       for (uint32_t t = 0; t < rows; ++t) {
         row(t);
-        if ((t & 15) == 15 && kmax >= 0 && score0 - int(popcount_t(Mv)) > kmax) return false;
+        if ((t & 15) == 15 && kmax >= 0 && score0 - int(popcount_t(Mv)) > kmax) return kAbandoned;
       }
     }
   }
-  return true;
+  if (c_stop < chunks) return kPaused;
+#ifdef QGM_VAL_HIST
+  atomicAdd(&g_exit_hist[15], 1ull);
+#endif
+  return kDone;
 }
 
+// Validation in up to two phases on the map path: phase 1 runs every
+// candidate for its first c_split chunks of 32 rows and parks the survivors
+// (candidate index + Pv, Mv, score0) in a compact list; phase 2 resumes only
+// those. Candidates of random windows are abandoned around row 64 (n = 100)
+// while true hits run all n rows; mixed in one warp, every warp would run n
+// rows -- after the split, phase-1 warps stop at the split and phase-2 warps
+// are full of candidates that need the remaining rows.
+struct Parked {
+  uint32_t i, score0;
+  uint32_t pv[2], mv[2];  // T = u32 uses word 0
+};
+
 template <class T>
-__global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a) {
+__device__ __forceinline__ void pack_state(Parked& p, T Pv, T Mv) {
+  p.pv[0] = uint32_t(Pv);
+  p.mv[0] = uint32_t(Mv);
+  p.pv[1] = sizeof(T) == 8 ? uint32_t(uint64_t(Pv) >> 32) : 0u;
+  p.mv[1] = sizeof(T) == 8 ? uint32_t(uint64_t(Mv) >> 32) : 0u;
+}
+template <class T>
+__device__ __forceinline__ void unpack_state(const Parked& p, T& Pv, T& Mv) {
+  if (sizeof(T) == 8) {
+    Pv = T((uint64_t(p.pv[1]) << 32) | p.pv[0]);
+    Mv = T((uint64_t(p.mv[1]) << 32) | p.mv[0]);
+  } else {
+    Pv = T(p.pv[0]);
+    Mv = T(p.mv[0]);
+  }
+}
+
+// kPhase 0: every row (qgm_validate, or no split); 1: chunks [0, c_split),
+// survivors parked; 2: resume the parked candidates from chunk c_split.
+template <class T, int kPhase>
+__global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_split, Parked* __restrict__ park,
+                                                          unsigned long long* __restrict__ n_park) {
   const T mask = a.B >= sizeof(T) * 8 ? T(~T(0)) : T((T(1) << a.B) - 1);
   const uint64_t dmask = (uint64_t(1) << a.diag_bits) - 1;
-  for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < a.n; base += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t i = base + threadIdx.x;
-    bool kept = false, in_range = false;
+  const uint64_t total = kPhase == 2 ? *n_park : a.n;
+  for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < total; base += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t slot_i = base + threadIdx.x;
+    bool kept = false, in_range = false, parked = false;
     int k = 0;
     uint32_t start = 0, ref_start = 0, r = 0, c = 0;
     bool rev = false;
-    if (i < a.n) {
+    uint64_t i = slot_i;
+    Parked pk{};
+    if (kPhase == 2 && slot_i < total) {
+      pk = park[slot_i];
+      i = pk.i;
+    }
+    if (slot_i < total) {
       const uint64_t key = a.keys[i];
       r = uint32_t(key >> (a.diag_bits + 1));
       rev = (key >> a.diag_bits) & 1;
@@ -204,41 +261,57 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a) {
         in_range = true;
         T Pv = 0, Mv = 0;
         int score0 = 0;
+        if (kPhase == 2) {
+          unpack_state<T>(pk, Pv, Mv);
+          score0 = int(pk.score0);
+        }
         const int64_t F = cbeg + w0;
         // map path: abandon candidates that can no longer reach the threshold
         const int kmax = a.mode == 0 ? int((uint64_t(100 - a.pct) * n) / 100) : -1;
         const bool interior = w0 >= 0 && w0 + int64_t(L) <= Lc;
         const bool full = a.B == sizeof(T) * 8;
-        bool done;
+        const uint32_t cb0 = kPhase == 2 ? c_split : 0u, cb1 = kPhase == 1 ? c_split : 0xFFFFFFFFu;
+        int st;
         if (interior && full)
-          done = myers_rows<T, false, true>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax);
+          st = myers_rows<T, false, true>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax, cb0, cb1);
         else if (interior)
-          done = myers_rows<T, false, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax);
+          st = myers_rows<T, false, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax, cb0, cb1);
         else
-          done = myers_rows<T, true, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax);
-        int v = score0, best = score0;
-        unsigned tbest = 0;
-        for (unsigned t = 1; t < a.B; ++t) {
-          v += int((Pv >> t) & T(1)) - int((Mv >> t) & T(1));
-          if (v <= best) { best = v; tbest = t; }
+          st = myers_rows<T, true, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax, cb0, cb1);
+        if (kPhase == 1 && st == kPaused) {
+          parked = true;
+          pk.i = uint32_t(i);
+          pk.score0 = uint32_t(score0);
+          pack_state<T>(pk, Pv, Mv);
+        } else {
+          int v = score0, best = score0;
+          unsigned tbest = 0;
+          for (unsigned t = 1; t < a.B; ++t) {
+            v += int((Pv >> t) & T(1)) - int((Mv >> t) & T(1));
+            if (v <= best) { best = v; tbest = t; }
+          }
+          k = best;
+          start = a.B - 1 - tbest;
+          int64_t rs = w0 + int64_t(start);
+          rs = rs < 0 ? 0 : (rs > Lc - 1 ? Lc - 1 : rs);
+          ref_start = uint32_t(rs);
+          kept = st == kDone && k <= int(n) && uint64_t(100) * uint64_t(int64_t(n) - k) >= uint64_t(a.pct) * n;
         }
-        k = best;
-        start = a.B - 1 - tbest;
-        int64_t rs = w0 + int64_t(start);
-        rs = rs < 0 ? 0 : (rs > Lc - 1 ? Lc - 1 : rs);
-        ref_start = uint32_t(rs);
-        kept = done && k <= int(n) && uint64_t(100) * uint64_t(int64_t(n) - k) >= uint64_t(a.pct) * n;
       }
     }
+    if (kPhase == 1) {
+      const unsigned long long ps = warp_append(parked, n_park);
+      if (parked) park[ps] = pk;
+    }
     if (a.mode == 0) {
-      const bool emit = i < a.n && in_range && kept;
+      const bool emit = slot_i < total && in_range && kept;
       const unsigned long long slot = warp_append(emit, a.counter);
       if (emit) {
         const uint64_t gstart = __ldg(a.cbp + c) + ref_start;
         a.hit_keys[slot] = (uint64_t(r) << (a.diag_bits + 1)) | (gstart << 1) | uint64_t(rev);
         a.hit_vals[slot] = uint32_t(k);
       }
-    } else if (i < a.n) {
+    } else if (slot_i < total) {
       uint32_t* o = reinterpret_cast<uint32_t*>(static_cast<char*>(a.validated) + i * 20);
       o[0] = uint32_t(k);
       o[1] = start;
@@ -279,8 +352,32 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
   a.validated = d_validated;
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, kValThreads), uint64_t(kSMs) * 32));
   KernelScope ks(c, "k_validate");
-  if (band <= 32) QGM_KERNEL(c, k_validate<uint32_t>, grid, kValThreads, 0, a);
-  else QGM_KERNEL(c, k_validate<uint64_t>, grid, kValThreads, 0, a);
+  // map path: split after ~60% of the rows when at least one chunk remains
+  // (a lower bound on the cost only becomes large enough to abandon a random
+  // window past about half the read, profiles/r01/README.md)
+  const uint32_t chunks = (reads.max_len + 31) / 32;
+  const uint32_t c_split = uint32_t((reads.max_len * 0.6 + 16) / 32);
+  if (mode == 0 && c_split >= 1 && c_split < chunks) {
+    DBuf<Parked> park(c, n);
+    DBuf<unsigned long long> np(c, 1);
+    np.zero();
+    if (band <= 32) {
+      QGM_KERNEL(c, (k_validate<uint32_t, 1>), grid, kValThreads, 0, a, c_split, park.p, np.p);
+      QGM_KERNEL(c, (k_validate<uint32_t, 2>), grid, kValThreads, 0, a, c_split, park.p, np.p);
+    } else {
+      QGM_KERNEL(c, (k_validate<uint64_t, 1>), grid, kValThreads, 0, a, c_split, park.p, np.p);
+      QGM_KERNEL(c, (k_validate<uint64_t, 2>), grid, kValThreads, 0, a, c_split, park.p, np.p);
+    }
+    return;
+  }
+  if (band <= 32) QGM_KERNEL(c, (k_validate<uint32_t, 0>), grid, kValThreads, 0, a, 0u, nullptr, nullptr);
+  else QGM_KERNEL(c, (k_validate<uint64_t, 0>), grid, kValThreads, 0, a, 0u, nullptr, nullptr);
 }
 
 }  // namespace qgm
+
+#ifdef QGM_VAL_HIST
+extern "C" int qgm_debug_validate_hist(unsigned long long* out) {
+  return int(cudaMemcpyFromSymbol(out, qgm::g_exit_hist, sizeof(unsigned long long) * 16));
+}
+#endif
