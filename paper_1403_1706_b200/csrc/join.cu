@@ -51,7 +51,6 @@ constexpr int kJoinWarps = kJoinThreads / 32;
 #endif
 constexpr int kItems = QGM_JOIN_ITEMS;    // read q-grams (= lookups) per lane per step
 constexpr int kRanges = 32 * kItems;
-constexpr int kStage = 64;                // staged keys per warp
 constexpr uint32_t kInline = 4;           // intervals up to this length are expanded in-lane
 constexpr uint32_t kMaxWords = 2048;      // group words per sub-bin (q = 16)
 constexpr uint32_t kPosMask = (1u << kPackedPosBits) - 1u;
@@ -80,15 +79,16 @@ struct JoinArgs {
   unsigned long long* stats;
 };
 
-// One (reference occurrence k, join item it) pair -> candidate key; false if
-// its strand is not requested or the run-start rule suppresses it (the
-// (q+1)-gram one base to the left on the same diagonal also matches).
-// Op: O, or the shared-memory slice of a staged sub-bin (generic pointer).
+// One (reference occurrence k, join item it) pair: true if it yields a
+// candidate -- its strand is requested and the run-start rule does not
+// suppress it (the (q+1)-gram one base to the left on the same diagonal also
+// matches). xp = the occurrence's padded coordinate; the item is returned
+// with its fr bit replaced by the candidate's strand. Op: O, or the
+// shared-memory slice of a staged sub-bin (generic pointer).
 template <bool kRunStart, bool kPacked>
-__device__ __forceinline__ bool expand(const JoinArgs& a, const uint32_t* Op, uint32_t k, uint64_t it,
-                                       uint64_t& key) {
+__device__ __forceinline__ bool match(const JoinArgs& a, const uint32_t* Op, uint32_t k, uint64_t& it, uint32_t& xp) {
   const uint32_t ov = Op[k];
-  const uint32_t xp = kPacked ? (ov & kPosMask) : ov;
+  xp = kPacked ? (ov & kPosMask) : ov;
   const uint32_t ex = kPacked ? (ov >> kPackedPosBits) : uint32_t(__ldg(a.X + k));
   const uint32_t rev = ((ex >> 3) ^ uint32_t(it >> kItemFrShift)) & 1u;
   if (!((a.strands >> rev) & 1)) return false;
@@ -96,33 +96,53 @@ __device__ __forceinline__ bool expand(const JoinArgs& a, const uint32_t* Op, ui
     const uint32_t rbase = uint32_t(it >> (rev ? kItemRbShift : kItemFbShift)) & 7u;
     if ((ex & 7u) == rbase && rbase < 4) return false;
   }
+  it = (it & ~(uint64_t(1) << kItemFrShift)) | (uint64_t(rev) << kItemFrShift);
+  return true;
+}
+
+// Candidate key of a matched pair (item with the strand in its fr bit).
+__device__ __forceinline__ uint64_t make_key(const JoinArgs& a, uint64_t it, uint32_t xp) {
+  const uint32_t rev = uint32_t(it >> kItemFrShift) & 1u;
   const uint32_t pp = uint32_t(it);
   const uint32_t r = a.by_m.div(pp), o = pp - r * a.m;
   uint32_t off = o;  // forward: d = p - o
   if (rev) off = a.tail_ok ? uint32_t(it >> kItemTailShift) & kItemTailMax : __ldg(a.rlen + r) - a.q - o;  // d = p - (n - q - o)
-  key = (uint64_t(r) << (a.diag_bits + 1)) | (uint64_t(rev) << a.diag_bits) | uint64_t(xp - off);
-  return true;
+  return (uint64_t(r) << (a.diag_bits + 1)) | (uint64_t(rev) << a.diag_bits) | uint64_t(xp - off);
 }
 
-// Per-warp join state: the compaction list and the key staging buffer.
+// Per-warp join state: the compaction list and the emission buffer. Only
+// ~9% of the visited occurrences yield a candidate (run-start rule), so the
+// matched pairs are buffered (item + coordinate) and their keys built 32 at a
+// time by the whole warp, then written as one coalesced run -- instead of
+// building keys in whichever lanes happen to match in every round.
+constexpr uint32_t kEmitCap = 64;
 struct WarpLists {
   uint32_t* k0;
   uint32_t* k1;
   uint8_t* slot;
-  uint64_t* out;
+  uint64_t* eit;  // kEmitCap matched items
+  uint32_t* exp;  // their coordinates
   uint32_t staged = 0;
   unsigned long long n_hit = 0, n_occ = 0;
 };
 
-__device__ __forceinline__ void flush_keys(const JoinArgs& a, WarpLists& L) {
+// keys of the last `cnt` (<= 32) buffered pairs -> one run of the output
+__device__ __forceinline__ void drain(const JoinArgs& a, WarpLists& L, uint32_t cnt) {
   const unsigned lane = lane_id();
   unsigned long long base = 0;
-  if (lane == 0 && L.staged) base = atomicAdd(a.counter, (unsigned long long)L.staged);
+  if (lane == 0) base = atomicAdd(a.counter, (unsigned long long)cnt);
   base = __shfl_sync(kFull, base, 0);
-  for (uint32_t i = lane; i < L.staged; i += 32)
-    if (base + i < a.cap_out) a.out[base + i] = L.out[i];
-  L.staged = 0;
+  if (lane < cnt) {
+    const uint32_t e = L.staged - cnt + lane;
+    const uint64_t key = make_key(a, L.eit[e], L.exp[e]);
+    if (base + lane < a.cap_out) a.out[base + lane] = key;
+  }
+  L.staged -= cnt;
   __syncwarp();
+}
+
+__device__ __forceinline__ void flush_keys(const JoinArgs& a, WarpLists& L) {
+  while (L.staged) drain(a, L, min(L.staged, 32u));
 }
 
 // The read q-gram items [my_lo, my_hi) of sub-bin `sb` (one warp): look up
@@ -135,12 +155,16 @@ __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI
                                            uint32_t w0, uint32_t gsub, uint32_t my_lo, uint32_t my_hi,
                                            WarpLists& L) {
   const unsigned lane = lane_id();
-  auto stage_key = [&](bool emit, uint64_t key) {  // all lanes call it
+  auto stage = [&](bool emit, uint64_t it, uint32_t xp) {  // all lanes call it
     const unsigned m = __ballot_sync(kFull, emit);
-    if (emit) L.out[L.staged + __popc(m & lanemask_lt())] = key;
+    if (emit) {
+      const uint32_t e = L.staged + __popc(m & lanemask_lt());
+      L.eit[e] = it;
+      L.exp[e] = xp;
+    }
     L.staged += __popc(m);
     __syncwarp();
-    if (L.staged > kStage - 32) flush_keys(a, L);
+    if (L.staged >= 32) drain(a, L, 32);
   };
   uint64_t pn[kItems];  // next step's items, loaded one step ahead
 #pragma unroll
@@ -204,9 +228,10 @@ __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI
       const uint32_t nin = longi ? 0u : len;
       const uint32_t rounds = __reduce_max_sync(kFull, nin);
       for (uint32_t t = 0; t < rounds; ++t) {
-        uint64_t key = 0;
-        const bool emit = t < nin && expand<kRunStart, kPacked>(a, Op, k0 + t, it, key);
-        stage_key(emit, key);
+        uint64_t mit = it;
+        uint32_t xp = 0;
+        const bool emit = t < nin && match<kRunStart, kPacked>(a, Op, k0 + t, mit, xp);
+        stage(emit, mit, xp);
       }
       unsigned lm = __ballot_sync(kFull, longi);
       while (lm) {
@@ -215,9 +240,10 @@ __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI
         const uint32_t lk0 = __shfl_sync(kFull, k0, src), llen = __shfl_sync(kFull, len, src);
         const uint64_t lit = __shfl_sync(kFull, it, src);
         for (uint32_t t0 = 0; t0 < llen; t0 += 32) {
-          uint64_t key = 0;
-          const bool emit = t0 + lane < llen && expand<kRunStart, kPacked>(a, Op, lk0 + t0 + lane, lit, key);
-          stage_key(emit, key);
+          uint64_t mit = lit;
+          uint32_t xp = 0;
+          const bool emit = t0 + lane < llen && match<kRunStart, kPacked>(a, Op, lk0 + t0 + lane, mit, xp);
+          stage(emit, mit, xp);
         }
       }
     }
@@ -247,7 +273,8 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
   __shared__ uint32_t s_k0[kJoinWarps][kRanges];
   __shared__ uint32_t s_k1[kJoinWarps][kRanges];
   __shared__ uint8_t s_slot[kJoinWarps][kRanges];  // item slot u*32 + lane
-  __shared__ uint64_t s_out[kJoinWarps][kStage];
+  __shared__ uint64_t s_eit[kJoinWarps][kEmitCap];
+  __shared__ uint32_t s_exp[kJoinWarps][kEmitCap];
   __shared__ __align__(8) uint64_t s_bar;
 
   const unsigned wid = threadIdx.x >> 5;
@@ -255,7 +282,8 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
   L.k0 = s_k0[wid];
   L.k1 = s_k1[wid];
   L.slot = s_slot[wid];
-  L.out = s_out[wid];
+  L.eit = s_eit[wid];
+  L.exp = s_exp[wid];
   const bool bulk_I = a.r16 != nullptr;  // sub-bins of >= 8 group words: whole 16-byte chunks
   if (threadIdx.x == 0) mbar_init(&s_bar, 1);
   __syncthreads();
@@ -372,7 +400,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
   __shared__ uint32_t s_k0[kWsCons][kRanges];
   __shared__ uint32_t s_k1[kWsCons][kRanges];
   __shared__ uint8_t s_slot[kWsCons][kRanges];
-  __shared__ uint64_t s_out[kWsCons][kStage];
+  __shared__ uint64_t s_eit[kWsCons][kEmitCap];
+  __shared__ uint32_t s_exp[kWsCons][kEmitCap];
   __shared__ StageMeta meta[2];
   __shared__ __align__(8) uint64_t full[2], empty[2];
   const unsigned wid = threadIdx.x >> 5, lane = lane_id();
@@ -474,7 +503,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
   L.k0 = s_k0[wid];
   L.k1 = s_k1[wid];
   L.slot = s_slot[wid];
-  L.out = s_out[wid];
+  L.eit = s_eit[wid];
+  L.exp = s_exp[wid];
   for (uint32_t k = 0;; ++k) {
     const uint32_t s = k & 1, j = k >> 1;
     mbar_wait(&full[s], j & 1u);
