@@ -33,10 +33,15 @@
 namespace qgm {
 namespace {
 
-constexpr int kPartThreads = 512;
+#ifndef QGM_PART_THREADS
+#define QGM_PART_THREADS 256
+#endif
+constexpr int kPartThreads = QGM_PART_THREADS;
+constexpr int kPartMinBlocks = 1024 / kPartThreads;  // 64 registers per thread
 constexpr unsigned kBinBits = 8;
 constexpr uint32_t kBins = 1u << kBinBits;
-constexpr uint32_t kChunk = 4096;  // q-gram slots per chunk; staging = 32 KiB
+constexpr uint32_t kChunk = 8 * kPartThreads;  // q-gram slots per chunk; staging = 8 B each
+static_assert(kPartThreads >= int(kBins), "the P1 chunk scan gives every bin its own thread");
 constexpr uint32_t kPer = kChunk / kPartThreads;
 constexpr unsigned kP1CodeShift = 40, kP1MetaShift = 33;
 
@@ -136,7 +141,7 @@ __global__ void k_bin_offsets(const uint32_t* __restrict__ soff, uint32_t nbins,
   for (uint32_t b = threadIdx.x; b <= nbins; b += blockDim.x) boff[b] = soff[b << sub];
 }
 
-__global__ void __launch_bounds__(kPartThreads, 2) k_part_scatter(ItemGen gen, uint32_t n_items, unsigned shift,
+__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(ItemGen gen, uint32_t n_items, unsigned shift,
                                                                   const uint32_t* __restrict__ boff,
                                                                   uint32_t* __restrict__ cursor,
                                                                   uint64_t* __restrict__ out) {
@@ -244,7 +249,7 @@ __device__ __forceinline__ uint32_t bin_search(const uint32_t* sboff, uint32_t n
   return lo;
 }
 
-__global__ void __launch_bounds__(kPartThreads, 2) k_refine_scatter(const uint64_t* __restrict__ in, uint32_t n,
+__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter(const uint64_t* __restrict__ in, uint32_t n,
                                                                     const uint32_t* __restrict__ boff, Refine rf,
                                                                     unsigned sub, const uint32_t* __restrict__ off,
                                                                     uint32_t* __restrict__ cursor,
