@@ -553,20 +553,31 @@ void prepare_ref_index(Ctx& c, const Ref& ref, unsigned q) {
   index_from_buckets(c, B, false, ref.qidx.can, packed ? nullptr : &ref.qidx.extra);
   ref.qidx.packed = packed;
   ref.qidx.palindromes = n_pal;
-  const unsigned sub_bits = std::min(2 * q, 16u), cs = 2 * q - sub_bits;
-  ref.qidx.sub_bits = sub_bits;
-  if (cs >= 8) {  // >= 8 group words per sub-bin: whole 16-byte bulk copies of I and r16
-    const uint32_t n_sub = 1u << sub_bits;
-    ref.qidx.sb_d.alloc(c, n_sub + 1);
-    ref.qidx.sb_o.alloc(c, n_sub + 1);
-    QGM_KERNEL(c, k_subbin_bounds, unsigned(ceil_div(n_sub + 1, 256)), 256, 0, ref.qidx.can.S.p,
-               ref.qidx.can.S1.p, n_sub, cs, ref.qidx.sb_d.p, ref.qidx.sb_o.p);
-    const uint64_t groups = ref.qidx.can.groups;
-    ref.qidx.r16.alloc(c, groups);
-    QGM_KERNEL(c, k_rank16, unsigned(std::min<uint64_t>(ceil_div(groups, 256), kSMs * 16)), 256, 0,
-               ref.qidx.can.S.p, groups, cs - 5, ref.qidx.sb_d.p, ref.qidx.r16.p);
-  }
   ref.qidx.q = q;
+  subbin_tables(c, ref, std::min(2 * q, 16u));
+}
+
+void subbin_tables(Ctx& c, const Ref& ref, unsigned sub_bits) {
+  RefQIndex& X = ref.qidx;
+  if (X.sub_bits == sub_bits) return;
+  const unsigned q = X.q, cs = 2 * q - sub_bits;
+  X.sub_bits = sub_bits;
+  X.sb_d.release();
+  X.sb_o.release();
+  X.r16.release();
+  // >= 8 group words per sub-bin (whole 16-byte bulk copies of I and r16) and
+  // <= 2^16 codes (group starts inside a sub-bin fit 16 bits)
+  if (cs >= 8 && cs <= 16) {
+    const uint32_t n_sub = 1u << sub_bits;
+    X.sb_d.alloc(c, n_sub + 1);
+    X.sb_o.alloc(c, n_sub + 1);
+    QGM_KERNEL(c, k_subbin_bounds, unsigned(ceil_div(n_sub + 1, 256)), 256, 0, X.can.S.p, X.can.S1.p, n_sub, cs,
+               X.sb_d.p, X.sb_o.p);
+    const uint64_t groups = X.can.groups;
+    X.r16.alloc(c, groups);
+    QGM_KERNEL(c, k_rank16, unsigned(std::min<uint64_t>(ceil_div(groups, 256), kSMs * 16)), 256, 0, X.can.S.p,
+               groups, cs - 5, X.sb_d.p, X.r16.p);
+  }
 }
 
 void sample_index(Ctx& c, const Index& in, Index& out) {

@@ -199,7 +199,7 @@ struct RefQIndex {
   // min(2q, 16)): its distinct-code range [sb_d[s], sb_d[s+1]) of S' and
   // occurrence range [sb_o[s], sb_o[s+1]) of O; built when a sub-bin spans
   // >= 8 group words (the join stages these slices with bulk copies)
-  unsigned sub_bits = 0;
+  unsigned sub_bits = ~0u;
   DBuf<uint32_t> sb_d, sb_o;
   DBuf<uint16_t> r16;  // per group word: S[w] - sb_d[sub-bin of w] (group start inside its sub-bin)
 };
@@ -273,6 +273,9 @@ void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool packed, Buckets& out, u
 // position whose forward q-gram occurs more than `threshold` times among the
 // windows of its chromosome; drops the cached reference index.
 void mask_repeats(Ctx& c, Ref& ref, unsigned q, uint64_t threshold);
+// (Re)build the per-sub-bin tables of the cached reference index for sub-bins
+// of 2^sub_bits code prefixes (no-op when they already match).
+void subbin_tables(Ctx& c, const Ref& ref, unsigned sub_bits);
 void index_from_buckets(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_t>* extra);
 void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sampled, Index& out);
 void prepare_ref_index(Ctx& c, const Ref& ref, unsigned q);

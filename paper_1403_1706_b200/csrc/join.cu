@@ -535,6 +535,7 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   if (read_bits + 1 + ref.diag_bits > 64) throw InputError("read batch too large for the 64-bit candidate key");
   if (reads.max_len + 64 > ref.gap) throw InputError("reads longer than the reference padding supports");
   prepare_ref_index(c, ref, rp.q);
+  subbin_tables(c, ref, rp.sub_bits);
   const RefQIndex& X = ref.qidx;
   JoinArgs a;
   a.items = rp.pairs.p;

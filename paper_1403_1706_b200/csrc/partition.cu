@@ -345,7 +345,17 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   gen.n_items = n_items;
   const unsigned bits = std::min(2 * q, kBinBits);
   const unsigned shift = 2 * q - bits;
-  const unsigned key_bits = std::min(2 * q, 16u);
+  // sub-bins of ~256+ read q-grams: small batches get fewer, wider sub-bins
+  // (per-sub-bin staging and synchronisation are the join's fixed costs);
+  // at most 16 bits, at least the first pass's bits, and a sub-bin never
+  // spans more than 2^16 codes (u16 group starts) -- so q=16 always uses 16
+  unsigned key_bits = std::min(2 * q, 16u);
+  {
+    unsigned want = 8;
+    while (want < 16 && (uint64_t(n_items) >> (want + 1)) >= 256) ++want;
+    want = std::max(want, 2 * q > 16 ? 2 * q - 16 : 0u);
+    key_bits = std::min(key_bits, std::max(want, std::min(2 * q, kBinBits)));
+  }
   out.q = q;
   out.bins = 1u << bits;
   out.sub_bits = key_bits;
