@@ -206,17 +206,11 @@ void make_ref_planes(Ctx& c, Ref& ref) {
 // ------------------------------------------------------------------ pipeline
 static void finish_reads(Ctx& c, Reads& r) {
   make_read_planes(c, r);
-  DBuf<uint32_t> mx(c, 2);
-  mx.zero();
+  r.lens.alloc(c, 2);
+  r.lens.zero();
   if (r.n)
     QGM_KERNEL(c, k_minmax_u32, unsigned(std::min<uint64_t>(ceil_div(r.n, 256), kSMs * 4)), 256, 0, r.lengths.p,
-               uint64_t(r.n), mx.p);
-  uint32_t h[2] = {0, 0};
-  QGM_CUDA(cudaMemcpyAsync(h, mx.p, 8, cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaStreamSynchronize(c.stream));
-  r.max_len = h[0];
-  r.min_len = r.n ? ~h[1] : 0;
-  if (r.max_len > r.stride) throw InputError("read longer than the stride");
+               uint64_t(r.n), r.lens.p);
 }
 
 static void check_reads_shape(uint32_t n_reads, uint32_t stride) {
@@ -271,24 +265,28 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   }
   out.stats[6] = fst[0];
   out.stats[7] = fst[1];
+  // cnt[0]: validated hits, cnt[1]: unique candidates (read back together
+  // after validation: no host round trip between dedup and validation)
+  DBuf<unsigned long long> cnt(c, 2);
+  cnt.zero();
   {
     StageScope s(c, kStageSort);
-    n_u = dedup_keys(c, keys.p, n_raw, alt);  // unique candidates, any order (validation is per key)
+    dedup_keys_async(c, keys.p, n_raw, alt, cnt.p + 1);  // unique candidates, any order (validation is per key)
   }
   if (after_filter) after_filter();
-  DBuf<uint64_t> hkeys(c, std::max<uint64_t>(n_u, 1)), hkeys_alt;
-  DBuf<uint32_t> hvals(c, std::max<uint64_t>(n_u, 1)), hvals_alt;
+  const uint64_t n_bound = std::max<uint64_t>(n_raw, 1);
+  DBuf<uint64_t> hkeys(c, n_bound), hkeys_alt;
+  DBuf<uint32_t> hvals(c, n_bound), hvals_alt;
   uint64_t n_val = 0;
   {
     StageScope s(c, kStageValidate);
-    DBuf<unsigned long long> cnt(c, 1);
-    cnt.zero();
-    validate_candidates(c, reads, ref, alt.p, n_u, rb, P.band_width, P.pct_identity, 0, hkeys.p, hvals.p, cnt.p,
-                        nullptr);
-    unsigned long long h = 0;
-    QGM_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    validate_candidates(c, reads, ref, alt.p, n_raw, rb, P.band_width, P.pct_identity, 0, hkeys.p, hvals.p, cnt.p,
+                        nullptr, cnt.p + 1);
+    unsigned long long h[2] = {0, 0};
+    QGM_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     QGM_CUDA(cudaStreamSynchronize(c.stream));
-    n_val = h;
+    n_val = h[0];
+    n_u = h[1];
   }
   keys.release();
   alt.release();

@@ -67,7 +67,35 @@ __global__ void __launch_bounds__(kDedupThreads) k_tile_emit(const uint64_t* __r
   }
 }
 
+__global__ void k_store_count(const uint32_t* __restrict__ total, unsigned long long* __restrict__ out) {
+  *out = *total;
+}
+
 }  // namespace
+
+void dedup_keys_async(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out, unsigned long long* d_count) {
+  if (n == 0) {
+    QGM_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
+    if (out.n == 0) out.alloc(c, 1);
+    return;
+  }
+  uint64_t T = kTile;
+  while (T < n + n / 2) T <<= 1;  // load factor <= 2/3
+  DBuf<uint64_t> table(c, T);
+  QGM_CUDA(cudaMemsetAsync(table.p, 0xFF, T * sizeof(uint64_t), c.stream));
+  {
+    KernelScope ks(c, "k_hash_insert");
+    const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
+    QGM_KERNEL(c, k_hash_insert, grid, 256, 0, keys, n, table.p, T - 1);
+  }
+  const uint32_t tiles = uint32_t(T / kTile);
+  DBuf<uint32_t> counts(c, tiles + 1), total(c, 1);
+  QGM_KERNEL(c, k_tile_count, tiles, kDedupThreads, 0, table.p, T, counts.p);
+  exclusive_scan_u32(c, counts.p, counts.p, tiles, total.p, nullptr);
+  if (out.n < n) out.alloc(c, n);
+  QGM_KERNEL(c, k_tile_emit, tiles, kDedupThreads, 0, table.p, counts.p, out.p);
+  QGM_KERNEL(c, k_store_count, 1, 1, 0, total.p, d_count);
+}
 
 uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out) {
   if (n == 0) return 0;

@@ -213,7 +213,7 @@ uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Re
   if (idx.stride != reads.stride || idx.n_reads != reads.n)
     throw InputError("index was built over a different read buffer");
   if (read_bits + 1 + ref.diag_bits > 64) throw InputError("read batch too large for the 64-bit candidate key");
-  if (reads.max_len + 64 > ref.gap) throw InputError("reads longer than the reference padding supports");
+  if (uint64_t(reads.stride) + 64 > ref.gap) throw InputError("reads longer than the reference padding supports");
   FilterArgs a;
   a.ref = ref.words.p;
   a.mask = ref.mask.p;

@@ -533,6 +533,12 @@ void index_from_buckets(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf
 }
 
 void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sampled, Index& out) {
+  if (reads.lens.p) {  // the upload's length check (qgm_reads_upload does not synchronise)
+    uint32_t lens[2] = {0, 0};
+    QGM_CUDA(cudaMemcpyAsync(lens, reads.lens.p, 8, cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    if (lens[0] > reads.stride) throw InputError("read longer than the stride");
+  }
   Buckets B;
   bucket_reads(c, reads, q, w, B);
   index_from_buckets(c, B, sampled, out, nullptr);

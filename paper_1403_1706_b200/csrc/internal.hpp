@@ -147,7 +147,9 @@ struct DBuf {
 // per-read bit planes (lo/hi bit of every base, MSB-first, one guard word in
 // front) for the validation kernel.
 struct Reads {
-  uint32_t n = 0, stride = 0, W = 0, Wp = 0, max_len = 0, min_len = 0;
+  uint32_t n = 0, stride = 0, W = 0, Wp = 0;
+  DBuf<uint32_t> lens;     // device: {max length, ~min length} (no host round trip at upload;
+                           // the first synchronising stage checks max <= stride)
   DBuf<uint64_t> words;    // n * W
   DBuf<uint32_t> lengths;  // n
   DBuf<uint2> planes;      // n * Wp, word 0 of every read is a zero guard
@@ -255,6 +257,9 @@ uint64_t select_u64(Ctx& c, const uint64_t* keys, const uint32_t* vals, const ui
 // dedup.cu -- unique keys (any order) of keys[0, n) into `out` (grown as
 // needed); returns their count.
 uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out);
+// Same without a host round trip: `out` is sized n (the bound) and the unique
+// count lands in d_count (device).
+void dedup_keys_async(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out, unsigned long long* d_count);
 
 // radix_sort.cu -- stable LSD radix sort of u64 keys (+ optional u32 values)
 // on bits [begin_bit, end_bit). Sorted data ends up in keys/vals (buffers may
@@ -320,9 +325,12 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
 // validate.cu
 // mode 0: append kept hits as (hit key, k) to hit_keys/hit_vals (counter in
 //         *d_count); mode 1: write one qgm_validated per candidate.
+// d_n (nullable): the exact candidate count in device memory, n then only
+// bounds it (no host round trip between dedup and validation).
 void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint64_t* cand_keys, uint64_t n,
                          unsigned read_bits, unsigned band, unsigned pct, int mode, uint64_t* hit_keys,
-                         uint32_t* hit_vals, unsigned long long* d_count, void* d_validated);
+                         uint32_t* hit_vals, unsigned long long* d_count, void* d_validated,
+                         const unsigned long long* d_n = nullptr);
 
 // strata.cu -- dedup (read, chrom, ref_start, strand) keeping min k, then
 // best-stratum / all; writes qgm_hit records, returns their count.

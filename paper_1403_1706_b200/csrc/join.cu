@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
 uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Ref& ref, int strands, int mode,
                      unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats) {
   if (read_bits + 1 + ref.diag_bits > 64) throw InputError("read batch too large for the 64-bit candidate key");
-  if (reads.max_len + 64 > ref.gap) throw InputError("reads longer than the reference padding supports");
+  if (uint64_t(reads.stride) + 64 > ref.gap) throw InputError("reads longer than the reference padding supports");
   prepare_ref_index(c, ref, rp.q);
   subbin_tables(c, ref, rp.sub_bits);
   const RefQIndex& X = ref.qidx;

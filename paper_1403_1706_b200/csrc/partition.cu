@@ -223,7 +223,7 @@ struct Refine {
   uint32_t stride;
   FastDiv by_stride;
   unsigned q;
-  int uniform;
+  const uint32_t* lens;  // {max, ~min} read length (device)
   __device__ __forceinline__ uint32_t key(uint64_t it, uint32_t bin) const {
     return (bin << (shift - kshift)) | (uint32_t(it >> kP1CodeShift) >> kshift);
   }
@@ -231,7 +231,7 @@ struct Refine {
     const uint32_t pp = uint32_t(it);
     const uint32_t r = by_stride.div(pp), o = pp - r * stride;
     // every read of the batch has length `stride` (the usual case): no load
-    const uint32_t n = uniform ? stride : __ldg(lengths + r);
+    const uint32_t n = ~__ldg(lens + 1) == stride ? stride : __ldg(lengths + r);
     const uint32_t tail = min(n - q - o, kItemTailMax);
     const uint32_t lmask = kshift ? (1u << kshift) - 1u : 0u;
     return (uint64_t(uint32_t(it >> kP1CodeShift) & lmask) << kItemCodeShift) |
@@ -385,9 +385,11 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   DBuf<uint32_t> total(c, 1);
   exclusive_scan_u32(c, h2.p, out.soff.p, keys + 1, total.p, nullptr);
   QGM_KERNEL(c, k_bin_offsets, 1, 256, 0, out.soff.p, 1u << bits, sub, out.boff.p);
-  uint32_t V = 0;
+  uint32_t V = 0, lens[2] = {0, 0};
   QGM_CUDA(cudaMemcpyAsync(&V, total.p, 4, cudaMemcpyDeviceToHost, c.stream));
+  QGM_CUDA(cudaMemcpyAsync(lens, reads.lens.p, 8, cudaMemcpyDeviceToHost, c.stream));
   QGM_CUDA(cudaStreamSynchronize(c.stream));
+  if (lens[0] > reads.stride) throw InputError("read longer than the stride");
   if (V == 0) return empty();
   out.V = V;
   DBuf<uint32_t> hist(c, kBins + 1);  // per-bin cursors of P1
@@ -411,7 +413,7 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   rf.stride = reads.stride;
   rf.by_stride = FastDiv(std::max<uint32_t>(reads.stride, 1));
   rf.q = q;
-  rf.uniform = reads.min_len == reads.stride;
+  rf.lens = reads.lens.p;
   const unsigned grid2 = unsigned(std::min<uint64_t>(ceil_div(V, kChunk), uint64_t(kSMs) * 4));
   h2.zero();  // per-key cursors
   out.pairs.alloc(c, V + 2);  // +2: the join bulk-copies whole 16-byte pairs of items

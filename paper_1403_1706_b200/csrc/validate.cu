@@ -36,7 +36,8 @@ struct ValArgs {
   uint32_t n_chrom;
   uint64_t gap;
   const uint64_t* keys;
-  uint64_t n;
+  uint64_t n;                         // candidates (an upper bound when d_n is set)
+  const unsigned long long* d_n;      // nullable: the exact count, in device memory
   unsigned diag_bits;
   unsigned B;
   unsigned pct;
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_
                                                           unsigned long long* __restrict__ n_park) {
   const T mask = a.B >= sizeof(T) * 8 ? T(~T(0)) : T((T(1) << a.B) - 1);
   const uint64_t dmask = (uint64_t(1) << a.diag_bits) - 1;
-  const uint64_t total = kPhase == 2 ? *n_park : a.n;
+  const uint64_t total = kPhase == 2 ? *n_park : (a.d_n ? *a.d_n : a.n);
   for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < total; base += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t slot_i = base + threadIdx.x;
     bool kept = false, in_range = false, parked = false;
@@ -326,7 +327,8 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_
 
 void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint64_t* cand_keys, uint64_t n,
                          unsigned read_bits, unsigned band, unsigned pct, int mode, uint64_t* hit_keys,
-                         uint32_t* hit_vals, unsigned long long* d_count, void* d_validated) {
+                         uint32_t* hit_vals, unsigned long long* d_count, void* d_validated,
+                         const unsigned long long* d_n) {
   if (band == 0 || band > 64) throw InputError("band width must be in [1, 64]");
   if (pct > 100) throw InputError("percent identity must be in [0, 100]");
   if (read_bits + 1 + ref.diag_bits > 64) throw InputError("read batch too large for the 64-bit hit key");
@@ -342,6 +344,7 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
   a.gap = ref.gap;
   a.keys = cand_keys;
   a.n = n;
+  a.d_n = d_n;
   a.diag_bits = ref.diag_bits;
   a.B = band;
   a.pct = pct;
@@ -355,8 +358,8 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
   // map path: split after ~60% of the rows when at least one chunk remains
   // (a lower bound on the cost only becomes large enough to abandon a random
   // window past about half the read, profiles/r01/README.md)
-  const uint32_t chunks = (reads.max_len + 31) / 32;
-  const uint32_t c_split = uint32_t((reads.max_len * 0.6 + 16) / 32);
+  const uint32_t chunks = (reads.stride + 31) / 32;
+  const uint32_t c_split = uint32_t((reads.stride * 0.6 + 16) / 32);
   if (mode == 0 && c_split >= 1 && c_split < chunks) {
     DBuf<Parked> park(c, n);
     DBuf<unsigned long long> np(c, 1);

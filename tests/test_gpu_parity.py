@@ -262,3 +262,18 @@ def test_partition_counter_wrap_with_a_dominant_qgram(ctx, oracle):
     want, ost = oracle.map(ref, cb, codes, 100, lengths, q=16, mode=0)
     assert st["index_occurrences"] == lengths.size * 85
     assert _same(got, want), (got.size, want.size)
+
+
+def test_read_longer_than_stride_is_an_input_error(ctx):
+    """The upload does not synchronise; the first stage that does reports a
+    read longer than its stride as QGM_ERR_INPUT (seq.hpp's input_error)."""
+    import paper_1403_1706_b200 as qgm
+    ref = qgm.random_reference(71, 50_000)
+    cb = np.array([0, 50_000], np.uint64)
+    codes, lengths, *_ = qgm.simulate_reads(72, ref, cb, 100, 100, 0.0)
+    lengths = lengths.copy()
+    lengths[17] = 101
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    with pytest.raises(qgm.InputError):
+        ctx.map(reads, R, q=12, mode=0)
