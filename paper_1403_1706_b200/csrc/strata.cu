@@ -170,9 +170,16 @@ __global__ void k_seg_emit(const uint64_t* __restrict__ skeys, const uint32_t* _
 
 // big segments: flag[i] = 1 for hits of reads with big[r] != 0
 __global__ void k_big_flags(const uint64_t* __restrict__ skeys, uint64_t n, unsigned rshift,
-                            const uint32_t* __restrict__ big, uint32_t* __restrict__ flags) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-    flags[i] = big[skeys[i] >> rshift] != 0;
+                            const uint32_t* __restrict__ big, uint32_t* __restrict__ flags,
+                            uint32_t* __restrict__ n_big) {
+  uint32_t mine = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t f = big[skeys[i] >> rshift] != 0;
+    flags[i] = f;
+    mine += f;
+  }
+  mine = warp_reduce_sum(mine);
+  if (lane_id() == 0 && mine) atomicAdd(n_big, mine);
 }
 
 __global__ void k_big_writeback(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t nb,
@@ -215,14 +222,15 @@ uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBu
     // back into their segments, reduce them (one host round trip when there
     // are none: their hit count is read back together with the kept total)
     DBuf<uint32_t> flags(c, n), fpos(c, n), kept_off(c, uint64_t(n_reads) + 1);
-    QGM_KERNEL(c, k_big_flags, grid, 256, 0, skeys.p, n, rshift, big.p, flags.p);
-    exclusive_scan_u32(c, flags.p, fpos.p, n, total.p, nullptr);
+    total.zero();
+    QGM_KERNEL(c, k_big_flags, grid, 256, 0, skeys.p, n, rshift, big.p, flags.p, total.p);
     exclusive_scan_u32(c, kept.p, kept_off.p, uint64_t(n_reads) + 1, total.p + 1, nullptr);
     uint32_t h[2] = {0, 0};
     QGM_CUDA(cudaMemcpyAsync(h, total.p, 8, cudaMemcpyDeviceToHost, c.stream));
     QGM_CUDA(cudaStreamSynchronize(c.stream));
     const uint32_t nb = h[0];
     if (nb) {
+      exclusive_scan_u32(c, flags.p, fpos.p, n, nullptr, nullptr);
       DBuf<uint64_t> bk(c, nb), bk_alt;
       DBuf<uint32_t> bv(c, nb), bv_alt;
       select_u64(c, skeys.p, svals.p, flags.p, n, bk.p, bv.p);
