@@ -64,7 +64,9 @@ void* Ctx::block_alloc(size_t bytes, size_t& cls) {
     live_bytes += cls;
     return p;
   }
-  if (cached_bytes > (size_t(16) << 30)) block_trim();  // bound the cache when sizes drift
+  // no size cap: the cache is trimmed only when the pool is out of memory
+  // (a cap made repeat-heavy batches -- tens of GB of cached candidate
+  // buffers -- trim and synchronise on almost every allocation)
   void* p = nullptr;
   cudaError_t e = cudaMallocAsync(&p, cls, stream);
   if (e == cudaErrorMemoryAllocation && !free_blocks.empty()) {
@@ -265,9 +267,10 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   }
   out.stats[6] = fst[0];
   out.stats[7] = fst[1];
-  // cnt[0]: validated hits, cnt[1]: unique candidates (read back together
-  // after validation: no host round trip between dedup and validation)
-  DBuf<unsigned long long> cnt(c, 2);
+  // cnt[0]: validated hits, cnt[1]: unique candidates, cnt[2]: reads with
+  // more than 32 hits -- read back together after validation (no host round
+  // trip between dedup, validation and the strata's per-read counts)
+  DBuf<unsigned long long> cnt(c, 3);
   cnt.zero();
   {
     StageScope s(c, kStageSort);
@@ -282,17 +285,24 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
     StageScope s(c, kStageValidate);
     validate_candidates(c, reads, ref, alt.p, n_raw, rb, P.band_width, P.pct_identity, 0, hkeys.p, hvals.p, cnt.p,
                         nullptr, cnt.p + 1);
-    unsigned long long h[2] = {0, 0};
+  }
+  DBuf<uint32_t> per_read;
+  bool big = false;
+  {
+    StageScope s(c, kStageStrata);
+    strata_count(c, ref, hkeys.p, cnt.p, n_bound, reads.n, per_read, cnt.p + 2);
+    unsigned long long h[3] = {0, 0, 0};
     QGM_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     QGM_CUDA(cudaStreamSynchronize(c.stream));
     n_val = h[0];
     n_u = h[1];
+    big = h[2] != 0;
   }
   keys.release();
   alt.release();
   {
     StageScope s(c, kStageStrata);
-    out.n = stratify_unsorted(c, ref, hkeys, hvals, n_val, reads.n, int(P.mode), out.hits);
+    out.n = stratify_unsorted(c, ref, hkeys, hvals, n_val, reads.n, int(P.mode), per_read, big, out.hits);
   }
   out.stats[0] = n_raw;
   out.stats[1] = n_u;

@@ -235,7 +235,11 @@ uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Re
   DBuf<unsigned long long> counter(c, 3);  // {emitted, lookups hit, occurrences}
   a.counter = counter.p;
   a.stats = counter.p + 1;
-  if (keys.n == 0) keys.alloc(c, std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16));
+  // sized for the larger of 16 per read and the last batch's count on this
+  // context (+1/8), so a steady stream of similar batches never re-runs
+  if (keys.n == 0)
+    keys.alloc(c, std::max<uint64_t>(std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16),
+                                     c.last_raw_candidates + c.last_raw_candidates / 8));
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(ref.total, kFilterThreads * 4),
                                                                           uint64_t(kSMs) * 8)));
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -259,6 +263,7 @@ uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Re
       fstats[0] = h[1];
       fstats[1] = h[2];
     }
+    c.last_raw_candidates = h[0];
     if (h[0] <= keys.n) return h[0];
     keys.alloc(c, h[0] + h[0] / 8);  // exact size known now: one re-run
   }

@@ -25,6 +25,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t copy_stream = nullptr;  // H2D / D2H of qgm_map_host_batches (created on first use)
+  uint64_t last_raw_candidates = 0;    // sizes the next batch's candidate buffer
   std::string err;
   uint64_t launches = 0;
   bool profile = false;
@@ -334,9 +335,15 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
 
 // strata.cu -- dedup (read, chrom, ref_start, strand) keeping min k, then
 // best-stratum / all; writes qgm_hit records, returns their count.
-// Same output from hits in any order (per-read counting sort; map path).
+// Same output from hits in any order (map path): strata_count (hits per read,
+// *d_big += reads with more than 32 hits; d_n = device hit count, n_max its
+// bound) runs before the host reads the validation's counts back, then
+// stratify_unsorted uses a per-read counting sort, or -- when big -- the
+// radix-sorted path.
+void strata_count(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const unsigned long long* d_n, uint64_t n_max,
+                  uint32_t n_reads, DBuf<uint32_t>& cnt, unsigned long long* d_big);
 uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBuf<uint32_t>& hit_vals, uint64_t n,
-                           uint32_t n_reads, int mode, DBuf<uint8_t>& out);
+                           uint32_t n_reads, int mode, DBuf<uint32_t>& cnt, bool big, DBuf<uint8_t>& out);
 uint64_t stratify_hits(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const uint32_t* hit_vals, uint64_t n,
                        uint32_t n_reads, unsigned read_bits, int mode, DBuf<uint8_t>& out);
 

@@ -559,7 +559,11 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   DBuf<unsigned long long> counter(c, 3);
   a.counter = counter.p;
   a.stats = counter.p + 1;
-  if (keys.n == 0) keys.alloc(c, std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16));
+  // sized for the larger of 16 per read and the last batch's count on this
+  // context (+1/8), so a steady stream of similar batches never re-runs
+  if (keys.n == 0)
+    keys.alloc(c, std::max<uint64_t>(std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16),
+                                     c.last_raw_candidates + c.last_raw_candidates / 8));
   const bool rs = mode == 1;
   // Kernel choice (measured, profiles/r01/README.md): the warp-specialised
   // pipeline wins when sub-bins are staged and hold a few hundred to a couple
@@ -629,6 +633,7 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
       fstats[0] = h[1];
       fstats[1] = h[2];
     }
+    c.last_raw_candidates = h[0];
     if (h[0] <= keys.n) return h[0];
     keys.alloc(c, h[0] + h[0] / 8);
   }

@@ -9,9 +9,9 @@
 // sort by read (count, scan, scatter) gives every read its segment (~1.3 hits
 // at C2); one thread per read sorts its segment in registers/local memory,
 // dedups, finds the read's minimum and counts the kept groups; a scan of the
-// kept counts places the records. Reads with more than kSmallSeg hits
-// (repeats) are sorted by the LSD radix sort on the subset of their hits,
-// written back into their (contiguous, read-ordered) segments.
+// kept counts places the records. A batch with a read of more than kSmallSeg
+// hits (repeats; a thread would walk its segment serially) is instead radix-
+// sorted as a whole and reduced by the sorted-input kernels below.
 //
 // Sorted-input path (stratify_hits, hits radix-sorted by the caller):
 //   K1: first hit of every group keeps the group's minimum k and folds it
@@ -21,6 +21,8 @@
 #include "internal.hpp"
 
 namespace qgm {
+uint64_t stratify_hits(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const uint32_t* hit_vals, uint64_t n,
+                       uint32_t n_reads, unsigned read_bits, int mode, DBuf<uint8_t>& out);
 namespace {
 
 __global__ void k_group_min(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t n,
@@ -68,10 +70,14 @@ __global__ void k_emit(const uint64_t* __restrict__ keys, uint64_t n, unsigned d
 // ------------------------------------------------------------ segmented path
 constexpr uint32_t kSmallSeg = 32;
 
-__global__ void k_count_reads(const uint64_t* __restrict__ keys, uint64_t n, unsigned rshift,
-                              uint32_t* __restrict__ cnt) {
+// hits per read; n_big (device) counts the reads that pass kSmallSeg hits.
+// n (nullable) = the hit count in device memory, n_max bounds it.
+__global__ void k_count_reads(const uint64_t* __restrict__ keys, const unsigned long long* __restrict__ n_dev,
+                              uint64_t n_max, unsigned rshift, uint32_t* __restrict__ cnt,
+                              unsigned long long* __restrict__ n_big) {
+  const uint64_t n = n_dev ? *n_dev : n_max;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-    atomicAdd(cnt + (keys[i] >> rshift), 1u);
+    if (atomicAdd(cnt + (keys[i] >> rshift), 1u) == kSmallSeg) atomicAdd(n_big, 1ull);
 }
 
 // cnt[r] counts down while hits are placed (segment filled from its end)
@@ -89,36 +95,27 @@ __global__ void k_scatter_reads(const uint64_t* __restrict__ keys, const uint32_
 
 // per read: sort the segment (small ones here, big ones by the caller),
 // group minima, the read's minimum, keep marks (value ~0u = dropped), kept count
+// per read (every segment <= kSmallSeg hits): sort the segment, group
+// minima, the read's minimum, keep marks (value ~0u = dropped), kept count
 __global__ void k_seg_reduce(uint64_t* __restrict__ skeys, uint32_t* __restrict__ svals,
-                             const uint32_t* __restrict__ off, uint32_t n_reads, int mode, int sorted_big,
-                             uint32_t* __restrict__ kept, uint32_t* __restrict__ big) {
+                             const uint32_t* __restrict__ off, uint32_t n_reads, int mode,
+                             uint32_t* __restrict__ kept) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_reads; r += gridDim.x * blockDim.x) {
     const uint32_t b = off[r], m = off[r + 1] - b;
     uint32_t nk = 0;
-    if (sorted_big) {  // second launch: only the big segments, now sorted
-      if (!big[r]) continue;
-    } else if (m > kSmallSeg) {
-      big[r] = m;  // sorted by the caller, then reduced in a second launch
-      kept[r] = 0;
-      continue;
-    } else {
-      big[r] = 0;
-    }
     uint64_t* K = skeys + b;
     uint32_t* V = svals + b;
-    if (m <= kSmallSeg) {  // insertion sort by key
-      for (uint32_t i = 1; i < m; ++i) {
-        const uint64_t x = K[i];
-        const uint32_t v = V[i];
-        uint32_t j = i;
-        while (j > 0 && K[j - 1] > x) {
-          K[j] = K[j - 1];
-          V[j] = V[j - 1];
-          --j;
-        }
-        K[j] = x;
-        V[j] = v;
+    for (uint32_t i = 1; i < m; ++i) {  // insertion sort by key
+      const uint64_t x = K[i];
+      const uint32_t v = V[i];
+      uint32_t j = i;
+      while (j > 0 && K[j - 1] > x) {
+        K[j] = K[j - 1];
+        V[j] = V[j - 1];
+        --j;
       }
+      K[j] = x;
+      V[j] = v;
     }
     // group minima in place (first of a group holds it; later members get
     // value ~0u), then the read minimum
@@ -168,85 +165,52 @@ __global__ void k_seg_emit(const uint64_t* __restrict__ skeys, const uint32_t* _
   }
 }
 
-// big segments: flag[i] = 1 for hits of reads with big[r] != 0
-__global__ void k_big_flags(const uint64_t* __restrict__ skeys, uint64_t n, unsigned rshift,
-                            const uint32_t* __restrict__ big, uint32_t* __restrict__ flags,
-                            uint32_t* __restrict__ n_big) {
-  uint32_t mine = 0;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t f = big[skeys[i] >> rshift] != 0;
-    flags[i] = f;
-    mine += f;
-  }
-  mine = warp_reduce_sum(mine);
-  if (lane_id() == 0 && mine) atomicAdd(n_big, mine);
-}
-
-__global__ void k_big_writeback(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t nb,
-                                const uint32_t* __restrict__ flags_pos, const uint32_t* __restrict__ flags,
-                                uint64_t n, uint64_t* __restrict__ skeys, uint32_t* __restrict__ svals) {
-  // the i-th flagged slot of the segment arrays receives the i-th sorted key
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-    if (flags[i]) {
-      const uint32_t j = flags_pos[i];
-      skeys[i] = keys[j];
-      svals[i] = vals[j];
-    }
-}
-
 }  // namespace
 
+void strata_count(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const unsigned long long* d_n, uint64_t n_max,
+                  uint32_t n_reads, DBuf<uint32_t>& cnt, unsigned long long* d_big) {
+  cnt.alloc(c, uint64_t(n_reads) + 1);
+  cnt.zero();
+  if (n_max == 0 || n_reads == 0) return;
+  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n_max, 256), uint64_t(kSMs) * 16));
+  QGM_KERNEL(c, k_count_reads, grid, 256, 0, hit_keys, d_n, n_max, ref.diag_bits + 1, cnt.p, d_big);
+}
+
 uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBuf<uint32_t>& hit_vals, uint64_t n,
-                           uint32_t n_reads, int mode, DBuf<uint8_t>& out) {
+                           uint32_t n_reads, int mode, DBuf<uint32_t>& cnt, bool big, DBuf<uint8_t>& out) {
   if (n == 0 || n_reads == 0) {
     out.alloc(c, 16);
     return 0;
   }
   if (n > 0xFFFFFFFFull) throw InputError("strata: more than 2^32-1 hits");
   const unsigned rshift = ref.diag_bits + 1;
+  KernelScope ks(c, "k_strata_seg");
+  if (big) {
+    // a read with more than kSmallSeg hits (repeats): a thread would walk its
+    // segment serially -- sort every hit and use the sorted-input kernels
+    DBuf<uint64_t> k_alt;
+    DBuf<uint32_t> v_alt;
+    radix_sort(c, hit_keys, k_alt, &hit_vals, &v_alt, n, 0, int(rshift + bit_width_u64(n_reads)));
+    return stratify_hits(c, ref, hit_keys.p, hit_vals.p, n, n_reads, 0, mode, out);
+  }
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
   const unsigned rgrid = unsigned(std::min<uint64_t>(ceil_div(n_reads, 128), uint64_t(kSMs) * 16));
-  DBuf<uint32_t> cnt(c, uint64_t(n_reads) + 1), off(c, uint64_t(n_reads) + 1), kept(c, uint64_t(n_reads) + 1),
-      big(c, n_reads), total(c, 2);
-  cnt.zero();
+  DBuf<uint32_t> off(c, uint64_t(n_reads) + 1), kept(c, uint64_t(n_reads) + 1), total(c, 1);
   kept.zero();
-  {
-    KernelScope ks(c, "k_strata_seg");
-    QGM_KERNEL(c, k_count_reads, grid, 256, 0, hit_keys.p, n, rshift, cnt.p);
-    exclusive_scan_u32(c, cnt.p, off.p, uint64_t(n_reads) + 1, nullptr, nullptr);
-    DBuf<uint64_t> skeys(c, n);
-    DBuf<uint32_t> svals(c, n);
-    QGM_KERNEL(c, k_scatter_reads, grid, 256, 0, hit_keys.p, hit_vals.p, n, rshift, off.p, cnt.p, skeys.p, svals.p);
-    QGM_KERNEL(c, k_seg_reduce, rgrid, 128, 0, skeys.p, svals.p, off.p, n_reads, mode, 0, kept.p, big.p);
-    // reads with more than kSmallSeg hits: radix-sort their hits, write them
-    // back into their segments, reduce them (one host round trip when there
-    // are none: their hit count is read back together with the kept total)
-    DBuf<uint32_t> flags(c, n), fpos(c, n), kept_off(c, uint64_t(n_reads) + 1);
-    total.zero();
-    QGM_KERNEL(c, k_big_flags, grid, 256, 0, skeys.p, n, rshift, big.p, flags.p, total.p);
-    exclusive_scan_u32(c, kept.p, kept_off.p, uint64_t(n_reads) + 1, total.p + 1, nullptr);
-    uint32_t h[2] = {0, 0};
-    QGM_CUDA(cudaMemcpyAsync(h, total.p, 8, cudaMemcpyDeviceToHost, c.stream));
-    QGM_CUDA(cudaStreamSynchronize(c.stream));
-    const uint32_t nb = h[0];
-    if (nb) {
-      exclusive_scan_u32(c, flags.p, fpos.p, n, nullptr, nullptr);
-      DBuf<uint64_t> bk(c, nb), bk_alt;
-      DBuf<uint32_t> bv(c, nb), bv_alt;
-      select_u64(c, skeys.p, svals.p, flags.p, n, bk.p, bv.p);
-      radix_sort(c, bk, bk_alt, &bv, &bv_alt, nb, 0, int(rshift + bit_width_u64(n_reads)));
-      QGM_KERNEL(c, k_big_writeback, grid, 256, 0, bk.p, bv.p, nb, fpos.p, flags.p, n, skeys.p, svals.p);
-      QGM_KERNEL(c, k_seg_reduce, rgrid, 128, 0, skeys.p, svals.p, off.p, n_reads, mode, 1, kept.p, big.p);
-      exclusive_scan_u32(c, kept.p, kept_off.p, uint64_t(n_reads) + 1, total.p + 1, nullptr);
-      QGM_CUDA(cudaMemcpyAsync(h + 1, total.p + 1, 4, cudaMemcpyDeviceToHost, c.stream));
-      QGM_CUDA(cudaStreamSynchronize(c.stream));
-    }
-    const uint32_t nk = h[1];
-    out.alloc(c, std::max<uint64_t>(uint64_t(nk) * 16, 16));
-    QGM_KERNEL(c, k_seg_emit, rgrid, 128, 0, skeys.p, svals.p, off.p, kept_off.p, n_reads, ref.diag_bits, ref.d_cbp.p,
-               ref.n_chrom, reinterpret_cast<uint4*>(out.p));
-    return nk;
-  }
+  exclusive_scan_u32(c, cnt.p, off.p, uint64_t(n_reads) + 1, nullptr, nullptr);
+  DBuf<uint64_t> skeys(c, n);
+  DBuf<uint32_t> svals(c, n);
+  QGM_KERNEL(c, k_scatter_reads, grid, 256, 0, hit_keys.p, hit_vals.p, n, rshift, off.p, cnt.p, skeys.p, svals.p);
+  QGM_KERNEL(c, k_seg_reduce, rgrid, 128, 0, skeys.p, svals.p, off.p, n_reads, mode, kept.p);
+  DBuf<uint32_t> kept_off(c, uint64_t(n_reads) + 1);
+  exclusive_scan_u32(c, kept.p, kept_off.p, uint64_t(n_reads) + 1, total.p, nullptr);
+  uint32_t nk = 0;
+  QGM_CUDA(cudaMemcpyAsync(&nk, total.p, 4, cudaMemcpyDeviceToHost, c.stream));
+  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  out.alloc(c, std::max<uint64_t>(uint64_t(nk) * 16, 16));
+  QGM_KERNEL(c, k_seg_emit, rgrid, 128, 0, skeys.p, svals.p, off.p, kept_off.p, n_reads, ref.diag_bits, ref.d_cbp.p,
+             ref.n_chrom, reinterpret_cast<uint4*>(out.p));
+  return nk;
 }
 
 uint64_t stratify_hits(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const uint32_t* hit_vals, uint64_t n,

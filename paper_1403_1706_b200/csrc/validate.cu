@@ -16,6 +16,8 @@
 //   Z   = carry chain of zero steps along t through Pv (Myers' addition trick)
 //   new Pv/Mv from the diagonal deltas D1 = ~Z and D1<<1; score of t=0 += D1&1
 // ~20 integer ops per row (VALIDATE_OPS_PER_ROW in DESIGN.md).
+#include <cstdlib>
+
 #include "internal.hpp"
 
 namespace qgm {
@@ -224,13 +226,13 @@ __device__ __forceinline__ void unpack_state(const Parked& p, T& Pv, T& Mv) {
 // survivors parked; 2: resume the parked candidates from chunk c_split.
 template <class T, int kPhase>
 __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_split, Parked* __restrict__ park,
-                                                          unsigned long long* __restrict__ n_park) {
+                                                          unsigned long long* __restrict__ n_park, uint64_t park_cap) {
   const T mask = a.B >= sizeof(T) * 8 ? T(~T(0)) : T((T(1) << a.B) - 1);
   const uint64_t dmask = (uint64_t(1) << a.diag_bits) - 1;
-  const uint64_t total = kPhase == 2 ? *n_park : (a.d_n ? *a.d_n : a.n);
+  const uint64_t total = kPhase == 2 ? min(uint64_t(*n_park), park_cap) : (a.d_n ? *a.d_n : a.n);
   for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < total; base += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t slot_i = base + threadIdx.x;
-    bool kept = false, in_range = false, parked = false;
+    bool kept = false, in_range = false, parked = false, finish = false;
     int k = 0;
     uint32_t start = 0, ref_start = 0, r = 0, c = 0;
     bool rev = false;
@@ -240,6 +242,21 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_
       pk = park[slot_i];
       i = pk.i;
     }
+    // candidate geometry (set when in range)
+    T Pv = 0, Mv = 0;
+    int score0 = 0, st = kAbandoned, kmax = -1;
+    uint32_t n = 0, L = 0;
+    int64_t cbeg = 0, cend = 0, Lc = 0, w0 = 0, F = 0;
+    bool interior = false;
+    auto run = [&](uint32_t cb0, uint32_t cb1) {
+      const bool full = a.B == sizeof(T) * 8;
+      if (interior && full)
+        st = myers_rows<T, false, true>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax, cb0, cb1);
+      else if (interior)
+        st = myers_rows<T, false, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax, cb0, cb1);
+      else
+        st = myers_rows<T, true, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax, cb0, cb1);
+    };
     if (slot_i < total) {
       const uint64_t key = a.keys[i];
       r = uint32_t(key >> (a.diag_bits + 1));
@@ -252,57 +269,55 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_
       }
       c = lo;
       const int64_t d = int64_t(gp) - int64_t(__ldg(a.cbp + c));
-      const int64_t cbeg = int64_t(__ldg(a.cb + c)), cend = int64_t(__ldg(a.cb + c + 1));
-      const int64_t Lc = cend - cbeg;
-      const uint32_t n = __ldg(a.rlen + r);
-      const uint32_t L = n + a.B - 1;
+      cbeg = int64_t(__ldg(a.cb + c));
+      cend = int64_t(__ldg(a.cb + c + 1));
+      Lc = cend - cbeg;
+      n = __ldg(a.rlen + r);
+      L = n + a.B - 1;
       const int64_t H = (int64_t(a.B) - 1) / 2;
-      const int64_t w0 = d - H;
+      w0 = d - H;
       if (n > 0 && w0 + int64_t(L) > 0 && w0 < Lc) {
         in_range = true;
-        T Pv = 0, Mv = 0;
-        int score0 = 0;
         if (kPhase == 2) {
           unpack_state<T>(pk, Pv, Mv);
           score0 = int(pk.score0);
         }
-        const int64_t F = cbeg + w0;
+        F = cbeg + w0;
         // map path: abandon candidates that can no longer reach the threshold
-        const int kmax = a.mode == 0 ? int((uint64_t(100 - a.pct) * n) / 100) : -1;
-        const bool interior = w0 >= 0 && w0 + int64_t(L) <= Lc;
-        const bool full = a.B == sizeof(T) * 8;
-        const uint32_t cb0 = kPhase == 2 ? c_split : 0u, cb1 = kPhase == 1 ? c_split : 0xFFFFFFFFu;
-        int st;
-        if (interior && full)
-          st = myers_rows<T, false, true>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax, cb0, cb1);
-        else if (interior)
-          st = myers_rows<T, false, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax, cb0, cb1);
-        else
-          st = myers_rows<T, true, false>(a, r, rev, n, F, L, cbeg, cend, mask, Pv, Mv, score0, kmax, cb0, cb1);
-        if (kPhase == 1 && st == kPaused) {
-          parked = true;
-          pk.i = uint32_t(i);
-          pk.score0 = uint32_t(score0);
-          pack_state<T>(pk, Pv, Mv);
-        } else {
-          int v = score0, best = score0;
-          unsigned tbest = 0;
-          for (unsigned t = 1; t < a.B; ++t) {
-            v += int((Pv >> t) & T(1)) - int((Mv >> t) & T(1));
-            if (v <= best) { best = v; tbest = t; }
-          }
-          k = best;
-          start = a.B - 1 - tbest;
-          int64_t rs = w0 + int64_t(start);
-          rs = rs < 0 ? 0 : (rs > Lc - 1 ? Lc - 1 : rs);
-          ref_start = uint32_t(rs);
-          kept = st == kDone && k <= int(n) && uint64_t(100) * uint64_t(int64_t(n) - k) >= uint64_t(a.pct) * n;
-        }
+        kmax = a.mode == 0 ? int((uint64_t(100 - a.pct) * n) / 100) : -1;
+        interior = w0 >= 0 && w0 + int64_t(L) <= Lc;
+        run(kPhase == 2 ? c_split : 0u, kPhase == 1 ? c_split : 0xFFFFFFFFu);
+        parked = kPhase == 1 && st == kPaused;
+        finish = !parked;
       }
     }
     if (kPhase == 1) {
       const unsigned long long ps = warp_append(parked, n_park);
-      if (parked) park[ps] = pk;
+      if (parked) {
+        if (ps < park_cap) {
+          pk.i = uint32_t(i);
+          pk.score0 = uint32_t(score0);
+          pack_state<T>(pk, Pv, Mv);
+          park[ps] = pk;
+        } else {  // no room left: finish here
+          run(c_split, 0xFFFFFFFFu);
+          finish = true;
+        }
+      }
+    }
+    if (finish) {
+      int v = score0, best = score0;
+      unsigned tbest = 0;
+      for (unsigned t = 1; t < a.B; ++t) {
+        v += int((Pv >> t) & T(1)) - int((Mv >> t) & T(1));
+        if (v <= best) { best = v; tbest = t; }
+      }
+      k = best;
+      start = a.B - 1 - tbest;
+      int64_t rs = w0 + int64_t(start);
+      rs = rs < 0 ? 0 : (rs > Lc - 1 ? Lc - 1 : rs);
+      ref_start = uint32_t(rs);
+      kept = st == kDone && k <= int(n) && uint64_t(100) * uint64_t(int64_t(n) - k) >= uint64_t(a.pct) * n;
     }
     if (a.mode == 0) {
       const bool emit = slot_i < total && in_range && kept;
@@ -361,20 +376,25 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
   const uint32_t chunks = (reads.stride + 31) / 32;
   const uint32_t c_split = uint32_t((reads.stride * 0.6 + 16) / 32);
   if (mode == 0 && c_split >= 1 && c_split < chunks) {
-    DBuf<Parked> park(c, n);
+    // survivors parked for phase 2, at most 16M (candidates beyond finish in
+    // phase 1)
+    uint64_t cap = std::min<uint64_t>(n, uint64_t(1) << 24);
+    if (const char* e = std::getenv("QGM_VAL_PARK_CAP")) cap = std::min<uint64_t>(cap, std::strtoull(e, nullptr, 10));  // test knob
+    cap = std::max<uint64_t>(cap, 1);
+    DBuf<Parked> park(c, cap);
     DBuf<unsigned long long> np(c, 1);
     np.zero();
     if (band <= 32) {
-      QGM_KERNEL(c, (k_validate<uint32_t, 1>), grid, kValThreads, 0, a, c_split, park.p, np.p);
-      QGM_KERNEL(c, (k_validate<uint32_t, 2>), grid, kValThreads, 0, a, c_split, park.p, np.p);
+      QGM_KERNEL(c, (k_validate<uint32_t, 1>), grid, kValThreads, 0, a, c_split, park.p, np.p, cap);
+      QGM_KERNEL(c, (k_validate<uint32_t, 2>), grid, kValThreads, 0, a, c_split, park.p, np.p, cap);
     } else {
-      QGM_KERNEL(c, (k_validate<uint64_t, 1>), grid, kValThreads, 0, a, c_split, park.p, np.p);
-      QGM_KERNEL(c, (k_validate<uint64_t, 2>), grid, kValThreads, 0, a, c_split, park.p, np.p);
+      QGM_KERNEL(c, (k_validate<uint64_t, 1>), grid, kValThreads, 0, a, c_split, park.p, np.p, cap);
+      QGM_KERNEL(c, (k_validate<uint64_t, 2>), grid, kValThreads, 0, a, c_split, park.p, np.p, cap);
     }
     return;
   }
-  if (band <= 32) QGM_KERNEL(c, (k_validate<uint32_t, 0>), grid, kValThreads, 0, a, 0u, nullptr, nullptr);
-  else QGM_KERNEL(c, (k_validate<uint64_t, 0>), grid, kValThreads, 0, a, 0u, nullptr, nullptr);
+  if (band <= 32) QGM_KERNEL(c, (k_validate<uint32_t, 0>), grid, kValThreads, 0, a, 0u, nullptr, nullptr, uint64_t(0));
+  else QGM_KERNEL(c, (k_validate<uint64_t, 0>), grid, kValThreads, 0, a, 0u, nullptr, nullptr, uint64_t(0));
 }
 
 }  // namespace qgm

@@ -277,3 +277,17 @@ def test_read_longer_than_stride_is_an_input_error(ctx):
     reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
     with pytest.raises(qgm.InputError):
         ctx.map(reads, R, q=12, mode=0)
+
+
+def test_validation_park_overflow_finishes_in_phase_one(ctx, oracle, monkeypatch):
+    """More phase-1 survivors than the parking capacity (forced to 500): the
+    extra candidates are finished in phase 1; hits identical to the oracle."""
+    import paper_1403_1706_b200 as qgm
+    monkeypatch.setenv("QGM_VAL_PARK_CAP", "500")
+    ref, cb, codes, lengths, tp, ts = _c1(qgm, n_reads=5000, L=500_000)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    got, st = ctx.map(reads, R, q=12, mode=1)
+    want, ost = oracle.map(ref, cb, codes, 100, lengths, q=12, mode=1)
+    assert st["validated"] == ost["validated"]
+    assert _same(got, want), (got.size, want.size)
