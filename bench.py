@@ -186,6 +186,28 @@ def algorithmic_bytes(kernel, cfg, st, ref_bp, n_reads):
     return None
 
 
+def bind_to_gpu_numa(local):
+    """Run this rank on the host cores NVML reports as local to its GPU, so the
+    pinned read/hit buffers live on the GPU's NUMA node (PCIe copies do not
+    cross sockets). Returns the core count, or None when NVML is unavailable."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        idx = int(vis.split(",")[local]) if vis and vis.split(",")[0].isdigit() else local
+        h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+        n_words = (os.cpu_count() + 63) // 64
+        mask = pynvml.nvmlDeviceGetCpuAffinity(h, n_words)
+        cpus = {64 * w + b for w, m in enumerate(mask) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception:
+        return None
+    return None
+
+
 def run_gpu(args):
     import torch
     import paper_1403_1706_b200 as qgm
@@ -193,6 +215,7 @@ def run_gpu(args):
     from paper_1403_1706_b200 import sharding
 
     rank, world, local = sharding.world()
+    numa_cores = bind_to_gpu_numa(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -296,11 +319,17 @@ def run_gpu(args):
     barrier()
     e2e1_ms = sum(e2e1_times)
 
+    # the streamed API takes the reads as one dense 2-bit stream (2 bits per
+    # base, no per-read padding) and, all reads being `rlen` long, no length
+    # array: 25 MB per 1M x 100 bp batch
+    uniform = bool(np.all(lengths == rlen))
+    h_dense = torch.from_numpy(qgm.pack_codes(codes).view(np.int64)).pin_memory()
+
     def run_batches(K):
         arr = (qgm.Batch * K)()
         for i in range(K):
-            arr[i] = qgm.Batch(h_words.data_ptr(), h_len.data_ptr(), n_reads, rlen, h_hits.data_ptr(), cap, 0,
-                               qgm.MapStats())
+            arr[i] = qgm.Batch(h_dense.data_ptr(), None if uniform else h_len.data_ptr(), n_reads, rlen,
+                               h_hits.data_ptr(), cap, 0, qgm.MapStats(), qgm.READS_DENSE, 0)
         ctx._check(lib.qgm_map_host_batches(ctx.h, arr, K, R.h, C.byref(params)))
         return arr[K - 1].n_out
 
@@ -367,10 +396,12 @@ def run_gpu(args):
                    "pct_identity": pct, "parallelism": f"read-sharded x{world} (reference replicated)",
                    "l2": "flushed between steps (512 MiB device write outside the step events)"},
         "e2e": {"value": round(e2e_value, 1), "unit": "reads/s", "ms_per_step": round(e2e_ms / args.steps, 3),
-                "h2d_bytes_per_step": int(words.nbytes + lengths.nbytes), "d2h_bytes_per_step": int(n_hits * 16),
-                "api": "qgm_map_host_batches (streamed; copies overlap mapping)"},
+                "h2d_bytes_per_step": int((n_reads * rlen + 31) // 32 * 8 + (0 if uniform else lengths.nbytes)),
+                "d2h_bytes_per_step": int(n_hits * 16),
+                "api": "qgm_map_host_batches (streamed; copies overlap mapping; dense 2-bit reads)"},
         "e2e_unpipelined": {"value": round(e2e1_value, 1), "unit": "reads/s", "ms_per_step": round(e2e1_ms / args.steps, 3),
-                            "api": "qgm_map_host, one call per batch"},
+                            "api": "qgm_map_host, one call per batch",
+                            "h2d_bytes_per_step": int(words.nbytes + lengths.nbytes)},
         "gpu_launches": int(launches),
         "roofline": roof,
         "stage_roofline": stage_roof,
@@ -381,8 +412,10 @@ def run_gpu(args):
         "kernels_ms_per_launch": {k: round(v, 4) for k, v in per_launch.items()},
         "counts": st,
         "reference_prepare_s": round(ref_prepare_s, 3),
+        "host_binding": {"cores": numa_cores, "rule": "NVML CPU affinity of the rank's GPU"},
     }
     if rank == 0 and world == 1 and not args.no_cpu:
+        os.sched_setaffinity(0, set(range(os.cpu_count())))  # the CPU baseline gets every host core
         line["cpu_baseline"] = cpu_baseline(args, cfg, ref, cb, codes, lengths, samples=1)
     if rank == 0:
         print(json.dumps(line), flush=True)

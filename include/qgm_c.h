@@ -228,15 +228,19 @@ int qgm_map_host(qgm_ctx* ctx, const uint64_t* reads2bit, const uint32_t* length
 /* One read buffer of a streamed run (run_map's bounded-queue pipeline,
  * SPEC.md:521-528 / PAPER.md:238-262). Host buffers; pinned memory lets the
  * copies overlap the mapping. */
+#define QGM_READS_PADDED 0u /* qgm_pack_reads: ceil(stride/32) words per read */
+#define QGM_READS_DENSE 1u  /* one 2-bit stream, read r = bases [r*stride, (r+1)*stride) (qgm_pack_codes) */
 typedef struct qgm_batch {
-  const uint64_t* reads2bit; /* qgm_pack_reads layout */
-  const uint32_t* lengths;
+  const uint64_t* reads2bit; /* layout below */
+  const uint32_t* lengths;   /* NULL: every read has length `stride` */
   uint32_t n_reads;
   uint32_t stride;
   qgm_hit* out;              /* capacity `cap` records */
   uint64_t cap;
   uint64_t n_out;            /* out: hit count (the required capacity when it exceeds cap) */
   qgm_map_stats stats;       /* out */
+  uint32_t layout;           /* QGM_READS_PADDED or QGM_READS_DENSE */
+  uint32_t reserved;
 } qgm_batch;
 /* Maps the batches in order, same results as qgm_map_host per batch: the
  * reads of batch i+1 are uploaded on a second stream while batch i is

@@ -86,7 +86,11 @@ class MapStats(C.Structure):
 class Batch(C.Structure):
     """qgm_batch (include/qgm_c.h): one read buffer of qgm_map_host_batches."""
     _fields_ = [("reads2bit", C.c_void_p), ("lengths", C.c_void_p), ("n_reads", C.c_uint32), ("stride", C.c_uint32),
-                ("out", C.c_void_p), ("cap", C.c_uint64), ("n_out", C.c_uint64), ("stats", MapStats)]
+                ("out", C.c_void_p), ("cap", C.c_uint64), ("n_out", C.c_uint64), ("stats", MapStats),
+                ("layout", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+READS_PADDED, READS_DENSE = 0, 1
 
 
 # Every symbol include/qgm_c.h declares (checked by tests/test_capi_symbols.py).
@@ -354,16 +358,22 @@ class Context:
 
     def map_host_batches(self, batches, ref, params=None, **kw):
         """Streamed e2e entry (qgm_map_host_batches): `batches` is a list of
-        (words, lengths, stride) host arrays; returns [(hits, stats), ...].
+        (words, lengths, stride[, layout, n_reads]) host arrays -- layout
+        READS_DENSE takes a qgm_pack_codes stream, lengths None means every
+        read has length `stride`; returns [(hits, stats), ...].
         Pinned host arrays let the copies overlap the mapping."""
         p = params or make_params(**kw)
         arr = (Batch * len(batches))()
         keep = []
-        for i, (words, lengths, stride) in enumerate(batches):
-            lengths = np.ascontiguousarray(lengths, dtype=np.uint32)
-            out = np.zeros(max(64, lengths.size * 4), dtype=HIT_DTYPE)
+        for i, bt in enumerate(batches):
+            words, lengths, stride = bt[:3]
+            layout = bt[3] if len(bt) > 3 else READS_PADDED
+            n_reads = bt[4] if len(bt) > 4 else np.asarray(lengths).size
+            lengths = None if lengths is None else np.ascontiguousarray(lengths, dtype=np.uint32)
+            out = np.zeros(max(64, n_reads * 4), dtype=HIT_DTYPE)
             keep.append((words, lengths, out))
-            arr[i] = Batch(_ptr(words), _ptr(lengths), lengths.size, stride, _ptr(out), out.size, 0, MapStats())
+            arr[i] = Batch(_ptr(words), _ptr(lengths) if lengths is not None else None, n_reads, stride, _ptr(out),
+                           out.size, 0, MapStats(), layout, 0)
         rc = self.lib.qgm_map_host_batches(self.h, arr, len(batches), ref.h, C.byref(p))
         if rc == 1 and any(arr[i].n_out > arr[i].cap for i in range(len(batches))):
             for i, (words, lengths, out) in enumerate(keep):

@@ -2,6 +2,7 @@
 // lifetime, host<->device staging, and the orchestration of the five stages
 // for qgm_map. No exception crosses this file's exported functions.
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -161,6 +162,28 @@ __global__ void k_read_planes(const uint64_t* __restrict__ words, uint32_t n_rea
   }
 }
 
+// dense 2-bit stream (read r = bases [r*stride, (r+1)*stride)) -> W words per read
+__global__ void k_unpack_dense(const uint64_t* __restrict__ dense, uint32_t n_reads, uint32_t stride, uint32_t W,
+                               uint64_t* __restrict__ words) {
+  const uint64_t total = uint64_t(n_reads) * W;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total; t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = t / W;
+    const uint32_t k = uint32_t(t - r * W);
+    const uint64_t b0 = r * stride + 32ull * k;  // first base of this word in the stream
+    const uint64_t i = b0 >> 5;
+    const unsigned sh = unsigned(b0 & 31) * 2;
+    uint64_t w = __ldg(dense + i) << sh;
+    if (sh) w |= __ldg(dense + i + 1) >> (64 - sh);
+    const uint32_t nb = min(32u, stride - 32 * k);  // bases of this read in the word
+    if (nb < 32) w &= ~(~0ull >> (2 * nb));         // zero padding past the read
+    words[t] = w;
+  }
+}
+
+__global__ void k_fill_u32(uint32_t* __restrict__ p, uint64_t n, uint32_t v) {
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n; t += uint64_t(gridDim.x) * blockDim.x) p[t] = v;
+}
+
 __global__ void k_ref_planes(const uint64_t* __restrict__ words, uint64_t nw, uint2* __restrict__ planes) {
   for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < nw; k += uint64_t(gridDim.x) * blockDim.x)
     planes[k + 2] = to_planes(words[k]);
@@ -220,10 +243,10 @@ static void check_reads_shape(uint32_t n_reads, uint32_t stride) {
   if (n_reads > (1u << 27)) throw InputError("at most 2^27 reads per batch");
 }
 
-// after_filter: called (host side) once filtration and candidate dedup are
-// done -- qgm_map_host_batches enqueues its copies there, so they overlap the
-// compute-bound validation rather than the L2-sensitive partition, join and
-// hash dedup.
+// after_filter: called (host side) once the validation is enqueued --
+// qgm_map_host_batches enqueues its copies there, so they overlap the
+// compute-bound validation (and the strata) rather than the L2-sensitive
+// partition, join and hash dedup.
 static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_map_params& P,
                          const std::function<void()>& after_filter = {}) {
   if (P.q == 0 || P.q > 16) throw InputError("q must be in [1, 16]");
@@ -267,6 +290,11 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   }
   out.stats[6] = fst[0];
   out.stats[7] = fst[1];
+  static const int hook_at = [] {  // experiment knob: 0 after the join, 1 after dedup, 2 after validation
+    const char* e = std::getenv("QGM_HOOK");
+    return e ? std::atoi(e) : 2;
+  }();
+  if (after_filter && hook_at == 0) after_filter();
   // cnt[0]: validated hits, cnt[1]: unique candidates, cnt[2]: reads with
   // more than 32 hits -- read back together after validation (no host round
   // trip between dedup, validation and the strata's per-read counts)
@@ -276,7 +304,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
     StageScope s(c, kStageSort);
     dedup_keys_async(c, keys.p, n_raw, alt, cnt.p + 1);  // unique candidates, any order (validation is per key)
   }
-  if (after_filter) after_filter();
+  if (after_filter && hook_at == 1) after_filter();
   const uint64_t n_bound = std::max<uint64_t>(n_raw, 1);
   DBuf<uint64_t> hkeys(c, n_bound), hkeys_alt;
   DBuf<uint32_t> hvals(c, n_bound), hvals_alt;
@@ -286,6 +314,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
     validate_candidates(c, reads, ref, alt.p, n_raw, rb, P.band_width, P.pct_identity, 0, hkeys.p, hvals.p, cnt.p,
                         nullptr, cnt.p + 1);
   }
+  if (after_filter && hook_at == 2) after_filter();
   DBuf<uint32_t> per_read;
   bool big = false;
   {
@@ -905,6 +934,7 @@ int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, c
   struct Slot {
     qgm::DBuf<uint64_t> words;
     qgm::DBuf<uint32_t> lens;
+    qgm::DBuf<uint64_t> dense;  // staging of a QGM_READS_DENSE batch
     cudaEvent_t h2d = nullptr;
   };
   struct Pending {
@@ -927,26 +957,36 @@ int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, c
     }
     // both slots sized for the largest batch up front (allocated on the
     // compute stream's block cache, released after both streams are idle)
-    uint64_t max_w = 1, max_n = 1;
+    uint64_t max_w = 1, max_n = 1, max_d = 1;
     for (uint32_t i = 0; i < n_batches; ++i) {
       const qgm_batch& b = batches[i];
       qgm::check_reads_shape(b.n_reads, b.stride);
-      require(b.n_reads == 0 || (b.reads2bit && b.lengths), "null read buffers");
+      require(b.n_reads == 0 || b.reads2bit, "null read buffers");
+      require(b.layout == QGM_READS_PADDED || b.layout == QGM_READS_DENSE, "unknown read layout");
       max_w = std::max<uint64_t>(max_w, uint64_t(b.n_reads) * ((b.stride + 31) / 32) + 1);
       max_n = std::max<uint64_t>(max_n, b.n_reads);
+      if (b.layout == QGM_READS_DENSE) max_d = std::max<uint64_t>(max_d, qgm::ceil_div(uint64_t(b.n_reads) * b.stride, 32) + 1);
     }
     for (auto& s : slot) {
       s.words.alloc(c, max_w);
       s.lens.alloc(c, max_n);
+      s.dense.alloc(c, max_d);
     }
     QGM_CUDA(cudaStreamSynchronize(c.stream));  // allocations visible before the copy stream writes
     auto h2d = [&](uint32_t i) {
       const qgm_batch& b = batches[i];
       Slot& s = slot[i & 1];
-      const uint64_t nw = uint64_t(b.n_reads) * ((b.stride + 31) / 32);
-      if (nw) QGM_CUDA(cudaMemcpyAsync(s.words.p, b.reads2bit, nw * 8, cudaMemcpyHostToDevice, cs));
-      QGM_CUDA(cudaMemsetAsync(s.words.p + nw, 0, 8, cs));
-      if (b.n_reads) QGM_CUDA(cudaMemcpyAsync(s.lens.p, b.lengths, uint64_t(b.n_reads) * 4, cudaMemcpyHostToDevice, cs));
+      if (b.layout == QGM_READS_DENSE) {
+        const uint64_t nd = qgm::ceil_div(uint64_t(b.n_reads) * b.stride, 32);
+        if (nd) QGM_CUDA(cudaMemcpyAsync(s.dense.p, b.reads2bit, nd * 8, cudaMemcpyHostToDevice, cs));
+        QGM_CUDA(cudaMemsetAsync(s.dense.p + nd, 0, 8, cs));
+      } else {
+        const uint64_t nw = uint64_t(b.n_reads) * ((b.stride + 31) / 32);
+        if (nw) QGM_CUDA(cudaMemcpyAsync(s.words.p, b.reads2bit, nw * 8, cudaMemcpyHostToDevice, cs));
+        QGM_CUDA(cudaMemsetAsync(s.words.p + nw, 0, 8, cs));
+      }
+      if (b.n_reads && b.lengths)
+        QGM_CUDA(cudaMemcpyAsync(s.lens.p, b.lengths, uint64_t(b.n_reads) * 4, cudaMemcpyHostToDevice, cs));
       QGM_CUDA(cudaEventRecord(s.h2d, cs));
     };
     auto d2h = [&](uint32_t i) {  // batch i's hits, after its mapping (comp event)
@@ -969,6 +1009,15 @@ int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, c
       r.n = b.n_reads;
       r.stride = b.stride;
       r.W = (b.stride + 31) / 32;
+      {  // expand a dense batch / fill uniform lengths on the compute stream
+        const unsigned g = unsigned(std::min<uint64_t>(qgm::ceil_div(std::max<uint64_t>(uint64_t(r.n) * r.W, 1), 256),
+                                                       qgm::kSMs * 16));
+        if (b.layout == QGM_READS_DENSE && r.n) {
+          QGM_KERNEL(c, qgm::k_unpack_dense, g, 256, 0, s.dense.p, r.n, r.stride, r.W, s.words.p);
+          QGM_CUDA(cudaMemsetAsync(s.words.p + uint64_t(r.n) * r.W, 0, 8, c.stream));
+        }
+        if (!b.lengths && r.n) QGM_KERNEL(c, qgm::k_fill_u32, g, 256, 0, s.lens.p, uint64_t(r.n), r.stride);
+      }
       r.words.swap(s.words);
       r.lengths.swap(s.lens);
       struct Back {  // the slot keeps its buffers whatever happens

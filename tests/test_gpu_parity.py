@@ -241,6 +241,21 @@ def test_streamed_batches_equal_single_calls(ctx):
     for (words, lengths, stride), (hits, st) in zip(batches, got):
         want, wst = ctx.map_host(words, lengths, stride, R, q=14, mode=1)
         assert _same(hits, want) and st == wst
+    # the same batches as dense 2-bit streams; uniform-length ones without a
+    # length array
+    dense = []
+    for i, (words, lengths, stride) in enumerate(batches):
+        codes = np.zeros(lengths.size * stride, np.uint8)
+        for r in range(lengths.size):  # unpack the padded words back to codes
+            W = (stride + 31) // 32
+            for k in range(stride):
+                w = int(words[r * W + k // 32])
+                codes[r * stride + k] = (w >> (62 - 2 * (k % 32))) & 3
+        uniform = bool(np.all(lengths == stride))
+        dense.append((qgm.pack_codes(codes), None if uniform else lengths, stride, qgm.READS_DENSE, lengths.size))
+    got2 = ctx.map_host_batches(dense, R, q=14, mode=1)
+    for (h1, s1), (h2, s2) in zip(got, got2):
+        assert _same(h1, h2) and s1 == s2
 
 
 def test_partition_counter_wrap_with_a_dominant_qgram(ctx, oracle):

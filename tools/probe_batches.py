@@ -10,6 +10,8 @@ ctx = qgm.Context(0, stream=stream.cuda_stream)
 R = qgm.Reference.from_codes(ctx, ref, cb); R.prepare(16)
 words = qgm.pack_read_codes(codes, 100)
 h_words = torch.from_numpy(words.view(np.int64)).pin_memory()
+h_dense = torch.from_numpy(qgm.pack_codes(codes).view(np.int64)).pin_memory()
+DENSE = len(sys.argv) > 1 and sys.argv[1] == "dense"
 h_len = torch.from_numpy(lengths.view(np.int32)).pin_memory()
 cap = 4_000_000
 h_hits = torch.empty(cap * 16, dtype=torch.uint8).pin_memory()
@@ -18,7 +20,10 @@ lib = ctx.lib
 def run(K):
     arr = (qgm.Batch * K)()
     for i in range(K):
-        arr[i] = qgm.Batch(h_words.data_ptr(), h_len.data_ptr(), len(lengths), 100, h_hits.data_ptr(), cap, 0, qgm.MapStats())
+        if DENSE:
+            arr[i] = qgm.Batch(h_dense.data_ptr(), None, len(lengths), 100, h_hits.data_ptr(), cap, 0, qgm.MapStats(), 1, 0)
+        else:
+            arr[i] = qgm.Batch(h_words.data_ptr(), h_len.data_ptr(), len(lengths), 100, h_hits.data_ptr(), cap, 0, qgm.MapStats(), 0, 0)
     ctx._check(lib.qgm_map_host_batches(ctx.h, arr, K, R.h, C.byref(params)))
 run(3)
 for K in (1, 2, 5, 10):
