@@ -243,10 +243,11 @@ static void check_reads_shape(uint32_t n_reads, uint32_t stride) {
   if (n_reads > (1u << 27)) throw InputError("at most 2^27 reads per batch");
 }
 
-// after_filter: called (host side) once the validation is enqueued --
+// after_filter: called (host side) once the candidate dedup is enqueued --
 // qgm_map_host_batches enqueues its copies there, so they overlap the
 // compute-bound validation (and the strata) rather than the L2-sensitive
-// partition, join and hash dedup.
+// partition and join (QGM_HOOK=0/1/2: after the join / the dedup / the
+// validation, measured within noise of each other).
 static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_map_params& P,
                          const std::function<void()>& after_filter = {}) {
   if (P.q == 0 || P.q > 16) throw InputError("q must be in [1, 16]");
@@ -292,7 +293,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   out.stats[7] = fst[1];
   static const int hook_at = [] {  // experiment knob: 0 after the join, 1 after dedup, 2 after validation
     const char* e = std::getenv("QGM_HOOK");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : 1;
   }();
   if (after_filter && hook_at == 0) after_filter();
   // cnt[0]: validated hits, cnt[1]: unique candidates, cnt[2]: reads with
