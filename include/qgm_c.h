@@ -191,6 +191,9 @@ int qgm_ref_prepare(qgm_ctx* ctx, qgm_ref* ref, uint32_t q);
 int qgm_ref_mask_repeats(qgm_ctx* ctx, qgm_ref* ref, uint32_t q, uint64_t threshold);
 /* The current mask, ceil(total/64) words (all zero when there is none). */
 int qgm_ref_mask_download(qgm_ctx* ctx, const qgm_ref* ref, uint64_t* mask_bits);
+/* |P|: reference positions in P for q (windows inside a chromosome, not
+ * masked) -- the P_size of mapping_quality. */
+int qgm_ref_positions(qgm_ctx* ctx, qgm_ref* ref, uint32_t q, uint64_t* positions);
 void qgm_ref_destroy(qgm_ref* ref);
 
 /* ---- filtration: Alg. 2 -------------- */
@@ -217,6 +220,10 @@ int qgm_map(qgm_ctx* ctx, const qgm_reads* reads, const qgm_ref* ref, const qgm_
 int qgm_hits_count(const qgm_hits* h, uint64_t* n);
 int qgm_hits_stats(const qgm_hits* h, qgm_map_stats* out);
 int qgm_hits_download(qgm_ctx* ctx, const qgm_hits* h, qgm_hit* out);
+/* hit_rank of every record, in download order: the number
+ * of the read's records whose identity is >= the record's (edits <=). In
+ * best-stratum mode that is the size of the read's best stratum. */
+int qgm_hits_ranks(qgm_ctx* ctx, const qgm_hits* h, uint32_t* rank);
 void qgm_hits_destroy(qgm_hits* h);
 /* One call from host buffers to host hits: upload reads, build the index,
  * map, download (the e2e path). *n_out = hit count; if it exceeds cap the

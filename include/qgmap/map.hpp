@@ -141,11 +141,23 @@ struct MappedHit {
   auto operator<=>(const MappedHit&) const = default;
 };
 
+// mapping_quality: min{-10 log10((R-1)/|P|),
+// 255}, R = 1 -> 255, rounded half up, floored at 0. Host floating point: the
+// quality is reported, never compared bit-exactly.
+inline unsigned mapping_quality(std::uint32_t rank, std::uint64_t p_size) {
+  if (rank <= 1) return 255;
+  const double q = -10.0 * std::log10(double(rank - 1) / double(p_size ? p_size : 1));
+  const double r = std::floor(std::min(q, 255.0) + 0.5);
+  return r < 0 ? 0u : unsigned(r);
+}
+
 // One read buffer against the whole reference: index build, filtration,
-// candidate sort/dedup, validation, dedup + strata -- all on the device.
-// Output sorted by (read, chrom, ref_start, strand).
-inline std::vector<MappedHit> map_reads(const DeviceReference& ref, const PackedReadText& text,
-                                        const MapParams& p = {}, qgm_map_stats* stats = nullptr) {
+// candidate dedup, validation, dedup + strata -- all on the device. Output
+// sorted by (read, chrom, ref_start, strand); with `ranks`, also the
+// hit_rank R of every record.
+inline std::vector<MappedHit> map_reads_ranked(const DeviceReference& ref, const PackedReadText& text,
+                                               const MapParams& p, qgm_map_stats* stats,
+                                               std::vector<std::uint32_t>* ranks) {
   auto ctx = ref.context();
   auto reads = device::upload_reads(text, ctx);
   const qgm_map_params mp{p.q, p.group_width, p.sampled ? 1u : 0u, p.band.band_width, p.band.percent(),
@@ -161,7 +173,17 @@ inline std::vector<MappedHit> map_reads(const DeviceReference& ref, const Packed
   std::vector<MappedHit> out(n);
   for (std::uint64_t i = 0; i < n; ++i)
     out[i] = {raw[i].read_id, raw[i].chrom, raw[i].ref_start, raw[i].edits, raw[i].strand};
+  if (ranks) {
+    ranks->assign(n, 0);
+    ctx->check(qgm_hits_ranks(ctx->get(), h, ranks->data()));
+  }
   return out;
+}
+
+
+inline std::vector<MappedHit> map_reads(const DeviceReference& ref, const PackedReadText& text,
+                                        const MapParams& p = {}, qgm_map_stats* stats = nullptr) {
+  return map_reads_ranked(ref, text, p, stats, nullptr);
 }
 
 }  // namespace qgmap

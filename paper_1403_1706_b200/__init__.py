@@ -100,6 +100,7 @@ EXPORTS = (
     "qgm_pack_reads", "qgm_reads_upload", "qgm_reads_from_device", "qgm_reads_destroy", "qgm_index_build",
     "qgm_index_sample", "qgm_index_normalize", "qgm_index_info_get", "qgm_index_download", "qgm_index_lookup",
     "qgm_index_destroy", "qgm_ref_upload", "qgm_ref_prepare", "qgm_ref_mask_repeats", "qgm_ref_mask_download",
+    "qgm_ref_positions", "qgm_hits_ranks",
     "qgm_ref_destroy", "qgm_filter", "qgm_cands_count",
     "qgm_cands_download", "qgm_cands_unique", "qgm_cands_destroy", "qgm_validate", "qgm_map", "qgm_hits_count",
     "qgm_hits_stats", "qgm_hits_download", "qgm_hits_destroy", "qgm_map_host", "qgm_map_host_batches",
@@ -151,6 +152,8 @@ def load_library(path: str = LIB_PATH):
         "qgm_ref_prepare": (i32, [P, P, u32]),
         "qgm_ref_mask_repeats": (i32, [P, P, u32, u64]),
         "qgm_ref_mask_download": (i32, [P, P, P]),
+        "qgm_ref_positions": (i32, [P, P, u32, C.POINTER(u64)]),
+        "qgm_hits_ranks": (i32, [P, P, P]),
         "qgm_ref_destroy": (None, [P]),
         "qgm_filter": (i32, [P, P, P, P, i32, i32, C.POINTER(P)]),
         "qgm_cands_count": (i32, [P, C.POINTER(u64)]),
@@ -193,6 +196,16 @@ def load_synth(path: str = SYNTH_PATH):
 
 
 # ----------------------------------------------------------------- host codec
+def mapping_quality(rank, p_size: int):
+    """mapping_quality: min{-10 log10((R-1)/|P|), 255}, R=1 ->
+    255, rounded half up, floored at 0 (host floating point; vectorised)."""
+    r = np.asarray(rank, dtype=np.float64)
+    with np.errstate(divide="ignore"):
+        q = -10.0 * np.log10(np.maximum(r - 1.0, 0.0) / max(p_size, 1))
+    q = np.floor(np.minimum(q, 255.0) + 0.5)
+    return np.where(r <= 1, 255, np.maximum(q, 0)).astype(np.uint8)
+
+
 def pack_codes(codes: np.ndarray) -> np.ndarray:
     """1-byte codes (0..3) -> 2-bit MSB-first uint64 words (qgm_c.h layout)."""
     codes = np.ascontiguousarray(codes, dtype=np.uint8)
@@ -323,8 +336,9 @@ class Context:
                                           pct_identity, _ptr(out)))
         return out
 
-    def map(self, reads, ref, params: MapParams | None = None, **kw):
-        """Returns (hits[HIT_DTYPE], stats dict)."""
+    def map(self, reads, ref, params: MapParams | None = None, ranks: bool = False, **kw):
+        """Returns (hits[HIT_DTYPE], stats dict) -- with ranks=True also the
+        hit_rank of every record: (hits, stats, ranks)."""
         p = params or make_params(**kw)
         h = P()
         self._check(self.lib.qgm_map(self.h, reads.h, ref.h, C.byref(p), C.byref(h)))
@@ -335,7 +349,12 @@ class Context:
             self._check(self.lib.qgm_hits_stats(h, C.byref(st)))
             out = np.zeros(n.value, dtype=HIT_DTYPE)
             self._check(self.lib.qgm_hits_download(self.h, h, _ptr(out)))
-            return out, {f: getattr(st, f) for f, _ in MapStats._fields_}
+            stats = {f: getattr(st, f) for f, _ in MapStats._fields_}
+            if not ranks:
+                return out, stats
+            r = np.zeros(max(n.value, 1), dtype=np.uint32)
+            self._check(self.lib.qgm_hits_ranks(self.h, h, _ptr(r)))
+            return out, stats, r[: n.value]
         finally:
             self.lib.qgm_hits_destroy(h)
 
@@ -464,6 +483,12 @@ class Reference:
         words = np.zeros(max((total + 63) // 64, 1), np.uint64)
         self.ctx._check(self.ctx.lib.qgm_ref_mask_download(self.ctx.h, self.h, _ptr(words)))
         return np.unpackbits(words.view(np.uint8), bitorder="little")[:total]
+
+    def positions(self, q: int) -> int:
+        """|P| for q: reference positions in P (mapping_quality's P_size)."""
+        v = C.c_uint64()
+        self.ctx._check(self.ctx.lib.qgm_ref_positions(self.ctx.h, self.h, q, C.byref(v)))
+        return v.value
 
     def prepare(self, q: int):
         """Build the reference-side q-group index for q (qgm_ref_prepare)."""

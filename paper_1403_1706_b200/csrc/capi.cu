@@ -334,6 +334,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
     StageScope s(c, kStageStrata);
     out.n = stratify_unsorted(c, ref, hkeys, hvals, n_val, reads.n, int(P.mode), per_read, big, out.hits);
   }
+  out.n_reads = reads.n;
   out.stats[0] = n_raw;
   out.stats[1] = n_u;
   out.stats[2] = n_val;
@@ -890,6 +891,29 @@ int qgm_hits_download(qgm_ctx* ctx, const qgm_hits* h, qgm_hit* out) {
     if (h->h.n)
       QGM_CUDA(cudaMemcpyAsync(out, h->h.hits.p, h->h.n * 16, cudaMemcpyDeviceToHost, ctx->c.stream));
     QGM_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int qgm_hits_ranks(qgm_ctx* ctx, const qgm_hits* h, uint32_t* rank) {
+  if (!ctx || !h || (!rank && h->h.n)) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    qgm::DBuf<uint32_t> r;
+    qgm::hit_ranks(ctx->c, h->h.hits, h->h.n, h->h.n_reads, r);
+    if (h->h.n) QGM_CUDA(cudaMemcpyAsync(rank, r.p, h->h.n * 4, cudaMemcpyDeviceToHost, ctx->c.stream));
+    QGM_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int qgm_ref_positions(qgm_ctx* ctx, qgm_ref* ref, uint32_t q, uint64_t* positions) {
+  if (!ctx || !ref || !positions) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    require(q >= 1 && q <= 16, "q must be in [1, 16]");
+    require(ref->r.padded_total < (uint64_t(1) << 32), "reference index: more than 2^32-1 padded bases");
+    qgm::prepare_ref_index(ctx->c, ref->r, q);
+    QGM_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    *positions = ref->r.qidx.positions;
   });
 }
 

@@ -559,6 +559,7 @@ void prepare_ref_index(Ctx& c, const Ref& ref, unsigned q) {
   index_from_buckets(c, B, false, ref.qidx.can, packed ? nullptr : &ref.qidx.extra);
   ref.qidx.packed = packed;
   ref.qidx.palindromes = n_pal;
+  ref.qidx.positions = B.V - n_pal;
   ref.qidx.q = q;
   subbin_tables(c, ref, std::min(2 * q, 16u));
 }

@@ -202,6 +202,7 @@ struct RefQIndex {
   // min(2q, 16)): its distinct-code range [sb_d[s], sb_d[s+1]) of S' and
   // occurrence range [sb_o[s], sb_o[s+1]) of O; built when a sub-bin spans
   // >= 8 group words (the join stages these slices with bulk copies)
+  uint64_t positions = 0;  // reference positions in P (|P| of mapping_quality)
   unsigned sub_bits = ~0u;
   DBuf<uint32_t> sb_d, sb_o;
   DBuf<uint16_t> r16;  // per group word: S[w] - sb_d[sub-bin of w] (group start inside its sub-bin)
@@ -237,6 +238,7 @@ struct Cands {
 
 struct HitsObj {
   uint64_t n = 0;
+  uint32_t n_reads = 0;
   // raw, unique, validated, hits, index distinct, index occurrences,
   // filtration lookups with the occupancy bit set, occurrences visited
   uint64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -344,6 +346,9 @@ void strata_count(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const unsign
                   uint32_t n_reads, DBuf<uint32_t>& cnt, unsigned long long* d_big);
 uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBuf<uint32_t>& hit_vals, uint64_t n,
                            uint32_t n_reads, int mode, DBuf<uint32_t>& cnt, bool big, DBuf<uint8_t>& out);
+// hit-rank of every output record: #records of its read
+// whose identity is >= its own (edits <= its edits).
+void hit_ranks(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, uint32_t n_reads, DBuf<uint32_t>& rank);
 uint64_t stratify_hits(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const uint32_t* hit_vals, uint64_t n,
                        uint32_t n_reads, unsigned read_bits, int mode, DBuf<uint8_t>& out);
 

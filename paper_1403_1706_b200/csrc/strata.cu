@@ -165,7 +165,49 @@ __global__ void k_seg_emit(const uint64_t* __restrict__ skeys, const uint32_t* _
   }
 }
 
+// hit-rank: keys = read << 16 | edits of the output records,
+// sorted; the rank of a record = #records of its read with edits <= its
+// edits (identity is monotone in edits for a fixed read) = upper_bound(key) -
+// lower_bound(read << 16) in the sorted keys.
+__global__ void k_rank_keys(const uint4* __restrict__ hits, uint64_t n, uint64_t* __restrict__ keys,
+                            uint32_t* __restrict__ idx) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint4 h = hits[i];
+    keys[i] = (uint64_t(h.x) << 16) | (h.w & 0xFFFFu);
+    idx[i] = uint32_t(i);
+  }
+}
+
+__device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* a, uint64_t n, uint64_t v) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_ranks(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
+                        uint32_t* __restrict__ rank) {
+  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < n; j += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t k = keys[j];
+    const uint64_t hi = lower_bound_u64(keys, n, k + 1), lo = lower_bound_u64(keys, n, (k >> 16) << 16);
+    rank[idx[j]] = uint32_t(hi - lo);
+  }
+}
+
 }  // namespace
+
+void hit_ranks(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, uint32_t n_reads, DBuf<uint32_t>& rank) {
+  rank.alloc(c, std::max<uint64_t>(n, 1));
+  if (n == 0) return;
+  DBuf<uint64_t> keys(c, n), keys_alt;
+  DBuf<uint32_t> idx(c, n), idx_alt;
+  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
+  QGM_KERNEL(c, k_rank_keys, grid, 256, 0, reinterpret_cast<const uint4*>(hits.p), n, keys.p, idx.p);
+  radix_sort(c, keys, keys_alt, &idx, &idx_alt, n, 0, int(16 + bit_width_u64(n_reads)));
+  QGM_KERNEL(c, k_ranks, grid, 256, 0, keys.p, idx.p, n, rank.p);
+}
 
 void strata_count(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const unsigned long long* d_n, uint64_t n_max,
                   uint32_t n_reads, DBuf<uint32_t>& cnt, unsigned long long* d_big) {

@@ -185,3 +185,38 @@ TEST_CASE("device repeat mask equals the oracle's, per chromosome, and maps iden
     }
   }
 }
+
+TEST_CASE("mapping_quality: SPEC examples (SPEC.md:455-457)") {
+  CHECK(mapping_quality(1, 12345) == 255);
+  CHECK(mapping_quality(2, 1000000) == 60);
+  CHECK(mapping_quality(11, 1000000) == 50);
+  CHECK(mapping_quality(1000001, 1000000) == 0);  // floored at 0
+  for (unsigned r = 2; r < 200; ++r) CHECK(mapping_quality(r + 1, 1000000) <= mapping_quality(r, 1000000));
+}
+
+TEST_CASE("hit_rank on the device: counts of identity >= own, per read (SPEC.md:446-451)") {
+  for (std::uint64_t seed : {41u, 42u}) {
+    std::mt19937_64 g(seed);
+    auto in = tu::make_instance(g, 3, 20000, 300, 40, 110, 0.02, 12, false);
+    DeviceReference ref(in.ref);
+    for (StratumMode mode : {StratumMode::all, StratumMode::best_stratum}) {
+      MapParams p;
+      p.q = 12;
+      p.mode = mode;
+      std::vector<std::uint32_t> R;
+      const auto hits = map_reads_ranked(ref, in.text, p, nullptr, &R);
+      REQUIRE(R.size() == hits.size());
+      for (std::size_t i = 0; i < hits.size(); ++i) {
+        std::uint32_t want = 0;
+        for (const auto& h : hits)
+          if (h.read_id == hits[i].read_id && h.edits <= hits[i].edits) ++want;
+        CHECK(R[i] == want);
+        if (mode == StratumMode::best_stratum) {  // the size of the read's best stratum
+          std::uint32_t same = 0;
+          for (const auto& h : hits) same += h.read_id == hits[i].read_id;
+          CHECK(R[i] == same);
+        }
+      }
+    }
+  }
+}

@@ -306,3 +306,33 @@ def test_validation_park_overflow_finishes_in_phase_one(ctx, oracle, monkeypatch
     want, ost = oracle.map(ref, cb, codes, 100, lengths, q=12, mode=1)
     assert st["validated"] == ost["validated"]
     assert _same(got, want), (got.size, want.size)
+
+
+def test_hit_rank_and_mapq(ctx):
+    """hit_rank from the device against a direct count over the output, the
+    mapping quality from it, and the hit-rank separation
+    property of SPEC.md:499 on a repetitive reference: true origins are more
+    frequent among R=1 hits than among R>1 hits."""
+    import paper_1403_1706_b200 as qgm
+    L = 400_000
+    ref = qgm.repetitive_reference(81, L)
+    cb = np.array([0, L], np.uint64)
+    codes, lengths, tc, tp, ts = qgm.simulate_reads(82, ref, cb, 4000, 100, 0.03)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    hits, st, rank = ctx.map(reads, R, q=12, mode=1, ranks=True)
+    want = np.zeros(hits.size, np.uint32)
+    order = np.argsort(hits["read_id"], kind="stable")
+    bounds = np.searchsorted(hits["read_id"][order], np.unique(hits["read_id"]))
+    for b, e in zip(bounds, list(bounds[1:]) + [hits.size]):
+        idx = order[b:e]
+        ed = hits["edits"][idx]
+        want[idx] = (ed[None, :] <= ed[:, None]).sum(1)
+    assert np.array_equal(rank, want)
+    assert (rank > 1).sum() > 100
+    P = R.positions(12)
+    assert P == L - 12 + 1  # one chromosome, no mask
+    mq = qgm.mapping_quality(rank, P)
+    assert np.all(mq[rank == 1] == 255) and np.all(mq[rank > 1] < 255)
+    true = np.abs(hits["ref_start"].astype(np.int64) - tp[hits["read_id"]].astype(np.int64)) <= 8
+    assert true[rank == 1].mean() > true[rank > 1].mean()
