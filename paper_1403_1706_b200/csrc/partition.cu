@@ -249,10 +249,22 @@ __device__ __forceinline__ uint32_t bin_search(const uint32_t* sboff, uint32_t n
   return lo;
 }
 
+// first and last P1 bin of every P2 chunk (bfirst | blast << 16), so that the
+// scatter threads do not each binary-search the bin offsets
+__global__ void k_chunk_bins(const uint32_t* __restrict__ boff, uint32_t nbins, uint32_t n,
+                             uint32_t* __restrict__ chunk_bins) {
+  const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
+  for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < n_chunks; ch += gridDim.x * blockDim.x) {
+    const uint32_t c0 = ch * kChunk, c1 = min(n, c0 + kChunk);
+    chunk_bins[ch] = bin_search(boff, nbins, c0) | (bin_search(boff, nbins, c1 - 1) << 16);
+  }
+}
+
 __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter(const uint64_t* __restrict__ in, uint32_t n,
                                                                     const uint32_t* __restrict__ boff, Refine rf,
                                                                     unsigned sub, const uint32_t* __restrict__ off,
                                                                     uint32_t* __restrict__ cursor,
+                                                                    const uint32_t* __restrict__ chunk_bins,
                                                                     uint64_t* __restrict__ out) {
   extern __shared__ uint64_t stage[];  // kChunk join items, then kChunk u16 window keys
   uint16_t* skey = reinterpret_cast<uint16_t*>(stage + kChunk);
@@ -264,7 +276,12 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
   const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
   for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
     const uint32_t c0 = ch * kChunk, c1 = min(n, c0 + kChunk);
-    const uint32_t bfirst = bin_search(sboff, rf.nbins, c0), blast = bin_search(sboff, rf.nbins, c1 - 1);
+    if (threadIdx.x == 0 && ch + gridDim.x < n_chunks) {  // next chunk -> L2 while this one is sorted
+      const uint32_t n0 = c0 + gridDim.x * kChunk, n1 = min(n, n0 + kChunk);
+      bulk_prefetch_l2(in + n0, ((n1 - n0) * 8u) & ~15u);
+    }
+    const uint32_t cb = __ldg(chunk_bins + ch);
+    const uint32_t bfirst = cb & 0xFFFFu, blast = cb >> 16;
     const uint32_t base = (rf.key(in[c0], bfirst) >> sub) << sub;
     const uint32_t width = (((rf.key(in[c1 - 1], blast) >> sub) + 1) << sub) - base;
     uint32_t b = bfirst;
@@ -419,10 +436,13 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   out.pairs.alloc(c, V + 2);  // +2: the join bulk-copies whole 16-byte pairs of items
   const size_t smem2 = kChunk * (sizeof(uint64_t) + sizeof(uint16_t));
   QGM_CUDA(cudaFuncSetAttribute(k_refine_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+  const uint32_t n_chunks2 = uint32_t(ceil_div(V, kChunk));
+  DBuf<uint32_t> chunk_bins(c, n_chunks2);
+  QGM_KERNEL(c, k_chunk_bins, unsigned(ceil_div(n_chunks2, 256)), 256, 0, out.boff.p, 1u << bits, V, chunk_bins.p);
   {
     KernelScope ks(c, "k_refine_scatter");
     QGM_KERNEL(c, k_refine_scatter, grid2, kPartThreads, smem2, p1.p, V, out.boff.p, rf, sub, out.soff.p, h2.p,
-               out.pairs.p);
+               chunk_bins.p, out.pairs.p);
   }
 }
 
