@@ -318,12 +318,16 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
     const uint32_t k0 = threadIdx.x * per, k1 = min(width, k0 + per);
     uint32_t s = 0;
     for (uint32_t k = k0; k < k1; ++k) s += cnt[k];
+    // the first key's reservation is issued before the scan (its round trip
+    // overlaps the barriers); usually per == 1
+    const uint32_t c_first = k0 < k1 ? cnt[k0] : 0u;
+    const uint32_t g_first = c_first ? off[base + k0] + atomicAdd(cursor + base + k0, c_first) : 0u;
     uint32_t tot;
     uint32_t run = block_exclusive_scan<uint32_t>(s, ws, &tot);
     for (uint32_t k = k0; k < k1; ++k) {
       const uint32_t cv = cnt[k];
       lofs[k] = run;
-      gdst[k] = cv ? off[base + k] + atomicAdd(cursor + base + k, cv) : 0u;
+      gdst[k] = k == k0 ? g_first : cv ? off[base + k] + atomicAdd(cursor + base + k, cv) : 0u;
       cnt[k] = run;
       run += cv;
     }
