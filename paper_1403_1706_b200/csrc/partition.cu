@@ -8,13 +8,15 @@
 //                  code bits) in shared memory (packed u16 counters) and
 //                  flushes them with global atomics;
 //   scan         : sub-bin offsets; the P1 bin offsets are their prefixes;
-//   P1 scatter   : per chunk of 4096 q-gram slots, a local counting sort by
+//   P1 scatter   : per chunk of 2048 q-gram slots (runs of 8 consecutive
+//                  slots per thread sharing one register window of read
+//                  bases), a local counting sort by
 //                  bin in shared memory, one global atomic per bin to reserve
 //                  the chunk's run, then runs copied out with consecutive
 //                  threads writing consecutive 8-byte slots (full sectors;
 //                  ~16 items = one 128 B line per bin per chunk at q=16);
 //   P2 refine    : the same staged counting sort on the next code bits (up to
-//                  16 in total), per chunk of 4096 bin-ordered items, writing
+//                  16 in total), per chunk of 2048 bin-ordered items, writing
 //                  the final join items at the offsets P0 already counted.
 // ncu on an earlier single-pass scatter (12-bit bins, items written straight
 // from registers) showed 1.6 GB of read-for-ownership and 2.1 GB of writes for
@@ -43,14 +45,13 @@ constexpr uint32_t kBins = 1u << kBinBits;
 constexpr uint32_t kChunk = 8 * kPartThreads;  // q-gram slots per chunk; staging = 8 B each
 static_assert(kPartThreads >= int(kBins), "the P1 chunk scan gives every bin its own thread");
 constexpr uint32_t kPer = kChunk / kPartThreads;
+constexpr int kRun = 8;  // consecutive q-gram slots per thread (P0, P1)
+static_assert(kPer % kRun == 0, "");
 constexpr unsigned kP1CodeShift = 40, kP1MetaShift = 33;
 
-// One q-gram slot t = r * span + o: every load depends only on t, so a
-// thread issues the loads of all its slots before using any of them (the
-// read-word loads of a warp's 32 consecutive slots hit the same few lines).
-struct Slot {
-  uint32_t r, o, n;
-  uint64_t wm, w0, w1;  // read words k-1 (kMeta only), k, k+1 with k = o / 32
+struct Run {
+  uint32_t r, o0, nA, nB;
+  uint64_t A, B;  // 32-base windows from base o0-1 of read r and base -1 of read r+1
 };
 
 struct ItemGen {
@@ -59,35 +60,45 @@ struct ItemGen {
   uint32_t W, span, stride, n_items;
   FastDiv by_span;
   unsigned q;
-  template <bool kMeta>
-  __device__ __forceinline__ void fetch(uint32_t t, Slot& s) const {
-    t = min(t, n_items - 1);  // slots past the end load something valid and are dropped
-    s.r = by_span.div(t);
-    s.o = t - s.r * span;
-    s.n = __ldg(lengths + s.r);
-    const uint64_t* w = words + uint64_t(s.r) * W + (s.o >> 5);
-    s.w0 = __ldg(w);
-    s.w1 = __ldg(w + 1);  // the read's own words, or the next read's / the guard word
-    s.wm = kMeta && s.o >= 32 ? __ldg(w - 1) : 0ull;
+  // ---- runs: R consecutive slots per thread share their read words. A run
+  // lies in one read, or (span >= R) crosses into the next read once. Each
+  // read's bases come from one 32-base window starting at base o-1, so a
+  // slot's code, left base and right base are shifts of a register.
+  __device__ __forceinline__ uint64_t window(uint32_t r, uint32_t o) const {
+    const uint64_t* w = words + uint64_t(r) * W;
+    const uint32_t b = o + 31;  // base o-1, one word up: word -1 (zero) for o == 0
+    const int k = int(b >> 5) - 1;
+    const unsigned sh = 2 * (b & 31);
+    const uint64_t w0 = k >= 0 ? __ldg(w + k) : 0ull;
+    const uint64_t w1 = __ldg(w + k + 1);  // the read's own word, the next read's or the guard word
+    return (w0 << sh) | ((w1 >> 1) >> (63 - sh));
   }
-  // canonical code g of a fetched slot; f = the read's own code
-  __device__ __forceinline__ bool code(uint32_t t, const Slot& s, uint32_t& f, uint32_t& g) const {
-    const unsigned sh = 2 * (s.o & 31);
-    const uint64_t hi = sh ? (s.w0 << sh) | (s.w1 >> (64 - sh)) : s.w0;
-    f = uint32_t(hi >> (64 - 2 * q));
+  template <int R>
+  __device__ __forceinline__ void fetch_run(uint32_t t0, Run& u) const {
+    t0 = min(t0, n_items - 1);  // runs past the end load something valid and are dropped
+    u.r = by_span.div(t0);
+    u.o0 = t0 - u.r * span;
+    u.nA = __ldg(lengths + u.r);
+    u.A = window(u.r, u.o0);
+    const bool cross = R > 1 && u.o0 + R > span && u.r + 1 < n_items / span;
+    u.nB = cross ? __ldg(lengths + u.r + 1) : 0u;
+    u.B = cross ? window(u.r + 1, 0) : 0ull;
+  }
+  // slot j of a fetched run: canonical code g, own code f, meta, position
+  template <int R>
+  __device__ __forceinline__ bool run_slot(uint32_t t0, const Run& u, uint32_t j, uint32_t& f, uint32_t& g,
+                                           uint32_t& m, uint32_t& pos) const {
+    const uint32_t o1 = u.o0 + j;
+    const bool inB = R > 1 && o1 >= span;
+    const uint32_t o = inB ? o1 - span : o1, p = inB ? o : j, n = inB ? u.nB : u.nA;
+    const uint64_t w = inB ? u.B : u.A;
+    f = uint32_t((w << (2 * p + 2)) >> (64 - 2 * q));
     g = canon_code(f, q);
-    return t < n_items && s.o + q <= s.n;
-  }
-  // P1 fields: read base at o-1 (4 = none), complement of the base at o+q
-  // (4 = none), fr = (f != g)
-  __device__ __forceinline__ uint32_t meta(const Slot& s, uint32_t f, uint32_t g) const {
-    const int rel_l = int(s.o & 31) - 1;               // in [-1, 30]
-    const uint32_t rel_r = (s.o & 31) + q;             // in [1, 47]
-    const uint32_t bl = rel_l < 0 ? uint32_t(s.wm) & 3u : uint32_t(s.w0 >> (62 - 2 * rel_l)) & 3u;
-    const uint32_t br = rel_r < 32 ? uint32_t(s.w0 >> (62 - 2 * rel_r)) & 3u : uint32_t(s.w1 >> (62 - 2 * (rel_r - 32))) & 3u;
-    const uint32_t fb = s.o ? bl : 4u;
-    const uint32_t rb = s.o + q < s.n ? 3u - br : 4u;
-    return fb | (rb << 3) | (uint32_t(f != g) << 6);
+    const uint32_t bl = uint32_t(w >> (62 - 2 * p)) & 3u;
+    const uint32_t br = uint32_t(w >> (62 - 2 * (p + q + 1))) & 3u;
+    m = (o ? bl : 4u) | ((o + q < n ? 3u - br : 4u) << 3) | (uint32_t(f != g) << 6);
+    pos = (u.r + uint32_t(inB)) * stride + o;
+    return t0 + j < n_items && o + q <= n;
   }
 };
 
@@ -100,6 +111,7 @@ struct ItemGen {
 // 65536 to the global count and takes back the carry it pushed into its
 // neighbour.
 constexpr int kHistThreads = 1024;
+template <int R>
 __global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen gen, uint32_t n_items, uint32_t per_cta,
                                                                  unsigned kshift, uint32_t keys,
                                                                  uint32_t* __restrict__ hist) {
@@ -116,15 +128,19 @@ __global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen gen, ui
       if (sh == 0) atomicSub(h2 + (key >> 1), 1u << 16);  // the carry went into the high counter
     }
   };
-  for (uint32_t t0 = c0; t0 < c1; t0 += 4 * kHistThreads) {
-    Slot sl[4];
+  constexpr int kRuns = R == 1 ? 4 : 1;  // runs in flight per thread
+  for (uint32_t t0 = c0; t0 < c1; t0 += kRuns * R * kHistThreads) {
+    Run u[kRuns];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) gen.fetch<false>(t0 + k * kHistThreads + threadIdx.x, sl[k]);
+    for (int h = 0; h < kRuns; ++h) gen.fetch_run<R>(t0 + (h * kHistThreads + threadIdx.x) * R, u[h]);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t t = t0 + k * kHistThreads + threadIdx.x;
-      uint32_t f, g;
-      if (t < c1 && gen.code(t, sl[k], f, g)) count(g >> kshift);
+    for (int h = 0; h < kRuns; ++h) {
+      const uint32_t tr = t0 + (h * kHistThreads + threadIdx.x) * R;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        uint32_t f, g, m, pos;
+        if (gen.run_slot<R>(tr, u[h], j, f, g, m, pos) && tr + j < c1) count(g >> kshift);
+      }
     }
   }
   __syncthreads();
@@ -141,6 +157,7 @@ __global__ void k_bin_offsets(const uint32_t* __restrict__ soff, uint32_t nbins,
   for (uint32_t b = threadIdx.x; b <= nbins; b += blockDim.x) boff[b] = soff[b << sub];
 }
 
+template <int R>
 __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(ItemGen gen, uint32_t n_items, unsigned shift,
                                                                   const uint32_t* __restrict__ boff,
                                                                   uint32_t* __restrict__ cursor,
@@ -151,6 +168,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
   __shared__ uint32_t ws[33];
   const uint32_t lmask = shift ? (1u << shift) - 1u : 0u;
   const uint32_t n_chunks = (n_items + kChunk - 1) / kChunk;
+  constexpr uint32_t kRuns = kPer / R;
   for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
     const uint32_t c0 = ch * kChunk;
     for (uint32_t b = threadIdx.x; b < kBins; b += kPartThreads) cnt[b] = 0;
@@ -158,19 +176,23 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
     uint64_t item[kPer];
     uint32_t bin[kPer];  // ~0u = no q-gram at this slot
 #pragma unroll
-    for (uint32_t h = 0; h < kPer; h += 4) {
-      Slot sl[4];
+    for (uint32_t h0 = 0; h0 < kRuns; h0 += (kRuns < 4 ? kRuns : 4)) {
+      constexpr uint32_t kIn = kRuns < 4 ? kRuns : 4;  // runs whose loads are issued together
+      Run u[kIn];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) gen.fetch<true>(c0 + (h + k) * kPartThreads + threadIdx.x, sl[k]);
+      for (uint32_t h = 0; h < kIn; ++h) gen.fetch_run<R>(c0 + ((h0 + h) * kPartThreads + threadIdx.x) * R, u[h]);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t t = c0 + (h + k) * kPartThreads + threadIdx.x;
-        uint32_t f, g;
-        const bool ok = gen.code(t, sl[k], f, g);
-        const uint32_t pos = sl[k].r * gen.stride + sl[k].o;
-        item[h + k] = (uint64_t(g & lmask) << kP1CodeShift) | (uint64_t(gen.meta(sl[k], f, g)) << kP1MetaShift) | pos;
-        bin[h + k] = ok ? g >> shift : ~0u;
-        if (ok) atomicAdd(cnt + bin[h + k], 1u);
+      for (uint32_t h = 0; h < kIn; ++h) {
+        const uint32_t tr = c0 + ((h0 + h) * kPartThreads + threadIdx.x) * R;
+#pragma unroll
+        for (uint32_t j = 0; j < R; ++j) {
+          const uint32_t e = (h0 + h) * R + j;
+          uint32_t f, g, m, pos;
+          const bool ok = gen.run_slot<R>(tr, u[h], j, f, g, m, pos);
+          item[e] = (uint64_t(g & lmask) << kP1CodeShift) | (uint64_t(m) << kP1MetaShift) | pos;
+          bin[e] = ok ? g >> shift : ~0u;
+          if (ok) atomicAdd(cnt + bin[e], 1u);
+        }
       }
     }
     __syncthreads();
@@ -360,6 +382,9 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   gen.stride = reads.stride;
   gen.by_span = FastDiv(std::max<uint32_t>(gen.span, 1));
   gen.q = q;
+  // runs of kRun slots per thread when a run crosses at most one read
+  // boundary; one slot per thread for reads shorter than q + kRun - 1
+  const bool runs = gen.span >= uint32_t(kRun);
   const uint64_t n_items64 = uint64_t(reads.n) * gen.span;
   if (n_items64 > 0xFFFFFFFFull - kChunk) throw InputError("read batch has more than 2^32-1 q-gram slots");
   const uint32_t n_items = uint32_t(n_items64);
@@ -396,11 +421,12 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   DBuf<uint32_t> h2(c, keys + 1);
   h2.zero();
   {
-    const uint32_t per_cta = uint32_t(ceil_div(ceil_div(n_items, uint64_t(kSMs)), 4 * kHistThreads) * 4 * kHistThreads);
+    const uint32_t per_cta = uint32_t(ceil_div(ceil_div(n_items, uint64_t(kSMs)), 8 * kHistThreads) * 8 * kHistThreads);
     const size_t hsmem = size_t((keys + 1) / 2) * 4;
-    QGM_CUDA(cudaFuncSetAttribute(k_part_hist16, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsmem)));
+    auto kern = runs ? k_part_hist16<kRun> : k_part_hist16<1>;
+    QGM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsmem)));
     KernelScope ks(c, "k_part_hist");
-    QGM_KERNEL(c, k_part_hist16, unsigned(ceil_div(n_items, per_cta)), kHistThreads, hsmem, gen, n_items, per_cta,
+    QGM_KERNEL(c, kern, unsigned(ceil_div(n_items, per_cta)), kHistThreads, hsmem, gen, n_items, per_cta,
                2 * q - key_bits, keys, h2.p);
   }
   DBuf<uint32_t> total(c, 1);
@@ -417,11 +443,12 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   hist.zero();
   DBuf<uint64_t> p1(c, V);
   const size_t smem = kChunk * (sizeof(uint64_t) + sizeof(uint8_t));
-  QGM_CUDA(cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  auto p1kern = runs ? k_part_scatter<kRun> : k_part_scatter<1>;
+  QGM_CUDA(cudaFuncSetAttribute(p1kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n_items, kChunk), uint64_t(kSMs) * 4));
   {
     KernelScope ks(c, "k_part_scatter");
-    QGM_KERNEL(c, k_part_scatter, grid, kPartThreads, smem, gen, n_items, shift, out.boff.p, hist.p, p1.p);
+    QGM_KERNEL(c, p1kern, grid, kPartThreads, smem, gen, n_items, shift, out.boff.p, hist.p, p1.p);
   }
   // P2: refine to the top min(2q, 16) code bits (short reuse distance of the
   // reference-index sectors in the join) and convert to join items. Runs even

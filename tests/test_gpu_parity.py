@@ -147,12 +147,14 @@ def test_c2_full_size_hit_parity_with_oracle(ctx, oracle):
     assert _same(got, want), (got.size, want.size)
 
 
-@pytest.mark.parametrize("stride,band", [(130, 32), (600, 64)])
+@pytest.mark.parametrize("stride,band", [(18, 32), (20, 32), (130, 32), (600, 64)])
 def test_variable_length_reads_match_oracle(ctx, oracle, stride, band):
     """Reads of mixed lengths (some shorter than q, some filling the stride),
     several chromosomes, both modes: exercises the per-read length paths (the
     join item's n - q - o field, and -- for strides above q + 511 -- the
-    join's reload of the read length)."""
+    join's reload of the read length). Strides 18 and 20 at q=12 leave 7 and 9
+    q-gram slots per read: the partition's one-slot-per-thread path and its
+    8-slot runs that cross a read boundary."""
     import paper_1403_1706_b200 as qgm
     L = 400_000
     ref = qgm.random_reference(21, L)
