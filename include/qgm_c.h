@@ -224,6 +224,23 @@ int qgm_hits_download(qgm_ctx* ctx, const qgm_hits* h, qgm_hit* out);
  * of the read's records whose identity is >= the record's (edits <=). In
  * best-stratum mode that is the size of the read's best stratum. */
 int qgm_hits_ranks(qgm_ctx* ctx, const qgm_hits* h, uint32_t* rank);
+/* traceback_cigar (DESIGN.md Appendix B.8) of every record,
+ * in download order: the oriented read against its chromosome from ref_start,
+ * anchored start, free end, band |j - i| <= band_width - 1. ops[i * max_ops
+ * + x] are BAM-style (length << 4 | op, M = 0, I = 1, D = 2). Fails with
+ * QGM_ERR_INPUT if a record needs more than max_ops operations (out[].n_ops
+ * then holds the counts). reads/ref must be the ones the hits were mapped
+ * from. */
+typedef struct qgm_cigar_info {
+  uint32_t ref_start; /* alignment start; > the hit's ref_start when leading deletions were dropped */
+  uint16_t n_ops;     /* CIGAR operations */
+  uint16_t edits;     /* I + D + mismatched M columns (<= the hit's edits when its alignment is in the band) */
+} qgm_cigar_info;
+int qgm_hits_cigar(qgm_ctx* ctx, const qgm_hits* h, const qgm_reads* reads, const qgm_ref* ref,
+                   uint32_t band_width, uint32_t max_ops, uint32_t* ops, qgm_cigar_info* out);
+/* The same for host hit records (e.g. from qgm_map_host). */
+int qgm_cigar_records(qgm_ctx* ctx, const qgm_reads* reads, const qgm_ref* ref, const qgm_hit* hits, uint64_t n,
+                      uint32_t band_width, uint32_t max_ops, uint32_t* ops, qgm_cigar_info* out);
 void qgm_hits_destroy(qgm_hits* h);
 /* One call from host buffers to host hits: upload reads, build the index,
  * map, download (the e2e path). *n_out = hit count; if it exceeds cap the

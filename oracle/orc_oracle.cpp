@@ -83,6 +83,34 @@ int orc_validate_cands(const uint8_t* ref_codes, const uint64_t* chrom_begin, ui
   });
 }
 
+// traceback_cigar (Appendix B.8) of explicit 16-byte hit records. ops: n *
+// max_ops u32 (BAM-style); info per hit: {ref_start u32, n_ops u16, edits u16}
+// (n_ops > max_ops: truncated).
+int orc_cigar(const uint8_t* ref_codes, const uint64_t* chrom_begin, uint32_t n_chrom, const uint8_t* read_codes,
+              uint32_t stride, const uint32_t* lengths, uint32_t n_reads, const void* hits, uint64_t n_hits,
+              unsigned B, uint32_t max_ops, unsigned threads, uint32_t* ops, void* info) {
+  return orc::guarded([&] {
+    auto ref = orc::make_ref(ref_codes, chrom_begin, n_chrom, nullptr);
+    auto rs = orc::make_reads(read_codes, stride, lengths, n_reads);
+    auto* hr = static_cast<const orc::HitRec*>(hits);
+    struct Info { uint32_t ref_start; uint16_t n_ops, edits; };
+    auto* inf = static_cast<Info*>(info);
+    parallel_chunks(n_hits, threads, [&](size_t b, size_t e) {
+      for (size_t i = b; i < e; ++i) {
+        const orc::HitRec& h = hr[i];
+        if (h.read >= rs.count() || h.chrom + 1 >= ref.chrom_begin.size()) throw input_error("hit out of range");
+        const uint32_t n = rs.lengths[h.read];
+        std::vector<uint8_t> rd(rs.read(h.read), rs.read(h.read) + n);
+        if (h.strand) rd = reverse_complement(rd.data(), n);
+        const uint8_t* chrom = ref.codes.data() + ref.chrom_begin[h.chrom];
+        const Cigar c = traceback_cigar(rd.data(), n, chrom, int64_t(ref.len(h.chrom)), h.ref_start, B);
+        inf[i] = {c.ref_start, uint16_t(c.ops.size()), uint16_t(c.edits)};
+        for (size_t t = 0; t < c.ops.size() && t < max_ops; ++t) ops[i * max_ops + t] = c.ops[t];
+      }
+    });
+  });
+}
+
 // Whole path with the restated index: stats = {raw, unique, kept, hits}.
 int orc_map(const uint8_t* ref_codes, const uint64_t* chrom_begin, uint32_t n_chrom, const uint8_t* mask,
             const uint8_t* read_codes, uint32_t stride, const uint32_t* lengths, uint32_t n_reads,

@@ -25,6 +25,7 @@ HIT_DTYPE = np.dtype([("read_id", "<u4"), ("chrom", "<u4"), ("ref_start", "<u4")
                       ("strand", "u1"), ("reserved", "u1")])
 VAL_DTYPE = np.dtype([("edits", "<i4"), ("start", "<u4"), ("ref_start", "<u4"), ("kept", "u1"),
                       ("in_range", "u1"), ("r0", "u1"), ("r1", "u1"), ("r2", "<u4")])
+CIGAR_DTYPE = np.dtype([("ref_start", "<u4"), ("n_ops", "<u2"), ("edits", "<u2")])
 REFHIT_DTYPE = np.dtype([("diagonal", "<i8"), ("read_id", "<u4"), ("pad", "<u4")])
 
 P = C.c_void_p
@@ -122,6 +123,21 @@ class Oracle:
         self.b.check(f(_p(ref_codes), _p(cb), cb.size - 1, _p(read_codes), stride, _p(lengths), lengths.size,
                        _p(cands), cands.size, band, pct, int(use_dp), threads, _p(out)))
         return out
+
+    def cigar(self, ref_codes, chrom_begin, read_codes, stride, lengths, hits, band=32, max_ops=64, threads=0):
+        """traceback_cigar (DESIGN.md Appendix B.8) of hit records -> (ops[n, max_ops] u32, info)."""
+        ref_codes = np.ascontiguousarray(ref_codes, dtype=np.uint8)
+        cb = np.ascontiguousarray(chrom_begin, dtype=np.uint64)
+        read_codes, lengths = _reads_args(read_codes, stride, lengths)
+        hits = np.ascontiguousarray(hits, dtype=HIT_DTYPE)
+        ops = np.zeros((hits.size, max_ops), np.uint32)
+        info = np.zeros(hits.size, CIGAR_DTYPE)
+        f = self.lib.orc_cigar
+        f.argtypes = [P, P, C.c_uint32, P, C.c_uint32, P, C.c_uint32, P, C.c_uint64, C.c_uint32, C.c_uint32,
+                      C.c_uint32, P, P]
+        self.b.check(f(_p(ref_codes), _p(cb), cb.size - 1, _p(read_codes), stride, _p(lengths), lengths.size,
+                       _p(hits), hits.size, band, max_ops, threads, _p(ops), _p(info)))
+        return ops, info
 
     def map(self, ref_codes, chrom_begin, read_codes, stride, lengths, q=16, w=32, sampled=False, band=32, pct=80,
             mode=0, strands=3, mask=None, threads=0):
@@ -271,3 +287,8 @@ def repeat_mask(ref_codes, chrom_begin, q, threshold):
         _, inv, cnt = np.unique(code, return_inverse=True, return_counts=True)
         mask[b:b + code.size] = cnt[inv] > threshold
     return mask
+
+
+def cigar_string(ops, n_ops):
+    """BAM-style ops (length << 4 | op, M=0 I=1 D=2) -> CIGAR text."""
+    return "".join(f"{int(x) >> 4}{'MID'[int(x) & 15]}" for x in ops[:n_ops])

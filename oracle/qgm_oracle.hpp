@@ -499,6 +499,85 @@ inline std::vector<Hit> stratify(std::vector<Hit> hits, int mode) {
   return out;
 }
 
+// ---------------------------------------------------------------- traceback
+// traceback_cigar, frozen as DESIGN.md Appendix B.8: the
+// oriented read (n bases) against the chromosome from ref_start, global at the
+// start (D[0][j] = j, D[i][0] = i), free at the end, cells restricted to the
+// band |j - i| <= W with W = B - 1 (the validation band widened to both sides:
+// it holds every alignment the validation band allowed from this start).
+// Column j >= 1 is chromosome base ref_start + j - 1 (kSentinel past the end).
+// End = the largest j with minimal D[n][j] among the columns inside the
+// chromosome (or j = max(0, n - W) if none is in the band). Traceback prefers M (diagonal),
+// then I (read base against no reference base), then D; leading D operations
+// are dropped and move ref_start right ("possibly improved ref_start").
+// ops are BAM-style: length << 4 | op with M = 0, I = 1, D = 2.
+struct Cigar {
+  uint32_t ref_start = 0;
+  int edits = 0;  // I + D + mismatched M columns of the reported alignment
+  std::vector<uint32_t> ops;
+  std::string str() const {
+    std::string o;
+    for (uint32_t x : ops) o += std::to_string(x >> 4) + "MID"[x & 15];
+    return o;
+  }
+};
+
+inline Cigar traceback_cigar(const uint8_t* rd, uint32_t n, const uint8_t* chrom, int64_t Lc, uint32_t ref_start,
+                             unsigned B) {
+  if (B == 0 || B > kMaxBand) throw input_error("band must be in [1, 64]");
+  const int64_t W = int64_t(B) - 1, J = int64_t(n) + W;
+  auto base = [&](int64_t j) -> uint8_t {  // column j >= 1
+    const int64_t x = int64_t(ref_start) + j - 1;
+    return x >= 0 && x < Lc ? chrom[x] : kSentinel;
+  };
+  std::vector<std::vector<int>> D(n + 1, std::vector<int>(size_t(J + 1), kInf));
+  auto in_band = [&](int64_t i, int64_t j) { return j >= 0 && j <= J && j - i <= W && i - j <= W; };
+  for (int64_t j = 0; j <= std::min<int64_t>(J, W); ++j) D[0][j] = int(j);
+  for (int64_t i = 1; i <= int64_t(n); ++i)
+    for (int64_t j = std::max<int64_t>(0, i - W); j <= std::min(J, i + W); ++j) {
+      int b = kInf;
+      if (j == 0) b = int(i);
+      else {
+        if (D[i - 1][j - 1] < kInf) b = std::min(b, D[i - 1][j - 1] + (rd[i - 1] == base(j) ? 0 : 1));
+        if (in_band(i - 1, j) && D[i - 1][j] < kInf) b = std::min(b, D[i - 1][j] + 1);
+        if (D[i][j - 1] < kInf) b = std::min(b, D[i][j - 1] + 1);
+      }
+      D[i][j] = b;
+    }
+  // end column: in the chromosome when the band reaches it (no alignment
+  // running into the sentinels past its end), the largest j on ties (a
+  // trailing mismatch or deletion rather than an insertion)
+  const int64_t jlo = std::max<int64_t>(0, int64_t(n) - W);
+  const int64_t jhi = std::min(J, std::max(Lc - int64_t(ref_start), jlo));
+  int64_t je = -1;
+  for (int64_t j = jlo; j <= jhi; ++j)
+    if (je < 0 || D[n][j] <= D[n][je]) je = j;
+  Cigar c;
+  c.ref_start = ref_start;
+  c.edits = D[n][je];
+  std::vector<uint32_t> rev;  // ops from the end
+  auto push = [&](uint32_t op) {
+    if (!rev.empty() && (rev.back() & 15) == op) rev.back() += 16;
+    else rev.push_back(16 | op);
+  };
+  int64_t i = n, j = je;
+  while (i > 0 || j > 0) {
+    if (i == 0) { push(2); --j; continue; }
+    if (j == 0) { push(1); --i; continue; }
+    const int cur = D[i][j];
+    if (D[i - 1][j - 1] < kInf && D[i - 1][j - 1] + (rd[i - 1] == base(j) ? 0 : 1) == cur) { push(0); --i; --j; }
+    else if (in_band(i - 1, j) && D[i - 1][j] < kInf && D[i - 1][j] + 1 == cur) { push(1); --i; }
+    else { push(2); --j; }
+  }
+  if (!rev.empty() && (rev.back() & 15) == 2) {  // leading deletions
+    c.ref_start += rev.back() >> 4;
+    c.edits -= int(rev.back() >> 4);
+    rev.pop_back();
+  }
+  c.ops.assign(rev.rbegin(), rev.rend());
+  return c;
+}
+
 struct Stats {
   uint64_t raw = 0, unique = 0, validated_kept = 0, hits = 0;
 };

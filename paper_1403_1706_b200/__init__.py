@@ -46,6 +46,7 @@ VALIDATED_DTYPE = np.dtype([("edits", "<i4"), ("start", "<u4"), ("ref_start", "<
                             ("in_range", "u1"), ("r0", "u1"), ("r1", "u1"), ("r2", "<u4")])
 HIT_DTYPE = np.dtype([("read_id", "<u4"), ("chrom", "<u4"), ("ref_start", "<u4"), ("edits", "<u2"),
                       ("strand", "u1"), ("reserved", "u1")])
+CIGAR_DTYPE = np.dtype([("ref_start", "<u4"), ("n_ops", "<u2"), ("edits", "<u2")])
 assert CANDIDATE_DTYPE.itemsize == 24 and VALIDATED_DTYPE.itemsize == 20 and HIT_DTYPE.itemsize == 16
 
 
@@ -100,7 +101,7 @@ EXPORTS = (
     "qgm_pack_reads", "qgm_reads_upload", "qgm_reads_from_device", "qgm_reads_destroy", "qgm_index_build",
     "qgm_index_sample", "qgm_index_normalize", "qgm_index_info_get", "qgm_index_download", "qgm_index_lookup",
     "qgm_index_destroy", "qgm_ref_upload", "qgm_ref_prepare", "qgm_ref_mask_repeats", "qgm_ref_mask_download",
-    "qgm_ref_positions", "qgm_hits_ranks",
+    "qgm_ref_positions", "qgm_hits_ranks", "qgm_hits_cigar", "qgm_cigar_records",
     "qgm_ref_destroy", "qgm_filter", "qgm_cands_count",
     "qgm_cands_download", "qgm_cands_unique", "qgm_cands_destroy", "qgm_validate", "qgm_map", "qgm_hits_count",
     "qgm_hits_stats", "qgm_hits_download", "qgm_hits_destroy", "qgm_map_host", "qgm_map_host_batches",
@@ -154,6 +155,8 @@ def load_library(path: str = LIB_PATH):
         "qgm_ref_mask_download": (i32, [P, P, P]),
         "qgm_ref_positions": (i32, [P, P, u32, C.POINTER(u64)]),
         "qgm_hits_ranks": (i32, [P, P, P]),
+        "qgm_hits_cigar": (i32, [P, P, P, P, u32, u32, P, P]),
+        "qgm_cigar_records": (i32, [P, P, P, P, u64, u32, u32, P, P]),
         "qgm_ref_destroy": (None, [P]),
         "qgm_filter": (i32, [P, P, P, P, i32, i32, C.POINTER(P)]),
         "qgm_cands_count": (i32, [P, C.POINTER(u64)]),
@@ -357,6 +360,19 @@ class Context:
             return out, stats, r[: n.value]
         finally:
             self.lib.qgm_hits_destroy(h)
+
+    def cigar(self, reads, ref, hits: np.ndarray, band_width: int = 32, max_ops: int | None = None):
+        """traceback_cigar (DESIGN.md Appendix B.8) of hit
+        records on the device: (ops[n, max_ops] u32 BAM-style, info[CIGAR_DTYPE]).
+        max_ops defaults to 2 * (stride + band_width) + 1, enough for any record."""
+        hits = np.ascontiguousarray(hits, dtype=HIT_DTYPE)
+        if max_ops is None:
+            max_ops = 2 * (reads.stride + band_width) + 1
+        ops = np.zeros((hits.size, max_ops), np.uint32)
+        info = np.zeros(hits.size, CIGAR_DTYPE)
+        self._check(self.lib.qgm_cigar_records(self.h, reads.h, ref.h, _ptr(hits), hits.size, band_width, max_ops,
+                                               _ptr(ops), _ptr(info)))
+        return ops, info
 
     def map_host(self, words: np.ndarray, lengths: np.ndarray, stride: int, ref, params=None, out=None, **kw):
         """e2e entry: host reads in, host hits out (qgm_map_host)."""
@@ -567,3 +583,8 @@ class Index:
             self.close()
         except Exception:
             pass
+
+
+def cigar_string(ops: np.ndarray, n_ops: int) -> str:
+    """BAM-style ops (length << 4 | op, M=0 I=1 D=2) -> CIGAR text."""
+    return "".join(f"{int(x) >> 4}{'MID'[int(x) & 15]}" for x in ops[:n_ops])

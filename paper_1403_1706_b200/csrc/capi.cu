@@ -905,6 +905,50 @@ int qgm_hits_ranks(qgm_ctx* ctx, const qgm_hits* h, uint32_t* rank) {
   });
 }
 
+namespace {
+int cigar_impl(qgm_ctx* ctx, const qgm::DBuf<uint8_t>* dev_hits, const qgm_hit* host_hits, uint64_t n,
+               const qgm_reads* reads, const qgm_ref* ref, uint32_t band_width, uint32_t max_ops, uint32_t* ops,
+               qgm_cigar_info* out) {
+  if (!ctx || !reads || !ref || (n && (!ops || !out))) return QGM_ERR_INPUT;
+  return guard(ctx, [&] {
+    activate(ctx);
+    require(band_width >= 1 && band_width <= 64, "band_width must be in [1, 64]");
+    require(max_ops >= 1, "max_ops must be positive");
+    qgm::DBuf<uint8_t> up;
+    if (!dev_hits) {
+      up.alloc(ctx->c, std::max<uint64_t>(n, 1) * 16);
+      if (n) QGM_CUDA(cudaMemcpyAsync(up.p, host_hits, n * 16, cudaMemcpyHostToDevice, ctx->c.stream));
+      dev_hits = &up;
+    }
+    qgm::DBuf<uint32_t> d_ops;
+    qgm::DBuf<uint2> d_info;
+    qgm::hits_cigar(ctx->c, *dev_hits, n, reads->r, ref->r, band_width, max_ops, d_ops, d_info);
+    if (n) {
+      QGM_CUDA(cudaMemcpyAsync(ops, d_ops.p, n * max_ops * 4, cudaMemcpyDeviceToHost, ctx->c.stream));
+      QGM_CUDA(cudaMemcpyAsync(out, d_info.p, n * 8, cudaMemcpyDeviceToHost, ctx->c.stream));
+    }
+    QGM_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    uint32_t need = 0;
+    for (uint64_t i = 0; i < n; ++i) need = std::max<uint32_t>(need, out[i].n_ops);
+    if (need > max_ops)
+      throw qgm::InputError("cigar: a record needs " + std::to_string(need) + " operations, max_ops is " +
+                            std::to_string(max_ops));
+  });
+}
+}  // namespace
+
+int qgm_hits_cigar(qgm_ctx* ctx, const qgm_hits* h, const qgm_reads* reads, const qgm_ref* ref,
+                   uint32_t band_width, uint32_t max_ops, uint32_t* ops, qgm_cigar_info* out) {
+  if (!h) return QGM_ERR_INPUT;
+  return cigar_impl(ctx, &h->h.hits, nullptr, h->h.n, reads, ref, band_width, max_ops, ops, out);
+}
+
+int qgm_cigar_records(qgm_ctx* ctx, const qgm_reads* reads, const qgm_ref* ref, const qgm_hit* hits, uint64_t n,
+                      uint32_t band_width, uint32_t max_ops, uint32_t* ops, qgm_cigar_info* out) {
+  if (!hits && n) return QGM_ERR_INPUT;
+  return cigar_impl(ctx, nullptr, hits, n, reads, ref, band_width, max_ops, ops, out);
+}
+
 int qgm_ref_positions(qgm_ctx* ctx, qgm_ref* ref, uint32_t q, uint64_t* positions) {
   if (!ctx || !ref || !positions) return QGM_ERR_INPUT;
   return guard(ctx, [&] {

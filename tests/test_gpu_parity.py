@@ -338,3 +338,82 @@ def test_hit_rank_and_mapq(ctx):
     assert np.all(mq[rank == 1] == 255) and np.all(mq[rank > 1] < 255)
     true = np.abs(hits["ref_start"].astype(np.int64) - tp[hits["read_id"]].astype(np.int64)) <= 8
     assert true[rank == 1].mean() > true[rank > 1].mean()
+
+
+def _oracle_cigar(oracle, ref, cb, codes, stride, lengths, hits, band):
+    ops, info = oracle.cigar(ref, cb, codes, stride, lengths, hits, band=band, max_ops=2 * (stride + band) + 1)
+    return ops, info
+
+
+@pytest.mark.parametrize("band", [32, 64])
+def test_cigar_matches_oracle_on_mapped_hits(ctx, oracle, band):
+    """traceback_cigar (Appendix B.8) of every all-mode hit of a C1-shaped run
+    with indels, several chromosomes (reads overhanging their ends), both
+    strands: device ops and info bit-identical to oracle::traceback_cigar; the
+    64-bit band word (B=32) and the 128-bit one (B=64)."""
+    import paper_1403_1706_b200 as qgm
+    L = 600_000
+    ref = qgm.random_reference(31, L)
+    cb = np.array([0, 200_000, 200_150, 410_000, L], np.uint64)
+    codes, lengths, *_ = qgm.simulate_reads(32, ref, cb, 4000, 100, 0.05)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    hits, st = ctx.map(reads, R, q=12, mode=1, band_width=band)
+    assert hits.size > 3000
+    ops, info = ctx.cigar(reads, R, hits, band_width=band)
+    wops, winfo = _oracle_cigar(oracle, ref, cb, codes, 100, lengths, hits, band)
+    assert np.array_equal(info, winfo)
+    for i in range(hits.size):
+        k = int(info["n_ops"][i])
+        assert np.array_equal(ops[i, :k], wops[i, :k]), i
+    # the validated alignment lies in the traceback band: never more edits
+    # than the hit's k once the dropped leading deletions are counted back
+    assert np.all(info["edits"].astype(int) + (info["ref_start"].astype(int) - hits["ref_start"].astype(int))
+                  <= hits["edits"].astype(int) + (hits["ref_start"] == 0) * band)
+    s = qgm.cigar_string(ops[0], info["n_ops"][0])
+    assert s and s[-1] in "MID"
+
+
+def test_cigar_random_records_and_edges_match_oracle(ctx, oracle):
+    """Arbitrary records (random starts, both strands, starts at a
+    chromosome's first and last base, a 1-base chromosome, short reads,
+    B = 1 and odd bands) -- ties and clamped ends, not only good alignments."""
+    import paper_1403_1706_b200 as qgm
+    rng = np.random.default_rng(41)
+    L = 50_000
+    ref = qgm.random_reference(42, L)
+    cb = np.array([0, 1, 20_000, 20_040, L], np.uint64)
+    stride = 70
+    codes, lengths, *_ = qgm.simulate_reads(43, ref, cb, 600, stride, 0.08)
+    lengths = np.minimum(lengths, rng.integers(1, stride + 1, lengths.size).astype(np.uint32))
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, stride)
+    n = 3000
+    hits = np.zeros(n, qgm.HIT_DTYPE)
+    hits["read_id"] = rng.integers(0, lengths.size, n)
+    hits["chrom"] = rng.integers(0, cb.size - 1, n)
+    clen = (cb[1:] - cb[:-1]).astype(np.int64)
+    pos = rng.integers(0, 1 << 30, n) % clen[hits["chrom"]]
+    pos[::7] = 0
+    pos[1::7] = clen[hits["chrom"][1::7]] - 1
+    hits["ref_start"] = pos
+    hits["strand"] = rng.integers(0, 2, n)
+    for band in (1, 7, 32, 33, 64):
+        ops, info = ctx.cigar(reads, R, hits, band_width=band)
+        wops, winfo = _oracle_cigar(oracle, ref, cb, codes, stride, lengths, hits, band)
+        assert np.array_equal(info, winfo), band
+        m = np.arange(ops.shape[1])[None, :] < info["n_ops"][:, None]
+        assert np.array_equal(np.where(m, ops, 0), np.where(m, wops, 0)), band
+
+
+def test_cigar_spec_examples_on_device(ctx):
+    import paper_1403_1706_b200 as qgm
+    enc = lambda s: np.array(["ACGT".index(c) for c in s], np.uint8)  # noqa: E731
+    cases = [("ACGT", "ACGT", "4M", 0), ("ACGT", "ACGGT", "2M1D2M", 0), ("ACGT", "ACT", "2M1I1M", 0),
+             ("ACGT", "CCACGTCC", "4M", 2)]
+    for read, chrom, want, start in cases:
+        R = qgm.Reference.from_codes(ctx, enc(chrom), np.array([0, len(chrom)], np.uint64))
+        reads = qgm.Reads.from_codes(ctx, enc(read), np.array([len(read)], np.uint32), len(read))
+        h = np.zeros(1, qgm.HIT_DTYPE)
+        ops, info = ctx.cigar(reads, R, h)
+        assert qgm.cigar_string(ops[0], info["n_ops"][0]) == want and info["ref_start"][0] == start

@@ -11,6 +11,7 @@ pinned to SPEC.md's worked examples and to a banded anchored-start DP below.
 """
 import json
 import os
+import re
 
 import numpy as np
 import pytest
@@ -261,3 +262,84 @@ def test_pack_reads_golden_against_this_repos_codec():
                              capture_output=True, text=True, check=True).stdout.split("\n")
         assert [int(x) for x in out[0].split()] == g["codes"]
         assert [int(x) for x in out[1].split()] == g["valid"]
+
+
+# ----------------------------------------------------------------- traceback
+def _cigar1(oracle, read, chrom, start, B):
+    from oracle.pyoracle import HIT_DTYPE, cigar_string
+    h = np.zeros(1, HIT_DTYPE)
+    h["ref_start"] = start
+    ops, info = oracle.cigar(np.asarray(chrom, np.uint8), np.array([0, len(chrom)], np.uint64),
+                             np.asarray(read, np.uint8), len(read), np.array([len(read)], np.uint32), h, band=B,
+                             max_ops=2 * (len(read) + B) + 1)
+    return cigar_string(ops[0], info["n_ops"][0]), int(info["ref_start"][0]), int(info["edits"][0])
+
+
+def walk_cigar(cigar, read, chrom, start):
+    """(read bases consumed, reference bases consumed, edits) of a CIGAR text."""
+    i = j = e = 0
+    for ln, op in re.findall(r"(\d+)([MID])", cigar):
+        ln = int(ln)
+        if op == "M":
+            e += sum(int(read[i + x] != (chrom[start + j + x] if start + j + x < len(chrom) else 4))
+                     for x in range(ln))
+            i += ln
+            j += ln
+        elif op == "I":
+            i += ln
+            e += ln
+        else:
+            j += ln
+            e += ln
+    return i, j, e
+
+
+def test_spec_cigar_examples(oracle):
+    # SPEC.md:480-483 traceback_cigar examples
+    assert _cigar1(oracle, enc("ACGT"), enc("ACGT"), 0, 32) == ("4M", 0, 0)
+    assert _cigar1(oracle, enc("ACGT"), enc("ACGGT"), 0, 32) == ("2M1D2M", 0, 1)
+    c, _, e = _cigar1(oracle, enc("ACGT"), enc("ACT"), 0, 32)
+    assert "1I" in c and e == 1
+    # leading deletions move the start ("possibly improved ref_start")
+    assert _cigar1(oracle, enc("ACGT"), enc("CCACGTCC"), 0, 32) == ("4M", 2, 0)
+
+
+def test_cigar_cost_matches_reference_anchored_distance(oracle):
+    """With a band wider than the DP (B = 64 > n, L) the traceback's cost is
+    the reference's own unbanded anchored_start_distance (oracles.hpp:116-135,
+    golden values) at every start; with the validation's band it lies between
+    that and the banded k (the validated alignment is inside the band)."""
+    for g in GOLDEN["banded"]:
+        read, win, B, k = g["read"], g["window"], g["B"], g["k"]
+        if len(read) == 0:
+            continue
+        for s, anch in enumerate(g["anchored"]):
+            if s >= len(win):
+                continue
+            c, s2, e = _cigar1(oracle, read, win, s, 64)
+            assert e + (s2 - s) == anch, (g, s)
+            c, s2, e = _cigar1(oracle, read, win, s, B)
+            assert e + (s2 - s) >= anch
+        _, ks = oracle.validate_pair(np.array(read, np.uint8), np.array(win, np.uint8), B)
+        c, s2, e = _cigar1(oracle, read, win, ks, B)
+        assert e + (s2 - ks) <= k
+
+
+def test_cigar_is_a_consistent_alignment(oracle):
+    rng = np.random.default_rng(29)
+    for it in range(600):
+        n = int(rng.integers(1, 60))
+        B = int(rng.integers(1, 65))
+        chrom = rng.integers(0, 4, int(rng.integers(n // 2 + 1, 3 * n + 8))).astype(np.uint8)
+        start = int(rng.integers(0, chrom.size))
+        read = chrom[start:start + n].copy()
+        if read.size < n:
+            read = np.concatenate([read, rng.integers(0, 4, n - read.size).astype(np.uint8)])
+        for _ in range(int(rng.integers(0, 6))):
+            p = int(rng.integers(0, n))
+            read[p] = rng.integers(0, 4)
+        c, s2, e = _cigar1(oracle, read, chrom, start, B)
+        i, j, e2 = walk_cigar(c, read, chrom, s2)
+        assert i == n and e2 == e, (c, n, e, e2)
+        assert re.match(r"^\d+[MI]", c), c  # leading deletions were dropped
+        assert s2 >= start
