@@ -345,6 +345,7 @@ def run_gpu(args):
     ktimes = ctx.kernel_times(reset=True)
     stimes = ctx.stage_times(reset=True, host=True)
     ctx.profile(False)
+    post = postprocess_pass(ctx, lib, C, qgm, R, d_words, d_len, n_reads, rlen, params, band)
     dev_ms, e2e_ms, e2e1_ms = sharding.max_over_ranks([dev_ms, e2e_ms, e2e1_ms], dist, device=f"cuda:{local}")
     total_reads = n_reads * args.steps * world
     value = sharding.weak_scaling_value(n_reads, args.steps, world, dev_ms)
@@ -414,6 +415,7 @@ def run_gpu(args):
         "counts": st,
         "reference_prepare_s": round(ref_prepare_s, 3),
         "host_binding": {"cores": numa_cores, "rule": "NVML CPU affinity of the rank's GPU"},
+        "postprocess": post,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         os.sched_setaffinity(0, set(range(os.cpu_count())))  # the CPU baseline gets every host core
@@ -424,6 +426,49 @@ def run_gpu(args):
     ctx.close()
     if dist:
         dist.destroy_process_group()
+
+
+def postprocess_pass(ctx, lib, C, qgm, R, d_words, d_len, n_reads, rlen, params, band):
+    """SPEC.md:446-483 tail on one batch's device-resident hits (not part of
+    `value`): hit_rank (k_rank_keys + radix sort + k_ranks) and
+    traceback_cigar (k_cigar), kernel times from CUDA events, second of two
+    runs."""
+    rd = C.c_void_p()
+    ctx._check(lib.qgm_reads_from_device(ctx.h, C.c_void_p(d_words.data_ptr()), C.c_void_p(d_len.data_ptr()),
+                                         n_reads, rlen, C.byref(rd)))
+    h = C.c_void_p()
+    try:
+        ctx._check(lib.qgm_map(ctx.h, rd, R.h, C.byref(params), C.byref(h)))
+        n = C.c_uint64()
+        lib.qgm_hits_count(h, C.byref(n))
+        n = n.value
+        if n == 0:
+            return None
+        max_ops = 48
+        ops = np.empty(n * max_ops, np.uint32)
+        info = np.empty(n, qgm.CIGAR_DTYPE)
+        ranks = np.empty(n, np.uint32)
+        ctx.profile(True)
+        for it in range(2):
+            ctx.kernel_times(reset=True)
+            ctx._check(lib.qgm_hits_ranks(ctx.h, h, C.c_void_p(ranks.ctypes.data)))
+            st = lib.qgm_hits_cigar(ctx.h, h, rd, R.h, band, max_ops, C.c_void_p(ops.ctypes.data),
+                                    C.c_void_p(info.ctypes.data))
+            if st != 0:  # a record needs more operations
+                max_ops = int(info["n_ops"].max())
+                ops = np.empty(n * max_ops, np.uint32)
+                ctx._check(lib.qgm_hits_cigar(ctx.h, h, rd, R.h, band, max_ops, C.c_void_p(ops.ctypes.data),
+                                              C.c_void_p(info.ctypes.data)))
+            kt = ctx.kernel_times(reset=True)
+        ctx.profile(False)
+        cig_ms = kt.get("k_cigar", (0.0, 1))[0]
+        return {"hits": n, "k_cigar_ms": round(cig_ms, 4), "cigar_hits_per_s": round(n / (cig_ms / 1e3), 1),
+                "cigar_ops_max": int(info["n_ops"].max()), "cigar_edits_mean": round(float(info["edits"].mean()), 3),
+                "rank_ms": round(sum(v[0] for k, v in kt.items() if k != "k_cigar"), 4)}
+    finally:
+        if h:
+            lib.qgm_hits_destroy(h)
+        lib.qgm_reads_destroy(rd)
 
 
 def cpu_baseline(args, cfg, ref, cb, codes, lengths, samples=1):

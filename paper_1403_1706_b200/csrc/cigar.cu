@@ -15,19 +15,21 @@
 //    with j >= 0 crosses column 0 at some row i0 having paid at least i0 =
 //    D[i0][0], so the extended DP equals the anchored one on j >= 0, and the
 //    band needs no infinity inside it;
-//  * every row's (Pv, Mv, D[i][0]) is kept in a per-thread scratch slot
-//    ([row][slot] layout, so a warp's row store is one contiguous segment;
-//    slots are reused by the grid-stride loop and stay L2-resident), and the
-//    traceback rebuilds D[i][t] = D[i][0] + popc(Pv & bits 1..t) -
-//    popc(Mv & bits 1..t) from them.
+//  * every row's diagonal steps D1 are kept in a per-thread scratch slot (one
+//    word per read row; [row][slot], reused by the grid-stride loop); the
+//    traceback decides each step on bits alone
+//    (see the kernel) and walks the row deltas Pv/Mv upwards by inverting
+//    the forward update.
 // A 64-bit band word covers B <= 32 (2W + 1 <= 63); B <= 64 uses 128 bits.
+#include <cstdlib>
+
 #include "internal.hpp"
 
 namespace qgm {
 namespace {
 
 // 128-bit band word as two u64 halves (add with carry; shifts by any amount)
-struct U128 {
+struct alignas(16) U128 {
   uint64_t lo = 0, hi = 0;
   __device__ U128() = default;
   __device__ U128(int v) : lo(uint64_t(int64_t(v))), hi(v < 0 ? ~0ull : 0ull) {}
@@ -88,13 +90,66 @@ struct CigarArgs {
   unsigned int* bad;   // set when a hit does not fit the reads / reference
 };
 
+// Sequential 2-bit base reader over a packed MSB-first stream: one word load
+// per 32 bases; dir = +1 ascending, -1 descending. Positions outside
+// [lo, hi) read as 4 (no match) and never load.
+struct BaseStream {
+  const uint64_t* w;
+  int32_t pos, lo, hi, dir, cur_word;
+  uint64_t cur;
+  __device__ __forceinline__ void init(const uint64_t* words, int32_t p, int32_t l, int32_t h, int32_t d) {
+    w = words;
+    pos = p;
+    lo = l;
+    hi = h;
+    dir = d;
+    cur_word = INT32_MIN;
+  }
+  template <bool kChecked>
+  __device__ __forceinline__ uint32_t next() {
+    const int32_t p = pos;
+    pos += dir;
+    if (kChecked && (p < lo || p >= hi)) return 4u;
+    const int32_t wi = p >> 5;
+    if (wi != cur_word) {
+      cur = __ldg(w + wi);
+      cur_word = wi;
+    }
+    return uint32_t(cur >> (62 - 2 * (p & 31))) & 3u;
+  }
+};
+
+// Random access to a packed MSB-first stream with the last word cached (the
+// traceback's positions move by at most one per step).
+struct CachedBases {
+  const uint64_t* w;
+  int32_t cw = INT32_MIN;
+  uint64_t cur = 0;
+  __device__ __forceinline__ uint32_t at(int32_t p) {
+    const int32_t wi = p >> 5;
+    if (wi != cw) {
+      cur = __ldg(w + wi);
+      cw = wi;
+    }
+    return uint32_t(cur >> (62 - 2 * (p & 31))) & 3u;
+  }
+};
+
 template <class T>
-__global__ void __launch_bounds__(128) k_cigar(CigarArgs a, T* __restrict__ sP, T* __restrict__ sM,
-                                               uint16_t* __restrict__ sS) {
+__device__ __forceinline__ uint32_t bit_at(const T& x, unsigned t) {
+  return uint32_t(x >> t) & 1u;
+}
+
+template <class T>
+__global__ void __launch_bounds__(128) k_cigar(CigarArgs a, T* __restrict__ rows_buf) {
   const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned W = a.W, top = 2 * W;
   const T one = T(1);
   const T mask = (one << (top + 1)) - one;
+  // row i >= 1's D1 at my_rows[(i - 1) * rstep]: [row][slot] scratch, so a
+  // warp's row store is one contiguous segment
+  T* const my_rows = rows_buf + slot;
+  const uint64_t rstep = a.nslots;
   for (uint64_t h = slot; h < a.n_hits; h += a.nslots) {
     const uint4 hit = __ldg(a.hits + h);
     const uint32_t r = hit.x, chrom = hit.y, strand = (hit.w >> 16) & 1u;
@@ -110,58 +165,51 @@ __global__ void __launch_bounds__(128) k_cigar(CigarArgs a, T* __restrict__ sP, 
       a.info[h] = make_uint2(hit.z, 0u);
       continue;
     }
-    const uint64_t gb = __ldg(a.cb + chrom);
-    const int64_t Lc = int64_t(__ldg(a.cb + chrom + 1) - gb);
-    const uint64_t* rw = a.read_words + uint64_t(r) * a.W_words;
-    auto read_base = [&](uint32_t i) -> uint32_t {  // oriented read base i
-      return strand ? 3u - base_at(rw, n - 1 - i) : base_at(rw, i);
-    };
-    auto ref_base = [&](int64_t x) -> uint32_t {  // chromosome position x; 4 = outside
-      return x >= 0 && x < Lc ? base_at(a.ref_words, gb + uint64_t(x)) : 4u;
-    };
+    const int64_t gb = int64_t(__ldg(a.cb + chrom));
+    const int64_t Lc = int64_t(__ldg(a.cb + chrom + 1)) - gb;
+    // chromosome positions are 32-bit offsets from the word holding its first
+    // base (chromosomes are < 2^31 bases; the reference may exceed 2^32)
+    const uint64_t* cw = a.ref_words + (uint64_t(gb) >> 5);
+    const int32_t c0 = int32_t(gb & 31);
+    // oriented read bases in order; the complement is applied below
+    BaseStream rd, rf;
+    {
+      const uint64_t* rw = a.read_words + uint64_t(r) * a.W_words;
+      if (strand) rd.init(rw, int32_t(n) - 1, 0, int32_t(n), -1);
+      else rd.init(rw, 0, 0, int32_t(n), 1);
+    }
+    // reference from chromosome position rs - W
+    rf.init(cw, c0 + int32_t(rs) - int32_t(W), c0, c0 + int32_t(Lc), 1);
     // ---- forward pass. Row 0 (extended): D[0][t] = |t - W|.
     T P = (mask >> (W + 1)) << (W + 1);  // +1 deltas at t in (W, 2W]
     T M = ((one << (W + 1)) - one) & ~one;  // -1 deltas at t in [1, W]
     uint32_t s0 = W;
-    auto store = [&](uint32_t i) {
-      const uint64_t o = uint64_t(i) * a.nslots + slot;
-      sP[o] = P;
-      sM[o] = M;
-      sS[o] = uint16_t(s0);
+    // band window of row 1 as bit planes (base bit 0, base bit 1, inside the
+    // chromosome): bit t <-> chromosome position rs - W + t; each slide
+    // shifts down and inserts the next position at the top
+    T pl = 0, ph = 0, pv = 0;
+    const T topbit = one << top;
+    auto slide = [&](uint32_t b) {
+      pl = (pl >> 1) | ((b & 1u) && b < 4u ? topbit : T(0));
+      ph = (ph >> 1) | ((b & 2u) && b < 4u ? topbit : T(0));
+      pv = (pv >> 1) | (b < 4u ? topbit : T(0));
     };
-    store(0);
-    // Eq masks of row 1: t <-> chromosome position rs - W + t
-    T m0 = 0, m1 = 0, m2 = 0, m3 = 0;
-    for (unsigned t = 0; t <= top; ++t) {
-      const uint32_t b = ref_base(rs - int64_t(W) + t);
-      const T bit = one << t;
-      m0 |= b == 0 ? bit : T(0);
-      m1 |= b == 1 ? bit : T(0);
-      m2 |= b == 2 ? bit : T(0);
-      m3 |= b == 3 ? bit : T(0);
-    }
+    for (unsigned t = 0; t <= top; ++t) slide(rf.next<true>());
     for (uint32_t i = 1; i <= n; ++i) {
-      const uint32_t c = read_base(i - 1);
-      const T Eq = c == 0 ? m0 : c == 1 ? m1 : c == 2 ? m2 : m3;
+      uint32_t c = rd.next<false>();
+      c = strand ? 3u - c : c;
+      const T Eq = ((c & 1u) ? pl : ~pl) & ((c & 2u) ? ph : ~ph) & pv;
       const T X = Eq | (M >> 1);
       const T Pp = P >> 1;
       const T Z = ((((X & Pp) + Pp) ^ Pp) | X) & mask;
       const T D1 = ~Z & mask;
       const T Bs = (D1 << 1) & mask;
       const T up = Bs & ~D1, dn = D1 & ~Bs, zr = ~(P | M);
-      const T nP = ((P & ~up) | (zr & dn)) & mask & ~one;
-      const T nM = ((M & ~dn) | (zr & up)) & mask & ~one;
-      P = nP;
-      M = nM;
+      P = ((P & ~up) | (zr & dn)) & mask & ~one;
+      M = ((M & ~dn) | (zr & up)) & mask & ~one;
       s0 += uint32_t(D1 & one);
-      store(i);
-      // slide the masks to row i + 1: the new top cell is position rs + i + W
-      const uint32_t b = ref_base(rs + int64_t(i) + W);
-      const T bit = one << top;
-      m0 = (m0 >> 1) | (b == 0 ? bit : T(0));
-      m1 = (m1 >> 1) | (b == 1 ? bit : T(0));
-      m2 = (m2 >> 1) | (b == 2 ? bit : T(0));
-      m3 = (m3 >> 1) | (b == 3 ? bit : T(0));
+      my_rows[uint64_t(i - 1) * rstep] = D1;  // what the traceback needs of row i
+      slide(rf.next<true>());  // row i + 1 looks one position further
     }
     // ---- end column: the largest j with minimal D[n][j], j in [jlo, jhi]
     const int64_t J = int64_t(n) + W;
@@ -173,14 +221,22 @@ __global__ void __launch_bounds__(128) k_cigar(CigarArgs a, T* __restrict__ sP, 
     {
       int v = int(s0);
       for (unsigned t = 0; t <= thi; ++t) {
-        if (t) v += int(uint32_t(P >> t) & 1u) - int(uint32_t(M >> t) & 1u);
+        if (t) v += int(bit_at(P, t)) - int(bit_at(M, t));
         if (t >= tlo && v <= best) {
           best = v;
           te = t;
         }
       }
     }
-    // ---- traceback from (n, te); ops are emitted from the end
+    // ---- traceback from (n, te) on bits only: with delta = D[i][t] -
+    // D[i-1][t] (the row's D1) and h = D[i-1][t+1] - D[i-1][t] (the deltas
+    // along t of row i-1, Pv/Mv),
+    //   M  iff  delta == mismatch(i, j)      (diagonal predecessor)
+    //   I  iff  delta == h + 1, t < 2W       (vertical predecessor (i-1, t+1))
+    //   D  otherwise                          (horizontal (i, t-1))
+    // Row i-1's Pv/Mv come from row i's by inverting the forward update with
+    // row i's D1, so only D1 is stored; the match bit is re-read from the
+    // bases (cached words: the positions move by at most one per step).
     uint32_t* out = a.ops + h * a.max_ops;
     uint32_t n_ops = 0, run_op = 3, run_len = 0;
     auto emit = [&](uint32_t op) {
@@ -195,14 +251,21 @@ __global__ void __launch_bounds__(128) k_cigar(CigarArgs a, T* __restrict__ sP, 
       run_op = op;
       run_len = 1;
     };
-    auto dval = [&](const T& p, const T& m, uint32_t s, unsigned t) -> int {
-      const T low = ((one << t) - one) << 1;  // bits 1..t
-      return int(s) + int(BandBits<T>::popc(p & low)) - int(BandBits<T>::popc(m & low));
+    CachedBases rb{a.read_words + uint64_t(r) * a.W_words}, fb{cw};
+    T rD1 = 0;  // row i
+    auto enter_row = [&](int64_t i) {  // row i >= 1; P/M become row i-1's deltas
+      rD1 = my_rows[uint64_t(i - 1) * rstep];
+      const T Bs = (rD1 << 1) & mask;
+      const T up = Bs & ~rD1, dn = rD1 & ~Bs, z = ~(P | M) & mask;
+      const T oP = ((P & ~dn) | (z & up)) & mask & ~one;
+      const T oM = ((M & ~up) | (z & dn)) & mask & ~one;
+      P = oP;
+      M = oM;
     };
     int64_t i = n;
     unsigned t = te;
-    int cur = best;
-    // a path has at most n + j_end steps; more means inconsistent DP rows
+    if (n > 0) enter_row(i);
+    // a path has at most n + j_end steps; more means inconsistent rows
     for (int64_t guard = int64_t(n) + J + 1;; --guard) {
       const int64_t j = i + int64_t(t) - int64_t(W);
       if (i == 0 && j == 0) break;
@@ -213,39 +276,36 @@ __global__ void __launch_bounds__(128) k_cigar(CigarArgs a, T* __restrict__ sP, 
       if (i == 0) {
         emit(2);
         --t;
-        --cur;
         continue;
       }
       if (j == 0) {
         emit(1);
         --i;
         ++t;
-        --cur;
         continue;
       }
-      const uint64_t o = uint64_t(i - 1) * a.nslots + slot;
-      const T pu = sP[o], mu = sM[o];
-      const uint32_t su = sS[o];
-      const int dd = dval(pu, mu, su, t);
-      if (dd + (read_base(uint32_t(i - 1)) == ref_base(rs + j - 1) ? 0 : 1) == cur) {
+      const uint32_t delta = bit_at(rD1, t);
+      const uint32_t rbase = strand ? 3u - rb.at(int32_t(n - i)) : rb.at(int32_t(i - 1));
+      const int64_t x = rs + j - 1;  // >= 0
+      const uint32_t mism = x < Lc ? uint32_t(rbase != fb.at(c0 + int32_t(x))) : 1u;
+      if (delta == mism) {
         emit(0);
-        cur = dd;
         --i;
+        if (i > 0) enter_row(i);
         continue;
       }
       if (t < top) {
-        const int vu = dval(pu, mu, su, t + 1);
-        if (vu + 1 == cur) {
+        const int hh = int(bit_at(P, t + 1)) - int(bit_at(M, t + 1));
+        if (int(delta) == hh + 1) {
           emit(1);
-          cur = vu;
           --i;
           ++t;
+          if (i > 0) enter_row(i);
           continue;
         }
       }
       emit(2);
       --t;
-      --cur;
     }
     // the last run emitted is the alignment's first; a leading D run moves the start
     uint32_t lead = 0;
@@ -272,6 +332,8 @@ void hits_cigar(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, const Reads& read
                 uint32_t max_ops, DBuf<uint32_t>& ops, DBuf<uint2>& info) {
   if (band == 0 || band > 64) throw InputError("band must be in [1, 64]");
   if (max_ops == 0) throw InputError("max_ops must be positive");
+  for (uint32_t k = 0; k < ref.n_chrom; ++k)
+    if (ref.cb[k + 1] - ref.cb[k] >= (uint64_t(1) << 31) - 64) throw InputError("cigar: chromosome of 2^31 bases or more");
   ops.alloc(c, std::max<uint64_t>(n * max_ops, 1));
   info.alloc(c, std::max<uint64_t>(n, 1));
   if (n == 0) return;
@@ -289,30 +351,29 @@ void hits_cigar(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, const Reads& read
   a.max_ops = max_ops;
   a.rows = reads.stride + 1;
   const bool wide = band > 32;
-  const size_t per_row = (wide ? 32 : 16) + 2;
-  // slots: enough warps per SM to hide the row recurrence, scratch bounded
-  // (kept near L2 size for 100 bp reads)
-  const uint64_t budget = uint64_t(256) << 20;
-  uint64_t blocks = std::min<uint64_t>(ceil_div(n, 128), uint64_t(kSMs) * 4);
-  blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, budget / (uint64_t(a.rows) * per_row * 128)));
-  a.nslots = uint32_t(blocks * 128);
-  DBuf<uint8_t> scratch(c, uint64_t(a.rows) * a.nslots * per_row + 64);
+  const size_t per_row = wide ? 16 : 8;  // one D1 word per read row
+  // 1024 threads per SM: the row recurrence is a dependent chain, occupancy
+  // hides it (C2, 1M hits: 4 CTAs of 128 per SM 1.98 ms, 8 CTAs 1.58 ms;
+  // shared-memory rows, which cap the SM at ~280 threads, 2.99 ms). Scratch
+  // bounded for long reads.
+  const uint32_t threads = 128;
+  uint64_t bps = 8;
+  if (const char* e = std::getenv("QGM_CIGAR_BPS")) bps = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+  const uint64_t budget = uint64_t(512) << 20;
+  uint64_t blocks = std::min<uint64_t>(ceil_div(n, threads), uint64_t(kSMs) * bps);
+  blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, budget / (uint64_t(a.rows) * per_row * threads)));
+  DBuf<uint8_t> scratch(c, uint64_t(a.rows) * blocks * threads * per_row + 64);
+  a.nslots = uint32_t(blocks * threads);
   DBuf<unsigned int> bad(c, 1);
   bad.zero();
   a.ops = ops.p;
   a.info = info.p;
   a.bad = bad.p;
-  const uint64_t cells = uint64_t(a.rows) * a.nslots;
   KernelScope ks(c, "k_cigar");
-  if (wide) {
-    auto* P = reinterpret_cast<U128*>(scratch.p);
-    QGM_KERNEL(c, k_cigar<U128>, unsigned(blocks), 128, 0, a, P, P + cells,
-               reinterpret_cast<uint16_t*>(P + 2 * cells));
-  } else {
-    auto* P = reinterpret_cast<uint64_t*>(scratch.p);
-    QGM_KERNEL(c, k_cigar<uint64_t>, unsigned(blocks), 128, 0, a, P, P + cells,
-               reinterpret_cast<uint16_t*>(P + 2 * cells));
-  }
+  if (wide)
+    QGM_KERNEL(c, k_cigar<U128>, unsigned(blocks), threads, 0, a, reinterpret_cast<U128*>(scratch.p));
+  else
+    QGM_KERNEL(c, k_cigar<uint64_t>, unsigned(blocks), threads, 0, a, reinterpret_cast<uint64_t*>(scratch.p));
   unsigned int h_bad = 0;
   QGM_CUDA(cudaMemcpyAsync(&h_bad, bad.p, 4, cudaMemcpyDeviceToHost, c.stream));
   QGM_CUDA(cudaStreamSynchronize(c.stream));

@@ -201,6 +201,7 @@ __global__ void k_ranks(const uint64_t* __restrict__ keys, const uint32_t* __res
 void hit_ranks(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, uint32_t n_reads, DBuf<uint32_t>& rank) {
   rank.alloc(c, std::max<uint64_t>(n, 1));
   if (n == 0) return;
+  KernelScope ks(c, "hit_rank");
   DBuf<uint64_t> keys(c, n), keys_alt;
   DBuf<uint32_t> idx(c, n), idx_alt;
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));

@@ -417,3 +417,24 @@ def test_cigar_spec_examples_on_device(ctx):
         h = np.zeros(1, qgm.HIT_DTYPE)
         ops, info = ctx.cigar(reads, R, h)
         assert qgm.cigar_string(ops[0], info["n_ops"][0]) == want and info["ref_start"][0] == start
+
+
+def test_cigar_long_reads_use_global_rows_and_match_oracle(ctx, oracle):
+    """Reads too long for the shared-memory rows (300 bp at B=64: 301 rows x
+    16 B x 32 threads > 113 KiB) take the global-scratch path; 500 bp at B=32
+    too."""
+    import paper_1403_1706_b200 as qgm
+    L = 300_000
+    ref = qgm.random_reference(51, L)
+    cb = np.array([0, 120_000, L], np.uint64)
+    for stride, band in ((300, 64), (500, 32), (300, 32)):
+        codes, lengths, *_ = qgm.simulate_reads(52 + stride, ref, cb, 300, stride, 0.04)
+        R = qgm.Reference.from_codes(ctx, ref, cb)
+        reads = qgm.Reads.from_codes(ctx, codes, lengths, stride)
+        hits, st = ctx.map(reads, R, q=14, mode=1, band_width=band, pct_identity=70)
+        assert hits.size > 200
+        ops, info = ctx.cigar(reads, R, hits, band_width=band)
+        wops, winfo = _oracle_cigar(oracle, ref, cb, codes, stride, lengths, hits, band)
+        assert np.array_equal(info, winfo), (stride, band)
+        m = np.arange(ops.shape[1])[None, :] < info["n_ops"][:, None]
+        assert np.array_equal(np.where(m, ops, 0), np.where(m, wops, 0)), (stride, band)
