@@ -4,8 +4,10 @@
 // C++ wrappers of include/qgm_c.h.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "qgmap/qgroup_index.hpp"
@@ -151,13 +153,63 @@ inline unsigned mapping_quality(std::uint32_t rank, std::uint64_t p_size) {
   return r < 0 ? 0u : unsigned(r);
 }
 
+// traceback_cigar (DESIGN.md Appendix B.8) of one record:
+// the alignment's start (leading deletions dropped), its edits and the CIGAR
+// as BAM-style ops (length << 4 | op, M = 0, I = 1, D = 2).
+struct Alignment {
+  std::uint32_t ref_start = 0;
+  std::uint16_t edits = 0;
+  std::vector<std::uint32_t> ops;
+  std::string cigar() const {
+    std::string o;
+    for (std::uint32_t x : ops) o += std::to_string(x >> 4) + "MID"[x & 15];
+    return o.empty() ? "*" : o;
+  }
+  std::uint32_t ref_span() const {  // reference bases consumed (M and D)
+    std::uint32_t s = 0;
+    for (std::uint32_t x : ops) s += (x & 15) != 1 ? x >> 4 : 0;
+    return s;
+  }
+};
+
+namespace detail {
+inline std::vector<Alignment> unpack_alignments(const std::vector<std::uint32_t>& ops,
+                                                const std::vector<qgm_cigar_info>& info, std::uint32_t max_ops) {
+  std::vector<Alignment> out(info.size());
+  for (std::size_t i = 0; i < info.size(); ++i) {
+    out[i].ref_start = info[i].ref_start;
+    out[i].edits = info[i].edits;
+    out[i].ops.assign(ops.begin() + std::ptrdiff_t(i * max_ops), ops.begin() + std::ptrdiff_t(i * max_ops + info[i].n_ops));
+  }
+  return out;
+}
+// Calls fn(max_ops, ops, info) until every record fits: the first try
+// assumes 2 * band + 16 operations (any hit the validation keeps at 80%
+// identity), a record needing more is retried once with enough.
+template <class Fn>
+std::vector<Alignment> run_cigar(const device::Context& ctx, std::uint64_t n, unsigned band, Fn&& fn) {
+  std::uint32_t max_ops = 2 * band + 16;
+  for (int attempt = 0;; ++attempt) {
+    std::vector<std::uint32_t> ops(std::max<std::uint64_t>(n * max_ops, 1));
+    std::vector<qgm_cigar_info> info(n);
+    const int st = fn(max_ops, ops.data(), info.data());
+    if (st == QGM_OK) return unpack_alignments(ops, info, max_ops);
+    std::uint32_t need = 0;
+    for (const auto& x : info) need = std::max<std::uint32_t>(need, x.n_ops);
+    if (st != QGM_ERR_INPUT || need <= max_ops || attempt > 0) ctx.check(st);
+    max_ops = need;
+  }
+}
+}  // namespace detail
+
 // One read buffer against the whole reference: index build, filtration,
 // candidate dedup, validation, dedup + strata -- all on the device. Output
 // sorted by (read, chrom, ref_start, strand); with `ranks`, also the
 // hit_rank R of every record.
 inline std::vector<MappedHit> map_reads_ranked(const DeviceReference& ref, const PackedReadText& text,
                                                const MapParams& p, qgm_map_stats* stats,
-                                               std::vector<std::uint32_t>* ranks) {
+                                               std::vector<std::uint32_t>* ranks,
+                                               std::vector<Alignment>* aligns = nullptr) {
   auto ctx = ref.context();
   auto reads = device::upload_reads(text, ctx);
   const qgm_map_params mp{p.q, p.group_width, p.sampled ? 1u : 0u, p.band.band_width, p.band.percent(),
@@ -176,6 +228,13 @@ inline std::vector<MappedHit> map_reads_ranked(const DeviceReference& ref, const
   if (ranks) {
     ranks->assign(n, 0);
     ctx->check(qgm_hits_ranks(ctx->get(), h, ranks->data()));
+  }
+  if (aligns) {  // CIGAR of every record while the reads are on the device
+    *aligns = detail::run_cigar(*ctx, n, p.band.band_width,
+                                [&](std::uint32_t max_ops, std::uint32_t* ops, qgm_cigar_info* info) {
+                                  return qgm_hits_cigar(ctx->get(), h, reads.get(), ref.get(), p.band.band_width,
+                                                        max_ops, ops, info);
+                                });
   }
   return out;
 }

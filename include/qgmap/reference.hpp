@@ -61,6 +61,13 @@ class DeviceReference {
   void mask_repeats(unsigned q, std::uint64_t threshold = 1000) {
     context()->check(qgm_ref_mask_repeats(context()->get(), get(), q, threshold));
   }
+  // |P| for q-grams of length q: unmasked positions of both strands (the
+  // P_size of mapping_quality).
+  std::uint64_t positions(unsigned q) const {
+    std::uint64_t n = 0;
+    context()->check(qgm_ref_positions(context()->get(), get(), q, &n));
+    return n;
+  }
   // The current mask, one byte per base (1 = not in P).
   std::vector<std::uint8_t> mask() const {
     const std::uint64_t total = chrom_begin_.back();

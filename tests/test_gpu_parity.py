@@ -18,7 +18,7 @@ from qgm_testutil import ROOT
 
 pytestmark = pytest.mark.gpu
 
-CPP = ["test_qgroup_index", "test_filter", "test_validate", "test_map"]
+CPP = ["test_qgroup_index", "test_filter", "test_validate", "test_map", "test_pipeline"]
 
 
 @pytest.mark.parametrize("name", CPP)
