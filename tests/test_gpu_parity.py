@@ -438,3 +438,28 @@ def test_cigar_long_reads_use_global_rows_and_match_oracle(ctx, oracle):
         assert np.array_equal(info, winfo), (stride, band)
         m = np.arange(ops.shape[1])[None, :] < info["n_ops"][:, None]
         assert np.array_equal(np.where(m, ops, 0), np.where(m, wops, 0)), (stride, band)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_reference_sharded_pieces_reproduce_the_whole_reference(ctx, mode):
+    """SURVEY 8(f) row 2 on one GPU: the shares of a 4-way reference split are
+    mapped one after another on the device (each rank's work), owned hits kept
+    and combined as the exchange step would (MIN of k per read, union): the
+    result equals mapping the whole reference."""
+    import paper_1403_1706_b200 as qgm
+    from paper_1403_1706_b200 import refshard
+    L = 400_000
+    ref = qgm.random_reference(61, L)
+    ref[300_000:300_500] = ref[50_000:50_500]
+    cb = np.array([0, 180_000, 180_300, L], np.uint64)
+    codes, lengths, *_ = qgm.simulate_reads(62, ref, cb, 5000, 100, 0.04)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    want, _ = ctx.map(reads, qgm.Reference.from_codes(ctx, ref, cb), q=14, mode=mode)
+    parts = []
+    for pieces in refshard.plan(cb, 4, 100, 32):
+        pc, pcb, _ = refshard.piece_reference(ref, cb, pieces)
+        local, _ = ctx.map(reads, qgm.Reference.from_codes(ctx, pc, pcb), q=14, mode=1)
+        parts.append(refshard.own_and_translate(local, pieces))
+    got = refshard.combine(np.concatenate(parts), lengths.size, mode)
+    assert got.size == want.size and got.size > 4000
+    assert np.array_equal(got, want)
