@@ -10,7 +10,7 @@ import sys
 def main():
     rep, kern = sys.argv[1], sys.argv[2]
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-    out = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kern, "--page", "source", "--csv", "--print-source",
+    out = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kern, "-c", "1", "--page", "source", "--csv", "--print-source",
                           "cuda,sass"], capture_output=True, text=True).stdout
     res, fname, hdr = [], "?", None
     for row in csv.reader(io.StringIO(out)):
