@@ -196,12 +196,46 @@ __global__ void k_ranks(const uint64_t* __restrict__ keys, const uint32_t* __res
   }
 }
 
+// hit-rank straight from the output order: the records of a read are
+// contiguous (strata emits them read by read), so a record's rank is a count
+// over its own run. Runs longer than kRankRun set *long_run and are left to
+// the sorted path.
+constexpr uint32_t kRankRun = 64;
+__global__ void k_rank_runs(const uint4* __restrict__ hits, uint64_t n, uint32_t* __restrict__ rank,
+                            unsigned int* __restrict__ long_run) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint4 h = __ldg(hits + i);
+    const uint32_t e = h.w & 0xFFFFu;
+    uint64_t lo = i, hi = i + 1;
+    while (lo > 0 && i - lo < kRankRun && __ldg(&hits[lo - 1].x) == h.x) --lo;
+    while (hi < n && hi - i < kRankRun && __ldg(&hits[hi].x) == h.x) ++hi;
+    if (i - lo == kRankRun || hi - i == kRankRun) {
+      atomicOr(long_run, 1u);
+      continue;
+    }
+    uint32_t c = 0;
+    for (uint64_t j = lo; j < hi; ++j) c += (__ldg(&hits[j].w) & 0xFFFFu) <= e;
+    rank[i] = c;
+  }
+}
+
 }  // namespace
 
 void hit_ranks(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, uint32_t n_reads, DBuf<uint32_t>& rank) {
   rank.alloc(c, std::max<uint64_t>(n, 1));
   if (n == 0) return;
   KernelScope ks(c, "hit_rank");
+  {
+    DBuf<unsigned int> long_run(c, 1);
+    long_run.zero();
+    const unsigned g = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
+    QGM_KERNEL(c, k_rank_runs, g, 256, 0, reinterpret_cast<const uint4*>(hits.p), n, rank.p, long_run.p);
+    unsigned int h_long = 0;
+    QGM_CUDA(cudaMemcpyAsync(&h_long, long_run.p, 4, cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    if (!h_long) return;
+  }
+  // a read with more than kRankRun records: sort (read, edits) keys
   DBuf<uint64_t> keys(c, n), keys_alt;
   DBuf<uint32_t> idx(c, n), idx_alt;
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));

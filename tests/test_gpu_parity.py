@@ -338,6 +338,22 @@ def test_hit_rank_and_mapq(ctx):
     assert np.all(mq[rank == 1] == 255) and np.all(mq[rank > 1] < 255)
     true = np.abs(hits["ref_start"].astype(np.int64) - tp[hits["read_id"]].astype(np.int64)) <= 8
     assert true[rank == 1].mean() > true[rank > 1].mean()
+    # both device paths: runs of <= 64 records per read counted in place, and
+    # the sorted fallback once one read has more
+    assert np.bincount(hits["read_id"]).max() > 64
+    for L2, n2 in ((200_000, 3000), (30_000, 500)):
+        ref2 = qgm.random_reference(83, L2)
+        ref2[10_000:10_100] = ref2[20_000:20_100]
+        cb2 = np.array([0, L2], np.uint64)
+        codes2, lengths2, *_ = qgm.simulate_reads(84, ref2, cb2, n2, 100, 0.03)
+        h2, _, r2 = ctx.map(qgm.Reads.from_codes(ctx, codes2, lengths2, 100), qgm.Reference.from_codes(ctx, ref2, cb2),
+                            q=12, mode=1, pct_identity=50, ranks=True)
+        w2 = np.zeros(h2.size, np.uint32)
+        for r in np.unique(h2["read_id"]):
+            idx = np.nonzero(h2["read_id"] == r)[0]
+            ed = h2["edits"][idx]
+            w2[idx] = (ed[None, :] <= ed[:, None]).sum(1)
+        assert np.array_equal(r2, w2)
 
 
 def _oracle_cigar(oracle, ref, cb, codes, stride, lengths, hits, band):
