@@ -79,6 +79,8 @@ struct CigarArgs {
   const uint32_t* lengths;
   uint32_t n_reads, W_words;
   const uint64_t* ref_words;
+  const uint2* ref_planes;  // {lo, hi} bit planes, planes[k + 2] = word k, bit 31 - j = base 32k + j
+  uint64_t n_planes;
   const uint64_t* cb;  // chromosome begins (n_chrom + 1)
   uint32_t n_chrom;
   unsigned W;          // band half-width = B - 1
@@ -95,41 +97,62 @@ struct CigarArgs {
 // [lo, hi) read as 4 (no match) and never load.
 struct BaseStream {
   const uint64_t* w;
-  int32_t pos, lo, hi, dir, cur_word;
-  uint64_t cur;
+  int32_t pos, lo, hi, dir, cur_word, wlo, whi;
+  uint64_t cur, nxt;
+  __device__ __forceinline__ uint64_t load(int32_t wi) const { return wi >= wlo && wi <= whi ? __ldg(w + wi) : 0ull; }
+  // the word after the current one (in the walk's direction) is always in
+  // flight: a lane crossing a word boundary never waits for memory (lanes of
+  // a warp cross at different steps, so a blocking reload would stall the
+  // warp about every step)
   __device__ __forceinline__ void init(const uint64_t* words, int32_t p, int32_t l, int32_t h, int32_t d) {
     w = words;
     pos = p;
     lo = l;
     hi = h;
     dir = d;
-    cur_word = INT32_MIN;
+    wlo = l >> 5;
+    whi = (h - 1) >> 5;
+    cur_word = p >> 5;
+    cur = load(cur_word);
+    nxt = load(cur_word + d);
   }
   template <bool kChecked>
   __device__ __forceinline__ uint32_t next() {
     const int32_t p = pos;
     pos += dir;
-    if (kChecked && (p < lo || p >= hi)) return 4u;
     const int32_t wi = p >> 5;
-    if (wi != cur_word) {
-      cur = __ldg(w + wi);
+    if (wi != cur_word) {  // one word further in the walk's direction
+      cur = nxt;
       cur_word = wi;
+      nxt = load(wi + dir);
     }
+    if (kChecked && (p < lo || p >= hi)) return 4u;
     return uint32_t(cur >> (62 - 2 * (p & 31))) & 3u;
   }
 };
 
-// Random access to a packed MSB-first stream with the last word cached (the
-// traceback's positions move by at most one per step).
-struct CachedBases {
+// The traceback's positions in a stream only move one way (by 0 or 1 per
+// step); the same two-word window, advanced on demand.
+struct BackBases {
   const uint64_t* w;
-  int32_t cw = INT32_MIN;
-  uint64_t cur = 0;
+  int32_t dir, cur_word, wlo, whi;
+  uint64_t cur, nxt;
+  __device__ __forceinline__ uint64_t load(int32_t wi) const { return wi >= wlo && wi <= whi ? __ldg(w + wi) : 0ull; }
+  __device__ __forceinline__ void init(const uint64_t* words, int32_t p, int32_t l, int32_t h, int32_t d) {
+    w = words;
+    dir = d;
+    wlo = l >> 5;
+    whi = (h - 1) >> 5;
+    cur_word = p >> 5;
+    cur = load(cur_word);
+    nxt = load(cur_word + d);
+  }
   __device__ __forceinline__ uint32_t at(int32_t p) {
     const int32_t wi = p >> 5;
-    if (wi != cw) {
-      cur = __ldg(w + wi);
-      cw = wi;
+    if (wi != cur_word) {
+      cur = wi == cur_word + dir ? nxt : load(wi);
+      cur_word = wi;
+      nxt = load(wi + dir);
     }
     return uint32_t(cur >> (62 - 2 * (p & 31))) & 3u;
   }
@@ -178,8 +201,8 @@ __global__ void __launch_bounds__(128) k_cigar(CigarArgs a, T* __restrict__ rows
       if (strand) rd.init(rw, int32_t(n) - 1, 0, int32_t(n), -1);
       else rd.init(rw, 0, 0, int32_t(n), 1);
     }
-    // reference from chromosome position rs - W
-    rf.init(cw, c0 + int32_t(rs) - int32_t(W), c0, c0 + int32_t(Lc), 1);
+    // reference bases slid into the band, from chromosome position rs + W + 1
+    rf.init(cw, c0 + int32_t(rs) + int32_t(W) + 1, c0, c0 + int32_t(Lc), 1);
     // ---- forward pass. Row 0 (extended): D[0][t] = |t - W|.
     T P = (mask >> (W + 1)) << (W + 1);  // +1 deltas at t in (W, 2W]
     T M = ((one << (W + 1)) - one) & ~one;  // -1 deltas at t in [1, W]
@@ -187,14 +210,38 @@ __global__ void __launch_bounds__(128) k_cigar(CigarArgs a, T* __restrict__ rows
     // band window of row 1 as bit planes (base bit 0, base bit 1, inside the
     // chromosome): bit t <-> chromosome position rs - W + t; each slide
     // shifts down and inserts the next position at the top
-    T pl = 0, ph = 0, pv = 0;
+    T pl, ph, pv;
+    {  // row 1's window straight from the reference bit planes
+      const int64_t g0 = gb + rs - int64_t(W);  // >= -63: the planes have two zero words in front
+      const int64_t k0 = g0 >> 5;
+      const unsigned off = unsigned(g0 & 31);
+      auto word = [&](int64_t k, bool hi) -> uint64_t {
+        const int64_t x = min(max(k + 2, int64_t(0)), int64_t(a.n_planes) - 1);
+        const uint2 v = __ldg(a.ref_planes + x);
+        return __brev(hi ? v.y : v.x);
+      };
+      auto bits64 = [&](int64_t k, bool hi) -> uint64_t {  // plane bits [32k + off, 32k + off + 64)
+        const uint64_t lo = word(k, hi) | (word(k + 1, hi) << 32);
+        return off ? (lo >> off) | (word(k + 2, hi) << (64 - off)) : lo;
+      };
+      if constexpr (sizeof(T) == 8) {
+        pl = T(bits64(k0, false)) & mask;
+        ph = T(bits64(k0, true)) & mask;
+      } else {
+        pl = T(bits64(k0, false), bits64(k0 + 2, false)) & mask;
+        ph = T(bits64(k0, true), bits64(k0 + 2, true)) & mask;
+      }
+      // inside the chromosome: t in [max(0, W - rs), min(2W + 1, Lc - rs + W))
+      const unsigned tl = unsigned(max(int64_t(0), int64_t(W) - rs));
+      const unsigned th = unsigned(min(int64_t(top) + 1, Lc - rs + int64_t(W)));
+      pv = th > tl ? (((one << th) - one) & ~((one << tl) - one)) : T(0);
+    }
     const T topbit = one << top;
     auto slide = [&](uint32_t b) {
       pl = (pl >> 1) | ((b & 1u) && b < 4u ? topbit : T(0));
       ph = (ph >> 1) | ((b & 2u) && b < 4u ? topbit : T(0));
       pv = (pv >> 1) | (b < 4u ? topbit : T(0));
     };
-    for (unsigned t = 0; t <= top; ++t) slide(rf.next<true>());
     for (uint32_t i = 1; i <= n; ++i) {
       uint32_t c = rd.next<false>();
       c = strand ? 3u - c : c;
@@ -251,10 +298,17 @@ __global__ void __launch_bounds__(128) k_cigar(CigarArgs a, T* __restrict__ rows
       run_op = op;
       run_len = 1;
     };
-    CachedBases rb{a.read_words + uint64_t(r) * a.W_words}, fb{cw};
-    T rD1 = 0;  // row i
+    // read bases walk down (forward strand) or up (reverse strand: raw
+    // index n - i), the reference down from the end column
+    BackBases rb, fb;
+    rb.init(a.read_words + uint64_t(r) * a.W_words, strand ? 0 : int32_t(n) - 1, 0, int32_t(n),
+            strand ? 1 : -1);
+    fb.init(cw, c0 + int32_t(rs + (int64_t(n) + int64_t(te) - int64_t(W)) - 1), c0, c0 + int32_t(Lc), -1);
+    T rD1 = 0, pre = 0;  // row i, and row i - 1 already in flight
+    auto row_at = [&](int64_t i) { return i >= 1 ? my_rows[uint64_t(i - 1) * rstep] : T(0); };
     auto enter_row = [&](int64_t i) {  // row i >= 1; P/M become row i-1's deltas
-      rD1 = my_rows[uint64_t(i - 1) * rstep];
+      rD1 = pre;
+      pre = row_at(i - 1);
       const T Bs = (rD1 << 1) & mask;
       const T up = Bs & ~rD1, dn = rD1 & ~Bs, z = ~(P | M) & mask;
       const T oP = ((P & ~dn) | (z & up)) & mask & ~one;
@@ -264,6 +318,7 @@ __global__ void __launch_bounds__(128) k_cigar(CigarArgs a, T* __restrict__ rows
     };
     int64_t i = n;
     unsigned t = te;
+    pre = row_at(i);
     if (n > 0) enter_row(i);
     // a path has at most n + j_end steps; more means inconsistent rows
     for (int64_t guard = int64_t(n) + J + 1;; --guard) {
@@ -345,6 +400,8 @@ void hits_cigar(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, const Reads& read
   a.n_reads = reads.n;
   a.W_words = reads.W;
   a.ref_words = ref.words.p;
+  a.ref_planes = ref.planes.p;
+  a.n_planes = ref.planes.n;
   a.cb = ref.d_cb.p;
   a.n_chrom = ref.n_chrom;
   a.W = band - 1;
