@@ -363,14 +363,17 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
       mbar_wait(&s_bar, phase);
       phase ^= 1u;
     }
-    const uint32_t* S1p = staged ? sS1 - sA : a.S1;
-    const uint32_t* Op = staged ? sO - oA : a.O;
     // the sub-bin's items split evenly over the warps (no warp idles at the
     // end-of-sub-bin barrier while another runs a second full round)
     const uint32_t nitems = b1 - b0;
     const uint32_t my_lo = b0 + uint32_t(uint64_t(nitems) * wid / kJoinWarps);
     const uint32_t my_hi = b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kJoinWarps);
-    join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi, L);
+    if (staged) {  // S'/O accesses from shared-derived pointers only: LDS
+      join_items<kRunStart, kPacked>(a, sI, sR, sS1 - sA, sO - oA, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi,
+                                     L);
+    } else {
+      join_items<kRunStart, kPacked>(a, sI, sR, a.S1, a.O, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi, L);
+    }
     __syncthreads();  // the staging buffers are rewritten for the next sub-bin
   }
   join_stats(a, L);
@@ -514,14 +517,22 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
     uint16_t* sR;
     uint64_t* sIt;
     stage(s, sI, sR, sS1, sO, sIt);
-    const uint32_t* S1p = M.staged ? sS1 - M.sA : a.S1;
-    const uint32_t* Op = M.staged ? sO - M.oA : a.O;
-    const uint64_t* Ip = M.items_staged ? sIt - M.iA : a.items;
     const uint32_t w0 = uint32_t((uint64_t(M.sb) << a.code_shift) >> 5);
     const uint32_t nitems = M.b1 - M.b0;
     const uint32_t my_lo = M.b0 + uint32_t(uint64_t(nitems) * wid / kWsCons);
     const uint32_t my_hi = M.b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kWsCons);
-    join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, Ip, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
+    if (M.staged && M.items_staged) {
+      // everything in shared memory: pointers derived from the shared
+      // buffers only, so every access compiles to LDS (no generic LD and its
+      // 64-bit address arithmetic)
+      join_items<kRunStart, kPacked>(a, sI, sR, sS1 - M.sA, sO - M.oA, sIt - M.iA, M.d0, w0, M.sb << a.code_shift,
+                                     my_lo, my_hi, L);
+    } else {
+      const uint32_t* S1p = M.staged ? sS1 - M.sA : a.S1;
+      const uint32_t* Op = M.staged ? sO - M.oA : a.O;
+      const uint64_t* Ip = M.items_staged ? sIt - M.iA : a.items;
+      join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, Ip, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
