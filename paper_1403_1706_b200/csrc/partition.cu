@@ -249,11 +249,13 @@ struct Refine {
   __device__ __forceinline__ uint32_t key(uint64_t it, uint32_t bin) const {
     return (bin << (shift - kshift)) | (uint32_t(it >> kP1CodeShift) >> kshift);
   }
-  __device__ __forceinline__ uint64_t convert(uint64_t it) const {
+  // uniform: every read of the batch has length `stride` (the usual case;
+  // read once per CTA from lens)
+  __device__ __forceinline__ uint64_t convert(uint64_t it, bool uniform) const {
     const uint32_t pp = uint32_t(it);
     const uint32_t r = by_stride.div(pp), o = pp - r * stride;
     // every read of the batch has length `stride` (the usual case): no load
-    const uint32_t n = ~__ldg(lens + 1) == stride ? stride : __ldg(lengths + r);
+    const uint32_t n = uniform ? stride : __ldg(lengths + r);
     const uint32_t tail = min(n - q - o, kItemTailMax);
     const uint32_t lmask = kshift ? (1u << kshift) - 1u : 0u;
     return (uint64_t(uint32_t(it >> kP1CodeShift) & lmask) << kItemCodeShift) |
@@ -271,14 +273,18 @@ __device__ __forceinline__ uint32_t bin_search(const uint32_t* sboff, uint32_t n
   return lo;
 }
 
-// first and last P1 bin of every P2 chunk (bfirst | blast << 16), so that the
-// scatter threads do not each binary-search the bin offsets
-__global__ void k_chunk_bins(const uint32_t* __restrict__ boff, uint32_t nbins, uint32_t n,
-                             uint32_t* __restrict__ chunk_bins) {
+// per P2 chunk: {first P1 bin | last P1 bin << 16, first key of the
+// chunk's key window, window width}, so a scatter CTA starts a chunk without
+// a dependent load or a binary search
+__global__ void k_chunk_info(const uint64_t* __restrict__ in, uint32_t n, const uint32_t* __restrict__ boff,
+                             Refine rf, unsigned sub, uint4* __restrict__ info) {
   const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
   for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < n_chunks; ch += gridDim.x * blockDim.x) {
     const uint32_t c0 = ch * kChunk, c1 = min(n, c0 + kChunk);
-    chunk_bins[ch] = bin_search(boff, nbins, c0) | (bin_search(boff, nbins, c1 - 1) << 16);
+    const uint32_t bfirst = bin_search(boff, rf.nbins, c0), blast = bin_search(boff, rf.nbins, c1 - 1);
+    const uint32_t base = (rf.key(in[c0], bfirst) >> sub) << sub;
+    const uint32_t width = (((rf.key(in[c1 - 1], blast) >> sub) + 1) << sub) - base;
+    info[ch] = make_uint4(bfirst | (blast << 16), base, width, 0u);
   }
 }
 
@@ -286,7 +292,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
                                                                     const uint32_t* __restrict__ boff, Refine rf,
                                                                     unsigned sub, const uint32_t* __restrict__ off,
                                                                     uint32_t* __restrict__ cursor,
-                                                                    const uint32_t* __restrict__ chunk_bins,
+                                                                    const uint4* __restrict__ chunk_info,
                                                                     uint64_t* __restrict__ out) {
   extern __shared__ uint64_t stage[];  // kChunk join items, then kChunk u16 window keys
   uint16_t* skey = reinterpret_cast<uint16_t*>(stage + kChunk);
@@ -296,23 +302,27 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
   for (uint32_t b = threadIdx.x; b <= rf.nbins; b += kPartThreads) sboff[b] = boff[b];
   __syncthreads();
   const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
+  const bool uniform = ~__ldg(rf.lens + 1) == rf.stride;
+  uint4 ci_next = blockIdx.x < n_chunks ? __ldg(chunk_info + blockIdx.x) : make_uint4(0, 0, 0, 0);
   for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
     const uint32_t c0 = ch * kChunk, c1 = min(n, c0 + kChunk);
-    if (threadIdx.x == 0 && ch + gridDim.x < n_chunks) {  // next chunk -> L2 while this one is sorted
-      const uint32_t n0 = c0 + gridDim.x * kChunk, n1 = min(n, n0 + kChunk);
-      bulk_prefetch_l2(in + n0, ((n1 - n0) * 8u) & ~15u);
+    const uint4 ci = ci_next;
+    if (ch + gridDim.x < n_chunks) {  // next chunk: its info one iteration ahead, its items -> L2
+      ci_next = __ldg(chunk_info + ch + gridDim.x);
+      if (threadIdx.x == 0) {
+        const uint32_t n0 = c0 + gridDim.x * kChunk, n1 = min(n, n0 + kChunk);
+        bulk_prefetch_l2(in + n0, ((n1 - n0) * 8u) & ~15u);
+      }
     }
-    const uint32_t cb = __ldg(chunk_bins + ch);
-    const uint32_t bfirst = cb & 0xFFFFu, blast = cb >> 16;
-    const uint32_t base = (rf.key(in[c0], bfirst) >> sub) << sub;
-    const uint32_t width = (((rf.key(in[c1 - 1], blast) >> sub) + 1) << sub) - base;
+    const uint32_t bfirst = ci.x & 0xFFFFu, blast = ci.x >> 16;
+    const uint32_t base = ci.y, width = ci.z;
     uint32_t b = bfirst;
     if (width > kLocal) {
       for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) {
         while (sboff[b + 1] <= i) ++b;
         const uint64_t it = in[i];
         const uint32_t k = rf.key(it, b);
-        out[off[k] + atomicAdd(cursor + k, 1u)] = rf.convert(it);
+        out[off[k] + atomicAdd(cursor + k, 1u)] = rf.convert(it, uniform);
       }
       continue;
     }
@@ -331,7 +341,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
       if (i < c1 && bfirst != blast)
         while (sboff[b + 1] <= i) ++b;
       kk[k] = i < c1 ? rf.key(v[k], b) - base : ~0u;
-      v[k] = rf.convert(v[k]);
+      v[k] = rf.convert(v[k], uniform);
       if (i < c1) atomicAdd(cnt + kk[k], 1u);
     }
     __syncthreads();
@@ -468,12 +478,12 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   const size_t smem2 = kChunk * (sizeof(uint64_t) + sizeof(uint16_t));
   QGM_CUDA(cudaFuncSetAttribute(k_refine_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
   const uint32_t n_chunks2 = uint32_t(ceil_div(V, kChunk));
-  DBuf<uint32_t> chunk_bins(c, n_chunks2);
-  QGM_KERNEL(c, k_chunk_bins, unsigned(ceil_div(n_chunks2, 256)), 256, 0, out.boff.p, 1u << bits, V, chunk_bins.p);
+  DBuf<uint4> chunk_info(c, n_chunks2);
+  QGM_KERNEL(c, k_chunk_info, unsigned(ceil_div(n_chunks2, 256)), 256, 0, p1.p, V, out.boff.p, rf, sub, chunk_info.p);
   {
     KernelScope ks(c, "k_refine_scatter");
     QGM_KERNEL(c, k_refine_scatter, grid2, kPartThreads, smem2, p1.p, V, out.boff.p, rf, sub, out.soff.p, h2.p,
-               chunk_bins.p, out.pairs.p);
+               chunk_info.p, out.pairs.p);
   }
 }
 
