@@ -428,6 +428,7 @@ void qgm_ctx_destroy(qgm_ctx* ctx) {
   for (auto e : ctx->c.ev_pool) cudaEventDestroy(e);
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
   if (ctx->c.copy_stream) cudaStreamDestroy(ctx->c.copy_stream);
+  if (ctx->c.d2h_stream) cudaStreamDestroy(ctx->c.d2h_stream);
   delete ctx;
 }
 
@@ -1018,7 +1019,8 @@ int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, c
     activate(ctx);
     qgm::Ctx& c = ctx->c;
     if (!c.copy_stream) QGM_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
-    const cudaStream_t cs = c.copy_stream;
+    if (!c.d2h_stream) QGM_CUDA(cudaStreamCreateWithFlags(&c.d2h_stream, cudaStreamNonBlocking));
+    const cudaStream_t cs = c.copy_stream, ds = c.d2h_stream;
     for (auto& s : slot) QGM_CUDA(cudaEventCreateWithFlags(&s.h2d, cudaEventDisableTiming));
     for (auto& p : pend) {
       QGM_CUDA(cudaEventCreateWithFlags(&p.comp, cudaEventDisableTiming));
@@ -1064,10 +1066,10 @@ int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, c
       if (p.h.n > b.cap) {
         overflow = 1;
       } else if (p.h.n) {
-        QGM_CUDA(cudaStreamWaitEvent(cs, p.comp, 0));
-        QGM_CUDA(cudaMemcpyAsync(b.out, p.h.hits.p, p.h.n * 16, cudaMemcpyDeviceToHost, cs));
+        QGM_CUDA(cudaStreamWaitEvent(ds, p.comp, 0));
+        QGM_CUDA(cudaMemcpyAsync(b.out, p.h.hits.p, p.h.n * 16, cudaMemcpyDeviceToHost, ds));
       }
-      QGM_CUDA(cudaEventRecord(p.done, cs));
+      QGM_CUDA(cudaEventRecord(p.done, ds));
     };
     if (n_batches) h2d(0);
     for (uint32_t i = 0; i < n_batches; ++i) {
@@ -1126,9 +1128,11 @@ int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, c
     }
     if (n_batches) d2h(n_batches - 1);
     QGM_CUDA(cudaStreamSynchronize(cs));
+    QGM_CUDA(cudaStreamSynchronize(ds));
     QGM_CUDA(cudaStreamSynchronize(c.stream));
   });
   if (ctx->c.copy_stream) cudaStreamSynchronize(ctx->c.copy_stream);
+  if (ctx->c.d2h_stream) cudaStreamSynchronize(ctx->c.d2h_stream);
   cudaStreamSynchronize(ctx->c.stream);
   for (auto& p : pend) {
     p.h = qgm::HitsObj();

@@ -24,7 +24,9 @@ struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  cudaStream_t copy_stream = nullptr;  // H2D / D2H of qgm_map_host_batches (created on first use)
+  cudaStream_t copy_stream = nullptr;  // H2D of qgm_map_host_batches (created on first use)
+  cudaStream_t d2h_stream = nullptr;   // its D2H: a second stream, so uploads and downloads
+                                       // use separate copy engines and overlap each other
   uint64_t last_raw_candidates = 0;    // sizes the next batch's candidate buffer
   std::string err;
   uint64_t launches = 0;
