@@ -248,6 +248,8 @@ static void check_reads_shape(uint32_t n_reads, uint32_t stride) {
 // compute-bound validation (and the strata) rather than the L2-sensitive
 // partition and join (QGM_HOOK=0/1/2: after the join / the dedup / the
 // validation, measured within noise of each other).
+constexpr uint64_t kDedupDirectMax = uint64_t(10) << 20;  // raw keys whose hash table (<= 16M slots) stays L2-resident
+
 static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_map_params& P,
                          const std::function<void()>& after_filter = {}) {
   if (P.q == 0 || P.q > 16) throw InputError("q must be in [1, 16]");
@@ -301,9 +303,28 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   // trip between dedup, validation and the strata's per-read counts)
   DBuf<unsigned long long> cnt(c, 3);
   cnt.zero();
+  // Candidate dedup only pays when the set has duplicates to remove: above
+  // ~10M keys the hash table leaves L2 (C3: 7.6 ms of atomics in DRAM for 1%
+  // duplicates), so a large set is first sampled and deduplicated only if
+  // more than 10% of it repeats. Skipping it cannot change a hit: validation
+  // is a pure function of the key and the strata keep one hit per (read,
+  // chromosome, start, strand). unique_candidates then reports the raw count.
+  bool dedup = true;
+  uint64_t direct_max = kDedupDirectMax;
+  if (const char* e = std::getenv("QGM_DEDUP_DIRECT_MAX")) direct_max = std::strtoull(e, nullptr, 10);  // tests
+  if (n_raw > direct_max) {
+    StageScope s(c, kStageSort);
+    dedup = estimate_dup_fraction(c, keys.p, n_raw, ref.diag_bits + 1) > 0.10;
+  }
   {
     StageScope s(c, kStageSort);
-    dedup_keys_async(c, keys.p, n_raw, alt, cnt.p + 1);  // unique candidates, any order (validation is per key)
+    if (dedup) {
+      dedup_keys_async(c, keys.p, n_raw, alt, cnt.p + 1);  // unique candidates, any order (validation is per key)
+    } else {
+      alt.swap(keys);
+      const unsigned long long nr = n_raw;
+      QGM_CUDA(cudaMemcpyAsync(cnt.p + 1, &nr, sizeof(nr), cudaMemcpyHostToDevice, c.stream));
+    }
   }
   if (after_filter && hook_at == 1) after_filter();
   const uint64_t n_bound = std::max<uint64_t>(n_raw, 1);

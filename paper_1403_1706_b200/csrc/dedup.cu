@@ -71,6 +71,19 @@ __global__ void k_store_count(const uint32_t* __restrict__ total, unsigned long 
   *out = *total;
 }
 
+// keys of every (mask+1)-th read (read id = key >> rshift) appended to out
+__global__ void k_sample_reads(const uint64_t* __restrict__ keys, uint64_t n, unsigned rshift, uint64_t mask,
+                               uint64_t* __restrict__ out, unsigned long long* __restrict__ n_out) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * uint64_t(blockDim.x); i0 < n; i0 += stride) {  // warp-uniform trip count
+    const uint64_t i = i0 + threadIdx.x;
+    const uint64_t k = i < n ? keys[i] : 0ull;
+    const bool take = i < n && ((k >> rshift) & mask) == 0;
+    const unsigned long long at = warp_append(take, n_out);
+    if (take) out[at] = k;
+  }
+}
+
 }  // namespace
 
 void dedup_keys_async(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out, unsigned long long* d_count) {
@@ -118,6 +131,27 @@ uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& ou
   if (out.n < h) out.alloc(c, std::max<uint64_t>(h, 1));
   QGM_KERNEL(c, k_tile_emit, tiles, kDedupThreads, 0, table.p, counts.p, out.p);
   return h;
+}
+
+// Duplicate fraction 1 - unique/raw of a candidate set, estimated from the
+// keys of every 64th read: duplicates are (read, strand, diagonal) repeats of
+// one read, so a read sample keeps their rate. One pass over the keys, a small
+// (L2-resident) hash of the sample, one host round trip.
+double estimate_dup_fraction(Ctx& c, const uint64_t* keys, uint64_t n, unsigned rshift) {
+  if (n == 0) return 0.0;
+  const uint64_t cap = n / 16 + 4096;  // expected n / 64
+  DBuf<uint64_t> sample(c, cap);
+  DBuf<unsigned long long> ns(c, 1);
+  ns.zero();
+  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
+  QGM_KERNEL(c, k_sample_reads, grid, 256, 0, keys, n, rshift, 63ull, sample.p, ns.p);
+  unsigned long long m = 0;
+  QGM_CUDA(cudaMemcpyAsync(&m, ns.p, sizeof(m), cudaMemcpyDeviceToHost, c.stream));
+  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  if (m == 0 || m > cap) return 1.0;  // no usable sample: assume duplicates (keep the dedup)
+  DBuf<uint64_t> uniq;
+  const uint64_t u = dedup_keys(c, sample.p, m, uniq);
+  return 1.0 - double(u) / double(m);
 }
 
 }  // namespace qgm

@@ -265,6 +265,8 @@ uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& ou
 // Same without a host round trip: `out` is sized n (the bound) and the unique
 // count lands in d_count (device).
 void dedup_keys_async(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out, unsigned long long* d_count);
+// Estimated duplicate fraction of a candidate set (keys of every 64th read).
+double estimate_dup_fraction(Ctx& c, const uint64_t* keys, uint64_t n, unsigned rshift);
 
 // radix_sort.cu -- stable LSD radix sort of u64 keys (+ optional u32 values)
 // on bits [begin_bit, end_bit). Sorted data ends up in keys/vals (buffers may

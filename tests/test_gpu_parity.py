@@ -479,3 +479,28 @@ def test_reference_sharded_pieces_reproduce_the_whole_reference(ctx, mode):
     got = refshard.combine(np.concatenate(parts), lengths.size, mode)
     assert got.size == want.size and got.size > 4000
     assert np.array_equal(got, want)
+
+
+def test_large_candidate_sets_skip_the_dedup_only_when_it_cannot_pay(ctx, oracle, monkeypatch):
+    """Above the L2-resident hash size the candidate dedup is decided from a
+    1/64 read sample (forced here by lowering the size limit): a random
+    reference at q=10 (~50 random candidates per read, ~2% duplicates) skips
+    it, a repetitive one (mostly duplicates) keeps it; the hits equal the
+    oracle's either way."""
+    import paper_1403_1706_b200 as qgm
+    monkeypatch.setenv("QGM_DEDUP_DIRECT_MAX", "1000")
+    for rep, seed, q in ((False, 91, 10), (True, 92, 12)):
+        L = 300_000
+        ref = qgm.repetitive_reference(seed, L) if rep else qgm.random_reference(seed, L)
+        cb = np.array([0, L], np.uint64)
+        codes, lengths, *_ = qgm.simulate_reads(seed + 1, ref, cb, 4000, 100, 0.03)
+        R = qgm.Reference.from_codes(ctx, ref, cb)
+        reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+        for mode in (0, 1):
+            got, st = ctx.map(reads, R, q=q, mode=mode)
+            want, ost = oracle.map(ref, cb, codes, 100, lengths, q=q, mode=mode)
+            assert _same(got, want), (rep, mode)
+            skipped = st["unique_candidates"] == st["raw_candidates"]
+            assert skipped == (not rep), (rep, st)
+            if not skipped:
+                assert st["unique_candidates"] == ost["unique_candidates"]
