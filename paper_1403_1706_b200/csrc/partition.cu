@@ -45,6 +45,7 @@ constexpr uint32_t kBins = 1u << kBinBits;
 constexpr uint32_t kChunk = 8 * kPartThreads;  // q-gram slots per chunk; staging = 8 B each
 static_assert(kPartThreads >= int(kBins), "the P1 chunk scan gives every bin its own thread");
 constexpr uint32_t kPer = kChunk / kPartThreads;
+static_assert(kBins <= 256 && kChunk <= (1u << 24), "P1 packs bin | rank << 8 in 32 bits");
 constexpr int kRun = 8;  // consecutive q-gram slots per thread (P0, P1)
 static_assert(kPer % kRun == 0, "");
 constexpr unsigned kP1CodeShift = 40, kP1MetaShift = 33;
@@ -190,33 +191,32 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
           uint32_t f, g, m, pos;
           const bool ok = gen.run_slot<R>(tr, u[h], j, f, g, m, pos);
           item[e] = (uint64_t(g & lmask) << kP1CodeShift) | (uint64_t(m) << kP1MetaShift) | pos;
-          bin[e] = ok ? g >> shift : ~0u;
-          if (ok) atomicAdd(cnt + bin[e], 1u);
+          // bin | rank among the chunk's items of that bin << 8 (the count's
+          // atomic returns the rank, so placement needs no second atomic)
+          bin[e] = ok ? (g >> shift) | (atomicAdd(cnt + (g >> shift), 1u) << 8) : ~0u;
         }
       }
     }
     __syncthreads();
+    uint32_t total;  // valid items in the chunk
     {  // local exclusive offsets; reserve the chunk's run in every bin
       const uint32_t b = threadIdx.x;
       const uint32_t v = b < kBins ? cnt[b] : 0u;
-      uint32_t tot;
-      const uint32_t ex = block_exclusive_scan<uint32_t>(v, ws, &tot);
+      const uint32_t ex = block_exclusive_scan<uint32_t>(v, ws, &total);
       if (b < kBins) {
         lofs[b] = ex;
         gdst[b] = v ? boff[b] + atomicAdd(cursor + b, v) : 0u;
-        cnt[b] = ex;  // becomes the local placement cursor
       }
     }
     __syncthreads();
 #pragma unroll
     for (uint32_t k = 0; k < kPer; ++k)
       if (bin[k] != ~0u) {
-        const uint32_t slot = atomicAdd(cnt + bin[k], 1u);
+        const uint32_t b = bin[k] & 0xFFu, slot = lofs[b] + (bin[k] >> 8);
         stage[slot] = item[k];
-        sbin[slot] = uint8_t(bin[k]);
+        sbin[slot] = uint8_t(b);
       }
     __syncthreads();
-    const uint32_t total = cnt[kBins - 1];  // == number of valid items in the chunk
     for (uint32_t i = threadIdx.x; i < total; i += kPartThreads) {
       const uint32_t b = sbin[i];
       out[gdst[b] + (i - lofs[b])] = stage[i];
