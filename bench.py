@@ -241,7 +241,14 @@ def run_gpu(args):
     # device-resident inputs for `value`
     d_words = torch.from_numpy(words.view(np.int64)).to(f"cuda:{local}")
     d_len = torch.from_numpy(lengths.view(np.int32)).to(f"cuda:{local}")
-    # pinned host inputs / outputs for `e2e`
+    # pinned host inputs / outputs for `e2e`, allocated before anything else
+    # large (placement of pinned pages allocated late in the process varied
+    # the streamed time by up to 20% between processes on one box)
+    # the streamed API takes the reads as one dense 2-bit stream (2 bits per
+    # base, no per-read padding) and, all reads being `rlen` long, no length
+    # array: 25 MB per 1M x 100 bp batch
+    uniform = bool(np.all(lengths == rlen))
+    h_dense = torch.from_numpy(qgm.pack_codes(codes).view(np.int64)).pin_memory()
     h_words = torch.from_numpy(words.view(np.int64)).pin_memory()
     h_len = torch.from_numpy(lengths.view(np.int32)).pin_memory()
     cap = n_reads * 4  # resized from the measured hit count before the e2e pass
@@ -303,11 +310,6 @@ def run_gpu(args):
     if st["hits"] > cap:
         cap = int(st["hits"] * 1.05) + 1024
         h_hits = torch.empty(cap * 16, dtype=torch.uint8).pin_memory()
-    # the streamed API takes the reads as one dense 2-bit stream (2 bits per
-    # base, no per-read padding) and, all reads being `rlen` long, no length
-    # array: 25 MB per 1M x 100 bp batch
-    uniform = bool(np.all(lengths == rlen))
-    h_dense = torch.from_numpy(qgm.pack_codes(codes).view(np.int64)).pin_memory()
 
     def run_batches(K):
         arr = (qgm.Batch * K)()
