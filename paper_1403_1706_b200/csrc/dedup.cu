@@ -67,6 +67,33 @@ __global__ void __launch_bounds__(kDedupThreads) k_tile_emit(const uint64_t* __r
   }
 }
 
+// One pass over the table: each CTA reserves its tile's run of the output
+// with one atomic (tile order is irrelevant: validation is per key) and
+// writes the tile's keys there. The counter ends as the unique count.
+__global__ void __launch_bounds__(kDedupThreads) k_tile_compact(const uint64_t* __restrict__ table,
+                                                                uint64_t* __restrict__ out,
+                                                                unsigned long long* __restrict__ counter) {
+  __shared__ uint32_t ws[33];
+  __shared__ unsigned long long s_base;
+  constexpr int kPerThread = kTile / kDedupThreads;
+  const uint64_t base = uint64_t(blockIdx.x) * kTile;
+  uint64_t v[kPerThread];
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < kPerThread; ++j) {  // coalesced; a thread's keys go to consecutive outputs
+    v[j] = table[base + uint64_t(j) * kDedupThreads + threadIdx.x];
+    c += v[j] != kEmpty;
+  }
+  uint32_t tot;
+  const uint32_t ex = block_exclusive_scan<uint32_t>(c, ws, &tot);
+  if (threadIdx.x == 0) s_base = tot ? atomicAdd(counter, (unsigned long long)tot) : 0ull;
+  __syncthreads();
+  uint64_t o = s_base + ex;
+#pragma unroll
+  for (int j = 0; j < kPerThread; ++j)
+    if (v[j] != kEmpty) out[o++] = v[j];
+}
+
 __global__ void k_store_count(const uint32_t* __restrict__ total, unsigned long long* __restrict__ out) {
   *out = *total;
 }
@@ -102,12 +129,9 @@ void dedup_keys_async(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& 
     QGM_KERNEL(c, k_hash_insert, grid, 256, 0, keys, n, table.p, T - 1);
   }
   const uint32_t tiles = uint32_t(T / kTile);
-  DBuf<uint32_t> counts(c, tiles + 1), total(c, 1);
-  QGM_KERNEL(c, k_tile_count, tiles, kDedupThreads, 0, table.p, T, counts.p);
-  exclusive_scan_u32(c, counts.p, counts.p, tiles, total.p, nullptr);
   if (out.n < n) out.alloc(c, n);
-  QGM_KERNEL(c, k_tile_emit, tiles, kDedupThreads, 0, table.p, counts.p, out.p);
-  QGM_KERNEL(c, k_store_count, 1, 1, 0, total.p, d_count);
+  QGM_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
+  QGM_KERNEL(c, k_tile_compact, tiles, kDedupThreads, 0, table.p, out.p, d_count);
 }
 
 uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out) {
