@@ -504,3 +504,50 @@ def test_large_candidate_sets_skip_the_dedup_only_when_it_cannot_pay(ctx, oracle
             assert skipped == (not rep), (rep, st)
             if not skipped:
                 assert st["unique_candidates"] == ost["unique_candidates"]
+
+
+def test_randomised_configurations_match_oracle(ctx, oracle):
+    """A seeded sweep over the parameter space the C ABI accepts -- q 4..16,
+    band 1..64, identity 0..100%, both modes, one strand or both, 1-6
+    chromosomes (some shorter than a read), read lengths 1..stride, error
+    rates up to 12%, optional repeat mask -- every configuration bit-identical
+    to the oracle, stats included, and the CIGARs of the hits too."""
+    import paper_1403_1706_b200 as qgm
+    rng = np.random.default_rng(2026)
+    for case in range(24):
+        q = int(rng.integers(4, 17))
+        band = int(rng.choice([1, 2, 7, 16, 31, 32, 33, 48, 64]))
+        pct = int(rng.choice([0, 50, 70, 80, 90, 100]))
+        mode = int(rng.integers(0, 2))
+        strands = int(rng.choice([1, 2, 3]))
+        n_chrom = int(rng.integers(1, 7))
+        L = int(rng.integers(20_000, 120_000))
+        ref = qgm.random_reference(int(rng.integers(1 << 30)), L)
+        cuts = np.sort(rng.choice(np.arange(1, L), n_chrom - 1, replace=False)) if n_chrom > 1 else np.array([], int)
+        cb = np.concatenate([[0], cuts, [L]]).astype(np.uint64)
+        stride = int(rng.choice([20, 64, 100, 150, 255]))
+        n_reads = int(rng.integers(50, 800))
+        err = float(rng.choice([0.0, 0.03, 0.08, 0.12]))
+        codes, lengths, *_ = qgm.simulate_reads(int(rng.integers(1 << 30)), ref, cb, n_reads, stride, err)
+        if rng.random() < 0.5:
+            lengths = np.minimum(lengths, rng.integers(1, stride + 1, lengths.size).astype(np.uint32))
+        mask = None
+        if rng.random() < 0.3:
+            from oracle.pyoracle import repeat_mask
+            mask = repeat_mask(ref, cb, q, int(rng.integers(1, 4)))
+        R = qgm.Reference.from_codes(ctx, ref, cb, mask=mask)
+        reads = qgm.Reads.from_codes(ctx, codes, lengths, stride)
+        got, st = ctx.map(reads, R, q=q, mode=mode, band_width=band, pct_identity=pct, strands=strands)
+        want, ost = oracle.map(ref, cb, codes, stride, lengths, q=q, mode=mode, band=band, pct=pct, strands=strands,
+                               mask=mask)
+        info = dict(case=case, q=q, band=band, pct=pct, mode=mode, strands=strands, chroms=n_chrom, stride=stride,
+                    err=err, mask=mask is not None, got=got.size, want=want.size)
+        assert _same(got, want), info
+        assert st["unique_candidates"] == ost["unique_candidates"], info
+        assert st["validated"] == ost["validated"], info
+        if got.size:  # and the traceback of every hit
+            ops, cinfo = ctx.cigar(reads, R, got, band_width=band)
+            wops, winfo = oracle.cigar(ref, cb, codes, stride, lengths, got, band=band, max_ops=ops.shape[1])
+            assert np.array_equal(cinfo, winfo), info
+            m = np.arange(ops.shape[1])[None, :] < cinfo["n_ops"][:, None]
+            assert np.array_equal(np.where(m, ops, 0), np.where(m, wops, 0)), info
