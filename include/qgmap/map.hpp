@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "qgmap/packed_words.hpp"
 #include "qgmap/qgroup_index.hpp"
 #include "qgmap/reference.hpp"
 
@@ -206,12 +207,11 @@ std::vector<Alignment> run_cigar(const device::Context& ctx, std::uint64_t n, un
 // candidate dedup, validation, dedup + strata -- all on the device. Output
 // sorted by (read, chrom, ref_start, strand); with `ranks`, also the
 // hit_rank R of every record.
-inline std::vector<MappedHit> map_reads_ranked(const DeviceReference& ref, const PackedReadText& text,
-                                               const MapParams& p, qgm_map_stats* stats,
-                                               std::vector<std::uint32_t>* ranks,
-                                               std::vector<Alignment>* aligns = nullptr) {
+namespace detail {
+inline std::vector<MappedHit> map_uploaded(const DeviceReference& ref, const device::ReadsHandle& reads,
+                                           const MapParams& p, qgm_map_stats* stats,
+                                           std::vector<std::uint32_t>* ranks, std::vector<Alignment>* aligns) {
   auto ctx = ref.context();
-  auto reads = device::upload_reads(text, ctx);
   const qgm_map_params mp{p.q, p.group_width, p.sampled ? 1u : 0u, p.band.band_width, p.band.percent(),
                           unsigned(p.mode), unsigned(p.strands), 0};
   qgm_hits* h = nullptr;
@@ -230,15 +230,35 @@ inline std::vector<MappedHit> map_reads_ranked(const DeviceReference& ref, const
     ctx->check(qgm_hits_ranks(ctx->get(), h, ranks->data()));
   }
   if (aligns) {  // CIGAR of every record while the reads are on the device
-    *aligns = detail::run_cigar(*ctx, n, p.band.band_width,
-                                [&](std::uint32_t max_ops, std::uint32_t* ops, qgm_cigar_info* info) {
-                                  return qgm_hits_cigar(ctx->get(), h, reads.get(), ref.get(), p.band.band_width,
-                                                        max_ops, ops, info);
-                                });
+    *aligns = run_cigar(*ctx, n, p.band.band_width,
+                        [&](std::uint32_t max_ops, std::uint32_t* ops, qgm_cigar_info* info) {
+                          return qgm_hits_cigar(ctx->get(), h, reads.get(), ref.get(), p.band.band_width, max_ops,
+                                                ops, info);
+                        });
   }
   return out;
 }
+}  // namespace detail
 
+inline std::vector<MappedHit> map_reads_ranked(const DeviceReference& ref, const PackedReadText& text,
+                                               const MapParams& p, qgm_map_stats* stats,
+                                               std::vector<std::uint32_t>* ranks,
+                                               std::vector<Alignment>* aligns = nullptr) {
+  return detail::map_uploaded(ref, device::upload_reads(text, ref.context()), p, stats, ranks, aligns);
+}
+
+// The same for reads already in the device's 2-bit layout (pack_words): no
+// 1-byte codes or position list on the host.
+inline std::vector<MappedHit> map_packed_reads(const DeviceReference& ref, const PackedWords& pw, const MapParams& p,
+                                               qgm_map_stats* stats = nullptr,
+                                               std::vector<std::uint32_t>* ranks = nullptr,
+                                               std::vector<Alignment>* aligns = nullptr) {
+  auto ctx = ref.context();
+  qgm_reads* r = nullptr;
+  ctx->check(qgm_reads_upload(ctx->get(), pw.words.data(), pw.lengths.data(), std::uint32_t(pw.lengths.size()),
+                              pw.stride, &r));
+  return detail::map_uploaded(ref, device::ReadsHandle(ctx, r), p, stats, ranks, aligns);
+}
 
 inline std::vector<MappedHit> map_reads(const DeviceReference& ref, const PackedReadText& text,
                                         const MapParams& p = {}, qgm_map_stats* stats = nullptr) {

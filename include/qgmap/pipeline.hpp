@@ -35,7 +35,7 @@ inline RunStats run_map(std::istream& fastq, std::ostream& sam, const Reference&
   rng_engine rng(opt.seed);
   struct Buffer {
     std::vector<FastqRecord> recs;
-    PackedReadText text;
+    PackedWords words;  // the device read layout, straight from the sequences
   };
   auto load = [&]() {  // parse + encode one buffer (worker thread; rng used only here)
     Buffer b;
@@ -47,7 +47,7 @@ inline RunStats run_map(std::istream& fastq, std::ostream& sam, const Reference&
       seqs.push_back(r.seq);
       stride = std::max<std::uint32_t>(stride, std::uint32_t(r.seq.size()));
     }
-    b.text = pack_reads(seqs, stride, p.q, rng);
+    b.words = pack_words(seqs, stride, rng);
     return b;
   };
   RunStats st;
@@ -58,7 +58,7 @@ inline RunStats run_map(std::istream& fastq, std::ostream& sam, const Reference&
     next = std::async(std::launch::async, load);
     std::vector<std::uint32_t> ranks;
     std::vector<Alignment> aligns;
-    const auto hits = map_reads_ranked(dref, cur.text, p, nullptr, &ranks, &aligns);
+    const auto hits = map_packed_reads(dref, cur.words, p, nullptr, &ranks, &aligns);
     std::vector<std::string> names, seqs, quals;
     names.reserve(cur.recs.size());
     for (auto& r : cur.recs) {

@@ -6,6 +6,7 @@
 #include <sstream>
 
 #include "qgmap/fastq.hpp"
+#include "qgmap/packed_words.hpp"
 #include "qgmap/sam.hpp"
 
 using namespace qgmap;
@@ -85,4 +86,26 @@ TEST_CASE("SAM records: SPEC emit_sam examples on given hits") {
   CHECK(L[2] == "q2\t0\tchrA\t21\t60\t4M\t*\t0\t0\tGGTT\tIIII\tNM:i:0");
   CHECK(L[3] == "q2\t256\tchrB\t41\t60\t4M\t*\t0\t0\tGGTT\tIIII\tNM:i:0");
   CHECK(L[4] == "q3\t4\t*\t0\t0\t*\t*\t0\t0\tTTTT\tIIII");
+}
+
+TEST_CASE("pack_words equals pack_reads + PackedReadText::pack (N bases drawn in the same order)") {
+  std::mt19937_64 g(3);
+  std::vector<std::string> reads;
+  for (int r = 0; r < 3000; ++r) {
+    std::string s(g() % 130, 'A');
+    for (auto& c : s) c = "ACGTNacgtn"[g() % 10];
+    if (r % 17 == 0) s.clear();
+    reads.push_back(s);
+  }
+  rng_engine a(11), b(11);
+  const auto text = pack_reads(reads, 130, 12, a);
+  const auto pw = pack_words(reads, 130, b, 4);
+  CHECK(pw.words == text.pack());
+  CHECK(pw.lengths == text.read_lengths);
+  CHECK(a() == b());  // the same number of draws
+  std::vector<std::string> bad{"ACGT", "ACXT"};
+  rng_engine c(1);
+  CHECK_THROWS_AS(pack_words(bad, 8, c), input_error);
+  std::vector<std::string> longr{"ACGTACGTA"};
+  CHECK_THROWS_AS(pack_words(longr, 8, c), input_error);
 }
