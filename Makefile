@@ -37,6 +37,9 @@ tests/cpp/build/%: tests/cpp/%.cpp tests/cpp/catch_main.cpp tests/cpp/catch2/cat
 	@mkdir -p $(dir $@)
 	$(CXX) $(HOSTFLAGS) -Iinclude -Itests/cpp -Ioracle -o $@ $< tests/cpp/catch_main.cpp -L$(PKG) -lqgm_b200 -Wl,-rpath,'$$ORIGIN/../../../$(PKG)'
 
+tools/run_map_bench: tools/run_map_bench.cpp $(wildcard include/qgmap/*.hpp) include/qgm_c.h $(LIB)
+	$(CXX) $(HOSTFLAGS) -Iinclude -o $@ $< -L$(PKG) -lqgm_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
 clean:
-	rm -rf build tests/cpp/build $(LIB) $(SYNTH)
+	rm -rf build tests/cpp/build $(LIB) $(SYNTH) tools/run_map_bench
 	$(MAKE) -C oracle clean
