@@ -214,9 +214,22 @@ void make_read_planes(Ctx& c, Reads& r) {
   r.Wp = r.W + 2;
   r.planes.alloc(c, std::max<uint64_t>(uint64_t(r.n) * r.Wp, 1));
   const uint64_t total = uint64_t(r.n) * r.Wp;
-  if (total)
-    QGM_KERNEL(c, k_read_planes, unsigned(std::min<uint64_t>(ceil_div(total, 256), kSMs * 16)), 256, 0, r.words.p,
-               r.n, r.W, r.Wp, r.planes.p);
+  if (!total) return;
+  // on the side stream, after everything the compute stream has queued (the
+  // words, and any earlier user of the planes block); consumers wait on
+  // planes_ev (Ctx::wait_planes)
+  if (!c.side_stream) {
+    QGM_CUDA(cudaStreamCreateWithFlags(&c.side_stream, cudaStreamNonBlocking));
+    QGM_CUDA(cudaEventCreateWithFlags(&c.side_ev, cudaEventDisableTiming));
+    QGM_CUDA(cudaEventCreateWithFlags(&c.planes_ev, cudaEventDisableTiming));
+  }
+  QGM_CUDA(cudaEventRecord(c.side_ev, c.stream));
+  QGM_CUDA(cudaStreamWaitEvent(c.side_stream, c.side_ev, 0));
+  k_read_planes<<<unsigned(std::min<uint64_t>(ceil_div(total, 256), kSMs * 16)), 256, 0, c.side_stream>>>(
+      r.words.p, r.n, r.W, r.Wp, r.planes.p);
+  ++c.launches;
+  QGM_LAUNCH_CHECK();
+  QGM_CUDA(cudaEventRecord(c.planes_ev, c.side_stream));
 }
 
 void make_ref_planes(Ctx& c, Ref& ref) {
@@ -450,6 +463,12 @@ void qgm_ctx_destroy(qgm_ctx* ctx) {
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
   if (ctx->c.copy_stream) cudaStreamDestroy(ctx->c.copy_stream);
   if (ctx->c.d2h_stream) cudaStreamDestroy(ctx->c.d2h_stream);
+  if (ctx->c.side_stream) {
+    cudaStreamSynchronize(ctx->c.side_stream);
+    cudaStreamDestroy(ctx->c.side_stream);
+    cudaEventDestroy(ctx->c.side_ev);
+    cudaEventDestroy(ctx->c.planes_ev);
+  }
   delete ctx;
 }
 
@@ -567,6 +586,7 @@ int qgm_reads_from_device(qgm_ctx* ctx, const uint64_t* w, const uint32_t* len, 
 void qgm_reads_destroy(qgm_reads* r) {
   if (!r) return;
   cudaSetDevice(r->owner->c.device);
+  r->owner->c.wait_planes();  // the planes block goes back to the stream-ordered cache
   delete r;
 }
 

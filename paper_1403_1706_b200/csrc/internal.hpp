@@ -27,6 +27,14 @@ struct Ctx {
   cudaStream_t copy_stream = nullptr;  // H2D of qgm_map_host_batches (created on first use)
   cudaStream_t d2h_stream = nullptr;   // its D2H: a second stream, so uploads and downloads
                                        // use separate copy engines and overlap each other
+  // side stream: the reads' bit planes (validation input) are built there,
+  // concurrently with the partition and the join; planes_ev marks the last
+  // planes build and every planes consumer / release waits for it
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t side_ev = nullptr, planes_ev = nullptr;
+  void wait_planes() {
+    if (planes_ev) cudaStreamWaitEvent(stream, planes_ev, 0);
+  }
   uint64_t last_raw_candidates = 0;    // sizes the next batch's candidate buffer
   std::string err;
   uint64_t launches = 0;

@@ -348,6 +348,7 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
   if (pct > 100) throw InputError("percent identity must be in [0, 100]");
   if (read_bits + 1 + ref.diag_bits > 64) throw InputError("read batch too large for the 64-bit hit key");
   if (n == 0) return;
+  c.wait_planes();  // the reads' planes are built on the side stream
   ValArgs a;
   a.rplanes = reads.planes.p;
   a.rlen = reads.lengths.p;
