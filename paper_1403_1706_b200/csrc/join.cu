@@ -51,7 +51,10 @@ constexpr int kJoinWarps = kJoinThreads / 32;
 #endif
 constexpr int kItems = QGM_JOIN_ITEMS;    // read q-grams (= lookups) per lane per step
 constexpr int kRanges = 32 * kItems;
-constexpr uint32_t kInline = 4;           // intervals up to this length are expanded in-lane
+#ifndef QGM_JOIN_INLINE
+#define QGM_JOIN_INLINE 4
+#endif
+constexpr uint32_t kInline = QGM_JOIN_INLINE;  // intervals up to this length are expanded in-lane
 constexpr uint32_t kMaxWords = 2048;      // group words per sub-bin (q = 16)
 constexpr uint32_t kPosMask = (1u << kPackedPosBits) - 1u;
 

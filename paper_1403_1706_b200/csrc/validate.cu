@@ -23,7 +23,10 @@
 namespace qgm {
 namespace {
 
-constexpr int kValThreads = 128;
+#ifndef QGM_VAL_THREADS
+#define QGM_VAL_THREADS 128
+#endif
+constexpr int kValThreads = QGM_VAL_THREADS;
 #ifdef QGM_VAL_HIST
 __device__ unsigned long long g_exit_hist[16];  // debug: abandon row / 16, [15] = ran to the end
 #endif
