@@ -271,7 +271,6 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   if (P.mode > 1) throw InputError("mode must be best-stratum (0) or all (1)");
   const int strands = P.strands ? int(P.strands) : 3;
   const unsigned rb = read_bits_for(reads.n);
-  const int key_bits = int(rb + 1 + ref.diag_bits);
   HitsObj out;
   DBuf<uint64_t> keys, alt;
   uint64_t n_raw, n_u;

@@ -31,7 +31,7 @@ namespace {
 // 128-bit band word as two u64 halves (add with carry; shifts by any amount)
 struct alignas(16) U128 {
   uint64_t lo = 0, hi = 0;
-  __device__ U128() = default;
+  U128() = default;
   __device__ U128(int v) : lo(uint64_t(int64_t(v))), hi(v < 0 ? ~0ull : 0ull) {}
   __device__ U128(uint64_t l, uint64_t h) : lo(l), hi(h) {}
   __device__ explicit operator uint32_t() const { return uint32_t(lo); }
@@ -61,15 +61,6 @@ struct alignas(16) U128 {
     if (n >= 64) return {a.hi >> (n - 64), 0ull};
     return {(a.lo >> n) | (a.hi << (64 - n)), a.hi >> n};
   }
-  __device__ U128& operator|=(U128 b) { return *this = *this | b; }
-};
-
-template <class T> struct BandBits;
-template <> struct BandBits<uint64_t> {
-  __device__ static __forceinline__ unsigned popc(uint64_t x) { return __popcll(x); }
-};
-template <> struct BandBits<U128> {
-  __device__ static __forceinline__ unsigned popc(U128 x) { return __popcll(x.lo) + __popcll(x.hi); }
 };
 
 struct CigarArgs {

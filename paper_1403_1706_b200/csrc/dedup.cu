@@ -94,10 +94,6 @@ __global__ void __launch_bounds__(kDedupThreads) k_tile_compact(const uint64_t* 
     if (v[j] != kEmpty) out[o++] = v[j];
 }
 
-__global__ void k_store_count(const uint32_t* __restrict__ total, unsigned long long* __restrict__ out) {
-  *out = *total;
-}
-
 // keys of every (mask+1)-th read (read id = key >> rshift) appended to out
 __global__ void k_sample_reads(const uint64_t* __restrict__ keys, uint64_t n, unsigned rshift, uint64_t mask,
                                uint64_t* __restrict__ out, unsigned long long* __restrict__ n_out) {
