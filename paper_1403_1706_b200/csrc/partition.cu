@@ -39,7 +39,10 @@ namespace {
 #define QGM_PART_THREADS 256
 #endif
 constexpr int kPartThreads = QGM_PART_THREADS;
-constexpr int kPartMinBlocks = 1024 / kPartThreads;  // 64 registers per thread
+#ifndef QGM_PART_MINB
+#define QGM_PART_MINB (1024 / QGM_PART_THREADS)
+#endif
+constexpr int kPartMinBlocks = QGM_PART_MINB;  // 4: 64 registers per thread
 constexpr unsigned kBinBits = 8;
 constexpr uint32_t kBins = 1u << kBinBits;
 constexpr uint32_t kChunk = 8 * kPartThreads;  // q-gram slots per chunk; staging = 8 B each
