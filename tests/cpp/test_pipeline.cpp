@@ -173,3 +173,36 @@ TEST_CASE("run_map: every read has a record, CIGARs are consistent, buffering do
   };
   CHECK(strip_n(run(7, 3)) == strip_n(a));
 }
+
+TEST_CASE("map_packed_reads(pack_words) equals map_reads(pack_reads) for the same seed, CIGARs included") {
+  Fixture fx;
+  DeviceReference dref(fx.ref);
+  std::mt19937_64 g(9);
+  std::vector<base_code> all;
+  for (char ch : fx.chrom) all.push_back(base_code(std::string("ACGT").find(ch)));
+  std::vector<std::string> seqs;
+  for (int r = 0; r < 500; ++r) {
+    const std::size_t len = 30 + g() % 90, pos = g() % (all.size() - len - 10);
+    auto rd = tu::sample_read(all, pos, len, 0.04, g() & 1, g);
+    std::string s;
+    for (auto c : rd) s += decode_base(c);
+    if (r % 9 == 0) s[g() % s.size()] = 'N';
+    seqs.push_back(s);
+  }
+  MapParams p = params(StratumMode::all);
+  rng_engine a(5), b(5);
+  const auto text = pack_reads(seqs, 120, p.q, a);
+  const auto pw = pack_words(seqs, 120, b);
+  std::vector<std::uint32_t> ra, rb;
+  std::vector<Alignment> aa, ab;
+  const auto ha = map_reads_ranked(dref, text, p, nullptr, &ra, &aa);
+  const auto hb = map_packed_reads(dref, pw, p, nullptr, &rb, &ab);
+  REQUIRE(ha.size() > 400);
+  CHECK(ha == hb);
+  CHECK(ra == rb);
+  REQUIRE(aa.size() == ab.size());
+  for (std::size_t i = 0; i < aa.size(); ++i) {
+    CHECK(aa[i].cigar() == ab[i].cigar());
+    CHECK(aa[i].ref_start == ab[i].ref_start);
+  }
+}
