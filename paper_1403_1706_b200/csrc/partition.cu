@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
 // fallback for chunks whose window is wider (tiny bins). The P1 bin of item i
 // is found from the bin offsets (staged in shared memory) with a per-thread
 // cursor that only moves forward.
-constexpr uint32_t kLocal = 2048;
+constexpr uint32_t kLocal = 1024;
 
 struct Refine {
   unsigned shift;    // code bits below the P1 bin (in the P1 item)
@@ -297,36 +297,54 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
                                                                     uint32_t* __restrict__ cursor,
                                                                     const uint4* __restrict__ chunk_info,
                                                                     uint64_t* __restrict__ out) {
-  extern __shared__ uint64_t stage[];  // kChunk join items, then kChunk u16 window keys
+  // dynamic: the chunk's items as loaded by TMA (kChunk u64), the sorted
+  // join items (kChunk u64), their window keys (kChunk u16)
+  extern __shared__ __align__(16) uint64_t sdyn[];
+  uint64_t* sin = sdyn;
+  uint64_t* stage = sdyn + kChunk;
   uint16_t* skey = reinterpret_cast<uint16_t*>(stage + kChunk);
   __shared__ uint32_t cnt[kLocal], lofs[kLocal], gdst[kLocal];
   __shared__ uint32_t sboff[kBins + 1];
   __shared__ uint32_t ws[33];
+  __shared__ __align__(8) uint64_t s_bar;
   for (uint32_t b = threadIdx.x; b <= rf.nbins; b += kPartThreads) sboff[b] = boff[b];
-  __syncthreads();
   const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
+  // one elected thread moves each chunk's items into shared memory with a
+  // bulk copy issued while the previous chunk is sorted and written out
+  auto fetch = [&](uint32_t ch) {
+    const uint32_t a0 = ch * kChunk, a1 = min(n, a0 + kChunk);
+    const uint32_t bytes = ((a1 - a0) * 8u + 15u) & ~15u;  // the buffer holds n + 2 items
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&s_bar, bytes);
+    bulk_g2s(sin, in + a0, bytes, &s_bar);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    if (blockIdx.x < n_chunks) fetch(blockIdx.x);
+  }
+  __syncthreads();
+  uint32_t phase = 0;
   const bool uniform = ~__ldg(rf.lens + 1) == rf.stride;
   uint4 ci_next = blockIdx.x < n_chunks ? __ldg(chunk_info + blockIdx.x) : make_uint4(0, 0, 0, 0);
   for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
     const uint32_t c0 = ch * kChunk, c1 = min(n, c0 + kChunk);
     const uint4 ci = ci_next;
-    if (ch + gridDim.x < n_chunks) {  // next chunk: its info one iteration ahead, its items -> L2
-      ci_next = __ldg(chunk_info + ch + gridDim.x);
-      if (threadIdx.x == 0) {
-        const uint32_t n0 = c0 + gridDim.x * kChunk, n1 = min(n, n0 + kChunk);
-        bulk_prefetch_l2(in + n0, ((n1 - n0) * 8u) & ~15u);
-      }
-    }
+    const bool more = ch + gridDim.x < n_chunks;
+    if (more) ci_next = __ldg(chunk_info + ch + gridDim.x);  // next chunk's info one iteration ahead
+    mbar_wait(&s_bar, phase);
+    phase ^= 1u;
     const uint32_t bfirst = ci.x & 0xFFFFu, blast = ci.x >> 16;
     const uint32_t base = ci.y, width = ci.z;
     uint32_t b = bfirst;
     if (width > kLocal) {
       for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) {
         while (sboff[b + 1] <= i) ++b;
-        const uint64_t it = in[i];
+        const uint64_t it = sin[i - c0];
         const uint32_t k = rf.key(it, b);
         out[off[k] + atomicAdd(cursor + k, 1u)] = rf.convert(it, uniform);
       }
+      __syncthreads();  // every thread is done with sin
+      if (threadIdx.x == 0 && more) fetch(ch + gridDim.x);
       continue;
     }
     for (uint32_t k = threadIdx.x; k < width; k += kPartThreads) cnt[k] = 0;
@@ -334,9 +352,9 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
     uint64_t v[kPer];
     uint32_t kk[kPer];
 #pragma unroll
-    for (uint32_t k = 0; k < kPer; ++k) {  // every load first
+    for (uint32_t k = 0; k < kPer; ++k) {
       const uint32_t i = c0 + k * kPartThreads + threadIdx.x;
-      v[k] = __ldg(in + min(i, c1 - 1));
+      v[k] = sin[min(i, c1 - 1) - c0];
     }
 #pragma unroll
     for (uint32_t k = 0; k < kPer; ++k) {
@@ -348,6 +366,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
       if (i < c1) atomicAdd(cnt + kk[k], 1u);
     }
     __syncthreads();
+    if (threadIdx.x == 0 && more) fetch(ch + gridDim.x);  // every thread has its items in registers
     // exclusive scan of cnt[0, width): each thread owns a contiguous run
     const uint32_t per = (width + kPartThreads - 1) / kPartThreads;
     const uint32_t k0 = threadIdx.x * per, k1 = min(width, k0 + per);
@@ -454,7 +473,7 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   out.V = V;
   DBuf<uint32_t> hist(c, kBins + 1);  // per-bin cursors of P1
   hist.zero();
-  DBuf<uint64_t> p1(c, V);
+  DBuf<uint64_t> p1(c, V + 2);  // +2: P2 bulk-copies whole 16-byte pairs
   const size_t smem = kChunk * (sizeof(uint64_t) + sizeof(uint8_t));
   auto p1kern = runs ? k_part_scatter<kRun> : k_part_scatter<1>;
   QGM_CUDA(cudaFuncSetAttribute(p1kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -478,7 +497,7 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   const unsigned grid2 = unsigned(std::min<uint64_t>(ceil_div(V, kChunk), uint64_t(kSMs) * 4));
   h2.zero();  // per-key cursors
   out.pairs.alloc(c, V + 2);  // +2: the join bulk-copies whole 16-byte pairs of items
-  const size_t smem2 = kChunk * (sizeof(uint64_t) + sizeof(uint16_t));
+  const size_t smem2 = kChunk * (2 * sizeof(uint64_t) + sizeof(uint16_t));
   QGM_CUDA(cudaFuncSetAttribute(k_refine_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
   const uint32_t n_chunks2 = uint32_t(ceil_div(V, kChunk));
   DBuf<uint4> chunk_info(c, n_chunks2);
