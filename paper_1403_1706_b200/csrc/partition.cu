@@ -238,6 +238,14 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
 // is found from the bin offsets (staged in shared memory) with a per-thread
 // cursor that only moves forward.
 constexpr uint32_t kLocal = 1024;
+// P2 geometry: its own chunk (items bulk-copied into shared memory) and CTA size
+#ifndef QGM_P2_THREADS
+#define QGM_P2_THREADS 256
+#endif
+constexpr int kP2Threads = QGM_P2_THREADS;
+constexpr int kP2MinBlocks = 1024 / kP2Threads;
+constexpr uint32_t kP2Per = 8;
+constexpr uint32_t kP2Chunk = kP2Per * kP2Threads;
 
 struct Refine {
   unsigned shift;    // code bits below the P1 bin (in the P1 item)
@@ -281,9 +289,9 @@ __device__ __forceinline__ uint32_t bin_search(const uint32_t* sboff, uint32_t n
 // a dependent load or a binary search
 __global__ void k_chunk_info(const uint64_t* __restrict__ in, uint32_t n, const uint32_t* __restrict__ boff,
                              Refine rf, unsigned sub, uint4* __restrict__ info) {
-  const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
+  const uint32_t n_chunks = (n + kP2Chunk - 1) / kP2Chunk;
   for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < n_chunks; ch += gridDim.x * blockDim.x) {
-    const uint32_t c0 = ch * kChunk, c1 = min(n, c0 + kChunk);
+    const uint32_t c0 = ch * kP2Chunk, c1 = min(n, c0 + kP2Chunk);
     const uint32_t bfirst = bin_search(boff, rf.nbins, c0), blast = bin_search(boff, rf.nbins, c1 - 1);
     const uint32_t base = (rf.key(in[c0], bfirst) >> sub) << sub;
     const uint32_t width = (((rf.key(in[c1 - 1], blast) >> sub) + 1) << sub) - base;
@@ -291,28 +299,28 @@ __global__ void k_chunk_info(const uint64_t* __restrict__ in, uint32_t n, const 
   }
 }
 
-__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter(const uint64_t* __restrict__ in, uint32_t n,
+__global__ void __launch_bounds__(kP2Threads, kP2MinBlocks) k_refine_scatter(const uint64_t* __restrict__ in, uint32_t n,
                                                                     const uint32_t* __restrict__ boff, Refine rf,
                                                                     unsigned sub, const uint32_t* __restrict__ off,
                                                                     uint32_t* __restrict__ cursor,
                                                                     const uint4* __restrict__ chunk_info,
                                                                     uint64_t* __restrict__ out) {
-  // dynamic: the chunk's items as loaded by TMA (kChunk u64), the sorted
-  // join items (kChunk u64), their window keys (kChunk u16)
+  // dynamic: the chunk's items as loaded by TMA (kP2Chunk u64), the sorted
+  // join items (kP2Chunk u64), their window keys (kP2Chunk u16)
   extern __shared__ __align__(16) uint64_t sdyn[];
   uint64_t* sin = sdyn;
-  uint64_t* stage = sdyn + kChunk;
-  uint16_t* skey = reinterpret_cast<uint16_t*>(stage + kChunk);
+  uint64_t* stage = sdyn + kP2Chunk;
+  uint16_t* skey = reinterpret_cast<uint16_t*>(stage + kP2Chunk);
   __shared__ uint32_t cnt[kLocal], lofs[kLocal], gdst[kLocal];
   __shared__ uint32_t sboff[kBins + 1];
   __shared__ uint32_t ws[33];
   __shared__ __align__(8) uint64_t s_bar;
-  for (uint32_t b = threadIdx.x; b <= rf.nbins; b += kPartThreads) sboff[b] = boff[b];
-  const uint32_t n_chunks = (n + kChunk - 1) / kChunk;
+  for (uint32_t b = threadIdx.x; b <= rf.nbins; b += kP2Threads) sboff[b] = boff[b];
+  const uint32_t n_chunks = (n + kP2Chunk - 1) / kP2Chunk;
   // one elected thread moves each chunk's items into shared memory with a
   // bulk copy issued while the previous chunk is sorted and written out
   auto fetch = [&](uint32_t ch) {
-    const uint32_t a0 = ch * kChunk, a1 = min(n, a0 + kChunk);
+    const uint32_t a0 = ch * kP2Chunk, a1 = min(n, a0 + kP2Chunk);
     const uint32_t bytes = ((a1 - a0) * 8u + 15u) & ~15u;  // the buffer holds n + 2 items
     fence_proxy_async();
     mbar_arrive_expect_tx(&s_bar, bytes);
@@ -327,7 +335,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
   const bool uniform = ~__ldg(rf.lens + 1) == rf.stride;
   uint4 ci_next = blockIdx.x < n_chunks ? __ldg(chunk_info + blockIdx.x) : make_uint4(0, 0, 0, 0);
   for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
-    const uint32_t c0 = ch * kChunk, c1 = min(n, c0 + kChunk);
+    const uint32_t c0 = ch * kP2Chunk, c1 = min(n, c0 + kP2Chunk);
     const uint4 ci = ci_next;
     const bool more = ch + gridDim.x < n_chunks;
     if (more) ci_next = __ldg(chunk_info + ch + gridDim.x);  // next chunk's info one iteration ahead
@@ -337,7 +345,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
     const uint32_t base = ci.y, width = ci.z;
     uint32_t b = bfirst;
     if (width > kLocal) {
-      for (uint32_t i = c0 + threadIdx.x; i < c1; i += kPartThreads) {
+      for (uint32_t i = c0 + threadIdx.x; i < c1; i += kP2Threads) {
         while (sboff[b + 1] <= i) ++b;
         const uint64_t it = sin[i - c0];
         const uint32_t k = rf.key(it, b);
@@ -347,18 +355,18 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
       if (threadIdx.x == 0 && more) fetch(ch + gridDim.x);
       continue;
     }
-    for (uint32_t k = threadIdx.x; k < width; k += kPartThreads) cnt[k] = 0;
+    for (uint32_t k = threadIdx.x; k < width; k += kP2Threads) cnt[k] = 0;
     __syncthreads();
-    uint64_t v[kPer];
-    uint32_t kk[kPer];
+    uint64_t v[kP2Per];
+    uint32_t kk[kP2Per];
 #pragma unroll
-    for (uint32_t k = 0; k < kPer; ++k) {
-      const uint32_t i = c0 + k * kPartThreads + threadIdx.x;
+    for (uint32_t k = 0; k < kP2Per; ++k) {
+      const uint32_t i = c0 + k * kP2Threads + threadIdx.x;
       v[k] = sin[min(i, c1 - 1) - c0];
     }
 #pragma unroll
-    for (uint32_t k = 0; k < kPer; ++k) {
-      const uint32_t i = c0 + k * kPartThreads + threadIdx.x;
+    for (uint32_t k = 0; k < kP2Per; ++k) {
+      const uint32_t i = c0 + k * kP2Threads + threadIdx.x;
       if (i < c1 && bfirst != blast)
         while (sboff[b + 1] <= i) ++b;
       kk[k] = i < c1 ? rf.key(v[k], b) - base : ~0u;
@@ -368,7 +376,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
     __syncthreads();
     if (threadIdx.x == 0 && more) fetch(ch + gridDim.x);  // every thread has its items in registers
     // exclusive scan of cnt[0, width): each thread owns a contiguous run
-    const uint32_t per = (width + kPartThreads - 1) / kPartThreads;
+    const uint32_t per = (width + kP2Threads - 1) / kP2Threads;
     const uint32_t k0 = threadIdx.x * per, k1 = min(width, k0 + per);
     uint32_t s = 0;
     for (uint32_t k = k0; k < k1; ++k) s += cnt[k];
@@ -387,14 +395,14 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_refine_scatter
     }
     __syncthreads();
 #pragma unroll
-    for (uint32_t k = 0; k < kPer; ++k)
+    for (uint32_t k = 0; k < kP2Per; ++k)
       if (kk[k] != ~0u) {
         const uint32_t slot = atomicAdd(cnt + kk[k], 1u);
         stage[slot] = v[k];
         skey[slot] = uint16_t(kk[k]);
       }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < c1 - c0; i += kPartThreads) {
+    for (uint32_t i = threadIdx.x; i < c1 - c0; i += kP2Threads) {
       const uint32_t k = skey[i];
       out[gdst[k] + (i - lofs[k])] = stage[i];
     }
@@ -494,17 +502,17 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   rf.by_stride = FastDiv(std::max<uint32_t>(reads.stride, 1));
   rf.q = q;
   rf.lens = reads.lens.p;
-  const unsigned grid2 = unsigned(std::min<uint64_t>(ceil_div(V, kChunk), uint64_t(kSMs) * 4));
+  const unsigned grid2 = unsigned(std::min<uint64_t>(ceil_div(V, kP2Chunk), uint64_t(kSMs) * kP2MinBlocks));
   h2.zero();  // per-key cursors
   out.pairs.alloc(c, V + 2);  // +2: the join bulk-copies whole 16-byte pairs of items
-  const size_t smem2 = kChunk * (2 * sizeof(uint64_t) + sizeof(uint16_t));
+  const size_t smem2 = kP2Chunk * (2 * sizeof(uint64_t) + sizeof(uint16_t));
   QGM_CUDA(cudaFuncSetAttribute(k_refine_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
-  const uint32_t n_chunks2 = uint32_t(ceil_div(V, kChunk));
+  const uint32_t n_chunks2 = uint32_t(ceil_div(V, kP2Chunk));
   DBuf<uint4> chunk_info(c, n_chunks2);
   QGM_KERNEL(c, k_chunk_info, unsigned(ceil_div(n_chunks2, 256)), 256, 0, p1.p, V, out.boff.p, rf, sub, chunk_info.p);
   {
     KernelScope ks(c, "k_refine_scatter");
-    QGM_KERNEL(c, k_refine_scatter, grid2, kPartThreads, smem2, p1.p, V, out.boff.p, rf, sub, out.soff.p, h2.p,
+    QGM_KERNEL(c, k_refine_scatter, grid2, kP2Threads, smem2, p1.p, V, out.boff.p, rf, sub, out.soff.p, h2.p,
                chunk_info.p, out.pairs.p);
   }
 }
