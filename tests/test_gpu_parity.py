@@ -551,3 +551,26 @@ def test_randomised_configurations_match_oracle(ctx, oracle):
             assert np.array_equal(cinfo, winfo), info
             m = np.arange(ops.shape[1])[None, :] < cinfo["n_ops"][:, None]
             assert np.array_equal(np.where(m, ops, 0), np.where(m, wops, 0)), info
+
+
+def test_cigar_max_ops_overflow_is_an_input_error_with_counts(ctx):
+    """qgm_cigar_records with too small a max_ops: QGM_ERR_INPUT, every n_ops
+    filled in so the caller can retry (include/qgm_c.h)."""
+    import ctypes as C
+    import paper_1403_1706_b200 as qgm
+    L = 50_000
+    ref = qgm.random_reference(71, L)
+    cb = np.array([0, L], np.uint64)
+    codes, lengths, *_ = qgm.simulate_reads(72, ref, cb, 300, 100, 0.08)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    hits, _ = ctx.map(reads, R, q=12, mode=1)
+    ops_ok, info_ok = ctx.cigar(reads, R, hits)
+    assert info_ok["n_ops"].max() > 1
+    ops = np.zeros(hits.size, np.uint32)
+    info = np.zeros(hits.size, qgm.CIGAR_DTYPE)
+    rc = ctx.lib.qgm_cigar_records(ctx.h, reads.h, R.h, hits.ctypes.data_as(C.c_void_p), hits.size, 32, 1,
+                                   ops.ctypes.data_as(C.c_void_p), info.ctypes.data_as(C.c_void_p))
+    assert rc == 1  # QGM_ERR_INPUT
+    assert np.array_equal(info["n_ops"], info_ok["n_ops"])
+    assert "max_ops" in ctx.lib.qgm_last_error(ctx.h).decode()
