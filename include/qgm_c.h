@@ -224,7 +224,7 @@ int qgm_hits_download(qgm_ctx* ctx, const qgm_hits* h, qgm_hit* out);
  * of the read's records whose identity is >= the record's (edits <=). In
  * best-stratum mode that is the size of the read's best stratum. */
 int qgm_hits_ranks(qgm_ctx* ctx, const qgm_hits* h, uint32_t* rank);
-/* traceback_cigar (DESIGN.md Appendix B.8) of every record,
+/* traceback_cigar (DESIGN.md section 2 item 9) of every record,
  * in download order: the oriented read against its chromosome from ref_start,
  * anchored start, free end, band |j - i| <= band_width - 1. ops[i * max_ops
  * + x] are BAM-style (length << 4 | op, M = 0, I = 1, D = 2). Fails with

@@ -154,7 +154,7 @@ inline unsigned mapping_quality(std::uint32_t rank, std::uint64_t p_size) {
   return r < 0 ? 0u : unsigned(r);
 }
 
-// traceback_cigar (DESIGN.md Appendix B.8) of one record:
+// traceback_cigar (DESIGN.md section 2 item 9) of one record:
 // the alignment's start (leading deletions dropped), its edits and the CIGAR
 // as BAM-style ops (length << 4 | op, M = 0, I = 1, D = 2).
 struct Alignment {

@@ -83,7 +83,7 @@ int orc_validate_cands(const uint8_t* ref_codes, const uint64_t* chrom_begin, ui
   });
 }
 
-// traceback_cigar (Appendix B.8) of explicit 16-byte hit records. ops: n *
+// traceback_cigar (DESIGN.md section 2 item 9) of explicit 16-byte hit records. ops: n *
 // max_ops u32 (BAM-style); info per hit: {ref_start u32, n_ops u16, edits u16}
 // (n_ops > max_ops: truncated).
 int orc_cigar(const uint8_t* ref_codes, const uint64_t* chrom_begin, uint32_t n_chrom, const uint8_t* read_codes,

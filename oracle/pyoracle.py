@@ -125,7 +125,7 @@ class Oracle:
         return out
 
     def cigar(self, ref_codes, chrom_begin, read_codes, stride, lengths, hits, band=32, max_ops=64, threads=0):
-        """traceback_cigar (DESIGN.md Appendix B.8) of hit records -> (ops[n, max_ops] u32, info)."""
+        """traceback_cigar (DESIGN.md section 2 item 9) of hit records -> (ops[n, max_ops] u32, info)."""
         ref_codes = np.ascontiguousarray(ref_codes, dtype=np.uint8)
         cb = np.ascontiguousarray(chrom_begin, dtype=np.uint64)
         read_codes, lengths = _reads_args(read_codes, stride, lengths)

@@ -500,7 +500,7 @@ inline std::vector<Hit> stratify(std::vector<Hit> hits, int mode) {
 }
 
 // ---------------------------------------------------------------- traceback
-// traceback_cigar, frozen as DESIGN.md Appendix B.8: the
+// traceback_cigar, frozen as DESIGN.md section 2 item 9: the
 // oriented read (n bases) against the chromosome from ref_start, global at the
 // start (D[0][j] = j, D[i][0] = i), free at the end, cells restricted to the
 // band |j - i| <= W with W = B - 1 (the validation band widened to both sides:

@@ -362,7 +362,7 @@ class Context:
             self.lib.qgm_hits_destroy(h)
 
     def cigar(self, reads, ref, hits: np.ndarray, band_width: int = 32, max_ops: int | None = None):
-        """traceback_cigar (DESIGN.md Appendix B.8) of hit
+        """traceback_cigar (DESIGN.md section 2 item 9) of hit
         records on the device: (ops[n, max_ops] u32 BAM-style, info[CIGAR_DTYPE]).
         max_ops defaults to 2 * (stride + band_width) + 1, enough for any record."""
         hits = np.ascontiguousarray(hits, dtype=HIT_DTYPE)

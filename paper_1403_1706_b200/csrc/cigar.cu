@@ -1,6 +1,6 @@
 // cigar.cu -- traceback_cigar of mapped hits on the device.
 //
-// Semantics (DESIGN.md Appendix B.8, restated by oracle::traceback_cigar): the
+// Semantics (DESIGN.md section 2 item 9, restated by oracle::traceback_cigar): the
 // oriented read against the chromosome from the hit's ref_start, global at the
 // start (D[0][j] = j, D[i][0] = i), free at the end, band |j - i| <= W = B - 1;
 // end = the largest j with minimal D[n][j] inside the chromosome; traceback

@@ -361,7 +361,7 @@ uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBu
 // hit-rank of every output record: #records of its read
 // whose identity is >= its own (edits <= its edits).
 void hit_ranks(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, uint32_t n_reads, DBuf<uint32_t>& rank);
-// cigar.cu -- traceback_cigar (Appendix B.8) of every hit record: ops (n *
+// cigar.cu -- traceback_cigar (DESIGN.md section 2 item 9) of every hit record: ops (n *
 // max_ops BAM-style u32) and info {ref_start, n_ops | edits << 16}.
 void hits_cigar(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, const Reads& reads, const Ref& ref, unsigned band,
                 uint32_t max_ops, DBuf<uint32_t>& ops, DBuf<uint2>& info);

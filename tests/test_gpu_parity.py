@@ -363,7 +363,7 @@ def _oracle_cigar(oracle, ref, cb, codes, stride, lengths, hits, band):
 
 @pytest.mark.parametrize("band", [32, 64])
 def test_cigar_matches_oracle_on_mapped_hits(ctx, oracle, band):
-    """traceback_cigar (Appendix B.8) of every all-mode hit of a C1-shaped run
+    """traceback_cigar (DESIGN.md section 2 item 9) of every all-mode hit of a C1-shaped run
     with indels, several chromosomes (reads overhanging their ends), both
     strands: device ops and info bit-identical to oracle::traceback_cigar; the
     64-bit band word (B=32) and the 128-bit one (B=64)."""
