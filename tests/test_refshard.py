@@ -87,3 +87,24 @@ def test_reference_sharded_map_equals_single_process(tmp_path, world_size, mode)
     got = np.concatenate(parts)
     assert got.size == want.size and got.size > 1000
     assert np.array_equal(got, want)
+
+
+def test_plan_edge_cases_tiny_references_and_empty_chromosomes():
+    from paper_1403_1706_b200 import refshard
+    # more ranks than bases, and an empty chromosome in the middle
+    cb = np.array([0, 3, 3, 5], np.uint64)
+    shares = refshard.plan(cb, 8, 100, 32)
+    owned = sorted((p.chrom, p.own_begin, p.own_end) for s in shares for p in s)
+    assert sum(e - b for _, b, e in owned) == 5
+    assert all(c != 1 for c, _, _ in owned)  # the empty chromosome owns nothing
+    assert sum(1 for s in shares if not s) >= 3
+    # piece references carry the mask slice
+    ref = np.arange(5, dtype=np.uint8) % 4
+    mask = np.array([0, 1, 0, 1, 1], np.uint8)
+    for s in shares:
+        codes, pcb, m = refshard.piece_reference(ref, cb, s, mask)
+        assert codes.size == int(pcb[-1]) and (m is None or m.size == codes.size)
+    # own_and_translate on an empty share keeps nothing
+    import paper_1403_1706_b200 as qgm
+    h = np.zeros(3, qgm.HIT_DTYPE)
+    assert refshard.own_and_translate(h, []).size == 0
