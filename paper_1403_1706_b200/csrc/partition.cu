@@ -10,14 +10,16 @@
 //   scan         : sub-bin offsets; the P1 bin offsets are their prefixes;
 //   P1 scatter   : per chunk of 2048 q-gram slots (runs of 8 consecutive
 //                  slots per thread sharing one register window of read
-//                  bases), a local counting sort by
-//                  bin in shared memory, one global atomic per bin to reserve
-//                  the chunk's run, then runs copied out with consecutive
-//                  threads writing consecutive 8-byte slots (full sectors;
-//                  ~16 items = one 128 B line per bin per chunk at q=16);
-//   P2 refine    : the same staged counting sort on the next code bits (up to
-//                  16 in total), per chunk of 2048 bin-ordered items, writing
-//                  the final join items at the offsets P0 already counted.
+//                  bases), a local counting sort by bin in shared memory
+//                  (the count atomic's return value is the item's rank),
+//                  one global atomic per bin to reserve the chunk's run,
+//                  then runs copied out with consecutive threads writing
+//                  consecutive 8-byte slots;
+//   P2 refine    : the same staged counting sort on the next code bits (up
+//                  to 16 in total), per chunk of 2048 bin-ordered items that
+//                  a bulk copy (mbarrier) brings into shared memory while
+//                  the previous chunk is written out, producing the final
+//                  join items at the offsets P0 already counted.
 // ncu on an earlier single-pass scatter (12-bit bins, items written straight
 // from registers) showed 1.6 GB of read-for-ownership and 2.1 GB of writes for
 // 0.68 GB of output: partial sectors of 2.4M concurrently open runs.
