@@ -339,9 +339,11 @@ class Context:
                                           pct_identity, _ptr(out)))
         return out
 
-    def map(self, reads, ref, params: MapParams | None = None, ranks: bool = False, **kw):
+    def map(self, reads, ref, params: MapParams | None = None, ranks: bool = False, cigars: bool = False, **kw):
         """Returns (hits[HIT_DTYPE], stats dict) -- with ranks=True also the
-        hit_rank of every record: (hits, stats, ranks)."""
+        hit_rank of every record, with cigars=True also
+        (ops, info) of traceback_cigar computed from the device-resident hits
+        (SPEC.md:476-483): (hits, stats[, ranks][, (ops, info)])."""
         p = params or make_params(**kw)
         h = P()
         self._check(self.lib.qgm_map(self.h, reads.h, ref.h, C.byref(p), C.byref(h)))
@@ -353,11 +355,19 @@ class Context:
             out = np.zeros(n.value, dtype=HIT_DTYPE)
             self._check(self.lib.qgm_hits_download(self.h, h, _ptr(out)))
             stats = {f: getattr(st, f) for f, _ in MapStats._fields_}
-            if not ranks:
-                return out, stats
-            r = np.zeros(max(n.value, 1), dtype=np.uint32)
-            self._check(self.lib.qgm_hits_ranks(self.h, h, _ptr(r)))
-            return out, stats, r[: n.value]
+            res = [out, stats]
+            if ranks:
+                r = np.zeros(max(n.value, 1), dtype=np.uint32)
+                self._check(self.lib.qgm_hits_ranks(self.h, h, _ptr(r)))
+                res.append(r[: n.value])
+            if cigars:
+                band = (params or make_params(**kw)).band_width
+                max_ops = 2 * (reads.stride + band) + 1
+                ops = np.zeros((n.value, max_ops), np.uint32)
+                info = np.zeros(n.value, CIGAR_DTYPE)
+                self._check(self.lib.qgm_hits_cigar(self.h, h, reads.h, ref.h, band, max_ops, _ptr(ops), _ptr(info)))
+                res.append((ops, info))
+            return tuple(res)
         finally:
             self.lib.qgm_hits_destroy(h)
 

@@ -574,3 +574,24 @@ def test_cigar_max_ops_overflow_is_an_input_error_with_counts(ctx):
     assert rc == 1  # QGM_ERR_INPUT
     assert np.array_equal(info["n_ops"], info_ok["n_ops"])
     assert "max_ops" in ctx.lib.qgm_last_error(ctx.h).decode()
+
+
+def test_map_returns_ranks_and_cigars_from_device_hits(ctx):
+    """ctx.map(..., ranks=True, cigars=True): ranks and CIGARs computed from
+    the device-resident hits equal the separate calls on downloaded hits."""
+    import paper_1403_1706_b200 as qgm
+    L = 80_000
+    ref = qgm.random_reference(81, L)
+    cb = np.array([0, L], np.uint64)
+    codes, lengths, *_ = qgm.simulate_reads(82, ref, cb, 400, 100, 0.05)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    hits, st, ranks, (ops, info) = ctx.map(reads, R, q=12, mode=1, ranks=True, cigars=True)
+    h2, _, r2 = ctx.map(reads, R, q=12, mode=1, ranks=True)
+    ops2, info2 = ctx.cigar(reads, R, h2)
+    assert np.array_equal(hits, h2) and np.array_equal(ranks, r2)
+    assert np.array_equal(info, info2)
+    m = np.arange(ops.shape[1])[None, :] < info["n_ops"][:, None]
+    assert np.array_equal(np.where(m, ops, 0), np.where(m, ops2[:, : ops.shape[1]], 0))
+    hits3, st3, (ops3, info3) = ctx.map(reads, R, q=12, mode=1, cigars=True)
+    assert np.array_equal(info3, info)
