@@ -361,9 +361,9 @@ inline VRes validate_dp(const uint8_t* rd, uint32_t n, const uint8_t* win, uint3
   const auto fwd = banded_bottom_row(rd, n, win, L, B);
   int k = kInf;
   for (int v : fwd) k = std::min(k, v);
-  std::vector<uint8_t> rr(rd, rd + n), rw(win, win + L);
-  std::reverse(rr.begin(), rr.end());
-  std::reverse(rw.begin(), rw.end());
+  std::vector<uint8_t> rr(n), rw(L);  // reversed read and window
+  for (uint32_t x = 0; x < n; ++x) rr[x] = rd[n - 1 - x];
+  for (uint32_t x = 0; x < L; ++x) rw[x] = win[L - 1 - x];
   const auto bwd = banded_bottom_row(rr.data(), n, rw.data(), L, B);
   int64_t jmax = -1;
   for (uint32_t j = 0; j <= L; ++j) if (bwd[j] == k) jmax = j;
