@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 
 import numpy as np
 
@@ -262,11 +263,16 @@ class Context:
 
     def __init__(self, device: int = 0, stream: int | None = None):
         self.lib = load_library()
+        self._children = weakref.WeakSet()  # Reads / Reference / Index handles owned by this context
         h = P()
         self._check(self.lib.qgm_ctx_create(device, C.byref(h)), None)
         self.h = h
         if stream is not None:
             self._check(self.lib.qgm_ctx_set_stream(self.h, P(stream)))
+
+    def _adopt(self, obj):
+        self._children.add(obj)
+        return obj
 
     def _check(self, rc, h=...):
         if rc == 0:
@@ -276,7 +282,11 @@ class Context:
         raise {1: InputError, 2: LogicError, 3: CudaError}.get(rc, QgmError)(msg)
 
     def close(self):
+        """Destroy the context; every live child handle is released first
+        (a child's native destroy touches its context)."""
         if getattr(self, "h", None):
+            for child in list(getattr(self, "_children", ())):
+                child.close()
             self.lib.qgm_ctx_destroy(self.h)
             self.h = None
 
@@ -361,11 +371,18 @@ class Context:
                 self._check(self.lib.qgm_hits_ranks(self.h, h, _ptr(r)))
                 res.append(r[: n.value])
             if cigars:
-                band = (params or make_params(**kw)).band_width
-                max_ops = 2 * (reads.stride + band) + 1
-                ops = np.zeros((n.value, max_ops), np.uint32)
+                # like map.hpp run_cigar: a small record first, one retry at
+                # the size the longest record needs
+                band = p.band_width
+                max_ops = 2 * band + 16
                 info = np.zeros(n.value, CIGAR_DTYPE)
-                self._check(self.lib.qgm_hits_cigar(self.h, h, reads.h, ref.h, band, max_ops, _ptr(ops), _ptr(info)))
+                ops = np.zeros((n.value, max_ops), np.uint32)
+                rc = self.lib.qgm_hits_cigar(self.h, h, reads.h, ref.h, band, max_ops, _ptr(ops), _ptr(info))
+                if rc == 1 and n.value and int(info["n_ops"].max()) > max_ops:
+                    max_ops = int(info["n_ops"].max())
+                    ops = np.zeros((n.value, max_ops), np.uint32)
+                    rc = self.lib.qgm_hits_cigar(self.h, h, reads.h, ref.h, band, max_ops, _ptr(ops), _ptr(info))
+                self._check(rc)
                 res.append((ops, info))
             return tuple(res)
         finally:
@@ -456,6 +473,7 @@ class Reads:
         h = P()
         ctx._check(ctx.lib.qgm_reads_upload(ctx.h, _ptr(words), _ptr(lengths), lengths.size, stride, C.byref(h)))
         self.h = h
+        ctx._adopt(self)
 
     @classmethod
     def from_codes(cls, ctx, codes: np.ndarray, lengths: np.ndarray, stride: int):
@@ -463,7 +481,8 @@ class Reads:
 
     def close(self):
         if getattr(self, "h", None):
-            self.ctx.lib.qgm_reads_destroy(self.h)
+            if getattr(self.ctx, "h", None):  # the context destroys nothing twice
+                self.ctx.lib.qgm_reads_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -485,6 +504,7 @@ class Reference:
         h = P()
         ctx._check(ctx.lib.qgm_ref_upload(ctx.h, _ptr(words), _ptr(cb), cb.size - 1, _ptr(mb), C.byref(h)))
         self.h = h
+        ctx._adopt(self)
 
     @classmethod
     def from_codes(cls, ctx, codes: np.ndarray, chrom_begin, mask: np.ndarray | None = None):
@@ -523,7 +543,8 @@ class Reference:
 
     def close(self):
         if getattr(self, "h", None):
-            self.ctx.lib.qgm_ref_destroy(self.h)
+            if getattr(self.ctx, "h", None):  # the context destroys nothing twice
+                self.ctx.lib.qgm_ref_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -538,6 +559,7 @@ class Index:
 
     def __init__(self, ctx: Context, h):
         self.ctx, self.h = ctx, h
+        ctx._adopt(self)
         info = IndexInfo()
         ctx._check(ctx.lib.qgm_index_info_get(h, C.byref(info)))
         self.info = {f: getattr(info, f) for f, _ in IndexInfo._fields_}
@@ -585,7 +607,8 @@ class Index:
 
     def close(self):
         if getattr(self, "h", None):
-            self.ctx.lib.qgm_index_destroy(self.h)
+            if getattr(self.ctx, "h", None):  # the context destroys nothing twice
+                self.ctx.lib.qgm_index_destroy(self.h)
             self.h = None
 
     def __del__(self):

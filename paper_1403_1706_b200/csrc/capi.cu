@@ -1131,11 +1131,13 @@ int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, c
       }
       r.words.swap(s.words);
       r.lengths.swap(s.lens);
-      struct Back {  // the slot keeps its buffers whatever happens
+      struct Back {  // the slot keeps its buffers whatever happens; the planes
+                     // block returns to the cache only after its side-stream build
+        qgm::Ctx& c;
         qgm::Reads& r;
         Slot& s;
-        ~Back() { r.words.swap(s.words); r.lengths.swap(s.lens); }
-      } back{r, s};
+        ~Back() { r.words.swap(s.words); r.lengths.swap(s.lens); c.wait_planes(); }
+      } back{c, r, s};
       {
         qgm::StageScope st(c, qgm::kStageReads);
         qgm::finish_reads(c, r);

@@ -95,15 +95,17 @@ __global__ void __launch_bounds__(kDedupThreads) k_tile_compact(const uint64_t* 
 }
 
 // keys of every (mask+1)-th read (read id = key >> rshift) appended to out
+// (at most cap are stored; n_out keeps counting past cap so the caller sees
+// the overflow)
 __global__ void k_sample_reads(const uint64_t* __restrict__ keys, uint64_t n, unsigned rshift, uint64_t mask,
-                               uint64_t* __restrict__ out, unsigned long long* __restrict__ n_out) {
+                               uint64_t* __restrict__ out, uint64_t cap, unsigned long long* __restrict__ n_out) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i0 = blockIdx.x * uint64_t(blockDim.x); i0 < n; i0 += stride) {  // warp-uniform trip count
     const uint64_t i = i0 + threadIdx.x;
     const uint64_t k = i < n ? keys[i] : 0ull;
     const bool take = i < n && ((k >> rshift) & mask) == 0;
     const unsigned long long at = warp_append(take, n_out);
-    if (take) out[at] = k;
+    if (take && at < cap) out[at] = k;
   }
 }
 
@@ -164,7 +166,7 @@ double estimate_dup_fraction(Ctx& c, const uint64_t* keys, uint64_t n, unsigned 
   DBuf<unsigned long long> ns(c, 1);
   ns.zero();
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
-  QGM_KERNEL(c, k_sample_reads, grid, 256, 0, keys, n, rshift, 63ull, sample.p, ns.p);
+  QGM_KERNEL(c, k_sample_reads, grid, 256, 0, keys, n, rshift, 63ull, sample.p, cap, ns.p);
   unsigned long long m = 0;
   QGM_CUDA(cudaMemcpyAsync(&m, ns.p, sizeof(m), cudaMemcpyDeviceToHost, c.stream));
   QGM_CUDA(cudaStreamSynchronize(c.stream));

@@ -113,9 +113,7 @@ struct ItemGen {
 // u32 word (128 KiB for 16-bit keys) -- and flushes the non-zero counts with
 // global atomics. The P1 bin offsets and the P2 sub-bin offsets both come
 // from this one histogram, so the refinement needs no counting pass. A u16
-// counter that wraps (more than 65535 equal keys in one CTA's share) hands
-// 65536 to the global count and takes back the carry it pushed into its
-// neighbour.
+// counter hands 0x8000 to the global count whenever it reaches 0x8000.
 constexpr int kHistThreads = 1024;
 template <int R>
 __global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen gen, uint32_t n_items, uint32_t per_cta,
@@ -126,12 +124,19 @@ __global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen gen, ui
   for (uint32_t i = threadIdx.x; i < words; i += kHistThreads) h2[i] = 0;
   __syncthreads();
   const uint32_t c0 = blockIdx.x * per_cta, c1 = min(n_items, c0 + per_cta);
+  // Hand-off at half range: the increment that takes a counter from 0x7FFF
+  // to 0x8000 moves 0x8000 to the global count and subtracts it. Counters
+  // rise by 1 per atomic, so exactly one increment sees 0x7FFF per 0x8000
+  // counted. Until the subtraction lands the counter can only climb by the
+  // increments issued in that window (same-address shared atomics retire at
+  // most one per clock: a window of 0x8000 cycles would be needed), so it
+  // never reaches 0xFFFF and never carries into its neighbour.
   auto count = [&](uint32_t key) {
     const uint32_t sh = (key & 1u) * 16u;
     const uint32_t old = atomicAdd(h2 + (key >> 1), 1u << sh);
-    if (((old >> sh) & 0xFFFFu) == 0xFFFFu) {  // wrapped
-      atomicAdd(hist + key, 65536u);
-      if (sh == 0) atomicSub(h2 + (key >> 1), 1u << 16);  // the carry went into the high counter
+    if (((old >> sh) & 0xFFFFu) == 0x7FFFu) {
+      atomicAdd(hist + key, 0x8000u);
+      atomicSub(h2 + (key >> 1), 0x8000u << sh);
     }
   };
   constexpr int kRuns = R == 1 ? 4 : 1;  // runs in flight per thread

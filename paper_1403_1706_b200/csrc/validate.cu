@@ -350,8 +350,11 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
   if (band == 0 || band > 64) throw InputError("band width must be in [1, 64]");
   if (pct > 100) throw InputError("percent identity must be in [0, 100]");
   if (read_bits + 1 + ref.diag_bits > 64) throw InputError("read batch too large for the 64-bit hit key");
+  // the reads' planes are built on the side stream: order the compute stream
+  // after them even when there is nothing to validate (the planes block goes
+  // back to the stream-ordered cache when the Reads object is released)
+  c.wait_planes();
   if (n == 0) return;
-  c.wait_planes();  // the reads' planes are built on the side stream
   ValArgs a;
   a.rplanes = reads.planes.p;
   a.rlen = reads.lengths.p;

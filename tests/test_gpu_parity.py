@@ -263,7 +263,8 @@ def test_streamed_batches_equal_single_calls(ctx):
 def test_partition_counter_wrap_with_a_dominant_qgram(ctx, oracle):
     """100k poly-A reads first in the batch put more than 65535 copies of one
     canonical q-gram into a single histogram CTA's share (the packed u16
-    shared-memory counters wrap and hand 65536 to the global count); the
+    shared-memory counter hands 0x8000 to the global count every time it
+    reaches 0x8000); the
     20k ordinary reads behind them must still map exactly like the oracle."""
     import paper_1403_1706_b200 as qgm
     L = 400_000
