@@ -174,8 +174,11 @@ void qgm_index_destroy(qgm_index* idx);
 
 /* ---- reference: ReferenceIndex sequences ---------------- */
 /* ref2bit: the concatenated chromosomes in the 2-bit format; chrom_begin:
- * n_chrom+1 base offsets; mask_bits (nullable): bit x of word x/64 set =
- * position x excluded from P (repeat mask). */
+ * n_chrom+1 base offsets (host); mask_bits (nullable): bit x of word x/64 set =
+ * position x excluded from P (repeat mask). ref2bit and
+ * mask_bits may be host or device pointers (unified addressing): a multi-GPU
+ * run uploads the reference once and broadcasts the 2-bit words over NVLink,
+ * then every rank calls this with its device copy. */
 int qgm_ref_upload(qgm_ctx* ctx, const uint64_t* ref2bit, const uint64_t* chrom_begin, uint32_t n_chrom,
                    const uint64_t* mask_bits, qgm_ref** out);
 /* Build (and cache on ref) the reference-side q-group indexes for q, one per

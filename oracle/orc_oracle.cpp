@@ -123,10 +123,22 @@ int orc_map(const uint8_t* ref_codes, const uint64_t* chrom_begin, uint32_t n_ch
     P.q = q; P.band = band; P.pct = pct; P.mode = mode; P.strands = strands;
     Stats st;
     std::vector<Hit> h;
-    if (w == 64) h = map_with_index(ref, rs, build_index<uint64_t>(rs, q, sampled != 0), P, threads, &st);
-    else h = map_with_index(ref, rs, build_index<uint32_t>(rs, q, sampled != 0), P, threads, &st);
+    auto t0 = std::chrono::steady_clock::now();
+    if (w == 64) {
+      auto ix = build_index<uint64_t>(rs, q, sampled != 0);
+      st.sec_index = seconds_since(t0);
+      h = map_with_index(ref, rs, ix, P, threads, &st);
+    } else {
+      auto ix = build_index<uint32_t>(rs, q, sampled != 0);
+      st.sec_index = seconds_since(t0);
+      h = map_with_index(ref, rs, ix, P, threads, &st);
+    }
     *hits = orc::make_buf(orc::to_recs(h));
-    if (stats) { stats[0] = st.raw; stats[1] = st.unique; stats[2] = st.validated_kept; stats[3] = st.hits; }
+    if (stats) {
+      stats[0] = st.raw; stats[1] = st.unique; stats[2] = st.validated_kept; stats[3] = st.hits;
+      const double sec[5] = {st.sec_index, st.sec_filter, st.sec_sort, st.sec_validate, st.sec_strata};
+      for (int i = 0; i < 5; ++i) stats[4 + i] = uint64_t(sec[i] * 1e9);  // stage nanoseconds
+    }
   });
 }
 

@@ -152,14 +152,17 @@ def _map(lib, name, b, ref_codes, chrom_begin, read_codes, stride, lengths, q, w
     read_codes, lengths = _reads_args(read_codes, stride, lengths)
     m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
     h = P()
-    stats = np.zeros(4, dtype=np.uint64)
+    stats = np.zeros(9, dtype=np.uint64)  # 4 counts + 5 stage nanoseconds
     f = getattr(lib, name)
     f.argtypes = [P, P, C.c_uint32, P, P, C.c_uint32, P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.c_uint32,
                   C.c_uint32, C.c_int, C.c_int, C.c_uint32, C.POINTER(P), P]
     b.check(f(_p(ref_codes), _p(cb), cb.size - 1, _p(m), _p(read_codes), stride, _p(lengths), lengths.size, q, w,
               int(sampled), band, pct, mode, strands, threads, C.byref(h), _p(stats)))
     hits = b.take(h, HIT_DTYPE)
-    return hits, dict(zip(("raw_candidates", "unique_candidates", "validated", "hits"), stats.tolist()))
+    st = dict(zip(("raw_candidates", "unique_candidates", "validated", "hits"), stats[:4].tolist()))
+    st["stage_seconds"] = dict(zip(("index", "filter", "sort_unique", "validate", "strata"),
+                                   (round(float(x) / 1e9, 4) for x in stats[4:])))
+    return hits, st
 
 
 class RefShim:

@@ -25,6 +25,8 @@
 #pragma once
 
 #include <algorithm>
+#include <type_traits>
+#include <chrono>
 #include <atomic>
 #include <bit>
 #include <cstdint>
@@ -255,6 +257,18 @@ std::vector<Cand> filter(const RefSet& ref, const ReadSet& reads, const IndexT& 
                          int strands = 3, bool run_start = false, unsigned threads = 1) {
   const auto& O = idx.positions();
   const uint32_t m = reads.stride;
+  // the index's arrays, read directly so the random probes can be prefetched
+  using W = std::decay_t<decltype(idx.occupancy()[0])>;
+  constexpr unsigned gw = sizeof(W) * 8;
+  const W* I = idx.occupancy().data();
+  const uint32_t* S = idx.group_starts().data();
+  const uint32_t* S1 = idx.occ_starts().data();
+  const bool smp = idx.sampled();
+  auto group_base = [&](size_t i) -> uint32_t {  // qgroup_index.hpp:91-96
+    if (!smp) return S[i];
+    const uint32_t even = S[i / 2];
+    return (i & 1) ? even + uint32_t(std::popcount(I[i - 1])) : even;
+  };
   struct Job { uint32_t c; uint64_t b, e; };
   std::vector<Job> jobs;
   const uint64_t step = 1 << 16;
@@ -265,27 +279,60 @@ std::vector<Cand> filter(const RefSet& ref, const ReadSet& reads, const IndexT& 
   }
   std::vector<std::vector<Cand>> parts(jobs.size());
   parallel_chunks(jobs.size(), threads, [&](size_t jb, size_t je) {
+    // Positions in blocks of kBlk: (1) rolling codes, prefetch the occupancy
+    // word and group start of every lookup; (2) occupancy test + rank,
+    // prefetch the S' pair; (3) expand the intervals. Same candidates as a
+    // position-by-position index_pair loop (Alg. 2), with
+    // ~2 x kBlk independent memory probes in flight instead of one.
+    constexpr unsigned kBlk = 64;
+    uint32_t code[2][kBlk];
+    int64_t slot[2][kBlk];
+    const uint32_t cmask = q == 16 ? 0xFFFFFFFFu : (1u << (2 * q)) - 1u;
     for (size_t j = jb; j < je; ++j) {
       const Job& J = jobs[j];
       const uint64_t cb = ref.chrom_begin[J.c];
       const uint8_t* R = ref.codes.data() + cb;
       auto& out = parts[j];
-      for (uint64_t p = J.b; p < J.e; ++p) {
-        if (ref.masked(cb + p)) continue;
-        const uint32_t gf = encode_qgram(R + p, q);
-        const bool prev_ok = p >= 1 && !ref.masked(cb + p - 1);
-        if (strands & 1) {
-          if (auto pr = idx.index_pair(gf)) {
-            for (uint32_t k = pr->first; k < pr->second; ++k) {
+      uint32_t gf = 0;
+      for (uint64_t p0 = J.b; p0 < J.e; p0 += kBlk) {
+        const unsigned nb = unsigned(std::min<uint64_t>(kBlk, J.e - p0));
+        for (unsigned t = 0; t < nb; ++t) {
+          const uint64_t p = p0 + t;
+          gf = p == J.b ? encode_qgram(R + p, q) : (((gf << 2) | R[p + q - 1]) & cmask);
+          code[0][t] = gf;
+          code[1][t] = rc_qgram(gf, q);
+          for (int s = 0; s < 2; ++s) {
+            __builtin_prefetch(I + code[s][t] / gw);
+            __builtin_prefetch(S + (smp ? code[s][t] / gw / 2 : code[s][t] / gw));
+          }
+        }
+        for (unsigned t = 0; t < nb; ++t)
+          for (int s = 0; s < 2; ++s) {
+            slot[s][t] = -1;
+            if (!((strands >> s) & 1) || ref.masked(cb + p0 + t)) continue;
+            const uint32_t g = code[s][t];
+            const size_t i = g / gw;
+            const unsigned jj = g % gw;
+            const W word = I[i];
+            if (!((word >> jj) & W(1))) continue;
+            const uint32_t b = group_base(i) + IndexT::rank_below(word, jj);
+            slot[s][t] = b;
+            __builtin_prefetch(S1 + b);
+          }
+        for (unsigned t = 0; t < nb; ++t) {
+          const uint64_t p = p0 + t;
+          const bool prev_ok = p >= 1 && !ref.masked(cb + p - 1);
+          if (slot[0][t] >= 0) {
+            const uint32_t k0 = S1[slot[0][t]], k1 = S1[slot[0][t] + 1];
+            for (uint32_t k = k0; k < k1; ++k) {
               const uint32_t r = O[k] / m, o = O[k] % m;
               if (run_start && prev_ok && o >= 1 && R[p - 1] == reads.read(r)[o - 1]) continue;
               out.push_back({r, J.c, int64_t(p) - int64_t(o), 0});
             }
           }
-        }
-        if (strands & 2) {
-          if (auto pr = idx.index_pair(rc_qgram(gf, q))) {
-            for (uint32_t k = pr->first; k < pr->second; ++k) {
+          if (slot[1][t] >= 0) {
+            const uint32_t k0 = S1[slot[1][t]], k1 = S1[slot[1][t] + 1];
+            for (uint32_t k = k0; k < k1; ++k) {
               const uint32_t r = O[k] / m, o = O[k] % m, n = reads.lengths[r];
               if (run_start && prev_ok && o + q + 1 <= n &&
                   uint8_t(3u - R[p - 1]) == reads.read(r)[o + q])
@@ -379,16 +426,22 @@ inline VRes validate_dp(const uint8_t* rd, uint32_t n, const uint8_t* win, uint3
 inline VRes validate_myers(const uint8_t* rd, uint32_t n, const uint8_t* win, uint32_t L, unsigned B) {
   if (B == 0 || B > kMaxBand || L != n + B - 1) throw input_error("band/window mismatch");
   const uint64_t mask = B == 64 ? ~uint64_t(0) : ((uint64_t(1) << B) - 1);
+  // peq[c] bit y: reversed window rw[y] = win[L-1-y] equals base c (the
+  // sentinel matches nothing); row i's Eq is the 64-bit slice at y = i-1
+  const size_t nw = (L + 63) / 64 + 2;
+  thread_local std::vector<uint64_t> peq;
+  peq.assign(4 * nw, 0);
+  for (uint32_t y = 0; y < L; ++y) {
+    const uint8_t wc = win[L - 1 - y];
+    if (wc < 4) peq[wc * nw + y / 64] |= uint64_t(1) << (y % 64);
+  }
   uint64_t Pv = 0, Mv = 0;
   int64_t score0 = 0;  // D[i][0]
   for (uint32_t i = 1; i <= n; ++i) {
     const uint8_t c = rd[n - i];  // reversed read at row i: rr[i-1] = rd[n-1-(i-1)]
-    uint64_t Eq = 0;
-    for (unsigned t = 0; t < B; ++t) {
-      // reversed window at column i-1+t: rw[y] = win[L-1-y]
-      const uint8_t wc = win[L - 1 - (i - 1 + t)];
-      if (wc == c) Eq |= uint64_t(1) << t;
-    }
+    const uint64_t* pw = peq.data() + size_t(c & 3) * nw;
+    const uint32_t y = i - 1, wi = y / 64, sh = y % 64;
+    const uint64_t Eq = c < 4 ? ((pw[wi] >> sh) | (sh ? pw[wi + 1] << (64 - sh) : 0)) & mask : 0;
     const uint64_t X = Eq | (Mv >> 1);
     const uint64_t Pp = Pv >> 1;
     const uint64_t Z = ((((X & Pp) + Pp) ^ Pp) | X) & mask;
@@ -456,14 +509,16 @@ inline Validated validate_candidate(const RefSet& ref, const ReadSet& reads, con
   Validated v{0, 0, 0, false, false};
   if (w0 + int64_t(L) <= 0 || w0 >= Lc) return v;
   v.in_range = true;
-  std::vector<uint8_t> win(L);
+  thread_local std::vector<uint8_t> win, rd;  // reused: no allocation per candidate
+  win.resize(L);
   const uint8_t* R = ref.codes.data() + ref.chrom_begin[c.chrom];
   for (uint32_t j = 0; j < L; ++j) {
     const int64_t x = w0 + j;
     win[j] = (x >= 0 && x < Lc) ? R[x] : kSentinel;
   }
-  std::vector<uint8_t> rd(reads.read(c.read), reads.read(c.read) + n);
-  if (c.strand) rd = reverse_complement(rd.data(), n);
+  rd.resize(n);
+  const uint8_t* src = reads.read(c.read);
+  for (uint32_t j = 0; j < n; ++j) rd[j] = c.strand ? uint8_t(3u - src[n - 1 - j]) : src[j];
   const VRes r = use_dp ? validate_dp(rd.data(), n, win.data(), L, B)
                         : validate_myers(rd.data(), n, win.data(), L, B);
   v.k = r.k;
@@ -580,7 +635,13 @@ inline Cigar traceback_cigar(const uint8_t* rd, uint32_t n, const uint8_t* chrom
 
 struct Stats {
   uint64_t raw = 0, unique = 0, validated_kept = 0, hits = 0;
+  // wall seconds per stage: index build (filled by the caller), filtration,
+  // sort + unique, validation, strata
+  double sec_index = 0, sec_filter = 0, sec_sort = 0, sec_validate = 0, sec_strata = 0;
 };
+inline double seconds_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
 
 // run_map core for one read buffer: filter every chromosome,
 // dedup candidates, validate, stratify.
@@ -589,11 +650,16 @@ std::vector<Hit> map_with_index(const RefSet& ref, const ReadSet& reads, const I
                                 const Params& P, unsigned threads = 1, Stats* st = nullptr) {
   if (P.band == 0 || P.band > kMaxBand) throw input_error("band must be in [1, 64]");
   if (P.pct > 100) throw input_error("percent identity must be in [0, 100]");
+  auto t0 = std::chrono::steady_clock::now();
   std::vector<Cand> c = filter(ref, reads, idx, P.q, P.strands, /*run_start=*/false, threads);
   if (st) st->raw = c.size();
+  if (st) st->sec_filter = seconds_since(t0);
+  t0 = std::chrono::steady_clock::now();
   parallel_sort_by_read(c, reads.count(), threads, [](const Cand& x) { return x.read; });
   c.erase(std::unique(c.begin(), c.end()), c.end());
   if (st) st->unique = c.size();
+  if (st) st->sec_sort = seconds_since(t0);
+  t0 = std::chrono::steady_clock::now();
   std::vector<Hit> hits_all(c.size());
   std::vector<uint8_t> keep(c.size(), 0);
   parallel_chunks(c.size(), threads, [&](size_t b, size_t e) {
@@ -608,6 +674,8 @@ std::vector<Hit> map_with_index(const RefSet& ref, const ReadSet& reads, const I
   std::vector<Hit> kept;
   for (size_t i = 0; i < c.size(); ++i) if (keep[i]) kept.push_back(hits_all[i]);
   if (st) st->validated_kept = kept.size();
+  if (st) st->sec_validate = seconds_since(t0);
+  t0 = std::chrono::steady_clock::now();
   // stratify per contiguous read range, in parallel (input sorted by read)
   threads = eff_threads(threads);
   std::vector<size_t> cuts{0};
@@ -625,6 +693,7 @@ std::vector<Hit> map_with_index(const RefSet& ref, const ReadSet& reads, const I
   std::vector<Hit> out;
   for (auto& o : outs) out.insert(out.end(), o.begin(), o.end());
   if (st) st->hits = out.size();
+  if (st) st->sec_strata = seconds_since(t0);
   return out;
 }
 

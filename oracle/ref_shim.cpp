@@ -170,6 +170,7 @@ int ref_map(const uint8_t* ref_codes, const uint64_t* chrom_begin, uint32_t n_ch
   return guarded_ref([&] {
     auto ref = orc::make_ref(ref_codes, chrom_begin, n_chrom, mask);
     auto rs = orc::make_reads(read_codes, stride, lengths, n_reads);
+    auto t0 = std::chrono::steady_clock::now();  // stage 1 = pack_encoded_reads + build_qgroup_index
     auto text = make_text(read_codes, stride, lengths, n_reads, q);
     qgm_oracle::Params P;
     P.q = q; P.band = band; P.pct = pct; P.mode = mode; P.strands = strands;
@@ -179,14 +180,20 @@ int ref_map(const uint8_t* ref_codes, const uint64_t* chrom_begin, uint32_t n_ch
     if (w == 64) {
       auto ix = qgmap::build_qgroup_index<uint64_t>(text, th);
       if (sampled) ix = qgmap::sample_group_starts(ix);
+      st.sec_index = qgm_oracle::seconds_since(t0);
       h = qgm_oracle::map_with_index(ref, rs, ix, P, th, &st);
     } else {
       auto ix = qgmap::build_qgroup_index<uint32_t>(text, th);
       if (sampled) ix = qgmap::sample_group_starts(ix);
+      st.sec_index = qgm_oracle::seconds_since(t0);
       h = qgm_oracle::map_with_index(ref, rs, ix, P, th, &st);
     }
     *hits = orc::make_buf(orc::to_recs(h));
-    if (stats) { stats[0] = st.raw; stats[1] = st.unique; stats[2] = st.validated_kept; stats[3] = st.hits; }
+    if (stats) {
+      stats[0] = st.raw; stats[1] = st.unique; stats[2] = st.validated_kept; stats[3] = st.hits;
+      const double sec[5] = {st.sec_index, st.sec_filter, st.sec_sort, st.sec_validate, st.sec_strata};
+      for (int i = 0; i < 5; ++i) stats[4 + i] = uint64_t(sec[i] * 1e9);  // stage nanoseconds
+    }
   });
 }
 

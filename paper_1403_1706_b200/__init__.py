@@ -495,14 +495,21 @@ class Reads:
 class Reference:
     """Reference sequences on the device (concatenated chromosomes, optional repeat mask)."""
 
-    def __init__(self, ctx: Context, words: np.ndarray, chrom_begin, mask_bits: np.ndarray | None = None):
+    def __init__(self, ctx: Context, words, chrom_begin, mask_bits: np.ndarray | None = None):
+        """words: the 2-bit words as a host array, or an int device pointer
+        (e.g. the broadcast copy of a multi-GPU run; qgm_ref_upload takes
+        either)."""
         self.ctx = ctx
         cb = np.ascontiguousarray(chrom_begin, dtype=np.uint64)
         self.chrom_begin = cb
-        words = np.ascontiguousarray(words, dtype=np.uint64)
+        if isinstance(words, int):
+            wp = P(words)
+        else:
+            words = np.ascontiguousarray(words, dtype=np.uint64)
+            wp = _ptr(words)
         mb = None if mask_bits is None else np.ascontiguousarray(mask_bits, dtype=np.uint64)
         h = P()
-        ctx._check(ctx.lib.qgm_ref_upload(ctx.h, _ptr(words), _ptr(cb), cb.size - 1, _ptr(mb), C.byref(h)))
+        ctx._check(ctx.lib.qgm_ref_upload(ctx.h, wp, _ptr(cb), cb.size - 1, _ptr(mb), C.byref(h)))
         self.h = h
         ctx._adopt(self)
 

@@ -706,7 +706,7 @@ int qgm_ref_upload(qgm_ctx* ctx, const uint64_t* ref2bit, const uint64_t* chrom_
     require(r.diag_bits <= 40, "reference too large");
     const uint64_t nw = qgm::ceil_div(r.total, 32);
     r.words.alloc(c, nw + 1);
-    if (nw) QGM_CUDA(cudaMemcpyAsync(r.words.p, ref2bit, nw * 8, cudaMemcpyHostToDevice, c.stream));
+    if (nw) QGM_CUDA(cudaMemcpyAsync(r.words.p, ref2bit, nw * 8, cudaMemcpyDefault, c.stream));  // host or device
     QGM_CUDA(cudaMemsetAsync(r.words.p + nw, 0, 8, c.stream));
     r.d_cb.alloc(c, n_chrom + 1);
     r.d_cbp.alloc(c, n_chrom + 1);
@@ -715,7 +715,7 @@ int qgm_ref_upload(qgm_ctx* ctx, const uint64_t* ref2bit, const uint64_t* chrom_
     if (mask_bits) {
       const uint64_t mw = qgm::ceil_div(r.total, 64);
       r.mask.alloc(c, std::max<uint64_t>(mw, 1));
-      if (mw) QGM_CUDA(cudaMemcpyAsync(r.mask.p, mask_bits, mw * 8, cudaMemcpyHostToDevice, c.stream));
+      if (mw) QGM_CUDA(cudaMemcpyAsync(r.mask.p, mask_bits, mw * 8, cudaMemcpyDefault, c.stream));
     }
     qgm::make_ref_planes(c, r);
     QGM_CUDA(cudaStreamSynchronize(c.stream));

@@ -1,8 +1,10 @@
-"""World-size-2 gloo tests (CPU) of the multi-GPU plumbing used by bench.py:
-read sharding, max-over-ranks timing and hit-count aggregation. Each rank maps
-its shard with the CPU oracle (the stand-in for its GPU) and the union of the
-per-rank hits must equal the single-process result: sharding reads changes
-nothing but read ids."""
+"""World-size-2 gloo tests (CPU) of the multi-GPU plumbing bench.py uses
+(paper_1403_1706_b200/sharding.py): read blocks per rank (weak and strong
+scaling), the reference broadcast, max-over-ranks timing, and the end-of-run
+HostGather of every rank's hits into one shared host buffer. Each rank maps
+its blocks with the CPU oracle (the stand-in for its GPU); the gathered hits
+must equal the single-process result over the same reads, and the parity
+digest must not depend on the world size."""
 import os
 import socket
 
@@ -11,6 +13,8 @@ import pytest
 import torch.multiprocessing as mp
 
 from qgm_testutil import ROOT
+
+L, BLOCK, N_BLOCKS = 200_000, 500, 4
 
 
 def _free_port():
@@ -21,28 +25,47 @@ def _free_port():
     return p
 
 
+def _data():
+    import paper_1403_1706_b200 as qgm
+    ref = qgm.random_reference(3, L)
+    cb = np.array([0, 120_000, L], np.uint64)
+    return qgm, ref, cb
+
+
+def _block(qgm, ref, cb, b):
+    codes, lengths, *_ = qgm.simulate_reads(1000 + b, ref, cb, BLOCK, 100, 0.03)
+    return codes, lengths
+
+
 def _worker(rank, world_size, port, out_dir):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
     from oracle.pyoracle import Oracle
     from paper_1403_1706_b200 import sharding
-    import paper_1403_1706_b200 as qgm
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world_size)
-    L, N = 200_000, 1_500
-    ref = qgm.random_reference(3, L)
-    cb = np.array([0, 120_000, L], np.uint64)
-    codes, lengths, *_ = qgm.simulate_reads(4, ref, cb, N, 100, 0.03)
-    b, e = sharding.shard_range(N, rank, world_size)
-    hits, st = Oracle().map(ref, cb, codes[b * 100:e * 100], 100, lengths[b:e], q=12, mode=1, threads=2)
-    hits["read_id"] += b
-    ms = [float(10 + rank)]
-    mx = sharding.max_over_ranks(ms, dist)
-    tot = sharding.sum_over_ranks([hits.size], dist)
-    np.save(os.path.join(out_dir, f"hits_{rank}.npy"), hits)
-    np.save(os.path.join(out_dir, f"red_{rank}.npy"), np.array([mx[0], tot[0]]))
+    qgm, ref, cb = _data()
+    # the reference: rank 0's words broadcast to every rank
+    words = qgm.pack_codes(ref) if rank == 0 else None
+    t, _ = sharding.broadcast_reference(words, (L + 31) // 32 + 1, dist, "cpu")
+    np.save(os.path.join(out_dir, f"ref_{rank}.npy"), t.numpy())
+    # strong scaling: the job's N_BLOCKS blocks split over the ranks
+    blocks = sharding.read_blocks(rank, world_size, total_blocks=N_BLOCKS)
+    parts = []
+    for b in blocks:
+        codes, lengths = _block(qgm, ref, cb, b)
+        hits, _ = Oracle().map(ref, cb, codes, 100, lengths, q=12, mode=1, threads=2)
+        parts.append(hits)
+    g = sharding.HostGather(dist, "cpu")
+    got = g.gather(parts, qgm.HIT_DTYPE)
+    mx = sharding.max_over_ranks([float(10 + rank)], dist)
+    if rank == 0:
+        segs = [b for r in range(world_size) for b in sharding.read_blocks(r, world_size, total_blocks=N_BLOCKS)]
+        got["read_id"] += np.repeat(np.array(segs, np.uint64) * BLOCK, g.last["segments"]).astype(np.uint32)
+        np.save(os.path.join(out_dir, "gathered.npy"), got)
+        np.save(os.path.join(out_dir, "max.npy"), np.array(mx))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -58,24 +81,46 @@ def test_shard_range_covers_reads_once():
             assert max(sizes) - min(sizes) <= 1
 
 
+def test_read_blocks_weak_and_strong():
+    from paper_1403_1706_b200 import sharding
+    assert sharding.read_blocks(2, 4, blocks_per_rank=3) == [6, 7, 8]
+    for G in (1, 2, 4, 8):
+        allb = [b for r in range(G) for b in sharding.read_blocks(r, G, total_blocks=8)]
+        assert allb == list(range(8))  # the same job at every world size
+
+
 def test_weak_scaling_value():
     from paper_1403_1706_b200 import sharding
     assert sharding.weak_scaling_value(1_000_000, 5, 4, 2000.0) == pytest.approx(1e7)
 
 
-def test_two_rank_gloo_sharded_map_equals_single_process(tmp_path, oracle):
+def test_hits_digest_is_order_free():
     import paper_1403_1706_b200 as qgm
+    from paper_1403_1706_b200 import sharding
+    h = np.zeros(5, qgm.HIT_DTYPE)
+    h["read_id"] = [3, 1, 2, 1, 0]
+    h["ref_start"] = [9, 8, 7, 6, 5]
+    assert sharding.hits_digest(h) == sharding.hits_digest(h[::-1].copy())
+    h2 = h.copy()
+    h2["edits"][0] = 1
+    assert sharding.hits_digest(h) != sharding.hits_digest(h2)
+
+
+@pytest.mark.parametrize("world_size", [2, 3])
+def test_gloo_gather_of_sharded_maps_equals_single_process(tmp_path, oracle, world_size):
+    from paper_1403_1706_b200 import sharding
     port = _free_port()
-    mp.start_processes(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True, start_method="spawn")
-    parts = [np.load(tmp_path / f"hits_{r}.npy") for r in range(2)]
-    red = [np.load(tmp_path / f"red_{r}.npy") for r in range(2)]
-    merged = np.concatenate(parts)
-    L, N = 200_000, 1_500
-    ref = qgm.random_reference(3, L)
-    cb = np.array([0, 120_000, L], np.uint64)
-    codes, lengths, *_ = qgm.simulate_reads(4, ref, cb, N, 100, 0.03)
+    mp.start_processes(_worker, args=(world_size, port, str(tmp_path)), nprocs=world_size, join=True,
+                       start_method="spawn")
+    qgm, ref, cb = _data()
+    words = qgm.pack_codes(ref)
+    for r in range(world_size):
+        assert np.array_equal(np.load(tmp_path / f"ref_{r}.npy").view(np.uint64), words[: (L + 31) // 32 + 1])
+    got = np.load(tmp_path / "gathered.npy")
+    codes = np.concatenate([_block(qgm, ref, cb, b)[0] for b in range(N_BLOCKS)])
+    lengths = np.concatenate([_block(qgm, ref, cb, b)[1] for b in range(N_BLOCKS)])
     whole, _ = oracle.map(ref, cb, codes, 100, lengths, q=12, mode=1, threads=2)
+    assert sharding.hits_digest(got) == sharding.hits_digest(whole)
     cols = ("read_id", "chrom", "ref_start", "edits", "strand")
-    assert all(np.array_equal(merged[c], whole[c]) for c in cols)
-    assert all(r[0] == 11.0 for r in red)          # max over ranks
-    assert all(r[1] == merged.size for r in red)   # hit counts summed
+    assert all(np.array_equal(got[c], whole[c]) for c in cols)
+    assert float(np.load(tmp_path / "max.npy")[0]) == 10.0 + world_size - 1
