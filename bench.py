@@ -588,6 +588,131 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
+def run_refshard(args):
+    """--shard ref: every rank maps the SAME read batch
+    against its share of the reference (refshard.plan: equal owned lengths,
+    chromosomes cut where a share fills); the hit records stay on the device
+    and the exchange -- MIN all-reduce of each read's best k (best mode) and an
+    all-to-all of the records to the read's owner -- runs on CUDA tensors over
+    NCCL (gloo + host tensors when ranks share a GPU). One step = one batch
+    mapped by the whole job; timed on the host around the synchronised step
+    (the exchange is host-driven), max over ranks."""
+    import ctypes as C
+
+    import torch
+
+    import paper_1403_1706_b200 as qgm
+    from paper_1403_1706_b200 import refshard, sharding
+
+    rank, world, device, dist, backend, oversub = init_dist(args)
+    xdev = "cpu" if backend == "gloo" else f"cuda:{device}"
+    coll_dev = xdev
+    cfg = CONFIGS[args.config]
+    q, mode, band, rlen = cfg["q"], cfg["mode"], cfg["band"], cfg["rlen"]
+    ref, cb = make_reference(qgm, cfg)
+    codes, lengths = make_block(qgm, cfg, ref, cb, 0)
+    ctx = qgm.Context(device)
+    mask = None
+    if cfg["mask_threshold"]:  # counted over whole chromosomes, then sliced per piece
+        Rw = qgm.Reference.from_codes(ctx, ref, cb).mask_repeats(q, cfg["mask_threshold"])
+        mask = Rw.mask()
+        Rw.close()
+    mine = refshard.plan(cb, world, rlen, band)[rank]
+    pc, pcb, pm = refshard.piece_reference(ref, cb, mine, mask)
+    t0 = time.perf_counter()
+    R = qgm.Reference.from_codes(ctx, pc, pcb, mask=pm).prepare(q) if mine else None
+    prep_s = time.perf_counter() - t0
+    words = qgm.pack_read_codes(codes, rlen)
+    d_words = torch.from_numpy(words.view(np.int64)).to(f"cuda:{device}")
+    d_len = torch.from_numpy(lengths.view(np.int32)).to(f"cuda:{device}")
+    pall = qgm.make_params(q=q, mode=1, band_width=band, pct_identity=cfg["pct"])
+    lib = ctx.lib
+    n_reads = lengths.size
+
+    def step():
+        t_map = time.perf_counter()
+        local = torch.zeros((0, 4), dtype=torch.int32, device=xdev)
+        st = None
+        if R is not None:
+            rd, h = C.c_void_p(), C.c_void_p()
+            ctx._check(lib.qgm_reads_from_device(ctx.h, C.c_void_p(d_words.data_ptr()), C.c_void_p(d_len.data_ptr()),
+                                                 n_reads, rlen, C.byref(rd)))
+            try:
+                ctx._check(lib.qgm_map(ctx.h, rd, R.h, C.byref(pall), C.byref(h)))
+                n = C.c_uint64()
+                lib.qgm_hits_count(h, C.byref(n))
+                s_ = qgm.MapStats()
+                lib.qgm_hits_stats(h, C.byref(s_))
+                st = {f: getattr(s_, f) for f, _ in qgm.MapStats._fields_}
+                local = torch.empty((n.value, 4), dtype=torch.int32, device=f"cuda:{device}")
+                if n.value:
+                    ctx._check(lib.qgm_hits_download(ctx.h, h, C.c_void_p(local.data_ptr())))
+            finally:
+                lib.qgm_hits_destroy(h)
+                lib.qgm_reads_destroy(rd)
+            local = refshard.own_and_translate(local.to(xdev), mine)
+        if xdev.startswith("cuda"):
+            torch.cuda.synchronize(device)
+        t_x = time.perf_counter()
+        out = refshard.combine(local, n_reads, mode, dist)
+        if xdev.startswith("cuda"):
+            torch.cuda.synchronize(device)
+        t_end = time.perf_counter()
+        return out, st, (t_x - t_map) * 1e3, (t_end - t_x) * 1e3
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    times, xms, mms = [], [], []
+    with ClockSampler(device, period=args.clock_period) as clk:
+        for _ in range(args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            out, st, m_ms, x_ms = step()
+            times.append((time.perf_counter() - t0) * 1e3)
+            mms.append(m_ms)
+            xms.append(x_ms)
+    clocks = clk.summary()
+    tot, xsum, msum = sharding.max_over_ranks([sum(times), sum(xms), sum(mms)], dist, device=coll_dev)
+    mine_hits = refshard.from_records(out)
+    gathered = sharding.HostGather(dist, coll_dev).gather(mine_hits)
+    line = None
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(n_reads * args.steps / (tot / 1e3), 1), "unit": "reads/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps, 3),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+                "data": "synthetic (seeded reference and simulated reads)", "shard": "reference",
+                "config": dict(config_dict(args.config, cfg, world), reads_per_step=n_reads,
+                               parallelism=f"reference sharded over {world} rank(s), reads replicated"),
+                "map_ms_per_step": round(msum / args.steps, 3), "exchange_ms_per_step": round(xsum / args.steps, 3),
+                "exchange": {"backend": backend or "none (world 1)", "device": xdev,
+                             "steps": "MIN all-reduce of per-read k (best mode) + all-to-all of 16-byte records"},
+                "piece_prepare_s": round(prep_s, 3), "clocks": clocks, "counts_rank0": st,
+                "hits": int(gathered.size), "digest": sharding.hits_digest(gathered)}
+        if oversub:
+            line["oversubscribed"] = True
+        if args.check != "off":  # whole reference on rank 0's GPU: same hits?
+            Rw = qgm.Reference.from_codes(ctx, ref, cb, mask=mask)
+            reads = qgm.Reads(ctx, words, lengths, rlen)
+            want, _ = ctx.map(reads, Rw, q=q, mode=mode, band_width=band, pct_identity=cfg["pct"])
+            line["parity"] = {"ok": sharding.hits_digest(want) == line["digest"], "whole_reference_hits": int(want.size),
+                              "what": "digest of the gathered per-owner hits vs one GPU mapping the whole reference"}
+            reads.close()
+            Rw.close()
+        print(json.dumps(line), flush=True)
+    if R is not None:
+        R.close()
+    ctx.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def postprocess_pass(ctx, lib, C, qgm, R, d_words, d_len, n_reads, rlen, params, band):
     """SPEC.md:446-483 tail on one batch's device-resident hits (not part of
     `value`): hit_rank and traceback_cigar, CUDA-event kernel times, second of
@@ -762,6 +887,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (parity still per --check)")
     ap.add_argument("--cpu-samples", type=int, default=1, help="cpu_baseline: best of this many runs")
     ap.add_argument("--clock-period", type=float, default=0.005, help="NVML clock sampling period (s)")
+    ap.add_argument("--shard", default="reads", choices=["reads", "ref"],
+                    help="reads: read-sharded replicas (default); ref: reference sharded, reads replicated, "
+                         "device-resident exchange (SURVEY 8(f) row 2)")
     # internal: the CPU leg child process
     ap.add_argument("--cpu-leg", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--sample", type=int, default=0, help=argparse.SUPPRESS)
@@ -776,6 +904,8 @@ def main():
         relaunch_under_torchrun(args)
     if args.impl == "reference":
         return run_reference(args)
+    if args.shard == "ref":
+        return run_refshard(args)
     return run_gpu(args)
 
 

@@ -222,6 +222,8 @@ int qgm_map(qgm_ctx* ctx, const qgm_reads* reads, const qgm_ref* ref, const qgm_
             qgm_hits** out);
 int qgm_hits_count(const qgm_hits* h, uint64_t* n);
 int qgm_hits_stats(const qgm_hits* h, qgm_map_stats* out);
+/* out: n records, host or device memory (a device destination keeps the
+ * hits on the GPU, e.g. for the reference-sharded exchange over NCCL). */
 int qgm_hits_download(qgm_ctx* ctx, const qgm_hits* h, qgm_hit* out);
 /* hit_rank of every record, in download order: the number
  * of the read's records whose identity is >= the record's (edits <=). In

@@ -358,13 +358,29 @@ void parallel_sort_by_read(std::vector<T>& v, uint32_t n_reads, unsigned threads
   threads = eff_threads(threads);
   if (threads <= 1 || v.size() < 100000 || n_reads == 0) { std::sort(v.begin(), v.end()); return; }
   const unsigned nb = threads * 4;
-  std::vector<size_t> cnt(nb + 1, 0);
   auto bucket = [&](const T& x) { return unsigned(uint64_t(read_of(x)) * nb / n_reads); };
-  for (auto& x : v) cnt[bucket(x) + 1]++;
-  for (unsigned b = 0; b < nb; ++b) cnt[b + 1] += cnt[b];
+  // per-thread bucket counts over contiguous slices, then a parallel scatter
+  const size_t per = (v.size() + threads - 1) / threads;
+  std::vector<std::vector<size_t>> tc(threads, std::vector<size_t>(nb, 0));
+  parallel_chunks(threads, threads, [&](size_t t0, size_t t1) {
+    for (size_t t = t0; t < t1; ++t)
+      for (size_t i = t * per; i < std::min(v.size(), (t + 1) * per); ++i) tc[t][bucket(v[i])]++;
+  });
+  std::vector<size_t> cnt(nb + 1, 0);
+  for (unsigned b = 0; b < nb; ++b) {
+    size_t run = cnt[b];
+    for (unsigned t = 0; t < threads; ++t) {
+      const size_t c = tc[t][b];
+      tc[t][b] = run;
+      run += c;
+    }
+    cnt[b + 1] = run;
+  }
   std::vector<T> tmp(v.size());
-  std::vector<size_t> cur(cnt.begin(), cnt.end() - 1);
-  for (auto& x : v) tmp[cur[bucket(x)]++] = x;
+  parallel_chunks(threads, threads, [&](size_t t0, size_t t1) {
+    for (size_t t = t0; t < t1; ++t)
+      for (size_t i = t * per; i < std::min(v.size(), (t + 1) * per); ++i) tmp[tc[t][bucket(v[i])]++] = v[i];
+  });
   parallel_chunks(nb, threads, [&](size_t b0, size_t b1) {
     for (size_t b = b0; b < b1; ++b) std::sort(tmp.begin() + cnt[b], tmp.begin() + cnt[b + 1]);
   });

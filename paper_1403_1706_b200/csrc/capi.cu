@@ -346,7 +346,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   {
     StageScope s(c, kStageValidate);
     validate_candidates(c, reads, ref, alt.p, n_raw, rb, P.band_width, P.pct_identity, 0, hkeys.p, hvals.p, cnt.p,
-                        nullptr, cnt.p + 1);
+                        nullptr, cnt.p + 1, P.mode == 0);
   }
   if (after_filter && hook_at == 2) after_filter();
   DBuf<uint32_t> per_read;
@@ -929,8 +929,8 @@ int qgm_hits_download(qgm_ctx* ctx, const qgm_hits* h, qgm_hit* out) {
   return guard(ctx, [&] {
     activate(ctx);
     qgm::StageScope s(ctx->c, qgm::kStageD2H);
-    if (h->h.n)
-      QGM_CUDA(cudaMemcpyAsync(out, h->h.hits.p, h->h.n * 16, cudaMemcpyDeviceToHost, ctx->c.stream));
+    if (h->h.n)  // host or device destination (unified addressing)
+      QGM_CUDA(cudaMemcpyAsync(out, h->h.hits.p, h->h.n * 16, cudaMemcpyDefault, ctx->c.stream));
     QGM_CUDA(cudaStreamSynchronize(ctx->c.stream));
   });
 }

@@ -381,6 +381,7 @@ void hits_cigar(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, const Reads& read
   for (uint32_t k = 0; k < ref.n_chrom; ++k)
     if (ref.cb[k + 1] - ref.cb[k] >= (uint64_t(1) << 31) - 64) throw InputError("cigar: chromosome of 2^31 bases or more");
   ops.alloc(c, std::max<uint64_t>(n * max_ops, 1));
+  ops.zero();  // slots past a record's n_ops read as 0 (the whole array is copied out)
   info.alloc(c, std::max<uint64_t>(n, 1));
   if (n == 0) return;
   CigarArgs a;

@@ -313,19 +313,21 @@ uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Re
 // partition.cu -- the batch's read q-grams grouped by the top min(2q,16)
 // bits of their CANONICAL code (sub-bins), one 64-bit join item each:
 //   bits  0..31  read text position pp = r * stride + o
-//   bits 32..40  tail = n_r - q - o (clamped to 511; the join reloads n_r when
-//                stride - q > 511)
-//   bits 41..43  read base at o - 1 (forward run-start compare), 4 = none
-//   bits 44..46  complement of the read base at o + q (reverse run-start
+//   bits 33..35  read base at o - 1 (forward run-start compare), 4 = none
+//   bits 36..38  complement of the read base at o + q (reverse run-start
 //                compare), 4 = none
-//   bit  47      fr = (read code != canonical code)
-//   bits 48..63  the canonical code bits below the sub-bin prefix
-constexpr unsigned kItemTailShift = 32, kItemFbShift = 41, kItemRbShift = 44, kItemFrShift = 47, kItemCodeShift = 48;
-constexpr uint32_t kItemTailMax = 511;
+//   bit  39      fr = (read code != canonical code)
+//   bits 40..63  the canonical code bits below the first pass's 8-bit bin
+//                (the join ORs them with its sub-bin prefix; the bits the
+//                refinement grouped by are implied by the sub-bin)
+// The first pass writes the item in its final form; the refinement only
+// permutes items.
+constexpr unsigned kItemFbShift = 33, kItemRbShift = 36, kItemFrShift = 39, kItemCodeShift = 40;
 struct Partitioned {
   unsigned q = 0;
   uint32_t bins = 0, V = 0;
   unsigned sub_bits = 0;  // sub-bin = code >> (2q - sub_bits); sub_bits = min(2q, 16)
+  bool uniform = false;   // every read has length `stride` (n - q - o from pp alone)
   DBuf<uint32_t> boff;    // 8-bit bin offsets (first pass)
   DBuf<uint32_t> soff;    // sub-bin offsets, 2^sub_bits + 1 entries
   DBuf<uint64_t> pairs;
@@ -341,11 +343,13 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
 // mode 0: append kept hits as (hit key, k) to hit_keys/hit_vals (counter in
 //         *d_count); mode 1: write one qgm_validated per candidate.
 // d_n (nullable): the exact candidate count in device memory, n then only
-// bounds it (no host round trip between dedup and validation).
+// bounds it (no host round trip between dedup and validation). best: the
+// strata mode is best-stratum (a per-read bound may drop candidates whose k
+// exceeds a kept hit of their read; kept hits of the best stratum are exact).
 void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint64_t* cand_keys, uint64_t n,
                          unsigned read_bits, unsigned band, unsigned pct, int mode, uint64_t* hit_keys,
                          uint32_t* hit_vals, unsigned long long* d_count, void* d_validated,
-                         const unsigned long long* d_n = nullptr);
+                         const unsigned long long* d_n = nullptr, bool best = false);
 
 // strata.cu -- dedup (read, chrom, ref_start, strand) keeping min k, then
 // best-stratum / all; writes qgm_hit records, returns their count.

@@ -73,7 +73,8 @@ struct JoinArgs {
   const uint32_t* rlen;
   uint32_t m;
   FastDiv by_m;
-  int tail_ok;  // item tails are exact (stride - q <= kItemTailMax)
+  int uniform;  // every read has length m (n - q - o needs no length load)
+  int lean;     // join_items_lean (QGM_JOIN_LEAN=1)
   int strands;
   unsigned diag_bits;
   uint64_t* out;
@@ -109,7 +110,7 @@ __device__ __forceinline__ uint64_t make_key(const JoinArgs& a, uint64_t it, uin
   const uint32_t pp = uint32_t(it);
   const uint32_t r = a.by_m.div(pp), o = pp - r * a.m;
   uint32_t off = o;  // forward: d = p - o
-  if (rev) off = a.tail_ok ? uint32_t(it >> kItemTailShift) & kItemTailMax : __ldg(a.rlen + r) - a.q - o;  // d = p - (n - q - o)
+  if (rev) off = (a.uniform ? a.m : __ldg(a.rlen + r)) - a.q - o;  // d = p - (n - q - o)
   return (uint64_t(r) << (a.diag_bits + 1)) | (uint64_t(rev) << a.diag_bits) | uint64_t(xp - off);
 }
 
@@ -254,6 +255,87 @@ __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI
   }
 }
 
+// Lean variant of join_items: no compaction list. Every lane expands the
+// occurrence interval of its own read q-gram in place (one occurrence per
+// round, rounds = the warp's longest interval up to kInline); intervals
+// longer than kInline (repeats) are expanded by the whole warp as above.
+// Trades some lane utilisation for fewer shared-memory round trips.
+template <bool kRunStart, bool kPacked>
+__device__ __forceinline__ void join_items_lean(const JoinArgs& a, const uint32_t* sI, const uint16_t* sR,
+                                                const uint32_t* S1p, const uint32_t* Op, const uint64_t* Ip,
+                                                uint32_t d0, uint32_t w0, uint32_t gsub, uint32_t my_lo,
+                                                uint32_t my_hi, WarpLists& L) {
+  const unsigned lane = lane_id();
+  auto stage = [&](bool emit, uint64_t it, uint32_t xp) {  // all lanes call it
+    const unsigned m = __ballot_sync(kFull, emit);
+    if (!m) return;
+    if (emit) {
+      const uint32_t e = L.staged + __popc(m & lanemask_lt());
+      L.eit[e] = it;
+      L.exp[e] = xp;
+    }
+    L.staged += __popc(m);
+    __syncwarp();
+    if (L.staged >= 32) drain(a, L, 32);
+  };
+  for (uint32_t base = my_lo; base < my_hi; base += 32 * kItems) {  // warp-uniform bound
+    uint64_t it[kItems];
+    uint32_t k0[kItems], len[kItems];
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) {
+      const uint32_t i = base + u * 32 + lane;
+      it[u] = i < my_hi ? Ip[i] : ~0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) {
+      const bool ok = it[u] != ~0ull;
+      const uint32_t g = gsub | uint32_t(it[u] >> kItemCodeShift);
+      const uint32_t wl = ok ? (g >> 5) - w0 : 0u, bit = g & 31u;
+      const uint32_t w = sI[wl];
+      const bool hit = ok && ((w >> bit) & 1u);
+      const uint32_t b = d0 + sR[wl] + __popc(w & ((1u << bit) - 1u));
+      k0[u] = hit ? S1p[b] : 0u;
+      len[u] = hit ? S1p[b + 1] - k0[u] : 0u;
+      L.n_hit += len[u] != 0;
+      L.n_occ += len[u];
+    }
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) {
+      const bool longi = len[u] > kInline;
+      const uint32_t nin = longi ? 0u : len[u];
+      const uint32_t rounds = __reduce_max_sync(kFull, nin);
+      for (uint32_t t = 0; t < rounds; ++t) {
+        uint64_t mit = it[u];
+        uint32_t xp = 0;
+        const bool emit = t < nin && match<kRunStart, kPacked>(a, Op, k0[u] + t, mit, xp);
+        stage(emit, mit, xp);
+      }
+      unsigned lm = __ballot_sync(kFull, longi);
+      while (lm) {
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint32_t lk0 = __shfl_sync(kFull, k0[u], src), llen = __shfl_sync(kFull, len[u], src);
+        const uint64_t lit = __shfl_sync(kFull, it[u], src);
+        for (uint32_t t0 = 0; t0 < llen; t0 += 32) {
+          uint64_t mit = lit;
+          uint32_t xp = 0;
+          const bool emit = t0 + lane < llen && match<kRunStart, kPacked>(a, Op, lk0 + t0 + lane, mit, xp);
+          stage(emit, mit, xp);
+        }
+      }
+    }
+  }
+}
+
+template <bool kRunStart, bool kPacked>
+__device__ __forceinline__ void join_dispatch(bool lean, const JoinArgs& a, const uint32_t* sI, const uint16_t* sR,
+                                              const uint32_t* S1p, const uint32_t* Op, const uint64_t* Ip,
+                                              uint32_t d0, uint32_t w0, uint32_t gsub, uint32_t my_lo,
+                                              uint32_t my_hi, WarpLists& L) {
+  if (lean) join_items_lean<kRunStart, kPacked>(a, sI, sR, S1p, Op, Ip, d0, w0, gsub, my_lo, my_hi, L);
+  else join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, Ip, d0, w0, gsub, my_lo, my_hi, L);
+}
+
 __device__ __forceinline__ void join_stats(const JoinArgs& a, WarpLists& L) {
   flush_keys(a, L);
   const unsigned long long h = warp_reduce_sum(L.n_hit), o = warp_reduce_sum(L.n_occ);
@@ -372,10 +454,11 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
     const uint32_t my_lo = b0 + uint32_t(uint64_t(nitems) * wid / kJoinWarps);
     const uint32_t my_hi = b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kJoinWarps);
     if (staged) {  // S'/O accesses from shared-derived pointers only: LDS
-      join_items<kRunStart, kPacked>(a, sI, sR, sS1 - sA, sO - oA, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi,
-                                     L);
+      join_dispatch<kRunStart, kPacked>(a.lean, a, sI, sR, sS1 - sA, sO - oA, a.items, d0, w0, sb << a.code_shift,
+                                        my_lo, my_hi, L);
     } else {
-      join_items<kRunStart, kPacked>(a, sI, sR, a.S1, a.O, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi, L);
+      join_dispatch<kRunStart, kPacked>(a.lean, a, sI, sR, a.S1, a.O, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi,
+                                        L);
     }
     __syncthreads();  // the staging buffers are rewritten for the next sub-bin
   }
@@ -528,13 +611,13 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
       // everything in shared memory: pointers derived from the shared
       // buffers only, so every access compiles to LDS (no generic LD and its
       // 64-bit address arithmetic)
-      join_items<kRunStart, kPacked>(a, sI, sR, sS1 - M.sA, sO - M.oA, sIt - M.iA, M.d0, w0, M.sb << a.code_shift,
-                                     my_lo, my_hi, L);
+      join_dispatch<kRunStart, kPacked>(a.lean, a, sI, sR, sS1 - M.sA, sO - M.oA, sIt - M.iA, M.d0, w0,
+                                        M.sb << a.code_shift, my_lo, my_hi, L);
     } else {
       const uint32_t* S1p = M.staged ? sS1 - M.sA : a.S1;
       const uint32_t* Op = M.staged ? sO - M.oA : a.O;
       const uint64_t* Ip = M.items_staged ? sIt - M.iA : a.items;
-      join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, Ip, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
+      join_dispatch<kRunStart, kPacked>(a.lean, a, sI, sR, S1p, Op, Ip, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -567,7 +650,11 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   a.rlen = reads.lengths.p;
   a.m = reads.stride;
   a.by_m = FastDiv(std::max<uint32_t>(reads.stride, 1));
-  a.tail_ok = reads.stride <= rp.q + kItemTailMax;
+  a.uniform = rp.uniform;
+  {
+    const char* e = std::getenv("QGM_JOIN_LEAN");  // experiment knob until measured
+    a.lean = e && e[0] == '1';
+  }
   a.strands = strands;
   a.diag_bits = ref.diag_bits;
   DBuf<unsigned long long> counter(c, 3);

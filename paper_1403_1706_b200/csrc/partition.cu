@@ -25,13 +25,8 @@
 // 0.68 GB of output: partial sectors of 2.4M concurrently open runs.
 //
 // Everything the join needs from the read text is gathered in P1, where the
-// read words are at hand (the join and P2 never touch the reads' bases). P1
-// item (the bin's code bits are implied by the item's position):
-//   bits  0..31 pp = r * stride + o        bits 33..35 read base at o-1 (4 = none)
-//   bits 36..38 complement of read[o+q]    bit  39     fr = (code != canonical)
-//   bits 40..63 canonical code bits below the P1 bin
-// P2 drops the next 8 implied bits and adds tail = n - q - o (join item layout
-// in internal.hpp).
+// read words are at hand (the join and P2 never touch the reads' bases): P1
+// writes the final join item (layout in internal.hpp), P2 only moves it.
 #include "internal.hpp"
 
 namespace qgm {
@@ -53,23 +48,26 @@ constexpr uint32_t kPer = kChunk / kPartThreads;
 static_assert(kBins <= 256 && kChunk <= (1u << 24), "P1 packs bin | rank << 8 in 32 bits");
 constexpr int kRun = 8;  // consecutive q-gram slots per thread (P0, P1)
 static_assert(kPer % kRun == 0, "");
-constexpr unsigned kP1CodeShift = 40, kP1MetaShift = 33;
+constexpr unsigned kP1CodeShift = kItemCodeShift, kP1MetaShift = kItemFbShift;  // P1 writes final join items
 
+// Runs: R consecutive q-gram slots of ONE read -- a read's slots [0, span)
+// are rpr = ceil(span / R) runs, the last one partial -- all cut from one
+// 32-base register window that starts at base o0 - 1 (q + R + 1 <= 32), so a
+// slot's code, left base and right base are constant shifts of a register.
+// Q = compile-time q (0: the runtime value), so every shift is an immediate.
 struct Run {
-  uint32_t r, o0, nA, nB;
-  uint64_t A, B;  // 32-base windows from base o0-1 of read r and base -1 of read r+1
+  uint32_t r, o0, n;
+  uint64_t A;
 };
 
+template <int Q>
 struct ItemGen {
   const uint64_t* words;
   const uint32_t* lengths;
-  uint32_t W, span, stride, n_items;
-  FastDiv by_span;
-  unsigned q;
-  // ---- runs: R consecutive slots per thread share their read words. A run
-  // lies in one read, or (span >= R) crosses into the next read once. Each
-  // read's bases come from one 32-base window starting at base o-1, so a
-  // slot's code, left base and right base are shifts of a register.
+  uint32_t W, stride, rpr, n_runs;
+  FastDiv by_rpr;
+  unsigned q_rt;
+  __device__ __forceinline__ unsigned q() const { return Q ? unsigned(Q) : q_rt; }
   __device__ __forceinline__ uint64_t window(uint32_t r, uint32_t o) const {
     const uint64_t* w = words + uint64_t(r) * W;
     const uint32_t b = o + 31;  // base o-1, one word up: word -1 (zero) for o == 0
@@ -80,31 +78,26 @@ struct ItemGen {
     return (w0 << sh) | ((w1 >> 1) >> (63 - sh));
   }
   template <int R>
-  __device__ __forceinline__ void fetch_run(uint32_t t0, Run& u) const {
-    t0 = min(t0, n_items - 1);  // runs past the end load something valid and are dropped
-    u.r = by_span.div(t0);
-    u.o0 = t0 - u.r * span;
-    u.nA = __ldg(lengths + u.r);
+  __device__ __forceinline__ void fetch_run(uint32_t run, Run& u) const {
+    run = min(run, n_runs - 1);  // runs past the end load something valid and are dropped
+    u.r = by_rpr.div(run);
+    u.o0 = (run - u.r * rpr) * R;
+    u.n = __ldg(lengths + u.r);
     u.A = window(u.r, u.o0);
-    const bool cross = R > 1 && u.o0 + R > span && u.r + 1 < n_items / span;
-    u.nB = cross ? __ldg(lengths + u.r + 1) : 0u;
-    u.B = cross ? window(u.r + 1, 0) : 0ull;
   }
   // slot j of a fetched run: canonical code g, own code f, meta, position
   template <int R>
-  __device__ __forceinline__ bool run_slot(uint32_t t0, const Run& u, uint32_t j, uint32_t& f, uint32_t& g,
+  __device__ __forceinline__ bool run_slot(uint32_t run, const Run& u, uint32_t j, uint32_t& f, uint32_t& g,
                                            uint32_t& m, uint32_t& pos) const {
-    const uint32_t o1 = u.o0 + j;
-    const bool inB = R > 1 && o1 >= span;
-    const uint32_t o = inB ? o1 - span : o1, p = inB ? o : j, n = inB ? u.nB : u.nA;
-    const uint64_t w = inB ? u.B : u.A;
-    f = uint32_t((w << (2 * p + 2)) >> (64 - 2 * q));
+    const unsigned q = this->q();
+    const uint32_t o = u.o0 + j;
+    f = uint32_t((u.A << (2 * j + 2)) >> (64 - 2 * q));
     g = canon_code(f, q);
-    const uint32_t bl = uint32_t(w >> (62 - 2 * p)) & 3u;
-    const uint32_t br = uint32_t(w >> (62 - 2 * (p + q + 1))) & 3u;
-    m = (o ? bl : 4u) | ((o + q < n ? 3u - br : 4u) << 3) | (uint32_t(f != g) << 6);
-    pos = (u.r + uint32_t(inB)) * stride + o;
-    return t0 + j < n_items && o + q <= n;
+    const uint32_t bl = uint32_t(u.A >> (62 - 2 * j)) & 3u;
+    const uint32_t br = uint32_t(u.A >> (62 - 2 * (j + q + 1))) & 3u;
+    m = (o ? bl : 4u) | ((o + q < u.n ? 3u - br : 4u) << 3) | (uint32_t(f != g) << 6);
+    pos = u.r * stride + o;
+    return run < n_runs && o + q <= u.n;
   }
 };
 
@@ -115,15 +108,14 @@ struct ItemGen {
 // from this one histogram, so the refinement needs no counting pass. A u16
 // counter hands 0x8000 to the global count whenever it reaches 0x8000.
 constexpr int kHistThreads = 1024;
-template <int R>
-__global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen gen, uint32_t n_items, uint32_t per_cta,
-                                                                 unsigned kshift, uint32_t keys,
-                                                                 uint32_t* __restrict__ hist) {
+template <int Q, int R>
+__global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen<Q> gen, uint32_t per_cta, unsigned kshift,
+                                                                 uint32_t keys, uint32_t* __restrict__ hist) {
   extern __shared__ uint32_t h2[];  // keys / 2 words (keys >= 2)
   const uint32_t words = (keys + 1) / 2;
   for (uint32_t i = threadIdx.x; i < words; i += kHistThreads) h2[i] = 0;
   __syncthreads();
-  const uint32_t c0 = blockIdx.x * per_cta, c1 = min(n_items, c0 + per_cta);
+  const uint32_t c0 = blockIdx.x * per_cta, c1 = min(gen.n_runs, c0 + per_cta);  // runs
   // Hand-off at half range: the increment that takes a counter from 0x7FFF
   // to 0x8000 moves 0x8000 to the global count and subtracts it. Counters
   // rise by 1 per atomic, so exactly one increment sees 0x7FFF per 0x8000
@@ -131,27 +123,38 @@ __global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen gen, ui
   // increments issued in that window (same-address shared atomics retire at
   // most one per clock: a window of 0x8000 cycles would be needed), so it
   // never reaches 0xFFFF and never carries into its neighbour.
-  auto count = [&](uint32_t key) {
-    const uint32_t sh = (key & 1u) * 16u;
-    const uint32_t old = atomicAdd(h2 + (key >> 1), 1u << sh);
-    if (((old >> sh) & 0xFFFFu) == 0x7FFFu) {
-      atomicAdd(hist + key, 0x8000u);
-      atomicSub(h2 + (key >> 1), 0x8000u << sh);
-    }
-  };
+  // The hand-offs of a run are collected in a bit mask and applied after its
+  // slots (no branch around every counting atomic).
   constexpr int kRuns = R == 1 ? 4 : 1;  // runs in flight per thread
-  for (uint32_t t0 = c0; t0 < c1; t0 += kRuns * R * kHistThreads) {
+  constexpr int kSlots = kRuns * R;
+  for (uint32_t t0 = c0; t0 < c1; t0 += kRuns * kHistThreads) {
     Run u[kRuns];
 #pragma unroll
-    for (int h = 0; h < kRuns; ++h) gen.fetch_run<R>(t0 + (h * kHistThreads + threadIdx.x) * R, u[h]);
+    for (int h = 0; h < kRuns; ++h) gen.template fetch_run<R>(t0 + h * kHistThreads + threadIdx.x, u[h]);
+    uint32_t key[kSlots];
+    uint32_t pend = 0;
 #pragma unroll
     for (int h = 0; h < kRuns; ++h) {
-      const uint32_t tr = t0 + (h * kHistThreads + threadIdx.x) * R;
+      const uint32_t tr = t0 + h * kHistThreads + threadIdx.x;
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         uint32_t f, g, m, pos;
-        if (gen.run_slot<R>(tr, u[h], j, f, g, m, pos) && tr + j < c1) count(g >> kshift);
+        const bool ok = gen.template run_slot<R>(tr, u[h], j, f, g, m, pos) && tr < c1;
+        const uint32_t k = g >> kshift, sh = (k & 1u) * 16u;
+        key[h * R + j] = k;
+        // unconditional (an invalid slot adds 0): no branch around the atomic
+        const uint32_t old = atomicAdd(h2 + (k >> 1), uint32_t(ok) << sh);
+        pend |= uint32_t(ok && ((old >> sh) & 0xFFFFu) == 0x7FFFu) << (h * R + j);
       }
+    }
+    if (pend) {
+#pragma unroll
+      for (int e = 0; e < kSlots; ++e)
+        if ((pend >> e) & 1u) {
+          const uint32_t sh = (key[e] & 1u) * 16u;
+          atomicAdd(hist + key[e], 0x8000u);
+          atomicSub(h2 + (key[e] >> 1), 0x8000u << sh);
+        }
     }
   }
   __syncthreads();
@@ -168,8 +171,8 @@ __global__ void k_bin_offsets(const uint32_t* __restrict__ soff, uint32_t nbins,
   for (uint32_t b = threadIdx.x; b <= nbins; b += blockDim.x) boff[b] = soff[b << sub];
 }
 
-template <int R>
-__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(ItemGen gen, uint32_t n_items, unsigned shift,
+template <int Q, int R>
+__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(ItemGen<Q> gen, unsigned shift,
                                                                   const uint32_t* __restrict__ boff,
                                                                   uint32_t* __restrict__ cursor,
                                                                   uint64_t* __restrict__ out) {
@@ -178,10 +181,11 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
   __shared__ uint32_t cnt[kBins], lofs[kBins], gdst[kBins];
   __shared__ uint32_t ws[33];
   const uint32_t lmask = shift ? (1u << shift) - 1u : 0u;
-  const uint32_t n_chunks = (n_items + kChunk - 1) / kChunk;
-  constexpr uint32_t kRuns = kPer / R;
+  constexpr uint32_t kRuns = kPer / R;  // runs per thread per chunk
+  constexpr uint32_t kChunkRuns = kRuns * kPartThreads;
+  const uint32_t n_chunks = (gen.n_runs + kChunkRuns - 1) / kChunkRuns;
   for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
-    const uint32_t c0 = ch * kChunk;
+    const uint32_t c0 = ch * kChunkRuns;
     for (uint32_t b = threadIdx.x; b < kBins; b += kPartThreads) cnt[b] = 0;
     __syncthreads();
     uint64_t item[kPer];
@@ -191,15 +195,15 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
       constexpr uint32_t kIn = kRuns < 4 ? kRuns : 4;  // runs whose loads are issued together
       Run u[kIn];
 #pragma unroll
-      for (uint32_t h = 0; h < kIn; ++h) gen.fetch_run<R>(c0 + ((h0 + h) * kPartThreads + threadIdx.x) * R, u[h]);
+      for (uint32_t h = 0; h < kIn; ++h) gen.template fetch_run<R>(c0 + (h0 + h) * kPartThreads + threadIdx.x, u[h]);
 #pragma unroll
       for (uint32_t h = 0; h < kIn; ++h) {
-        const uint32_t tr = c0 + ((h0 + h) * kPartThreads + threadIdx.x) * R;
+        const uint32_t tr = c0 + (h0 + h) * kPartThreads + threadIdx.x;
 #pragma unroll
         for (uint32_t j = 0; j < R; ++j) {
           const uint32_t e = (h0 + h) * R + j;
           uint32_t f, g, m, pos;
-          const bool ok = gen.run_slot<R>(tr, u[h], j, f, g, m, pos);
+          const bool ok = gen.template run_slot<R>(tr, u[h], j, f, g, m, pos);
           item[e] = (uint64_t(g & lmask) << kP1CodeShift) | (uint64_t(m) << kP1MetaShift) | pos;
           // bin | rank among the chunk's items of that bin << 8 (the count's
           // atomic returns the rank, so placement needs no second atomic)
@@ -255,29 +259,11 @@ constexpr uint32_t kP2Per = 8;
 constexpr uint32_t kP2Chunk = kP2Per * kP2Threads;
 
 struct Refine {
-  unsigned shift;    // code bits below the P1 bin (in the P1 item)
-  unsigned kshift;   // code bits below the refined key (in the join item)
+  unsigned shift;    // code bits below the P1 bin (in the item)
+  unsigned kshift;   // code bits below the refined key
   uint32_t nbins;    // P1 bins
-  // join-item conversion
-  const uint32_t* lengths;
-  uint32_t stride;
-  FastDiv by_stride;
-  unsigned q;
-  const uint32_t* lens;  // {max, ~min} read length (device)
   __device__ __forceinline__ uint32_t key(uint64_t it, uint32_t bin) const {
     return (bin << (shift - kshift)) | (uint32_t(it >> kP1CodeShift) >> kshift);
-  }
-  // uniform: every read of the batch has length `stride` (the usual case;
-  // read once per CTA from lens)
-  __device__ __forceinline__ uint64_t convert(uint64_t it, bool uniform) const {
-    const uint32_t pp = uint32_t(it);
-    const uint32_t r = by_stride.div(pp), o = pp - r * stride;
-    // every read of the batch has length `stride` (the usual case): no load
-    const uint32_t n = uniform ? stride : __ldg(lengths + r);
-    const uint32_t tail = min(n - q - o, kItemTailMax);
-    const uint32_t lmask = kshift ? (1u << kshift) - 1u : 0u;
-    return (uint64_t(uint32_t(it >> kP1CodeShift) & lmask) << kItemCodeShift) |
-           (uint64_t((it >> kP1MetaShift) & 0x7Fu) << kItemFbShift) | (uint64_t(tail) << kItemTailShift) | pp;
   }
 };
 
@@ -339,7 +325,6 @@ __global__ void __launch_bounds__(kP2Threads, kP2MinBlocks) k_refine_scatter(con
   }
   __syncthreads();
   uint32_t phase = 0;
-  const bool uniform = ~__ldg(rf.lens + 1) == rf.stride;
   uint4 ci_next = blockIdx.x < n_chunks ? __ldg(chunk_info + blockIdx.x) : make_uint4(0, 0, 0, 0);
   for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
     const uint32_t c0 = ch * kP2Chunk, c1 = min(n, c0 + kP2Chunk);
@@ -356,7 +341,7 @@ __global__ void __launch_bounds__(kP2Threads, kP2MinBlocks) k_refine_scatter(con
         while (sboff[b + 1] <= i) ++b;
         const uint64_t it = sin[i - c0];
         const uint32_t k = rf.key(it, b);
-        out[off[k] + atomicAdd(cursor + k, 1u)] = rf.convert(it, uniform);
+        out[off[k] + atomicAdd(cursor + k, 1u)] = it;
       }
       __syncthreads();  // every thread is done with sin
       if (threadIdx.x == 0 && more) fetch(ch + gridDim.x);
@@ -377,7 +362,6 @@ __global__ void __launch_bounds__(kP2Threads, kP2MinBlocks) k_refine_scatter(con
       if (i < c1 && bfirst != blast)
         while (sboff[b + 1] <= i) ++b;
       kk[k] = i < c1 ? rf.key(v[k], b) - base : ~0u;
-      v[k] = rf.convert(v[k], uniform);
       if (i < c1) atomicAdd(cnt + kk[k], 1u);
     }
     __syncthreads();
@@ -419,23 +403,70 @@ __global__ void __launch_bounds__(kP2Threads, kP2MinBlocks) k_refine_scatter(con
 
 }  // namespace
 
-void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
-  if (q == 0 || q > 16) throw InputError("q must be in [1, 16]");
-  ItemGen gen;
+// P0 + P1 for one (Q, R) instantiation (Q = compile-time q or 0, R = run length).
+template <int Q, int R>
+static void p0_p1(Ctx& c, const ItemGen<Q>& gen, const Reads& reads, unsigned q, unsigned key_bits, unsigned bits,
+                  Partitioned& out, DBuf<uint32_t>& h2, DBuf<uint64_t>& p1, uint32_t& V) {
+  const uint32_t keys = 1u << key_bits;
+  const unsigned sub = key_bits - bits, shift = 2 * q - bits;
+  {
+    const uint32_t per_cta = uint32_t(ceil_div(ceil_div(gen.n_runs, uint64_t(kSMs)), kHistThreads) * kHistThreads);
+    const size_t hsmem = size_t((keys + 1) / 2) * 4;
+    auto kern = k_part_hist16<Q, R>;
+    QGM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsmem)));
+    KernelScope ks(c, "k_part_hist");
+    QGM_KERNEL(c, kern, unsigned(ceil_div(gen.n_runs, per_cta)), kHistThreads, hsmem, gen, per_cta,
+               2 * q - key_bits, keys, h2.p);
+  }
+  DBuf<uint32_t> total(c, 1);
+  exclusive_scan_u32(c, h2.p, out.soff.p, keys + 1, total.p, nullptr);
+  QGM_KERNEL(c, k_bin_offsets, 1, 256, 0, out.soff.p, 1u << bits, sub, out.boff.p);
+  uint32_t lens[2] = {0, 0};
+  QGM_CUDA(cudaMemcpyAsync(&V, total.p, 4, cudaMemcpyDeviceToHost, c.stream));
+  QGM_CUDA(cudaMemcpyAsync(lens, reads.lens.p, 8, cudaMemcpyDeviceToHost, c.stream));
+  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  if (lens[0] > reads.stride) throw InputError("read longer than the stride");
+  out.uniform = ~lens[1] == reads.stride;
+  if (V == 0) return;
+  DBuf<uint32_t> hist(c, kBins + 1);  // per-bin cursors of P1
+  hist.zero();
+  p1.alloc(c, V + 2);  // +2: P2 bulk-copies whole 16-byte pairs
+  const size_t smem = kChunk * (sizeof(uint64_t) + sizeof(uint8_t));
+  auto p1kern = k_part_scatter<Q, R>;
+  QGM_CUDA(cudaFuncSetAttribute(p1kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const uint32_t chunk_runs = kChunk / R;
+  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(gen.n_runs, chunk_runs), uint64_t(kSMs) * 4));
+  KernelScope ks(c, "k_part_scatter");
+  QGM_KERNEL(c, p1kern, grid, kPartThreads, smem, gen, shift, out.boff.p, hist.p, p1.p);
+}
+
+template <int Q>
+static void p0_p1_runs(Ctx& c, const Reads& reads, unsigned q, uint32_t span, unsigned key_bits, unsigned bits,
+                       Partitioned& out, DBuf<uint32_t>& h2, DBuf<uint64_t>& p1, uint32_t& V) {
+  ItemGen<Q> gen;
   gen.words = reads.words.p;
   gen.lengths = reads.lengths.p;
   gen.W = reads.W;
-  gen.span = reads.stride >= q ? reads.stride - q + 1 : 0;
   gen.stride = reads.stride;
-  gen.by_span = FastDiv(std::max<uint32_t>(gen.span, 1));
-  gen.q = q;
-  // runs of kRun slots per thread when a run crosses at most one read
-  // boundary; one slot per thread for reads shorter than q + kRun - 1
-  const bool runs = gen.span >= uint32_t(kRun);
-  const uint64_t n_items64 = uint64_t(reads.n) * gen.span;
+  gen.q_rt = q;
+  // runs of kRun slots per thread; one slot per thread for reads with fewer
+  // than kRun q-gram slots
+  const int R = span >= uint32_t(kRun) ? kRun : 1;
+  gen.rpr = uint32_t(ceil_div(span, R));
+  gen.by_rpr = FastDiv(std::max<uint32_t>(gen.rpr, 1));
+  const uint64_t n_runs = uint64_t(reads.n) * gen.rpr;
+  if (n_runs * R > 0xFFFFFFFFull - kChunk) throw InputError("read batch has more than 2^32-1 q-gram slots");
+  gen.n_runs = uint32_t(n_runs);
+  if (R == kRun) p0_p1<Q, kRun>(c, gen, reads, q, key_bits, bits, out, h2, p1, V);
+  else p0_p1<Q, 1>(c, gen, reads, q, key_bits, bits, out, h2, p1, V);
+}
+
+void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
+  if (q == 0 || q > 16) throw InputError("q must be in [1, 16]");
+  const uint32_t span = reads.stride >= q ? reads.stride - q + 1 : 0;
+  const uint64_t n_items64 = uint64_t(reads.n) * span;
   if (n_items64 > 0xFFFFFFFFull - kChunk) throw InputError("read batch has more than 2^32-1 q-gram slots");
   const uint32_t n_items = uint32_t(n_items64);
-  gen.n_items = n_items;
   const unsigned bits = std::min(2 * q, kBinBits);
   const unsigned shift = 2 * q - bits;
   // sub-bins of ~256+ read q-grams: small batches get fewer, wider sub-bins
@@ -461,42 +492,19 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
     out.soff.zero();
   };
   if (n_items == 0) return empty();
-  // P0: histogram of the refined keys (the P1 bins are its prefixes)
+  // P0: histogram of the refined keys (the P1 bins are its prefixes); P1
   const uint32_t keys = 1u << key_bits;
   const unsigned sub = key_bits - bits;
   out.soff.alloc(c, keys + 1);
   DBuf<uint32_t> h2(c, keys + 1);
   h2.zero();
-  {
-    const uint32_t per_cta = uint32_t(ceil_div(ceil_div(n_items, uint64_t(kSMs)), 8 * kHistThreads) * 8 * kHistThreads);
-    const size_t hsmem = size_t((keys + 1) / 2) * 4;
-    auto kern = runs ? k_part_hist16<kRun> : k_part_hist16<1>;
-    QGM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsmem)));
-    KernelScope ks(c, "k_part_hist");
-    QGM_KERNEL(c, kern, unsigned(ceil_div(n_items, per_cta)), kHistThreads, hsmem, gen, n_items, per_cta,
-               2 * q - key_bits, keys, h2.p);
-  }
-  DBuf<uint32_t> total(c, 1);
-  exclusive_scan_u32(c, h2.p, out.soff.p, keys + 1, total.p, nullptr);
-  QGM_KERNEL(c, k_bin_offsets, 1, 256, 0, out.soff.p, 1u << bits, sub, out.boff.p);
-  uint32_t V = 0, lens[2] = {0, 0};
-  QGM_CUDA(cudaMemcpyAsync(&V, total.p, 4, cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaMemcpyAsync(lens, reads.lens.p, 8, cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaStreamSynchronize(c.stream));
-  if (lens[0] > reads.stride) throw InputError("read longer than the stride");
+  DBuf<uint64_t> p1;
+  uint32_t V = 0;
+  if (q == 16) p0_p1_runs<16>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
+  else if (q == 12) p0_p1_runs<12>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
+  else p0_p1_runs<0>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
   if (V == 0) return empty();
   out.V = V;
-  DBuf<uint32_t> hist(c, kBins + 1);  // per-bin cursors of P1
-  hist.zero();
-  DBuf<uint64_t> p1(c, V + 2);  // +2: P2 bulk-copies whole 16-byte pairs
-  const size_t smem = kChunk * (sizeof(uint64_t) + sizeof(uint8_t));
-  auto p1kern = runs ? k_part_scatter<kRun> : k_part_scatter<1>;
-  QGM_CUDA(cudaFuncSetAttribute(p1kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n_items, kChunk), uint64_t(kSMs) * 4));
-  {
-    KernelScope ks(c, "k_part_scatter");
-    QGM_KERNEL(c, p1kern, grid, kPartThreads, smem, gen, n_items, shift, out.boff.p, hist.p, p1.p);
-  }
   // P2: refine to the top min(2q, 16) code bits (short reuse distance of the
   // reference-index sectors in the join) and convert to join items. Runs even
   // when P1 already grouped by every key bit (2q <= 8): then it only converts.
@@ -504,11 +512,6 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   rf.shift = shift;
   rf.kshift = 2 * q - key_bits;
   rf.nbins = 1u << bits;
-  rf.lengths = reads.lengths.p;
-  rf.stride = reads.stride;
-  rf.by_stride = FastDiv(std::max<uint32_t>(reads.stride, 1));
-  rf.q = q;
-  rf.lens = reads.lens.p;
   const unsigned grid2 = unsigned(std::min<uint64_t>(ceil_div(V, kP2Chunk), uint64_t(kSMs) * kP2MinBlocks));
   h2.zero();  // per-key cursors
   out.pairs.alloc(c, V + 2);  // +2: the join bulk-copies whole 16-byte pairs of items

@@ -82,92 +82,145 @@ def piece_reference(ref_codes, chrom_begin, pieces: list[Piece], mask=None):
     return codes, np.array(out_cb, dtype=np.uint64), m
 
 
-def own_and_translate(hits: np.ndarray, pieces: list[Piece]) -> np.ndarray:
-    """Keep the hits whose ref_start a piece owns; piece-relative (chrom,
-    ref_start) -> whole-reference chromosome coordinates."""
-    if hits.size == 0 or not pieces:
-        return hits[:0]
-    pc = hits["chrom"].astype(np.int64)
-    begin = np.array([p.begin for p in pieces], np.int64)[pc]
-    ob = np.array([p.own_begin for p in pieces], np.int64)[pc]
-    oe = np.array([p.own_end for p in pieces], np.int64)[pc]
-    chrom = np.array([p.chrom for p in pieces], np.int64)[pc]
-    pos = hits["ref_start"].astype(np.int64) + begin
+# ------------------------------------------------------------------ records
+# The exchange runs on 16-byte hit records (qgm_hit, HIT_DTYPE) held in torch
+# tensors on the rank's device: int32 view [n, 4] = read_id, chrom, ref_start,
+# edits | strand << 16. Nothing crosses the host between the map and the
+# sorted per-owner result; NCCL (or gloo for CPU tensors) carries the MIN
+# all-reduce and the all-to-all.
+
+def to_records(hits: np.ndarray, device="cpu"):
+    """HIT_DTYPE numpy records -> int32 [n, 4] tensor on `device`."""
+    import torch
+    h = np.ascontiguousarray(hits)
+    return torch.from_numpy(h.view(np.int32).reshape(-1, 4).copy()).to(device)
+
+
+def from_records(rec) -> np.ndarray:
+    """int32 [n, 4] tensor -> HIT_DTYPE numpy records."""
+    from . import HIT_DTYPE
+    return np.ascontiguousarray(rec.cpu().numpy()).view(HIT_DTYPE).reshape(-1)
+
+
+def _u32(col):
+    import torch
+    return col.to(torch.int64) & 0xFFFFFFFF
+
+
+def own_and_translate(rec, pieces: list[Piece]):
+    """Keep the records whose ref_start a piece owns; piece-relative (chrom,
+    ref_start) -> whole-reference chromosome coordinates. rec: int32 [n, 4]
+    tensor (numpy HIT_DTYPE records are accepted and returned as numpy)."""
+    import torch
+    if isinstance(rec, np.ndarray):
+        return from_records(own_and_translate(to_records(rec), pieces))
+    if rec.shape[0] == 0 or not pieces:
+        return rec[:0]
+    dev = rec.device
+    tab = torch.tensor([[p.begin, p.own_begin, p.own_end, p.chrom] for p in pieces], dtype=torch.int64, device=dev)
+    pc = _u32(rec[:, 1])
+    begin, ob, oe, chrom = (tab[:, i][pc] for i in range(4))
+    pos = _u32(rec[:, 2]) + begin
     keep = (pos >= ob) & (pos < oe)
-    out = hits[keep].copy()
-    out["chrom"] = chrom[keep]
-    out["ref_start"] = pos[keep]
+    out = rec[keep].clone()
+    out[:, 1] = chrom[keep].to(torch.int32)
+    out[:, 2] = pos[keep].to(torch.int32)  # < 2^32 (chromosomes < 2^32 - 1 bases), two's complement wraps
     return out
 
 
-def _sorted(h: np.ndarray) -> np.ndarray:
-    return h[np.lexsort((h["strand"], h["ref_start"], h["chrom"], h["read_id"]))] if h.size else h
-
-
-def best_stratum_filter(hits: np.ndarray, n_reads: int, dist=None, device="cpu") -> np.ndarray:
-    """All-reduce MIN of every read's smallest edit count; keep the hits at it."""
+def sort_records(rec):
+    """Sort by (read, chrom, ref_start, strand) -- the map's output order."""
     import torch
+    if rec.shape[0] == 0:
+        return rec
+    key = (_u32(rec[:, 1]) << 33) | (_u32(rec[:, 2]) << 1) | ((rec[:, 3].to(torch.int64) >> 16) & 1)
+    o1 = torch.sort(key, stable=True).indices
+    rec = rec[o1]
+    o2 = torch.sort(_u32(rec[:, 0]), stable=True).indices
+    return rec[o2]
 
-    kmin = np.full(n_reads, np.iinfo(np.int32).max, np.int32)
-    if hits.size:
-        np.minimum.at(kmin, hits["read_id"].astype(np.int64), hits["edits"].astype(np.int32))
+
+def best_stratum_filter(rec, n_reads: int, dist=None):
+    """All-reduce MIN of every read's smallest edit count; keep the records at it."""
+    import torch
+    dev = rec.device
+    big = torch.iinfo(torch.int32).max
+    kmin = torch.full((n_reads,), big, dtype=torch.int32, device=dev)
+    read = _u32(rec[:, 0])
+    k = (rec[:, 3] & 0xFFFF).to(torch.int32)
+    if rec.shape[0]:
+        kmin.scatter_reduce_(0, read, k, reduce="amin")
     if dist is not None and dist.is_initialized():
-        t = torch.from_numpy(kmin).to(device)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        kmin = t.cpu().numpy()
-    return hits[hits["edits"].astype(np.int32) == kmin[hits["read_id"].astype(np.int64)]] if hits.size else hits
+        dist.all_reduce(kmin, op=dist.ReduceOp.MIN)
+    return rec[k == kmin[read]] if rec.shape[0] else rec
 
 
-def exchange_to_owners(hits: np.ndarray, n_reads: int, dist=None, device="cpu") -> np.ndarray:
-    """All-to-all of hit records to the rank owning the read's range; the
-    result is this rank's reads' hits sorted by (read, chrom, ref_start,
-    strand)."""
+def exchange_to_owners(rec, n_reads: int, dist=None):
+    """All-to-all of the records to the rank owning the read's range
+    (sharding.shard_range); returns this rank's reads' records sorted by
+    (read, chrom, ref_start, strand)."""
     import torch
-
     if dist is None or not dist.is_initialized():
-        return _sorted(hits)
-    G, me = dist.get_world_size(), dist.get_rank()
-    starts = np.array([sharding.shard_range(n_reads, g, G)[0] for g in range(G)] + [n_reads], np.int64)
-    dest = np.searchsorted(starts, hits["read_id"].astype(np.int64), side="right") - 1
-    order = np.argsort(dest, kind="stable")
-    send = np.ascontiguousarray(hits[order])
-    send_counts = np.bincount(dest, minlength=G).astype(np.int64)
-    sc = torch.from_numpy(send_counts).to(device)
-    rc = torch.empty_like(sc)
-    dist.all_to_all_single(rc, sc)
-    recv_counts = rc.cpu().numpy()
-    rec = hits.dtype.itemsize
-    sbuf = torch.from_numpy(send.view(np.uint8).copy()).to(device)
-    rbuf = torch.empty(int(recv_counts.sum()) * rec, dtype=torch.uint8, device=device)
-    dist.all_to_all_single(rbuf, sbuf, [int(x) * rec for x in recv_counts], [int(x) * rec for x in send_counts])
-    got = rbuf.cpu().numpy().view(hits.dtype)
-    return _sorted(got)
+        return sort_records(rec)
+    G = dist.get_world_size()
+    dev = rec.device
+    starts = torch.tensor([sharding.shard_range(n_reads, g, G)[0] for g in range(G)], dtype=torch.int64, device=dev)
+    dest = torch.searchsorted(starts, _u32(rec[:, 0]), right=True) - 1
+    order = torch.sort(dest, stable=True).indices
+    send = rec[order].contiguous()
+    send_counts = torch.bincount(dest, minlength=G).to(torch.int64)
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts)
+    rc = recv_counts.tolist()
+    sc = send_counts.tolist()
+    recv = torch.empty((int(sum(rc)), 4), dtype=torch.int32, device=dev)
+    dist.all_to_all_single(recv, send, rc, sc)
+    return sort_records(recv)
 
 
-def combine(local_hits: np.ndarray, n_reads: int, mode: int, dist=None, device="cpu") -> np.ndarray:
-    """The exchange step: best-stratum MIN (mode 0) then hits to the read owners."""
-    h = best_stratum_filter(local_hits, n_reads, dist, device) if mode == 0 else local_hits
-    return exchange_to_owners(h, n_reads, dist, device)
+def combine(local, n_reads: int, mode: int, dist=None):
+    """The exchange step: best-stratum MIN (mode 0) then records to the read
+    owners. local: int32 [n, 4] tensor (or numpy HIT_DTYPE records, returned
+    as numpy)."""
+    if isinstance(local, np.ndarray):
+        return from_records(combine(to_records(local), n_reads, mode, dist))
+    rec = best_stratum_filter(local, n_reads, dist) if mode == 0 else local
+    return exchange_to_owners(rec, n_reads, dist)
 
 
 def map_ref_sharded(ctx, reads, ref_codes, chrom_begin, rank: int, world_size: int, params=None, mask=None,
                     dist=None, device="cpu", **kw):
     """One rank's part of a reference-sharded map of a whole read batch on the
-    device: plan, upload this rank's pieces, map (all mode), keep owned hits,
-    exchange. Returns this rank's reads' hits (whole-reference coordinates)."""
-    from . import Reference, make_params
+    device: plan, upload this rank's pieces, map (all mode), download the hit
+    records into a tensor on `device` (device to device for a CUDA device),
+    keep the owned ones, exchange. Returns this rank's reads' records (int32
+    [n, 4] tensor on `device`, whole-reference coordinates)."""
+    import ctypes as C
+
+    import torch
+
+    from . import MapParams, MapStats, Reference, make_params
 
     p = params or make_params(**kw)
     shares = plan(chrom_begin, world_size, reads.stride, p.band_width)
     mine = shares[rank]
+    local = torch.zeros((0, 4), dtype=torch.int32, device=device)
     if mine:
         codes, cb, m = piece_reference(ref_codes, chrom_begin, mine, mask)
         R = Reference.from_codes(ctx, codes, cb, mask=m)
         q = make_params(q=p.q, group_width=p.group_width, sampled=p.sampled, band_width=p.band_width,
                         pct_identity=p.pct_identity, mode=1, strands=p.strands)
-        local, _ = ctx.map(reads, R, q)
+        lib = ctx.lib
+        h = C.c_void_p()
+        ctx._check(lib.qgm_map(ctx.h, reads.h, R.h, C.byref(q), C.byref(h)))
+        try:
+            n = C.c_uint64()
+            ctx._check(lib.qgm_hits_count(h, C.byref(n)))
+            local = torch.empty((n.value, 4), dtype=torch.int32, device=device)
+            if n.value:
+                ctx._check(lib.qgm_hits_download(ctx.h, h, C.c_void_p(local.data_ptr())))
+        finally:
+            lib.qgm_hits_destroy(h)
+        R.close()
         local = own_and_translate(local, mine)
-    else:
-        from . import HIT_DTYPE
-        local = np.zeros(0, HIT_DTYPE)
-    return combine(local, reads.n, p.mode, dist, device)
+    return combine(local, reads.n, p.mode, dist)

@@ -15,8 +15,8 @@ tools=("$@")
 for t in "${tools[@]}"; do
   extra=()
   [ "$t" = memcheck ] && extra=(--leak-check no)
-  [ "$t" = racecheck ] && extra=(--racecheck-report hazard)
-  timeout 1500 compute-sanitizer --tool "$t" "${extra[@]}" --error-exitcode 9 --print-limit 200 \
+  [ "$t" = racecheck ] && extra=(--racecheck-report hazard --num-cuda-barriers 16)
+  timeout ${SAN_TIMEOUT:-900} compute-sanitizer --tool "$t" "${extra[@]}" --error-exitcode 9 --print-limit 200 \
     python tools/sanitize_workload.py > "gpurun_out/sanitize_$t.log" 2>&1
   echo "$t exit=$?" | tee -a gpurun_out/sanitize_summary.txt
   tail -3 "gpurun_out/sanitize_$t.log" | tee -a gpurun_out/sanitize_summary.txt
