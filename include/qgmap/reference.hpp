@@ -1,7 +1,10 @@
 // qgmap/reference.hpp -- reference sequences for the device path: the sequence
 // part of SPEC's ReferenceIndex (per-chromosome 2-bit
-// sequences + the repeat mask). The q-gram-sorted P list of the spec is not
-// needed: filtration streams every unmasked position of the packed reference.
+// sequences + the repeat mask). The q-gram-sorted P list of the spec is built
+// on the device by Reference::prepare (qgm_ref_prepare): one canonical q-group
+// index over the unmasked positions of both strands, which the production
+// filtration joins against the batch's code-sorted read q-grams (join.cu).
+// Only references beyond 2^32 padded bases take the streaming k_filter path.
 #pragma once
 
 #include <cstdint>

@@ -274,7 +274,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   HitsObj out;
   DBuf<uint64_t> keys, alt;
   uint64_t n_raw, n_u;
-  uint64_t fst[2] = {0, 0};
+  uint64_t fst[3] = {0, 0, 0};
   if (P.group_width && P.group_width != 32 && P.group_width != 64) throw InputError("group width must be 32 or 64");
   if (ref.padded_total < (uint64_t(1) << 32)) {
     // production path: read q-grams bucket-sorted by code, joined with the
@@ -286,11 +286,11 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
       StageScope s(c, kStageIndex);
       partition_reads(c, reads, P.q, rbk);
     }
-    out.stats[5] = rbk.V;
     {
       StageScope s(c, kStageFilter);
       n_raw = join_filter(c, rbk, reads, ref, strands, QGM_FILTER_RUN_START, rb, keys, fst);
     }
+    out.stats[5] = fst[2];  // exact read q-gram count, read back with the candidate count
   } else {
     // references beyond 2^32 bases: stream the reference against the read index (filter.cu)
     Index idx;
@@ -346,24 +346,39 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   {
     StageScope s(c, kStageValidate);
     validate_candidates(c, reads, ref, alt.p, n_raw, rb, P.band_width, P.pct_identity, 0, hkeys.p, hvals.p, cnt.p,
-                        nullptr, cnt.p + 1, P.mode == 0);
+                        nullptr, cnt.p + 1);
   }
   if (after_filter && hook_at == 2) after_filter();
   DBuf<uint32_t> per_read;
-  bool big = false;
+  bool big = false, speculative_done = false;
   {
     StageScope s(c, kStageStrata);
     strata_count(c, ref, hkeys.p, cnt.p, n_bound, reads.n, per_read, cnt.p + 2);
+    // The per-read counting-sort strata run on the device counts (output sized
+    // for n_raw records) so that one read-back after them returns every count;
+    // a batch with a read of > 32 hits (repeats) then takes the radix path.
+    // Above 1 GiB of bound-sized output the counts are read back first.
+    const bool speculative = n_bound <= (uint64_t(1) << 26);
+    DBuf<uint32_t> kept_total(c, 1);
+    if (speculative)
+      stratify_unsorted_dev(c, ref, hkeys.p, hvals.p, cnt.p, n_bound, reads.n, int(P.mode), per_read, cnt.p + 2,
+                            out.hits, kept_total.p);
     unsigned long long h[3] = {0, 0, 0};
+    uint32_t kept = 0;
     QGM_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    if (speculative) QGM_CUDA(cudaMemcpyAsync(&kept, kept_total.p, 4, cudaMemcpyDeviceToHost, c.stream));
     QGM_CUDA(cudaStreamSynchronize(c.stream));
     n_val = h[0];
     n_u = h[1];
     big = h[2] != 0;
+    if (speculative && !big) {
+      out.n = kept;
+      speculative_done = true;
+    }
   }
   keys.release();
   alt.release();
-  {
+  if (!speculative_done) {
     StageScope s(c, kStageStrata);
     out.n = stratify_unsorted(c, ref, hkeys, hvals, n_val, reads.n, int(P.mode), per_read, big, out.hits);
   }

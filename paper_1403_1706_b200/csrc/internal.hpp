@@ -327,7 +327,12 @@ struct Partitioned {
   unsigned q = 0;
   uint32_t bins = 0, V = 0;
   unsigned sub_bits = 0;  // sub-bin = code >> (2q - sub_bits); sub_bits = min(2q, 16)
-  bool uniform = false;   // every read has length `stride` (n - q - o from pp alone)
+  // V above is the host-side bound n_reads * (stride - q + 1) (exact for
+  // uniform batches); the exact values stay on the device, read back with the
+  // join's candidate count (no host round trip inside the partition):
+  // flags[0] = V, flags[1] = every read has length `stride` (n - q - o from pp
+  // alone), flags[2] = a read is longer than the stride (input error)
+  DBuf<uint32_t> flags;
   DBuf<uint32_t> boff;    // 8-bit bin offsets (first pass)
   DBuf<uint32_t> soff;    // sub-bin offsets, 2^sub_bits + 1 entries
   DBuf<uint64_t> pairs;
@@ -343,13 +348,11 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
 // mode 0: append kept hits as (hit key, k) to hit_keys/hit_vals (counter in
 //         *d_count); mode 1: write one qgm_validated per candidate.
 // d_n (nullable): the exact candidate count in device memory, n then only
-// bounds it (no host round trip between dedup and validation). best: the
-// strata mode is best-stratum (a per-read bound may drop candidates whose k
-// exceeds a kept hit of their read; kept hits of the best stratum are exact).
+// bounds it (no host round trip between dedup and validation).
 void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint64_t* cand_keys, uint64_t n,
                          unsigned read_bits, unsigned band, unsigned pct, int mode, uint64_t* hit_keys,
                          uint32_t* hit_vals, unsigned long long* d_count, void* d_validated,
-                         const unsigned long long* d_n = nullptr, bool best = false);
+                         const unsigned long long* d_n = nullptr);
 
 // strata.cu -- dedup (read, chrom, ref_start, strand) keeping min k, then
 // best-stratum / all; writes qgm_hit records, returns their count.
@@ -362,6 +365,15 @@ void strata_count(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const unsign
                   uint32_t n_reads, DBuf<uint32_t>& cnt, unsigned long long* d_big);
 uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBuf<uint32_t>& hit_vals, uint64_t n,
                            uint32_t n_reads, int mode, DBuf<uint32_t>& cnt, bool big, DBuf<uint8_t>& out);
+// The per-read counting-sort path of stratify_unsorted with the hit count and
+// the big flag left on the device (no host round trip before the output is
+// written): every kernel reads *d_n and does nothing when *d_big != 0 (the
+// caller then runs stratify_unsorted's radix path); `out` is sized for n_max
+// records; *d_kept receives the record count.
+void stratify_unsorted_dev(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const uint32_t* hit_vals,
+                           const unsigned long long* d_n, uint64_t n_max, uint32_t n_reads, int mode,
+                           DBuf<uint32_t>& cnt, const unsigned long long* d_big, DBuf<uint8_t>& out,
+                           uint32_t* d_kept);
 // hit-rank of every output record: #records of its read
 // whose identity is >= its own (edits <= its edits).
 void hit_ranks(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, uint32_t n_reads, DBuf<uint32_t>& rank);

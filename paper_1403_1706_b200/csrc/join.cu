@@ -73,8 +73,7 @@ struct JoinArgs {
   const uint32_t* rlen;
   uint32_t m;
   FastDiv by_m;
-  int uniform;  // every read has length m (n - q - o needs no length load)
-  int lean;     // join_items_lean (QGM_JOIN_LEAN=1)
+  const uint32_t* uniform;  // device flag: every read has length m (n - q - o needs no length load)
   int strands;
   unsigned diag_bits;
   uint64_t* out;
@@ -105,12 +104,12 @@ __device__ __forceinline__ bool match(const JoinArgs& a, const uint32_t* Op, uin
 }
 
 // Candidate key of a matched pair (item with the strand in its fr bit).
-__device__ __forceinline__ uint64_t make_key(const JoinArgs& a, uint64_t it, uint32_t xp) {
+__device__ __forceinline__ uint64_t make_key(const JoinArgs& a, uint64_t it, uint32_t xp, bool uniform) {
   const uint32_t rev = uint32_t(it >> kItemFrShift) & 1u;
   const uint32_t pp = uint32_t(it);
   const uint32_t r = a.by_m.div(pp), o = pp - r * a.m;
   uint32_t off = o;  // forward: d = p - o
-  if (rev) off = (a.uniform ? a.m : __ldg(a.rlen + r)) - a.q - o;  // d = p - (n - q - o)
+  if (rev) off = (uniform ? a.m : __ldg(a.rlen + r)) - a.q - o;  // d = p - (n - q - o)
   return (uint64_t(r) << (a.diag_bits + 1)) | (uint64_t(rev) << a.diag_bits) | uint64_t(xp - off);
 }
 
@@ -119,7 +118,12 @@ __device__ __forceinline__ uint64_t make_key(const JoinArgs& a, uint64_t it, uin
 // matched pairs are buffered (item + coordinate) and their keys built 32 at a
 // time by the whole warp, then written as one coalesced run -- instead of
 // building keys in whichever lanes happen to match in every round.
-constexpr uint32_t kEmitCap = 64;
+#ifndef QGM_JOIN_DRAIN
+#define QGM_JOIN_DRAIN 64
+#endif
+constexpr uint32_t kDrain = QGM_JOIN_DRAIN;  // keys per output reservation (one global atomic)
+static_assert(kDrain % 32 == 0, "");
+constexpr uint32_t kEmitCap = kDrain + 32;
 struct WarpLists {
   uint32_t* k0;
   uint32_t* k1;
@@ -127,26 +131,31 @@ struct WarpLists {
   uint64_t* eit;  // kEmitCap matched items
   uint32_t* exp;  // their coordinates
   uint32_t staged = 0;
+  bool uniform = false;  // *JoinArgs::uniform, loaded once per thread
   unsigned long long n_hit = 0, n_occ = 0;
 };
 
-// keys of the last `cnt` (<= 32) buffered pairs -> one run of the output
+// keys of the last `cnt` (<= kDrain) buffered pairs -> one run of the output
+// (one global atomic per kDrain keys: the shared candidate counter is the
+// join's only point of contention)
 __device__ __forceinline__ void drain(const JoinArgs& a, WarpLists& L, uint32_t cnt) {
   const unsigned lane = lane_id();
   unsigned long long base = 0;
   if (lane == 0) base = atomicAdd(a.counter, (unsigned long long)cnt);
   base = __shfl_sync(kFull, base, 0);
-  if (lane < cnt) {
-    const uint32_t e = L.staged - cnt + lane;
-    const uint64_t key = make_key(a, L.eit[e], L.exp[e]);
-    if (base + lane < a.cap_out) a.out[base + lane] = key;
-  }
+#pragma unroll
+  for (uint32_t j = 0; j < kDrain; j += 32)
+    if (j + lane < cnt) {
+      const uint32_t e = L.staged - cnt + j + lane;
+      const uint64_t key = make_key(a, L.eit[e], L.exp[e], L.uniform);
+      if (base + j + lane < a.cap_out) a.out[base + j + lane] = key;
+    }
   L.staged -= cnt;
   __syncwarp();
 }
 
 __device__ __forceinline__ void flush_keys(const JoinArgs& a, WarpLists& L) {
-  while (L.staged) drain(a, L, min(L.staged, 32u));
+  while (L.staged) drain(a, L, min(L.staged, kDrain));
 }
 
 // The read q-gram items [my_lo, my_hi) of sub-bin `sb` (one warp): look up
@@ -168,7 +177,7 @@ __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI
     }
     L.staged += __popc(m);
     __syncwarp();
-    if (L.staged >= 32) drain(a, L, 32);
+    if (L.staged >= kDrain) drain(a, L, kDrain);
   };
   uint64_t pn[kItems];  // next step's items, loaded one step ahead
 #pragma unroll
@@ -255,87 +264,6 @@ __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI
   }
 }
 
-// Lean variant of join_items: no compaction list. Every lane expands the
-// occurrence interval of its own read q-gram in place (one occurrence per
-// round, rounds = the warp's longest interval up to kInline); intervals
-// longer than kInline (repeats) are expanded by the whole warp as above.
-// Trades some lane utilisation for fewer shared-memory round trips.
-template <bool kRunStart, bool kPacked>
-__device__ __forceinline__ void join_items_lean(const JoinArgs& a, const uint32_t* sI, const uint16_t* sR,
-                                                const uint32_t* S1p, const uint32_t* Op, const uint64_t* Ip,
-                                                uint32_t d0, uint32_t w0, uint32_t gsub, uint32_t my_lo,
-                                                uint32_t my_hi, WarpLists& L) {
-  const unsigned lane = lane_id();
-  auto stage = [&](bool emit, uint64_t it, uint32_t xp) {  // all lanes call it
-    const unsigned m = __ballot_sync(kFull, emit);
-    if (!m) return;
-    if (emit) {
-      const uint32_t e = L.staged + __popc(m & lanemask_lt());
-      L.eit[e] = it;
-      L.exp[e] = xp;
-    }
-    L.staged += __popc(m);
-    __syncwarp();
-    if (L.staged >= 32) drain(a, L, 32);
-  };
-  for (uint32_t base = my_lo; base < my_hi; base += 32 * kItems) {  // warp-uniform bound
-    uint64_t it[kItems];
-    uint32_t k0[kItems], len[kItems];
-#pragma unroll
-    for (int u = 0; u < kItems; ++u) {
-      const uint32_t i = base + u * 32 + lane;
-      it[u] = i < my_hi ? Ip[i] : ~0ull;
-    }
-#pragma unroll
-    for (int u = 0; u < kItems; ++u) {
-      const bool ok = it[u] != ~0ull;
-      const uint32_t g = gsub | uint32_t(it[u] >> kItemCodeShift);
-      const uint32_t wl = ok ? (g >> 5) - w0 : 0u, bit = g & 31u;
-      const uint32_t w = sI[wl];
-      const bool hit = ok && ((w >> bit) & 1u);
-      const uint32_t b = d0 + sR[wl] + __popc(w & ((1u << bit) - 1u));
-      k0[u] = hit ? S1p[b] : 0u;
-      len[u] = hit ? S1p[b + 1] - k0[u] : 0u;
-      L.n_hit += len[u] != 0;
-      L.n_occ += len[u];
-    }
-#pragma unroll
-    for (int u = 0; u < kItems; ++u) {
-      const bool longi = len[u] > kInline;
-      const uint32_t nin = longi ? 0u : len[u];
-      const uint32_t rounds = __reduce_max_sync(kFull, nin);
-      for (uint32_t t = 0; t < rounds; ++t) {
-        uint64_t mit = it[u];
-        uint32_t xp = 0;
-        const bool emit = t < nin && match<kRunStart, kPacked>(a, Op, k0[u] + t, mit, xp);
-        stage(emit, mit, xp);
-      }
-      unsigned lm = __ballot_sync(kFull, longi);
-      while (lm) {
-        const int src = __ffs(lm) - 1;
-        lm &= lm - 1;
-        const uint32_t lk0 = __shfl_sync(kFull, k0[u], src), llen = __shfl_sync(kFull, len[u], src);
-        const uint64_t lit = __shfl_sync(kFull, it[u], src);
-        for (uint32_t t0 = 0; t0 < llen; t0 += 32) {
-          uint64_t mit = lit;
-          uint32_t xp = 0;
-          const bool emit = t0 + lane < llen && match<kRunStart, kPacked>(a, Op, lk0 + t0 + lane, mit, xp);
-          stage(emit, mit, xp);
-        }
-      }
-    }
-  }
-}
-
-template <bool kRunStart, bool kPacked>
-__device__ __forceinline__ void join_dispatch(bool lean, const JoinArgs& a, const uint32_t* sI, const uint16_t* sR,
-                                              const uint32_t* S1p, const uint32_t* Op, const uint64_t* Ip,
-                                              uint32_t d0, uint32_t w0, uint32_t gsub, uint32_t my_lo,
-                                              uint32_t my_hi, WarpLists& L) {
-  if (lean) join_items_lean<kRunStart, kPacked>(a, sI, sR, S1p, Op, Ip, d0, w0, gsub, my_lo, my_hi, L);
-  else join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, Ip, d0, w0, gsub, my_lo, my_hi, L);
-}
-
 __device__ __forceinline__ void join_stats(const JoinArgs& a, WarpLists& L) {
   flush_keys(a, L);
   const unsigned long long h = warp_reduce_sum(L.n_hit), o = warp_reduce_sum(L.n_occ);
@@ -369,6 +297,7 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
   L.slot = s_slot[wid];
   L.eit = s_eit[wid];
   L.exp = s_exp[wid];
+  L.uniform = __ldg(a.uniform) != 0;
   const bool bulk_I = a.r16 != nullptr;  // sub-bins of >= 8 group words: whole 16-byte chunks
   if (threadIdx.x == 0) mbar_init(&s_bar, 1);
   __syncthreads();
@@ -454,10 +383,10 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
     const uint32_t my_lo = b0 + uint32_t(uint64_t(nitems) * wid / kJoinWarps);
     const uint32_t my_hi = b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kJoinWarps);
     if (staged) {  // S'/O accesses from shared-derived pointers only: LDS
-      join_dispatch<kRunStart, kPacked>(a.lean, a, sI, sR, sS1 - sA, sO - oA, a.items, d0, w0, sb << a.code_shift,
+      join_items<kRunStart, kPacked>(a, sI, sR, sS1 - sA, sO - oA, a.items, d0, w0, sb << a.code_shift,
                                         my_lo, my_hi, L);
     } else {
-      join_dispatch<kRunStart, kPacked>(a.lean, a, sI, sR, a.S1, a.O, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi,
+      join_items<kRunStart, kPacked>(a, sI, sR, a.S1, a.O, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi,
                                         L);
     }
     __syncthreads();  // the staging buffers are rewritten for the next sub-bin
@@ -498,8 +427,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
   if (threadIdx.x == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
-    mbar_init(&empty[0], kWsCons);
-    mbar_init(&empty[1], kWsCons);
+    mbar_init(&empty[0], kWsCons * 32);  // every consumer thread releases the buffer
+    mbar_init(&empty[1], kWsCons * 32);
   }
   __syncthreads();
   auto stage = [&](uint32_t s, uint32_t*& sI, uint16_t*& sR, uint32_t*& sS1, uint32_t*& sO, uint64_t*& sIt) {
@@ -594,6 +523,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
   L.slot = s_slot[wid];
   L.eit = s_eit[wid];
   L.exp = s_exp[wid];
+  L.uniform = __ldg(a.uniform) != 0;
   for (uint32_t k = 0;; ++k) {
     const uint32_t s = k & 1, j = k >> 1;
     mbar_wait(&full[s], j & 1u);
@@ -611,16 +541,18 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
       // everything in shared memory: pointers derived from the shared
       // buffers only, so every access compiles to LDS (no generic LD and its
       // 64-bit address arithmetic)
-      join_dispatch<kRunStart, kPacked>(a.lean, a, sI, sR, sS1 - M.sA, sO - M.oA, sIt - M.iA, M.d0, w0,
+      join_items<kRunStart, kPacked>(a, sI, sR, sS1 - M.sA, sO - M.oA, sIt - M.iA, M.d0, w0,
                                         M.sb << a.code_shift, my_lo, my_hi, L);
     } else {
       const uint32_t* S1p = M.staged ? sS1 - M.sA : a.S1;
       const uint32_t* Op = M.staged ? sO - M.oA : a.O;
       const uint64_t* Ip = M.items_staged ? sIt - M.iA : a.items;
-      join_dispatch<kRunStart, kPacked>(a.lean, a, sI, sR, S1p, Op, Ip, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
+      join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, Ip, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    // one arrive per consumer thread (not lane 0 after a __syncwarp): each
+    // thread's own reads of meta[s] and the staged slices are then ordered
+    // before the producer's refill by the barrier itself
+    mbar_arrive(&empty[s]);
   }
   join_stats(a, L);
 }
@@ -650,11 +582,7 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   a.rlen = reads.lengths.p;
   a.m = reads.stride;
   a.by_m = FastDiv(std::max<uint32_t>(reads.stride, 1));
-  a.uniform = rp.uniform;
-  {
-    const char* e = std::getenv("QGM_JOIN_LEAN");  // experiment knob until measured
-    a.lean = e && e[0] == '1';
-  }
+  a.uniform = rp.flags.p + 1;
   a.strands = strands;
   a.diag_bits = ref.diag_bits;
   DBuf<unsigned long long> counter(c, 3);
@@ -727,12 +655,18 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
       QGM_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(threads), args, smem, c.stream));
       ++c.launches;
     }
+    // the one host round trip of the filtration: candidate count, join
+    // statistics and the partition's flags (exact V, length check)
     unsigned long long h[3] = {0, 0, 0};
+    uint32_t fl[4] = {0, 0, 0, 0};
     QGM_CUDA(cudaMemcpyAsync(h, counter.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaMemcpyAsync(fl, rp.flags.p, sizeof(fl), cudaMemcpyDeviceToHost, c.stream));
     QGM_CUDA(cudaStreamSynchronize(c.stream));
+    if (fl[2]) throw InputError("read longer than the stride");
     if (fstats) {
       fstats[0] = h[1];
       fstats[1] = h[2];
+      fstats[2] = fl[0];
     }
     c.last_raw_candidates = h[0];
     if (h[0] <= keys.n) return h[0];

@@ -165,10 +165,17 @@ __global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen<Q> gen,
   }
 }
 
-// P1 bin offsets from the refined-key offsets: boff[b] = soff[b << sub]
+// P1 bin offsets from the refined-key offsets: boff[b] = soff[b << sub]; and
+// the batch flags (Partitioned::flags) from the upload's length extremes
 __global__ void k_bin_offsets(const uint32_t* __restrict__ soff, uint32_t nbins, unsigned sub,
-                              uint32_t* __restrict__ boff) {
+                              uint32_t* __restrict__ boff, const uint32_t* __restrict__ lens, uint32_t stride,
+                              uint32_t keys, uint32_t* __restrict__ flags) {
   for (uint32_t b = threadIdx.x; b <= nbins; b += blockDim.x) boff[b] = soff[b << sub];
+  if (threadIdx.x == 0) {
+    flags[0] = soff[keys];
+    flags[1] = ~lens[1] == stride;
+    flags[2] = lens[0] > stride;
+  }
 }
 
 template <int Q, int R>
@@ -280,8 +287,9 @@ __device__ __forceinline__ uint32_t bin_search(const uint32_t* sboff, uint32_t n
 // per P2 chunk: {first P1 bin | last P1 bin << 16, first key of the
 // chunk's key window, window width}, so a scatter CTA starts a chunk without
 // a dependent load or a binary search
-__global__ void k_chunk_info(const uint64_t* __restrict__ in, uint32_t n, const uint32_t* __restrict__ boff,
-                             Refine rf, unsigned sub, uint4* __restrict__ info) {
+__global__ void k_chunk_info(const uint64_t* __restrict__ in, const uint32_t* __restrict__ n_dev,
+                             const uint32_t* __restrict__ boff, Refine rf, unsigned sub, uint4* __restrict__ info) {
+  const uint32_t n = *n_dev;
   const uint32_t n_chunks = (n + kP2Chunk - 1) / kP2Chunk;
   for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < n_chunks; ch += gridDim.x * blockDim.x) {
     const uint32_t c0 = ch * kP2Chunk, c1 = min(n, c0 + kP2Chunk);
@@ -292,7 +300,8 @@ __global__ void k_chunk_info(const uint64_t* __restrict__ in, uint32_t n, const 
   }
 }
 
-__global__ void __launch_bounds__(kP2Threads, kP2MinBlocks) k_refine_scatter(const uint64_t* __restrict__ in, uint32_t n,
+__global__ void __launch_bounds__(kP2Threads, kP2MinBlocks) k_refine_scatter(const uint64_t* __restrict__ in,
+                                                                    const uint32_t* __restrict__ n_dev,
                                                                     const uint32_t* __restrict__ boff, Refine rf,
                                                                     unsigned sub, const uint32_t* __restrict__ off,
                                                                     uint32_t* __restrict__ cursor,
@@ -308,6 +317,7 @@ __global__ void __launch_bounds__(kP2Threads, kP2MinBlocks) k_refine_scatter(con
   __shared__ uint32_t sboff[kBins + 1];
   __shared__ uint32_t ws[33];
   __shared__ __align__(8) uint64_t s_bar;
+  const uint32_t n = *n_dev;  // V (the grid is sized by its host-side bound)
   for (uint32_t b = threadIdx.x; b <= rf.nbins; b += kP2Threads) sboff[b] = boff[b];
   const uint32_t n_chunks = (n + kP2Chunk - 1) / kP2Chunk;
   // one elected thread moves each chunk's items into shared memory with a
@@ -418,19 +428,14 @@ static void p0_p1(Ctx& c, const ItemGen<Q>& gen, const Reads& reads, unsigned q,
     QGM_KERNEL(c, kern, unsigned(ceil_div(gen.n_runs, per_cta)), kHistThreads, hsmem, gen, per_cta,
                2 * q - key_bits, keys, h2.p);
   }
-  DBuf<uint32_t> total(c, 1);
-  exclusive_scan_u32(c, h2.p, out.soff.p, keys + 1, total.p, nullptr);
-  QGM_KERNEL(c, k_bin_offsets, 1, 256, 0, out.soff.p, 1u << bits, sub, out.boff.p);
-  uint32_t lens[2] = {0, 0};
-  QGM_CUDA(cudaMemcpyAsync(&V, total.p, 4, cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaMemcpyAsync(lens, reads.lens.p, 8, cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaStreamSynchronize(c.stream));
-  if (lens[0] > reads.stride) throw InputError("read longer than the stride");
-  out.uniform = ~lens[1] == reads.stride;
-  if (V == 0) return;
+  exclusive_scan_u32(c, h2.p, out.soff.p, keys + 1, nullptr, nullptr);
+  // no host round trip: V stays on the device (flags[0]); buffers are sized by
+  // the slot count, which equals V for a batch of full-length reads
+  QGM_KERNEL(c, k_bin_offsets, 1, 256, 0, out.soff.p, 1u << bits, sub, out.boff.p, reads.lens.p, reads.stride, keys,
+             out.flags.p);
   DBuf<uint32_t> hist(c, kBins + 1);  // per-bin cursors of P1
   hist.zero();
-  p1.alloc(c, V + 2);  // +2: P2 bulk-copies whole 16-byte pairs
+  p1.alloc(c, uint64_t(V) + 2);  // +2: P2 bulk-copies whole 16-byte pairs
   const size_t smem = kChunk * (sizeof(uint64_t) + sizeof(uint8_t));
   auto p1kern = k_part_scatter<Q, R>;
   QGM_CUDA(cudaFuncSetAttribute(p1kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -484,14 +489,16 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   out.bins = 1u << bits;
   out.sub_bits = key_bits;
   out.boff.alloc(c, kBins + 1);
+  out.flags.alloc(c, 4);
   out.V = 0;
-  auto empty = [&] {  // no read has a q-gram
+  if (n_items == 0) {  // no read has a q-gram
+    out.flags.zero();
     out.boff.zero();
     out.pairs.alloc(c, 1);
     out.soff.alloc(c, (1u << key_bits) + 1);
     out.soff.zero();
-  };
-  if (n_items == 0) return empty();
+    return;
+  }
   // P0: histogram of the refined keys (the P1 bins are its prefixes); P1
   const uint32_t keys = 1u << key_bits;
   const unsigned sub = key_bits - bits;
@@ -499,11 +506,10 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   DBuf<uint32_t> h2(c, keys + 1);
   h2.zero();
   DBuf<uint64_t> p1;
-  uint32_t V = 0;
+  uint32_t V = n_items;  // bound; the exact count is flags[0]
   if (q == 16) p0_p1_runs<16>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
   else if (q == 12) p0_p1_runs<12>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
   else p0_p1_runs<0>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
-  if (V == 0) return empty();
   out.V = V;
   // P2: refine to the top min(2q, 16) code bits (short reuse distance of the
   // reference-index sectors in the join) and convert to join items. Runs even
@@ -519,10 +525,11 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   QGM_CUDA(cudaFuncSetAttribute(k_refine_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
   const uint32_t n_chunks2 = uint32_t(ceil_div(V, kP2Chunk));
   DBuf<uint4> chunk_info(c, n_chunks2);
-  QGM_KERNEL(c, k_chunk_info, unsigned(ceil_div(n_chunks2, 256)), 256, 0, p1.p, V, out.boff.p, rf, sub, chunk_info.p);
+  QGM_KERNEL(c, k_chunk_info, unsigned(ceil_div(n_chunks2, 256)), 256, 0, p1.p, out.flags.p, out.boff.p, rf, sub,
+             chunk_info.p);
   {
     KernelScope ks(c, "k_refine_scatter");
-    QGM_KERNEL(c, k_refine_scatter, grid2, kP2Threads, smem2, p1.p, V, out.boff.p, rf, sub, out.soff.p, h2.p,
+    QGM_KERNEL(c, k_refine_scatter, grid2, kP2Threads, smem2, p1.p, out.flags.p, out.boff.p, rf, sub, out.soff.p, h2.p,
                chunk_info.p, out.pairs.p);
   }
 }

@@ -80,10 +80,16 @@ __global__ void k_count_reads(const uint64_t* __restrict__ keys, const unsigned 
     if (atomicAdd(cnt + (keys[i] >> rshift), 1u) == kSmallSeg) atomicAdd(n_big, 1ull);
 }
 
-// cnt[r] counts down while hits are placed (segment filled from its end)
+// cnt[r] counts down while hits are placed (segment filled from its end).
+// n_dev / big (nullable): device hit count, and the flag that hands the batch
+// to the radix path (then nothing is placed)
 __global__ void k_scatter_reads(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t n,
                                 unsigned rshift, const uint32_t* __restrict__ off, uint32_t* __restrict__ cnt,
-                                uint64_t* __restrict__ skeys, uint32_t* __restrict__ svals) {
+                                uint64_t* __restrict__ skeys, uint32_t* __restrict__ svals,
+                                const unsigned long long* __restrict__ n_dev = nullptr,
+                                const unsigned long long* __restrict__ big = nullptr) {
+  if (big && *big) return;
+  if (n_dev) n = *n_dev;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t k = keys[i];
     const uint32_t r = uint32_t(k >> rshift);
@@ -99,7 +105,8 @@ __global__ void k_scatter_reads(const uint64_t* __restrict__ keys, const uint32_
 // minima, the read's minimum, keep marks (value ~0u = dropped), kept count
 __global__ void k_seg_reduce(uint64_t* __restrict__ skeys, uint32_t* __restrict__ svals,
                              const uint32_t* __restrict__ off, uint32_t n_reads, int mode,
-                             uint32_t* __restrict__ kept) {
+                             uint32_t* __restrict__ kept, const unsigned long long* __restrict__ big = nullptr) {
+  if (big && *big) return;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_reads; r += gridDim.x * blockDim.x) {
     const uint32_t b = off[r], m = off[r + 1] - b;
     uint32_t nk = 0;
@@ -145,7 +152,8 @@ __global__ void k_seg_reduce(uint64_t* __restrict__ skeys, uint32_t* __restrict_
 __global__ void k_seg_emit(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
                            const uint32_t* __restrict__ off, const uint32_t* __restrict__ kept_off, uint32_t n_reads,
                            unsigned diag_bits, const uint64_t* __restrict__ cbp, uint32_t n_chrom,
-                           uint4* __restrict__ out) {
+                           uint4* __restrict__ out, const unsigned long long* __restrict__ big = nullptr) {
+  if (big && *big) return;
   const uint64_t dmask = (uint64_t(1) << diag_bits) - 1;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_reads; r += gridDim.x * blockDim.x) {
     uint32_t o = kept_off[r];
@@ -288,6 +296,34 @@ uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBu
   QGM_KERNEL(c, k_seg_emit, rgrid, 128, 0, skeys.p, svals.p, off.p, kept_off.p, n_reads, ref.diag_bits, ref.d_cbp.p,
              ref.n_chrom, reinterpret_cast<uint4*>(out.p));
   return nk;
+}
+
+void stratify_unsorted_dev(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const uint32_t* hit_vals,
+                           const unsigned long long* d_n, uint64_t n_max, uint32_t n_reads, int mode,
+                           DBuf<uint32_t>& cnt, const unsigned long long* d_big, DBuf<uint8_t>& out,
+                           uint32_t* d_kept) {
+  out.alloc(c, std::max<uint64_t>(n_max * 16, 16));
+  if (n_max == 0 || n_reads == 0) {
+    QGM_CUDA(cudaMemsetAsync(d_kept, 0, 4, c.stream));
+    return;
+  }
+  if (n_max > 0xFFFFFFFFull) throw InputError("strata: more than 2^32-1 hits");
+  const unsigned rshift = ref.diag_bits + 1;
+  KernelScope ks(c, "k_strata_seg");
+  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n_max, 256), uint64_t(kSMs) * 16));
+  const unsigned rgrid = unsigned(std::min<uint64_t>(ceil_div(n_reads, 128), uint64_t(kSMs) * 16));
+  DBuf<uint32_t> off(c, uint64_t(n_reads) + 1), kept(c, uint64_t(n_reads) + 1);
+  kept.zero();
+  exclusive_scan_u32(c, cnt.p, off.p, uint64_t(n_reads) + 1, nullptr, nullptr);
+  DBuf<uint64_t> skeys(c, n_max);
+  DBuf<uint32_t> svals(c, n_max);
+  QGM_KERNEL(c, k_scatter_reads, grid, 256, 0, hit_keys, hit_vals, n_max, rshift, off.p, cnt.p, skeys.p, svals.p, d_n,
+             d_big);
+  QGM_KERNEL(c, k_seg_reduce, rgrid, 128, 0, skeys.p, svals.p, off.p, n_reads, mode, kept.p, d_big);
+  DBuf<uint32_t> kept_off(c, uint64_t(n_reads) + 1);
+  exclusive_scan_u32(c, kept.p, kept_off.p, uint64_t(n_reads) + 1, d_kept, nullptr);
+  QGM_KERNEL(c, k_seg_emit, rgrid, 128, 0, skeys.p, svals.p, off.p, kept_off.p, n_reads, ref.diag_bits, ref.d_cbp.p,
+             ref.n_chrom, reinterpret_cast<uint4*>(out.p), d_big);
 }
 
 uint64_t stratify_hits(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const uint32_t* hit_vals, uint64_t n,

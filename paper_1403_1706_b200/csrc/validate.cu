@@ -51,10 +51,6 @@ struct ValArgs {
   uint32_t* hit_vals;
   unsigned long long* counter;
   void* validated;
-  // best-stratum map path: per read, the smallest k of a kept hit found so
-  // far (atomicMin; 0xFFFFFFFF = none). A candidate whose lower bound exceeds
-  // it cannot be in the read's best stratum (nullable).
-  uint32_t* kb;
 };
 
 struct Win { uint32_t lo, hi, v; };
@@ -229,24 +225,14 @@ __device__ __forceinline__ void unpack_state(const Parked& p, T& Pv, T& Mv) {
   }
 }
 
-// Park lists of the phased map path.
-struct ParkList {
-  Parked* p;
-  unsigned long long* n;
-  uint64_t cap;
-};
-
 // kPhase 0: every row (qgm_validate, or no split); 1: chunks [0, c_split),
-// survivors parked -- into A, or, with split_lb >= 0, into A when their lower
-// bound is <= split_lb (likely true hits) and B otherwise; 2: resume the
-// parked candidates of `in` from chunk c_split (with a.kb: first checked
-// against the read's best kept k so far, which then bounds the remaining rows).
+// survivors parked; 2: resume the parked candidates from chunk c_split.
 template <class T, int kPhase>
-__global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_split, ParkList A, ParkList B,
-                                                          int split_lb, ParkList in) {
+__global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_split, Parked* __restrict__ park,
+                                                          unsigned long long* __restrict__ n_park, uint64_t park_cap) {
   const T mask = a.B >= sizeof(T) * 8 ? T(~T(0)) : T((T(1) << a.B) - 1);
   const uint64_t dmask = (uint64_t(1) << a.diag_bits) - 1;
-  const uint64_t total = kPhase == 2 ? min(uint64_t(*in.n), in.cap) : (a.d_n ? *a.d_n : a.n);
+  const uint64_t total = kPhase == 2 ? min(uint64_t(*n_park), park_cap) : (a.d_n ? *a.d_n : a.n);
   for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < total; base += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t slot_i = base + threadIdx.x;
     bool kept = false, in_range = false, parked = false, finish = false;
@@ -256,7 +242,7 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_
     uint64_t i = slot_i;
     Parked pk{};
     if (kPhase == 2 && slot_i < total) {
-      pk = in.p[slot_i];
+      pk = park[slot_i];
       i = pk.i;
     }
     // candidate geometry (set when in range)
@@ -295,35 +281,27 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_
       w0 = d - H;
       if (n > 0 && w0 + int64_t(L) > 0 && w0 < Lc) {
         in_range = true;
+        if (kPhase == 2) {
+          unpack_state<T>(pk, Pv, Mv);
+          score0 = int(pk.score0);
+        }
         F = cbeg + w0;
         // map path: abandon candidates that can no longer reach the threshold
         kmax = a.mode == 0 ? int((uint64_t(100 - a.pct) * n) / 100) : -1;
         interior = w0 >= 0 && w0 + int64_t(L) <= Lc;
-        if (kPhase == 2) {
-          unpack_state<T>(pk, Pv, Mv);
-          score0 = int(pk.score0);
-          if (a.kb) kmax = min(kmax, int(min(*(volatile uint32_t*)(a.kb + r), 0x7FFFFFFFu)));
-          if (score0 - int(popcount_t(Mv)) > kmax) st = kAbandoned;  // cannot reach the best stratum / threshold
-          else run(c_split, 0xFFFFFFFFu);
-        } else {
-          run(0u, kPhase == 1 ? c_split : 0xFFFFFFFFu);
-        }
+        run(kPhase == 2 ? c_split : 0u, kPhase == 1 ? c_split : 0xFFFFFFFFu);
         parked = kPhase == 1 && st == kPaused;
         finish = !parked;
       }
     }
     if (kPhase == 1) {
-      const bool toB = parked && split_lb >= 0 && score0 - int(popcount_t(Mv)) > split_lb;
-      const unsigned long long pa = warp_append(parked && !toB, A.n);
-      const unsigned long long pb = warp_append(toB, B.n);
+      const unsigned long long ps = warp_append(parked, n_park);
       if (parked) {
-        const ParkList& Lst = toB ? B : A;
-        const unsigned long long ps = toB ? pb : pa;
-        if (ps < Lst.cap) {
+        if (ps < park_cap) {
           pk.i = uint32_t(i);
           pk.score0 = uint32_t(score0);
           pack_state<T>(pk, Pv, Mv);
-          Lst.p[ps] = pk;
+          park[ps] = pk;
         } else {  // no room left: finish here
           run(c_split, 0xFFFFFFFFu);
           finish = true;
@@ -343,7 +321,6 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_
       rs = rs < 0 ? 0 : (rs > Lc - 1 ? Lc - 1 : rs);
       ref_start = uint32_t(rs);
       kept = st == kDone && k <= int(n) && uint64_t(100) * uint64_t(int64_t(n) - k) >= uint64_t(a.pct) * n;
-      if (kept && a.kb) atomicMin(a.kb + r, uint32_t(k));
     }
     if (a.mode == 0) {
       const bool emit = slot_i < total && in_range && kept;
@@ -369,7 +346,7 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_
 void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint64_t* cand_keys, uint64_t n,
                          unsigned read_bits, unsigned band, unsigned pct, int mode, uint64_t* hit_keys,
                          uint32_t* hit_vals, unsigned long long* d_count, void* d_validated,
-                         const unsigned long long* d_n, bool best) {
+                         const unsigned long long* d_n) {
   if (band == 0 || band > 64) throw InputError("band width must be in [1, 64]");
   if (pct > 100) throw InputError("percent identity must be in [0, 100]");
   if (read_bits + 1 + ref.diag_bits > 64) throw InputError("read batch too large for the 64-bit hit key");
@@ -398,64 +375,33 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
   a.hit_vals = hit_vals;
   a.counter = d_count;
   a.validated = d_validated;
-  a.kb = nullptr;
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, kValThreads), uint64_t(kSMs) * 32));
   KernelScope ks(c, "k_validate");
-  const ParkList none{nullptr, nullptr, 0};
-  auto launch = [&](int phase, uint32_t c_split, ParkList A, ParkList B, int split_lb, ParkList in) {
-    if (band <= 32) {
-      if (phase == 1) QGM_KERNEL(c, (k_validate<uint32_t, 1>), grid, kValThreads, 0, a, c_split, A, B, split_lb, in);
-      else if (phase == 2) QGM_KERNEL(c, (k_validate<uint32_t, 2>), grid, kValThreads, 0, a, c_split, A, B, split_lb, in);
-      else QGM_KERNEL(c, (k_validate<uint32_t, 0>), grid, kValThreads, 0, a, c_split, A, B, split_lb, in);
-    } else {
-      if (phase == 1) QGM_KERNEL(c, (k_validate<uint64_t, 1>), grid, kValThreads, 0, a, c_split, A, B, split_lb, in);
-      else if (phase == 2) QGM_KERNEL(c, (k_validate<uint64_t, 2>), grid, kValThreads, 0, a, c_split, A, B, split_lb, in);
-      else QGM_KERNEL(c, (k_validate<uint64_t, 0>), grid, kValThreads, 0, a, c_split, A, B, split_lb, in);
-    }
-  };
-  const uint32_t chunks = (reads.stride + 31) / 32;
-  const char* cap_env = std::getenv("QGM_VAL_PARK_CAP");  // test knob
-  auto park_cap = [&](uint64_t want) {
-    uint64_t cap = std::min<uint64_t>(n, want);
-    if (cap_env && cap_env[0]) cap = std::min<uint64_t>(cap, std::strtoull(cap_env, nullptr, 10));
-    return std::max<uint64_t>(cap, 1);
-  };
-  const char* bb = std::getenv("QGM_VAL_BEST_BOUND");  // A/B knob: 0 disables the per-read bound
-  if (mode == 0 && best && chunks >= 2 && !(bb && bb[0] == '0')) {
-    // Best-stratum map path: every candidate runs its first 32 rows; those
-    // whose lower bound is still small (likely true hits: at most a third of
-    // the threshold's k) are parked in A and finished first, recording each
-    // read's best kept k (atomicMin); the rest (B) resume against that bound
-    // and mostly stop at once. Exact for the best stratum: a dropped
-    // candidate's k exceeds that of a kept hit of its read.
-    DBuf<uint32_t> kb(c, std::max<uint32_t>(reads.n, 1));
-    QGM_CUDA(cudaMemsetAsync(kb.p, 0xFF, kb.bytes(), c.stream));
-    a.kb = kb.p;
-    DBuf<Parked> pa(c, park_cap(uint64_t(1) << 24)), pb(c, park_cap(uint64_t(1) << 28));
-    DBuf<unsigned long long> np(c, 2);
-    np.zero();
-    const ParkList A{pa.p, np.p, pa.n}, B{pb.p, np.p + 1, pb.n};
-    const int split_lb = std::max(2, int((100 - pct) * reads.stride / 300));
-    launch(1, 1, A, B, split_lb, none);
-    launch(2, 1, none, none, -1, A);
-    launch(2, 1, none, none, -1, B);
-    return;
-  }
   // map path: split after ~60% of the rows when at least one chunk remains
   // (a lower bound on the cost only becomes large enough to abandon a random
   // window past about half the read, profiles/r01/README.md)
+  const uint32_t chunks = (reads.stride + 31) / 32;
   const uint32_t c_split = uint32_t((reads.stride * 0.6 + 16) / 32);
   if (mode == 0 && c_split >= 1 && c_split < chunks) {
-    // survivors parked for phase 2, at most 16M (candidates beyond finish in phase 1)
-    DBuf<Parked> park(c, park_cap(uint64_t(1) << 24));
+    // survivors parked for phase 2, at most 16M (candidates beyond finish in
+    // phase 1)
+    uint64_t cap = std::min<uint64_t>(n, uint64_t(1) << 24);
+    if (const char* e = std::getenv("QGM_VAL_PARK_CAP")) cap = std::min<uint64_t>(cap, std::strtoull(e, nullptr, 10));  // test knob
+    cap = std::max<uint64_t>(cap, 1);
+    DBuf<Parked> park(c, cap);
     DBuf<unsigned long long> np(c, 1);
     np.zero();
-    const ParkList A{park.p, np.p, park.n};
-    launch(1, c_split, A, none, -1, none);
-    launch(2, c_split, none, none, -1, A);
+    if (band <= 32) {
+      QGM_KERNEL(c, (k_validate<uint32_t, 1>), grid, kValThreads, 0, a, c_split, park.p, np.p, cap);
+      QGM_KERNEL(c, (k_validate<uint32_t, 2>), grid, kValThreads, 0, a, c_split, park.p, np.p, cap);
+    } else {
+      QGM_KERNEL(c, (k_validate<uint64_t, 1>), grid, kValThreads, 0, a, c_split, park.p, np.p, cap);
+      QGM_KERNEL(c, (k_validate<uint64_t, 2>), grid, kValThreads, 0, a, c_split, park.p, np.p, cap);
+    }
     return;
   }
-  launch(0, 0, none, none, -1, none);
+  if (band <= 32) QGM_KERNEL(c, (k_validate<uint32_t, 0>), grid, kValThreads, 0, a, 0u, nullptr, nullptr, uint64_t(0));
+  else QGM_KERNEL(c, (k_validate<uint64_t, 0>), grid, kValThreads, 0, a, 0u, nullptr, nullptr, uint64_t(0));
 }
 
 }  // namespace qgm
