@@ -346,7 +346,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   {
     StageScope s(c, kStageValidate);
     validate_candidates(c, reads, ref, alt.p, n_raw, rb, P.band_width, P.pct_identity, 0, hkeys.p, hvals.p, cnt.p,
-                        nullptr, cnt.p + 1);
+                        nullptr, cnt.p + 1, P.q);
   }
   if (after_filter && hook_at == 2) after_filter();
   DBuf<uint32_t> per_read;

@@ -348,11 +348,13 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
 // mode 0: append kept hits as (hit key, k) to hit_keys/hit_vals (counter in
 //         *d_count); mode 1: write one qgm_validated per candidate.
 // d_n (nullable): the exact candidate count in device memory, n then only
-// bounds it (no host round trip between dedup and validation).
+// bounds it (no host round trip between dedup and validation). seed_q: the
+// filtration's q (every candidate has a q-row exact seed; it places the map
+// path's phase split).
 void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint64_t* cand_keys, uint64_t n,
                          unsigned read_bits, unsigned band, unsigned pct, int mode, uint64_t* hit_keys,
                          uint32_t* hit_vals, unsigned long long* d_count, void* d_validated,
-                         const unsigned long long* d_n = nullptr);
+                         const unsigned long long* d_n = nullptr, unsigned seed_q = 0);
 
 // strata.cu -- dedup (read, chrom, ref_start, strand) keeping min k, then
 // best-stratum / all; writes qgm_hit records, returns their count.

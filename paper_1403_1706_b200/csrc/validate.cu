@@ -110,27 +110,58 @@ template <> struct Band<uint64_t> {
   }
 };
 
+// Lower bound of min_t D[i][t] over the band row from D[i][0] = score0 and
+// the row's steps (Pv / Mv bit t: D[i][t] - D[i][t-1] = +1 / -1), in
+// segments of 8 diagonals: D at a segment's first diagonal is exact (score0
+// plus the steps before it) and inside the segment at most its -1 steps are
+// subtracted. Tighter than the whole-row bound D[i][0] - popc(Mv) (on a
+// simulated random window, n = 100, B = 32, k_max = 20, it passes k_max at
+// row ~48 instead of ~62) for 4 extra popcounts per 16 rows; measured on
+// B200: C3 validation 12.82 -> 12.64 ms, C2 0.559 -> 0.554 ms (segments of 4
+// cost more than they save; QGM_VAL_SEG >= the word width = whole row).
+#ifndef QGM_VAL_SEG
+#define QGM_VAL_SEG 8
+#endif
+template <class T>
+__device__ __forceinline__ int row_lower_bound(int score0, T Pv, T Mv) {
+  constexpr int kBits = int(sizeof(T) * 8), kSeg = QGM_VAL_SEG < kBits ? QGM_VAL_SEG : kBits;
+  if (kSeg == kBits) return score0 - int(popcount_t(Mv));  // one segment: the whole row
+  int lb = score0 - int(popcount_t(T(Mv & T((T(1) << (kSeg % kBits)) - T(1)))));
+#pragma unroll
+  for (int s = kSeg; s < kBits; s += kSeg) {
+    const T below = (T(1) << s) - T(1);                                      // steps of diagonals < s
+    const T upto = s + kSeg >= kBits ? T(~T(0)) : (T(1) << (s + kSeg)) - T(1);  // ... of diagonals < s + kSeg
+    lb = min(lb, score0 + int(popcount_t(T(Pv & below))) - int(popcount_t(T(Mv & upto))));
+  }
+  return lb;
+}
+
 // Returns false when the candidate was abandoned early: every path crosses
-// every row with non-decreasing cost, so k >= min_t D[i][t] >= D[i][0] -
-// popc(Mv) at any row i; once that bound exceeds kmax the candidate cannot
-// pass the identity threshold (used by the map path only, kmax < 0 = never).
-// Rows of chunks [c_begin, c_end) (32 rows per chunk). Returns kAbandoned,
-// kDone (the last row was processed) or kPaused (stopped at c_end < chunks).
+// every row with non-decreasing cost, so k >= min_t D[i][t] >=
+// row_lower_bound at any row i; once that bound exceeds kmax the candidate
+// cannot pass the identity threshold (used by the map path only, kmax < 0 =
+// never).
+// Rows [r_begin, min(n, r_end)) of the reversed read, r_begin a multiple of
+// 16 (chunks of 32 rows share one read word and window shift; each chunk
+// runs as two unrolled halves of 16 rows, the bound checked after each).
+// Returns kAbandoned, kDone (the last row was processed) or kPaused (stopped
+// at r_end < n).
 constexpr int kAbandoned = 0, kDone = 1, kPaused = 2;
 template <class T, bool kCheck, bool kFull>
 __device__ __forceinline__ int myers_rows(const ValArgs& a, uint32_t r, bool rev, uint32_t n, int64_t F, uint32_t L,
                                           int64_t cbeg, int64_t cend, T mask_rt, T& Pv, T& Mv, int& score0,
-                                          int kmax, uint32_t c_begin, uint32_t c_end) {
+                                          int kmax, uint32_t r_begin, uint32_t r_end) {
   // kFull: the band fills the word (B = 32 / 64), every mask is a no-op
   const T mask = kFull ? T(~T(0)) : mask_rt;
   constexpr int NW = Band<T>::kWords;
   const uint2* rp = a.rplanes + uint64_t(r) * a.Wp;
+  const uint32_t c_begin = r_begin >> 5;
   Win w[NW + 1];
 #pragma unroll
   for (int i = 0; i <= NW; ++i)
     w[i] = load_win(a.fplanes, F + int64_t(L) - 32 * int64_t(c_begin + i + 1), cbeg, cend, !kCheck);
-  const uint32_t chunks = (n + 31) >> 5;
-  const uint32_t c_stop = min(chunks, c_end);
+  const uint32_t r_stop = min(n, r_end);
+  const uint32_t c_stop = (r_stop + 31) >> 5;
   for (uint32_t c = c_begin; c < c_stop; ++c) {
     if (c > c_begin) {
 #pragma unroll
@@ -168,27 +199,38 @@ __device__ __forceinline__ int myers_rows(const ValArgs& a, uint32_t r, bool rev
       Mv = nM;
       score0 += int(D1 & T(1));
     };
-    const uint32_t rows = min(32u, n - 32 * c);
-    if (rows == 32) {  // whole chunk: constant shift amounts, no per-row loop control
-#pragma unroll
-      for (uint32_t t = 0; t < 32; ++t) {
-        row(t);
-        if ((t & 15) == 15 && kmax >= 0 && score0 - int(popcount_t(Mv)) > kmax) {
+    auto abandon = [&](uint32_t row_end) {
+      if (kmax >= 0 && row_lower_bound<T>(score0, Pv, Mv) > kmax) {
 #ifdef QGM_VAL_HIST
-          atomicAdd(&g_exit_hist[min(14u, (32 * c + t) / 16)], 1ull);
+        atomicAdd(&g_exit_hist[min(14u, row_end / 16)], 1ull);
 #endif
-          return kAbandoned;
-        }
+        return true;
       }
-    } else {
+      return false;
+    };
+    // rows [t, t_hi) of this chunk: whole halves unrolled (constant shift
+    // amounts, no per-row loop control), the read's last partial half looped
+    uint32_t t = c == c_begin ? (r_begin & 31) : 0u;
+    const uint32_t t_hi = min(32u, r_stop - 32 * c);
+    if (t == 0 && t_hi >= 16) {
+#pragma unroll
+      for (uint32_t u = 0; u < 16; ++u) row(u);
+      if (abandon(32 * c + 16)) return kAbandoned;
+      t = 16;
+    }
+    if (t == 16 && t_hi == 32) {
+#pragma unroll
+      for (uint32_t u = 16; u < 32; ++u) row(u);
+      if (abandon(32 * c + 32)) return kAbandoned;
+      t = 32;
+    }
 #pragma unroll 4
-      for (uint32_t t = 0; t < rows; ++t) {
-        row(t);
-        if ((t & 15) == 15 && kmax >= 0 && score0 - int(popcount_t(Mv)) > kmax) return kAbandoned;
-      }
+    for (; t < t_hi; ++t) {
+      row(t);
+      if ((t & 15) == 15 && abandon(32 * c + t + 1)) return kAbandoned;
     }
   }
-  if (c_stop < chunks) return kPaused;
+  if (r_stop < n) return kPaused;
 #ifdef QGM_VAL_HIST
   atomicAdd(&g_exit_hist[15], 1ull);
 #endif
@@ -196,12 +238,12 @@ __device__ __forceinline__ int myers_rows(const ValArgs& a, uint32_t r, bool rev
 }
 
 // Validation in up to two phases on the map path: phase 1 runs every
-// candidate for its first c_split chunks of 32 rows and parks the survivors
-// (candidate index + Pv, Mv, score0) in a compact list; phase 2 resumes only
-// those. Candidates of random windows are abandoned around row 64 (n = 100)
-// while true hits run all n rows; mixed in one warp, every warp would run n
-// rows -- after the split, phase-1 warps stop at the split and phase-2 warps
-// are full of candidates that need the remaining rows.
+// candidate for its first r_split rows and parks the survivors (candidate
+// index + Pv, Mv, score0) in a compact list; phase 2 resumes only those.
+// Candidates of random windows are abandoned around row 48 (n = 100) while
+// true hits run all n rows; mixed in one warp, every warp would run n rows --
+// after the split, phase-1 warps stop at the split and phase-2 warps are full
+// of candidates that need the remaining rows.
 struct Parked {
   uint32_t i, score0;
   uint32_t pv[2], mv[2];  // T = u32 uses word 0
@@ -225,10 +267,11 @@ __device__ __forceinline__ void unpack_state(const Parked& p, T& Pv, T& Mv) {
   }
 }
 
-// kPhase 0: every row (qgm_validate, or no split); 1: chunks [0, c_split),
-// survivors parked; 2: resume the parked candidates from chunk c_split.
+// kPhase 0: every row (qgm_validate, or no split); 1: rows [0, r_split),
+// survivors parked; 2: resume the parked candidates from row r_split (a
+// multiple of 16).
 template <class T, int kPhase>
-__global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_split, Parked* __restrict__ park,
+__global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t r_split, Parked* __restrict__ park,
                                                           unsigned long long* __restrict__ n_park, uint64_t park_cap) {
   const T mask = a.B >= sizeof(T) * 8 ? T(~T(0)) : T((T(1) << a.B) - 1);
   const uint64_t dmask = (uint64_t(1) << a.diag_bits) - 1;
@@ -289,7 +332,7 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_
         // map path: abandon candidates that can no longer reach the threshold
         kmax = a.mode == 0 ? int((uint64_t(100 - a.pct) * n) / 100) : -1;
         interior = w0 >= 0 && w0 + int64_t(L) <= Lc;
-        run(kPhase == 2 ? c_split : 0u, kPhase == 1 ? c_split : 0xFFFFFFFFu);
+        run(kPhase == 2 ? r_split : 0u, kPhase == 1 ? r_split : 0xFFFFFFFFu);
         parked = kPhase == 1 && st == kPaused;
         finish = !parked;
       }
@@ -303,7 +346,7 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_
           pack_state<T>(pk, Pv, Mv);
           park[ps] = pk;
         } else {  // no room left: finish here
-          run(c_split, 0xFFFFFFFFu);
+          run(r_split, 0xFFFFFFFFu);
           finish = true;
         }
       }
@@ -346,7 +389,7 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t c_
 void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint64_t* cand_keys, uint64_t n,
                          unsigned read_bits, unsigned band, unsigned pct, int mode, uint64_t* hit_keys,
                          uint32_t* hit_vals, unsigned long long* d_count, void* d_validated,
-                         const unsigned long long* d_n) {
+                         const unsigned long long* d_n, unsigned seed_q) {
   if (band == 0 || band > 64) throw InputError("band width must be in [1, 64]");
   if (pct > 100) throw InputError("percent identity must be in [0, 100]");
   if (read_bits + 1 + ref.diag_bits > 64) throw InputError("read batch too large for the 64-bit hit key");
@@ -377,12 +420,15 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
   a.validated = d_validated;
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, kValThreads), uint64_t(kSMs) * 32));
   KernelScope ks(c, "k_validate");
-  // map path: split after ~60% of the rows when at least one chunk remains
-  // (a lower bound on the cost only becomes large enough to abandon a random
-  // window past about half the read, profiles/r01/README.md)
-  const uint32_t chunks = (reads.stride + 31) / 32;
-  const uint32_t c_split = uint32_t((reads.stride * 0.6 + 16) / 32);
-  if (mode == 0 && c_split >= 1 && c_split < chunks) {
+  // map path: split where a candidate's lower bound has passed k_max unless
+  // it is a true hit: the DP's minimum grows ~0.42 per row on a random
+  // window, plus the q rows of the seed match every candidate has (row ~64
+  // of 100 at 80% identity, ~128 of 250 at 80%; measured, profiles/r02/
+  // README.md), rounded to 16 rows
+  const uint32_t kmax = uint32_t((uint64_t(100 - pct) * reads.stride) / 100);
+  uint32_t r_split = (uint32_t(double(kmax) / 0.42) + seed_q + 8) & ~15u;
+  if (const char* e = std::getenv("QGM_VAL_SPLIT")) r_split = uint32_t(std::atoi(e)) & ~15u;  // A/B knob
+  if (mode == 0 && r_split >= 16 && r_split < reads.stride) {
     // survivors parked for phase 2, at most 16M (candidates beyond finish in
     // phase 1)
     uint64_t cap = std::min<uint64_t>(n, uint64_t(1) << 24);
@@ -392,11 +438,11 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
     DBuf<unsigned long long> np(c, 1);
     np.zero();
     if (band <= 32) {
-      QGM_KERNEL(c, (k_validate<uint32_t, 1>), grid, kValThreads, 0, a, c_split, park.p, np.p, cap);
-      QGM_KERNEL(c, (k_validate<uint32_t, 2>), grid, kValThreads, 0, a, c_split, park.p, np.p, cap);
+      QGM_KERNEL(c, (k_validate<uint32_t, 1>), grid, kValThreads, 0, a, r_split, park.p, np.p, cap);
+      QGM_KERNEL(c, (k_validate<uint32_t, 2>), grid, kValThreads, 0, a, r_split, park.p, np.p, cap);
     } else {
-      QGM_KERNEL(c, (k_validate<uint64_t, 1>), grid, kValThreads, 0, a, c_split, park.p, np.p, cap);
-      QGM_KERNEL(c, (k_validate<uint64_t, 2>), grid, kValThreads, 0, a, c_split, park.p, np.p, cap);
+      QGM_KERNEL(c, (k_validate<uint64_t, 1>), grid, kValThreads, 0, a, r_split, park.p, np.p, cap);
+      QGM_KERNEL(c, (k_validate<uint64_t, 2>), grid, kValThreads, 0, a, r_split, park.p, np.p, cap);
     }
     return;
   }

@@ -2,7 +2,8 @@
 # A/B of library builds on the GPU box: one short bench line per (config,
 # build) with per-kernel times. Builds: the in-tree library ("new"),
 # build/libqgm_old.so (OLD=1) and build/var_<v>.so (VARS="v1 v2", made by
-# tools/build_variant.sh). Usage: CFGS="C3shard C2" VARS="d32" bash tools/ab.sh
+# tools/build_variant.sh) and the in-tree library under environment knobs
+# (ENVS="tag:VAR=value ..."). Usage: CFGS="C3shard C2" VARS="d32" bash tools/ab.sh
 set -u
 cd /root/repo
 run() { tag=$1; shift; env "$@" timeout 600 python bench.py --config $CFG --steps 3 --warmup 2 --check off --no-cpu 2>/dev/null | python -c "
@@ -13,4 +14,5 @@ for CFG in ${CFGS:-C3shard C2 C1}; do
 run new X=1
 [ -n "${OLD:-}" ] && run old QGM_LIB=/root/repo/build/libqgm_old.so
 for v in ${VARS:-}; do run $v QGM_LIB=/root/repo/build/var_$v.so; done
+for e in ${ENVS:-}; do run ${e%%:*} ${e#*:}; done
 done
