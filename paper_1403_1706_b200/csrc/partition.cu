@@ -37,9 +37,9 @@ namespace {
 #endif
 constexpr int kPartThreads = QGM_PART_THREADS;
 #ifndef QGM_PART_MINB
-#define QGM_PART_MINB (1024 / QGM_PART_THREADS)
+#define QGM_PART_MINB 3
 #endif
-constexpr int kPartMinBlocks = QGM_PART_MINB;  // 4: 64 registers per thread
+constexpr int kPartMinBlocks = QGM_PART_MINB;  // 3: 85 registers per thread (the pipelined P1 spills at 64)
 constexpr unsigned kBinBits = 8;
 constexpr uint32_t kBins = 1u << kBinBits;
 constexpr uint32_t kChunk = 8 * kPartThreads;  // q-gram slots per chunk; staging = 8 B each
@@ -57,8 +57,15 @@ constexpr unsigned kP1CodeShift = kItemCodeShift, kP1MetaShift = kItemFbShift;  
 // Q = compile-time q (0: the runtime value), so every shift is an immediate.
 struct Run {
   uint32_t r, o0, n;
-  uint64_t A;
+  uint64_t A;  // 32 read bases from o0 - 1, MSB-first
 };
+
+// reverse complement of 32 MSB-first bases: complement, reverse the 2-bit groups
+__device__ __forceinline__ uint64_t revcomp32(uint64_t a) {
+  const uint64_t x = ~a;
+  const uint64_t r = (uint64_t(__brev(uint32_t(x))) << 32) | __brev(uint32_t(x >> 32));
+  return ((r >> 1) & 0x5555555555555555ull) | ((r & 0x5555555555555555ull) << 1);
+}
 
 template <int Q>
 struct ItemGen {
@@ -85,14 +92,17 @@ struct ItemGen {
     u.n = __ldg(lengths + u.r);
     u.A = window(u.r, u.o0);
   }
-  // slot j of a fetched run: canonical code g, own code f, meta, position
+  // slot j of a fetched run: canonical code g, own code f, meta, position.
+  // RC = revcomp32(u.A), computed once per run by the caller.
   template <int R>
-  __device__ __forceinline__ bool run_slot(uint32_t run, const Run& u, uint32_t j, uint32_t& f, uint32_t& g,
-                                           uint32_t& m, uint32_t& pos) const {
+  __device__ __forceinline__ bool run_slot(uint32_t run, const Run& u, uint64_t RC, uint32_t j, uint32_t& f,
+                                           uint32_t& g, uint32_t& m, uint32_t& pos) const {
     const unsigned q = this->q();
     const uint32_t o = u.o0 + j;
     f = uint32_t((u.A << (2 * j + 2)) >> (64 - 2 * q));
-    g = canon_code(f, q);
+    // rc(f): bases j+1 .. j+q of A sit at bits [2j+2, 2j+2+2q) of RC
+    const uint32_t rc = uint32_t(RC >> (2 * j + 2)) & (q == 16 ? 0xFFFFFFFFu : (1u << (2 * q)) - 1u);
+    g = f * 0x9E3779B1u <= rc * 0x9E3779B1u ? f : rc;  // canon_code(f, q)
     const uint32_t bl = uint32_t(u.A >> (62 - 2 * j)) & 3u;
     const uint32_t br = uint32_t(u.A >> (62 - 2 * (j + q + 1))) & 3u;
     m = (o ? bl : 4u) | ((o + q < u.n ? 3u - br : 4u) << 3) | (uint32_t(f != g) << 6);
@@ -136,10 +146,11 @@ __global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen<Q> gen,
 #pragma unroll
     for (int h = 0; h < kRuns; ++h) {
       const uint32_t tr = t0 + h * kHistThreads + threadIdx.x;
+      const uint64_t RC = revcomp32(u[h].A);
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         uint32_t f, g, m, pos;
-        const bool ok = gen.template run_slot<R>(tr, u[h], j, f, g, m, pos) && tr < c1;
+        const bool ok = gen.template run_slot<R>(tr, u[h], RC, j, f, g, m, pos) && tr < c1;
         const uint32_t k = g >> kshift, sh = (k & 1u) * 16u;
         key[h * R + j] = k;
         // unconditional (an invalid slot adds 0): no branch around the atomic
@@ -178,6 +189,11 @@ __global__ void k_bin_offsets(const uint32_t* __restrict__ soff, uint32_t nbins,
   }
 }
 
+// P1, software-pipelined over the CTA's chunks: while chunk i's bin runs are
+// being reserved (one global cursor atomic per bin, the round trip that
+// dominated the stalls of the unpipelined loop) and written out, the items of
+// chunk i+1 are generated and counted, and the read words of chunk i+2 are
+// already in flight.
 template <int Q, int R>
 __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(ItemGen<Q> gen, unsigned shift,
                                                                   const uint32_t* __restrict__ boff,
@@ -185,64 +201,83 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
                                                                   uint64_t* __restrict__ out) {
   extern __shared__ uint64_t stage[];  // kChunk items, bin-sorted, then kChunk u8 bins
   uint8_t* sbin = reinterpret_cast<uint8_t*>(stage + kChunk);
-  __shared__ uint32_t cnt[kBins], lofs[kBins], gdst[kBins];
+  __shared__ uint32_t cnt[2][kBins], lofs[kBins], delta[kBins];
   __shared__ uint32_t ws[33];
   const uint32_t lmask = shift ? (1u << shift) - 1u : 0u;
   constexpr uint32_t kRuns = kPer / R;  // runs per thread per chunk
   constexpr uint32_t kChunkRuns = kRuns * kPartThreads;
   const uint32_t n_chunks = (gen.n_runs + kChunkRuns - 1) / kChunkRuns;
-  for (uint32_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
-    const uint32_t c0 = ch * kChunkRuns;
-    for (uint32_t b = threadIdx.x; b < kBins; b += kPartThreads) cnt[b] = 0;
-    __syncthreads();
-    uint64_t item[kPer];
-    uint32_t bin[kPer];  // ~0u = no q-gram at this slot
+  uint32_t ch = blockIdx.x;
+  if (ch >= n_chunks) return;  // CTA-uniform
+  const uint32_t b = threadIdx.x;  // the bin this thread scans / reserves (b < kBins)
+  for (uint32_t i = b; i < 2 * kBins; i += kPartThreads) (&cnt[0][0])[i] = 0;
+  Run u[kRuns];
+  auto fetch = [&](uint32_t c) {
 #pragma unroll
-    for (uint32_t h0 = 0; h0 < kRuns; h0 += (kRuns < 4 ? kRuns : 4)) {
-      constexpr uint32_t kIn = kRuns < 4 ? kRuns : 4;  // runs whose loads are issued together
-      Run u[kIn];
+    for (uint32_t h = 0; h < kRuns; ++h) gen.template fetch_run<R>(c * kChunkRuns + h * kPartThreads + b, u[h]);
+  };
+  uint64_t item[kPer];
+  uint32_t bin[kPer];  // bin | rank among the chunk's items of that bin << 8; ~0u = no q-gram at this slot
+  // items of chunk c from the fetched runs (counted into cnt[par]); then the
+  // runs of the CTA's next chunk are fetched
+  auto generate = [&](uint32_t c, uint32_t par) {
 #pragma unroll
-      for (uint32_t h = 0; h < kIn; ++h) gen.template fetch_run<R>(c0 + (h0 + h) * kPartThreads + threadIdx.x, u[h]);
+    for (uint32_t h = 0; h < kRuns; ++h) {
+      const uint32_t tr = c * kChunkRuns + h * kPartThreads + b;
+      const uint64_t RC = revcomp32(u[h].A);
 #pragma unroll
-      for (uint32_t h = 0; h < kIn; ++h) {
-        const uint32_t tr = c0 + (h0 + h) * kPartThreads + threadIdx.x;
-#pragma unroll
-        for (uint32_t j = 0; j < R; ++j) {
-          const uint32_t e = (h0 + h) * R + j;
-          uint32_t f, g, m, pos;
-          const bool ok = gen.template run_slot<R>(tr, u[h], j, f, g, m, pos);
-          item[e] = (uint64_t(g & lmask) << kP1CodeShift) | (uint64_t(m) << kP1MetaShift) | pos;
-          // bin | rank among the chunk's items of that bin << 8 (the count's
-          // atomic returns the rank, so placement needs no second atomic)
-          bin[e] = ok ? (g >> shift) | (atomicAdd(cnt + (g >> shift), 1u) << 8) : ~0u;
-        }
+      for (uint32_t j = 0; j < R; ++j) {
+        const uint32_t e = h * R + j;
+        uint32_t f, g, m, pos;
+        const bool ok = gen.template run_slot<R>(tr, u[h], RC, j, f, g, m, pos);
+        item[e] = (uint64_t(g & lmask) << kP1CodeShift) | (uint64_t(m) << kP1MetaShift) | pos;
+        // the count's atomic returns the rank: placement needs no second atomic
+        bin[e] = ok ? (g >> shift) | (atomicAdd(&cnt[par][g >> shift], 1u) << 8) : ~0u;
       }
     }
-    __syncthreads();
-    uint32_t total;  // valid items in the chunk
-    {  // local exclusive offsets; reserve the chunk's run in every bin
-      const uint32_t b = threadIdx.x;
-      const uint32_t v = b < kBins ? cnt[b] : 0u;
-      const uint32_t ex = block_exclusive_scan<uint32_t>(v, ws, &total);
-      if (b < kBins) {
-        lofs[b] = ex;
-        gdst[b] = v ? boff[b] + atomicAdd(cursor + b, v) : 0u;
-      }
+    if (c + gridDim.x < n_chunks) fetch(c + gridDim.x);
+  };
+  // local exclusive offsets of cnt[par]; the chunk's run in every bin reserved
+  // (the reservation's value is only needed at the write-out); cnt[par] reset
+  auto scan = [&](uint32_t par, uint32_t& g, uint32_t& total) {
+    const uint32_t v = b < kBins ? cnt[par][b] : 0u;
+    const uint32_t ex = block_exclusive_scan<uint32_t>(v, ws, &total);
+    if (b < kBins) {
+      lofs[b] = ex;
+      g = v ? boff[b] + atomicAdd(cursor + b, v) : 0u;
+      cnt[par][b] = 0;
     }
-    __syncthreads();
+  };
+  auto place = [&] {
 #pragma unroll
     for (uint32_t k = 0; k < kPer; ++k)
       if (bin[k] != ~0u) {
-        const uint32_t b = bin[k] & 0xFFu, slot = lofs[b] + (bin[k] >> 8);
+        const uint32_t bb = bin[k] & 0xFFu, slot = lofs[bb] + (bin[k] >> 8);
         stage[slot] = item[k];
-        sbin[slot] = uint8_t(b);
+        sbin[slot] = uint8_t(bb);
       }
+  };
+  fetch(ch);
+  __syncthreads();  // counters zeroed
+  uint32_t par = 0, g = 0, total = 0;
+  generate(ch, par);
+  __syncthreads();
+  scan(par, g, total);
+  __syncthreads();
+  place();
+  for (;;) {
+    const uint32_t nxt = ch + gridDim.x;
+    const bool more = nxt < n_chunks;  // CTA-uniform
+    if (more) generate(nxt, par ^ 1u);  // overlaps the reservation round trip
+    if (b < kBins) delta[b] = g - lofs[b];
+    __syncthreads();  // staged chunk and its destinations visible
+    for (uint32_t i = b; i < total; i += kPartThreads) out[delta[sbin[i]] + i] = stage[i];
+    if (!more) break;
+    par ^= 1u;
+    scan(par, g, total);  // its first barrier also ends the write-out
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < total; i += kPartThreads) {
-      const uint32_t b = sbin[i];
-      out[gdst[b] + (i - lofs[b])] = stage[i];
-    }
-    __syncthreads();
+    place();
+    ch = nxt;
   }
 }
 
@@ -440,7 +475,7 @@ static void p0_p1(Ctx& c, const ItemGen<Q>& gen, const Reads& reads, unsigned q,
   auto p1kern = k_part_scatter<Q, R>;
   QGM_CUDA(cudaFuncSetAttribute(p1kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const uint32_t chunk_runs = kChunk / R;
-  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(gen.n_runs, chunk_runs), uint64_t(kSMs) * 4));
+  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(gen.n_runs, chunk_runs), uint64_t(kSMs) * kPartMinBlocks));
   KernelScope ks(c, "k_part_scatter");
   QGM_KERNEL(c, p1kern, grid, kPartThreads, smem, gen, shift, out.boff.p, hist.p, p1.p);
 }
