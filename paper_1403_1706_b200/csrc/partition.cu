@@ -8,7 +8,7 @@
 //                  code bits) in shared memory (packed u16 counters) and
 //                  flushes them with global atomics;
 //   scan         : sub-bin offsets; the P1 bin offsets are their prefixes;
-//   P1 scatter   : per chunk of 2048 q-gram slots (runs of 8 consecutive
+//   P1 scatter   : per chunk of 4096 q-gram slots (runs of 8 consecutive
 //                  slots per thread sharing one register window of read
 //                  bases), a local counting sort by bin in shared memory
 //                  (the count atomic's return value is the item's rank),
@@ -32,14 +32,18 @@
 namespace qgm {
 namespace {
 
+// P1 geometry (measured, C2 P1 ms: 256 threads x 3 CTAs/SM 0.455, 384 x 2
+// 0.469, 512 x 2 0.407, 768 x 1 0.521, 1024 x 1 0.456): chunks of 4096 slots
+// give bin runs of ~16 items (128 B) per chunk, two CTAs per SM keep 64
+// registers free of spills for the pipelined loop.
 #ifndef QGM_PART_THREADS
-#define QGM_PART_THREADS 256
+#define QGM_PART_THREADS 512
 #endif
 constexpr int kPartThreads = QGM_PART_THREADS;
 #ifndef QGM_PART_MINB
-#define QGM_PART_MINB 3
+#define QGM_PART_MINB 2
 #endif
-constexpr int kPartMinBlocks = QGM_PART_MINB;  // 3: 85 registers per thread (the pipelined P1 spills at 64)
+constexpr int kPartMinBlocks = QGM_PART_MINB;
 constexpr unsigned kBinBits = 8;
 constexpr uint32_t kBins = 1u << kBinBits;
 constexpr uint32_t kChunk = 8 * kPartThreads;  // q-gram slots per chunk; staging = 8 B each
