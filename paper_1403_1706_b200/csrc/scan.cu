@@ -5,6 +5,7 @@
 // Reduce-then-scan over 4096-element tiles: (1) per-tile u64 sums, (2) one
 // CTA scans the tile sums, (3) every tile re-reads its elements, scans them in
 // shared memory and writes out. HBM traffic: 2 reads + 1 write per element.
+// Up to 2^17 elements a single CTA scans tile after tile (k_scan_single).
 #include "internal.hpp"
 
 namespace qgm {
@@ -81,6 +82,55 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(const uint32_t* in, 
   }
 }
 
+// Small inputs (the partition's key offsets, per-read counts of small
+// batches): one CTA walks the tiles in order with a running carry -- one
+// launch instead of three, one read and one write per element.
+constexpr int kSingleThreads = 512;
+constexpr int kSingleTile = kSingleThreads * kScanPer;
+constexpr uint64_t kSingleMax = uint64_t(1) << 17;
+
+__global__ void __launch_bounds__(kSingleThreads) k_scan_single(const uint32_t* in, uint32_t* out, uint64_t n,
+                                                                uint32_t* __restrict__ d_total,
+                                                                int* __restrict__ d_overflow) {
+  __shared__ uint32_t tile[kSingleTile + kSingleTile / 32];
+  __shared__ uint64_t ws[33];
+  uint64_t carry = 0;
+  for (uint64_t base = 0; base < n; base += kSingleTile) {
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+      const uint32_t li = j * kSingleThreads + threadIdx.x;
+      const uint64_t i = base + li;
+      tile[pad_idx(li)] = i < n ? in[i] : 0u;
+    }
+    __syncthreads();
+    uint64_t s = 0;
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) s += tile[pad_idx(threadIdx.x * kScanPer + j)];
+    uint64_t tot;
+    uint64_t run = block_exclusive_scan<uint64_t>(s, ws, &tot) + carry;
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+      const uint32_t li = pad_idx(threadIdx.x * kScanPer + j);
+      const uint32_t v = tile[li];
+      tile[li] = uint32_t(run);
+      run += v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+      const uint32_t li = j * kSingleThreads + threadIdx.x;
+      const uint64_t i = base + li;
+      if (i < n) out[i] = tile[pad_idx(li)];
+    }
+    carry += tot;
+    __syncthreads();  // the tile is rewritten next iteration
+  }
+  if (threadIdx.x == 0) {
+    if (d_total) *d_total = uint32_t(carry);
+    if (d_overflow) *d_overflow = carry > 0xFFFFFFFFull ? 1 : 0;
+  }
+}
+
 __global__ void k_select_flags(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ flags, uint64_t n,
                                uint32_t* __restrict__ f) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
@@ -106,6 +156,10 @@ void exclusive_scan_u32(Ctx& c, const uint32_t* in, uint32_t* out, uint64_t n, u
   if (n == 0) {
     if (d_total) QGM_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), c.stream));
     if (d_overflow) QGM_CUDA(cudaMemsetAsync(d_overflow, 0, sizeof(int), c.stream));
+    return;
+  }
+  if (n <= kSingleMax) {
+    QGM_KERNEL(c, k_scan_single, 1, kSingleThreads, 0, in, out, n, d_total, d_overflow);
     return;
   }
   const uint64_t tiles = ceil_div(n, kScanTile);
