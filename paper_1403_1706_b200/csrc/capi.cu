@@ -263,19 +263,125 @@ static void check_reads_shape(uint32_t n_reads, uint32_t stride) {
 // validation, measured within noise of each other).
 constexpr uint64_t kDedupDirectMax = uint64_t(10) << 20;  // raw keys whose hash table (<= 16M slots) stays L2-resident
 
+static int hook_point() {  // experiment knob: 0 after the join, 1 after dedup, 2 after validation
+  static const int h = [] {
+    const char* e = std::getenv("QGM_HOOK");
+    return e ? std::atoi(e) : 1;
+  }();
+  return h;
+}
+
+static uint64_t dedup_direct_max() {
+  if (const char* e = std::getenv("QGM_DEDUP_DIRECT_MAX")) return std::strtoull(e, nullptr, 10);  // tests
+  return kDedupDirectMax;
+}
+
+// The batch without a host round trip before its end: partition, join,
+// dedup, validation and strata all sized by the candidate-buffer capacity
+// (the larger of 16 per read and 1.125x the context's last count) and run on
+// the device counts; one read-back at the end returns every count. Taken
+// when that capacity is within the always-deduplicated range, so no decision
+// needs the count on the host. Returns false when the join's count exceeded
+// the capacity (keys truncated): the caller maps the batch again with the
+// round-trip path, which sizes the buffer from the count.
+static bool map_reads_async(Ctx& c, const Reads& reads, const Ref& ref, const qgm_map_params& P, int strands,
+                            unsigned rb, uint64_t cap, const std::function<void()>& after_filter, HitsObj& out) {
+  prepare_ref_index(c, ref, P.q);
+  Partitioned rbk;
+  {
+    StageScope s(c, kStageIndex);
+    partition_reads(c, reads, P.q, rbk);
+  }
+  DBuf<uint64_t> keys(c, cap), alt;
+  DBuf<unsigned long long> jc(c, 3);  // candidates, lookups that hit, occurrences
+  {
+    StageScope s(c, kStageFilter);
+    join_filter(c, rbk, reads, ref, strands, QGM_FILTER_RUN_START, rb, keys, nullptr, jc.p);
+  }
+  if (after_filter && hook_point() == 0) after_filter();
+  DBuf<unsigned long long> cnt(c, 3);  // validated hits, unique candidates, reads with > 32 hits
+  cnt.zero();
+  {
+    StageScope s(c, kStageSort);
+    dedup_keys_dev(c, keys.p, cap, jc.p, alt, cnt.p + 1);
+  }
+  if (after_filter && hook_point() == 1) after_filter();
+  DBuf<uint64_t> hkeys(c, cap);
+  DBuf<uint32_t> hvals(c, cap);
+  {
+    StageScope s(c, kStageValidate);
+    validate_candidates(c, reads, ref, alt.p, cap, rb, P.band_width, P.pct_identity, 0, hkeys.p, hvals.p, cnt.p,
+                        nullptr, cnt.p + 1, P.q);
+  }
+  if (after_filter && hook_point() == 2) after_filter();
+  DBuf<uint32_t> per_read, kept_total(c, 1);
+  unsigned long long jh[3] = {0, 0, 0}, h[3] = {0, 0, 0};
+  uint32_t fl[4] = {0, 0, 0, 0}, kept = 0;
+  {
+    StageScope s(c, kStageStrata);
+    strata_count(c, ref, hkeys.p, cnt.p, cap, reads.n, per_read, cnt.p + 2);
+    stratify_unsorted_dev(c, ref, hkeys.p, hvals.p, cnt.p, cap, reads.n, int(P.mode), per_read, cnt.p + 2, out.hits,
+                          kept_total.p);
+    // the batch's one host round trip
+    QGM_CUDA(cudaMemcpyAsync(jh, jc.p, sizeof(jh), cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaMemcpyAsync(fl, rbk.flags.p, sizeof(fl), cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaMemcpyAsync(&kept, kept_total.p, 4, cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaStreamSynchronize(c.stream));
+  }
+  if (fl[2]) throw InputError("read longer than the stride");
+  c.last_raw_candidates = jh[0];
+  if (jh[0] > cap) return false;
+  const uint64_t n_val = h[0];
+  out.n = kept;
+  if (h[2] != 0) {  // a read with > 32 hits: the radix-sorted strata on the known count
+    StageScope s(c, kStageStrata);
+    out.n = stratify_unsorted(c, ref, hkeys, hvals, n_val, reads.n, int(P.mode), per_read, true, out.hits);
+  }
+  out.n_reads = reads.n;
+  out.stats[0] = jh[0];
+  out.stats[1] = h[1];
+  out.stats[2] = n_val;
+  out.stats[3] = out.n;
+  out.stats[5] = fl[0];
+  out.stats[6] = jh[1];
+  out.stats[7] = jh[2];
+  return true;
+}
+
 static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_map_params& P,
-                         const std::function<void()>& after_filter = {}) {
+                         const std::function<void()>& after_filter_once = {}) {
+  bool hooked = false;  // the hook runs once even when the batch is mapped twice
+  const std::function<void()> after_filter = [&] {
+    if (after_filter_once && !hooked) {
+      hooked = true;
+      after_filter_once();
+    }
+  };
   if (P.q == 0 || P.q > 16) throw InputError("q must be in [1, 16]");
   if (P.band_width == 0 || P.band_width > 64) throw InputError("band width must be in [1, 64]");
   if (P.pct_identity > 100) throw InputError("percent identity must be in [0, 100]");
   if (P.mode > 1) throw InputError("mode must be best-stratum (0) or all (1)");
   const int strands = P.strands ? int(P.strands) : 3;
+  if (P.group_width && P.group_width != 32 && P.group_width != 64) throw InputError("group width must be 32 or 64");
+  if (ref.padded_total < (uint64_t(1) << 32)) {
+    const uint64_t cap = std::max<uint64_t>(std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16),
+                                            c.last_raw_candidates + c.last_raw_candidates / 8);
+    static const bool async_off = [] {
+      const char* e = std::getenv("QGM_MAP_ASYNC");  // A/B knob: 0 = always the round-trip path
+      return e && e[0] == '0';
+    }();
+    if (!async_off && cap <= dedup_direct_max()) {
+      HitsObj out;
+      if (map_reads_async(c, reads, ref, P, strands, read_bits_for(reads.n), cap, after_filter, out)) return out;
+      // truncated candidate set: map again below (the hook has run)
+    }
+  }
   const unsigned rb = read_bits_for(reads.n);
   HitsObj out;
   DBuf<uint64_t> keys, alt;
   uint64_t n_raw, n_u;
   uint64_t fst[3] = {0, 0, 0};
-  if (P.group_width && P.group_width != 32 && P.group_width != 64) throw InputError("group width must be 32 or 64");
   if (ref.padded_total < (uint64_t(1) << 32)) {
     // production path: read q-grams bucket-sorted by code, joined with the
     // per-strand reference q-group indexes (join.cu). group_width / sampled
@@ -305,10 +411,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   }
   out.stats[6] = fst[0];
   out.stats[7] = fst[1];
-  static const int hook_at = [] {  // experiment knob: 0 after the join, 1 after dedup, 2 after validation
-    const char* e = std::getenv("QGM_HOOK");
-    return e ? std::atoi(e) : 1;
-  }();
+  const int hook_at = hook_point();
   if (after_filter && hook_at == 0) after_filter();
   // cnt[0]: validated hits, cnt[1]: unique candidates, cnt[2]: reads with
   // more than 32 hits -- read back together after validation (no host round
@@ -322,9 +425,7 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   // is a pure function of the key and the strata keep one hit per (read,
   // chromosome, start, strand). unique_candidates then reports the raw count.
   bool dedup = true;
-  uint64_t direct_max = kDedupDirectMax;
-  if (const char* e = std::getenv("QGM_DEDUP_DIRECT_MAX")) direct_max = std::strtoull(e, nullptr, 10);  // tests
-  if (n_raw > direct_max) {
+  if (n_raw > dedup_direct_max()) {
     StageScope s(c, kStageSort);
     dedup = estimate_dup_fraction(c, keys.p, n_raw, ref.diag_bits + 1) > 0.10;
   }

@@ -94,6 +94,67 @@ __global__ void __launch_bounds__(kDedupThreads) k_tile_compact(const uint64_t* 
     if (v[j] != kEmpty) out[o++] = v[j];
 }
 
+// ---- device-sized variant (the host knows only a bound of the key count)
+// table slots for n keys: a power of two >= kTile with load <= 2/3 (the host
+// rule of dedup_keys / dedup_keys_async)
+__host__ __device__ __forceinline__ uint64_t table_slots(uint64_t n) {
+  uint64_t T = kTile;
+  while (T < n + n / 2) T <<= 1;
+  return T;
+}
+
+__device__ __forceinline__ uint64_t dev_count(const unsigned long long* d_n, uint64_t n_max) {
+  return min(uint64_t(*d_n), n_max);
+}
+
+__global__ void k_table_clear(uint64_t* __restrict__ table, const unsigned long long* __restrict__ d_n,
+                              uint64_t n_max) {
+  const uint64_t T = table_slots(dev_count(d_n, n_max));
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < T; i += uint64_t(gridDim.x) * blockDim.x)
+    table[i] = kEmpty;
+}
+
+__global__ void k_hash_insert_dev(const uint64_t* __restrict__ keys, const unsigned long long* __restrict__ d_n,
+                                  uint64_t n_max, uint64_t* __restrict__ table) {
+  const uint64_t n = dev_count(d_n, n_max), tmask = table_slots(n) - 1;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t key = keys[i];
+    uint64_t slot = mix64(key) & tmask;
+    while (true) {
+      const uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(table + slot), kEmpty, key);
+      if (prev == kEmpty || prev == key) break;
+      slot = (slot + 1) & tmask;
+    }
+  }
+}
+
+// k_tile_compact over the table of the device count (blocks past it return)
+__global__ void __launch_bounds__(kDedupThreads) k_tile_compact_dev(const uint64_t* __restrict__ table,
+                                                                    const unsigned long long* __restrict__ d_n,
+                                                                    uint64_t n_max, uint64_t* __restrict__ out,
+                                                                    unsigned long long* __restrict__ counter) {
+  __shared__ uint32_t ws[33];
+  __shared__ unsigned long long s_base;
+  constexpr int kPerThread = kTile / kDedupThreads;
+  const uint64_t base = uint64_t(blockIdx.x) * kTile;
+  if (base >= table_slots(dev_count(d_n, n_max))) return;  // CTA-uniform
+  uint64_t v[kPerThread];
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < kPerThread; ++j) {
+    v[j] = table[base + uint64_t(j) * kDedupThreads + threadIdx.x];
+    c += v[j] != kEmpty;
+  }
+  uint32_t tot;
+  const uint32_t ex = block_exclusive_scan<uint32_t>(c, ws, &tot);
+  if (threadIdx.x == 0) s_base = tot ? atomicAdd(counter, (unsigned long long)tot) : 0ull;
+  __syncthreads();
+  uint64_t o = s_base + ex;
+#pragma unroll
+  for (int j = 0; j < kPerThread; ++j)
+    if (v[j] != kEmpty) out[o++] = v[j];
+}
+
 // keys of every (mask+1)-th read (read id = key >> rshift) appended to out
 // (at most cap are stored; n_out keeps counting past cap so the caller sees
 // the overflow)
@@ -130,6 +191,23 @@ void dedup_keys_async(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& 
   if (out.n < n) out.alloc(c, n);
   QGM_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
   QGM_KERNEL(c, k_tile_compact, tiles, kDedupThreads, 0, table.p, out.p, d_count);
+}
+
+void dedup_keys_dev(Ctx& c, const uint64_t* keys, uint64_t n_max, const unsigned long long* d_n,
+                    DBuf<uint64_t>& out, unsigned long long* d_count) {
+  QGM_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
+  if (out.n < std::max<uint64_t>(n_max, 1)) out.alloc(c, std::max<uint64_t>(n_max, 1));
+  if (n_max == 0) return;
+  const uint64_t T = table_slots(n_max);
+  DBuf<uint64_t> table(c, T);
+  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n_max, 256), uint64_t(kSMs) * 16));
+  QGM_KERNEL(c, k_table_clear, unsigned(std::min<uint64_t>(ceil_div(T, 256), uint64_t(kSMs) * 16)), 256, 0, table.p,
+             d_n, n_max);
+  {
+    KernelScope ks(c, "k_hash_insert");
+    QGM_KERNEL(c, k_hash_insert_dev, grid, 256, 0, keys, d_n, n_max, table.p);
+  }
+  QGM_KERNEL(c, k_tile_compact_dev, unsigned(T / kTile), kDedupThreads, 0, table.p, d_n, n_max, out.p, d_count);
 }
 
 uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out) {

@@ -421,7 +421,7 @@ void finish_impl(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_
 
   const size_t smem = B.gpb * sizeof(W) + B.gpb * 4 + (B.gpb * B.w) * 4;
   auto launch = [&](auto kernel) {
-    QGM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kernel), size_t(smem));
     KernelScope ks(c, "k_bucket_emit");
     QGM_KERNEL(c, kernel, grid_b, kBuildThreads, smem, B.pairs.p, B.boff.p, dbase.p, B.buckets, uint32_t(B.gpb),
                reinterpret_cast<const W*>(out.I.p), out.S.p, out.S1.p, out.O.p, extra ? extra->p : nullptr);
@@ -519,7 +519,7 @@ void mask_repeats(Ctx& c, Ref& ref, unsigned q, uint64_t threshold) {
     if (B.V == 0) continue;
     const uint32_t lmask = uint32_t((uint64_t(1) << B.lb) - 1);
     const size_t smem = size_t(lmask + 1) * sizeof(uint32_t);
-    QGM_CUDA(cudaFuncSetAttribute(k_bucket_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ensure_dynamic_smem(reinterpret_cast<const void*>(k_bucket_mask), size_t(smem));
     QGM_KERNEL(c, k_bucket_mask, unsigned(std::min<uint64_t>(B.buckets, uint64_t(kSMs) * 8)), kBuildThreads, smem,
                B.pairs.p, B.boff.p, B.buckets, lmask, threshold, c0,
                reinterpret_cast<unsigned long long*>(ref.mask.p));

@@ -7,6 +7,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <type_traits>
 #include <string>
 #include <utility>
@@ -273,6 +276,10 @@ uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& ou
 // Same without a host round trip: `out` is sized n (the bound) and the unique
 // count lands in d_count (device).
 void dedup_keys_async(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out, unsigned long long* d_count);
+// The same with the key count on the device (*d_n, clamped to n_max): the
+// table is allocated for n_max and sized for *d_n by the kernels themselves.
+void dedup_keys_dev(Ctx& c, const uint64_t* keys, uint64_t n_max, const unsigned long long* d_n,
+                    DBuf<uint64_t>& out, unsigned long long* d_count);
 // Estimated duplicate fraction of a candidate set (keys of every 64th read).
 double estimate_dup_fraction(Ctx& c, const uint64_t* keys, uint64_t n, unsigned rshift);
 
@@ -342,7 +349,11 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out);
 // join.cu -- the same candidates as filter_reference, from a code-ordered
 // join of the partitioned read q-grams with the reference q-group indexes.
 uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Ref& ref, int strands, int mode,
-                     unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats = nullptr);
+                     unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats = nullptr,
+                     unsigned long long* dev_counter = nullptr);
+// dev_counter (nullable): launch only, no host round trip -- the candidate
+// count, join statistics and partition flags are the caller's to read back
+// (keys.n is the capacity; a count above it means the keys were truncated).
 
 // validate.cu
 // mode 0: append kept hits as (hit key, k) to hit_keys/hit_vals (counter in
@@ -386,14 +397,63 @@ void hits_cigar(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, const Reads& read
 uint64_t stratify_hits(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const uint32_t* hit_vals, uint64_t n,
                        uint32_t n_reads, unsigned read_bits, int mode, DBuf<uint8_t>& out);
 
+// Per-process memo of launch configuration queries (they cost host time on
+// every batch otherwise: small batches are bound by the host's enqueue rate).
+struct LaunchMemo {
+  std::mutex m;
+  std::map<std::tuple<int, const void*, int, size_t>, unsigned> grid;
+  std::map<std::pair<int, const void*>, size_t> smem;
+  std::map<std::pair<int, const void*>, cudaFuncAttributes> attrs;
+  static LaunchMemo& get() {
+    static LaunchMemo memo;
+    return memo;
+  }
+};
+
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
 // Persistent-grid size: SMs x resident CTAs per SM for this kernel/config
 // (one full wave; grid-stride kernels then never run a partial second wave).
 inline unsigned resident_grid(const void* kernel, int threads, size_t smem) {
-  int dev = 0, sms = kSMs, per = 1;
-  cudaGetDevice(&dev);
+  const int dev = current_device();
+  LaunchMemo& M = LaunchMemo::get();
+  std::lock_guard<std::mutex> lk(M.m);
+  auto it = M.grid.find({dev, kernel, threads, smem});
+  if (it != M.grid.end()) return it->second;
+  int sms = kSMs, per = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
-  return unsigned(std::max(1, sms * std::max(1, per)));
+  const unsigned g = unsigned(std::max(1, sms * std::max(1, per)));
+  M.grid[{dev, kernel, threads, smem}] = g;
+  return g;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a kernel needs
+// more dynamic shared memory than it was last configured for on this device.
+inline void ensure_dynamic_smem(const void* kernel, size_t smem) {
+  const int dev = current_device();
+  LaunchMemo& M = LaunchMemo::get();
+  std::lock_guard<std::mutex> lk(M.m);
+  size_t& have = M.smem[{dev, kernel}];
+  if (smem <= have) return;
+  QGM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  have = smem;
+}
+
+inline cudaFuncAttributes func_attributes(const void* kernel) {
+  const int dev = current_device();
+  LaunchMemo& M = LaunchMemo::get();
+  std::lock_guard<std::mutex> lk(M.m);
+  auto it = M.attrs.find({dev, kernel});
+  if (it != M.attrs.end()) return it->second;
+  cudaFuncAttributes fa;
+  QGM_CUDA(cudaFuncGetAttributes(&fa, kernel));
+  M.attrs[{dev, kernel}] = fa;
+  return fa;
 }
 
 inline unsigned bit_width_u64(uint64_t x) {

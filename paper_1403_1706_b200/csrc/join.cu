@@ -560,7 +560,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
 }  // namespace
 
 uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Ref& ref, int strands, int mode,
-                     unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats) {
+                     unsigned read_bits, DBuf<uint64_t>& keys, uint64_t* fstats,
+                     unsigned long long* dev_counter) {
   if (read_bits + 1 + ref.diag_bits > 64) throw InputError("read batch too large for the 64-bit candidate key");
   if (uint64_t(reads.stride) + 64 > ref.gap) throw InputError("reads longer than the reference padding supports");
   prepare_ref_index(c, ref, rp.q);
@@ -585,9 +586,17 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   a.uniform = rp.flags.p + 1;
   a.strands = strands;
   a.diag_bits = ref.diag_bits;
-  DBuf<unsigned long long> counter(c, 3);
-  a.counter = counter.p;
-  a.stats = counter.p + 1;
+  // {candidates, lookups that hit, occurrences visited}: the caller's
+  // buffer in the asynchronous form (read back with the batch's other
+  // counts), else this call's, read back below
+  DBuf<unsigned long long> own_counter;
+  unsigned long long* counter = dev_counter;
+  if (!counter) {
+    own_counter.alloc(c, 3);
+    counter = own_counter.p;
+  }
+  a.counter = counter;
+  a.stats = counter + 1;
   // sized for the larger of 16 per read and the last batch's count on this
   // context (+1/8), so a steady stream of similar batches never re-runs
   if (keys.n == 0)
@@ -617,11 +626,12 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   const int stages = use_ws ? 2 : 1;
   // staging capacity: what is left of the SM's shared memory share of one
   // CTA after the static arrays, I words and group starts (per stage)
-  cudaFuncAttributes fa;
-  QGM_CUDA(cudaFuncGetAttributes(&fa, kfn));
-  int dev = 0, smem_sm = 0;
-  QGM_CUDA(cudaGetDevice(&dev));
-  QGM_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  const cudaFuncAttributes fa = func_attributes(kfn);
+  static const int smem_sm = [] {
+    int v = 0;
+    QGM_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, current_device()));
+    return v;
+  }();
   // I words + u16 starts, padded to 16 bytes (the S'/O/item slices that follow are bulk-copy targets)
   const size_t fixed = (size_t(a.words) * 4 + (size_t((a.words + 1) / 2 + 3) & ~size_t(3)) * 4 + 15) & ~size_t(15);
   int64_t room = (int64_t(smem_sm) / per_sm - 1024 - int64_t(fa.sharedSizeBytes)) / stages - int64_t(fixed);
@@ -643,10 +653,10 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   a.cap = can_stage ? uint32_t(room / 8) & ~3u : 0u;
   uint32_t stage_words = uint32_t(fixed / 4) + 2 * a.cap + 2 * icap;
   const size_t smem = size_t(stages) * stage_words * 4;
-  QGM_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  ensure_dynamic_smem(reinterpret_cast<const void*>(kfn), size_t(smem));
   const unsigned grid = std::min<unsigned>(a.n_sub, resident_grid(kfn, threads, smem));
   for (int attempt = 0; attempt < 2; ++attempt) {
-    counter.zero();
+    QGM_CUDA(cudaMemsetAsync(counter, 0, 3 * sizeof(unsigned long long), c.stream));
     a.out = keys.p;
     a.cap_out = keys.n;
     if (rp.V > 0) {
@@ -655,11 +665,12 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
       QGM_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(threads), args, smem, c.stream));
       ++c.launches;
     }
+    if (dev_counter) return 0;  // asynchronous: the caller reads the counts (and checks keys.n) later
     // the one host round trip of the filtration: candidate count, join
     // statistics and the partition's flags (exact V, length check)
     unsigned long long h[3] = {0, 0, 0};
     uint32_t fl[4] = {0, 0, 0, 0};
-    QGM_CUDA(cudaMemcpyAsync(h, counter.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    QGM_CUDA(cudaMemcpyAsync(h, counter, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     QGM_CUDA(cudaMemcpyAsync(fl, rp.flags.p, sizeof(fl), cudaMemcpyDeviceToHost, c.stream));
     QGM_CUDA(cudaStreamSynchronize(c.stream));
     if (fl[2]) throw InputError("read longer than the stride");

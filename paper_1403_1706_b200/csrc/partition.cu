@@ -462,7 +462,7 @@ static void p0_p1(Ctx& c, const ItemGen<Q>& gen, const Reads& reads, unsigned q,
     const uint32_t per_cta = uint32_t(ceil_div(ceil_div(gen.n_runs, uint64_t(kSMs)), kHistThreads) * kHistThreads);
     const size_t hsmem = size_t((keys + 1) / 2) * 4;
     auto kern = k_part_hist16<Q, R>;
-    QGM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsmem)));
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), size_t(hsmem));
     KernelScope ks(c, "k_part_hist");
     QGM_KERNEL(c, kern, unsigned(ceil_div(gen.n_runs, per_cta)), kHistThreads, hsmem, gen, per_cta,
                2 * q - key_bits, keys, h2.p);
@@ -477,7 +477,7 @@ static void p0_p1(Ctx& c, const ItemGen<Q>& gen, const Reads& reads, unsigned q,
   p1.alloc(c, uint64_t(V) + 2);  // +2: P2 bulk-copies whole 16-byte pairs
   const size_t smem = kChunk * (sizeof(uint64_t) + sizeof(uint8_t));
   auto p1kern = k_part_scatter<Q, R>;
-  QGM_CUDA(cudaFuncSetAttribute(p1kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  ensure_dynamic_smem(reinterpret_cast<const void*>(p1kern), size_t(smem));
   const uint32_t chunk_runs = kChunk / R;
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(gen.n_runs, chunk_runs), uint64_t(kSMs) * kPartMinBlocks));
   KernelScope ks(c, "k_part_scatter");
@@ -561,7 +561,7 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   h2.zero();  // per-key cursors
   out.pairs.alloc(c, V + 2);  // +2: the join bulk-copies whole 16-byte pairs of items
   const size_t smem2 = kP2Chunk * (2 * sizeof(uint64_t) + sizeof(uint16_t));
-  QGM_CUDA(cudaFuncSetAttribute(k_refine_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+  ensure_dynamic_smem(reinterpret_cast<const void*>(k_refine_scatter), size_t(smem2));
   const uint32_t n_chunks2 = uint32_t(ceil_div(V, kP2Chunk));
   DBuf<uint4> chunk_info(c, n_chunks2);
   QGM_KERNEL(c, k_chunk_info, unsigned(ceil_div(n_chunks2, 256)), 256, 0, p1.p, out.flags.p, out.boff.p, rf, sub,
