@@ -478,6 +478,8 @@ def run_gpu(args):
     stimes = ctx.stage_times(reset=True, host=True)
     ctx.profile(False)
     post = postprocess_pass(ctx, lib, C, qgm, R, d_words[0], d_len[0], batches[0][1].size, rlen, params, band)
+    ibuild = index_build_pass(ctx, lib, C, qgm, stream, d_words[0], d_len[0], batches[0][1].size, rlen, q,
+                              load_peaks()[0])
 
     # ---------------- parity sample: rank 0's first batch, downloaded
     first = map_batch(0, keep=True) if rank == 0 else None
@@ -564,6 +566,7 @@ def run_gpu(args):
         "inputs_s": round(inputs_s, 2),
         "host_binding": {"cores": numa_cores, "rule": "NVML CPU affinity of the rank's GPU"},
         "postprocess": post,
+        "index_build": ibuild,
     }
     if world > 1:
         line["backend"] = backend
@@ -752,6 +755,40 @@ def postprocess_pass(ctx, lib, C, qgm, R, d_words, d_len, n_reads, rlen, params,
     finally:
         if h:
             lib.qgm_hits_destroy(h)
+        lib.qgm_reads_destroy(rd)
+
+
+def index_build_pass(ctx, lib, C, qgm, stream, d_words, d_len, n_reads, rlen, q, peak):
+    """build_qgroup_index<u32> (qgroup_index.hpp:124-180) of one batch through
+    the API (qgm_index_build: the full four-array read index of Alg. 1, not
+    used by the map path), CUDA events on the library stream, median of 3 after
+    a warm-up; algorithmic bytes N*n/4 (2-bit reads) + 8*Gq (I and S) +
+    4*(D+1) (S') + 4*V (O)."""
+    import torch
+    rd = C.c_void_p()
+    ctx._check(lib.qgm_reads_from_device(ctx.h, C.c_void_p(d_words.data_ptr()), C.c_void_p(d_len.data_ptr()),
+                                         n_reads, rlen, C.byref(rd)))
+    try:
+        times, info = [], None
+        for it in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            h = C.c_void_p()
+            ctx._check(lib.qgm_index_build(ctx.h, rd, q, 32, 0, C.byref(h)))
+            e1.record(stream)
+            e1.synchronize()
+            info = qgm.IndexInfo()
+            ctx._check(lib.qgm_index_info_get(h, C.byref(info)))
+            lib.qgm_index_destroy(h)
+            if it:
+                times.append(e0.elapsed_time(e1))
+        ms = statistics.median(times)
+        ab = n_reads * rlen / 4 + 8 * info.group_count + 4 * (info.distinct + 1) + 4 * info.occurrences
+        return {"api": "qgm_index_build (build_qgroup_index<uint32_t>, not sampled)", "q": q, "ms": round(ms, 4),
+                "groups": info.group_count, "distinct": info.distinct, "occurrences": info.occurrences,
+                "algorithmic_bytes": int(ab), "achieved_gbs": round(ab / (ms / 1e3) / 1e9, 1),
+                "frac": round(ab / (ms / 1e3) / 1e9 / peak, 4)}
+    finally:
         lib.qgm_reads_destroy(rd)
 
 

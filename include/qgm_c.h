@@ -47,6 +47,9 @@ extern "C" {
 #define QGM_FILTER_FULL 0      /* Alg. 2 multiset */
 #define QGM_FILTER_RUN_START 1 /* leftmost q-gram of each run per diagonal (same set) */
 #define QGM_FILTER_JOIN 2      /* flag: bucket-ordered join with the reference q-group index */
+#define QGM_FILTER_STREAM 4    /* flag: stream every reference position against the read index */
+/* Neither flag: the join when the reference is below 2^32 padded bases (the
+ * production filtration), else the streaming kernel. */
 
 typedef struct qgm_ctx qgm_ctx;
 typedef struct qgm_reads qgm_reads;

@@ -31,11 +31,15 @@ struct Hit {
 // full / run_start: stream the reference against the read index (filter.cu);
 // *_join: bucket-ordered join of the read q-grams with the reference q-group
 // indexes (join.cu, the path qgm_map uses). All four give the same candidate set.
+// full / run_start: the join below 2^32 padded reference bases, else the
+// streaming kernel; *_join / *_stream force either (same candidates).
 enum class FilterMode {
   full = QGM_FILTER_FULL,
   run_start = QGM_FILTER_RUN_START,
   full_join = QGM_FILTER_FULL | QGM_FILTER_JOIN,
-  run_start_join = QGM_FILTER_RUN_START | QGM_FILTER_JOIN
+  run_start_join = QGM_FILTER_RUN_START | QGM_FILTER_JOIN,
+  full_stream = QGM_FILTER_FULL | QGM_FILTER_STREAM,
+  run_start_stream = QGM_FILTER_RUN_START | QGM_FILTER_STREAM
 };
 
 // filter_reference over every unmasked reference position of

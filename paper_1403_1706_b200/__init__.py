@@ -39,6 +39,7 @@ MODE_ALL = 1
 FILTER_FULL = 0
 FILTER_RUN_START = 1
 FILTER_JOIN = 2  # flag: bucket-ordered join with the reference q-group index (join.cu)
+FILTER_STREAM = 4  # flag: streaming kernel (filter.cu); neither flag = the join below 2^32 padded bases
 STAGES = ("reads", "index", "filter", "sort_unique", "validate", "strata", "d2h", "other")
 
 CANDIDATE_DTYPE = np.dtype([("diagonal", "<i8"), ("read_id", "<u4"), ("chrom", "<u4"),

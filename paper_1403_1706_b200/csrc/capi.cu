@@ -890,8 +890,11 @@ int qgm_filter(qgm_ctx* ctx, const qgm_index* idx, const qgm_reads* reads, const
   int rc = guard(ctx, [&] {
     activate(ctx);
     require(strands >= 1 && strands <= 3, "strands must be 1, 2 or 3");
-    const int base_mode = mode & ~QGM_FILTER_JOIN;
+    const int base_mode = mode & ~(QGM_FILTER_JOIN | QGM_FILTER_STREAM);
     require(base_mode == QGM_FILTER_FULL || base_mode == QGM_FILTER_RUN_START, "unknown filter mode");
+    require(!((mode & QGM_FILTER_JOIN) && (mode & QGM_FILTER_STREAM)), "QGM_FILTER_JOIN and QGM_FILTER_STREAM exclude each other");
+    const bool join = (mode & QGM_FILTER_JOIN) ||
+                      (!(mode & QGM_FILTER_STREAM) && ref->r.padded_total < (uint64_t(1) << 32));
     qgm::Ctx& c = ctx->c;
     auto& C = cd->c;
     C.read_bits = qgm::read_bits_for(reads->r.n);
@@ -899,7 +902,7 @@ int qgm_filter(qgm_ctx* ctx, const qgm_index* idx, const qgm_reads* reads, const
     C.cbp = ref->r.cbp;
     if (idx->i.stride != reads->r.stride || idx->i.n_reads != reads->r.n)
       throw qgm::InputError("index was built over a different read buffer");
-    if (mode & QGM_FILTER_JOIN) {
+    if (join) {
       qgm::Partitioned rbk;
       qgm::partition_reads(c, reads->r, idx->i.q, rbk);
       qgm::StageScope s(c, qgm::kStageFilter);

@@ -69,11 +69,14 @@ void filter_vs_oracle(std::uint64_t seed, unsigned q, bool sampled, bool mask, i
       auto ors = qgm_oracle::filter(in.oref, in.oreads, ox, q, strands, true, 4);
       std::sort(ors.begin(), ors.end());
       CHECK(tu::to_oracle(filter_reference(ref, ix, FilterMode::run_start, strands)) == ors);
-      // the bucket-ordered join (join.cu) emits exactly the same multisets
+      // the default modes run the bucket-ordered join (join.cu); the forced
+      // join and the streaming kernel (filter.cu) emit exactly the same multisets
       auto wfull = qgm_oracle::filter(in.oref, in.oreads, ox, q, strands, false, 4);
       std::sort(wfull.begin(), wfull.end());
       CHECK(tu::to_oracle(filter_reference(ref, ix, FilterMode::full_join, strands)) == wfull);
       CHECK(tu::to_oracle(filter_reference(ref, ix, FilterMode::run_start_join, strands)) == ors);
+      CHECK(tu::to_oracle(filter_reference(ref, ix, FilterMode::full_stream, strands)) == wfull);
+      CHECK(tu::to_oracle(filter_reference(ref, ix, FilterMode::run_start_stream, strands)) == ors);
     }
   }
 }

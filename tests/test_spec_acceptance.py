@@ -65,7 +65,8 @@ def test_criterion3_pigeonhole_true_candidate_for_every_read(ctx):
     R = qgm.Reference.from_codes(ctx, ref, cb)
     reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
     idx = qgm.Index.build(ctx, reads, 16)
-    for mode in (qgm.FILTER_RUN_START, qgm.FILTER_RUN_START | qgm.FILTER_JOIN):
+    for mode in (qgm.FILTER_RUN_START, qgm.FILTER_RUN_START | qgm.FILTER_JOIN,
+                 qgm.FILTER_RUN_START | qgm.FILTER_STREAM):
         cands = ctx.filter(idx, reads, R, mode=mode, unique=True)
         key = set(zip(cands["read_id"].tolist(), cands["strand"].tolist(), cands["diagonal"].tolist()))
         missing = [r for r in range(lengths.size) if (r, int(strand[r]), int(pos[r])) not in key]

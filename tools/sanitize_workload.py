@@ -92,7 +92,7 @@ def main():
     small_c, small_l = codes[: 2000 * 100], lengths[:2000]
     reads = qgm.Reads.from_codes(ctx, small_c, small_l, 100)
     idx = qgm.Index.build(ctx, reads, 12)
-    cands = ctx.filter(idx, reads, R, mode=qgm.FILTER_RUN_START, unique=True)
+    cands = ctx.filter(idx, reads, R, mode=qgm.FILTER_RUN_START | qgm.FILTER_STREAM, unique=True)
     val = ctx.validate(reads, R, cands[:5000])
     print(f"api: {idx.info['occurrences']} occurrences, {cands.size} candidates, {int(val['kept'].sum())} kept",
           flush=True)
