@@ -836,14 +836,34 @@ def cpu_map(cfg, ref, cb, codes, lengths, threads, samples=1):
     return kind, best[0], hits, best[1]
 
 
+def run_gen_inputs(args):
+    """--gen-inputs PATH (child process): the config's reference and the
+    first `sample` reads of block 0, written to PATH (npz) -- so the CPU
+    processes (reference arm, CPU leg) never map the repo's synthetic-data
+    library, only numpy arrays and the reference / oracle code."""
+    import paper_1403_1706_b200 as qgm
+    cfg = CONFIGS[args.config]
+    ref, cb = make_reference(qgm, cfg)
+    codes, lengths = make_block(qgm, cfg, ref, cb, 0, args.sample or None)
+    np.savez(args.gen_inputs, ref=ref, cb=cb, codes=codes, lengths=lengths)
+
+
+def isolated_inputs(config, sample):
+    """(ref, chrom_begin, codes, lengths) generated in a child process."""
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "inputs.npz")
+        subprocess.run([sys.executable, os.path.abspath(__file__), "--config", config, "--gen-inputs", path,
+                        "--sample", str(sample)], check=True)
+        z = np.load(path)
+        return z["ref"], z["cb"], z["codes"], z["lengths"]
+
+
 def run_cpu_leg(args):
     """--cpu-leg (child of the GPU arm): the CPU path on the first `sample`
     reads of block 0 of rank 0, timed, compared with the GPU hits."""
-    import paper_1403_1706_b200 as qgm
     from paper_1403_1706_b200 import sharding
     cfg = CONFIGS[args.config]
-    ref, cb = make_reference(qgm, cfg)
-    codes, lengths = make_block(qgm, cfg, ref, cb, 0, args.sample)
+    ref, cb, codes, lengths = isolated_inputs(args.config, args.sample)
     threads = os.cpu_count() or 1
     kind, sec, hits, st = cpu_map(cfg, ref, cb, codes, lengths, threads, samples=args.cpu_samples)
     res = {"cpu_baseline": {
@@ -869,12 +889,10 @@ def run_reference(args):
     only), each step a bounded sample of the config's first batch."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
-    import paper_1403_1706_b200 as qgm
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", args.gpus))
-    ref, cb = make_reference(qgm, cfg)
     sample = min(cfg["cpu_sample"], cfg["batch"])
-    codes, lengths = make_block(qgm, cfg, ref, cb, 0, sample)
+    ref, cb, codes, lengths = isolated_inputs(args.config, sample)
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
         cpu_map(cfg, ref, cb, codes, lengths, threads)
@@ -932,7 +950,10 @@ def main():
     ap.add_argument("--sample", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--gpu-hits", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--leg-out", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--gen-inputs", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gen_inputs:
+        return run_gen_inputs(args)
     if args.cpu_leg:
         return run_cpu_leg(args)
     if args.check is None:
