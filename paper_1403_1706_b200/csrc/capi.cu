@@ -677,10 +677,10 @@ static int reads_common(qgm_ctx* ctx, const uint64_t* w, const uint32_t* len, ui
     r.stride = stride;
     r.W = (stride + 31) / 32;
     const uint64_t nw = uint64_t(n_reads) * r.W;
-    r.words.alloc(c, nw + 1);
+    r.words.alloc(c, nw + 2);  // 2 guard words: the partition bulk-copies whole 16-byte pairs
     r.lengths.alloc(c, std::max<uint32_t>(n_reads, 1));
     if (nw) QGM_CUDA(cudaMemcpyAsync(r.words.p, w, nw * 8, kind, c.stream));
-    QGM_CUDA(cudaMemsetAsync(r.words.p + nw, 0, 8, c.stream));
+    QGM_CUDA(cudaMemsetAsync(r.words.p + nw, 0, 16, c.stream));
     if (n_reads) QGM_CUDA(cudaMemcpyAsync(r.lengths.p, len, uint64_t(n_reads) * 4, kind, c.stream));
     qgm::finish_reads(c, r);
   });
@@ -1193,7 +1193,7 @@ int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, c
       qgm::check_reads_shape(b.n_reads, b.stride);
       require(b.n_reads == 0 || b.reads2bit, "null read buffers");
       require(b.layout == QGM_READS_PADDED || b.layout == QGM_READS_DENSE, "unknown read layout");
-      max_w = std::max<uint64_t>(max_w, uint64_t(b.n_reads) * ((b.stride + 31) / 32) + 1);
+      max_w = std::max<uint64_t>(max_w, uint64_t(b.n_reads) * ((b.stride + 31) / 32) + 2);
       max_n = std::max<uint64_t>(max_n, b.n_reads);
       if (b.layout == QGM_READS_DENSE) max_d = std::max<uint64_t>(max_d, qgm::ceil_div(uint64_t(b.n_reads) * b.stride, 32) + 1);
     }
@@ -1213,7 +1213,7 @@ int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, c
       } else {
         const uint64_t nw = uint64_t(b.n_reads) * ((b.stride + 31) / 32);
         if (nw) QGM_CUDA(cudaMemcpyAsync(s.words.p, b.reads2bit, nw * 8, cudaMemcpyHostToDevice, cs));
-        QGM_CUDA(cudaMemsetAsync(s.words.p + nw, 0, 8, cs));
+        QGM_CUDA(cudaMemsetAsync(s.words.p + nw, 0, 16, cs));
       }
       if (b.n_reads && b.lengths)
         QGM_CUDA(cudaMemcpyAsync(s.lens.p, b.lengths, uint64_t(b.n_reads) * 4, cudaMemcpyHostToDevice, cs));
@@ -1244,7 +1244,7 @@ int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, c
                                                        qgm::kSMs * 16));
         if (b.layout == QGM_READS_DENSE && r.n) {
           QGM_KERNEL(c, qgm::k_unpack_dense, g, 256, 0, s.dense.p, r.n, r.stride, r.W, s.words.p);
-          QGM_CUDA(cudaMemsetAsync(s.words.p + uint64_t(r.n) * r.W, 0, 8, c.stream));
+          QGM_CUDA(cudaMemsetAsync(s.words.p + uint64_t(r.n) * r.W, 0, 16, c.stream));
         }
         if (!b.lengths && r.n) QGM_KERNEL(c, qgm::k_fill_u32, g, 256, 0, s.lens.p, uint64_t(r.n), r.stride);
       }

@@ -93,8 +93,36 @@ struct ItemGen {
     run = min(run, n_runs - 1);  // runs past the end load something valid and are dropped
     u.r = by_rpr.div(run);
     u.o0 = (run - u.r * rpr) * R;
-    u.n = __ldg(lengths + u.r);
+    // a read longer than the stride is an input error (reported from the
+    // batch flags); clamped, every pass counts the same slots and no item
+    // exceeds the slot bound the buffers are sized by
+    u.n = min(__ldg(lengths + u.r), stride);
     u.A = window(u.r, u.o0);
+  }
+  // Staged read words: the 16-byte-aligned word range [a0, a0 + nw) under
+  // runs [c0, c1), up to and including the word after the range's last read
+  // (the next read's first word or a guard word).
+  __device__ __forceinline__ void word_range(uint32_t c0, uint32_t c1, uint32_t& a0, uint32_t& nw) const {
+    const uint32_t rlo = by_rpr.div(c0), rhi = by_rpr.div(c1 - 1);
+    a0 = (rlo * W) & ~1u;
+    nw = (((rhi + 1) * W + 2) & ~1u) - a0;
+  }
+  // fetch_run from words staged in shared memory (sw holds words from a0);
+  // n_uni: every read has this length (0: load it)
+  template <int R>
+  __device__ __forceinline__ void fetch_run_staged(uint32_t run, Run& u, const uint64_t* sw, uint32_t a0,
+                                                   uint32_t n_uni) const {
+    run = min(run, n_runs - 1);
+    u.r = by_rpr.div(run);
+    u.o0 = (run - u.r * rpr) * R;
+    u.n = n_uni ? n_uni : min(__ldg(lengths + u.r), stride);
+    const uint64_t* w = sw + (u.r * W - a0);
+    const uint32_t b = u.o0 + 31;
+    const int k = int(b >> 5) - 1;
+    const unsigned sh = 2 * (b & 31);
+    const uint64_t w0 = k >= 0 ? w[k] : 0ull;
+    const uint64_t w1 = w[k + 1];
+    u.A = (w0 << sh) | ((w1 >> 1) >> (63 - sh));
   }
   // slot j of a fetched run: canonical code g, own code f, meta, position.
   // RC = revcomp32(u.A), computed once per run by the caller.
@@ -196,17 +224,23 @@ __global__ void k_bin_offsets(const uint32_t* __restrict__ soff, uint32_t nbins,
 // P1, software-pipelined over the CTA's chunks: while chunk i's bin runs are
 // being reserved (one global cursor atomic per bin, the round trip that
 // dominated the stalls of the unpipelined loop) and written out, the items of
-// chunk i+1 are generated and counted, and the read words of chunk i+2 are
-// already in flight.
+// chunk i+1 are generated and counted, and the read words of chunk i+2 (a
+// contiguous range of reads) are on their way into shared memory by one bulk
+// copy (C2: 0.407 -> 0.403 ms; staging P0's words the same way cost more in
+// per-step barriers than it saved, 0.126 -> 0.146 ms).
 template <int Q, int R>
 __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(ItemGen<Q> gen, unsigned shift,
                                                                   const uint32_t* __restrict__ boff,
                                                                   uint32_t* __restrict__ cursor,
-                                                                  uint64_t* __restrict__ out) {
-  extern __shared__ uint64_t stage[];  // kChunk items, bin-sorted, then kChunk u8 bins
+                                                                  uint64_t* __restrict__ out, uint32_t sw_words,
+                                                                  const uint32_t* __restrict__ lens) {
+  // kChunk items, bin-sorted | kChunk u8 bins | 2 x sw_words staged read words
+  extern __shared__ __align__(16) uint64_t stage[];
   uint8_t* sbin = reinterpret_cast<uint8_t*>(stage + kChunk);
+  uint64_t* swb = reinterpret_cast<uint64_t*>(sbin + kChunk);
   __shared__ uint32_t cnt[2][kBins], lofs[kBins], delta[kBins];
   __shared__ uint32_t ws[33];
+  __shared__ __align__(8) uint64_t wbar[2];
   const uint32_t lmask = shift ? (1u << shift) - 1u : 0u;
   constexpr uint32_t kRuns = kPer / R;  // runs per thread per chunk
   constexpr uint32_t kChunkRuns = kRuns * kPartThreads;
@@ -215,16 +249,40 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
   if (ch >= n_chunks) return;  // CTA-uniform
   const uint32_t b = threadIdx.x;  // the bin this thread scans / reserves (b < kBins)
   for (uint32_t i = b; i < 2 * kBins; i += kPartThreads) (&cnt[0][0])[i] = 0;
+  // every read of the batch as long as the stride: no per-run length load
+  const uint32_t n_uni = ~__ldg(lens + 1) == gen.stride ? gen.stride : 0u;
+  // the read words of the CTA's i-th chunk arrive by one bulk copy into
+  // buffer i & 1, issued two chunks ahead
+  auto issue = [&](uint32_t i, uint32_t c) {  // thread 0
+    const uint32_t c0 = c * kChunkRuns, c1 = min(gen.n_runs, c0 + kChunkRuns);
+    uint32_t a0, nw;
+    gen.word_range(c0, c1, a0, nw);
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&wbar[i & 1], nw * 8u);
+    bulk_g2s(swb + (i & 1) * sw_words, gen.words + a0, nw * 8u, &wbar[i & 1]);
+  };
+  if (b == 0) {
+    mbar_init(&wbar[0], 1);
+    mbar_init(&wbar[1], 1);
+    issue(0, ch);
+    if (ch + gridDim.x < n_chunks) issue(1, ch + gridDim.x);
+  }
   Run u[kRuns];
-  auto fetch = [&](uint32_t c) {
+  auto fetch = [&](uint32_t i, uint32_t c) {  // the runs of the CTA's i-th chunk (chunk c)
+    mbar_wait(&wbar[i & 1], (i >> 1) & 1u);
+    const uint32_t c0 = c * kChunkRuns;
+    uint32_t a0, nw;
+    gen.word_range(c0, min(gen.n_runs, c0 + kChunkRuns), a0, nw);
 #pragma unroll
-    for (uint32_t h = 0; h < kRuns; ++h) gen.template fetch_run<R>(c * kChunkRuns + h * kPartThreads + b, u[h]);
+    for (uint32_t h = 0; h < kRuns; ++h)
+      gen.template fetch_run_staged<R>(c0 + h * kPartThreads + b, u[h], swb + (i & 1) * sw_words, a0, n_uni);
   };
   uint64_t item[kPer];
   uint32_t bin[kPer];  // bin | rank among the chunk's items of that bin << 8; ~0u = no q-gram at this slot
   // items of chunk c from the fetched runs (counted into cnt[par]); then the
   // runs of the CTA's next chunk are fetched
-  auto generate = [&](uint32_t c, uint32_t par) {
+  auto generate = [&](uint32_t i, uint32_t c, uint32_t par) {
+    fetch(i, c);
 #pragma unroll
     for (uint32_t h = 0; h < kRuns; ++h) {
       const uint32_t tr = c * kChunkRuns + h * kPartThreads + b;
@@ -239,7 +297,6 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
         bin[e] = ok ? (g >> shift) | (atomicAdd(&cnt[par][g >> shift], 1u) << 8) : ~0u;
       }
     }
-    if (c + gridDim.x < n_chunks) fetch(c + gridDim.x);
   };
   // local exclusive offsets of cnt[par]; the chunk's run in every bin reserved
   // (the reservation's value is only needed at the write-out); cnt[par] reset
@@ -261,21 +318,21 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
         sbin[slot] = uint8_t(bb);
       }
   };
-  fetch(ch);
-  __syncthreads();  // counters zeroed
-  uint32_t par = 0, g = 0, total = 0;
-  generate(ch, par);
+  __syncthreads();  // counters zeroed, barriers initialised
+  uint32_t par = 0, g = 0, total = 0, i = 0;
+  generate(0, ch, par);
   __syncthreads();
   scan(par, g, total);
   __syncthreads();
   place();
-  for (;;) {
+  for (;; ++i) {
     const uint32_t nxt = ch + gridDim.x;
     const bool more = nxt < n_chunks;  // CTA-uniform
-    if (more) generate(nxt, par ^ 1u);  // overlaps the reservation round trip
+    if (more) generate(i + 1, nxt, par ^ 1u);  // overlaps the reservation round trip
     if (b < kBins) delta[b] = g - lofs[b];
-    __syncthreads();  // staged chunk and its destinations visible
-    for (uint32_t i = b; i < total; i += kPartThreads) out[delta[sbin[i]] + i] = stage[i];
+    __syncthreads();  // staged chunk and its destinations visible; chunk i's words no longer read
+    if (b == 0 && nxt + gridDim.x < n_chunks) issue(i + 2, nxt + gridDim.x);
+    for (uint32_t x = b; x < total; x += kPartThreads) out[delta[sbin[x]] + x] = stage[x];
     if (!more) break;
     par ^= 1u;
     scan(par, g, total);  // its first barrier also ends the write-out
@@ -475,13 +532,16 @@ static void p0_p1(Ctx& c, const ItemGen<Q>& gen, const Reads& reads, unsigned q,
   DBuf<uint32_t> hist(c, kBins + 1);  // per-bin cursors of P1
   hist.zero();
   p1.alloc(c, uint64_t(V) + 2);  // +2: P2 bulk-copies whole 16-byte pairs
-  const size_t smem = kChunk * (sizeof(uint64_t) + sizeof(uint8_t));
+  const uint32_t chunk_runs = kChunk / R;
+  // staged words per chunk: the reads under chunk_runs runs (+2 partial) and
+  // the following word, rounded to 16-byte pairs
+  const uint32_t sw_words = ((chunk_runs / gen.rpr + 2) * reads.W + 4 + 1) & ~1u;
+  const size_t smem = kChunk * (sizeof(uint64_t) + sizeof(uint8_t)) + size_t(2) * sw_words * sizeof(uint64_t);
   auto p1kern = k_part_scatter<Q, R>;
   ensure_dynamic_smem(reinterpret_cast<const void*>(p1kern), size_t(smem));
-  const uint32_t chunk_runs = kChunk / R;
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(gen.n_runs, chunk_runs), uint64_t(kSMs) * kPartMinBlocks));
   KernelScope ks(c, "k_part_scatter");
-  QGM_KERNEL(c, p1kern, grid, kPartThreads, smem, gen, shift, out.boff.p, hist.p, p1.p);
+  QGM_KERNEL(c, p1kern, grid, kPartThreads, smem, gen, shift, out.boff.p, hist.p, p1.p, sw_words, reads.lens.p);
 }
 
 template <int Q>
