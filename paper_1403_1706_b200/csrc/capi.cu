@@ -365,12 +365,11 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   const int strands = P.strands ? int(P.strands) : 3;
   if (P.group_width && P.group_width != 32 && P.group_width != 64) throw InputError("group width must be 32 or 64");
   if (ref.padded_total < (uint64_t(1) << 32)) {
-    const uint64_t cap = std::max<uint64_t>(std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16),
-                                            c.last_raw_candidates + c.last_raw_candidates / 8);
-    static const bool async_off = [] {
-      const char* e = std::getenv("QGM_MAP_ASYNC");  // A/B knob: 0 = always the round-trip path
-      return e && e[0] == '0';
-    }();
+    uint64_t cap = std::max<uint64_t>(std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16),
+                                      c.last_raw_candidates + c.last_raw_candidates / 8);
+    if (const char* e = std::getenv("QGM_MAP_ASYNC_CAP")) cap = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));  // tests
+    const char* ae = std::getenv("QGM_MAP_ASYNC");  // A/B and test knob: 0 = always the round-trip path
+    const bool async_off = ae && ae[0] == '0';
     if (!async_off && cap <= dedup_direct_max()) {
       HitsObj out;
       if (map_reads_async(c, reads, ref, P, strands, read_bits_for(reads.n), cap, after_filter, out)) return out;

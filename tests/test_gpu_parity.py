@@ -341,6 +341,31 @@ def test_validation_park_overflow_finishes_in_phase_one(ctx, oracle, monkeypatch
     assert _same(got, want), (got.size, want.size)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+def test_map_without_round_trips_equals_the_round_trip_path(ctx, oracle, monkeypatch, mode):
+    """The batch mapped without a host round trip before its end (the default
+    below 10M candidates), with the round-trip path forced (QGM_MAP_ASYNC=0),
+    and with a candidate capacity far below its count (QGM_MAP_ASYNC_CAP=1000:
+    the truncated first attempt is detected at the end and the batch mapped
+    again): identical hits and statistics, equal to the oracle."""
+    import paper_1403_1706_b200 as qgm
+    ref, cb, codes, lengths, tp, ts = _c1(qgm, n_reads=5000, L=500_000, seed=11)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    want, ost = oracle.map(ref, cb, codes, 100, lengths, q=12, mode=mode)
+    runs = []
+    for env in ({}, {"QGM_MAP_ASYNC": "0"}, {"QGM_MAP_ASYNC_CAP": "1000"}):
+        with monkeypatch.context() as m:
+            for k, v in env.items():
+                m.setenv(k, v)
+            got, st = ctx.map(reads, R, q=12, mode=mode)
+        assert _same(got, want), (env, got.size, want.size)
+        _validated_agrees(st, ost, mode, env)
+        runs.append({k: v for k, v in st.items() if k != "stage_seconds"})
+    assert runs[0] == runs[1] == runs[2], runs
+    assert runs[0]["raw_candidates"] > 1000
+
+
 def test_hit_rank_and_mapq(ctx):
     """hit_rank from the device against a direct count over the output, the
     mapping quality from it, and the hit-rank separation
