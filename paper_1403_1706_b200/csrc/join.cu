@@ -155,6 +155,7 @@ __device__ __forceinline__ void drain(const JoinArgs& a, WarpLists& L, uint32_t 
 }
 
 __device__ __forceinline__ void flush_keys(const JoinArgs& a, WarpLists& L) {
+  __syncwarp();  // the last staged pairs visible to the whole warp
   while (L.staged) drain(a, L, min(L.staged, kDrain));
 }
 
@@ -170,14 +171,17 @@ __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI
   const unsigned lane = lane_id();
   auto stage = [&](bool emit, uint64_t it, uint32_t xp) {  // all lanes call it
     const unsigned m = __ballot_sync(kFull, emit);
+    if (!m) return;  // warp-uniform: ~90% of the pairs emit nothing
     if (emit) {
       const uint32_t e = L.staged + __popc(m & lanemask_lt());
       L.eit[e] = it;
       L.exp[e] = xp;
     }
     L.staged += __popc(m);
-    __syncwarp();
-    if (L.staged >= kDrain) drain(a, L, kDrain);
+    if (L.staged >= kDrain) {  // the staged slots become visible to the warp before they are read
+      __syncwarp();
+      drain(a, L, kDrain);
+    }
   };
   uint64_t pn[kItems];  // next step's items, loaded one step ahead
 #pragma unroll
