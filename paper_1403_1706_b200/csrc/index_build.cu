@@ -557,6 +557,14 @@ void prepare_ref_index(Ctx& c, const Ref& ref, unsigned q) {
   uint64_t n_pal = 0;
   bucket_ref(c, ref, q, packed, B, &n_pal);
   index_from_buckets(c, B, false, ref.qidx.can, packed ? nullptr : &ref.qidx.extra);
+  if (packed && ref.qidx.can.distinct) {
+    // sort every interval's packed words: (extra bits, position) order groups
+    // the occurrences by (strand flag, compare base) for the join's
+    // suppression skip (once per reference and q)
+    QGM_KERNEL(c, k_sort_intervals, unsigned(std::min<uint64_t>(ceil_div(ref.qidx.can.distinct, 128), kSMs * 16)),
+               128, 0, ref.qidx.can.S1.p, ref.qidx.can.distinct, ref.qidx.can.O.p);
+    ref.qidx.ex_sorted = true;
+  }
   ref.qidx.packed = packed;
   ref.qidx.palindromes = n_pal;
   ref.qidx.positions = B.V - n_pal;

@@ -208,6 +208,7 @@ struct Buckets {
 struct RefQIndex {
   unsigned q = 0;
   bool packed = false;
+  bool ex_sorted = false;  // packed O sorted inside every interval: grouped by (strand flag, compare base)
   uint64_t palindromes = 0;  // positions listed twice
   Index can;
   DBuf<uint8_t> extra;
