@@ -308,18 +308,18 @@ static bool map_reads_async(Ctx& c, const Reads& reads, const Ref& ref, const qg
   if (after_filter && hook_point() == 1) after_filter();
   DBuf<uint64_t> hkeys(c, cap);
   DBuf<uint32_t> hvals(c, cap);
+  DBuf<uint32_t> per_read(c, uint64_t(reads.n) + 1), kept_total(c, 1);  // hits per read, counted by validation
+  per_read.zero();
   {
     StageScope s(c, kStageValidate);
     validate_candidates(c, reads, ref, alt.p, cap, rb, P.band_width, P.pct_identity, 0, hkeys.p, hvals.p, cnt.p,
-                        nullptr, cnt.p + 1, P.q);
+                        nullptr, cnt.p + 1, P.q, per_read.p, cnt.p + 2);
   }
   if (after_filter && hook_point() == 2) after_filter();
-  DBuf<uint32_t> per_read, kept_total(c, 1);
   unsigned long long jh[3] = {0, 0, 0}, h[3] = {0, 0, 0};
   uint32_t fl[4] = {0, 0, 0, 0}, kept = 0;
   {
     StageScope s(c, kStageStrata);
-    strata_count(c, ref, hkeys.p, cnt.p, cap, reads.n, per_read, cnt.p + 2);
     stratify_unsorted_dev(c, ref, hkeys.p, hvals.p, cnt.p, cap, reads.n, int(P.mode), per_read, cnt.p + 2, out.hits,
                           kept_total.p);
     // the batch's one host round trip
@@ -443,17 +443,17 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   DBuf<uint64_t> hkeys(c, n_bound), hkeys_alt;
   DBuf<uint32_t> hvals(c, n_bound), hvals_alt;
   uint64_t n_val = 0;
+  DBuf<uint32_t> per_read(c, uint64_t(reads.n) + 1);  // hits per read, counted by validation
+  per_read.zero();
   {
     StageScope s(c, kStageValidate);
     validate_candidates(c, reads, ref, alt.p, n_raw, rb, P.band_width, P.pct_identity, 0, hkeys.p, hvals.p, cnt.p,
-                        nullptr, cnt.p + 1, P.q);
+                        nullptr, cnt.p + 1, P.q, per_read.p, cnt.p + 2);
   }
   if (after_filter && hook_at == 2) after_filter();
-  DBuf<uint32_t> per_read;
   bool big = false, speculative_done = false;
   {
     StageScope s(c, kStageStrata);
-    strata_count(c, ref, hkeys.p, cnt.p, n_bound, reads.n, per_read, cnt.p + 2);
     // The per-read counting-sort strata run on the device counts (output sized
     // for n_raw records) so that one read-back after them returns every count;
     // a batch with a read of > 32 hits (repeats) then takes the radix path.

@@ -366,17 +366,19 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
 void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint64_t* cand_keys, uint64_t n,
                          unsigned read_bits, unsigned band, unsigned pct, int mode, uint64_t* hit_keys,
                          uint32_t* hit_vals, unsigned long long* d_count, void* d_validated,
-                         const unsigned long long* d_n = nullptr, unsigned seed_q = 0);
+                         const unsigned long long* d_n = nullptr, unsigned seed_q = 0,
+                         uint32_t* per_read = nullptr, unsigned long long* d_big = nullptr);
+// per_read (nullable, n_reads + 1 zeroed u32): the map path's hits per read,
+// counted as they are emitted; *d_big += reads passing kSmallSeg hits (the
+// strata's radix path) -- counted while the hits are emitted (no pass over them).
+constexpr uint32_t kSmallSeg = 32;
 
 // strata.cu -- dedup (read, chrom, ref_start, strand) keeping min k, then
 // best-stratum / all; writes qgm_hit records, returns their count.
-// Same output from hits in any order (map path): strata_count (hits per read,
-// *d_big += reads with more than 32 hits; d_n = device hit count, n_max its
-// bound) runs before the host reads the validation's counts back, then
-// stratify_unsorted uses a per-read counting sort, or -- when big -- the
-// radix-sorted path.
-void strata_count(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const unsigned long long* d_n, uint64_t n_max,
-                  uint32_t n_reads, DBuf<uint32_t>& cnt, unsigned long long* d_big);
+// Same output from hits in any order (map path): validation counts the hits
+// per read as it emits them (per_read, *d_big += reads with more than
+// kSmallSeg hits); stratify_unsorted then uses a per-read counting sort, or --
+// when big -- the radix-sorted path.
 uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBuf<uint32_t>& hit_vals, uint64_t n,
                            uint32_t n_reads, int mode, DBuf<uint32_t>& cnt, bool big, DBuf<uint8_t>& out);
 // The per-read counting-sort path of stratify_unsorted with the hit count and

@@ -68,17 +68,6 @@ __global__ void k_emit(const uint64_t* __restrict__ keys, uint64_t n, unsigned d
 }
 
 // ------------------------------------------------------------ segmented path
-constexpr uint32_t kSmallSeg = 32;
-
-// hits per read; n_big (device) counts the reads that pass kSmallSeg hits.
-// n (nullable) = the hit count in device memory, n_max bounds it.
-__global__ void k_count_reads(const uint64_t* __restrict__ keys, const unsigned long long* __restrict__ n_dev,
-                              uint64_t n_max, unsigned rshift, uint32_t* __restrict__ cnt,
-                              unsigned long long* __restrict__ n_big) {
-  const uint64_t n = n_dev ? *n_dev : n_max;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-    if (atomicAdd(cnt + (keys[i] >> rshift), 1u) == kSmallSeg) atomicAdd(n_big, 1ull);
-}
 
 // cnt[r] counts down while hits are placed (segment filled from its end).
 // n_dev / big (nullable): device hit count, and the flag that hands the batch
@@ -250,15 +239,6 @@ void hit_ranks(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, uint32_t n_reads, 
   QGM_KERNEL(c, k_rank_keys, grid, 256, 0, reinterpret_cast<const uint4*>(hits.p), n, keys.p, idx.p);
   radix_sort(c, keys, keys_alt, &idx, &idx_alt, n, 0, int(16 + bit_width_u64(n_reads)));
   QGM_KERNEL(c, k_ranks, grid, 256, 0, keys.p, idx.p, n, rank.p);
-}
-
-void strata_count(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const unsigned long long* d_n, uint64_t n_max,
-                  uint32_t n_reads, DBuf<uint32_t>& cnt, unsigned long long* d_big) {
-  cnt.alloc(c, uint64_t(n_reads) + 1);
-  cnt.zero();
-  if (n_max == 0 || n_reads == 0) return;
-  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n_max, 256), uint64_t(kSMs) * 16));
-  QGM_KERNEL(c, k_count_reads, grid, 256, 0, hit_keys, d_n, n_max, ref.diag_bits + 1, cnt.p, d_big);
 }
 
 uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBuf<uint32_t>& hit_vals, uint64_t n,

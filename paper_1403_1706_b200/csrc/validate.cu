@@ -51,6 +51,8 @@ struct ValArgs {
   uint32_t* hit_vals;
   unsigned long long* counter;
   void* validated;
+  uint32_t* per_read;          // nullable: hits per read (map path)
+  unsigned long long* n_big;   // reads passing kSmallSeg hits
 };
 
 struct Win { uint32_t lo, hi, v; };
@@ -372,6 +374,7 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t r_
         const uint64_t gstart = __ldg(a.cbp + c) + ref_start;
         a.hit_keys[slot] = (uint64_t(r) << (a.diag_bits + 1)) | (gstart << 1) | uint64_t(rev);
         a.hit_vals[slot] = uint32_t(k);
+        if (a.per_read && atomicAdd(a.per_read + r, 1u) == kSmallSeg) atomicAdd(a.n_big, 1ull);
       }
     } else if (slot_i < total) {
       uint32_t* o = reinterpret_cast<uint32_t*>(static_cast<char*>(a.validated) + i * 20);
@@ -389,7 +392,8 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t r_
 void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint64_t* cand_keys, uint64_t n,
                          unsigned read_bits, unsigned band, unsigned pct, int mode, uint64_t* hit_keys,
                          uint32_t* hit_vals, unsigned long long* d_count, void* d_validated,
-                         const unsigned long long* d_n, unsigned seed_q) {
+                         const unsigned long long* d_n, unsigned seed_q, uint32_t* per_read,
+                         unsigned long long* d_big) {
   if (band == 0 || band > 64) throw InputError("band width must be in [1, 64]");
   if (pct > 100) throw InputError("percent identity must be in [0, 100]");
   if (read_bits + 1 + ref.diag_bits > 64) throw InputError("read batch too large for the 64-bit hit key");
@@ -418,6 +422,8 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
   a.hit_vals = hit_vals;
   a.counter = d_count;
   a.validated = d_validated;
+  a.per_read = per_read;
+  a.n_big = d_big;
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, kValThreads), uint64_t(kSMs) * 32));
   KernelScope ks(c, "k_validate");
   // map path: split where a candidate's lower bound has passed k_max unless

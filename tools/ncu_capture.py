@@ -26,7 +26,7 @@ sys.path.insert(0, ROOT)
 # ncu kernel name pattern -> bench.py KernelScope name
 NAMES = [("k_join", r"k_join"), ("k_part_hist", r"k_part_hist"), ("k_part_scatter", r"k_part_scatter"),
          ("k_refine_scatter", r"k_refine_scatter"), ("k_validate", r"k_validate"),
-         ("k_hash_insert", r"k_hash_insert"), ("k_strata_seg", r"k_seg_|k_count_reads|k_scatter_reads"),
+         ("k_hash_insert", r"k_hash_insert"), ("k_strata_seg", r"k_seg_|k_scatter_reads"),
          ("k_tile_compact", r"k_tile_compact")]
 
 
