@@ -528,6 +528,14 @@ def run_gpu(args):
         if inst:
             ent["issue_frac"] = round(inst / (per_launch["k_validate"] / 1e3) / (148 * 4 * clk_hz), 4)
         stage_roof["k_validate"] = ent
+        if dom == "k_validate":  # validation dominates (C3, C4, q=12): its INT-ALU roofline is the line's
+            roof = {"bound": "int32 alu", "kernel": "k_validate", "achieved": ent["achieved_tops"],
+                    "peak": ent["peak_tops"], "unit": "TOP/s", "frac": ent["frac"],
+                    "traffic": ncu.get("kernels", {}).get("k_validate", {}).get("dram_bytes"),
+                    "peak_source": "148 SMs x 128 INT32 lanes x measured SM clock",
+                    "ops_formula": ent["ops_formula"], "launch_ms": ent["ms"],
+                    "share_of_step": round(ktimes["k_validate"][0] / prof_steps / (sum(ptimes) / len(ptimes)), 4),
+                    "traffic_source": ncu.get("_path") if ncu else "no ncu capture of this library build"}
     step_mean = sum(ptimes) / len(ptimes)
     f_filt = (stimes.get("filter", 0.0) / prof_steps) / step_mean if step_mean else None
 

@@ -217,7 +217,7 @@ uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& ou
   DBuf<uint64_t> table(c, T);
   QGM_CUDA(cudaMemsetAsync(table.p, 0xFF, T * sizeof(uint64_t), c.stream));
   {
-    KernelScope ks(c, "k_hash_insert");
+    KernelScope ks(c, "k_hash_insert_sample");  // the dedup-skip estimate: not the batch's dedup
     const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
     QGM_KERNEL(c, k_hash_insert, grid, 256, 0, keys, n, table.p, T - 1);
   }
