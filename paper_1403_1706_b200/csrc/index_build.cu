@@ -36,6 +36,8 @@ namespace {
 constexpr unsigned kLowBits = 13;  // codes per bucket = 8192
 constexpr int kBuildThreads = 256;
 constexpr uint64_t kLowMask = (1u << kLowBits) - 1;
+constexpr size_t kMaxBuildSmem = 200 * 1024;  // dynamic shared memory of one emit CTA
+struct BuildRetry {};                         // a bucket geometry the emit cannot stage
 
 // Read q-grams: one slot per (read, offset) with offset <= stride-q; slots
 // past a read's length are idle (seq.hpp:135-137).
@@ -166,11 +168,11 @@ __global__ void k_pal_scan(RefSource src, uint64_t* __restrict__ out, unsigned l
   }
 }
 
-// bucketed item: extra (4 bits) << 45 | low code bits (13) << 32 | pos
+// bucketed item: extra (4 bits) << 48 | low code bits (lb <= 16) << 32 | pos
 __device__ __forceinline__ uint64_t pack_item(uint32_t extra, uint32_t glow, uint32_t pos) {
-  return (uint64_t(extra) << 45) | (uint64_t(glow) << 32) | pos;
+  return (uint64_t(extra) << 48) | (uint64_t(glow) << 32) | pos;
 }
-__device__ __forceinline__ uint32_t item_glow(uint64_t pr) { return uint32_t(pr >> 32) & uint32_t(kLowMask); }
+__device__ __forceinline__ uint32_t item_glow(uint64_t pr) { return uint32_t(pr >> 32) & 0xFFFFu; }
 
 template <class Src>
 __global__ void k_bucket_rank(Src src, uint64_t n_items, unsigned lb, uint32_t* __restrict__ bucket_cnt,
@@ -279,13 +281,21 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* _
       const uint32_t wi = gl / w;
       const uint32_t slot = atomicAdd(cnt + sloc[wi] + rank_below<W>(occ[wi], gl % w), 1u);
       O[b0 + slot] = uint32_t(pr);
-      if (kExtra) X[b0 + slot] = uint8_t(pr >> 45);
+      if (kExtra) X[b0 + slot] = uint8_t(pr >> 48);
     }
     __syncthreads();
   }
 }
 
 __global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
+
+__global__ void k_max_u32(const uint32_t* __restrict__ a, uint64_t n, uint32_t* __restrict__ out) {
+  uint32_t m = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    m = max(m, a[i]);
+  m = __reduce_max_sync(kFull, m);
+  if (lane_id() == 0 && m) atomicMax(out, m);
+}
 
 // group start of word w relative to its sub-bin (< 2^16: a sub-bin holds at
 // most 2^16 codes and this is an exclusive prefix)
@@ -411,15 +421,22 @@ void finish_impl(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_
                uint32_t(B.gpb), reinterpret_cast<W*>(out.I.p), dcnt.p);
   }
   DBuf<uint32_t> dbase(c, B.buckets + 1);
-  DBuf<uint32_t> dtotal(c, 1);
+  DBuf<uint32_t> dtotal(c, 2);  // total distinct codes, largest bucket's distinct count
+  dtotal.zero();
   exclusive_scan_u32(c, dcnt.p, dbase.p, B.buckets + 1, dtotal.p, nullptr);
-  uint32_t D = 0;
-  QGM_CUDA(cudaMemcpyAsync(&D, dtotal.p, 4, cudaMemcpyDeviceToHost, c.stream));
+  QGM_KERNEL(c, k_max_u32, unsigned(std::min<uint64_t>(ceil_div(B.buckets, 256), uint64_t(kSMs) * 4)), 256, 0,
+             dcnt.p, B.buckets, dtotal.p + 1);
+  uint32_t Dm[2] = {0, 0};
+  QGM_CUDA(cudaMemcpyAsync(Dm, dtotal.p, 8, cudaMemcpyDeviceToHost, c.stream));
   QGM_CUDA(cudaStreamSynchronize(c.stream));
+  const uint32_t D = Dm[0];
   out.distinct = D;
   out.S1.alloc(c, uint64_t(D) + 1);
 
-  const size_t smem = B.gpb * sizeof(W) + B.gpb * 4 + (B.gpb * B.w) * 4;
+  // the emit's per-code counters: one per distinct code of the bucket (the
+  // largest bucket's count), not one per code of the bucket's range
+  const size_t smem = B.gpb * sizeof(W) + B.gpb * 4 + size_t(std::max<uint32_t>(Dm[1], 1)) * 4;
+  if (smem > kMaxBuildSmem) throw BuildRetry{};
   auto launch = [&](auto kernel) {
     ensure_dynamic_smem(reinterpret_cast<const void*>(kernel), size_t(smem));
     KernelScope ks(c, "k_bucket_emit");
@@ -439,12 +456,12 @@ void finish_impl(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_
   QGM_KERNEL(c, k_set_u32, 1, 1, 0, out.S1.p + D, B.V);
 }
 
-void init_geometry(Buckets& B, unsigned q, unsigned w) {
+void init_geometry(Buckets& B, unsigned q, unsigned w, unsigned lb_max = kLowBits) {
   if (q == 0 || q > 16) throw InputError("q must be in [1, 16]");
   if (w != 32 && w != 64) throw InputError("group width must be 32 or 64");
   B.q = q;
   B.w = w;
-  B.lb = std::min(2 * q, kLowBits);
+  B.lb = std::min(2 * q, lb_max);
   B.hb = 2 * q - B.lb;
   const uint64_t space = uint64_t(1) << (2 * q);
   B.groups = ceil_div(space, w);
@@ -455,8 +472,8 @@ void init_geometry(Buckets& B, unsigned q, unsigned w) {
 
 }  // namespace
 
-void bucket_reads(Ctx& c, const Reads& reads, unsigned q, unsigned w, Buckets& out) {
-  init_geometry(out, q, w);
+void bucket_reads(Ctx& c, const Reads& reads, unsigned q, unsigned w, Buckets& out, unsigned lb_max) {
+  init_geometry(out, q, w, lb_max);
   ReadSource src;
   src.words = reads.words.p;
   src.lengths = reads.lengths.p;
@@ -539,9 +556,23 @@ void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sample
     QGM_CUDA(cudaStreamSynchronize(c.stream));
     if (lens[0] > reads.stride) throw InputError("read longer than the stride");
   }
-  Buckets B;
-  bucket_reads(c, reads, q, w, B);
-  index_from_buckets(c, B, sampled, out, nullptr);
+  // buckets of 2^16 codes when that leaves ~8k q-grams per bucket or fewer
+  // (C2: 65536 buckets of ~1300): 8x fewer per-bucket passes of the occupy /
+  // emit kernels and a scatter into 8x fewer frontiers than 2^13-code
+  // buckets; a bucket with too many distinct codes for the emit's shared
+  // counters falls back to 2^13
+  const uint64_t n_items = uint64_t(reads.n) * (reads.stride >= q ? reads.stride - q + 1 : 0);
+  const bool wide = 2 * q >= 24 && (n_items >> (2 * q - 16)) <= 8192;
+  for (int attempt = wide ? 0 : 1; attempt < 2; ++attempt) {
+    Buckets B;
+    bucket_reads(c, reads, q, w, B, attempt == 0 ? 16u : kLowBits);
+    try {
+      index_from_buckets(c, B, sampled, out, nullptr);
+    } catch (const BuildRetry&) {
+      continue;
+    }
+    break;
+  }
   out.stride = reads.stride;
   out.n_reads = reads.n;
 }

@@ -295,7 +295,7 @@ void make_read_planes(Ctx& c, Reads& r);
 void make_ref_planes(Ctx& c, Ref& ref);
 
 // index_build.cu
-void bucket_reads(Ctx& c, const Reads& reads, unsigned q, unsigned w, Buckets& out);
+void bucket_reads(Ctx& c, const Reads& reads, unsigned q, unsigned w, Buckets& out, unsigned lb_max = 13);
 void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool packed, Buckets& out, uint64_t* n_pal);
 // Repeat mask on the device: set the mask bit of every
 // position whose forward q-gram occurs more than `threshold` times among the
