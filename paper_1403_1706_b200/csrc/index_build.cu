@@ -172,7 +172,10 @@ __global__ void k_pal_scan(RefSource src, uint64_t* __restrict__ out, unsigned l
 __device__ __forceinline__ uint64_t pack_item(uint32_t extra, uint32_t glow, uint32_t pos) {
   return (uint64_t(extra) << 48) | (uint64_t(glow) << 32) | pos;
 }
-__device__ __forceinline__ uint32_t item_glow(uint64_t pr) { return uint32_t(pr >> 32) & 0xFFFFu; }
+// kG = 32 for these items, 40 for join items (partition.cu) of a raw-code
+// partition, whose low 16 code bits sit at bit 40 and position in bits 0..31
+template <int kG = 32>
+__device__ __forceinline__ uint32_t item_glow(uint64_t pr) { return uint32_t(pr >> kG) & 0xFFFFu; }
 
 template <class Src>
 __global__ void k_bucket_rank(Src src, uint64_t n_items, unsigned lb, uint32_t* __restrict__ bucket_cnt,
@@ -203,7 +206,7 @@ __global__ void k_bucket_scatter(Src src, uint64_t n_items, unsigned lb, const u
   }
 }
 
-template <class W>
+template <class W, int kG>
 __global__ void __launch_bounds__(kBuildThreads) k_bucket_occupy(const uint64_t* __restrict__ pairs,
                                                                  const uint32_t* __restrict__ boff,
                                                                  uint64_t buckets, uint32_t gpb,
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_occupy(const uint64_t*
     __syncthreads();
     const uint32_t b0 = boff[bk], b1 = boff[bk + 1];
     for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-      const uint32_t gl = item_glow(pairs[i]);
+      const uint32_t gl = item_glow<kG>(pairs[i]);
       atomicOr(reinterpret_cast<AW*>(occ + gl / w), AW(W(1) << (gl % w)));
     }
     __syncthreads();
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_occupy(const uint64_t*
   }
 }
 
-template <class W, bool kSampled, bool kExtra>
+template <class W, bool kSampled, bool kExtra, int kG>
 __global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* __restrict__ pairs,
                                                                const uint32_t* __restrict__ boff,
                                                                const uint32_t* __restrict__ dbase,
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* _
     __syncthreads();
     const uint32_t b0 = boff[bk], b1 = boff[bk + 1];
     for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-      const uint32_t gl = item_glow(pairs[i]);
+      const uint32_t gl = item_glow<kG>(pairs[i]);
       const uint32_t wi = gl / w;
       atomicAdd(cnt + sloc[wi] + rank_below<W>(occ[wi], gl % w), 1u);
     }
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* _
     __syncthreads();
     for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
       const uint64_t pr = pairs[i];
-      const uint32_t gl = item_glow(pr);
+      const uint32_t gl = item_glow<kG>(pr);
       const uint32_t wi = gl / w;
       const uint32_t slot = atomicAdd(cnt + sloc[wi] + rank_below<W>(occ[wi], gl % w), 1u);
       O[b0 + slot] = uint32_t(pr);
@@ -399,7 +402,7 @@ void bucket_impl(Ctx& c, const Src& src, uint64_t n_items, Buckets& B) {
   }
 }
 
-template <class W>
+template <class W, int kG>
 void finish_impl(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_t>* extra) {
   out.q = B.q;
   out.w = B.w;
@@ -417,7 +420,7 @@ void finish_impl(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_
   QGM_CUDA(cudaMemsetAsync(dcnt.p + B.buckets, 0, 4, c.stream));
   {
     KernelScope ks(c, "k_bucket_occupy");
-    QGM_KERNEL(c, k_bucket_occupy<W>, grid_b, kBuildThreads, B.gpb * sizeof(W), B.pairs.p, B.boff.p, B.buckets,
+    QGM_KERNEL(c, (k_bucket_occupy<W, kG>), grid_b, kBuildThreads, B.gpb * sizeof(W), B.pairs.p, B.boff.p, B.buckets,
                uint32_t(B.gpb), reinterpret_cast<W*>(out.I.p), dcnt.p);
   }
   DBuf<uint32_t> dbase(c, B.buckets + 1);
@@ -444,11 +447,11 @@ void finish_impl(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_
                reinterpret_cast<const W*>(out.I.p), out.S.p, out.S1.p, out.O.p, extra ? extra->p : nullptr);
   };
   if (sampled) {
-    if (extra) launch(k_bucket_emit<W, true, true>);
-    else launch(k_bucket_emit<W, true, false>);
+    if (extra) launch(k_bucket_emit<W, true, true, kG>);
+    else launch(k_bucket_emit<W, true, false, kG>);
   } else {
-    if (extra) launch(k_bucket_emit<W, false, true>);
-    else launch(k_bucket_emit<W, false, false>);
+    if (extra) launch(k_bucket_emit<W, false, true, kG>);
+    else launch(k_bucket_emit<W, false, false, kG>);
   }
   // sentinels: S[groups] = D (kept by sampling iff groups is even), S'[D] = V
   if (!sampled) QGM_KERNEL(c, k_set_u32, 1, 1, 0, out.S.p + B.groups, D);
@@ -545,8 +548,14 @@ void mask_repeats(Ctx& c, Ref& ref, unsigned q, uint64_t threshold) {
 }
 
 void index_from_buckets(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_t>* extra) {
-  if (B.w == 32) finish_impl<uint32_t>(c, B, sampled, out, extra);
-  else finish_impl<uint64_t>(c, B, sampled, out, extra);
+  if (B.join_items) {  // a raw-code partition's items (no extra byte)
+    if (B.w == 32) finish_impl<uint32_t, 40>(c, B, sampled, out, nullptr);
+    else finish_impl<uint64_t, 40>(c, B, sampled, out, nullptr);
+  } else if (B.w == 32) {
+    finish_impl<uint32_t, 32>(c, B, sampled, out, extra);
+  } else {
+    finish_impl<uint64_t, 32>(c, B, sampled, out, extra);
+  }
 }
 
 void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sampled, Index& out) {
@@ -565,7 +574,22 @@ void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sample
   const bool wide = 2 * q >= 24 && (n_items >> (2 * q - 16)) <= 8192;
   for (int attempt = wide ? 0 : 1; attempt < 2; ++attempt) {
     Buckets B;
-    bucket_reads(c, reads, q, w, B, attempt == 0 ? 16u : kLowBits);
+    if (attempt == 0) {
+      // 2^16-code buckets from the map path's two staged counting sorts over
+      // raw codes (partition.cu): the buckets are its sub-bins
+      init_geometry(B, q, w, 16);
+      Partitioned rp;
+      partition_reads(c, reads, q, rp, /*raw=*/true, /*force_key_bits=*/2 * q - B.lb);
+      uint32_t fl[4] = {0, 0, 0, 0};
+      QGM_CUDA(cudaMemcpyAsync(fl, rp.flags.p, sizeof(fl), cudaMemcpyDeviceToHost, c.stream));
+      QGM_CUDA(cudaStreamSynchronize(c.stream));
+      B.V = fl[0];
+      B.boff.swap(rp.soff);
+      B.pairs.swap(rp.pairs);
+      B.join_items = true;
+    } else {
+      bucket_reads(c, reads, q, w, B, kLowBits);
+    }
     try {
       index_from_buckets(c, B, sampled, out, nullptr);
     } catch (const BuildRetry&) {

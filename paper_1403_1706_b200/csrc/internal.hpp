@@ -188,6 +188,7 @@ struct Buckets {
   unsigned q = 0, w = 32, lb = 0, hb = 0;
   uint64_t groups = 0, buckets = 0, gpb = 0;
   uint32_t V = 0;
+  bool join_items = false;  // pairs are join items of a raw-code partition (partition.cu), lb = 16
   DBuf<uint32_t> boff;
   DBuf<uint64_t> pairs;
 };
@@ -345,7 +346,10 @@ struct Partitioned {
   DBuf<uint32_t> soff;    // sub-bin offsets, 2^sub_bits + 1 entries
   DBuf<uint64_t> pairs;
 };
-void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out);
+// raw: group by the q-grams' own codes (the read index of qgm_index_build)
+// instead of canonical codes; force_key_bits (0 = adaptive): the sub-bin width.
+void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out, bool raw = false,
+                     unsigned force_key_bits = 0);
 
 // join.cu -- the same candidates as filter_reference, from a code-ordered
 // join of the partitioned read q-grams with the reference q-group indexes.

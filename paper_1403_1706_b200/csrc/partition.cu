@@ -71,7 +71,9 @@ __device__ __forceinline__ uint64_t revcomp32(uint64_t a) {
   return ((r >> 1) & 0x5555555555555555ull) | ((r & 0x5555555555555555ull) << 1);
 }
 
-template <int Q>
+// kRaw: the q-gram's own code instead of its canonical code (the read-side
+// q-group index of qgm_index_build, keyed by raw codes)
+template <int Q, bool kRaw = false>
 struct ItemGen {
   const uint64_t* words;
   const uint32_t* lengths;
@@ -134,7 +136,7 @@ struct ItemGen {
     f = uint32_t((u.A << (2 * j + 2)) >> (64 - 2 * q));
     // rc(f): bases j+1 .. j+q of A sit at bits [2j+2, 2j+2+2q) of RC
     const uint32_t rc = uint32_t(RC >> (2 * j + 2)) & (q == 16 ? 0xFFFFFFFFu : (1u << (2 * q)) - 1u);
-    g = f * 0x9E3779B1u <= rc * 0x9E3779B1u ? f : rc;  // canon_code(f, q)
+    g = kRaw || f * 0x9E3779B1u <= rc * 0x9E3779B1u ? f : rc;  // canon_code(f, q)
     const uint32_t bl = uint32_t(u.A >> (62 - 2 * j)) & 3u;
     const uint32_t br = uint32_t(u.A >> (62 - 2 * (j + q + 1))) & 3u;
     m = (o ? bl : 4u) | ((o + q < u.n ? 3u - br : 4u) << 3) | (uint32_t(f != g) << 6);
@@ -150,8 +152,8 @@ struct ItemGen {
 // from this one histogram, so the refinement needs no counting pass. A u16
 // counter hands 0x8000 to the global count whenever it reaches 0x8000.
 constexpr int kHistThreads = 1024;
-template <int Q, int R>
-__global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen<Q> gen, uint32_t per_cta, unsigned kshift,
+template <int Q, int R, bool kRaw>
+__global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen<Q, kRaw> gen, uint32_t per_cta, unsigned kshift,
                                                                  uint32_t keys, uint32_t* __restrict__ hist) {
   extern __shared__ uint32_t h2[];  // keys / 2 words (keys >= 2)
   const uint32_t words = (keys + 1) / 2;
@@ -228,8 +230,8 @@ __global__ void k_bin_offsets(const uint32_t* __restrict__ soff, uint32_t nbins,
 // contiguous range of reads) are on their way into shared memory by one bulk
 // copy (C2: 0.407 -> 0.403 ms; staging P0's words the same way cost more in
 // per-step barriers than it saved, 0.126 -> 0.146 ms).
-template <int Q, int R>
-__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(ItemGen<Q> gen, unsigned shift,
+template <int Q, int R, bool kRaw>
+__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(ItemGen<Q, kRaw> gen, unsigned shift,
                                                                   const uint32_t* __restrict__ boff,
                                                                   uint32_t* __restrict__ cursor,
                                                                   uint64_t* __restrict__ out, uint32_t sw_words,
@@ -510,15 +512,15 @@ __global__ void __launch_bounds__(kP2Threads, kP2MinBlocks) k_refine_scatter(con
 }  // namespace
 
 // P0 + P1 for one (Q, R) instantiation (Q = compile-time q or 0, R = run length).
-template <int Q, int R>
-static void p0_p1(Ctx& c, const ItemGen<Q>& gen, const Reads& reads, unsigned q, unsigned key_bits, unsigned bits,
+template <int Q, int R, bool kRaw>
+static void p0_p1(Ctx& c, const ItemGen<Q, kRaw>& gen, const Reads& reads, unsigned q, unsigned key_bits, unsigned bits,
                   Partitioned& out, DBuf<uint32_t>& h2, DBuf<uint64_t>& p1, uint32_t& V) {
   const uint32_t keys = 1u << key_bits;
   const unsigned sub = key_bits - bits, shift = 2 * q - bits;
   {
     const uint32_t per_cta = uint32_t(ceil_div(ceil_div(gen.n_runs, uint64_t(kSMs)), kHistThreads) * kHistThreads);
     const size_t hsmem = size_t((keys + 1) / 2) * 4;
-    auto kern = k_part_hist16<Q, R>;
+    auto kern = k_part_hist16<Q, R, kRaw>;
     ensure_dynamic_smem(reinterpret_cast<const void*>(kern), size_t(hsmem));
     KernelScope ks(c, "k_part_hist");
     QGM_KERNEL(c, kern, unsigned(ceil_div(gen.n_runs, per_cta)), kHistThreads, hsmem, gen, per_cta,
@@ -537,17 +539,17 @@ static void p0_p1(Ctx& c, const ItemGen<Q>& gen, const Reads& reads, unsigned q,
   // the following word, rounded to 16-byte pairs
   const uint32_t sw_words = ((chunk_runs / gen.rpr + 2) * reads.W + 4 + 1) & ~1u;
   const size_t smem = kChunk * (sizeof(uint64_t) + sizeof(uint8_t)) + size_t(2) * sw_words * sizeof(uint64_t);
-  auto p1kern = k_part_scatter<Q, R>;
+  auto p1kern = k_part_scatter<Q, R, kRaw>;
   ensure_dynamic_smem(reinterpret_cast<const void*>(p1kern), size_t(smem));
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(gen.n_runs, chunk_runs), uint64_t(kSMs) * kPartMinBlocks));
   KernelScope ks(c, "k_part_scatter");
   QGM_KERNEL(c, p1kern, grid, kPartThreads, smem, gen, shift, out.boff.p, hist.p, p1.p, sw_words, reads.lens.p);
 }
 
-template <int Q>
+template <int Q, bool kRaw>
 static void p0_p1_runs(Ctx& c, const Reads& reads, unsigned q, uint32_t span, unsigned key_bits, unsigned bits,
                        Partitioned& out, DBuf<uint32_t>& h2, DBuf<uint64_t>& p1, uint32_t& V) {
-  ItemGen<Q> gen;
+  ItemGen<Q, kRaw> gen;
   gen.words = reads.words.p;
   gen.lengths = reads.lengths.p;
   gen.W = reads.W;
@@ -561,11 +563,11 @@ static void p0_p1_runs(Ctx& c, const Reads& reads, unsigned q, uint32_t span, un
   const uint64_t n_runs = uint64_t(reads.n) * gen.rpr;
   if (n_runs * R > 0xFFFFFFFFull - kChunk) throw InputError("read batch has more than 2^32-1 q-gram slots");
   gen.n_runs = uint32_t(n_runs);
-  if (R == kRun) p0_p1<Q, kRun>(c, gen, reads, q, key_bits, bits, out, h2, p1, V);
-  else p0_p1<Q, 1>(c, gen, reads, q, key_bits, bits, out, h2, p1, V);
+  if (R == kRun) p0_p1<Q, kRun, kRaw>(c, gen, reads, q, key_bits, bits, out, h2, p1, V);
+  else p0_p1<Q, 1, kRaw>(c, gen, reads, q, key_bits, bits, out, h2, p1, V);
 }
 
-void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
+void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out, bool raw, unsigned force_key_bits) {
   if (q == 0 || q > 16) throw InputError("q must be in [1, 16]");
   const uint32_t span = reads.stride >= q ? reads.stride - q + 1 : 0;
   const uint64_t n_items64 = uint64_t(reads.n) * span;
@@ -583,6 +585,11 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
     while (want < 16 && (uint64_t(n_items) >> (want + 1)) >= 256) ++want;
     want = std::max(want, 2 * q > 16 ? 2 * q - 16 : 0u);
     key_bits = std::min(key_bits, std::max(want, std::min(2 * q, kBinBits)));
+  }
+  if (force_key_bits) {
+    if (force_key_bits < std::min(2 * q, kBinBits) || force_key_bits > std::min(2 * q, 16u))
+      throw InternalError("partition: key width outside [first-pass bits, 16]");
+    key_bits = force_key_bits;
   }
   out.q = q;
   out.bins = 1u << bits;
@@ -606,9 +613,16 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out) {
   h2.zero();
   DBuf<uint64_t> p1;
   uint32_t V = n_items;  // bound; the exact count is flags[0]
-  if (q == 16) p0_p1_runs<16>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
-  else if (q == 12) p0_p1_runs<12>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
-  else p0_p1_runs<0>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
+  if (raw) {
+    if (q == 16) p0_p1_runs<16, true>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
+    else p0_p1_runs<0, true>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
+  } else if (q == 16) {
+    p0_p1_runs<16, false>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
+  } else if (q == 12) {
+    p0_p1_runs<12, false>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
+  } else {
+    p0_p1_runs<0, false>(c, reads, q, span, key_bits, bits, out, h2, p1, V);
+  }
   out.V = V;
   // P2: refine to the top min(2q, 16) code bits (short reuse distance of the
   // reference-index sectors in the join) and convert to join items. Runs even
