@@ -272,7 +272,8 @@ static int hook_point() {  // experiment knob: 0 after the join, 1 after dedup, 
 }
 
 static uint64_t dedup_direct_max() {
-  if (const char* e = std::getenv("QGM_DEDUP_DIRECT_MAX")) return std::strtoull(e, nullptr, 10);  // tests
+  const char* e = std::getenv("QGM_DEDUP_DIRECT_MAX");  // tests
+  if (e && e[0]) return std::strtoull(e, nullptr, 10);
   return kDedupDirectMax;
 }
 
@@ -367,7 +368,8 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   if (ref.padded_total < (uint64_t(1) << 32)) {
     uint64_t cap = std::max<uint64_t>(std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16),
                                       c.last_raw_candidates + c.last_raw_candidates / 8);
-    if (const char* e = std::getenv("QGM_MAP_ASYNC_CAP")) cap = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));  // tests
+    const char* ce = std::getenv("QGM_MAP_ASYNC_CAP");  // tests
+    if (ce && ce[0]) cap = std::max<uint64_t>(1, std::strtoull(ce, nullptr, 10));
     const char* ae = std::getenv("QGM_MAP_ASYNC");  // A/B and test knob: 0 = always the round-trip path
     const bool async_off = ae && ae[0] == '0';
     if (!async_off && cap <= dedup_direct_max()) {

@@ -332,6 +332,7 @@ def test_validation_park_overflow_finishes_in_phase_one(ctx, oracle, monkeypatch
     extra candidates are finished in phase 1; hits identical to the oracle."""
     import paper_1403_1706_b200 as qgm
     monkeypatch.setenv("QGM_VAL_PARK_CAP", "500")
+    monkeypatch.setenv("QGM_VAL_SPLIT", "64")  # two phases even for a batch this small
     ref, cb, codes, lengths, tp, ts = _c1(qgm, n_reads=5000, L=500_000)
     R = qgm.Reference.from_codes(ctx, ref, cb)
     reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)

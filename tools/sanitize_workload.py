@@ -60,9 +60,11 @@ def main():
 
     # validation park overflow branch + sampled dedup decision
     os.environ["QGM_VAL_PARK_CAP"] = "1000"
+    os.environ["QGM_VAL_SPLIT"] = "64"  # two phases even for this batch size
     os.environ["QGM_DEDUP_DIRECT_MAX"] = "20000"
     run(ctx, orc, "park overflow + sampled dedup", ref, cb, codes, lengths, 100, q=12, mode=0)
     os.environ["QGM_VAL_PARK_CAP"] = ""
+    os.environ["QGM_VAL_SPLIT"] = ""
     os.environ["QGM_DEDUP_DIRECT_MAX"] = ""
 
     # unpacked reference index (O without packed extra bits)
