@@ -181,9 +181,10 @@ struct Index {
   DBuf<uint32_t> O;       // occ
 };
 
-// Items bucketed by the top 2q-13 bits of their q-gram code (the first half
-// of the index build, index_build.cu). pairs[i] = extra << 45 | (code & 8191)
-// << 32 | position; bucket k holds pairs[boff[k], boff[k+1]).
+// Items bucketed by the top 2q-lb bits of their q-gram code (the first half
+// of the index build, index_build.cu). pairs[i] = extra << 48 | (code & (2^lb
+// - 1)) << 32 | position (or, join_items, a raw-code partition's items);
+// bucket k holds pairs[boff[k], boff[k+1]).
 struct Buckets {
   unsigned q = 0, w = 32, lb = 0, hb = 0;
   uint64_t groups = 0, buckets = 0, gpb = 0;

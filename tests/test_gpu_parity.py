@@ -98,6 +98,52 @@ def test_repetitive_reference_and_mask_match_oracle(ctx, oracle, monkeypatch, un
         assert _same(got, want), (m is None, got.size, want.size)
 
 
+@pytest.mark.parametrize("q,strands", [(12, 1), (12, 2), (16, 3), (16, 1)])
+def test_repeat_intervals_skip_only_suppressed_occurrences(ctx, oracle, q, strands):
+    """Tandem repeats give q-gram intervals of thousands of occurrences, where
+    the join skips the (strand flag, compare base) classes the run-start rule
+    suppresses (the reference intervals are sorted by that class): one strand
+    or both, every hit and statistic identical to the oracle."""
+    import paper_1403_1706_b200 as qgm
+    L = 300_000
+    ref = qgm.repetitive_reference(40 + q, L)
+    cb = np.array([0, 170_000, L], np.uint64)
+    codes, lengths, *_ = qgm.simulate_reads(41 + q, ref, cb, 3000, 100, 0.03)
+    R = qgm.Reference.from_codes(ctx, ref, cb)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, 100)
+    got, st = ctx.map(reads, R, q=q, mode=1, strands=strands)
+    want, ost = oracle.map(ref, cb, codes, 100, lengths, q=q, mode=1, strands=strands)
+    assert _same(got, want), (got.size, want.size)
+    assert st["unique_candidates"] == ost["unique_candidates"], (st, ost)
+    _validated_agrees(st, ost, 1)
+
+
+@pytest.mark.parametrize("skewed", [False, True])
+def test_read_index_build_wide_buckets_and_fallback(ctx, oracle, skewed):
+    """qgm_index_build at q=16 takes 2^16-code buckets from the raw-code
+    partition; a bucket with more distinct codes than the emit's shared
+    counters hold (every read = AAAAAAAA + 8 random bases: ~58k distinct codes
+    in bucket 0) falls back to 2^13-code buckets. Both equal the oracle's
+    build_qgroup_index (positions normalised inside intervals)."""
+    import paper_1403_1706_b200 as qgm
+    rng = np.random.default_rng(7 + skewed)
+    if skewed:
+        n, stride = 150_000, 16
+        codes = rng.integers(0, 4, n * stride).astype(np.uint8)
+        codes.reshape(n, stride)[:, :8] = 0
+    else:
+        n, stride = 20_000, 100
+        codes = rng.integers(0, 4, n * stride).astype(np.uint8)
+    lengths = np.full(n, stride, np.uint32)
+    reads = qgm.Reads.from_codes(ctx, codes, lengths, stride)
+    idx = qgm.Index.build(ctx, reads, 16).normalize()
+    I, S, S1, O = idx.arrays()
+    wI, wS, wS1, wO = oracle.build_index(codes, stride, lengths, 16)
+    from oracle.pyoracle import sort_intervals
+    assert np.array_equal(I, wI) and np.array_equal(S, wS) and np.array_equal(S1, wS1)
+    assert np.array_equal(O, sort_intervals(wS1, wO))
+
+
 def test_device_scan_matches_reference_semantics(ctx):
     import paper_1403_1706_b200 as qgm
     sums, tot = ctx.exclusive_scan(np.array([3, 0, 2], np.uint32))
