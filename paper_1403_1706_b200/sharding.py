@@ -154,13 +154,32 @@ class HostGather:
         rec = np.dtype(dtype).itemsize
         from multiprocessing import shared_memory
 
+        nbytes = max(int(offs[-1]) * rec, 1)
+        # POSIX shared memory (/dev/shm) when it has room for the job's
+        # records, else a file-backed mapping under the temp directory (a
+        # container's /dev/shm may be a few tens of MB)
         name = [None]
         if rank == 0:
-            shm = shared_memory.SharedMemory(create=True, size=max(int(offs[-1]) * rec, 1))
-            name = [shm.name]
+            import shutil
+            import tempfile
+            try:
+                room = shutil.disk_usage("/dev/shm").free
+            except OSError:
+                room = 0
+            if room > 2 * nbytes and not os.environ.get("QGM_GATHER_FILE"):  # (test knob: force the file)
+                shm = shared_memory.SharedMemory(create=True, size=nbytes)
+                name = [("shm", shm.name)]
+            else:
+                fd, path = tempfile.mkstemp(prefix=self.tag + "_gather_")
+                os.ftruncate(fd, nbytes)
+                os.close(fd)
+                name = [("file", path)]
         dist.broadcast_object_list(name, src=0)
-        if rank != 0:
-            shm = shared_memory.SharedMemory(name=name[0])
+        kind, where = name[0]
+        if kind == "file":
+            shm = _FileSegment(where, nbytes, owner=rank == 0)
+        elif rank != 0:
+            shm = shared_memory.SharedMemory(name=where)
         try:
             buf = np.ndarray((int(offs[-1]),), dtype=dtype, buffer=shm.buf)
             at = int(offs[rank])
@@ -175,10 +194,31 @@ class HostGather:
             shm.close()
             if rank == 0:
                 shm.unlink()
-        self.last = {"method": "all_gather(counts) + records into one POSIX shared host buffer at prefix offsets",
+        self.last = {"method": "all_gather(counts) + records into one shared host buffer at prefix offsets "
+                               f"({'POSIX shared memory' if kind == 'shm' else 'file mapping'})",
                      "counts": counts, "segments": segs, "bytes": int(offs[-1]) * rec,
                      "seconds": time.perf_counter() - t0}
         return out
+
+
+class _FileSegment:
+    """A file mapping with the SharedMemory interface HostGather uses."""
+
+    def __init__(self, path, nbytes, owner):
+        import mmap
+        self.path, self.owner = path, owner
+        self._f = open(path, "r+b")
+        self._m = mmap.mmap(self._f.fileno(), nbytes)
+        self.buf = memoryview(self._m)
+
+    def close(self):
+        self.buf.release()
+        self._m.close()
+        self._f.close()
+
+    def unlink(self):
+        if self.owner:
+            os.unlink(self.path)
 
 
 def hits_digest(hits: np.ndarray) -> str:

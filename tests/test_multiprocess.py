@@ -66,6 +66,8 @@ def _worker(rank, world_size, port, out_dir):
         got["read_id"] += np.repeat(np.array(segs, np.uint64) * BLOCK, g.last["segments"]).astype(np.uint32)
         np.save(os.path.join(out_dir, "gathered.npy"), got)
         np.save(os.path.join(out_dir, "max.npy"), np.array(mx))
+        with open(os.path.join(out_dir, "method.txt"), "w") as f:
+            f.write(g.last["method"])
     dist.barrier()
     dist.destroy_process_group()
 
@@ -106,9 +108,11 @@ def test_hits_digest_is_order_free():
     assert sharding.hits_digest(h) != sharding.hits_digest(h2)
 
 
-@pytest.mark.parametrize("world_size", [2, 3])
-def test_gloo_gather_of_sharded_maps_equals_single_process(tmp_path, oracle, world_size):
+@pytest.mark.parametrize("world_size,via_file", [(2, False), (3, False), (2, True)])
+def test_gloo_gather_of_sharded_maps_equals_single_process(tmp_path, oracle, monkeypatch, world_size, via_file):
     from paper_1403_1706_b200 import sharding
+    if via_file:  # the file-backed segment used when /dev/shm is too small
+        monkeypatch.setenv("QGM_GATHER_FILE", "1")
     port = _free_port()
     mp.start_processes(_worker, args=(world_size, port, str(tmp_path)), nprocs=world_size, join=True,
                        start_method="spawn")
@@ -124,3 +128,5 @@ def test_gloo_gather_of_sharded_maps_equals_single_process(tmp_path, oracle, wor
     cols = ("read_id", "chrom", "ref_start", "edits", "strand")
     assert all(np.array_equal(got[c], whole[c]) for c in cols)
     assert float(np.load(tmp_path / "max.npy")[0]) == 10.0 + world_size - 1
+    method = (tmp_path / "method.txt").read_text()
+    assert ("file mapping" in method) == via_file, method
