@@ -46,11 +46,17 @@ namespace {
 
 constexpr int kJoinThreads = 256;
 constexpr int kJoinWarps = kJoinThreads / 32;
-#ifndef QGM_JOIN_ITEMS
-#define QGM_JOIN_ITEMS 4
+// read q-grams (= lookups) per lane per step: the staged warp-specialised
+// join runs 4 (C2 join ms: 2 0.783, 3 0.873, 4 0.771); k_join, used where
+// S'/O are read from L2/HBM (C3, C4) or sub-bins are tiny, keeps 8 in flight
+// (C3 shard 4.50 -> 4.28 ms, C4 1.52 -> 1.38 ms against 4)
+#ifndef QGM_JOIN_ITEMS_WS
+#define QGM_JOIN_ITEMS_WS 4
 #endif
-constexpr int kItems = QGM_JOIN_ITEMS;    // read q-grams (= lookups) per lane per step
-constexpr int kRanges = 32 * kItems;
+#ifndef QGM_JOIN_ITEMS
+#define QGM_JOIN_ITEMS 8
+#endif
+constexpr int kItemsWs = QGM_JOIN_ITEMS_WS, kItemsJoin = QGM_JOIN_ITEMS;
 #ifndef QGM_JOIN_INLINE
 #define QGM_JOIN_INLINE 4
 #endif
@@ -196,7 +202,7 @@ __device__ __forceinline__ void skip_ranges(const uint32_t* Op, uint32_t lk0, ui
 // the staged occupancy words / group starts, expand the occurrence intervals
 // (S1p / Op / Ip: global arrays, or generic pointers into the staged slices), emit
 // the candidate keys.
-template <bool kRunStart, bool kPacked>
+template <bool kRunStart, bool kPacked, int kItems>
 __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI, const uint16_t* sR,
                                            const uint32_t* S1p, const uint32_t* Op, const uint64_t* Ip, uint32_t d0,
                                            uint32_t w0, uint32_t gsub, uint32_t my_lo, uint32_t my_hi,
@@ -328,9 +334,9 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
   uint16_t* sR = reinterpret_cast<uint16_t*>(s_dyn + nw);
   uint32_t* sS1 = s_dyn + ((nw + (((nw + 1) / 2 + 3) & ~3u) + 3) & ~3u);
   uint32_t* sO = sS1 + a.cap;
-  __shared__ uint32_t s_k0[kJoinWarps][kRanges];
-  __shared__ uint32_t s_k1[kJoinWarps][kRanges];
-  __shared__ uint8_t s_slot[kJoinWarps][kRanges];  // item slot u*32 + lane
+  __shared__ uint32_t s_k0[kJoinWarps][32 * kItemsJoin];
+  __shared__ uint32_t s_k1[kJoinWarps][32 * kItemsJoin];
+  __shared__ uint8_t s_slot[kJoinWarps][32 * kItemsJoin];  // item slot u*32 + lane
   __shared__ uint64_t s_eit[kJoinWarps][kEmitCap];
   __shared__ uint32_t s_exp[kJoinWarps][kEmitCap];
   __shared__ __align__(8) uint64_t s_bar;
@@ -428,10 +434,10 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
     const uint32_t my_lo = b0 + uint32_t(uint64_t(nitems) * wid / kJoinWarps);
     const uint32_t my_hi = b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kJoinWarps);
     if (staged) {  // S'/O accesses from shared-derived pointers only: LDS
-      join_items<kRunStart, kPacked>(a, sI, sR, sS1 - sA, sO - oA, a.items, d0, w0, sb << a.code_shift,
+      join_items<kRunStart, kPacked, kItemsJoin>(a, sI, sR, sS1 - sA, sO - oA, a.items, d0, w0, sb << a.code_shift,
                                         my_lo, my_hi, L);
     } else {
-      join_items<kRunStart, kPacked>(a, sI, sR, a.S1, a.O, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi,
+      join_items<kRunStart, kPacked, kItemsJoin>(a, sI, sR, a.S1, a.O, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi,
                                         L);
     }
     __syncthreads();  // the staging buffers are rewritten for the next sub-bin
@@ -460,9 +466,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
   // 2 stages: I [nw] | u16 starts | S' [cap] | O [cap] | items [icap] (u64)
   extern __shared__ __align__(16) uint32_t s_dyn[];
   const uint32_t nw = a.words;
-  __shared__ uint32_t s_k0[kWsCons][kRanges];
-  __shared__ uint32_t s_k1[kWsCons][kRanges];
-  __shared__ uint8_t s_slot[kWsCons][kRanges];
+  __shared__ uint32_t s_k0[kWsCons][32 * kItemsWs];
+  __shared__ uint32_t s_k1[kWsCons][32 * kItemsWs];
+  __shared__ uint8_t s_slot[kWsCons][32 * kItemsWs];
   __shared__ uint64_t s_eit[kWsCons][kEmitCap];
   __shared__ uint32_t s_exp[kWsCons][kEmitCap];
   __shared__ StageMeta meta[2];
@@ -586,13 +592,13 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
       // everything in shared memory: pointers derived from the shared
       // buffers only, so every access compiles to LDS (no generic LD and its
       // 64-bit address arithmetic)
-      join_items<kRunStart, kPacked>(a, sI, sR, sS1 - M.sA, sO - M.oA, sIt - M.iA, M.d0, w0,
+      join_items<kRunStart, kPacked, kItemsWs>(a, sI, sR, sS1 - M.sA, sO - M.oA, sIt - M.iA, M.d0, w0,
                                         M.sb << a.code_shift, my_lo, my_hi, L);
     } else {
       const uint32_t* S1p = M.staged ? sS1 - M.sA : a.S1;
       const uint32_t* Op = M.staged ? sO - M.oA : a.O;
       const uint64_t* Ip = M.items_staged ? sIt - M.iA : a.items;
-      join_items<kRunStart, kPacked>(a, sI, sR, S1p, Op, Ip, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
+      join_items<kRunStart, kPacked, kItemsWs>(a, sI, sR, S1p, Op, Ip, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
     }
     // one arrive per consumer thread (not lane 0 after a __syncwarp): each
     // thread's own reads of meta[s] and the staged slices are then ordered
