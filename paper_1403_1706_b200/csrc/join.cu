@@ -57,6 +57,7 @@ constexpr int kJoinWarps = kJoinThreads / 32;
 #define QGM_JOIN_ITEMS 8
 #endif
 constexpr int kItemsWs = QGM_JOIN_ITEMS_WS, kItemsJoin = QGM_JOIN_ITEMS;
+static_assert(kItemsWs <= 8 && kItemsJoin <= 8, "a list entry keeps its item slot u * 32 + lane in 8 bits");
 #ifndef QGM_JOIN_INLINE
 #define QGM_JOIN_INLINE 4
 #endif
