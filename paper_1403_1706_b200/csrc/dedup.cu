@@ -157,16 +157,37 @@ __global__ void __launch_bounds__(kDedupThreads) k_tile_compact_dev(const uint64
 
 // keys of every (mask+1)-th read (read id = key >> rshift) appended to out
 // (at most cap are stored; n_out keeps counting past cap so the caller sees
-// the overflow)
-__global__ void k_sample_reads(const uint64_t* __restrict__ keys, uint64_t n, unsigned rshift, uint64_t mask,
-                               uint64_t* __restrict__ out, uint64_t cap, unsigned long long* __restrict__ n_out) {
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t i0 = blockIdx.x * uint64_t(blockDim.x); i0 < n; i0 += stride) {  // warp-uniform trip count
-    const uint64_t i = i0 + threadIdx.x;
-    const uint64_t k = i < n ? keys[i] : 0ull;
-    const bool take = i < n && ((k >> rshift) & mask) == 0;
-    const unsigned long long at = warp_append(take, n_out);
-    if (take && at < cap) out[at] = k;
+// the overflow). Each CTA takes a tile of 16 keys per thread and reserves its
+// run of the output with one atomic (one per warp contended on the counter
+// like the join's did: C3, 118M keys).
+constexpr int kSamplePer = 16;
+__global__ void __launch_bounds__(256) k_sample_reads(const uint64_t* __restrict__ keys, uint64_t n, unsigned rshift,
+                                                     uint64_t mask, uint64_t* __restrict__ out, uint64_t cap,
+                                                     unsigned long long* __restrict__ n_out) {
+  __shared__ uint32_t ws[33];
+  __shared__ unsigned long long s_base;
+  const uint64_t tile = uint64_t(blockDim.x) * kSamplePer;
+  for (uint64_t t0 = blockIdx.x * tile; t0 < n; t0 += uint64_t(gridDim.x) * tile) {  // CTA-uniform trip count
+    uint64_t k[kSamplePer];
+    uint32_t take = 0;
+#pragma unroll
+    for (int j = 0; j < kSamplePer; ++j) {
+      const uint64_t i = t0 + uint64_t(j) * blockDim.x + threadIdx.x;
+      k[j] = i < n ? keys[i] : 0ull;
+      take |= uint32_t(i < n && ((k[j] >> rshift) & mask) == 0) << j;
+    }
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan<uint32_t>(__popc(take), ws, &tot);
+    if (threadIdx.x == 0) s_base = tot ? atomicAdd(n_out, (unsigned long long)tot) : 0ull;
+    __syncthreads();
+    uint64_t at = s_base + ex;
+#pragma unroll
+    for (int j = 0; j < kSamplePer; ++j)
+      if ((take >> j) & 1u) {
+        if (at < cap) out[at] = k[j];
+        ++at;
+      }
+    __syncthreads();  // s_base is rewritten by the next tile
   }
 }
 
@@ -243,8 +264,8 @@ double estimate_dup_fraction(Ctx& c, const uint64_t* keys, uint64_t n, unsigned 
   DBuf<uint64_t> sample(c, cap);
   DBuf<unsigned long long> ns(c, 1);
   ns.zero();
-  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
-  QGM_KERNEL(c, k_sample_reads, grid, 256, 0, keys, n, rshift, 63ull, sample.p, cap, ns.p);
+  QGM_KERNEL(c, k_sample_reads, unsigned(std::min<uint64_t>(ceil_div(n, 256 * kSamplePer), uint64_t(kSMs) * 8)), 256,
+             0, keys, n, rshift, 63ull, sample.p, cap, ns.p);
   unsigned long long m = 0;
   QGM_CUDA(cudaMemcpyAsync(&m, ns.p, sizeof(m), cudaMemcpyDeviceToHost, c.stream));
   QGM_CUDA(cudaStreamSynchronize(c.stream));
