@@ -359,8 +359,14 @@ constexpr uint32_t kLocal = 1024;
 #define QGM_P2_THREADS 256
 #endif
 constexpr int kP2Threads = QGM_P2_THREADS;
-constexpr int kP2MinBlocks = 1024 / kP2Threads;
-constexpr uint32_t kP2Per = 8;
+#ifndef QGM_P2_PER
+#define QGM_P2_PER 8
+#endif
+#ifndef QGM_P2_MINB
+#define QGM_P2_MINB (1024 / QGM_P2_THREADS)
+#endif
+constexpr int kP2MinBlocks = QGM_P2_MINB;
+constexpr uint32_t kP2Per = QGM_P2_PER;
 constexpr uint32_t kP2Chunk = kP2Per * kP2Threads;
 
 struct Refine {
