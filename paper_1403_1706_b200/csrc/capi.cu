@@ -432,8 +432,13 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   }
   {
     StageScope s(c, kStageSort);
-    if (dedup) {
+    if (dedup && (n_raw <= dedup_direct_max() || n_raw > 0xFFFFFFFFull)) {  // radix pass offsets are u32
       dedup_keys_async(c, keys.p, n_raw, alt, cnt.p + 1);  // unique candidates, any order (validation is per key)
+    } else if (dedup) {
+      // one table for all keys would leave L2 (C5: 752M keys, a 16 GB table,
+      // 48 ms of random DRAM read-modify-writes): partitioned on 8 key bits,
+      // each partition's table stays L2-resident
+      dedup_keys_partitioned(c, keys.p, n_raw, alt, cnt.p + 1);
     } else {
       alt.swap(keys);
       const unsigned long long nr = n_raw;

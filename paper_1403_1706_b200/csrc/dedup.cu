@@ -17,6 +17,7 @@ namespace {
 constexpr uint64_t kEmpty = ~0ull;  // never a key (the padded diagonal field is < 2^diag_bits - 1)
 constexpr int kTile = 4096;         // table slots per compaction tile
 constexpr int kDedupThreads = 256;
+constexpr uint64_t kPartKeys = uint64_t(4) << 20;  // keys per partition of dedup_keys_partitioned
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x ^= x >> 33;
@@ -70,7 +71,8 @@ __global__ void __launch_bounds__(kDedupThreads) k_tile_emit(const uint64_t* __r
 // One pass over the table: each CTA reserves its tile's run of the output
 // with one atomic (tile order is irrelevant: validation is per key) and
 // writes the tile's keys there. The counter ends as the unique count.
-__global__ void __launch_bounds__(kDedupThreads) k_tile_compact(const uint64_t* __restrict__ table,
+template <bool kReset>  // kReset: leave the tile empty again (the next partition reuses the table)
+__global__ void __launch_bounds__(kDedupThreads) k_tile_compact(uint64_t* __restrict__ table,
                                                                 uint64_t* __restrict__ out,
                                                                 unsigned long long* __restrict__ counter) {
   __shared__ uint32_t ws[33];
@@ -83,6 +85,7 @@ __global__ void __launch_bounds__(kDedupThreads) k_tile_compact(const uint64_t* 
   for (int j = 0; j < kPerThread; ++j) {  // coalesced; a thread's keys go to consecutive outputs
     v[j] = table[base + uint64_t(j) * kDedupThreads + threadIdx.x];
     c += v[j] != kEmpty;
+    if (kReset && v[j] != kEmpty) table[base + uint64_t(j) * kDedupThreads + threadIdx.x] = kEmpty;
   }
   uint32_t tot;
   const uint32_t ex = block_exclusive_scan<uint32_t>(c, ws, &tot);
@@ -211,7 +214,7 @@ void dedup_keys_async(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& 
   const uint32_t tiles = uint32_t(T / kTile);
   if (out.n < n) out.alloc(c, n);
   QGM_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
-  QGM_KERNEL(c, k_tile_compact, tiles, kDedupThreads, 0, table.p, out.p, d_count);
+  QGM_KERNEL(c, k_tile_compact<false>, tiles, kDedupThreads, 0, table.p, out.p, d_count);
 }
 
 void dedup_keys_dev(Ctx& c, const uint64_t* keys, uint64_t n_max, const unsigned long long* d_n,
@@ -229,6 +232,40 @@ void dedup_keys_dev(Ctx& c, const uint64_t* keys, uint64_t n_max, const unsigned
     QGM_KERNEL(c, k_hash_insert_dev, grid, 256, 0, keys, d_n, n_max, table.p);
   }
   QGM_KERNEL(c, k_tile_compact_dev, unsigned(T / kTile), kDedupThreads, 0, table.p, d_n, n_max, out.p, d_count);
+}
+
+void dedup_keys_partitioned(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out,
+                            unsigned long long* d_count) {
+  QGM_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
+  if (out.n < std::max<uint64_t>(n, 1)) out.alloc(c, std::max<uint64_t>(n, 1));
+  if (n == 0) return;
+  KernelScope ks(c, "k_hash_insert");
+  DBuf<uint64_t> part(c, n);
+  DBuf<uint32_t> starts(c, 257);
+  radix_digit_pass(c, keys, part.p, n, 0, starts.p);
+  std::vector<uint32_t> h(257);
+  QGM_CUDA(cudaMemcpyAsync(h.data(), starts.p, 257 * 4, cudaMemcpyDeviceToHost, c.stream));
+  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  // 256 / span partitions of consecutive digits, ~kPartKeys keys each (a
+  // table of <= 2^23 slots, 64 MB, stays in the 126 MB L2); fewer, larger
+  // partitions when the set is smaller (each costs two launches)
+  int span = 256;
+  while (span > 1 && n / (256 / span) > kPartKeys / 2) span >>= 1;
+  uint64_t most = 0;
+  for (int d = 0; d < 256; d += span) most = std::max<uint64_t>(most, h[d + span] - h[d]);
+  uint64_t T = kTile;
+  while (T < most + most / 2) T <<= 1;
+  DBuf<uint64_t> table(c, T);
+  QGM_CUDA(cudaMemsetAsync(table.p, 0xFF, T * sizeof(uint64_t), c.stream));  // once: each compaction resets its tiles
+  for (int d = 0; d < 256; d += span) {
+    const uint64_t np = h[d + span] - h[d];
+    if (np == 0) continue;
+    uint64_t Tp = kTile;
+    while (Tp < np + np / 2) Tp <<= 1;
+    const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(np, 256), uint64_t(kSMs) * 16));
+    QGM_KERNEL(c, k_hash_insert, grid, 256, 0, part.p + h[d], np, table.p, Tp - 1);
+    QGM_KERNEL(c, k_tile_compact<true>, unsigned(Tp / kTile), kDedupThreads, 0, table.p, out.p, d_count);
+  }
 }
 
 uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out) {

@@ -283,12 +283,21 @@ void dedup_keys_async(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& 
 // table is allocated for n_max and sized for *d_n by the kernels themselves.
 void dedup_keys_dev(Ctx& c, const uint64_t* keys, uint64_t n_max, const unsigned long long* d_n,
                     DBuf<uint64_t>& out, unsigned long long* d_count);
+// Above the L2-resident size: one radix pass splits the keys into 256
+// partitions on their low 8 bits (equal keys share every bit), then each
+// partition is deduplicated in its own L2-sized hash table; unique keys in
+// any order to out, their count to *d_count.
+void dedup_keys_partitioned(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out,
+                            unsigned long long* d_count);
 // Estimated duplicate fraction of a candidate set (keys of every 64th read).
 double estimate_dup_fraction(Ctx& c, const uint64_t* keys, uint64_t n, unsigned rshift);
 
 // radix_sort.cu -- stable LSD radix sort of u64 keys (+ optional u32 values)
 // on bits [begin_bit, end_bit). Sorted data ends up in keys/vals (buffers may
 // be swapped with the alternates).
+// One stable 8-bit digit pass (bits [shift, shift + 8)) of u64 keys from in
+// to out; digit d's keys land at [starts[d], starts[d+1]) (257 u32, device).
+void radix_digit_pass(Ctx& c, const uint64_t* in, uint64_t* out, uint64_t n, int shift, uint32_t* starts);
 void radix_sort(Ctx& c, DBuf<uint64_t>& keys, DBuf<uint64_t>& keys_alt, DBuf<uint32_t>* vals,
                 DBuf<uint32_t>* vals_alt, uint64_t n, int begin_bit, int end_bit);
 

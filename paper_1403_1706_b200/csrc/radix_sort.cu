@@ -118,7 +118,24 @@ __global__ void __launch_bounds__(kRadixThreads) k_downsweep(const uint64_t* __r
   }
 }
 
+__global__ void k_digit_starts(const uint32_t* __restrict__ hist, uint32_t n_tiles, uint64_t n,
+                               uint32_t* __restrict__ starts) {
+  const uint32_t d = threadIdx.x;
+  if (d < kBins) starts[d] = hist[uint64_t(d) * n_tiles];
+  if (d == 0) starts[kBins] = uint32_t(n);
+}
+
 }  // namespace
+
+void radix_digit_pass(Ctx& c, const uint64_t* in, uint64_t* out, uint64_t n, int shift, uint32_t* starts) {
+  if (n > 0xFFFFFFFFull) throw InputError("radix pass: more than 2^32-1 keys");
+  const uint32_t tiles = uint32_t(std::max<uint64_t>(ceil_div(n, kRadixTile), 1));
+  DBuf<uint32_t> hist(c, uint64_t(kBins) * tiles);
+  QGM_KERNEL(c, k_upsweep, tiles, kRadixThreads, 0, in, n, shift, hist.p, tiles);
+  exclusive_scan_u32(c, hist.p, hist.p, uint64_t(kBins) * tiles, nullptr, nullptr);
+  QGM_KERNEL(c, k_downsweep<false>, tiles, kRadixThreads, 0, in, nullptr, n, shift, hist.p, tiles, out, nullptr);
+  QGM_KERNEL(c, k_digit_starts, 1, kRadixThreads, 0, hist.p, tiles, n, starts);
+}
 
 void radix_sort(Ctx& c, DBuf<uint64_t>& keys, DBuf<uint64_t>& keys_alt, DBuf<uint32_t>* vals,
                 DBuf<uint32_t>* vals_alt, uint64_t n, int begin_bit, int end_bit) {
