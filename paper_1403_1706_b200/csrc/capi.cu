@@ -154,6 +154,7 @@ __device__ __forceinline__ uint2 to_planes(uint64_t w) { return make_uint2(compr
 
 __global__ void k_read_planes(const uint64_t* __restrict__ words, uint32_t n_reads, uint32_t W, uint32_t Wp,
                               uint2* __restrict__ planes) {
+  QGM_GRID_DEP();
   const uint64_t total = uint64_t(n_reads) * Wp;
   for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total; t += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t r = t / Wp;
@@ -165,6 +166,7 @@ __global__ void k_read_planes(const uint64_t* __restrict__ words, uint32_t n_rea
 // dense 2-bit stream (read r = bases [r*stride, (r+1)*stride)) -> W words per read
 __global__ void k_unpack_dense(const uint64_t* __restrict__ dense, uint32_t n_reads, uint32_t stride, uint32_t W,
                                uint64_t* __restrict__ words) {
+  QGM_GRID_DEP();
   const uint64_t total = uint64_t(n_reads) * W;
   for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total; t += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t r = t / W;
@@ -181,16 +183,19 @@ __global__ void k_unpack_dense(const uint64_t* __restrict__ dense, uint32_t n_re
 }
 
 __global__ void k_fill_u32(uint32_t* __restrict__ p, uint64_t n, uint32_t v) {
+  QGM_GRID_DEP();
   for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n; t += uint64_t(gridDim.x) * blockDim.x) p[t] = v;
 }
 
 __global__ void k_ref_planes(const uint64_t* __restrict__ words, uint64_t nw, uint2* __restrict__ planes) {
+  QGM_GRID_DEP();
   for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < nw; k += uint64_t(gridDim.x) * blockDim.x)
     planes[k + 2] = to_planes(words[k]);
 }
 
 // out[0] = max, out[1] = ~min (both folded with atomicMax; out zeroed)
 __global__ void k_minmax_u32(const uint32_t* __restrict__ v, uint64_t n, uint32_t* __restrict__ out) {
+  QGM_GRID_DEP();
   uint32_t m = 0, nm = 0;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     m = max(m, v[i]);
@@ -686,7 +691,7 @@ static int reads_common(qgm_ctx* ctx, const uint64_t* w, const uint32_t* len, ui
     r.words.alloc(c, nw + 2);  // 2 guard words: the partition bulk-copies whole 16-byte pairs
     r.lengths.alloc(c, std::max<uint32_t>(n_reads, 1));
     if (nw) QGM_CUDA(cudaMemcpyAsync(r.words.p, w, nw * 8, kind, c.stream));
-    QGM_CUDA(cudaMemsetAsync(r.words.p + nw, 0, 16, c.stream));
+    fill_bytes(c, r.words.p + nw, 0, 16);
     if (n_reads) QGM_CUDA(cudaMemcpyAsync(r.lengths.p, len, uint64_t(n_reads) * 4, kind, c.stream));
     qgm::finish_reads(c, r);
   });
@@ -829,7 +834,7 @@ int qgm_ref_upload(qgm_ctx* ctx, const uint64_t* ref2bit, const uint64_t* chrom_
     const uint64_t nw = qgm::ceil_div(r.total, 32);
     r.words.alloc(c, nw + 1);
     if (nw) QGM_CUDA(cudaMemcpyAsync(r.words.p, ref2bit, nw * 8, cudaMemcpyDefault, c.stream));  // host or device
-    QGM_CUDA(cudaMemsetAsync(r.words.p + nw, 0, 8, c.stream));
+    fill_bytes(c, r.words.p + nw, 0, 8);
     r.d_cb.alloc(c, n_chrom + 1);
     r.d_cbp.alloc(c, n_chrom + 1);
     QGM_CUDA(cudaMemcpyAsync(r.d_cb.p, r.cb.data(), (n_chrom + 1) * 8, cudaMemcpyHostToDevice, c.stream));
@@ -1250,7 +1255,7 @@ int qgm_map_host_batches(qgm_ctx* ctx, qgm_batch* batches, uint32_t n_batches, c
                                                        qgm::kSMs * 16));
         if (b.layout == QGM_READS_DENSE && r.n) {
           QGM_KERNEL(c, qgm::k_unpack_dense, g, 256, 0, s.dense.p, r.n, r.stride, r.W, s.words.p);
-          QGM_CUDA(cudaMemsetAsync(s.words.p + uint64_t(r.n) * r.W, 0, 16, c.stream));
+          fill_bytes(c, s.words.p + uint64_t(r.n) * r.W, 0, 16);
         }
         if (!b.lengths && r.n) QGM_KERNEL(c, qgm::k_fill_u32, g, 256, 0, s.lens.p, uint64_t(r.n), r.stride);
       }

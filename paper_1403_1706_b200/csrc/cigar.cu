@@ -156,6 +156,7 @@ __device__ __forceinline__ uint32_t bit_at(const T& x, unsigned t) {
 
 template <class T>
 __global__ void __launch_bounds__(128) k_cigar(CigarArgs a, T* __restrict__ rows_buf) {
+  QGM_GRID_DEP();
   const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned W = a.W, top = 2 * W;
   const T one = T(1);

@@ -30,6 +30,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 
 __global__ void k_hash_insert(const uint64_t* __restrict__ keys, uint64_t n, uint64_t* __restrict__ table,
                               uint64_t tmask) {
+  QGM_GRID_DEP();
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t key = keys[i];
     uint64_t slot = mix64(key) & tmask;
@@ -43,6 +44,7 @@ __global__ void k_hash_insert(const uint64_t* __restrict__ keys, uint64_t n, uin
 
 __global__ void __launch_bounds__(kDedupThreads) k_tile_count(const uint64_t* __restrict__ table, uint64_t T,
                                                               uint32_t* __restrict__ counts) {
+  QGM_GRID_DEP();
   __shared__ uint32_t ws[33];
   const uint64_t base = uint64_t(blockIdx.x) * kTile;
   uint32_t c = 0;
@@ -55,6 +57,7 @@ __global__ void __launch_bounds__(kDedupThreads) k_tile_count(const uint64_t* __
 __global__ void __launch_bounds__(kDedupThreads) k_tile_emit(const uint64_t* __restrict__ table,
                                                              const uint32_t* __restrict__ offs,
                                                              uint64_t* __restrict__ out) {
+  QGM_GRID_DEP();
   __shared__ uint32_t ws[33];
   const uint64_t base = uint64_t(blockIdx.x) * kTile;
   uint32_t run = offs[blockIdx.x];
@@ -75,6 +78,7 @@ template <bool kReset>  // kReset: leave the tile empty again (the next partitio
 __global__ void __launch_bounds__(kDedupThreads) k_tile_compact(uint64_t* __restrict__ table,
                                                                 uint64_t* __restrict__ out,
                                                                 unsigned long long* __restrict__ counter) {
+  QGM_GRID_DEP();
   __shared__ uint32_t ws[33];
   __shared__ unsigned long long s_base;
   constexpr int kPerThread = kTile / kDedupThreads;
@@ -112,6 +116,7 @@ __device__ __forceinline__ uint64_t dev_count(const unsigned long long* d_n, uin
 
 __global__ void k_table_clear(uint64_t* __restrict__ table, const unsigned long long* __restrict__ d_n,
                               uint64_t n_max) {
+  QGM_GRID_DEP();
   const uint64_t T = table_slots(dev_count(d_n, n_max));
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < T; i += uint64_t(gridDim.x) * blockDim.x)
     table[i] = kEmpty;
@@ -119,6 +124,7 @@ __global__ void k_table_clear(uint64_t* __restrict__ table, const unsigned long 
 
 __global__ void k_hash_insert_dev(const uint64_t* __restrict__ keys, const unsigned long long* __restrict__ d_n,
                                   uint64_t n_max, uint64_t* __restrict__ table) {
+  QGM_GRID_DEP();
   const uint64_t n = dev_count(d_n, n_max), tmask = table_slots(n) - 1;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t key = keys[i];
@@ -136,6 +142,7 @@ __global__ void __launch_bounds__(kDedupThreads) k_tile_compact_dev(const uint64
                                                                     const unsigned long long* __restrict__ d_n,
                                                                     uint64_t n_max, uint64_t* __restrict__ out,
                                                                     unsigned long long* __restrict__ counter) {
+  QGM_GRID_DEP();
   __shared__ uint32_t ws[33];
   __shared__ unsigned long long s_base;
   constexpr int kPerThread = kTile / kDedupThreads;
@@ -167,6 +174,7 @@ constexpr int kSamplePer = 16;
 __global__ void __launch_bounds__(256) k_sample_reads(const uint64_t* __restrict__ keys, uint64_t n, unsigned rshift,
                                                      uint64_t mask, uint64_t* __restrict__ out, uint64_t cap,
                                                      unsigned long long* __restrict__ n_out) {
+  QGM_GRID_DEP();
   __shared__ uint32_t ws[33];
   __shared__ unsigned long long s_base;
   const uint64_t tile = uint64_t(blockDim.x) * kSamplePer;
@@ -198,14 +206,14 @@ __global__ void __launch_bounds__(256) k_sample_reads(const uint64_t* __restrict
 
 void dedup_keys_async(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out, unsigned long long* d_count) {
   if (n == 0) {
-    QGM_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
+    fill_bytes(c, d_count, 0, sizeof(unsigned long long));
     if (out.n == 0) out.alloc(c, 1);
     return;
   }
   uint64_t T = kTile;
   while (T < n + n / 2) T <<= 1;  // load factor <= 2/3
   DBuf<uint64_t> table(c, T);
-  QGM_CUDA(cudaMemsetAsync(table.p, 0xFF, T * sizeof(uint64_t), c.stream));
+  fill_bytes(c, table.p, 0xFF, T * sizeof(uint64_t));
   {
     KernelScope ks(c, "k_hash_insert");
     const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
@@ -213,13 +221,13 @@ void dedup_keys_async(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& 
   }
   const uint32_t tiles = uint32_t(T / kTile);
   if (out.n < n) out.alloc(c, n);
-  QGM_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
+  fill_bytes(c, d_count, 0, sizeof(unsigned long long));
   QGM_KERNEL(c, k_tile_compact<false>, tiles, kDedupThreads, 0, table.p, out.p, d_count);
 }
 
 void dedup_keys_dev(Ctx& c, const uint64_t* keys, uint64_t n_max, const unsigned long long* d_n,
                     DBuf<uint64_t>& out, unsigned long long* d_count) {
-  QGM_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
+  fill_bytes(c, d_count, 0, sizeof(unsigned long long));
   if (out.n < std::max<uint64_t>(n_max, 1)) out.alloc(c, std::max<uint64_t>(n_max, 1));
   if (n_max == 0) return;
   const uint64_t T = table_slots(n_max);
@@ -236,7 +244,7 @@ void dedup_keys_dev(Ctx& c, const uint64_t* keys, uint64_t n_max, const unsigned
 
 void dedup_keys_partitioned(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& out,
                             unsigned long long* d_count) {
-  QGM_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
+  fill_bytes(c, d_count, 0, sizeof(unsigned long long));
   if (out.n < std::max<uint64_t>(n, 1)) out.alloc(c, std::max<uint64_t>(n, 1));
   if (n == 0) return;
   KernelScope ks(c, "k_hash_insert");
@@ -256,7 +264,7 @@ void dedup_keys_partitioned(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint6
   uint64_t T = kTile;
   while (T < most + most / 2) T <<= 1;
   DBuf<uint64_t> table(c, T);
-  QGM_CUDA(cudaMemsetAsync(table.p, 0xFF, T * sizeof(uint64_t), c.stream));  // once: each compaction resets its tiles
+  fill_bytes(c, table.p, 0xFF, T * sizeof(uint64_t));  // once: each compaction resets its tiles
   for (int d = 0; d < 256; d += span) {
     const uint64_t np = h[d + span] - h[d];
     if (np == 0) continue;
@@ -273,7 +281,7 @@ uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& ou
   uint64_t T = kTile;
   while (T < n + n / 2) T <<= 1;  // load factor <= 2/3: at C2 the table (64 MiB) stays L2-resident
   DBuf<uint64_t> table(c, T);
-  QGM_CUDA(cudaMemsetAsync(table.p, 0xFF, T * sizeof(uint64_t), c.stream));
+  fill_bytes(c, table.p, 0xFF, T * sizeof(uint64_t));
   {
     KernelScope ks(c, "k_hash_insert_sample");  // the dedup-skip estimate: not the batch's dedup
     const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));

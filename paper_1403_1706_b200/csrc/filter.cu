@@ -84,6 +84,7 @@ __device__ __forceinline__ bool index_pair(const FilterArgs& a, uint32_t g, uint
 
 template <class W, bool kSampled, bool kRunStart>
 __global__ void __launch_bounds__(kFilterThreads) k_filter(FilterArgs a) {
+  QGM_GRID_DEP();
   __shared__ uint32_t s_k0[kFilterWarps][64];
   __shared__ uint32_t s_pre[kFilterWarps][65];
   __shared__ uint64_t s_x[kFilterWarps][64];

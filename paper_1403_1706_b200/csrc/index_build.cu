@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_mask(const uint64_t* _
                                                                const uint32_t* __restrict__ boff, uint64_t buckets,
                                                                uint32_t lmask, uint64_t threshold, uint64_t c0,
                                                                unsigned long long* __restrict__ mask) {
+  QGM_GRID_DEP();
   extern __shared__ uint32_t cnt[];  // 2^lb counters
   for (uint64_t bk = blockIdx.x; bk < buckets; bk += gridDim.x) {
     for (uint32_t i = threadIdx.x; i <= lmask; i += blockDim.x) cnt[i] = 0;
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_mask(const uint64_t* _
 
 // Palindromic indexed positions (f == rc(f); even q only): count, then list.
 __global__ void k_pal_scan(RefSource src, uint64_t* __restrict__ out, unsigned long long* __restrict__ count) {
+  QGM_GRID_DEP();
   for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < src.L; base += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t x = base + threadIdx.x;
     uint32_t c;
@@ -180,6 +182,7 @@ __device__ __forceinline__ uint32_t item_glow(uint64_t pr) { return uint32_t(pr 
 template <class Src>
 __global__ void k_bucket_rank(Src src, uint64_t n_items, unsigned lb, uint32_t* __restrict__ bucket_cnt,
                               uint32_t* __restrict__ rank) {
+  QGM_GRID_DEP();
   for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < n_items; base += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t t = base + threadIdx.x;
     uint32_t g = 0, pos, extra, b = 0xFFFFFFFFu;
@@ -197,6 +200,7 @@ __global__ void k_bucket_rank(Src src, uint64_t n_items, unsigned lb, uint32_t* 
 template <class Src>
 __global__ void k_bucket_scatter(Src src, uint64_t n_items, unsigned lb, const uint32_t* __restrict__ boff,
                                  const uint32_t* __restrict__ rank, uint64_t* __restrict__ pairs) {
+  QGM_GRID_DEP();
   const uint32_t lmask = (1u << lb) - 1u;
   for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n_items;
        t += uint64_t(gridDim.x) * blockDim.x) {
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_occupy(const uint64_t*
                                                                  const uint32_t* __restrict__ boff,
                                                                  uint64_t buckets, uint32_t gpb,
                                                                  W* __restrict__ I, uint32_t* __restrict__ dcnt) {
+  QGM_GRID_DEP();
   using AW = typename std::conditional<sizeof(W) == 8, unsigned long long, unsigned>::type;
   constexpr unsigned w = GroupTraits<W>::width;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -246,6 +251,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* _
                                                                const W* __restrict__ I, uint32_t* __restrict__ S,
                                                                uint32_t* __restrict__ S1, uint32_t* __restrict__ O,
                                                                uint8_t* __restrict__ X) {
+  QGM_GRID_DEP();
   constexpr unsigned w = GroupTraits<W>::width;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   W* occ = reinterpret_cast<W*>(smem_raw);
@@ -290,9 +296,11 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* _
   }
 }
 
-__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
+__global__ void k_set_u32(uint32_t* p, uint32_t v) {
+  QGM_GRID_DEP(); *p = v; }
 
 __global__ void k_max_u32(const uint32_t* __restrict__ a, uint64_t n, uint32_t* __restrict__ out) {
+  QGM_GRID_DEP();
   uint32_t m = 0;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
     m = max(m, a[i]);
@@ -304,6 +312,7 @@ __global__ void k_max_u32(const uint32_t* __restrict__ a, uint64_t n, uint32_t* 
 // most 2^16 codes and this is an exclusive prefix)
 __global__ void k_rank16(const uint32_t* __restrict__ S, uint64_t groups, unsigned wshift,
                          const uint32_t* __restrict__ sb_d, uint16_t* __restrict__ r16) {
+  QGM_GRID_DEP();
   for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < groups; w += uint64_t(gridDim.x) * blockDim.x)
     r16[w] = uint16_t(S[w] - sb_d[w >> wshift]);
 }
@@ -312,6 +321,7 @@ __global__ void k_rank16(const uint32_t* __restrict__ S, uint64_t groups, unsign
 // range starts at S of its first word, its O range at S' of that
 __global__ void k_subbin_bounds(const uint32_t* __restrict__ S, const uint32_t* __restrict__ S1, uint32_t n_sub,
                                 unsigned cs, uint32_t* __restrict__ sb_d, uint32_t* __restrict__ sb_o) {
+  QGM_GRID_DEP();
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s <= n_sub; s += gridDim.x * blockDim.x) {
     const uint32_t d = S[uint32_t((uint64_t(s) << cs) >> 5)];
     sb_d[s] = d;
@@ -321,12 +331,14 @@ __global__ void k_subbin_bounds(const uint32_t* __restrict__ S, const uint32_t* 
 
 __global__ void k_sample_S(const uint32_t* __restrict__ S, uint64_t len_in, uint32_t* __restrict__ out,
                            uint64_t len_out) {
+  QGM_GRID_DEP();
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < len_out; i += uint64_t(gridDim.x) * blockDim.x)
     out[i] = S[2 * i];
 }
 
 // Thread per interval: insertion sort for short intervals, heap sort otherwise.
 __global__ void k_sort_intervals(const uint32_t* __restrict__ S1, uint64_t distinct, uint32_t* __restrict__ O) {
+  QGM_GRID_DEP();
   for (uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b < distinct; b += uint64_t(gridDim.x) * blockDim.x) {
     uint32_t* a = O + S1[b];
     const uint32_t n = S1[b + 1] - S1[b];
@@ -360,6 +372,7 @@ template <class W>
 __global__ void k_lookup(const W* __restrict__ I, const uint32_t* __restrict__ S, const uint32_t* __restrict__ S1,
                          bool sampled, const uint32_t* __restrict__ codes, uint64_t n, uint32_t* __restrict__ begin,
                          uint32_t* __restrict__ end) {
+  QGM_GRID_DEP();
   constexpr unsigned w = GroupTraits<W>::width;
   for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n; t += uint64_t(gridDim.x) * blockDim.x) {
     const uint32_t g = codes[t];
@@ -417,7 +430,7 @@ void finish_impl(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_
 
   const unsigned grid_b = unsigned(std::min<uint64_t>(B.buckets, uint64_t(kSMs) * 8));
   DBuf<uint32_t> dcnt(c, B.buckets + 1);
-  QGM_CUDA(cudaMemsetAsync(dcnt.p + B.buckets, 0, 4, c.stream));
+  fill_bytes(c, dcnt.p + B.buckets, 0, 4);
   {
     KernelScope ks(c, "k_bucket_occupy");
     QGM_KERNEL(c, (k_bucket_occupy<W, kG>), grid_b, kBuildThreads, B.gpb * sizeof(W), B.pairs.p, B.boff.p, B.buckets,

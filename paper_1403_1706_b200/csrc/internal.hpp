@@ -105,13 +105,46 @@ struct KernelScope {
   }
 };
 
-// Launch on the context stream, count it, surface launch errors.
+// Programmatic dependent launch. Every kernel of the library starts with
+// QGM_GRID_DEP(): wait until the grids it depends on have completed and
+// their writes are visible, then allow the next kernel of the stream to be
+// scheduled. Launched with programmatic stream serialization, a kernel's
+// CTAs are placed while its predecessor's last CTAs still run and start
+// the moment it completes, instead of the GPU draining at every boundary
+// (a batch is ~35 dependent launches; C1 is bound by those boundaries).
+// tests/test_capi_symbols.py checks that every __global__ begins with it.
+#define QGM_GRID_DEP() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+
+bool pdl_enabled();  // QGM_PDL=0: plain stream serialization (A/B)
+
+inline cudaLaunchConfig_t launch_config(Ctx& c, dim3 grid, dim3 block, size_t smem, cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cfg;
+}
+
+// Launch on the context stream (programmatic serialization), count it,
+// surface launch errors.
 #define QGM_KERNEL(ctx, kernel, grid, block, smem, ...)                          \
   do {                                                                         \
-    kernel<<<(grid), (block), (smem), (ctx).stream>>>(__VA_ARGS__);            \
+    cudaLaunchAttribute qgm_attr_[1];                                          \
+    const cudaLaunchConfig_t qgm_cfg_ =                                        \
+        ::qgm::launch_config((ctx), dim3(grid), dim3(block), size_t(smem), qgm_attr_); \
+    QGM_CUDA(cudaLaunchKernelEx(&qgm_cfg_, kernel, __VA_ARGS__));              \
     ++(ctx).launches;                                                          \
     QGM_LAUNCH_CHECK();                                                        \
   } while (0)
+
+// cudaMemsetAsync as a kernel of the stream: a memset node between two
+// kernels would end their programmatic overlap. value is a byte.
+void fill_bytes(Ctx& c, void* p, int value, size_t bytes);
 
 // --------------------------------------------------------------- memory
 // Device buffer from the context's block cache (Ctx::block_alloc).
@@ -149,7 +182,7 @@ struct DBuf {
   }
   size_t bytes() const { return n * sizeof(T); }
   void zero() {
-    if (n) QGM_CUDA(cudaMemsetAsync(p, 0, bytes(), ctx->stream));
+    if (n) fill_bytes(*ctx, p, 0, bytes());
   }
   void swap(DBuf& o) {
     std::swap(p, o.p); std::swap(n, o.n); std::swap(cls, o.cls); std::swap(ctx, o.ctx);

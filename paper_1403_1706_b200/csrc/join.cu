@@ -327,6 +327,7 @@ __device__ __forceinline__ void join_stats(const JoinArgs& a, WarpLists& L) {
 
 template <bool kRunStart, bool kPacked>
 __global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
+  QGM_GRID_DEP();
   // dynamic: I words [nw], u16 group starts [nw] (+pad to 16 B), S' slice
   // [cap], O slice [cap]
   extern __shared__ __align__(16) uint32_t s_dyn[];
@@ -464,6 +465,7 @@ struct StageMeta {
 
 template <bool kRunStart, bool kPacked>
 __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t stage_words, uint32_t icap) {
+  QGM_GRID_DEP();
   // 2 stages: I [nw] | u16 starts | S' [cap] | O [cap] | items [icap] (u64)
   extern __shared__ __align__(16) uint32_t s_dyn[];
   const uint32_t nw = a.words;
@@ -709,13 +711,15 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   ensure_dynamic_smem(reinterpret_cast<const void*>(kfn), size_t(smem));
   const unsigned grid = std::min<unsigned>(a.n_sub, resident_grid(kfn, threads, smem));
   for (int attempt = 0; attempt < 2; ++attempt) {
-    QGM_CUDA(cudaMemsetAsync(counter, 0, 3 * sizeof(unsigned long long), c.stream));
+    fill_bytes(c, counter, 0, 3 * sizeof(unsigned long long));
     a.out = keys.p;
     a.cap_out = keys.n;
     if (rp.V > 0) {
       KernelScope ks(c, "k_join");
       void* args[] = {&a, &stage_words, &icap};
-      QGM_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(threads), args, smem, c.stream));
+      cudaLaunchAttribute attr[1];
+      const cudaLaunchConfig_t cfg = launch_config(c, dim3(grid), dim3(threads), smem, attr);
+      QGM_CUDA(cudaLaunchKernelExC(&cfg, kfn, args));
       ++c.launches;
     }
     if (dev_counter) return 0;  // asynchronous: the caller reads the counts (and checks keys.n) later

@@ -155,6 +155,7 @@ constexpr int kHistThreads = 1024;
 template <int Q, int R, bool kRaw>
 __global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen<Q, kRaw> gen, uint32_t per_cta, unsigned kshift,
                                                                  uint32_t keys, uint32_t* __restrict__ hist) {
+  QGM_GRID_DEP();
   extern __shared__ uint32_t h2[];  // keys / 2 words (keys >= 2)
   const uint32_t words = (keys + 1) / 2;
   for (uint32_t i = threadIdx.x; i < words; i += kHistThreads) h2[i] = 0;
@@ -215,6 +216,7 @@ __global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen<Q, kRaw
 __global__ void k_bin_offsets(const uint32_t* __restrict__ soff, uint32_t nbins, unsigned sub,
                               uint32_t* __restrict__ boff, const uint32_t* __restrict__ lens, uint32_t stride,
                               uint32_t keys, uint32_t* __restrict__ flags) {
+  QGM_GRID_DEP();
   for (uint32_t b = threadIdx.x; b <= nbins; b += blockDim.x) boff[b] = soff[b << sub];
   if (threadIdx.x == 0) {
     flags[0] = soff[keys];
@@ -236,6 +238,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
                                                                   uint32_t* __restrict__ cursor,
                                                                   uint64_t* __restrict__ out, uint32_t sw_words,
                                                                   const uint32_t* __restrict__ lens) {
+  QGM_GRID_DEP();
   // kChunk items, bin-sorted | kChunk u8 bins | 2 x sw_words staged read words
   extern __shared__ __align__(16) uint64_t stage[];
   uint8_t* sbin = reinterpret_cast<uint8_t*>(stage + kChunk);
@@ -393,6 +396,7 @@ __device__ __forceinline__ uint32_t bin_search(const uint32_t* sboff, uint32_t n
 // a dependent load or a binary search
 __global__ void k_chunk_info(const uint64_t* __restrict__ in, const uint32_t* __restrict__ n_dev,
                              const uint32_t* __restrict__ boff, Refine rf, unsigned sub, uint4* __restrict__ info) {
+  QGM_GRID_DEP();
   const uint32_t n = *n_dev;
   const uint32_t n_chunks = (n + kP2Chunk - 1) / kP2Chunk;
   for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < n_chunks; ch += gridDim.x * blockDim.x) {
@@ -411,6 +415,7 @@ __global__ void __launch_bounds__(kP2Threads, kP2MinBlocks) k_refine_scatter(con
                                                                     uint32_t* __restrict__ cursor,
                                                                     const uint4* __restrict__ chunk_info,
                                                                     uint64_t* __restrict__ out) {
+  QGM_GRID_DEP();
   // dynamic: the chunk's items as loaded by TMA (kP2Chunk u64), the sorted
   // join items (kP2Chunk u64), their window keys (kP2Chunk u16)
   extern __shared__ __align__(16) uint64_t sdyn[];

@@ -27,6 +27,7 @@ __device__ __forceinline__ uint32_t digit_of(uint64_t k, int shift) { return uin
 
 __global__ void __launch_bounds__(kRadixThreads) k_upsweep(const uint64_t* __restrict__ keys, uint64_t n, int shift,
                                                            uint32_t* __restrict__ hist, uint32_t n_tiles) {
+  QGM_GRID_DEP();
   __shared__ uint32_t h[kBins];
   h[threadIdx.x] = 0;
   __syncthreads();
@@ -46,6 +47,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_downsweep(const uint64_t* __r
                                                              const uint32_t* __restrict__ offs, uint32_t n_tiles,
                                                              uint64_t* __restrict__ out_keys,
                                                              uint32_t* __restrict__ out_vals) {
+  QGM_GRID_DEP();
   __shared__ uint32_t wcnt[kRadixWarps][kBins];
   __shared__ uint32_t tile_off[kBins];
   __shared__ uint32_t glob_off[kBins];
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_downsweep(const uint64_t* __r
 
 __global__ void k_digit_starts(const uint32_t* __restrict__ hist, uint32_t n_tiles, uint64_t n,
                                uint32_t* __restrict__ starts) {
+  QGM_GRID_DEP();
   const uint32_t d = threadIdx.x;
   if (d < kBins) starts[d] = hist[uint64_t(d) * n_tiles];
   if (d == 0) starts[kBins] = uint32_t(n);

@@ -8,6 +8,8 @@
 // Up to 2^14 elements a single CTA scans tile after tile (k_scan_single).
 #include "internal.hpp"
 
+#include <cstdlib>
+
 namespace qgm {
 namespace {
 
@@ -19,6 +21,7 @@ __device__ __forceinline__ uint32_t pad_idx(uint32_t i) { return i + (i >> 5); }
 
 __global__ void __launch_bounds__(kScanThreads) k_tile_sums(const uint32_t* __restrict__ in, uint64_t n,
                                                             uint64_t* __restrict__ sums) {
+  QGM_GRID_DEP();
   __shared__ uint64_t ws[33];
   const uint64_t base = uint64_t(blockIdx.x) * kScanTile;
   uint64_t s = 0;
@@ -34,6 +37,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_sums(const uint32_t* __re
 
 __global__ void __launch_bounds__(1024) k_scan_sums(uint64_t* __restrict__ sums, uint64_t n_tiles,
                                                     uint32_t* __restrict__ d_total, int* __restrict__ d_overflow) {
+  QGM_GRID_DEP();
   __shared__ uint64_t ws[33];
   uint64_t carry = 0;
   for (uint64_t b = 0; b < n_tiles; b += blockDim.x) {
@@ -52,6 +56,7 @@ __global__ void __launch_bounds__(1024) k_scan_sums(uint64_t* __restrict__ sums,
 
 __global__ void __launch_bounds__(kScanThreads) k_tile_scan(const uint32_t* in, uint32_t* out, uint64_t n,
                                                             const uint64_t* __restrict__ sums) {
+  QGM_GRID_DEP();
   __shared__ uint32_t tile[kScanTile + kScanTile / 32];
   __shared__ uint64_t ws[33];
   const uint64_t base = uint64_t(blockIdx.x) * kScanTile;
@@ -92,6 +97,7 @@ constexpr uint64_t kSingleMax = uint64_t(1) << 14;  // 65537 elements: 32 us her
 __global__ void __launch_bounds__(kSingleThreads) k_scan_single(const uint32_t* in, uint32_t* out, uint64_t n,
                                                                 uint32_t* __restrict__ d_total,
                                                                 int* __restrict__ d_overflow) {
+  QGM_GRID_DEP();
   __shared__ uint32_t tile[kSingleTile + kSingleTile / 32];
   __shared__ uint64_t ws[33];
   uint64_t carry = 0;
@@ -133,6 +139,7 @@ __global__ void __launch_bounds__(kSingleThreads) k_scan_single(const uint32_t* 
 
 __global__ void k_select_flags(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ flags, uint64_t n,
                                uint32_t* __restrict__ f) {
+  QGM_GRID_DEP();
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
     f[i] = flags ? (flags[i] != 0) : (i == 0 || keys[i] != keys[i - 1]);
 }
@@ -140,6 +147,7 @@ __global__ void k_select_flags(const uint64_t* __restrict__ keys, const uint32_t
 __global__ void k_select_scatter(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                                  const uint32_t* __restrict__ flags, const uint32_t* __restrict__ pos, uint64_t n,
                                  uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals) {
+  QGM_GRID_DEP();
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     const bool sel = flags ? (flags[i] != 0) : (i == 0 || keys[i] != keys[i - 1]);
     if (sel) {
@@ -154,8 +162,8 @@ __global__ void k_select_scatter(const uint64_t* __restrict__ keys, const uint32
 void exclusive_scan_u32(Ctx& c, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* d_total,
                         int* d_overflow) {
   if (n == 0) {
-    if (d_total) QGM_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), c.stream));
-    if (d_overflow) QGM_CUDA(cudaMemsetAsync(d_overflow, 0, sizeof(int), c.stream));
+    if (d_total) fill_bytes(c, d_total, 0, sizeof(uint32_t));
+    if (d_overflow) fill_bytes(c, d_overflow, 0, sizeof(int));
     return;
   }
   if (n <= kSingleMax) {
@@ -182,6 +190,34 @@ uint64_t select_u64(Ctx& c, const uint64_t* keys, const uint32_t* vals, const ui
   QGM_CUDA(cudaMemcpyAsync(&h, total.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
   QGM_CUDA(cudaStreamSynchronize(c.stream));
   return h;
+}
+
+namespace {
+__global__ void __launch_bounds__(256) k_fill_bytes(uint8_t* __restrict__ p, uint32_t pattern, size_t bytes) {
+  QGM_GRID_DEP();
+  const size_t head = std::min<size_t>(bytes, (16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15);
+  const size_t body = (bytes - head) / 16, tail = head + body * 16;
+  const size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x, stride = size_t(gridDim.x) * blockDim.x;
+  if (t < head) p[t] = uint8_t(pattern);
+  if (t < bytes - tail) p[tail + t] = uint8_t(pattern);
+  uint4* q = reinterpret_cast<uint4*>(p + head);
+  const uint4 v = make_uint4(pattern, pattern, pattern, pattern);
+  for (size_t i = t; i < body; i += stride) q[i] = v;
+}
+}  // namespace
+
+void fill_bytes(Ctx& c, void* p, int value, size_t bytes) {
+  if (bytes == 0) return;
+  const unsigned grid = unsigned(std::min<size_t>(std::max<size_t>(ceil_div(bytes, size_t(16) * 256), 1), kSMs * 8));
+  QGM_KERNEL(c, k_fill_bytes, grid, 256, 0, static_cast<uint8_t*>(p), uint32_t(uint8_t(value)) * 0x01010101u, bytes);
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("QGM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 }  // namespace qgm

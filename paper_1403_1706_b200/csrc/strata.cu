@@ -28,6 +28,7 @@ namespace {
 __global__ void k_group_min(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t n,
                             unsigned diag_bits, uint32_t* __restrict__ readmin, uint32_t* __restrict__ first,
                             uint32_t* __restrict__ gmin) {
+  QGM_GRID_DEP();
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t k = keys[i];
     const bool f = i == 0 || keys[i - 1] != k;
@@ -43,6 +44,7 @@ __global__ void k_group_min(const uint64_t* __restrict__ keys, const uint32_t* _
 __global__ void k_keep(const uint64_t* __restrict__ keys, uint64_t n, unsigned diag_bits, int mode,
                        const uint32_t* __restrict__ readmin, const uint32_t* __restrict__ first,
                        const uint32_t* __restrict__ gmin, uint32_t* __restrict__ keep) {
+  QGM_GRID_DEP();
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
     keep[i] = first[i] && (mode == 1 || gmin[i] == readmin[keys[i] >> (diag_bits + 1)]);
 }
@@ -51,6 +53,7 @@ __global__ void k_emit(const uint64_t* __restrict__ keys, uint64_t n, unsigned d
                        const uint32_t* __restrict__ keep, const uint32_t* __restrict__ pos,
                        const uint32_t* __restrict__ gmin, const uint64_t* __restrict__ cbp, uint32_t n_chrom,
                        uint4* __restrict__ out) {
+  QGM_GRID_DEP();
   const uint64_t dmask = (uint64_t(1) << diag_bits) - 1;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     if (!keep[i]) continue;
@@ -75,8 +78,9 @@ __global__ void k_emit(const uint64_t* __restrict__ keys, uint64_t n, unsigned d
 __global__ void k_scatter_reads(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t n,
                                 unsigned rshift, const uint32_t* __restrict__ off, uint32_t* __restrict__ cnt,
                                 uint64_t* __restrict__ skeys, uint32_t* __restrict__ svals,
-                                const unsigned long long* __restrict__ n_dev = nullptr,
-                                const unsigned long long* __restrict__ big = nullptr) {
+                                const unsigned long long* __restrict__ n_dev,
+                                const unsigned long long* __restrict__ big) {
+  QGM_GRID_DEP();
   if (big && *big) return;
   if (n_dev) n = *n_dev;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -94,7 +98,8 @@ __global__ void k_scatter_reads(const uint64_t* __restrict__ keys, const uint32_
 // minima, the read's minimum, keep marks (value ~0u = dropped), kept count
 __global__ void k_seg_reduce(uint64_t* __restrict__ skeys, uint32_t* __restrict__ svals,
                              const uint32_t* __restrict__ off, uint32_t n_reads, int mode,
-                             uint32_t* __restrict__ kept, const unsigned long long* __restrict__ big = nullptr) {
+                             uint32_t* __restrict__ kept, const unsigned long long* __restrict__ big) {
+  QGM_GRID_DEP();
   if (big && *big) return;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_reads; r += gridDim.x * blockDim.x) {
     const uint32_t b = off[r], m = off[r + 1] - b;
@@ -141,7 +146,8 @@ __global__ void k_seg_reduce(uint64_t* __restrict__ skeys, uint32_t* __restrict_
 __global__ void k_seg_emit(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
                            const uint32_t* __restrict__ off, const uint32_t* __restrict__ kept_off, uint32_t n_reads,
                            unsigned diag_bits, const uint64_t* __restrict__ cbp, uint32_t n_chrom,
-                           uint4* __restrict__ out, const unsigned long long* __restrict__ big = nullptr) {
+                           uint4* __restrict__ out, const unsigned long long* __restrict__ big) {
+  QGM_GRID_DEP();
   if (big && *big) return;
   const uint64_t dmask = (uint64_t(1) << diag_bits) - 1;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_reads; r += gridDim.x * blockDim.x) {
@@ -168,6 +174,7 @@ __global__ void k_seg_emit(const uint64_t* __restrict__ skeys, const uint32_t* _
 // lower_bound(read << 16) in the sorted keys.
 __global__ void k_rank_keys(const uint4* __restrict__ hits, uint64_t n, uint64_t* __restrict__ keys,
                             uint32_t* __restrict__ idx) {
+  QGM_GRID_DEP();
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     const uint4 h = hits[i];
     keys[i] = (uint64_t(h.x) << 16) | (h.w & 0xFFFFu);
@@ -186,6 +193,7 @@ __device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* a, uint64_t 
 
 __global__ void k_ranks(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
                         uint32_t* __restrict__ rank) {
+  QGM_GRID_DEP();
   for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < n; j += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t k = keys[j];
     const uint64_t hi = lower_bound_u64(keys, n, k + 1), lo = lower_bound_u64(keys, n, (k >> 16) << 16);
@@ -200,6 +208,7 @@ __global__ void k_ranks(const uint64_t* __restrict__ keys, const uint32_t* __res
 constexpr uint32_t kRankRun = 64;
 __global__ void k_rank_runs(const uint4* __restrict__ hits, uint64_t n, uint32_t* __restrict__ rank,
                             unsigned int* __restrict__ long_run) {
+  QGM_GRID_DEP();
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     const uint4 h = __ldg(hits + i);
     const uint32_t e = h.w & 0xFFFFu;
@@ -265,8 +274,9 @@ uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBu
   exclusive_scan_u32(c, cnt.p, off.p, uint64_t(n_reads) + 1, nullptr, nullptr);
   DBuf<uint64_t> skeys(c, n);
   DBuf<uint32_t> svals(c, n);
-  QGM_KERNEL(c, k_scatter_reads, grid, 256, 0, hit_keys.p, hit_vals.p, n, rshift, off.p, cnt.p, skeys.p, svals.p);
-  QGM_KERNEL(c, k_seg_reduce, rgrid, 128, 0, skeys.p, svals.p, off.p, n_reads, mode, kept.p);
+  QGM_KERNEL(c, k_scatter_reads, grid, 256, 0, hit_keys.p, hit_vals.p, n, rshift, off.p, cnt.p, skeys.p, svals.p,
+             nullptr, nullptr);
+  QGM_KERNEL(c, k_seg_reduce, rgrid, 128, 0, skeys.p, svals.p, off.p, n_reads, mode, kept.p, nullptr);
   DBuf<uint32_t> kept_off(c, uint64_t(n_reads) + 1);
   exclusive_scan_u32(c, kept.p, kept_off.p, uint64_t(n_reads) + 1, total.p, nullptr);
   uint32_t nk = 0;
@@ -274,7 +284,7 @@ uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBu
   QGM_CUDA(cudaStreamSynchronize(c.stream));
   out.alloc(c, std::max<uint64_t>(uint64_t(nk) * 16, 16));
   QGM_KERNEL(c, k_seg_emit, rgrid, 128, 0, skeys.p, svals.p, off.p, kept_off.p, n_reads, ref.diag_bits, ref.d_cbp.p,
-             ref.n_chrom, reinterpret_cast<uint4*>(out.p));
+             ref.n_chrom, reinterpret_cast<uint4*>(out.p), nullptr);
   return nk;
 }
 
@@ -284,7 +294,7 @@ void stratify_unsorted_dev(Ctx& c, const Ref& ref, const uint64_t* hit_keys, con
                            uint32_t* d_kept) {
   out.alloc(c, std::max<uint64_t>(n_max * 16, 16));
   if (n_max == 0 || n_reads == 0) {
-    QGM_CUDA(cudaMemsetAsync(d_kept, 0, 4, c.stream));
+    fill_bytes(c, d_kept, 0, 4);
     return;
   }
   if (n_max > 0xFFFFFFFFull) throw InputError("strata: more than 2^32-1 hits");
@@ -314,7 +324,7 @@ uint64_t stratify_hits(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const u
     return 0;
   }
   DBuf<uint32_t> readmin(c, std::max<uint32_t>(n_reads, 1));
-  QGM_CUDA(cudaMemsetAsync(readmin.p, 0xFF, readmin.bytes(), c.stream));
+  fill_bytes(c, readmin.p, 0xFF, readmin.bytes());
   DBuf<uint32_t> first(c, n), gmin(c, n), keep(c, n), total(c, 1);
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
   QGM_KERNEL(c, k_group_min, grid, 256, 0, hit_keys, hit_vals, n, ref.diag_bits, readmin.p, first.p, gmin.p);

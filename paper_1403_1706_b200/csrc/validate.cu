@@ -275,6 +275,7 @@ __device__ __forceinline__ void unpack_state(const Parked& p, T& Pv, T& Mv) {
 template <class T, int kPhase>
 __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t r_split, Parked* __restrict__ park,
                                                           unsigned long long* __restrict__ n_park, uint64_t park_cap) {
+  QGM_GRID_DEP();
   const T mask = a.B >= sizeof(T) * 8 ? T(~T(0)) : T((T(1) << a.B) - 1);
   const uint64_t dmask = (uint64_t(1) << a.diag_bits) - 1;
   const uint64_t total = kPhase == 2 ? min(uint64_t(*n_park), park_cap) : (a.d_n ? *a.d_n : a.n);

@@ -39,6 +39,20 @@ def test_library_is_built_for_sm_100a():
 
 
 @pytest.mark.skipif(HAS_GPU, reason="checks the no-device error path")
+def test_every_kernel_begins_with_the_grid_dependency_wait():
+    """Kernels are launched with programmatic stream serialization (PDL), so a
+    kernel may start before its predecessor finishes; each must begin with
+    QGM_GRID_DEP() (griddepcontrol.wait) before touching memory."""
+    import glob
+    kernels = 0
+    for f in glob.glob(os.path.join(ROOT, "paper_1403_1706_b200", "csrc", "*.cu")):
+        text = open(f).read()
+        for m in re.finditer(r"__global__[^;{]*?\b(k_\w+)\s*\([^;{]*\)\s*\{\s*(\S+)", text, re.S):
+            kernels += 1
+            assert m.group(2).startswith("QGM_GRID_DEP()"), (os.path.basename(f), m.group(1))
+    assert kernels >= 50
+
+
 def test_no_device_is_a_loud_error_not_a_fallback():
     import paper_1403_1706_b200 as qgm
     with pytest.raises(qgm.QgmError):
