@@ -268,7 +268,7 @@ static void check_reads_shape(uint32_t n_reads, uint32_t stride) {
 // validation, measured within noise of each other).
 constexpr uint64_t kDedupDirectMax = uint64_t(10) << 20;  // raw keys whose hash table (<= 16M slots) stays L2-resident
 
-static int hook_point() {  // experiment knob: 0 after the join, 1 after dedup, 2 after validation
+static int hook_point() {  // experiment knob: 0 after the join, 1 after dedup, 2 after validation, 3 first
   static const int h = [] {
     const char* e = std::getenv("QGM_HOOK");
     return e ? std::atoi(e) : 1;
@@ -293,6 +293,7 @@ static uint64_t dedup_direct_max() {
 static bool map_reads_async(Ctx& c, const Reads& reads, const Ref& ref, const qgm_map_params& P, int strands,
                             unsigned rb, uint64_t cap, const std::function<void()>& after_filter, HitsObj& out) {
   prepare_ref_index(c, ref, P.q);
+  if (after_filter && hook_point() == 3) after_filter();
   Partitioned rbk;
   {
     StageScope s(c, kStageIndex);

@@ -325,8 +325,11 @@ __device__ __forceinline__ void join_stats(const JoinArgs& a, WarpLists& L) {
   }
 }
 
+#ifndef QGM_JOIN_MINB
+#define QGM_JOIN_MINB 4  // CTAs per SM the register budget of k_join is sized for
+#endif
 template <bool kRunStart, bool kPacked>
-__global__ void __launch_bounds__(kJoinThreads, 4) k_join(JoinArgs a) {
+__global__ void __launch_bounds__(kJoinThreads, QGM_JOIN_MINB) k_join(JoinArgs a) {
   QGM_GRID_DEP();
   // dynamic: I words [nw], u16 group starts [nw] (+pad to 16 B), S' slice
   // [cap], O slice [cap]
