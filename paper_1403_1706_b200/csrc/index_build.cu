@@ -210,7 +210,39 @@ __global__ void k_bucket_scatter(Src src, uint64_t n_items, unsigned lb, const u
   }
 }
 
-template <class W, int kG>
+// Items of one bucket held in registers: the first kItemRegs * kBuildThreads
+// are loaded together (all in flight at once -- the bucket kernels are bound
+// by the latency of these loads, not by bandwidth), the rest, if any, by a
+// plain loop.
+#ifndef QGM_IB_ITEMS
+#define QGM_IB_ITEMS 6
+#endif
+#ifndef QGM_IB_MINB
+#define QGM_IB_MINB 6
+#endif
+constexpr int kItemRegs = QGM_IB_ITEMS;
+
+// kPer > 0: gpb == kPer * kBuildThreads, thread t owns the contiguous group
+// words [t * kPer, (t + 1) * kPer) (16-byte vector accesses, popcounts
+// prefix-summed in registers); kPer == 0: any gpb, strided loops.
+template <class W, int kPer>
+struct GroupRun {
+  W x[kPer > 0 ? kPer : 1];
+  __device__ __forceinline__ void load(const W* __restrict__ src) {
+    static_assert(kPer == 0 || (kPer * sizeof(W)) % 16 == 0, "whole 16-byte vectors per thread");
+#pragma unroll
+    for (int v = 0; v < int(kPer * sizeof(W) / 16); ++v) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(src) + v);
+      reinterpret_cast<uint4*>(x)[v] = q;
+    }
+  }
+  __device__ __forceinline__ void store(W* dst) const {
+#pragma unroll
+    for (int v = 0; v < int(kPer * sizeof(W) / 16); ++v) reinterpret_cast<uint4*>(dst)[v] = reinterpret_cast<const uint4*>(x)[v];
+  }
+};
+
+template <class W, int kG, int kPer>
 __global__ void __launch_bounds__(kBuildThreads) k_bucket_occupy(const uint64_t* __restrict__ pairs,
                                                                  const uint32_t* __restrict__ boff,
                                                                  uint64_t buckets, uint32_t gpb,
@@ -222,19 +254,43 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_occupy(const uint64_t*
   W* occ = reinterpret_cast<W*>(smem_raw);
   __shared__ uint32_t ws[33];
   for (uint64_t bk = blockIdx.x; bk < buckets; bk += gridDim.x) {
+    const uint32_t b0 = boff[bk], b1 = boff[bk + 1];
+    uint64_t pr[kItemRegs];
+#pragma unroll
+    for (int u = 0; u < kItemRegs; ++u) {
+      const uint32_t i = b0 + threadIdx.x + u * kBuildThreads;
+      pr[u] = i < b1 ? pairs[i] : 0;
+    }
     for (uint32_t i = threadIdx.x; i < gpb; i += blockDim.x) occ[i] = W(0);
     __syncthreads();
-    const uint32_t b0 = boff[bk], b1 = boff[bk + 1];
-    for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+#pragma unroll
+    for (int u = 0; u < kItemRegs; ++u) {
+      const uint32_t i = b0 + threadIdx.x + u * kBuildThreads;
+      if (i < b1) {
+        const uint32_t gl = item_glow<kG>(pr[u]);
+        atomicOr(reinterpret_cast<AW*>(occ + gl / w), AW(W(1) << (gl % w)));
+      }
+    }
+    for (uint32_t i = b0 + threadIdx.x + kItemRegs * kBuildThreads; i < b1; i += blockDim.x) {
       const uint32_t gl = item_glow<kG>(pairs[i]);
       atomicOr(reinterpret_cast<AW*>(occ + gl / w), AW(W(1) << (gl % w)));
     }
     __syncthreads();
     uint32_t pc = 0;
-    for (uint32_t i = threadIdx.x; i < gpb; i += blockDim.x) {
-      const W x = occ[i];
-      I[bk * gpb + i] = x;
-      pc += GroupTraits<W>::popc(x);
+    if constexpr (kPer > 0) {
+      GroupRun<W, kPer> g;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        g.x[u] = occ[threadIdx.x * kPer + u];
+        pc += GroupTraits<W>::popc(g.x[u]);
+      }
+      g.store(I + bk * gpb + uint64_t(threadIdx.x) * kPer);
+    } else {
+      for (uint32_t i = threadIdx.x; i < gpb; i += blockDim.x) {
+        const W x = occ[i];
+        I[bk * gpb + i] = x;
+        pc += GroupTraits<W>::popc(x);
+      }
     }
     uint32_t tot;
     block_exclusive_scan<uint32_t>(pc, ws, &tot);
@@ -243,8 +299,8 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_occupy(const uint64_t*
   }
 }
 
-template <class W, bool kSampled, bool kExtra, int kG>
-__global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* __restrict__ pairs,
+template <class W, bool kSampled, bool kExtra, int kG, int kPer>
+__global__ void __launch_bounds__(kBuildThreads, QGM_IB_MINB) k_bucket_emit(const uint64_t* __restrict__ pairs,
                                                                const uint32_t* __restrict__ boff,
                                                                const uint32_t* __restrict__ dbase,
                                                                uint64_t buckets, uint32_t gpb,
@@ -259,39 +315,86 @@ __global__ void __launch_bounds__(kBuildThreads) k_bucket_emit(const uint64_t* _
   uint32_t* cnt = sloc + gpb;  // up to gpb*w counters
   __shared__ uint32_t ws[33];
   for (uint64_t bk = blockIdx.x; bk < buckets; bk += gridDim.x) {
-    for (uint32_t i = threadIdx.x; i < gpb; i += blockDim.x) {
-      const W x = I[bk * gpb + i];
-      occ[i] = x;
-      sloc[i] = GroupTraits<W>::popc(x);
-    }
-    __syncthreads();
-    const uint32_t D = block_scan_smem(sloc, gpb, ws);
+    const uint32_t b0 = boff[bk], b1 = boff[bk + 1];
     const uint32_t db = dbase[bk];
-    for (uint32_t i = threadIdx.x; i < gpb; i += blockDim.x) {
-      const uint64_t gi = bk * gpb + i;
-      if (!kSampled) S[gi] = db + sloc[i];
-      else if ((gi & 1) == 0) S[gi >> 1] = db + sloc[i];
+    // the bucket's items, kept in registers for both passes below
+    uint64_t pr[kItemRegs];
+#pragma unroll
+    for (int u = 0; u < kItemRegs; ++u) {
+      const uint32_t i = b0 + threadIdx.x + u * kBuildThreads;
+      pr[u] = i < b1 ? pairs[i] : 0;
+    }
+    uint32_t D;
+    if constexpr (kPer > 0) {
+      const uint32_t g0 = threadIdx.x * kPer;
+      GroupRun<W, kPer> g;
+      g.load(I + bk * gpb + g0);
+      uint32_t ex[kPer], sum = 0;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        ex[u] = sum;
+        sum += GroupTraits<W>::popc(g.x[u]);
+      }
+      const uint32_t run = block_exclusive_scan<uint32_t>(sum, ws, &D);
+      g.store(occ + g0);
+      if constexpr (kPer % 4 == 0) {  // the thread's group starts as whole 16-byte vectors
+#pragma unroll
+        for (int v = 0; v < kPer / 4; ++v) {
+          const uint4 loc = make_uint4(run + ex[4 * v], run + ex[4 * v + 1], run + ex[4 * v + 2], run + ex[4 * v + 3]);
+          reinterpret_cast<uint4*>(sloc + g0)[v] = loc;
+          if (!kSampled)
+            reinterpret_cast<uint4*>(S + bk * gpb + g0)[v] = make_uint4(db + loc.x, db + loc.y, db + loc.z, db + loc.w);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          sloc[g0 + u] = run + ex[u];
+          if (!kSampled) S[bk * gpb + g0 + u] = db + run + ex[u];
+        }
+      }
+      if (kSampled) {
+#pragma unroll
+        for (int u = 0; u < kPer; u += 2) S[(bk * gpb + g0 + u) >> 1] = db + run + ex[u];  // g0 + u even
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < gpb; i += blockDim.x) {
+        const W x = I[bk * gpb + i];
+        occ[i] = x;
+        sloc[i] = GroupTraits<W>::popc(x);
+      }
+      __syncthreads();
+      D = block_scan_smem(sloc, gpb, ws);
+      for (uint32_t i = threadIdx.x; i < gpb; i += blockDim.x) {
+        const uint64_t gi = bk * gpb + i;
+        if (!kSampled) S[gi] = db + sloc[i];
+        else if ((gi & 1) == 0) S[gi >> 1] = db + sloc[i];
+      }
     }
     for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
-    const uint32_t b0 = boff[bk], b1 = boff[bk + 1];
-    for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-      const uint32_t gl = item_glow<kG>(pairs[i]);
+    auto counter = [&](uint64_t p) {
+      const uint32_t gl = item_glow<kG>(p);
       const uint32_t wi = gl / w;
-      atomicAdd(cnt + sloc[wi] + rank_below<W>(occ[wi], gl % w), 1u);
-    }
+      return cnt + sloc[wi] + rank_below<W>(occ[wi], gl % w);
+    };
+#pragma unroll
+    for (int u = 0; u < kItemRegs; ++u)
+      if (b0 + threadIdx.x + u * kBuildThreads < b1) atomicAdd(counter(pr[u]), 1u);
+    for (uint32_t i = b0 + threadIdx.x + kItemRegs * kBuildThreads; i < b1; i += blockDim.x)
+      atomicAdd(counter(pairs[i]), 1u);
     __syncthreads();
     block_scan_smem(cnt, D, ws);
     for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) S1[db + i] = b0 + cnt[i];
     __syncthreads();
-    for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-      const uint64_t pr = pairs[i];
-      const uint32_t gl = item_glow<kG>(pr);
-      const uint32_t wi = gl / w;
-      const uint32_t slot = atomicAdd(cnt + sloc[wi] + rank_below<W>(occ[wi], gl % w), 1u);
-      O[b0 + slot] = uint32_t(pr);
-      if (kExtra) X[b0 + slot] = uint8_t(pr >> 48);
-    }
+    auto place = [&](uint64_t p) {
+      const uint32_t slot = atomicAdd(counter(p), 1u);
+      O[b0 + slot] = uint32_t(p);
+      if (kExtra) X[b0 + slot] = uint8_t(p >> 48);
+    };
+#pragma unroll
+    for (int u = 0; u < kItemRegs; ++u)
+      if (b0 + threadIdx.x + u * kBuildThreads < b1) place(pr[u]);
+    for (uint32_t i = b0 + threadIdx.x + kItemRegs * kBuildThreads; i < b1; i += blockDim.x) place(pairs[i]);
     __syncthreads();
   }
 }
@@ -431,10 +534,18 @@ void finish_impl(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_
   const unsigned grid_b = unsigned(std::min<uint64_t>(B.buckets, uint64_t(kSMs) * 8));
   DBuf<uint32_t> dcnt(c, B.buckets + 1);
   fill_bytes(c, dcnt.p + B.buckets, 0, 4);
+  // group words per thread of the vectorised bucket kernels (0: strided)
+  const int per = B.gpb * sizeof(W) == size_t(kBuildThreads) * 32 ? int(32 / sizeof(W))
+                  : B.gpb * sizeof(W) == size_t(kBuildThreads) * 16 ? int(16 / sizeof(W)) : 0;
   {
     KernelScope ks(c, "k_bucket_occupy");
-    QGM_KERNEL(c, (k_bucket_occupy<W, kG>), grid_b, kBuildThreads, B.gpb * sizeof(W), B.pairs.p, B.boff.p, B.buckets,
-               uint32_t(B.gpb), reinterpret_cast<W*>(out.I.p), dcnt.p);
+    auto occupy = [&](auto kernel) {
+      QGM_KERNEL(c, kernel, grid_b, kBuildThreads, B.gpb * sizeof(W), B.pairs.p, B.boff.p, B.buckets,
+                 uint32_t(B.gpb), reinterpret_cast<W*>(out.I.p), dcnt.p);
+    };
+    if (per == int(32 / sizeof(W))) occupy(k_bucket_occupy<W, kG, int(32 / sizeof(W))>);
+    else if (per == int(16 / sizeof(W))) occupy(k_bucket_occupy<W, kG, int(16 / sizeof(W))>);
+    else occupy(k_bucket_occupy<W, kG, 0>);
   }
   DBuf<uint32_t> dbase(c, B.buckets + 1);
   DBuf<uint32_t> dtotal(c, 2);  // total distinct codes, largest bucket's distinct count
@@ -459,12 +570,18 @@ void finish_impl(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_
     QGM_KERNEL(c, kernel, grid_b, kBuildThreads, smem, B.pairs.p, B.boff.p, dbase.p, B.buckets, uint32_t(B.gpb),
                reinterpret_cast<const W*>(out.I.p), out.S.p, out.S1.p, out.O.p, extra ? extra->p : nullptr);
   };
+  auto by_per = [&](auto kSampled, auto kExtra) {
+    constexpr bool S_ = decltype(kSampled)::value, E_ = decltype(kExtra)::value;
+    if (per == int(32 / sizeof(W))) launch(k_bucket_emit<W, S_, E_, kG, int(32 / sizeof(W))>);
+    else if (per == int(16 / sizeof(W))) launch(k_bucket_emit<W, S_, E_, kG, int(16 / sizeof(W))>);
+    else launch(k_bucket_emit<W, S_, E_, kG, 0>);
+  };
   if (sampled) {
-    if (extra) launch(k_bucket_emit<W, true, true, kG>);
-    else launch(k_bucket_emit<W, true, false, kG>);
+    if (extra) by_per(std::true_type{}, std::true_type{});
+    else by_per(std::true_type{}, std::false_type{});
   } else {
-    if (extra) launch(k_bucket_emit<W, false, true, kG>);
-    else launch(k_bucket_emit<W, false, false, kG>);
+    if (extra) by_per(std::false_type{}, std::true_type{});
+    else by_per(std::false_type{}, std::false_type{});
   }
   // sentinels: S[groups] = D (kept by sampling iff groups is even), S'[D] = V
   if (!sampled) QGM_KERNEL(c, k_set_u32, 1, 1, 0, out.S.p + B.groups, D);
