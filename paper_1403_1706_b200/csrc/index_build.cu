@@ -35,7 +35,6 @@ namespace {
 
 constexpr unsigned kLowBits = 13;  // codes per bucket = 8192
 constexpr int kBuildThreads = 256;
-constexpr uint64_t kLowMask = (1u << kLowBits) - 1;
 constexpr size_t kMaxBuildSmem = 200 * 1024;  // dynamic shared memory of one emit CTA
 struct BuildRetry {};                         // a bucket geometry the emit cannot stage
 
