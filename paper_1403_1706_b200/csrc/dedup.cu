@@ -9,6 +9,8 @@
 // (radix_sort.cu), which cost ~0.5 ms on C2's 5.2M keys; here: one memset,
 // one insert pass (8 B read + one CAS per key) and two streaming passes over
 // the table.
+#include <cstdlib>
+
 #include "internal.hpp"
 
 namespace qgm {
@@ -17,7 +19,7 @@ namespace {
 constexpr uint64_t kEmpty = ~0ull;  // never a key (the padded diagonal field is < 2^diag_bits - 1)
 constexpr int kTile = 4096;         // table slots per compaction tile
 constexpr int kDedupThreads = 256;
-constexpr uint64_t kPartKeys = uint64_t(4) << 20;  // keys per partition of dedup_keys_partitioned
+constexpr uint64_t kPartKeys = uint64_t(2) << 20;  // keys per partition of dedup_keys_partitioned (at most)
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x ^= x >> 33;
@@ -257,8 +259,11 @@ void dedup_keys_partitioned(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint6
   // 256 / span partitions of consecutive digits, ~kPartKeys keys each (a
   // table of <= 2^23 slots, 64 MB, stays in the 126 MB L2); fewer, larger
   // partitions when the set is smaller (each costs two launches)
+  uint64_t part_keys = kPartKeys;
+  const char* e = std::getenv("QGM_DEDUP_PART_KEYS");  // test knob: smaller partitions
+  if (e && e[0]) part_keys = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
   int span = 256;
-  while (span > 1 && n / (256 / span) > kPartKeys / 2) span >>= 1;
+  while (span > 1 && n / (256 / span) > part_keys) span >>= 1;
   uint64_t most = 0;
   for (int d = 0; d < 256; d += span) most = std::max<uint64_t>(most, h[d + span] - h[d]);
   uint64_t T = kTile;

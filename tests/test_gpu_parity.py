@@ -592,6 +592,9 @@ def test_large_candidate_sets_skip_the_dedup_only_when_it_cannot_pay(ctx, oracle
     oracle's either way."""
     import paper_1403_1706_b200 as qgm
     monkeypatch.setenv("QGM_DEDUP_DIRECT_MAX", "1000")
+    # kept dedup of a large set: one radix pass into partitions, each hashed
+    # in the reused L2-sized table (here forced to 256 partitions)
+    monkeypatch.setenv("QGM_DEDUP_PART_KEYS", "64")
     for rep, seed, q in ((False, 91, 10), (True, 92, 12)):
         L = 300_000
         ref = qgm.repetitive_reference(seed, L) if rep else qgm.random_reference(seed, L)
