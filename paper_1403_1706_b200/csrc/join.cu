@@ -96,13 +96,13 @@ struct JoinArgs {
 // matches). xp = the occurrence's padded coordinate; the item is returned
 // with its fr bit replaced by the candidate's strand. Op: O, or the
 // shared-memory slice of a staged sub-bin (generic pointer).
-template <bool kRunStart, bool kPacked>
+template <bool kRunStart, bool kPacked, bool kBoth>
 __device__ __forceinline__ bool match(const JoinArgs& a, const uint32_t* Op, uint32_t k, uint64_t& it, uint32_t& xp) {
   const uint32_t ov = Op[k];
   xp = kPacked ? (ov & kPosMask) : ov;
   const uint32_t ex = kPacked ? (ov >> kPackedPosBits) : uint32_t(__ldg(a.X + k));
   const uint32_t rev = ((ex >> 3) ^ uint32_t(it >> kItemFrShift)) & 1u;
-  if (!((a.strands >> rev) & 1)) return false;
+  if (!kBoth && !((a.strands >> rev) & 1)) return false;  // kBoth: both strands requested
   if (kRunStart) {
     const uint32_t rbase = uint32_t(it >> (rev ? kItemRbShift : kItemFbShift)) & 7u;
     if ((ex & 7u) == rbase && rbase < 4) return false;
@@ -234,7 +234,7 @@ __device__ __forceinline__ void skip_ranges(const uint32_t* Op, uint32_t lk0, ui
 // the staged occupancy words / group starts, expand the occurrence intervals
 // (S1p / Op / Ip: global arrays, or generic pointers into the staged slices), emit
 // the candidate keys.
-template <bool kRunStart, bool kPacked, int kItems>
+template <bool kRunStart, bool kPacked, bool kBoth, int kItems>
 __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI, const uint16_t* sR,
                                            const uint32_t* S1p, const uint32_t* Op, const uint64_t* Ip, uint32_t d0,
                                            uint32_t w0, uint32_t gsub, uint32_t my_lo, uint32_t my_hi,
@@ -318,7 +318,7 @@ __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI
       for (uint32_t t = 0; t < rounds; ++t) {
         uint64_t mit = it;
         uint32_t xp = 0;
-        const bool emit = t < nin && match<kRunStart, kPacked>(a, Op, k0 + t, mit, xp);
+        const bool emit = t < nin && match<kRunStart, kPacked, kBoth>(a, Op, k0 + t, mit, xp);
         stage(emit, mit, xp);
       }
       unsigned lm = __ballot_sync(kFull, longi);
@@ -347,7 +347,7 @@ __device__ __forceinline__ void join_items(const JoinArgs& a, const uint32_t* sI
           for (uint32_t t0 = lk0; t0 < lk0 + llen; t0 += 32) {
             uint64_t mit = lit;
             uint32_t xp = 0;
-            const bool emit = t0 + lane < lk0 + llen && match<kRunStart, kPacked>(a, Op, t0 + lane, mit, xp);
+            const bool emit = t0 + lane < lk0 + llen && match<kRunStart, kPacked, kBoth>(a, Op, t0 + lane, mit, xp);
             stage(emit, mit, xp);
           }
         }
@@ -369,7 +369,7 @@ __device__ __forceinline__ void join_stats(const JoinArgs& a, WarpLists& L) {
 #ifndef QGM_JOIN_MINB
 #define QGM_JOIN_MINB 4  // CTAs per SM the register budget of k_join is sized for
 #endif
-template <bool kRunStart, bool kPacked>
+template <bool kRunStart, bool kPacked, bool kBoth>
 __global__ void __launch_bounds__(kJoinThreads, QGM_JOIN_MINB) k_join(JoinArgs a) {
   QGM_GRID_DEP();
   // dynamic: I words [nw], u16 group starts [nw] (+pad to 16 B), S' slice
@@ -480,10 +480,10 @@ __global__ void __launch_bounds__(kJoinThreads, QGM_JOIN_MINB) k_join(JoinArgs a
     const uint32_t my_lo = b0 + uint32_t(uint64_t(nitems) * wid / kJoinWarps);
     const uint32_t my_hi = b0 + uint32_t(uint64_t(nitems) * (wid + 1) / kJoinWarps);
     if (staged) {  // S'/O accesses from shared-derived pointers only: LDS
-      join_items<kRunStart, kPacked, kItemsJoin>(a, sI, sR, sS1 - sA, sO - oA, a.items, d0, w0, sb << a.code_shift,
+      join_items<kRunStart, kPacked, kBoth, kItemsJoin>(a, sI, sR, sS1 - sA, sO - oA, a.items, d0, w0, sb << a.code_shift,
                                         my_lo, my_hi, L);
     } else {
-      join_items<kRunStart, kPacked, kItemsJoin>(a, sI, sR, a.S1, a.O, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi,
+      join_items<kRunStart, kPacked, kBoth, kItemsJoin>(a, sI, sR, a.S1, a.O, a.items, d0, w0, sb << a.code_shift, my_lo, my_hi,
                                         L);
     }
     __syncthreads();  // the staging buffers are rewritten for the next sub-bin
@@ -507,7 +507,7 @@ struct StageMeta {
   uint32_t sb, b0, b1, d0, sA, oA, iA, staged, items_staged, end;
 };
 
-template <bool kRunStart, bool kPacked>
+template <bool kRunStart, bool kPacked, bool kBoth>
 __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t stage_words, uint32_t icap) {
   QGM_GRID_DEP();
   // 2 stages: I [nw] | u16 starts | S' [cap] | O [cap] | items [icap] (u64)
@@ -639,13 +639,13 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_join_ws(JoinArgs a, uint32_t 
       // everything in shared memory: pointers derived from the shared
       // buffers only, so every access compiles to LDS (no generic LD and its
       // 64-bit address arithmetic)
-      join_items<kRunStart, kPacked, kItemsWs>(a, sI, sR, sS1 - M.sA, sO - M.oA, sIt - M.iA, M.d0, w0,
+      join_items<kRunStart, kPacked, kBoth, kItemsWs>(a, sI, sR, sS1 - M.sA, sO - M.oA, sIt - M.iA, M.d0, w0,
                                         M.sb << a.code_shift, my_lo, my_hi, L);
     } else {
       const uint32_t* S1p = M.staged ? sS1 - M.sA : a.S1;
       const uint32_t* Op = M.staged ? sO - M.oA : a.O;
       const uint64_t* Ip = M.items_staged ? sIt - M.iA : a.items;
-      join_items<kRunStart, kPacked, kItemsWs>(a, sI, sR, S1p, Op, Ip, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
+      join_items<kRunStart, kPacked, kBoth, kItemsWs>(a, sI, sR, S1p, Op, Ip, M.d0, w0, M.sb << a.code_shift, my_lo, my_hi, L);
     }
     // one arrive per consumer thread (not lane 0 after a __syncwarp): each
     // thread's own reads of meta[s] and the staged slices are then ordered
@@ -713,13 +713,20 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
   const bool stageable = X.packed && X.sb_d.p && X.sub_bits == rp.sub_bits;
   const char* ws_env = std::getenv("QGM_JOIN_WS");
   const bool use_ws = ws_env && ws_env[0] ? ws_env[0] == '1' : (stageable && per_sub >= 256 && per_sub <= 2048);
-  const void* kfn;
-  if (use_ws)
-    kfn = X.packed ? (rs ? (const void*)k_join_ws<true, true> : (const void*)k_join_ws<false, true>)
-                   : (rs ? (const void*)k_join_ws<true, false> : (const void*)k_join_ws<false, false>);
-  else
-    kfn = X.packed ? (rs ? (const void*)k_join<true, true> : (const void*)k_join<false, true>)
-                   : (rs ? (const void*)k_join<true, false> : (const void*)k_join<false, false>);
+  // kernel variant: warp-specialised or not, run-start rule, packed O,
+  // both strands requested (no per-occurrence strand test)
+  static const void* const kWs[8] = {
+      (const void*)k_join_ws<false, false, false>, (const void*)k_join_ws<false, false, true>,
+      (const void*)k_join_ws<false, true, false>,  (const void*)k_join_ws<false, true, true>,
+      (const void*)k_join_ws<true, false, false>,  (const void*)k_join_ws<true, false, true>,
+      (const void*)k_join_ws<true, true, false>,   (const void*)k_join_ws<true, true, true>};
+  static const void* const kPlain[8] = {
+      (const void*)k_join<false, false, false>, (const void*)k_join<false, false, true>,
+      (const void*)k_join<false, true, false>,  (const void*)k_join<false, true, true>,
+      (const void*)k_join<true, false, false>,  (const void*)k_join<true, false, true>,
+      (const void*)k_join<true, true, false>,   (const void*)k_join<true, true, true>};
+  const int variant = (rs ? 4 : 0) | (X.packed ? 2 : 0) | (strands == 3 ? 1 : 0);
+  const void* kfn = use_ws ? kWs[variant] : kPlain[variant];
   const int threads = use_ws ? kWsThreads : kJoinThreads;
   const int per_sm = use_ws ? 2 : 4;     // resident CTAs the staging is sized for
   const int stages = use_ws ? 2 : 1;
