@@ -372,8 +372,12 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
   const int strands = P.strands ? int(P.strands) : 3;
   if (P.group_width && P.group_width != 32 && P.group_width != 64) throw InputError("group width must be 32 or 64");
   if (ref.padded_total < (uint64_t(1) << 32)) {
-    uint64_t cap = std::max<uint64_t>(std::max<uint64_t>(1 << 20, uint64_t(reads.n) * 16),
-                                      c.last_raw_candidates + c.last_raw_candidates / 8);
+    // candidate capacity: 1.25x the context's last batch once there is one
+    // (a larger count re-maps the batch through the round-trip path), else
+    // 16 per read
+    uint64_t cap = c.last_raw_candidates ? c.last_raw_candidates + c.last_raw_candidates / 4
+                                         : uint64_t(reads.n) * 16;
+    cap = std::max<uint64_t>(cap, 1 << 20);
     const char* ce = std::getenv("QGM_MAP_ASYNC_CAP");  // tests
     if (ce && ce[0]) cap = std::max<uint64_t>(1, std::strtoull(ce, nullptr, 10));
     const char* ae = std::getenv("QGM_MAP_ASYNC");  // A/B and test knob: 0 = always the round-trip path
