@@ -205,9 +205,26 @@ __global__ void k_minmax_u32(const uint32_t* __restrict__ v, uint64_t n, uint32_
     m = max(m, __shfl_xor_sync(kFull, m, o));
     nm = max(nm, __shfl_xor_sync(kFull, nm, o));
   }
+  // one atomic pair per CTA (per warp, ~5k same-address atomics cost ~10 us
+  // for a 1M-read batch)
+  __shared__ uint32_t s_m[32], s_nm[32];
+  const unsigned wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (lane_id() == 0) {
-    atomicMax(out, m);
-    atomicMax(out + 1, nm);
+    s_m[wid] = m;
+    s_nm[wid] = nm;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    m = lane_id() < nw ? s_m[lane_id()] : 0u;
+    nm = lane_id() < nw ? s_nm[lane_id()] : 0u;
+    for (int o = 16; o > 0; o >>= 1) {
+      m = max(m, __shfl_xor_sync(kFull, m, o));
+      nm = max(nm, __shfl_xor_sync(kFull, nm, o));
+    }
+    if (lane_id() == 0) {
+      atomicMax(out, m);
+      atomicMax(out + 1, nm);
+    }
   }
 }
 
