@@ -26,7 +26,7 @@ job's reads do not depend on how many ranks map them.
             algorithmic bytes per launch / launch time,
             against MEASURED_PEAKS.json; `traffic` = ncu DRAM bytes of that
             kernel from profiles/<round>/ncu_<config>.json when it was captured
-            from this exact library build (sha256 stamp), else null.
+            from a build of these exact sources and flags (`build_stamp`), else null.
 * parity  : rank 0's first batch checked against the CPU path (reference
             build_qgroup_index + restated stages 2-5) in a SUBPROCESS (the GPU
             process never maps oracle/ code): digest of the sorted hit set of
@@ -139,8 +139,7 @@ def load_peaks():
 
 def lib_sha():
     import paper_1403_1706_b200 as qgm
-    with open(qgm.LIB_PATH, "rb") as f:
-        return hashlib.sha256(f.read()).hexdigest()[:16]
+    return qgm.build_stamp()  # sources + flags (nvcc output is not byte-reproducible)
 
 
 def cpu_info():
@@ -266,9 +265,10 @@ def validate_ops(cfg, st):
 
 
 def load_ncu(config, sha):
-    """ncu DRAM bytes / instruction counts per kernel captured from this exact
-    library build (tools/ncu_capture.py writes profiles/<round>/ncu_<config>.json
-    with the library's sha256 stamp); {} when absent or stale."""
+    """ncu DRAM bytes / instruction counts per kernel captured from a build of
+    these exact sources (tools/ncu_capture.py writes
+    profiles/<round>/ncu_<config>.json with the library's build stamp); {}
+    when absent or stale."""
     import glob
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_{config}.json")), reverse=True):
         d = json.load(open(p))

@@ -119,6 +119,28 @@ def _ptr(a):
     return a.ctypes.data_as(C.c_void_p) if a is not None else None
 
 
+def build_stamp() -> str:
+    """Identity of the library build for matching ncu evidence to it: the
+    sha256 of its CUDA sources and the Makefile (compiler flags) -- nvcc's
+    output is not byte-reproducible across rebuilds of the same sources. A
+    QGM_LIB override (an experiment build) is stamped by its bytes."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    if os.environ.get("QGM_LIB"):
+        with open(LIB_PATH, "rb") as f:
+            h.update(f.read())
+        return h.hexdigest()[:16]
+    root = os.path.dirname(_HERE)
+    files = sorted(glob.glob(os.path.join(_HERE, "csrc", "*.cu")) + glob.glob(os.path.join(_HERE, "csrc", "*.cuh")) +
+                   glob.glob(os.path.join(_HERE, "csrc", "*.hpp")) + [os.path.join(root, "Makefile")])
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def load_library(path: str = LIB_PATH):
     """Load libqgm_b200.so and declare the C ABI. Raises if it is missing."""
     global _lib

@@ -10,10 +10,10 @@
 
 bench.py uses `kernels.<name>.dram_bytes` as roofline.traffic and
 `kernels.k_validate.warp_inst` for the validation issue rate only when
-`lib_sha` equals the sha256 of the libqgm_b200.so it runs.
+`lib_sha` equals the build stamp (sha256 of the CUDA sources and Makefile)
+of the library it runs.
 """
 import csv
-import hashlib
 import io
 import json
 import os
@@ -88,8 +88,7 @@ def parse(config, csv_path, out_dir):
     for k in kern.values():
         k["launches"] = len(k["launches"])
         k["ncu_names"] = sorted(k["ncu_names"])
-    with open(qgm.LIB_PATH, "rb") as f:
-        sha = hashlib.sha256(f.read()).hexdigest()[:16]
+    sha = qgm.build_stamp()
     os.makedirs(out_dir, exist_ok=True)
     out = {"config": config, "lib_sha": sha, "what": "one map of the config's first batch under ncu "
            "(--clock-control none; per-kernel sums over the launches of that map)", "kernels": kern}
