@@ -355,11 +355,22 @@ __global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t r_
       }
     }
     if (finish) {
+      // k = min over the band row, tbest = the last diagonal attaining it
+      // (the smallest start); unrolled with constant shifts when the band
+      // fills the word
       int v = score0, best = score0;
       unsigned tbest = 0;
-      for (unsigned t = 1; t < a.B; ++t) {
-        v += int((Pv >> t) & T(1)) - int((Mv >> t) & T(1));
-        if (v <= best) { best = v; tbest = t; }
+      if (a.B == sizeof(T) * 8) {
+#pragma unroll
+        for (unsigned t = 1; t < sizeof(T) * 8; ++t) {
+          v += int((Pv >> t) & T(1)) - int((Mv >> t) & T(1));
+          if (v <= best) { best = v; tbest = t; }
+        }
+      } else {
+        for (unsigned t = 1; t < a.B; ++t) {
+          v += int((Pv >> t) & T(1)) - int((Mv >> t) & T(1));
+          if (v <= best) { best = v; tbest = t; }
+        }
       }
       k = best;
       start = a.B - 1 - tbest;
