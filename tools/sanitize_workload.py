@@ -3,7 +3,8 @@
 Reaches every kernel variant of the map path at sizes the sanitizers finish
 in minutes: plain and warp-specialised join, packed and unpacked reference
 index, the P0 u16 counter hand-off, parked two-phase validation (and its
-overflow branch), the sampled dedup decision, the strata radix path (reads
+overflow branch), the sampled dedup decision, the partitioned dedup, the
+strata radix path (reads
 with > 32 hits), hit ranks, CIGARs, streamed batches and the standalone
 filter / validate / index entry points. Every map is checked against the CPU
 oracle (test infrastructure), so a hazard that changes a result fails here too.
@@ -66,6 +67,18 @@ def main():
     os.environ["QGM_VAL_PARK_CAP"] = ""
     os.environ["QGM_VAL_SPLIT"] = ""
     os.environ["QGM_DEDUP_DIRECT_MAX"] = ""
+
+    # kept dedup of a large repetitive candidate set through the partitioned
+    # path: one radix pass, 256 partitions, the reused table reset by each
+    # compaction
+    os.environ["QGM_DEDUP_DIRECT_MAX"] = "1000"
+    os.environ["QGM_DEDUP_PART_KEYS"] = "64"
+    rref = qgm.repetitive_reference(92, 300_000)
+    rcb = np.array([0, 300_000], np.uint64)
+    rcodes, rlengths, *_ = qgm.simulate_reads(93, rref, rcb, 4000, 100, 0.03)
+    run(ctx, orc, "partitioned dedup", rref, rcb, rcodes, rlengths, 100, q=12, mode=1)
+    os.environ["QGM_DEDUP_DIRECT_MAX"] = ""
+    os.environ["QGM_DEDUP_PART_KEYS"] = ""
 
     # unpacked reference index (O without packed extra bits)
     os.environ["QGM_REF_UNPACKED"] = "1"
