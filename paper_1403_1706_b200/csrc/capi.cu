@@ -347,11 +347,8 @@ static bool map_reads_async(Ctx& c, const Reads& reads, const Ref& ref, const qg
     stratify_unsorted_dev(c, ref, hkeys.p, hvals.p, cnt.p, cap, reads.n, int(P.mode), per_read, cnt.p + 2, out.hits,
                           kept_total.p);
     // the batch's one host round trip
-    QGM_CUDA(cudaMemcpyAsync(jh, jc.p, sizeof(jh), cudaMemcpyDeviceToHost, c.stream));
-    QGM_CUDA(cudaMemcpyAsync(fl, rbk.flags.p, sizeof(fl), cudaMemcpyDeviceToHost, c.stream));
-    QGM_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-    QGM_CUDA(cudaMemcpyAsync(&kept, kept_total.p, 4, cudaMemcpyDeviceToHost, c.stream));
-    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    read_back(c, {{jc.p, jh, sizeof(jh)}, {rbk.flags.p, fl, sizeof(fl)}, {cnt.p, h, sizeof(h)},
+                  {kept_total.p, &kept, 4}});
   }
   if (fl[2]) throw InputError("read longer than the stride");
   c.last_raw_candidates = jh[0];
@@ -499,9 +496,10 @@ static HitsObj map_reads(Ctx& c, const Reads& reads, const Ref& ref, const qgm_m
                             out.hits, kept_total.p);
     unsigned long long h[3] = {0, 0, 0};
     uint32_t kept = 0;
-    QGM_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-    if (speculative) QGM_CUDA(cudaMemcpyAsync(&kept, kept_total.p, 4, cudaMemcpyDeviceToHost, c.stream));
-    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    if (speculative)
+      read_back(c, {{cnt.p, h, sizeof(h)}, {kept_total.p, &kept, 4}});
+    else
+      read_back(c, {{cnt.p, h, sizeof(h)}});
     n_val = h[0];
     n_u = h[1];
     big = h[2] != 0;
@@ -606,6 +604,7 @@ void qgm_ctx_destroy(qgm_ctx* ctx) {
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   ctx->c.block_trim();
+  if (ctx->c.tail_h) cudaFreeHost(ctx->c.tail_h);
   for (auto& m : ctx->c.marks) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
   for (auto e : ctx->c.ev_pool) cudaEventDestroy(e);
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);

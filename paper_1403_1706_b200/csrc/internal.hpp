@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <initializer_list>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -39,6 +40,8 @@ struct Ctx {
     if (planes_ev) cudaStreamWaitEvent(stream, planes_ev, 0);
   }
   uint64_t last_raw_candidates = 0;    // sizes the next batch's candidate buffer
+  uint32_t* tail_h = nullptr;          // mapped pinned page of read_back (host / device view)
+  uint32_t* tail_d = nullptr;
   std::string err;
   uint64_t launches = 0;
   bool profile = false;
@@ -145,6 +148,19 @@ inline cudaLaunchConfig_t launch_config(Ctx& c, dim3 grid, dim3 block, size_t sm
 // cudaMemsetAsync as a kernel of the stream: a memset node between two
 // kernels would end their programmatic overlap. value is a byte.
 void fill_bytes(Ctx& c, void* p, int value, size_t bytes);
+
+// Small device counters to host variables: one gather kernel into the
+// context's mapped pinned page and one stream synchronisation (instead of a
+// pageable cudaMemcpyAsync per counter, each a blocking round trip, and a
+// copy node that ends the programmatic overlap of the kernels before it).
+struct ReadSeg {
+  const void* src;  // device, 4-byte aligned
+  void* dst;        // host
+  size_t bytes;     // multiple of 4
+};
+constexpr int kMaxReadSegs = 8;
+constexpr size_t kReadBackBytes = 256;
+void read_back(Ctx& c, std::initializer_list<ReadSeg> segs);
 
 // --------------------------------------------------------------- memory
 // Device buffer from the context's block cache (Ctx::block_alloc).

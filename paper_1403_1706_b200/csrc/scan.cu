@@ -9,6 +9,8 @@
 #include "internal.hpp"
 
 #include <cstdlib>
+#include <cstring>
+#include <stdexcept>
 
 namespace qgm {
 namespace {
@@ -205,6 +207,46 @@ __global__ void __launch_bounds__(256) k_fill_bytes(uint8_t* __restrict__ p, uin
   for (size_t i = t; i < body; i += stride) q[i] = v;
 }
 }  // namespace
+
+namespace {
+struct ReadSegs {
+  const uint32_t* src[kMaxReadSegs];
+  uint32_t words[kMaxReadSegs];
+  int n;
+};
+// gathers small device counters into the context's mapped pinned page
+__global__ void k_read_back(ReadSegs s, uint32_t* __restrict__ out) {
+  QGM_GRID_DEP();
+  uint32_t o = 0;
+  for (int k = 0; k < s.n; ++k) {
+    for (uint32_t i = threadIdx.x; i < s.words[k]; i += blockDim.x) out[o + i] = s.src[k][i];
+    o += s.words[k];
+  }
+}
+}  // namespace
+
+void read_back(Ctx& c, std::initializer_list<ReadSeg> segs) {
+  if (!c.tail_h) {
+    QGM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c.tail_h), kReadBackBytes, cudaHostAllocMapped));
+    QGM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.tail_d), c.tail_h, 0));
+  }
+  ReadSegs s{};
+  size_t total = 0;
+  for (const ReadSeg& g : segs) {
+    if (s.n == kMaxReadSegs || g.bytes % 4 || total + g.bytes > kReadBackBytes)
+      throw std::logic_error("read_back: too many or unaligned segments");
+    s.src[s.n] = static_cast<const uint32_t*>(g.src);
+    s.words[s.n++] = uint32_t(g.bytes / 4);
+    total += g.bytes;
+  }
+  QGM_KERNEL(c, k_read_back, 1, 32, 0, s, c.tail_d);
+  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  const uint8_t* h = reinterpret_cast<const uint8_t*>(c.tail_h);
+  for (const ReadSeg& g : segs) {
+    std::memcpy(g.dst, h, g.bytes);
+    h += g.bytes;
+  }
+}
 
 void fill_bytes(Ctx& c, void* p, int value, size_t bytes) {
   if (bytes == 0) return;
