@@ -425,8 +425,7 @@ void hits_cigar(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, const Reads& read
   else
     QGM_KERNEL(c, k_cigar<uint64_t>, unsigned(blocks), threads, 0, a, reinterpret_cast<uint64_t*>(scratch.p));
   unsigned int h_bad = 0;
-  QGM_CUDA(cudaMemcpyAsync(&h_bad, bad.p, 4, cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  read_back(c, {{bad.p, &h_bad, 4}});
   if (h_bad & 1u) throw InputError("cigar: a hit's read or chromosome is not in the given reads / reference");
   if (h_bad & 2u) throw InputError("cigar: a read is longer than the reads' stride");
   if (h_bad & 4u) throw InternalError("cigar: traceback left the band");

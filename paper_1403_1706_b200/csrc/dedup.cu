@@ -254,8 +254,7 @@ void dedup_keys_partitioned(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint6
   DBuf<uint32_t> starts(c, 257);
   radix_digit_pass(c, keys, part.p, n, 0, starts.p);
   std::vector<uint32_t> h(257);
-  QGM_CUDA(cudaMemcpyAsync(h.data(), starts.p, 257 * 4, cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  read_back(c, {{starts.p, h.data(), 257 * 4}});
   // 256 / span partitions of consecutive digits, ~kPartKeys keys each (a
   // table of <= 2^23 slots, 64 MB, stays in the 126 MB L2); fewer, larger
   // partitions when the set is smaller (each costs two launches)
@@ -297,8 +296,7 @@ uint64_t dedup_keys(Ctx& c, const uint64_t* keys, uint64_t n, DBuf<uint64_t>& ou
   QGM_KERNEL(c, k_tile_count, tiles, kDedupThreads, 0, table.p, T, counts.p);
   exclusive_scan_u32(c, counts.p, counts.p, tiles, total.p, nullptr);
   uint32_t h = 0;
-  QGM_CUDA(cudaMemcpyAsync(&h, total.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  read_back(c, {{total.p, &h, sizeof(h)}});
   if (out.n < h) out.alloc(c, std::max<uint64_t>(h, 1));
   QGM_KERNEL(c, k_tile_emit, tiles, kDedupThreads, 0, table.p, counts.p, out.p);
   return h;
@@ -317,8 +315,7 @@ double estimate_dup_fraction(Ctx& c, const uint64_t* keys, uint64_t n, unsigned 
   QGM_KERNEL(c, k_sample_reads, unsigned(std::min<uint64_t>(ceil_div(n, 256 * kSamplePer), uint64_t(kSMs) * 8)), 256,
              0, keys, n, rshift, 63ull, sample.p, cap, ns.p);
   unsigned long long m = 0;
-  QGM_CUDA(cudaMemcpyAsync(&m, ns.p, sizeof(m), cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  read_back(c, {{ns.p, &m, sizeof(m)}});
   if (m == 0 || m > cap) return 1.0;  // no usable sample: assume duplicates (keep the dedup)
   DBuf<uint64_t> uniq;
   const uint64_t u = dedup_keys(c, sample.p, m, uniq);

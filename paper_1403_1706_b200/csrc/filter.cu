@@ -258,8 +258,7 @@ uint64_t filter_reference(Ctx& c, const Index& idx, const Reads& reads, const Re
       }
     }
     unsigned long long h[3] = {0, 0, 0};
-    QGM_CUDA(cudaMemcpyAsync(h, counter.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    read_back(c, {{counter.p, h, sizeof(h)}});
     if (fstats) {
       fstats[0] = h[1];
       fstats[1] = h[2];

@@ -507,8 +507,7 @@ void bucket_impl(Ctx& c, const Src& src, uint64_t n_items, Buckets& B) {
   DBuf<uint32_t> vtotal(c, 1);
   exclusive_scan_u32(c, bucket_cnt.p, B.boff.p, B.buckets + 1, vtotal.p, nullptr);
   uint32_t V = 0;
-  QGM_CUDA(cudaMemcpyAsync(&V, vtotal.p, 4, cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  read_back(c, {{vtotal.p, &V, 4}});
   B.V = V;
   B.pairs.alloc(c, std::max<uint64_t>(V, 1));
   if (n_items) {
@@ -553,8 +552,7 @@ void finish_impl(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf<uint8_
   QGM_KERNEL(c, k_max_u32, unsigned(std::min<uint64_t>(ceil_div(B.buckets, 256), uint64_t(kSMs) * 4)), 256, 0,
              dcnt.p, B.buckets, dtotal.p + 1);
   uint32_t Dm[2] = {0, 0};
-  QGM_CUDA(cudaMemcpyAsync(Dm, dtotal.p, 8, cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  read_back(c, {{dtotal.p, Dm, 8}});
   const uint32_t D = Dm[0];
   out.distinct = D;
   out.S1.alloc(c, uint64_t(D) + 1);
@@ -638,8 +636,7 @@ void bucket_ref(Ctx& c, const Ref& ref, unsigned q, bool packed, Buckets& out, u
     cnt.zero();
     const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(ref.total, 256), kSMs * 32));
     QGM_KERNEL(c, k_pal_scan, grid, 256, 0, src, nullptr, cnt.p);
-    QGM_CUDA(cudaMemcpyAsync(&np, cnt.p, sizeof(np), cudaMemcpyDeviceToHost, c.stream));
-    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    read_back(c, {{cnt.p, &np, sizeof(np)}});
     if (np) {
       pal.alloc(c, np);
       cnt.zero();
@@ -690,8 +687,7 @@ void index_from_buckets(Ctx& c, const Buckets& B, bool sampled, Index& out, DBuf
 void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sampled, Index& out) {
   if (reads.lens.p) {  // the upload's length check (qgm_reads_upload does not synchronise)
     uint32_t lens[2] = {0, 0};
-    QGM_CUDA(cudaMemcpyAsync(lens, reads.lens.p, 8, cudaMemcpyDeviceToHost, c.stream));
-    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    read_back(c, {{reads.lens.p, lens, 8}});
     if (lens[0] > reads.stride) throw InputError("read longer than the stride");
   }
   // buckets of 2^16 codes when that leaves ~8k q-grams per bucket or fewer
@@ -710,8 +706,7 @@ void build_index(Ctx& c, const Reads& reads, unsigned q, unsigned w, bool sample
       Partitioned rp;
       partition_reads(c, reads, q, rp, /*raw=*/true, /*force_key_bits=*/2 * q - B.lb);
       uint32_t fl[4] = {0, 0, 0, 0};
-      QGM_CUDA(cudaMemcpyAsync(fl, rp.flags.p, sizeof(fl), cudaMemcpyDeviceToHost, c.stream));
-      QGM_CUDA(cudaStreamSynchronize(c.stream));
+      read_back(c, {{rp.flags.p, fl, sizeof(fl)}});
       B.V = fl[0];
       B.boff.swap(rp.soff);
       B.pairs.swap(rp.pairs);

@@ -159,7 +159,7 @@ struct ReadSeg {
   size_t bytes;     // multiple of 4
 };
 constexpr int kMaxReadSegs = 8;
-constexpr size_t kReadBackBytes = 256;
+constexpr size_t kReadBackBytes = 4096;
 void read_back(Ctx& c, std::initializer_list<ReadSeg> segs);
 
 // --------------------------------------------------------------- memory

@@ -779,8 +779,7 @@ uint64_t join_filter(Ctx& c, const Partitioned& rp, const Reads& reads, const Re
     unsigned long long h[3] = {0, 0, 0};
     uint32_t fl[4] = {0, 0, 0, 0};
     QGM_CUDA(cudaMemcpyAsync(h, counter, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-    QGM_CUDA(cudaMemcpyAsync(fl, rp.flags.p, sizeof(fl), cudaMemcpyDeviceToHost, c.stream));
-    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    read_back(c, {{rp.flags.p, fl, sizeof(fl)}});
     if (fl[2]) throw InputError("read longer than the stride");
     if (fstats) {
       fstats[0] = h[1];

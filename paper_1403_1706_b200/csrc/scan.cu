@@ -189,8 +189,7 @@ uint64_t select_u64(Ctx& c, const uint64_t* keys, const uint32_t* vals, const ui
   exclusive_scan_u32(c, f.p, f.p, n, total.p, nullptr);
   QGM_KERNEL(c, k_select_scatter, grid, 256, 0, keys, vals, flags, f.p, n, out_keys, out_vals);
   uint32_t h = 0;
-  QGM_CUDA(cudaMemcpyAsync(&h, total.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  read_back(c, {{total.p, &h, sizeof(h)}});
   return h;
 }
 
@@ -239,7 +238,7 @@ void read_back(Ctx& c, std::initializer_list<ReadSeg> segs) {
     s.words[s.n++] = uint32_t(g.bytes / 4);
     total += g.bytes;
   }
-  QGM_KERNEL(c, k_read_back, 1, 32, 0, s, c.tail_d);
+  QGM_KERNEL(c, k_read_back, 1, 256, 0, s, c.tail_d);
   QGM_CUDA(cudaStreamSynchronize(c.stream));
   const uint8_t* h = reinterpret_cast<const uint8_t*>(c.tail_h);
   for (const ReadSeg& g : segs) {

@@ -237,8 +237,7 @@ void hit_ranks(Ctx& c, const DBuf<uint8_t>& hits, uint64_t n, uint32_t n_reads, 
     const unsigned g = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
     QGM_KERNEL(c, k_rank_runs, g, 256, 0, reinterpret_cast<const uint4*>(hits.p), n, rank.p, long_run.p);
     unsigned int h_long = 0;
-    QGM_CUDA(cudaMemcpyAsync(&h_long, long_run.p, 4, cudaMemcpyDeviceToHost, c.stream));
-    QGM_CUDA(cudaStreamSynchronize(c.stream));
+    read_back(c, {{long_run.p, &h_long, 4}});
     if (!h_long) return;
   }
   // a read with more than kRankRun records: sort (read, edits) keys
@@ -280,8 +279,7 @@ uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBu
   DBuf<uint32_t> kept_off(c, uint64_t(n_reads) + 1);
   exclusive_scan_u32(c, kept.p, kept_off.p, uint64_t(n_reads) + 1, total.p, nullptr);
   uint32_t nk = 0;
-  QGM_CUDA(cudaMemcpyAsync(&nk, total.p, 4, cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  read_back(c, {{total.p, &nk, 4}});
   out.alloc(c, std::max<uint64_t>(uint64_t(nk) * 16, 16));
   QGM_KERNEL(c, k_seg_emit, rgrid, 128, 0, skeys.p, svals.p, off.p, kept_off.p, n_reads, ref.diag_bits, ref.d_cbp.p,
              ref.n_chrom, reinterpret_cast<uint4*>(out.p), nullptr);
@@ -331,8 +329,7 @@ uint64_t stratify_hits(Ctx& c, const Ref& ref, const uint64_t* hit_keys, const u
   QGM_KERNEL(c, k_keep, grid, 256, 0, hit_keys, n, ref.diag_bits, mode, readmin.p, first.p, gmin.p, keep.p);
   exclusive_scan_u32(c, keep.p, first.p, n, total.p, nullptr);  // first <- output slots
   uint32_t kept = 0;
-  QGM_CUDA(cudaMemcpyAsync(&kept, total.p, 4, cudaMemcpyDeviceToHost, c.stream));
-  QGM_CUDA(cudaStreamSynchronize(c.stream));
+  read_back(c, {{total.p, &kept, 4}});
   out.alloc(c, std::max<uint64_t>(uint64_t(kept) * 16, 16));
   QGM_KERNEL(c, k_emit, grid, 256, 0, hit_keys, n, ref.diag_bits, keep.p, first.p, gmin.p, ref.d_cbp.p, ref.n_chrom,
              reinterpret_cast<uint4*>(out.p));
