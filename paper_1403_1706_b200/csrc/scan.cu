@@ -5,7 +5,7 @@
 // Reduce-then-scan over 4096-element tiles: (1) per-tile u64 sums, (2) one
 // CTA scans the tile sums, (3) every tile re-reads its elements, scans them in
 // shared memory and writes out. HBM traffic: 2 reads + 1 write per element.
-// Up to 2^14 elements a single CTA scans tile after tile (k_scan_single).
+// Up to 2^14 elements one CTA scans them in registers (k_scan_single).
 #include "internal.hpp"
 
 #include <cstdlib>
@@ -90,52 +90,59 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(const uint32_t* in, 
 }
 
 // Small inputs (the partition's key offsets, per-read counts of small
-// batches): one CTA walks the tiles in order with a running carry -- one
-// launch instead of three, one read and one write per element.
-constexpr int kSingleThreads = 512;
-constexpr int kSingleTile = kSingleThreads * kScanPer;
-constexpr uint64_t kSingleMax = uint64_t(1) << 14;  // 65537 elements: 32 us here vs ~15 us in three kernels
+// batches): one CTA, one tile; every thread scans 16 consecutive elements in
+// registers (16-byte vector loads and stores when aligned). One launch instead
+// of three, one read and one write per element.
+constexpr int kSingleThreads = 1024;
+constexpr uint64_t kSingleMax = uint64_t(kSingleThreads) * kScanPer;
 
 __global__ void __launch_bounds__(kSingleThreads) k_scan_single(const uint32_t* in, uint32_t* out, uint64_t n,
                                                                 uint32_t* __restrict__ d_total,
                                                                 int* __restrict__ d_overflow) {
   QGM_GRID_DEP();
-  __shared__ uint32_t tile[kSingleTile + kSingleTile / 32];
   __shared__ uint64_t ws[33];
-  uint64_t carry = 0;
-  for (uint64_t base = 0; base < n; base += kSingleTile) {
+  static_assert(kScanPer % 4 == 0, "");
+  const uint64_t b = uint64_t(threadIdx.x) * kScanPer;
+  const bool vec = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0 &&
+                   b + kScanPer <= n;
+  uint32_t v[kScanPer];
+  if (vec) {
 #pragma unroll
-    for (int j = 0; j < kScanPer; ++j) {
-      const uint32_t li = j * kSingleThreads + threadIdx.x;
-      const uint64_t i = base + li;
-      tile[pad_idx(li)] = i < n ? in[i] : 0u;
+    for (int j = 0; j < kScanPer / 4; ++j) {
+      const uint4 x = reinterpret_cast<const uint4*>(in + b)[j];
+      v[4 * j] = x.x;
+      v[4 * j + 1] = x.y;
+      v[4 * j + 2] = x.z;
+      v[4 * j + 3] = x.w;
     }
-    __syncthreads();
-    uint64_t s = 0;
+  } else {
 #pragma unroll
-    for (int j = 0; j < kScanPer; ++j) s += tile[pad_idx(threadIdx.x * kScanPer + j)];
-    uint64_t tot;
-    uint64_t run = block_exclusive_scan<uint64_t>(s, ws, &tot) + carry;
+    for (int j = 0; j < kScanPer; ++j) v[j] = b + j < n ? in[b + j] : 0u;
+  }
+  uint64_t s = 0;
 #pragma unroll
-    for (int j = 0; j < kScanPer; ++j) {
-      const uint32_t li = pad_idx(threadIdx.x * kScanPer + j);
-      const uint32_t v = tile[li];
-      tile[li] = uint32_t(run);
-      run += v;
-    }
-    __syncthreads();
+  for (int j = 0; j < kScanPer; ++j) s += v[j];
+  uint64_t tot;
+  // in == out is allowed: the scan's barriers order every read before any write
+  uint64_t run = block_exclusive_scan<uint64_t>(s, ws, &tot);
 #pragma unroll
-    for (int j = 0; j < kScanPer; ++j) {
-      const uint32_t li = j * kSingleThreads + threadIdx.x;
-      const uint64_t i = base + li;
-      if (i < n) out[i] = tile[pad_idx(li)];
-    }
-    carry += tot;
-    __syncthreads();  // the tile is rewritten next iteration
+  for (int j = 0; j < kScanPer; ++j) {
+    const uint32_t x = v[j];
+    v[j] = uint32_t(run);
+    run += x;
+  }
+  if (vec) {
+#pragma unroll
+    for (int j = 0; j < kScanPer / 4; ++j)
+      reinterpret_cast<uint4*>(out + b)[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j)
+      if (b + j < n) out[b + j] = v[j];
   }
   if (threadIdx.x == 0) {
-    if (d_total) *d_total = uint32_t(carry);
-    if (d_overflow) *d_overflow = carry > 0xFFFFFFFFull ? 1 : 0;
+    if (d_total) *d_total = uint32_t(tot);
+    if (d_overflow) *d_overflow = tot > 0xFFFFFFFFull ? 1 : 0;
   }
 }
 

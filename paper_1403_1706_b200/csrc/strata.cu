@@ -100,7 +100,13 @@ __global__ void k_seg_reduce(uint64_t* __restrict__ skeys, uint32_t* __restrict_
                              const uint32_t* __restrict__ off, uint32_t n_reads, int mode,
                              uint32_t* __restrict__ kept, const unsigned long long* __restrict__ big) {
   QGM_GRID_DEP();
-  if (big && *big) return;
+  // kept[0, n_reads] is written here in full (the scan after it reads n_reads
+  // + 1 entries), also when the batch goes to the radix path (zeros then)
+  if (blockIdx.x == 0 && threadIdx.x == 0) kept[n_reads] = 0;
+  if (big && *big) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_reads; r += gridDim.x * blockDim.x) kept[r] = 0;
+    return;
+  }
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_reads; r += gridDim.x * blockDim.x) {
     const uint32_t b = off[r], m = off[r + 1] - b;
     uint32_t nk = 0;
@@ -268,8 +274,7 @@ uint64_t stratify_unsorted(Ctx& c, const Ref& ref, DBuf<uint64_t>& hit_keys, DBu
   }
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(kSMs) * 16));
   const unsigned rgrid = unsigned(std::min<uint64_t>(ceil_div(n_reads, 128), uint64_t(kSMs) * 16));
-  DBuf<uint32_t> off(c, uint64_t(n_reads) + 1), kept(c, uint64_t(n_reads) + 1), total(c, 1);
-  kept.zero();
+  DBuf<uint32_t> off(c, uint64_t(n_reads) + 1), kept(c, uint64_t(n_reads) + 1), total(c, 1);  // kept: k_seg_reduce
   exclusive_scan_u32(c, cnt.p, off.p, uint64_t(n_reads) + 1, nullptr, nullptr);
   DBuf<uint64_t> skeys(c, n);
   DBuf<uint32_t> svals(c, n);
@@ -300,8 +305,7 @@ void stratify_unsorted_dev(Ctx& c, const Ref& ref, const uint64_t* hit_keys, con
   KernelScope ks(c, "k_strata_seg");
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n_max, 256), uint64_t(kSMs) * 16));
   const unsigned rgrid = unsigned(std::min<uint64_t>(ceil_div(n_reads, 128), uint64_t(kSMs) * 16));
-  DBuf<uint32_t> off(c, uint64_t(n_reads) + 1), kept(c, uint64_t(n_reads) + 1);
-  kept.zero();
+  DBuf<uint32_t> off(c, uint64_t(n_reads) + 1), kept(c, uint64_t(n_reads) + 1);  // kept: written by k_seg_reduce
   exclusive_scan_u32(c, cnt.p, off.p, uint64_t(n_reads) + 1, nullptr, nullptr);
   DBuf<uint64_t> skeys(c, n_max);
   DBuf<uint32_t> svals(c, n_max);
