@@ -215,9 +215,10 @@ __global__ void __launch_bounds__(kHistThreads, 1) k_part_hist16(ItemGen<Q, kRaw
 // the batch flags (Partitioned::flags) from the upload's length extremes
 __global__ void k_bin_offsets(const uint32_t* __restrict__ soff, uint32_t nbins, unsigned sub,
                               uint32_t* __restrict__ boff, const uint32_t* __restrict__ lens, uint32_t stride,
-                              uint32_t keys, uint32_t* __restrict__ flags) {
+                              uint32_t keys, uint32_t* __restrict__ flags, uint32_t* __restrict__ cursors) {
   QGM_GRID_DEP();
   for (uint32_t b = threadIdx.x; b <= nbins; b += blockDim.x) boff[b] = soff[b << sub];
+  for (uint32_t b = threadIdx.x; b <= kBins; b += blockDim.x) cursors[b] = 0;  // P1's per-bin cursors
   if (threadIdx.x == 0) {
     flags[0] = soff[keys];
     flags[1] = ~lens[1] == stride;
@@ -237,8 +238,11 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) k_part_scatter(I
                                                                   const uint32_t* __restrict__ boff,
                                                                   uint32_t* __restrict__ cursor,
                                                                   uint64_t* __restrict__ out, uint32_t sw_words,
-                                                                  const uint32_t* __restrict__ lens) {
+                                                                  const uint32_t* __restrict__ lens,
+                                                                  uint32_t* __restrict__ clear, uint32_t n_clear) {
   QGM_GRID_DEP();
+  // P0's histogram, read by the scan before this grid, becomes P2's per-key cursors
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_clear; i += gridDim.x * blockDim.x) clear[i] = 0;
   // kChunk items, bin-sorted | kChunk u8 bins | 2 x sw_words staged read words
   extern __shared__ __align__(16) uint64_t stage[];
   uint8_t* sbin = reinterpret_cast<uint8_t*>(stage + kChunk);
@@ -540,10 +544,9 @@ static void p0_p1(Ctx& c, const ItemGen<Q, kRaw>& gen, const Reads& reads, unsig
   exclusive_scan_u32(c, h2.p, out.soff.p, keys + 1, nullptr, nullptr);
   // no host round trip: V stays on the device (flags[0]); buffers are sized by
   // the slot count, which equals V for a batch of full-length reads
+  DBuf<uint32_t> hist(c, kBins + 1);  // per-bin cursors of P1 (zeroed by k_bin_offsets)
   QGM_KERNEL(c, k_bin_offsets, 1, 256, 0, out.soff.p, 1u << bits, sub, out.boff.p, reads.lens.p, reads.stride, keys,
-             out.flags.p);
-  DBuf<uint32_t> hist(c, kBins + 1);  // per-bin cursors of P1
-  hist.zero();
+             out.flags.p, hist.p);
   p1.alloc(c, uint64_t(V) + 2);  // +2: P2 bulk-copies whole 16-byte pairs
   const uint32_t chunk_runs = kChunk / R;
   // staged words per chunk: the reads under chunk_runs runs (+2 partial) and
@@ -554,7 +557,8 @@ static void p0_p1(Ctx& c, const ItemGen<Q, kRaw>& gen, const Reads& reads, unsig
   ensure_dynamic_smem(reinterpret_cast<const void*>(p1kern), size_t(smem));
   const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(gen.n_runs, chunk_runs), uint64_t(kSMs) * kPartMinBlocks));
   KernelScope ks(c, "k_part_scatter");
-  QGM_KERNEL(c, p1kern, grid, kPartThreads, smem, gen, shift, out.boff.p, hist.p, p1.p, sw_words, reads.lens.p);
+  QGM_KERNEL(c, p1kern, grid, kPartThreads, smem, gen, shift, out.boff.p, hist.p, p1.p, sw_words, reads.lens.p, h2.p,
+             keys + 1);
 }
 
 template <int Q, bool kRaw>
@@ -643,7 +647,7 @@ void partition_reads(Ctx& c, const Reads& reads, unsigned q, Partitioned& out, b
   rf.kshift = 2 * q - key_bits;
   rf.nbins = 1u << bits;
   const unsigned grid2 = unsigned(std::min<uint64_t>(ceil_div(V, kP2Chunk), uint64_t(kSMs) * kP2MinBlocks));
-  h2.zero();  // per-key cursors
+  // h2: P2's per-key cursors, zeroed by P1
   out.pairs.alloc(c, V + 2);  // +2: the join bulk-copies whole 16-byte pairs of items
   const size_t smem2 = kP2Chunk * (2 * sizeof(uint64_t) + sizeof(uint16_t));
   ensure_dynamic_smem(reinterpret_cast<const void*>(k_refine_scatter), size_t(smem2));
