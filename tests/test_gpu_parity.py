@@ -155,6 +155,16 @@ def test_device_scan_matches_reference_semantics(ctx):
         ctx.exclusive_scan(np.full(3, 0xF0000000, np.uint32))
 
 
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 1023, 10_001, 16_383, 16_384, 16_385, 65_537])
+def test_device_scan_around_the_single_cta_tile(ctx, n):
+    """The one-CTA register scan covers n <= 16384 (16 per thread, vector
+    loads only for full runs); above it the three-kernel tiled scan."""
+    v = np.random.default_rng(n).integers(0, 1 << 16, n).astype(np.uint32)
+    sums, tot = ctx.exclusive_scan(v)
+    ref = np.cumsum(v, dtype=np.uint64) - v
+    assert np.array_equal(sums, ref.astype(np.uint32)) and tot == int(v.sum(dtype=np.uint64))
+
+
 def test_c2_shape_properties(ctx):
     """Bench-size batch (1M reads against a 100 Mbp reference, q=16): the e2e
     host entry point equals the device-resident one; best-stratum hits are a
