@@ -23,8 +23,11 @@
 namespace qgm {
 namespace {
 
+// CTA size and row-bound segment (A/B, k_validate ms, 128 x 8 -> 256 x 16:
+// C2 0.546 -> 0.536, C4 2.326 -> 2.271, C4 B=64 4.51 -> 4.23, C3 shard 12.39
+// -> 12.13, C5m 1.60 -> 1.57; 512 threads helped only the C3 shard)
 #ifndef QGM_VAL_THREADS
-#define QGM_VAL_THREADS 128
+#define QGM_VAL_THREADS 256
 #endif
 constexpr int kValThreads = QGM_VAL_THREADS;
 #ifdef QGM_VAL_HIST
@@ -119,10 +122,11 @@ template <> struct Band<uint64_t> {
 // subtracted. Tighter than the whole-row bound D[i][0] - popc(Mv) (on a
 // simulated random window, n = 100, B = 32, k_max = 20, it passes k_max at
 // row ~48 instead of ~62) for 4 extra popcounts per 16 rows; measured on
-// B200: C3 validation 12.82 -> 12.64 ms, C2 0.559 -> 0.554 ms (segments of 4
-// cost more than they save; QGM_VAL_SEG >= the word width = whole row).
+// B200: C3 validation 12.82 -> 12.64 ms, C2 0.559 -> 0.554 ms with segments
+// of 8; 16 is better still with 256-thread CTAs (above); 4 costs more than it
+// saves; QGM_VAL_SEG >= the word width = whole row.
 #ifndef QGM_VAL_SEG
-#define QGM_VAL_SEG 8
+#define QGM_VAL_SEG 16
 #endif
 template <class T>
 __device__ __forceinline__ int row_lower_bound(int score0, T Pv, T Mv) {
