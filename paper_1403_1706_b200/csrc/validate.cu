@@ -30,6 +30,7 @@ namespace {
 #define QGM_VAL_THREADS 256
 #endif
 constexpr int kValThreads = QGM_VAL_THREADS;
+constexpr int kValThreadsBig = 512;
 #ifdef QGM_VAL_HIST
 __device__ unsigned long long g_exit_hist[16];  // debug: abandon row / 16, [15] = ran to the end
 #endif
@@ -276,8 +277,8 @@ __device__ __forceinline__ void unpack_state(const Parked& p, T& Pv, T& Mv) {
 // kPhase 0: every row (qgm_validate, or no split); 1: rows [0, r_split),
 // survivors parked; 2: resume the parked candidates from row r_split (a
 // multiple of 16).
-template <class T, int kPhase>
-__global__ void __launch_bounds__(kValThreads) k_validate(ValArgs a, uint32_t r_split, Parked* __restrict__ park,
+template <class T, int kPhase, int kThreads>
+__global__ void __launch_bounds__(kThreads) k_validate(ValArgs a, uint32_t r_split, Parked* __restrict__ park,
                                                           unsigned long long* __restrict__ n_park, uint64_t park_cap) {
   QGM_GRID_DEP();
   const T mask = a.B >= sizeof(T) * 8 ? T(~T(0)) : T((T(1) << a.B) - 1);
@@ -440,7 +441,6 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
   a.validated = d_validated;
   a.per_read = per_read;
   a.n_big = d_big;
-  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, kValThreads), uint64_t(kSMs) * 32));
   KernelScope ks(c, "k_validate");
   // map path: split where a candidate's lower bound has passed k_max unless
   // it is a true hit: the DP's minimum grows ~0.42 per row on a random
@@ -457,6 +457,16 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
   // the device, the context's last batch is the estimate
   const uint64_t n_est = d_n && c.last_raw_candidates ? std::min<uint64_t>(n, c.last_raw_candidates) : n;
   const bool split_pays = split_env || n_est >= uint64_t(2) * kSMs * 1024;
+  // CTA size: 512 threads for batches of tens of millions of candidates (C3
+  // shard: 12.13 -> 11.91 ms), 256 otherwise (C2 0.536 vs 0.560 with 512)
+  const bool wide = n_est >= (uint64_t(1) << 25);
+  const int threads = wide ? kValThreadsBig : kValThreads;
+  const unsigned grid = unsigned(std::min<uint64_t>(ceil_div(n, uint64_t(threads)), uint64_t(kSMs) * 32));
+#define QGM_VAL_LAUNCH(T, P, ...)                                                      \
+  do {                                                                               \
+    if (wide) QGM_KERNEL(c, (k_validate<T, P, kValThreadsBig>), grid, threads, 0, __VA_ARGS__); \
+    else QGM_KERNEL(c, (k_validate<T, P, kValThreads>), grid, threads, 0, __VA_ARGS__);        \
+  } while (0)
   if (mode == 0 && split_pays && r_split >= 16 && r_split < reads.stride) {
     // survivors parked for phase 2, at most 16M (candidates beyond finish in
     // phase 1)
@@ -468,16 +478,17 @@ void validate_candidates(Ctx& c, const Reads& reads, const Ref& ref, const uint6
     DBuf<unsigned long long> np(c, 1);
     np.zero();
     if (band <= 32) {
-      QGM_KERNEL(c, (k_validate<uint32_t, 1>), grid, kValThreads, 0, a, r_split, park.p, np.p, cap);
-      QGM_KERNEL(c, (k_validate<uint32_t, 2>), grid, kValThreads, 0, a, r_split, park.p, np.p, cap);
+      QGM_VAL_LAUNCH(uint32_t, 1, a, r_split, park.p, np.p, cap);
+      QGM_VAL_LAUNCH(uint32_t, 2, a, r_split, park.p, np.p, cap);
     } else {
-      QGM_KERNEL(c, (k_validate<uint64_t, 1>), grid, kValThreads, 0, a, r_split, park.p, np.p, cap);
-      QGM_KERNEL(c, (k_validate<uint64_t, 2>), grid, kValThreads, 0, a, r_split, park.p, np.p, cap);
+      QGM_VAL_LAUNCH(uint64_t, 1, a, r_split, park.p, np.p, cap);
+      QGM_VAL_LAUNCH(uint64_t, 2, a, r_split, park.p, np.p, cap);
     }
     return;
   }
-  if (band <= 32) QGM_KERNEL(c, (k_validate<uint32_t, 0>), grid, kValThreads, 0, a, 0u, nullptr, nullptr, uint64_t(0));
-  else QGM_KERNEL(c, (k_validate<uint64_t, 0>), grid, kValThreads, 0, a, 0u, nullptr, nullptr, uint64_t(0));
+  if (band <= 32) QGM_VAL_LAUNCH(uint32_t, 0, a, 0u, nullptr, nullptr, uint64_t(0));
+  else QGM_VAL_LAUNCH(uint64_t, 0, a, 0u, nullptr, nullptr, uint64_t(0));
+#undef QGM_VAL_LAUNCH
 }
 
 }  // namespace qgm
